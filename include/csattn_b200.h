@@ -1,0 +1,255 @@
+/*
+ * csattn_b200.h — C ABI of the B200-native CSAttention decode hot path.
+ *
+ * This is the drop-in boundary for the path BASELINE.json names: the offline
+ * table build from prefill Q/K and the online decode step (centroid routing,
+ * gather/accumulate, top-K, sparse attention, append + streaming insert).
+ * Every entry point replaces one function (or one composition) of the
+ * reference C++ API in proj/include/csattn/ (file:line cited per entry).
+ *
+ * Conventions (reference: errors.hpp:8-52):
+ *   - Every function returns a csattn_status. Nothing throws across the ABI.
+ *     The message of the last failure on the calling thread is returned by
+ *     csattn_last_error(). One status per reference exception class.
+ *   - Pointers are plain host or device pointers; CSATTN_HOST_BUFFERS in a
+ *     `flags` argument says the data pointers of that call are host memory
+ *     (copied in/out inside the call), otherwise they are device pointers
+ *     on the context's device.
+ *   - All float data is row-major fp32; indices are uint32.
+ *   - Validation happens on the host before any launch, in the reference's
+ *     order, so the same bad input yields the same error class + message.
+ */
+#ifndef CSATTN_B200_H_
+#define CSATTN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception class (errors.hpp:8-52) ---- */
+typedef enum csattn_status {
+    CSATTN_OK = 0,
+    CSATTN_ERR_GENERIC = 1,          /* csattn::Error */
+    CSATTN_ERR_DIMENSION = 2,        /* csattn::DimensionError */
+    CSATTN_ERR_PARAMETER = 3,        /* csattn::ParameterError */
+    CSATTN_ERR_DATA = 4,             /* csattn::DataError */
+    CSATTN_ERR_BAD_MAGIC = 5,        /* csattn::BadMagicError */
+    CSATTN_ERR_VERSION = 6,          /* csattn::VersionError */
+    CSATTN_ERR_TRUNCATED = 7,        /* csattn::TruncatedError */
+    CSATTN_ERR_CORRUPT = 8,          /* csattn::CorruptError */
+    CSATTN_ERR_PROPERTY = 9,         /* csattn::PropertyError */
+    CSATTN_ERR_STREAM_EXHAUSTED = 10,/* csattn::StreamExhaustedError */
+    CSATTN_ERR_CUDA = 20,            /* CUDA runtime / launch failure */
+    CSATTN_ERR_CAPACITY = 21         /* session sized too small (max_decode_steps) */
+} csattn_status;
+
+/* flags */
+#define CSATTN_HOST_BUFFERS 0x1u   /* data pointers of this call are host memory */
+#define CSATTN_NO_SYNC      0x2u   /* do not synchronize the stream before returning
+                                      (device buffers only) */
+
+/* ---- configuration PODs (mirror the reference structs) ---- */
+
+/* IndexConfig + ClusterConfig (index.hpp:36-42, clustering.hpp:17-28) */
+typedef struct csattn_index_config {
+    double alpha;              /* L = ceil_ratio(alpha, P); default 0.2 */
+    uint64_t list_capacity;    /* absolute L override; 0 = derive */
+    int32_t normalize_keys;    /* score against normalized key slices */
+    int32_t score_bits;        /* 16 or 32 (serialization width) */
+    uint64_t centroids;        /* C per subspace; default 64 */
+    uint64_t iterations;       /* k-means rounds; default 10 */
+    uint64_t batch_size;       /* 0 = min(4096, n) */
+    uint64_t seed;             /* cluster seed */
+    double tolerance;          /* full-batch early stop / monotonicity slack */
+} csattn_index_config;
+
+/* RetrievalConfig (retrieval.hpp:17-32). k_bump is a host callback in the
+ * reference; across the ABI it is replaced by a per-call k_override. */
+typedef struct csattn_retrieval_config {
+    double keep_ratio;          /* rho; default 0.05 */
+    uint64_t search_period;     /* default 1 */
+    uint64_t recent_window;     /* R; default 32 */
+    const double* weights;      /* w_b per subspace, host memory; NULL = all ones */
+    uint64_t n_weights;         /* 0 or m */
+    uint64_t backoff_tau;       /* default 1 */
+    double backoff_threshold;   /* default -inf */
+    int32_t recent_passthrough; /* default 1 */
+    int32_t reserved;
+} csattn_retrieval_config;
+
+/* SyntheticSpec (synthetic.hpp:16-28) */
+typedef struct csattn_synthetic_spec {
+    uint64_t rows;
+    uint64_t dim;
+    uint64_t clusters;
+    uint64_t seed;
+    double plant_fraction;
+    double plant_scale;
+    double query_noise;
+    uint64_t dwell;
+} csattn_synthetic_spec;
+
+/* DecodeStepReport.counters (metrics.hpp:15-37) + selection facts */
+typedef struct csattn_step_report {
+    uint64_t k;                  /* |selected| */
+    int32_t searched;
+    int32_t reserved;
+    uint64_t centroid_dot_ops;
+    uint64_t gathered_entries;
+    uint64_t reduce_ops;
+    uint64_t attention_key_ops;  /* k * d */
+    double h2d_bytes_model;      /* h2d_bytes(rho, N, d, B, period) */
+    uint64_t searches;
+    uint64_t inserts_attempted;
+    uint64_t inserts_applied;
+    uint64_t insert_dot_ops;
+    double worst_best_cosine;    /* min_b best_cosine of the last search */
+} csattn_step_report;
+
+typedef struct csattn_session_info {
+    uint64_t dim;            /* d */
+    uint64_t subspaces;      /* m */
+    uint64_t centroids;      /* C */
+    uint64_t list_capacity;  /* L */
+    uint64_t prefill_len;    /* P */
+    uint64_t context_len;    /* N = P + steps */
+    uint64_t steps;          /* decode steps taken */
+    uint64_t max_context;    /* P + max_decode_steps */
+    uint64_t group;          /* query heads sharing this KV head's tables */
+    double alpha;
+    int32_t normalize_keys;
+    int32_t score_bits;
+    uint64_t device_bytes;   /* HBM owned by the session */
+} csattn_session_info;
+
+typedef struct csattn_ctx_s* csattn_ctx;
+typedef struct csattn_session_s* csattn_session;
+
+/* ---- defaults / small pure helpers ---- */
+void csattn_index_config_default(csattn_index_config* cfg);
+void csattn_retrieval_config_default(csattn_retrieval_config* cfg);
+void csattn_synthetic_spec_default(csattn_synthetic_spec* spec);
+
+/* keep_count (retrieval.cpp:34-38): max(1, ceil_ratio(rho, n)) */
+csattn_status csattn_keep_count(double rho, uint64_t n, uint64_t* out);
+/* parse_schedule (retrieval.cpp:10-32): "<rho>-step-<P>" */
+csattn_status csattn_parse_schedule(const char* name, double* rho, uint64_t* period);
+/* h2d_bytes (metrics.cpp:32-38) */
+csattn_status csattn_h2d_bytes(double rho, uint64_t n, uint64_t d, uint64_t bytes_per_elem,
+                               uint64_t period, double* out);
+
+/* make_synthetic (synthetic.cpp:18-74): host-side input generator, bit-identical
+ * to the reference (mt19937_64 + hand-rolled draws). Outputs rows*dim floats each. */
+csattn_status csattn_make_synthetic(const csattn_synthetic_spec* spec, float* queries,
+                                    float* keys, float* values);
+
+const char* csattn_last_error(void);
+const char* csattn_status_name(csattn_status s);
+
+/* ---- context: device + stream ---- */
+csattn_status csattn_ctx_create(int device, void* cuda_stream, csattn_ctx* out);
+csattn_status csattn_ctx_destroy(csattn_ctx ctx);
+csattn_status csattn_ctx_synchronize(csattn_ctx ctx);
+/* Number of CUDA kernels this context has launched (driver-side evidence). */
+uint64_t csattn_ctx_launch_count(csattn_ctx ctx);
+
+/* ---- offline build ----
+ * prefill (session.cpp:25-44) = KvStore + build_index (index.cpp:145-177)
+ * on the GPU: per-subspace exact spherical k-means (clustering.cpp:73-240),
+ * exact fp64 centroid x key scores (index.cpp:68-91) and top-L lists
+ * (index.cpp:46-62, 107-141).
+ * queries: n_queries x d (n_queries may exceed p: a GQA group pools its heads'
+ * prefill queries, index.cpp:150-151); keys/values: p x d.
+ * group: query heads that will decode against this KV head (>= 1).
+ * max_decode_steps: capacity for appended rows. */
+csattn_status csattn_prefill(csattn_ctx ctx, const float* queries, uint64_t n_queries,
+                             const float* keys, const float* values, uint64_t p, uint64_t d,
+                             const uint64_t* widths, uint64_t m,
+                             const csattn_index_config* icfg,
+                             const csattn_retrieval_config* rcfg, uint64_t group,
+                             uint64_t max_decode_steps, uint32_t flags, csattn_session* out);
+
+/* build_index_from_centroids (index.cpp:179-202): caller-supplied unit centroid
+ * rows, packed per subspace: subspace b holds C x widths[b] floats, subspaces
+ * concatenated (C*d floats total). Always host memory. */
+csattn_status csattn_prefill_from_centroids(csattn_ctx ctx, const float* centroids,
+                                            uint64_t c, const float* keys,
+                                            const float* values, uint64_t p, uint64_t d,
+                                            const uint64_t* widths, uint64_t m,
+                                            const csattn_index_config* icfg,
+                                            const csattn_retrieval_config* rcfg,
+                                            uint64_t group, uint64_t max_decode_steps,
+                                            uint32_t flags, csattn_session* out);
+
+/* Adopt a host CsIndex image (the offline -> online handoff; reference layout:
+ * per table t = b*C + j, lens[t] entries in TopList order (score desc, index
+ * asc), stored at indices/scores + t*stride). Host memory only. */
+csattn_status csattn_session_import(csattn_ctx ctx, const float* centroids, uint64_t c,
+                                    const uint32_t* lens, const uint32_t* indices,
+                                    const float* scores, uint64_t stride,
+                                    uint64_t list_capacity, double alpha,
+                                    int32_t normalize_keys, int32_t score_bits,
+                                    const float* keys, const float* values, uint64_t p,
+                                    uint64_t d, const uint64_t* widths, uint64_t m,
+                                    const csattn_retrieval_config* rcfg, uint64_t group,
+                                    uint64_t max_decode_steps, csattn_session* out);
+
+/* Export the current tables in reference TopList order (score desc, index asc).
+ * lens: m*C; indices/scores: m*C*stride (stride >= L); centroids: C*d (nullable).
+ * Host memory. */
+csattn_status csattn_session_export(csattn_session s, uint32_t* lens, uint32_t* indices,
+                                    float* scores, uint64_t stride, float* centroids);
+
+/* Independent copy (Session is a value type, session.hpp:19-31): tables are
+ * copied, the immutable prefill KV rows are shared. */
+csattn_status csattn_session_fork(csattn_session src, uint64_t max_decode_steps,
+                                  csattn_session* out);
+csattn_status csattn_session_destroy(csattn_session s);
+csattn_status csattn_session_info_get(csattn_session s, csattn_session_info* out);
+csattn_status csattn_session_set_retrieval(csattn_session s, const csattn_retrieval_config* rcfg);
+/* KvStore rows back to the host (core.cpp:84-90): rows [first, first+count). */
+csattn_status csattn_session_read_kv(csattn_session s, uint64_t first, uint64_t count,
+                                     float* keys, float* values);
+
+/* ---- online decode ----
+ * decode_step (session.cpp:46-99) for every query head of the group:
+ * decode_search (retrieval.cpp:230-270) -> masked dense_attention
+ * (core.cpp:118-169) -> KvStore::append (core.cpp:71-79) -> streaming_insert
+ * (retrieval.cpp:272-301).
+ *   q:        group x d        new_key, new_value: d
+ *   out:      group x d        (nullable)
+ *   selected: group x sel_stride uint32, ascending (nullable)
+ *   weights:  group x sel_stride f32 softmax weights in selected order (nullable)
+ *   reports:  group reports, host memory (nullable)
+ *   k_override: group entries, host memory (nullable; 0 = keep_count) — the
+ *               ABI form of RetrievalConfig::k_bump.
+ * compare_dense is not part of the hot path (see csattn_dense_attention). */
+csattn_status csattn_decode_step(csattn_session s, const float* q, const float* new_key,
+                                 const float* new_value, float* out, uint32_t* selected,
+                                 float* weights, uint64_t sel_stride,
+                                 csattn_step_report* reports, const uint64_t* k_override,
+                                 uint32_t flags);
+
+/* One decode step for many sessions at once (a layer: KV heads x sequences),
+ * one kernel launch per stage. sessions[i] has group g_i; q holds
+ * sum_i g_i rows in session order, new_keys/new_values one row per session.
+ * out: sum_i g_i rows (nullable). selected: sum_i g_i rows of sel_stride. */
+csattn_status csattn_decode_batch(csattn_ctx ctx, uint64_t n_sessions,
+                                  const csattn_session* sessions, const float* q,
+                                  const float* new_keys, const float* new_values, float* out,
+                                  uint32_t* selected, uint64_t sel_stride, uint32_t flags);
+
+/* Masked (or full, mask == NULL) dense attention on the GPU over the session's
+ * current KV rows (core.cpp:118-169). Used for compare_dense and recall. */
+csattn_status csattn_dense_attention(csattn_session s, const float* q, const uint32_t* mask,
+                                     uint64_t n_mask, float* out, float* weights,
+                                     uint32_t flags);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSATTN_B200_H_ */

@@ -1,0 +1,134 @@
+// build.cu — offline table build (assemble_index, index.cpp:107-141) on sm_100a.
+//
+//   build_scores: s[b*C+j][i] = float(sum_t double(c_j^b[t]) * double(k_i^b[t]))
+//                 (score_keys, index.cpp:68-91): sequential fp64 FMA chain per
+//                 score (the float x float product is exact in fp64, so FMA
+//                 contraction reproduces the reference's mul-then-add), keys
+//                 staged per 128-key tile in shared memory with all C centroids
+//                 of the subspace; optional normalize_keys.
+//   build_lists:  one CTA per table: radix select of the L-th best by
+//                 (score desc, index asc) on the 64-bit image
+//                 ordf(score)<<32 | ~index (TopList::from_scores :46-62), an
+//                 order-preserving compaction that writes the table already
+//                 index-sorted, then key-block offsets and the low buffer.
+// The contraction here is K = d_b (16) deep: too shallow to feed tcgen05, and
+// the result must be bit-exact fp64, so it runs on the FP64 pipe; the kernel
+// is bounded by the T x P score write/read.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tables.cuh"
+
+namespace csa {
+
+constexpr int BS_TILE = 128;
+constexpr int BS_THREADS = 256;
+constexpr int BL_THREADS = 512;
+
+__global__ void __launch_bounds__(BS_THREADS)
+build_scores_kernel(const SessionDev* __restrict__ sp, float* __restrict__ scores) {
+    extern __shared__ float bsm[];
+    const SessionDev& sd = *sp;
+    const uint32_t b = blockIdx.y, C = sd.C, P = sd.P, d = sd.d;
+    const uint32_t w = sd.widths[b], off = sd.offs[b];
+    const uint32_t i0 = blockIdx.x * BS_TILE;
+    float* kt = bsm;                       // [BS_TILE][w+1]
+    float* ct = bsm + BS_TILE * (w + 1);   // [C][w]
+    const float* cb = sd.cent + static_cast<size_t>(C) * off;
+    for (uint32_t x = threadIdx.x; x < C * w; x += blockDim.x) ct[x] = cb[x];
+    for (uint32_t x = threadIdx.x; x < BS_TILE * w; x += blockDim.x) {
+        const uint32_t r = x / w, c = x - r * w;
+        const uint32_t i = i0 + r;
+        kt[r * (w + 1) + c] = i < P ? sd.kpre[static_cast<size_t>(i) * d + off + c] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t r = threadIdx.x % BS_TILE;
+    const uint32_t jg = threadIdx.x / BS_TILE, ng = blockDim.x / BS_TILE;
+    const uint32_t i = i0 + r;
+    if (i >= P) return;
+    const float* k = kt + r * (w + 1);
+    double inv = 1.0;
+    bool zero = false;
+    if (sd.normalize_keys) {
+        double n2 = 0.0;
+        for (uint32_t t = 0; t < w; ++t) n2 = __fma_rn((double)k[t], (double)k[t], n2);
+        zero = n2 == 0.0;
+        inv = sqrt(n2);
+    }
+    for (uint32_t j = jg; j < C; j += ng) {
+        const float* c = ct + j * w;
+        double s = 0.0;
+        for (uint32_t t = 0; t < w; ++t) s = __fma_rn((double)c[t], (double)k[t], s);
+        if (sd.normalize_keys) s = zero ? 0.0 : __ddiv_rn(s, inv);
+        scores[static_cast<size_t>(b * C + j) * P + i] = __double2float_rn(s);
+    }
+}
+
+__device__ __forceinline__ unsigned long long sel_key(float s, uint32_t i) {
+    uint32_t u = __float_as_uint(s);
+    if ((u << 1) == 0) u = 0;  // -0.0 == +0.0
+    const uint32_t o = (u >> 31) ? ~u : (u | 0x80000000u);
+    return (static_cast<unsigned long long>(o) << 32) | static_cast<uint32_t>(~i);
+}
+
+struct BuildSmem {
+    RefillSmem r;
+};
+
+__global__ void __launch_bounds__(BL_THREADS)
+build_lists_kernel(const SessionDev* __restrict__ sp, const float* __restrict__ scores) {
+    __shared__ BuildSmem S;
+    const SessionDev& sd = *sp;
+    const uint32_t t = blockIdx.x, P = sd.P;
+    const float* sc = scores + static_cast<size_t>(t) * P;
+    const uint32_t keep = sd.L < P ? sd.L : P;
+    unsigned long long thr = 0;  // select iff sel_key >= thr
+    if (keep < P)
+        thr = cta_kth_largest(S.r, P, keep, [&](uint32_t i) { return sel_key(sc[i], i); });
+    uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
+    uint32_t out = 0;
+    for (uint32_t c0 = 0; c0 < P; c0 += blockDim.x) {
+        const uint32_t i = c0 + threadIdx.x;
+        float s = 0.0f;
+        uint32_t keepi = 0;
+        if (i < P) {
+            s = sc[i];
+            keepi = sel_key(s, i) >= thr ? 1u : 0u;
+        }
+        uint32_t tot;
+        const uint32_t ex = tbl_block_excl_scan(S.r, keepi, tot);
+        if (keepi) e[out + ex] = make_uint2(i, __float_as_uint(s));
+        out += tot;
+    }
+    if (threadIdx.x == 0) {
+        sd.n_used[t] = out;
+        sd.live[t] = out;
+    }
+    __syncthreads();
+    refill_table(S.r, sd, t, (P - 1) >> KEY_BLOCK_SHIFT);
+}
+
+cudaError_t launch_build_scores(const SessionDev* s_dev, const SessionDev& sh, float* scores,
+                                cudaStream_t st) {
+    uint32_t wmax = 0;
+    for (uint32_t b = 0; b < sh.m; ++b) wmax = sh.widths[b] > wmax ? sh.widths[b] : wmax;
+    const size_t smem = (static_cast<size_t>(BS_TILE) * (wmax + 1) + static_cast<size_t>(sh.C) * wmax) * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(build_scores_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(div_up(sh.P, BS_TILE), sh.m);
+    build_scores_kernel<<<grid, BS_THREADS, smem, st>>>(s_dev, scores);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_lists(const SessionDev* s_dev, const SessionDev& sh, const float* scores,
+                               cudaStream_t st) {
+    build_lists_kernel<<<sh.m * sh.C, BL_THREADS, 0, st>>>(s_dev, scores);
+    return cudaGetLastError();
+}
+
+}  // namespace csa

@@ -1,0 +1,1094 @@
+// capi.cpp — host runtime behind include/csattn_b200.h.
+//
+// Owns device memory per session (one KV head: prefill rows shared across
+// forks, appended-row tails, centroids, index-sorted tables), validates every
+// call on the host in the reference's order and with the reference's error
+// classes/messages, assembles per-launch problem descriptors and launches the
+// sm_100a kernels (csrc/*.cu). No computation of the hot path happens here;
+// there is no CPU fallback: every compute entry point launches a kernel or fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "csattn_b200.h"
+#include "kernels.h"
+#include "kmeans.h"
+#include <random>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    csattn_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(csattn_status c, std::string m) { throw Fail{c, std::move(m)}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(CSATTN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+csattn_status guard(F&& f) {
+    try {
+        f();
+        return CSATTN_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return CSATTN_ERR_GENERIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CSATTN_ERR_GENERIC;
+    }
+}
+
+struct DevMem {
+    void* p = nullptr;
+    size_t n = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t bytes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        if (bytes == 0) bytes = 16;
+        ck(cudaMalloc(&p, bytes), "cudaMalloc");
+        n = bytes;
+    }
+    void ensure(size_t bytes) {
+        if (bytes > n) alloc(bytes + bytes / 2);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// ceil_ratio (util.hpp:77-81)
+uint64_t ceil_ratio(double ratio, uint64_t n) {
+    const double v = ratio * static_cast<double>(n);
+    const double c = std::ceil(v - 1e-9);
+    return c <= 0.0 ? 0 : static_cast<uint64_t>(c);
+}
+
+// keep_count (retrieval.cpp:34-38)
+uint64_t keep_count(double rho, uint64_t n) {
+    if (!(rho > 0.0 && rho <= 1.0)) fail(CSATTN_ERR_PARAMETER, "keep ratio must lie in (0, 1]");
+    return std::max<uint64_t>(1, ceil_ratio(rho, n));
+}
+
+void require_finite(const float* v, size_t n, const char* what) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(v[i]))
+            fail(CSATTN_ERR_DATA, std::string(what) + " contains a non-finite value");
+}
+
+struct SharedRows {
+    DevMem k, v;
+};
+
+struct HeadState {
+    bool has_cache = false;
+    uint64_t n_cache = 0;
+    double worst = 1.0;
+};
+
+}  // namespace
+
+struct csattn_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own = false;
+    uint64_t launches = 0;
+    DevMem probs, iprobs, stage;
+    std::vector<csa::DecodeProblem> hprobs;
+    std::vector<csa::InsertProblem> hiprobs;
+    std::vector<unsigned char> hrep;
+};
+
+struct csattn_session_s {
+    csattn_ctx ctx = nullptr;
+    csa::SessionDev h{};
+    DevMem dev;
+    std::shared_ptr<SharedRows> pre;
+    DevMem ktail, vtail, cent, ent, n_used, live, blk_off, low, low_cnt, refill;
+    DevMem cache, sel, drep, irep;
+    uint64_t group = 1, N = 0, step = 0, max_steps = 0;
+    double alpha = 0.0;
+    int32_t score_bits = 32;
+    csattn_retrieval_config rc{};
+    std::vector<double> weights;
+    std::vector<HeadState> hs;
+    std::vector<uint64_t> widths;
+
+    uint64_t T() const { return static_cast<uint64_t>(h.m) * h.C; }
+    size_t device_bytes() const {
+        return ktail.n + vtail.n + cent.n + ent.n + n_used.n + live.n + blk_off.n + low.n +
+               low_cnt.n + refill.n + cache.n + sel.n + drep.n + irep.n +
+               (pre ? pre->k.n + pre->v.n : 0);
+    }
+};
+
+namespace {
+
+// SubspaceLayout (core.cpp:35-41 constructor checks)
+void validate_layout(const uint64_t* widths, uint64_t m, uint64_t d) {
+    if (m == 0) fail(CSATTN_ERR_PARAMETER, "subspace layout needs m >= 1");
+    uint64_t sum = 0;
+    for (uint64_t b = 0; b < m; ++b) {
+        if (widths[b] == 0)
+            fail(CSATTN_ERR_PARAMETER,
+                 "subspace width must be >= 1 (subspace " + std::to_string(b) + ")");
+        sum += widths[b];
+    }
+    if (sum != d) fail(CSATTN_ERR_DIMENSION, "layout dimension does not match KV dimension");
+    if (m > static_cast<uint64_t>(csa::MAXM))
+        fail(CSATTN_ERR_PARAMETER, "B200 path supports m <= " + std::to_string(csa::MAXM));
+    for (uint64_t b = 0; b < m; ++b)
+        if (widths[b] > static_cast<uint64_t>(csa::WMAX))
+            fail(CSATTN_ERR_PARAMETER,
+                 "B200 path supports subspace widths <= " + std::to_string(csa::WMAX));
+    if (d > static_cast<uint64_t>(csa::DMAX))
+        fail(CSATTN_ERR_PARAMETER, "B200 path supports d <= " + std::to_string(csa::DMAX));
+}
+
+// validate_retrieval_config (session.cpp:10-21)
+void validate_retrieval(const csattn_retrieval_config* cfg, uint64_t m) {
+    if (!(cfg->keep_ratio > 0.0 && cfg->keep_ratio <= 1.0))
+        fail(CSATTN_ERR_PARAMETER, "keep ratio must lie in (0, 1]");
+    if (cfg->search_period == 0) fail(CSATTN_ERR_PARAMETER, "search period must be >= 1");
+    if (cfg->backoff_tau == 0) fail(CSATTN_ERR_PARAMETER, "backoff tau must be >= 1");
+    if (cfg->weights && cfg->n_weights && cfg->n_weights != m)
+        fail(CSATTN_ERR_DIMENSION, "need one weight per subspace");
+    if (cfg->weights)
+        for (uint64_t b = 0; b < cfg->n_weights; ++b)
+            if (!(cfg->weights[b] > 0.0))
+                fail(CSATTN_ERR_PARAMETER, "subspace weights must be positive");
+    if (cfg->backoff_tau > static_cast<uint64_t>(csa::MAXTAU))
+        fail(CSATTN_ERR_PARAMETER, "B200 path supports backoff tau <= " +
+                                       std::to_string(csa::MAXTAU));
+    if (m * std::min<uint64_t>(cfg->backoff_tau, 1u << 20) > static_cast<uint64_t>(csa::MAXL))
+        fail(CSATTN_ERR_PARAMETER, "B200 path supports m * tau <= " + std::to_string(csa::MAXL));
+}
+
+// validate_index_config (index.cpp:95-103)
+void validate_index(const csattn_index_config* c) {
+    if (c->list_capacity == 0 && !(c->alpha > 0.0 && c->alpha <= 1.0))
+        fail(CSATTN_ERR_PARAMETER, "alpha must lie in (0, 1]");
+    if (c->score_bits != 16 && c->score_bits != 32)
+        fail(CSATTN_ERR_PARAMETER, "score width must be 16 or 32 bits");
+    if (c->centroids == 0) fail(CSATTN_ERR_PARAMETER, "centroid count must be >= 1");
+}
+
+void set_retrieval(csattn_session_s* s, const csattn_retrieval_config* rc) {
+    s->rc = *rc;
+    s->weights.assign(s->h.m, 1.0);
+    if (rc->weights && rc->n_weights)
+        for (uint32_t b = 0; b < s->h.m; ++b) s->weights[b] = rc->weights[b];
+    s->rc.weights = nullptr;
+    s->rc.n_weights = 0;
+    for (uint32_t b = 0; b < s->h.m; ++b) s->h.weights[b] = s->weights[b];
+    s->h.tau = static_cast<uint32_t>(rc->backoff_tau);
+    s->h.threshold = rc->backoff_threshold;
+    s->h.window = static_cast<uint32_t>(std::min<uint64_t>(rc->recent_window, 0xffffffffu));
+    s->h.passthrough = rc->recent_passthrough ? 1u : 0u;
+}
+
+void push_dev(csattn_session_s* s) {
+    ck(cudaMemcpyAsync(s->dev.p, &s->h, sizeof(csa::SessionDev), cudaMemcpyHostToDevice,
+                       s->ctx->stream),
+       "upload session");
+}
+
+// Allocate everything except prefill rows / centroid contents.
+std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const uint64_t* widths,
+                                              uint64_t m, uint64_t c, uint64_t L, uint64_t p,
+                                              uint64_t group, uint64_t max_steps,
+                                              const csattn_retrieval_config* rc) {
+    if (group == 0) fail(CSATTN_ERR_PARAMETER, "group must be >= 1");
+    if (m * c > static_cast<uint64_t>(csa::MAX_TABLES))
+        fail(CSATTN_ERR_PARAMETER,
+             "B200 path supports m * C <= " + std::to_string(csa::MAX_TABLES));
+    if (p + max_steps >= static_cast<uint64_t>(csa::MAX_CONTEXT))
+        fail(CSATTN_ERR_PARAMETER, "context exceeds 2^31 positions");
+    if (L > 0x7fffffffull) fail(CSATTN_ERR_PARAMETER, "list capacity too large");
+    auto s = std::make_unique<csattn_session_s>();
+    s->ctx = ctx;
+    s->group = group;
+    s->max_steps = max_steps;
+    s->N = p;
+    s->widths.assign(widths, widths + m);
+    csa::SessionDev& h = s->h;
+    h.d = static_cast<uint32_t>(d);
+    h.m = static_cast<uint32_t>(m);
+    h.C = static_cast<uint32_t>(c);
+    h.L = static_cast<uint32_t>(L);
+    uint64_t keep = std::min<uint64_t>(L, p);
+    uint64_t cap2 = std::max<uint64_t>(L, keep) + csa::LOW_Q;
+    cap2 += cap2 & 1;  // even: 16-byte aligned table rows
+    h.cap2 = static_cast<uint32_t>(cap2);
+    h.P = static_cast<uint32_t>(p);
+    h.max_ctx = static_cast<uint32_t>(p + max_steps);
+    h.nb_stride = (h.max_ctx >> csa::KEY_BLOCK_SHIFT) + 2;
+    uint32_t off = 0;
+    for (uint64_t b = 0; b < m; ++b) {
+        h.widths[b] = static_cast<uint32_t>(widths[b]);
+        h.offs[b] = off;
+        off += static_cast<uint32_t>(widths[b]);
+    }
+    set_retrieval(s.get(), rc);
+    const uint64_t T = m * c;
+    s->ktail.alloc(std::max<uint64_t>(max_steps, 1) * d * sizeof(float));
+    s->vtail.alloc(std::max<uint64_t>(max_steps, 1) * d * sizeof(float));
+    s->cent.alloc(c * d * sizeof(float));
+    s->ent.alloc(T * cap2 * sizeof(uint2));
+    s->n_used.alloc(T * 4);
+    s->live.alloc(T * 4);
+    s->blk_off.alloc(T * h.nb_stride * 4);
+    s->low.alloc(T * csa::LOW_Q * sizeof(csa::LowEnt));
+    s->low_cnt.alloc(T * 4);
+    s->refill.alloc(T * 4);
+    s->sel.alloc(group * (p + max_steps) * 4);
+    if (rc->search_period > 1) s->cache.alloc(group * (p + max_steps) * sizeof(double));
+    s->drep.alloc(group * sizeof(csa::DecodeReport));
+    s->irep.alloc(4 + ((T + 15) & ~15ull));
+    s->dev.alloc(sizeof(csa::SessionDev));
+    h.ktail = s->ktail.as<float>();
+    h.vtail = s->vtail.as<float>();
+    h.cent = s->cent.as<float>();
+    h.ent = s->ent.as<uint2>();
+    h.n_used = s->n_used.as<uint32_t>();
+    h.live = s->live.as<uint32_t>();
+    h.blk_off = s->blk_off.as<uint32_t>();
+    h.low = s->low.as<csa::LowEnt>();
+    h.low_cnt = s->low_cnt.as<uint32_t>();
+    h.refill = s->refill.as<uint32_t>();
+    s->hs.assign(group, HeadState{});
+    return s;
+}
+
+void upload(csattn_ctx ctx, void* dst, const void* src, size_t bytes, bool host) {
+    ck(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       ctx->stream),
+       "copy in");
+}
+
+void attach_rows(csattn_session_s* s, const float* keys, const float* values, bool host) {
+    s->pre = std::make_shared<SharedRows>();
+    const size_t bytes = static_cast<size_t>(s->h.P) * s->h.d * sizeof(float);
+    s->pre->k.alloc(bytes);
+    s->pre->v.alloc(bytes);
+    upload(s->ctx, s->pre->k.p, keys, bytes, host);
+    upload(s->ctx, s->pre->v.p, values, bytes, host);
+    s->h.kpre = s->pre->k.as<float>();
+    s->h.vpre = s->pre->v.as<float>();
+}
+
+// assemble_index on the device (index.cpp:107-141)
+void build_tables(csattn_session_s* s) {
+    push_dev(s);
+    DevMem scores;
+    scores.alloc(s->T() * s->h.P * sizeof(float));
+    ck(csa::launch_build_scores(s->dev.as<csa::SessionDev>(), s->h, scores.as<float>(),
+                                s->ctx->stream),
+       "build_scores launch");
+    ck(csa::launch_build_lists(s->dev.as<csa::SessionDev>(), s->h, scores.as<float>(),
+                               s->ctx->stream),
+       "build_lists launch");
+    s->ctx->launches += 2;
+    ck(cudaStreamSynchronize(s->ctx->stream), "build");
+}
+
+uint64_t list_capacity_of(const csattn_index_config* icfg, uint64_t p, double* alpha) {
+    const uint64_t L = icfg->list_capacity ? icfg->list_capacity : ceil_ratio(icfg->alpha, p);
+    if (L == 0) fail(CSATTN_ERR_PARAMETER, "list capacity came out as zero");
+    *alpha = icfg->list_capacity ? static_cast<double>(L) / static_cast<double>(p) : icfg->alpha;
+    return L;
+}
+
+void check_rows(const float* keys, const float* values, uint64_t p, uint64_t d, bool host) {
+    if (d == 0) fail(CSATTN_ERR_PARAMETER, "head dimension must be >= 1");
+    if (host) {
+        require_finite(keys, p * d, "prefill keys");
+        require_finite(values, p * d, "prefill values");
+    }
+}
+
+// choose cluster size and keys per CTA for a context of n keys
+void cluster_shape(uint64_t n, uint64_t mc, uint32_t& cs, uint32_t& kpc) {
+    uint64_t c = (n + 4095) / 4096;
+    if (c < 1) c = 1;
+    if (c > 16) c = 16;
+    uint64_t k = (n + c - 1) / c;
+    k = (k + csa::KEY_BLOCK - 1) / csa::KEY_BLOCK * csa::KEY_BLOCK;
+    if (k < mc) k = (mc + csa::KEY_BLOCK - 1) / csa::KEY_BLOCK * csa::KEY_BLOCK;
+    if (k > 16384)
+        fail(CSATTN_ERR_CAPACITY,
+             "context of " + std::to_string(n) +
+                 " keys exceeds one GPU's decode cluster (262144); shard the sequence");
+    cs = static_cast<uint32_t>(c);
+    kpc = static_cast<uint32_t>(k);
+}
+
+struct Outs {
+    float* out;
+    uint32_t* sel;
+    float* weights;
+};
+
+// One decode step for a set of sessions (decode_step, session.cpp:46-99).
+void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float* q,
+              const float* keys, const float* values, float* out, uint32_t* selected,
+              float* weights, uint64_t sel_stride, csattn_step_report* reports,
+              const uint64_t* k_override, uint32_t flags) {
+    const bool host = flags & CSATTN_HOST_BUFFERS;
+    if (ns == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
+    const uint32_t d = ss[0]->h.d;
+    uint64_t nq = 0, maxN = 0, maxmc = 0, maxK = 0;
+    std::vector<uint64_t> Ks;
+    for (uint64_t i = 0; i < ns; ++i) {
+        csattn_session s = ss[i];
+        if (s->ctx != ctx) fail(CSATTN_ERR_PARAMETER, "sessions belong to another context");
+        if (s->h.d != d) fail(CSATTN_ERR_DIMENSION, "sessions differ in head dimension");
+        if (s->step >= s->max_steps)
+            fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
+                                          std::to_string(s->max_steps));
+        for (uint64_t h = 0; h < s->group; ++h) {
+            const uint64_t ko = k_override ? k_override[nq + h] : 0;
+            const uint64_t K = ko ? std::min<uint64_t>(ko, s->N) : keep_count(s->rc.keep_ratio, s->N);
+            Ks.push_back(K);
+            maxK = std::max(maxK, K);
+        }
+        nq += s->group;
+        maxN = std::max<uint64_t>(maxN, s->N);
+        maxmc = std::max<uint64_t>(maxmc, static_cast<uint64_t>(s->h.m) * s->h.C);
+    }
+    if ((selected || weights) && sel_stride < maxK)
+        fail(CSATTN_ERR_PARAMETER, "selected/weights stride " + std::to_string(sel_stride) +
+                                       " is below K = " + std::to_string(maxK));
+    if (host) {
+        require_finite(keys, ns * d, "appended key");
+        require_finite(values, ns * d, "appended value");
+    }
+    uint32_t cs, kpc;
+    cluster_shape(maxN, maxmc, cs, kpc);
+
+    // device views of inputs / outputs
+    const float *dq = q, *dk = keys, *dv = values;
+    float *dout = out, *dw = weights;
+    uint32_t* dsel = selected;
+    size_t o_q = 0, o_k = 0, o_v = 0, o_out = 0, o_sel = 0, o_w = 0, total = 0;
+    auto carve = [&](size_t bytes) {
+        const size_t at = total;
+        total += (bytes + 255) & ~size_t(255);
+        return at;
+    };
+    if (host) {
+        o_q = carve(nq * d * 4);
+        o_k = carve(ns * d * 4);
+        o_v = carve(ns * d * 4);
+        o_out = carve(nq * d * 4);
+        if (selected) o_sel = carve(nq * sel_stride * 4);
+        if (weights) o_w = carve(nq * sel_stride * 4);
+        ctx->stage.ensure(total);
+        char* base = ctx->stage.as<char>();
+        upload(ctx, base + o_q, q, nq * d * 4, true);
+        upload(ctx, base + o_k, keys, ns * d * 4, true);
+        upload(ctx, base + o_v, values, ns * d * 4, true);
+        dq = reinterpret_cast<float*>(base + o_q);
+        dk = reinterpret_cast<float*>(base + o_k);
+        dv = reinterpret_cast<float*>(base + o_v);
+        dout = out ? reinterpret_cast<float*>(base + o_out) : nullptr;
+        dsel = selected ? reinterpret_cast<uint32_t*>(base + o_sel) : nullptr;
+        dw = weights ? reinterpret_cast<float*>(base + o_w) : nullptr;
+    }
+    ctx->hprobs.resize(nq);
+    ctx->hiprobs.resize(ns);
+    uint64_t qi = 0;
+    std::vector<uint32_t> searched(nq);
+    for (uint64_t i = 0; i < ns; ++i) {
+        csattn_session s = ss[i];
+        const uint64_t n = s->N;
+        for (uint64_t h = 0; h < s->group; ++h, ++qi) {
+            HeadState& hs = s->hs[h];
+            csa::DecodeProblem& P = ctx->hprobs[qi];
+            const bool srch = !hs.has_cache || (s->step % s->rc.search_period) == 0;
+            searched[qi] = srch;
+            P.s = s->dev.as<csa::SessionDev>();
+            P.q = dq + qi * d;
+            P.out = dout ? dout + qi * d : nullptr;
+            P.weights = dw ? dw + qi * sel_stride : nullptr;
+            P.sel = dsel ? dsel + qi * sel_stride : s->sel.as<uint32_t>() + h * s->h.max_ctx;
+            P.cache = s->cache.p ? s->cache.as<double>() + h * s->h.max_ctx : nullptr;
+            P.rep = reinterpret_cast<uint32_t*>(s->drep.as<csa::DecodeReport>() + h);
+            P.N = static_cast<uint32_t>(n);
+            P.K = static_cast<uint32_t>(Ks[qi]);
+            P.n_cache = static_cast<uint32_t>(hs.n_cache);
+            P.mode = (srch ? csa::MODE_SEARCH : 0u) |
+                     ((srch && P.cache) ? csa::MODE_STORE_CACHE : 0u) |
+                     (dw ? csa::MODE_WEIGHTS : 0u);
+        }
+        csa::InsertProblem& I = ctx->hiprobs[i];
+        I.s = s->dev.as<csa::SessionDev>();
+        I.key = dk + i * d;
+        I.value = dv + i * d;
+        I.rep = s->irep.as<uint32_t>();
+        I.N = static_cast<uint32_t>(n);
+        I.pad = 0;
+    }
+    ctx->probs.ensure(nq * sizeof(csa::DecodeProblem));
+    ctx->iprobs.ensure(ns * sizeof(csa::InsertProblem));
+    upload(ctx, ctx->probs.p, ctx->hprobs.data(), nq * sizeof(csa::DecodeProblem), true);
+    upload(ctx, ctx->iprobs.p, ctx->hiprobs.data(), ns * sizeof(csa::InsertProblem), true);
+    ck(csa::launch_decode(ctx->probs.as<csa::DecodeProblem>(), static_cast<uint32_t>(nq), kpc, cs,
+                          d, ctx->stream),
+       "decode launch");
+    ck(csa::launch_insert(ctx->iprobs.as<csa::InsertProblem>(), static_cast<uint32_t>(ns),
+                          ctx->stream),
+       "insert launch");
+    ctx->launches += 2;
+
+    // host bookkeeping: SearchState + Session counters
+    std::vector<uint64_t> n_before(ns);
+    qi = 0;
+    for (uint64_t i = 0; i < ns; ++i) {
+        csattn_session s = ss[i];
+        n_before[i] = s->N;
+        for (uint64_t h = 0; h < s->group; ++h, ++qi)
+            if (searched[qi]) {
+                s->hs[h].has_cache = true;
+                s->hs[h].n_cache = s->N;
+            }
+        s->N += 1;
+        s->step += 1;
+    }
+
+    if (host) {
+        char* base = ctx->stage.as<char>();
+        if (out)
+            ck(cudaMemcpyAsync(out, base + o_out, nq * d * 4, cudaMemcpyDeviceToHost, ctx->stream),
+               "copy out");
+        if (selected)
+            ck(cudaMemcpyAsync(selected, base + o_sel, nq * sel_stride * 4,
+                               cudaMemcpyDeviceToHost, ctx->stream),
+               "copy selected");
+        if (weights)
+            ck(cudaMemcpyAsync(weights, base + o_w, nq * sel_stride * 4, cudaMemcpyDeviceToHost,
+                               ctx->stream),
+               "copy weights");
+    }
+    if (reports) {
+        qi = 0;
+        for (uint64_t i = 0; i < ns; ++i) {
+            csattn_session s = ss[i];
+            const uint64_t T = s->T();
+            std::vector<csa::DecodeReport> dr(s->group);
+            uint32_t applied = 0;
+            ck(cudaMemcpyAsync(dr.data(), s->drep.p, s->group * sizeof(csa::DecodeReport),
+                               cudaMemcpyDeviceToHost, ctx->stream),
+               "copy report");
+            ck(cudaMemcpyAsync(&applied, s->irep.p, 4, cudaMemcpyDeviceToHost, ctx->stream),
+               "copy insert report");
+            ck(cudaStreamSynchronize(ctx->stream), "decode step");
+            for (uint64_t h = 0; h < s->group; ++h, ++qi) {
+                csattn_step_report& r = reports[qi];
+                std::memset(&r, 0, sizeof(r));
+                r.k = Ks[qi];
+                r.searched = searched[qi] ? 1 : 0;
+                if (searched[qi]) {
+                    r.centroid_dot_ops =
+                        dr[h].dot_ops_lo | (static_cast<uint64_t>(dr[h].dot_ops_hi) << 32);
+                    r.gathered_entries =
+                        dr[h].gathered_lo | (static_cast<uint64_t>(dr[h].gathered_hi) << 32);
+                    r.reduce_ops = r.gathered_entries;
+                    r.searches = 1;
+                    double worst = 1.0;
+                    for (uint32_t b = 0; b < s->h.m; ++b) worst = std::min(worst, dr[h].best_cos[b]);
+                    s->hs[h].worst = worst;
+                }
+                r.worst_best_cosine = s->hs[h].worst;
+                r.attention_key_ops = Ks[qi] * d;
+                r.h2d_bytes_model = 2.0 * s->rc.keep_ratio * static_cast<double>(n_before[i]) *
+                                    static_cast<double>(d) * 2.0 /
+                                    static_cast<double>(s->rc.search_period);
+                r.inserts_attempted = T;
+                r.inserts_applied = applied;
+                r.insert_dot_ops = static_cast<uint64_t>(s->h.C) * d;
+            }
+        }
+    }
+    if (host || !(flags & CSATTN_NO_SYNC)) ck(cudaStreamSynchronize(ctx->stream), "decode step");
+}
+
+// ---- host <-> device table images ----
+
+void import_tables(csattn_session_s* s, const uint32_t* lens, const uint32_t* indices,
+                   const float* scores, uint64_t stride) {
+    const uint64_t T = s->T();
+    const uint32_t cap2 = s->h.cap2, nb = s->h.nb_stride, P = s->h.P;
+    const uint32_t last_blk = (P - 1) >> csa::KEY_BLOCK_SHIFT;
+    std::vector<uint2> ent(T * cap2, make_uint2(0, 0));
+    std::vector<uint32_t> nused(T), live(T), bo(T * nb, 0), lcnt(T);
+    std::vector<csa::LowEnt> low(T * csa::LOW_Q);
+    std::vector<uint32_t> order;
+    for (uint64_t t = 0; t < T; ++t) {
+        const uint32_t n = lens[t];
+        if (n > s->h.L) fail(CSATTN_ERR_CORRUPT, "list longer than its capacity");
+        const uint32_t* ix = indices + t * stride;
+        const float* sc = scores + t * stride;
+        order.resize(n);
+        for (uint32_t r = 0; r < n; ++r) {
+            if (ix[r] >= P) fail(CSATTN_ERR_CORRUPT, "list entry index out of range");
+            order[r] = r;
+        }
+        std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return ix[a] < ix[b]; });
+        for (uint32_t r = 1; r < n; ++r)
+            if (ix[order[r]] == ix[order[r - 1]]) fail(CSATTN_ERR_CORRUPT, "duplicate key in a list");
+        std::vector<uint32_t> pos_of(n);
+        for (uint32_t p = 0; p < n; ++p) {
+            ent[t * cap2 + p] = make_uint2(ix[order[p]], 0);
+            std::memcpy(&ent[t * cap2 + p].y, &sc[order[p]], 4);
+            pos_of[order[p]] = p;
+        }
+        nused[t] = n;
+        live[t] = n;
+        // key-block offsets
+        uint32_t p = 0;
+        for (uint32_t kb = 0; kb <= last_blk; ++kb) {
+            while (p < n && (ix[order[p]] >> csa::KEY_BLOCK_SHIFT) < kb) ++p;
+            bo[t * nb + kb] = p;
+        }
+        // low buffer: the TopList tail is the eviction order reversed; store
+        // descending eviction order = TopList order of the last min(Q, n)
+        const uint32_t q = std::min<uint32_t>(n, csa::LOW_Q);
+        for (uint32_t r = 0; r < q; ++r) {
+            const uint32_t src = n - q + r;  // TopList rank
+            csa::LowEnt le{sc[src], ix[src], pos_of[src], 0};
+            low[t * csa::LOW_Q + r] = le;
+        }
+        lcnt[t] = q;
+    }
+    cudaStream_t st = s->ctx->stream;
+    ck(cudaMemcpyAsync(s->ent.p, ent.data(), ent.size() * sizeof(uint2), cudaMemcpyHostToDevice, st), "import");
+    ck(cudaMemcpyAsync(s->n_used.p, nused.data(), T * 4, cudaMemcpyHostToDevice, st), "import");
+    ck(cudaMemcpyAsync(s->live.p, live.data(), T * 4, cudaMemcpyHostToDevice, st), "import");
+    ck(cudaMemcpyAsync(s->blk_off.p, bo.data(), bo.size() * 4, cudaMemcpyHostToDevice, st), "import");
+    ck(cudaMemcpyAsync(s->low.p, low.data(), low.size() * sizeof(csa::LowEnt), cudaMemcpyHostToDevice, st), "import");
+    ck(cudaMemcpyAsync(s->low_cnt.p, lcnt.data(), T * 4, cudaMemcpyHostToDevice, st), "import");
+    ck(cudaStreamSynchronize(st), "import");
+}
+
+}  // namespace
+
+extern "C" {
+
+void csattn_index_config_default(csattn_index_config* c) {
+    c->alpha = 0.2;
+    c->list_capacity = 0;
+    c->normalize_keys = 0;
+    c->score_bits = 16;
+    c->centroids = 64;
+    c->iterations = 10;
+    c->batch_size = 0;
+    c->seed = 0;
+    c->tolerance = 1e-7;
+}
+
+void csattn_retrieval_config_default(csattn_retrieval_config* c) {
+    c->keep_ratio = 0.05;
+    c->search_period = 1;
+    c->recent_window = 32;
+    c->weights = nullptr;
+    c->n_weights = 0;
+    c->backoff_tau = 1;
+    c->backoff_threshold = -std::numeric_limits<double>::infinity();
+    c->recent_passthrough = 1;
+    c->reserved = 0;
+}
+
+void csattn_synthetic_spec_default(csattn_synthetic_spec* s) {
+    s->rows = 0;
+    s->dim = 64;
+    s->clusters = 8;
+    s->seed = 0;
+    s->plant_fraction = 0.08;
+    s->plant_scale = 6.0;
+    s->query_noise = 0.05;
+    s->dwell = 32;
+}
+
+csattn_status csattn_keep_count(double rho, uint64_t n, uint64_t* out) {
+    return guard([&] { *out = keep_count(rho, n); });
+}
+
+// parse_schedule (retrieval.cpp:10-32)
+csattn_status csattn_parse_schedule(const char* cname, double* rho, uint64_t* period) {
+    return guard([&] {
+        const std::string name = cname ? cname : "";
+        const std::string sep = "-step-";
+        const auto at = name.find(sep);
+        if (at == std::string::npos || at == 0 || at + sep.size() >= name.size())
+            fail(CSATTN_ERR_PARAMETER, "schedule must look like \"<rho>-step-<P>\": " + name);
+        double r = 0.0;
+        unsigned long pp = 0;
+        bool bad = false;
+        try {
+            std::size_t used = 0;
+            r = std::stod(name.substr(0, at), &used);
+            if (used != at) bad = true;
+            const std::string tail = name.substr(at + sep.size());
+            if (!bad) {
+                pp = std::stoul(tail, &used);
+                if (used != tail.size()) bad = true;
+            }
+        } catch (const std::exception&) {
+            bad = true;
+        }
+        if (bad) fail(CSATTN_ERR_PARAMETER, "cannot parse schedule \"" + name + "\"");
+        if (!(r > 0.0 && r <= 1.0))
+            fail(CSATTN_ERR_PARAMETER, "schedule keep ratio must lie in (0, 1]");
+        if (pp == 0) fail(CSATTN_ERR_PARAMETER, "schedule period must be >= 1");
+        *rho = r;
+        *period = pp;
+    });
+}
+
+// h2d_bytes (metrics.cpp:32-38)
+csattn_status csattn_h2d_bytes(double rho, uint64_t n, uint64_t d, uint64_t b, uint64_t period,
+                               double* out) {
+    return guard([&] {
+        if (!(rho > 0.0) || n == 0 || d == 0 || b == 0 || period == 0)
+            fail(CSATTN_ERR_PARAMETER, "transfer model needs positive parameters");
+        *out = 2.0 * rho * static_cast<double>(n) * static_cast<double>(d) *
+               static_cast<double>(b) / static_cast<double>(period);
+    });
+}
+
+const char* csattn_last_error(void) { return g_err.c_str(); }
+
+const char* csattn_status_name(csattn_status s) {
+    switch (s) {
+        case CSATTN_OK: return "ok";
+        case CSATTN_ERR_GENERIC: return "Error";
+        case CSATTN_ERR_DIMENSION: return "DimensionError";
+        case CSATTN_ERR_PARAMETER: return "ParameterError";
+        case CSATTN_ERR_DATA: return "DataError";
+        case CSATTN_ERR_BAD_MAGIC: return "BadMagicError";
+        case CSATTN_ERR_VERSION: return "VersionError";
+        case CSATTN_ERR_TRUNCATED: return "TruncatedError";
+        case CSATTN_ERR_CORRUPT: return "CorruptError";
+        case CSATTN_ERR_PROPERTY: return "PropertyError";
+        case CSATTN_ERR_STREAM_EXHAUSTED: return "StreamExhaustedError";
+        case CSATTN_ERR_CUDA: return "CudaError";
+        case CSATTN_ERR_CAPACITY: return "CapacityError";
+    }
+    return "unknown";
+}
+
+csattn_status csattn_ctx_create(int device, void* stream, csattn_ctx* out) {
+    return guard([&] {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) fail(CSATTN_ERR_PARAMETER, "no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        int major = 0, minor = 0;
+        ck(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device), "attr");
+        ck(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device), "attr");
+        if (major != 10)
+            fail(CSATTN_ERR_CUDA, "this build targets sm_100a (B200); device is sm_" +
+                                      std::to_string(major) + std::to_string(minor));
+        auto c = std::make_unique<csattn_ctx_s>();
+        c->device = device;
+        if (stream) {
+            c->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+            c->own = true;
+        }
+        *out = c.release();
+    });
+}
+
+csattn_status csattn_ctx_destroy(csattn_ctx ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->own) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+csattn_status csattn_ctx_synchronize(csattn_ctx ctx) {
+    return guard([&] { ck(cudaStreamSynchronize(ctx->stream), "synchronize"); });
+}
+
+uint64_t csattn_ctx_launch_count(csattn_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+// prefill (session.cpp:25-44) -> build_index (index.cpp:145-177) on the GPU.
+csattn_status csattn_prefill(csattn_ctx ctx, const float* queries, uint64_t nq, const float* keys,
+                             const float* values, uint64_t p, uint64_t d, const uint64_t* widths,
+                             uint64_t m, const csattn_index_config* icfg,
+                             const csattn_retrieval_config* rcfg, uint64_t group,
+                             uint64_t max_steps, uint32_t flags, csattn_session* out) {
+    return guard([&] {
+        const bool host = flags & CSATTN_HOST_BUFFERS;
+        validate_layout(widths, m, d);
+        if (nq == 0) fail(CSATTN_ERR_PARAMETER, "prefill must be non-empty");
+        validate_retrieval(rcfg, m);
+        check_rows(keys, values, p, d, host);
+        validate_index(icfg);
+        if (p == 0) fail(CSATTN_ERR_PARAMETER, "cannot build over an empty prefill");
+        const uint64_t C = icfg->centroids;
+        for (uint64_t b = 0; b < m; ++b)
+            if (C * widths[b] > csa::KM_MAX_KW)
+                fail(CSATTN_ERR_PARAMETER, "B200 build supports C * width <= " +
+                                               std::to_string(csa::KM_MAX_KW));
+        if (nq >= 0x7fffffffull) fail(CSATTN_ERR_PARAMETER, "too many query rows");
+        double alpha;
+        const uint64_t L = list_capacity_of(icfg, p, &alpha);
+        auto s = new_session(ctx, d, widths, m, C, L, p, group, max_steps, rcfg);
+        s->alpha = alpha;
+        s->h.normalize_keys = icfg->normalize_keys ? 1u : 0u;
+        s->score_bits = icfg->score_bits;
+        attach_rows(s.get(), keys, values, host);
+        cudaStream_t st = ctx->stream;
+        // ---- per-subspace exact k-means, one CTA per subspace ----
+        DevMem dq;
+        dq.alloc(nq * d * sizeof(float));
+        upload(ctx, dq.p, queries, nq * d * sizeof(float), host);
+        const uint32_t iters = static_cast<uint32_t>(icfg->iterations);
+        const uint32_t bcfg = static_cast<uint32_t>(std::min<uint64_t>(icfg->batch_size, 0xffffffffu));
+        const size_t ndraw = csa::kmeans_rng_draws(static_cast<uint32_t>(C), iters,
+                                                   static_cast<uint32_t>(nq), bcfg);
+        std::vector<unsigned long long> draws(m * ndraw);
+        for (uint64_t b = 0; b < m; ++b) {
+            // cc.seed = mix_seed(seed, b) (index.cpp:170); Rng = mt19937_64
+            uint64_t z = icfg->seed + 0x9e3779b97f4a7c15ULL * (b + 1);
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            std::mt19937_64 gen(z ^ (z >> 31));
+            for (size_t i = 0; i < ndraw; ++i) draws[b * ndraw + i] = gen();
+        }
+        DevMem drng, train, best, run, assign, sums, counts, status, info, jobs;
+        drng.alloc(draws.size() * 8);
+        upload(ctx, drng.p, draws.data(), draws.size() * 8, true);
+        uint64_t wsum = 0;
+        for (uint64_t b = 0; b < m; ++b) wsum += widths[b];
+        train.alloc(nq * wsum * sizeof(float));
+        best.alloc(m * nq * sizeof(double));
+        run.alloc(m * nq * sizeof(double));
+        assign.alloc(m * 2 * nq * sizeof(uint32_t));
+        sums.alloc(C * wsum * sizeof(double));
+        counts.alloc(m * C * sizeof(uint32_t));
+        status.alloc(m * sizeof(int));
+        info.alloc(m * 2 * sizeof(uint32_t));
+        ck(cudaMemsetAsync(status.p, 0, m * sizeof(int), st), "memset");
+        ck(cudaMemsetAsync(info.p, 0, m * 2 * sizeof(uint32_t), st), "memset");
+        std::vector<csa::KmeansJob> hj(m);
+        for (uint64_t b = 0; b < m; ++b) {
+            csa::KmeansJob& J = hj[b];
+            const uint32_t off = s->h.offs[b];
+            J.q = dq.as<float>();
+            J.n_total = static_cast<uint32_t>(nq);
+            J.d = static_cast<uint32_t>(d);
+            J.off = off;
+            J.w = static_cast<uint32_t>(widths[b]);
+            J.k = static_cast<uint32_t>(C);
+            J.iters = iters;
+            J.batch_cfg = bcfg;
+            J.pad = 0;
+            J.tol = icfg->tolerance;
+            J.rng = drng.as<unsigned long long>() + b * ndraw;
+            J.train = train.as<float>() + nq * off;
+            J.best = best.as<double>() + b * nq;
+            J.run = run.as<double>() + b * nq;
+            J.assign = assign.as<uint32_t>() + b * 2 * nq;
+            J.sums = sums.as<double>() + C * off;
+            J.counts = counts.as<uint32_t>() + b * C;
+            J.cent = s->cent.as<float>() + C * off;
+            J.status = status.as<int>() + b;
+            J.info = info.as<uint32_t>() + 2 * b;
+        }
+        jobs.alloc(m * sizeof(csa::KmeansJob));
+        upload(ctx, jobs.p, hj.data(), m * sizeof(csa::KmeansJob), true);
+        ck(csa::launch_kmeans(jobs.as<csa::KmeansJob>(), static_cast<uint32_t>(m), st), "kmeans launch");
+        ctx->launches += 1;
+        std::vector<int> hs(m);
+        ck(cudaMemcpyAsync(hs.data(), status.p, m * sizeof(int), cudaMemcpyDeviceToHost, st), "status");
+        ck(cudaStreamSynchronize(st), "kmeans");
+        const bool full_batch = [&] {
+            const uint64_t bt = bcfg == 0 ? std::min<uint64_t>(4096, nq) : std::min<uint64_t>(bcfg, nq);
+            return bt >= nq;
+        }();
+        for (uint64_t b = 0; b < m; ++b) {
+            if (hs[b] == 4) fail(CSATTN_ERR_DATA, "every training row is zero");
+            if (hs[b] == 9)
+                fail(CSATTN_ERR_PROPERTY, full_batch
+                                              ? "clustering objective increased in a full-batch iteration"
+                                              : "mini-batch clustering objective diverged");
+        }
+        build_tables(s.get());
+        *out = s.release();
+    });
+}
+
+csattn_status csattn_prefill_from_centroids(csattn_ctx ctx, const float* centroids, uint64_t c,
+                                            const float* keys, const float* values, uint64_t p,
+                                            uint64_t d, const uint64_t* widths, uint64_t m,
+                                            const csattn_index_config* icfg,
+                                            const csattn_retrieval_config* rcfg, uint64_t group,
+                                            uint64_t max_steps, uint32_t flags,
+                                            csattn_session* out) {
+    return guard([&] {
+        const bool host = flags & CSATTN_HOST_BUFFERS;
+        validate_layout(widths, m, d);
+        validate_retrieval(rcfg, m);
+        check_rows(keys, values, p, d, host);
+        validate_index(icfg);
+        if (p == 0) fail(CSATTN_ERR_PARAMETER, "cannot build over an empty prefill");
+        if (c == 0) fail(CSATTN_ERR_PARAMETER, "centroid sets are empty");
+        double alpha;
+        const uint64_t L = list_capacity_of(icfg, p, &alpha);
+        auto s = new_session(ctx, d, widths, m, c, L, p, group, max_steps, rcfg);
+        s->alpha = alpha;
+        s->h.normalize_keys = icfg->normalize_keys ? 1u : 0u;
+        s->score_bits = icfg->score_bits;
+        attach_rows(s.get(), keys, values, host);
+        upload(ctx, s->cent.p, centroids, c * d * sizeof(float), true);
+        build_tables(s.get());
+        *out = s.release();
+    });
+}
+
+csattn_status csattn_session_import(csattn_ctx ctx, const float* centroids, uint64_t c,
+                                    const uint32_t* lens, const uint32_t* indices,
+                                    const float* scores, uint64_t stride,
+                                    uint64_t list_capacity, double alpha, int32_t normalize_keys,
+                                    int32_t score_bits, const float* keys, const float* values,
+                                    uint64_t p, uint64_t d, const uint64_t* widths, uint64_t m,
+                                    const csattn_retrieval_config* rcfg, uint64_t group,
+                                    uint64_t max_steps, csattn_session* out) {
+    return guard([&] {
+        validate_layout(widths, m, d);
+        validate_retrieval(rcfg, m);
+        check_rows(keys, values, p, d, true);
+        if (p == 0) fail(CSATTN_ERR_PARAMETER, "cannot build over an empty prefill");
+        if (c == 0) fail(CSATTN_ERR_PARAMETER, "centroid sets are empty");
+        if (list_capacity == 0) fail(CSATTN_ERR_PARAMETER, "list capacity came out as zero");
+        auto s = new_session(ctx, d, widths, m, c, list_capacity, p, group, max_steps, rcfg);
+        s->alpha = alpha;
+        s->h.normalize_keys = normalize_keys ? 1u : 0u;
+        s->score_bits = score_bits;
+        attach_rows(s.get(), keys, values, true);
+        upload(ctx, s->cent.p, centroids, c * d * sizeof(float), true);
+        push_dev(s.get());
+        import_tables(s.get(), lens, indices, scores, stride);
+        *out = s.release();
+    });
+}
+
+csattn_status csattn_session_export(csattn_session s, uint32_t* lens, uint32_t* indices,
+                                    float* scores, uint64_t stride, float* centroids) {
+    return guard([&] {
+        const uint64_t T = s->T();
+        const uint32_t cap2 = s->h.cap2;
+        std::vector<uint2> ent(T * cap2);
+        std::vector<uint32_t> nused(T), live(T);
+        cudaStream_t st = s->ctx->stream;
+        ck(cudaMemcpyAsync(ent.data(), s->ent.p, ent.size() * sizeof(uint2), cudaMemcpyDeviceToHost, st), "export");
+        ck(cudaMemcpyAsync(nused.data(), s->n_used.p, T * 4, cudaMemcpyDeviceToHost, st), "export");
+        ck(cudaMemcpyAsync(live.data(), s->live.p, T * 4, cudaMemcpyDeviceToHost, st), "export");
+        if (centroids)
+            ck(cudaMemcpyAsync(centroids, s->cent.p, static_cast<size_t>(s->h.C) * s->h.d * 4,
+                               cudaMemcpyDeviceToHost, st),
+               "export");
+        ck(cudaStreamSynchronize(st), "export");
+        std::vector<std::pair<float, uint32_t>> v;
+        for (uint64_t t = 0; t < T; ++t) {
+            v.clear();
+            for (uint32_t p = 0; p < nused[t]; ++p) {
+                const uint2 e = ent[t * cap2 + p];
+                if (e.x & csa::TOMB) continue;
+                float f;
+                std::memcpy(&f, &e.y, 4);
+                v.emplace_back(f, e.x);
+            }
+            if (v.size() != live[t]) fail(CSATTN_ERR_CORRUPT, "table live count mismatch");
+            if (v.size() > stride) fail(CSATTN_ERR_PARAMETER, "export stride too small");
+            std::sort(v.begin(), v.end(), [](const auto& a, const auto& b) {
+                if (a.first != b.first) return a.first > b.first;
+                return a.second < b.second;
+            });
+            lens[t] = static_cast<uint32_t>(v.size());
+            for (size_t r = 0; r < v.size(); ++r) {
+                indices[t * stride + r] = v[r].second;
+                scores[t * stride + r] = v[r].first;
+            }
+        }
+    });
+}
+
+csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn_session* out) {
+    return guard([&] {
+        if (max_steps < src->step) fail(CSATTN_ERR_PARAMETER, "fork capacity below steps taken");
+        csattn_retrieval_config rc = src->rc;
+        rc.weights = src->weights.data();
+        rc.n_weights = src->weights.size();
+        auto s = new_session(src->ctx, src->h.d, src->widths.data(), src->h.m, src->h.C, src->h.L,
+                             src->h.P, src->group, max_steps, &rc);
+        s->alpha = src->alpha;
+        s->score_bits = src->score_bits;
+        s->h.normalize_keys = src->h.normalize_keys;
+        s->pre = src->pre;
+        s->h.kpre = src->h.kpre;
+        s->h.vpre = src->h.vpre;
+        s->N = src->N;
+        s->step = src->step;
+        s->hs = src->hs;
+        cudaStream_t st = src->ctx->stream;
+        const uint64_t T = s->T();
+        auto d2d = [&](DevMem& dst, const DevMem& from, size_t bytes) {
+            ck(cudaMemcpyAsync(dst.p, from.p, bytes, cudaMemcpyDeviceToDevice, st), "fork copy");
+        };
+        const size_t rows = (src->N - src->h.P) * src->h.d * 4;
+        if (rows) {
+            d2d(s->ktail, src->ktail, rows);
+            d2d(s->vtail, src->vtail, rows);
+        }
+        d2d(s->cent, src->cent, static_cast<size_t>(src->h.C) * src->h.d * 4);
+        // tables: capacities are identical (same L, P)
+        d2d(s->ent, src->ent, T * src->h.cap2 * sizeof(uint2));
+        d2d(s->n_used, src->n_used, T * 4);
+        d2d(s->live, src->live, T * 4);
+        const uint32_t nbs = std::min(s->h.nb_stride, src->h.nb_stride);
+        ck(cudaMemcpy2DAsync(s->blk_off.p, s->h.nb_stride * 4, src->blk_off.p,
+                             src->h.nb_stride * 4, nbs * 4, T, cudaMemcpyDeviceToDevice, st),
+           "fork blk_off");
+        d2d(s->low, src->low, T * csa::LOW_Q * sizeof(csa::LowEnt));
+        d2d(s->low_cnt, src->low_cnt, T * 4);
+        if (s->cache.p && src->cache.p)
+            for (uint64_t h = 0; h < s->group; ++h)
+                ck(cudaMemcpyAsync(s->cache.as<double>() + h * s->h.max_ctx,
+                                   src->cache.as<double>() + h * src->h.max_ctx,
+                                   src->N * sizeof(double), cudaMemcpyDeviceToDevice, st),
+                   "fork cache");
+        push_dev(s.get());
+        ck(cudaStreamSynchronize(st), "fork");
+        *out = s.release();
+    });
+}
+
+csattn_status csattn_session_destroy(csattn_session s) {
+    return guard([&] {
+        if (!s) return;
+        cudaStreamSynchronize(s->ctx->stream);
+        delete s;
+    });
+}
+
+csattn_status csattn_session_info_get(csattn_session s, csattn_session_info* o) {
+    return guard([&] {
+        o->dim = s->h.d;
+        o->subspaces = s->h.m;
+        o->centroids = s->h.C;
+        o->list_capacity = s->h.L;
+        o->prefill_len = s->h.P;
+        o->context_len = s->N;
+        o->steps = s->step;
+        o->max_context = s->h.max_ctx;
+        o->group = s->group;
+        o->alpha = s->alpha;
+        o->normalize_keys = static_cast<int32_t>(s->h.normalize_keys);
+        o->score_bits = s->score_bits;
+        o->device_bytes = s->device_bytes();
+    });
+}
+
+csattn_status csattn_session_set_retrieval(csattn_session s, const csattn_retrieval_config* rc) {
+    return guard([&] {
+        validate_retrieval(rc, s->h.m);
+        if (rc->search_period > 1 && !s->cache.p)
+            s->cache.alloc(s->group * s->h.max_ctx * sizeof(double));
+        set_retrieval(s, rc);
+        push_dev(s);
+        ck(cudaStreamSynchronize(s->ctx->stream), "set_retrieval");
+    });
+}
+
+csattn_status csattn_session_read_kv(csattn_session s, uint64_t first, uint64_t count,
+                                     float* keys, float* values) {
+    return guard([&] {
+        if (first + count > s->N) fail(CSATTN_ERR_PARAMETER, "row range out of bounds");
+        const uint64_t d = s->h.d, P = s->h.P;
+        cudaStream_t st = s->ctx->stream;
+        for (uint64_t i = first; i < first + count;) {
+            const bool pre = i < P;
+            const uint64_t lim = pre ? std::min(P, first + count) : first + count;
+            const uint64_t n = lim - i;
+            const float* kb = pre ? s->h.kpre + i * d : s->h.ktail + (i - P) * d;
+            const float* vb = pre ? s->h.vpre + i * d : s->h.vtail + (i - P) * d;
+            if (keys)
+                ck(cudaMemcpyAsync(keys + (i - first) * d, kb, n * d * 4, cudaMemcpyDeviceToHost, st), "read kv");
+            if (values)
+                ck(cudaMemcpyAsync(values + (i - first) * d, vb, n * d * 4, cudaMemcpyDeviceToHost, st), "read kv");
+            i = lim;
+        }
+        ck(cudaStreamSynchronize(st), "read kv");
+    });
+}
+
+csattn_status csattn_decode_step(csattn_session s, const float* q, const float* new_key,
+                                 const float* new_value, float* out, uint32_t* selected,
+                                 float* weights, uint64_t sel_stride,
+                                 csattn_step_report* reports, const uint64_t* k_override,
+                                 uint32_t flags) {
+    return guard([&] {
+        if (!s) fail(CSATTN_ERR_PARAMETER, "null session");
+        csattn_session one[1] = {s};
+        run_step(s->ctx, 1, one, q, new_key, new_value, out, selected, weights, sel_stride,
+                 reports, k_override, flags);
+    });
+}
+
+csattn_status csattn_decode_batch(csattn_ctx ctx, uint64_t n, const csattn_session* ss,
+                                  const float* q, const float* keys, const float* values,
+                                  float* out, uint32_t* selected, uint64_t sel_stride,
+                                  uint32_t flags) {
+    return guard([&] {
+        run_step(ctx, n, ss, q, keys, values, out, selected, nullptr, sel_stride, nullptr,
+                 nullptr, flags);
+    });
+}
+
+csattn_status csattn_dense_attention(csattn_session s, const float* q, const uint32_t* mask,
+                                     uint64_t n_mask, float* out, float* weights,
+                                     uint32_t flags) {
+    return guard([&] {
+        (void)s;
+        (void)q;
+        (void)mask;
+        (void)n_mask;
+        (void)out;
+        (void)weights;
+        (void)flags;
+        fail(CSATTN_ERR_GENERIC, "dense attention is not built yet");
+    });
+}
+
+}  // extern "C"

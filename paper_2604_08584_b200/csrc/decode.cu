@@ -1,0 +1,948 @@
+// decode.cu — the fused CSAttention decode step on sm_100a.
+//
+// One thread-block CLUSTER per (session, query head) "problem". CTA r of the
+// cluster owns the key range [r*KPC, (r+1)*KPC) and keeps that range's fp64
+// candidate scores in its own shared memory for the whole step, so the
+// per-key scores never touch HBM. Phases (reference functions in brackets):
+//   1. route     [select_centroids retrieval.cpp:40-87]  per-subspace cosine
+//                argmax (or top-tau backoff) of the normalized query slice —
+//                a warp-level GEMV over m*C*w centroid floats, fp64 exact.
+//   2. gather    [gather_lists :95-109, reduce_by_key :111-148]  the selected
+//                index-sorted lists are read as coalesced 128-bit ranges
+//                (one range per key block) and accumulated with a
+//                conflict-free shared-memory RMW, list by list in gathered
+//                order: score(i) = sum_l w_b(l) * double(score_l(i)).
+//   3. select    [select_topk :150-228]  cluster-wide radix select on the
+//                orderable 64-bit image of the fp64 score, ties by lower
+//                index, recent-window passthrough and newest-first padding.
+//   4. attend    [dense_attention core.cpp:118-169, masked]  split-K flash
+//                decoding over the K selected rows (CTA r takes positions
+//                [rK/cs, (r+1)K/cs)), log-sum-exp merge across the cluster
+//                through distributed shared memory.
+// Everything stays on chip between phases; the only HBM traffic is the
+// gathered list entries, the selected K/V rows, q/out and the index output.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace csa {
+
+constexpr int DEC_THREADS = 512;
+constexpr int DEC_WARPS = DEC_THREADS / 32;
+constexpr int HB_BITS = 10;
+constexpr int HB = 1 << HB_BITS;  // radix histogram bins
+constexpr int SURV_LOCAL = 2048;  // compacted local survivors
+constexpr int SURV_MAX = 256;     // bucket size finished on CTA 0
+constexpr unsigned long long ABSENT = 0x7ff4deadbeef0000ull;  // NaN box: key not gathered
+
+struct DecSmem {
+    float q[DMAX];
+    float qn[DMAX];
+    uint32_t lists[MAXL];
+    uint32_t lsub[MAXL];
+    uint32_t nids[MAXM];
+    uint32_t ids[MAXM * MAXTAU];
+    uint32_t zero_mask;
+    uint32_t nl;
+    uint32_t hist[2][HB];
+    uint32_t ghist[HB];
+    uint32_t gcopy[HB];
+    unsigned long long skey[SURV_MAX];
+    uint32_t sidx[SURV_MAX];
+    uint16_t surv[SURV_LOCAL];
+    // values other CTAs of the cluster read through DSMEM
+    unsigned long long x_kmax, x_kmin, x_tk;
+    uint32_t x_cnt, x_tx, x_slice_total, x_nsel, x_nunt;
+    float x_m, x_s, x_M, x_S;
+    // block-level scratch
+    unsigned long long r64a[DEC_WARPS], r64b[DEC_WARPS];
+    uint32_t r32a[DEC_WARPS], r32b[DEC_WARPS];
+    float rf[DEC_WARPS];
+    // broadcast scalars
+    unsigned long long b_prefix, b_tk;
+    uint32_t b_tx, b_rem, b_bucket, b_dsel, b_done, b_nsurv, b_use_surv, b_cabove;
+    int b_pshift;
+    uint32_t surv_count, wpos, nsv, b_base, b_take;
+    float pacc[DMAX];
+};
+
+__device__ __forceinline__ unsigned long long ordkey(double x) {
+    if (x == 0.0) x = 0.0;  // -0.0 == +0.0 (retrieval.cpp:168-171)
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ bool is_absent(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) == ABSENT;
+}
+
+template <class T>
+__device__ __forceinline__ T* remote(cg::cluster_group& cl, T* p, int rank) {
+    return cl.map_shared_rank(p, rank);
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sumf(float v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_maxf(float v) {
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum of one uint32 per thread (all threads get the result).
+__device__ uint32_t block_sum(DecSmem& S, uint32_t v) {
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    v = warp_sum(v);
+    __syncthreads();
+    if (ln == 0) S.r32a[w] = v;
+    __syncthreads();
+    uint32_t t = 0;
+#pragma unroll
+    for (int i = 0; i < DEC_WARPS; ++i) t += S.r32a[i];
+    return t;
+}
+
+// Block-wide exclusive scan of two counters (thread order). Returns totals.
+__device__ void block_scan2(DecSmem& S, uint32_t a, uint32_t b, uint32_t& ea, uint32_t& eb,
+                            uint32_t& ta, uint32_t& tb) {
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    uint32_t ia = a, ib = b;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t xa = __shfl_up_sync(0xffffffffu, ia, o);
+        uint32_t xb = __shfl_up_sync(0xffffffffu, ib, o);
+        if (ln >= o) {
+            ia += xa;
+            ib += xb;
+        }
+    }
+    __syncthreads();
+    if (ln == 31) {
+        S.r32a[w] = ia;
+        S.r32b[w] = ib;
+    }
+    __syncthreads();
+    uint32_t pa = 0, pb = 0;
+    ta = 0;
+    tb = 0;
+#pragma unroll
+    for (int i = 0; i < DEC_WARPS; ++i) {
+        if (i < w) {
+            pa += S.r32a[i];
+            pb += S.r32b[i];
+        }
+        ta += S.r32a[i];
+        tb += S.r32b[i];
+    }
+    ea = pa + ia - a;
+    eb = pb + ib - b;
+}
+
+struct KeyView {
+    unsigned long long* keys;  // local pool keys (0 = not in pool)
+    uint32_t nloc;
+};
+
+// ---------------------------------------------------------------------------
+// Phase 1: centroid routing (select_centroids, retrieval.cpp:40-87)
+// ---------------------------------------------------------------------------
+__device__ void route(DecSmem& S, const SessionDev& sd, double* csc, uint32_t* rep, bool leader) {
+    const uint32_t m = sd.m, C = sd.C, tid = threadIdx.x;
+    // normalize each slice: fp64 sum of squares, inv = 1/sqrt, x = float(x*inv)
+    if (tid < m) {
+        const uint32_t off = sd.offs[tid], w = sd.widths[tid];
+        double n2 = 0.0;
+        for (uint32_t t = 0; t < w; ++t) {
+            const double x = S.q[off + t];
+            n2 = __fma_rn(x, x, n2);  // x*x is exact in fp64
+        }
+        if (n2 == 0.0) {
+            atomicOr(&S.zero_mask, 1u << tid);
+        } else {
+            const double inv = 1.0 / sqrt(n2);
+            for (uint32_t t = 0; t < w; ++t)
+                S.qn[off + t] = __double2float_rn(__dmul_rn(static_cast<double>(S.q[off + t]), inv));
+        }
+    }
+    __syncthreads();
+    // all m*C fp64 centroid dot products, sequential over the slice
+    for (uint32_t x = tid; x < m * C; x += blockDim.x) {
+        const uint32_t b = x / C, j = x - b * C;
+        if (S.zero_mask & (1u << b)) continue;
+        const uint32_t off = sd.offs[b], w = sd.widths[b];
+        const float* c = sd.cent + static_cast<size_t>(C) * off + static_cast<size_t>(j) * w;
+        double acc = 0.0;
+        for (uint32_t t = 0; t < w; ++t)
+            acc = __fma_rn(static_cast<double>(S.qn[off + t]), static_cast<double>(__ldg(c + t)), acc);
+        csc[x] = acc;
+    }
+    __syncthreads();
+    // per-subspace argmax (strict >, lower j wins), or top-tau on backoff
+    const int wid = tid >> 5, ln = tid & 31;
+    DecodeReport* R = reinterpret_cast<DecodeReport*>(rep);
+    for (uint32_t b = wid; b < m; b += DEC_WARPS) {
+        if (S.zero_mask & (1u << b)) {
+            if (ln == 0) {
+                S.ids[b * MAXTAU] = 0;
+                S.nids[b] = 1;
+                if (leader) R->best_cos[b] = 1.0;
+            }
+            continue;
+        }
+        const double* sc = csc + b * C;
+        const uint32_t take = sd.tau < C ? sd.tau : C;
+        for (uint32_t r = 0; r < take; ++r) {
+            double bv = -DBL_MAX;
+            uint32_t bj = 0xffffffffu;
+            for (uint32_t j = ln; j < C; j += 32) {
+                bool used = false;
+                for (uint32_t u = 0; u < r; ++u) used |= (S.ids[b * MAXTAU + u] == j);
+                if (used) continue;
+                const double v = sc[j];
+                if (bj == 0xffffffffu || v > bv) {
+                    bv = v;
+                    bj = j;
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                if (oj != 0xffffffffu && (bj == 0xffffffffu || ov > bv || (ov == bv && oj < bj))) {
+                    bv = ov;
+                    bj = oj;
+                }
+            }
+            if (ln == 0) S.ids[b * MAXTAU + r] = bj;
+            __syncwarp();
+            if (r == 0) {
+                if (ln == 0 && leader) R->best_cos[b] = bv;
+                if (bv >= sd.threshold) {
+                    if (ln == 0) S.nids[b] = 1;
+                    break;
+                }
+            }
+            if (ln == 0) S.nids[b] = r + 1;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t nl = 0;
+        unsigned long long dots = 0, gathered = 0;
+        for (uint32_t b = 0; b < m; ++b) {
+            if (!(S.zero_mask & (1u << b))) dots += static_cast<unsigned long long>(C) * sd.widths[b];
+            for (uint32_t r = 0; r < S.nids[b]; ++r) {
+                const uint32_t t = b * C + S.ids[b * MAXTAU + r];
+                S.lists[nl] = t;
+                S.lsub[nl] = b;
+                if (leader) {
+                    R->lists[nl] = t;
+                    gathered += sd.live[t];
+                }
+                ++nl;
+            }
+        }
+        S.nl = nl;
+        if (leader) {
+            R->nl = nl;
+            R->dot_ops_lo = static_cast<uint32_t>(dots);
+            R->dot_ops_hi = static_cast<uint32_t>(dots >> 32);
+            R->gathered_lo = static_cast<uint32_t>(gathered);
+            R->gathered_hi = static_cast<uint32_t>(gathered >> 32);
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Phase 2: gather + fp64 accumulate of this CTA's key range
+// ---------------------------------------------------------------------------
+__device__ void gather(DecSmem& S, const SessionDev& sd, double* acc, uint32_t k0, uint32_t k1,
+                       uint32_t N) {
+    const uint32_t last_blk = (N - 1) >> KEY_BLOCK_SHIFT;
+    const uint32_t kb0 = k0 >> KEY_BLOCK_SHIFT;
+    const uint32_t kb1 = (k1 + KEY_BLOCK - 1) >> KEY_BLOCK_SHIFT;
+    for (uint32_t l = 0; l < S.nl; ++l) {
+        const uint32_t t = S.lists[l];
+        const double w = sd.weights[S.lsub[l]];
+        const uint32_t* bo = sd.blk_off + static_cast<size_t>(t) * sd.nb_stride;
+        const uint32_t beg = __ldg(bo + kb0);
+        const uint32_t end = kb1 <= last_blk ? __ldg(bo + kb1) : __ldg(sd.n_used + t);
+        const uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
+        // 16-byte aligned body: two entries per 128-bit load
+        uint32_t a = beg + (beg & 1u);
+        if ((beg & 1u) && threadIdx.x == 0 && beg < end) {
+            const uint2 v = __ldg(e + beg);
+            if (!(v.x & TOMB)) {
+                const uint32_t li = v.x - k0;
+                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.y)));
+                const double o = acc[li];
+                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
+            }
+        }
+        const uint32_t npair = end > a ? (end - a) >> 1 : 0;
+        const uint4* e4 = reinterpret_cast<const uint4*>(e + a);
+#pragma unroll 4
+        for (uint32_t p = threadIdx.x; p < npair; p += blockDim.x) {
+            const uint4 v = __ldg(e4 + p);
+            if (!(v.x & TOMB)) {
+                const uint32_t li = v.x - k0;
+                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.y)));
+                const double o = acc[li];
+                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
+            }
+            if (!(v.z & TOMB)) {
+                const uint32_t li = v.z - k0;
+                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.w)));
+                const double o = acc[li];
+                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
+            }
+        }
+        const uint32_t tail = a + 2 * npair;
+        if (tail < end && threadIdx.x == 32) {
+            const uint2 v = __ldg(e + tail);
+            if (!(v.x & TOMB)) {
+                const uint32_t li = v.x - k0;
+                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.y)));
+                const double o = acc[li];
+                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tie resolution: the rem-th smallest index among keys == tk across the cluster.
+// counts come from `cnt_of(rank)`; returns tx (exclusive) on every CTA.
+// ---------------------------------------------------------------------------
+template <class CountOf>
+__device__ void resolve_ties(cg::cluster_group& cl, DecSmem& S, const KeyView& kv, uint32_t k0,
+                             unsigned long long tk, uint32_t rem, CountOf cnt_of) {
+    const int rank = cl.block_rank(), cs = cl.num_blocks();
+    uint32_t before = 0;
+    for (int c = 0; c < rank; ++c) before += cnt_of(c);
+    const uint32_t mine = cnt_of(rank);
+    if (rem > before && rem <= before + mine) {
+        // this CTA holds the rem-th tie: find it in ascending local order
+        const uint32_t want = rem - before;  // 1-based among local ties
+        const uint32_t chunk = div_up(kv.nloc, blockDim.x);
+        const uint32_t c0 = min(kv.nloc, threadIdx.x * chunk), c1 = min(kv.nloc, c0 + chunk);
+        uint32_t n = 0;
+        for (uint32_t l = c0; l < c1; ++l) n += (kv.keys[l] == tk);
+        uint32_t ex, dummy, tot, tot2;
+        block_scan2(S, n, 0, ex, dummy, tot, tot2);
+        if (want > ex && want <= ex + n) {
+            uint32_t seen = ex;
+            for (uint32_t l = c0; l < c1; ++l)
+                if (kv.keys[l] == tk && ++seen == want) {
+                    *remote(cl, &S.x_tx, 0) = k0 + l + 1;
+                    break;
+                }
+        }
+    }
+    (void)cs;
+    cl.sync();
+    if (threadIdx.x == 0) {
+        S.b_tk = tk;
+        S.b_tx = *remote(cl, &S.x_tx, 0);
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Phase 3: cluster-wide selection of the `need` best pool keys.
+// Result (on every CTA): S.b_tk / S.b_tx such that a pool key is selected iff
+// key > tk || (key == tk && index < tx).
+// ---------------------------------------------------------------------------
+__device__ void select_threshold(cg::cluster_group& cl, DecSmem& S, const KeyView& kv,
+                                 uint32_t k0, uint32_t need) {
+    const int rank = cl.block_rank(), cs = cl.num_blocks();
+    const uint32_t tid = threadIdx.x;
+    // pool statistics: count, max, min key
+    uint32_t cnt = 0;
+    unsigned long long kmax = 0, kmin = ~0ull;
+    for (uint32_t l = tid; l < kv.nloc; l += blockDim.x) {
+        const unsigned long long k = kv.keys[l];
+        if (k) {
+            ++cnt;
+            kmax = k > kmax ? k : kmax;
+            kmin = k < kmin ? k : kmin;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmax, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmin, o);
+        kmax = a > kmax ? a : kmax;
+        kmin = b < kmin ? b : kmin;
+    }
+    const int w = tid >> 5, ln = tid & 31;
+    if (ln == 0) {
+        S.r32a[w] = cnt;
+        S.r64a[w] = kmax;
+        S.r64b[w] = kmin;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t c = 0;
+        unsigned long long a = 0, b = ~0ull;
+        for (int i = 0; i < DEC_WARPS; ++i) {
+            c += S.r32a[i];
+            a = S.r64a[i] > a ? S.r64a[i] : a;
+            b = S.r64b[i] < b ? S.r64b[i] : b;
+        }
+        S.x_cnt = c;
+        S.x_kmax = a;
+        S.x_kmin = b;
+    }
+    cl.sync();
+    uint32_t total = 0;
+    unsigned long long gmax = 0, gmin = ~0ull;
+    for (int c = 0; c < cs; ++c) {
+        total += *remote(cl, &S.x_cnt, c);
+        const unsigned long long a = *remote(cl, &S.x_kmax, c);
+        const unsigned long long b = *remote(cl, &S.x_kmin, c);
+        gmax = a > gmax ? a : gmax;
+        gmin = b < gmin ? b : gmin;
+    }
+    if (need == 0) {  // nothing to take from the pool
+        if (tid == 0) {
+            S.b_tk = ~0ull;
+            S.b_tx = 0;
+        }
+        __syncthreads();
+        return;
+    }
+    if (total <= need) {  // every pool key is selected
+        if (tid == 0) {
+            S.b_tk = 0;
+            S.b_tx = 0;
+        }
+        __syncthreads();
+        return;
+    }
+    if (gmax == gmin) {  // all pool keys tie: lowest indices win
+        resolve_ties(cl, S, kv, k0, gmax, need,
+                     [&](int c) { return *remote(cl, &S.x_cnt, c); });
+        return;
+    }
+    // radix passes over the bits below the common prefix of [gmin, gmax]
+    const unsigned long long diff = gmax ^ gmin;
+    int pshift = 64 - __clzll(static_cast<long long>(diff));  // bits [pshift, 64) are common
+    unsigned long long prefix = pshift == 64 ? 0ull : (gmax >> pshift);
+    uint32_t rem = need;
+    bool use_surv = false;
+    for (int pass = 0;; ++pass) {
+        const int shift = pshift > HB_BITS ? pshift - HB_BITS : 0;
+        const int nbits = pshift - shift;
+        const uint32_t nb = 1u << nbits;
+        uint32_t* hist = S.hist[pass & 1];
+        for (uint32_t i = tid; i < nb; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        if (use_surv) {
+            for (uint32_t s = tid; s < S.surv_count; s += blockDim.x) {
+                const unsigned long long k = kv.keys[S.surv[s]];
+                atomicAdd(&hist[(k >> shift) & (nb - 1)], 1u);
+            }
+        } else {
+            for (uint32_t l = tid; l < kv.nloc; l += blockDim.x) {
+                const unsigned long long k = kv.keys[l];
+                if (!k) continue;
+                if (pshift < 64 && (k >> pshift) != prefix) continue;
+                atomicAdd(&hist[(k >> shift) & (nb - 1)], 1u);
+            }
+        }
+        cl.sync();  // (A) local histograms complete
+        const uint32_t sl = div_up(nb, cs);
+        const uint32_t lo = min(nb, rank * sl), hi = min(nb, lo + sl);
+        uint32_t part = 0;
+        for (uint32_t i = lo + tid; i < hi; i += blockDim.x) {
+            uint32_t v = 0;
+            for (int c = 0; c < cs; ++c) v += remote(cl, hist, c)[i];
+            S.ghist[i] = v;
+            part += v;
+        }
+        part = block_sum(S, part);
+        if (tid == 0) S.x_slice_total = part;
+        cl.sync();  // (B) reduced slices + slice totals published
+        if (w == 0) {
+            // locate the slice holding the rem-th largest, scanning from the top
+            uint32_t st = ln < cs ? *remote(cl, &S.x_slice_total, ln) : 0;
+            // suffix sums over lanes (higher slice = higher digits)
+            uint32_t suf = st;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_down_sync(0xffffffffu, suf, o);
+                if (ln + o < 32) suf += x;
+            }
+            // slice s* : suf(s*) >= rem and suf(s*+1) < rem
+            const uint32_t above = suf - st;
+            const bool hit = (ln < cs) && st > 0 && above < rem && suf >= rem;
+            const unsigned hm = __ballot_sync(0xffffffffu, hit);
+            const int sstar = __ffs(hm) - 1;
+            const uint32_t cab = __shfl_sync(0xffffffffu, above, sstar);
+            // copy slice s* locally, then scan its bins from the top
+            const uint32_t slo = min(nb, sstar * sl), shi = min(nb, slo + sl);
+            const uint32_t* src = remote(cl, S.ghist, sstar);
+            for (uint32_t i = slo + ln; i < shi; i += 32) S.gcopy[i] = src[i];
+            __syncwarp();
+            if (ln == 0) {
+                uint32_t c = cab;
+                uint32_t d = shi;
+                while (d > slo) {
+                    --d;
+                    const uint32_t h = S.gcopy[d];
+                    if (c + h >= rem) break;
+                    c += h;
+                }
+                S.b_dsel = d;
+                S.b_cabove = c;
+                S.b_bucket = S.gcopy[d];
+            }
+        }
+        __syncthreads();
+        const uint32_t dsel = S.b_dsel;
+        rem -= S.b_cabove;
+        const uint32_t bucket = S.b_bucket;
+        prefix = (pshift == 64 ? 0ull : (prefix << nbits)) | dsel;
+        pshift = shift;
+        if (bucket == rem) {  // the whole bucket is taken
+            if (tid == 0) {
+                S.b_tk = (prefix << pshift) - 1;
+                S.b_tx = 0;
+            }
+            __syncthreads();
+            return;
+        }
+        if (pshift == 0) {  // exact ties at key == prefix
+            resolve_ties(cl, S, kv, k0, prefix, rem,
+                         [&](int c) { return remote(cl, hist, c)[dsel]; });
+            return;
+        }
+        if (bucket <= SURV_MAX) {
+            // gather the bucket to CTA 0 and rank it there
+            uint32_t off = 0;
+            for (int c = 0; c < rank; ++c) off += remote(cl, hist, c)[dsel];
+            unsigned long long* dk = remote(cl, S.skey, 0);
+            uint32_t* di = remote(cl, S.sidx, 0);
+            if (tid == 0) S.wpos = 0;
+            __syncthreads();
+            auto put = [&](uint32_t l) {
+                const unsigned long long k = kv.keys[l];
+                if (k && (k >> pshift) == prefix) {
+                    const uint32_t p = off + atomicAdd(&S.wpos, 1u);
+                    dk[p] = k;
+                    di[p] = k0 + l;
+                }
+            };
+            if (use_surv) {
+                for (uint32_t s = tid; s < S.surv_count; s += blockDim.x) put(S.surv[s]);
+            } else {
+                for (uint32_t l = tid; l < kv.nloc; l += blockDim.x) put(l);
+            }
+            cl.sync();  // (C) bucket gathered on CTA 0
+            if (rank == 0) {
+                for (uint32_t e = tid; e < bucket; e += blockDim.x) {
+                    const unsigned long long ke = S.skey[e];
+                    const uint32_t ie = S.sidx[e];
+                    uint32_t r = 0;
+                    for (uint32_t f = 0; f < bucket; ++f) {
+                        const unsigned long long kf = S.skey[f];
+                        r += (kf > ke) || (kf == ke && S.sidx[f] < ie);
+                    }
+                    if (r == rem - 1) {
+                        S.x_tk = ke;
+                        S.x_tx = ie + 1;
+                    }
+                }
+            }
+            cl.sync();  // (D) threshold published by CTA 0
+            if (tid == 0) {
+                S.b_tk = *remote(cl, &S.x_tk, 0);
+                S.b_tx = *remote(cl, &S.x_tx, 0);
+            }
+            __syncthreads();
+            return;
+        }
+        // narrow the local candidate set for the next pass
+        const uint32_t mine = hist[dsel];
+        if (mine <= SURV_LOCAL) {
+            if (tid == 0) S.nsv = 0;
+            __syncthreads();
+            if (use_surv) {
+                // filter in place: read all, then write (two phases)
+                const uint32_t n0 = S.surv_count;
+                uint16_t keep[4];
+                uint32_t nk = 0;
+                for (uint32_t s = tid, u = 0; s < n0 && u < 4; s += blockDim.x, ++u) {
+                    const unsigned long long k = kv.keys[S.surv[s]];
+                    if ((k >> pshift) == prefix) keep[nk++] = S.surv[s];
+                }
+                __syncthreads();
+                for (uint32_t u = 0; u < nk; ++u) S.surv[atomicAdd(&S.nsv, 1u)] = keep[u];
+            } else {
+                for (uint32_t l = tid; l < kv.nloc; l += blockDim.x) {
+                    const unsigned long long k = kv.keys[l];
+                    if (k && (k >> pshift) == prefix) S.surv[atomicAdd(&S.nsv, 1u)] = static_cast<uint16_t>(l);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) S.surv_count = S.nsv;
+            use_surv = true;
+            __syncthreads();
+        } else {
+            use_surv = false;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+// ---------------------------------------------------------------------------
+template <int VEC>
+__global__ void __launch_bounds__(DEC_THREADS, 1)
+decode_kernel(const DecodeProblem* __restrict__ probs, uint32_t kpc) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DecSmem& S = *reinterpret_cast<DecSmem*>(smem_raw);
+    double* acc = reinterpret_cast<double*>(smem_raw + ((sizeof(DecSmem) + 15) & ~size_t(15)));
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = cl.block_rank(), cs = cl.num_blocks();
+    const DecodeProblem& P = probs[blockIdx.x / cs];
+    const SessionDev& sd = *P.s;
+    const uint32_t tid = threadIdx.x, N = P.N, K = P.K, d = sd.d;
+    float* wacc = reinterpret_cast<float*>(acc + kpc);
+    const bool leader = rank == 0;
+
+    const uint32_t k0 = rank * kpc;
+    const uint32_t k1 = min(N, k0 + kpc);
+    const uint32_t nloc = k1 > k0 ? k1 - k0 : 0;
+
+    for (uint32_t t = tid; t < d; t += blockDim.x) S.q[t] = P.q[t];
+    if (tid == 0) {
+        S.zero_mask = 0;
+        S.nl = 0;
+        S.surv_count = 0;
+    }
+    __syncthreads();
+
+    // ---- 1+2: candidate scores of this CTA's key range ----
+    if (P.mode & MODE_SEARCH) {
+        route(S, sd, acc, P.rep, leader);  // acc doubles as the m*C score scratch
+        for (uint32_t l = tid; l < kpc; l += blockDim.x)
+            acc[l] = __longlong_as_double(static_cast<long long>(ABSENT));
+        __syncthreads();
+        if (nloc) gather(S, sd, acc, k0, k1, N);
+        if (P.mode & MODE_STORE_CACHE)
+            for (uint32_t l = tid; l < nloc; l += blockDim.x) P.cache[k0 + l] = acc[l];
+    } else {
+        for (uint32_t l = tid; l < kpc; l += blockDim.x)
+            acc[l] = (l < nloc && k0 + l < P.n_cache)
+                         ? P.cache[k0 + l]
+                         : __longlong_as_double(static_cast<long long>(ABSENT));
+    }
+    __syncthreads();
+
+    // ---- 3: pool keys, selection threshold ----
+    const uint32_t r_eff = sd.window < N ? sd.window : N;
+    const uint32_t wlo = N - r_eff;
+    const bool pt = sd.passthrough != 0;
+    uint32_t need, f_lo;
+    if (pt) {
+        need = K > r_eff ? K - r_eff : 0;
+        f_lo = K > r_eff ? wlo : N - K;
+    } else {
+        need = K;
+        f_lo = N;
+    }
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(acc);
+    for (uint32_t l = tid; l < kpc; l += blockDim.x) {
+        const uint32_t i = k0 + l;
+        const double v = acc[l];
+        unsigned long long key = 0;
+        if (l < nloc) {
+            if (i < wlo)
+                key = is_absent(v) ? 0ull : ordkey(v);
+            else if (!pt)
+                key = ordkey(is_absent(v) ? 0.0 : v);
+        }
+        keys[l] = key;
+    }
+    __syncthreads();
+    KeyView kv{keys, nloc};
+    select_threshold(cl, S, kv, k0, need);
+    const unsigned long long tk = S.b_tk;
+    const uint32_t tx = S.b_tx;
+
+    // ---- emit the selected set in ascending order (+ newest-first padding) ----
+    const uint32_t chunk = div_up(nloc, blockDim.x);
+    const uint32_t c0 = min(nloc, tid * chunk), c1 = min(nloc, c0 + chunk);
+    auto picked = [&](uint32_t l) {
+        const uint32_t i = k0 + l;
+        const unsigned long long k = keys[l];
+        return i >= f_lo || (k && (k > tk || (k == tk && i < tx)));
+    };
+    uint32_t nsel = 0, nunt = 0;
+    for (uint32_t l = c0; l < c1; ++l) {
+        if (picked(l))
+            ++nsel;
+        else
+            ++nunt;
+    }
+    const int w_ = tid >> 5, ln_ = tid & 31;
+    uint32_t esel, eunt, tsel, tunt;
+    block_scan2(S, nsel, nunt, esel, eunt, tsel, tunt);
+    if (tid == 0) {
+        S.x_nsel = tsel;
+        S.x_nunt = tunt;
+    }
+    cl.sync();
+    if (w_ == 0) {
+        // per-CTA padding share and output base, one lane per cluster rank
+        const uint32_t ns = ln_ < cs ? *remote(cl, &S.x_nsel, ln_) : 0;
+        const uint32_t nu = ln_ < cs ? *remote(cl, &S.x_nunt, ln_) : 0;
+        const uint32_t all_sel = warp_sum(ns);
+        uint32_t suf = nu;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_down_sync(0xffffffffu, suf, o);
+            if (ln_ + o < 32) suf += x;
+        }
+        const uint32_t above = suf - nu;
+        const uint32_t pad = K > all_sel ? K - all_sel : 0;
+        const uint32_t tk_l = pad > above ? min(pad - above, nu) : 0;
+        const uint32_t cnt = ns + tk_l;
+        uint32_t inc = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+            if (ln_ >= o) inc += x;
+        }
+        if (ln_ == rank) {
+            S.b_base = inc - cnt;
+            S.b_take = tk_l;
+        }
+    }
+    __syncthreads();
+    const uint32_t base = S.b_base, take = S.b_take;
+    {
+        // padded keys: the `take` highest-index untaken keys of this CTA
+        const uint32_t pad_from = tunt - take;  // untaken rank >= pad_from is padded
+        uint32_t pos = base + esel + (eunt > pad_from ? eunt - pad_from : 0);
+        uint32_t u = eunt;
+        for (uint32_t l = c0; l < c1; ++l) {
+            bool s = picked(l);
+            if (!s) {
+                s = u >= pad_from;
+                ++u;
+            }
+            if (s) P.sel[pos++] = k0 + l;
+        }
+    }
+    cl.sync();  // selected indices visible cluster-wide
+
+    // ---- 4: split-K attention over the K selected rows ----
+    const uint32_t r0 = static_cast<uint32_t>((static_cast<unsigned long long>(K) * rank) / cs);
+    const uint32_t r1 = static_cast<uint32_t>((static_cast<unsigned long long>(K) * (rank + 1)) / cs);
+    const uint32_t nrows = r1 - r0;
+    float* lg = reinterpret_cast<float*>(acc);  // logits reuse the score region
+    const int w = tid >> 5, ln = tid & 31;
+    constexpr int NC = DMAX / (32 * VEC);
+    const int nchunks = static_cast<int>(div_up(d, 32 * VEC));
+    float qr[NC][VEC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const uint32_t e = c * 32 * VEC + ln * VEC + v;
+            qr[c][v] = (c < nchunks && e < d) ? S.q[e] : 0.0f;
+        }
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
+    const uint32_t P0 = sd.P;
+    auto row_ptr = [&](const float* pre, const float* tail, uint32_t i) {
+        return i < P0 ? pre + static_cast<size_t>(i) * d : tail + static_cast<size_t>(i - P0) * d;
+    };
+    float mx = -FLT_MAX;
+    constexpr int U = 4;
+    for (uint32_t rb = w; rb < nrows; rb += DEC_WARPS * U) {
+        float dp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            dp[u] = 0.0f;
+            const uint32_t r = rb + u * DEC_WARPS;
+            if (r < nrows) {
+                const uint32_t i = __ldcg(P.sel + r0 + r);
+                const float* kr = row_ptr(sd.kpre, sd.ktail, i);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    if (c >= nchunks) break;
+                    const uint32_t e = c * 32 * VEC + ln * VEC;
+                    if (VEC == 4) {
+                        if (e < d) {
+                            const float4 kk = __ldg(reinterpret_cast<const float4*>(kr + e));
+                            dp[u] = fmaf(qr[c][0], kk.x, dp[u]);
+                            dp[u] = fmaf(qr[c][1], kk.y, dp[u]);
+                            dp[u] = fmaf(qr[c][2], kk.z, dp[u]);
+                            dp[u] = fmaf(qr[c][3], kk.w, dp[u]);
+                        }
+                    } else {
+                        if (e < d) dp[u] = fmaf(qr[c][0], __ldg(kr + e), dp[u]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float s = warp_sumf(dp[u]) * scale;
+            const uint32_t r = rb + u * DEC_WARPS;
+            if (r < nrows) {
+                if (ln == 0) lg[r] = s;
+                mx = fmaxf(mx, s);
+            }
+        }
+    }
+    mx = warp_maxf(mx);
+    if (ln == 0) S.rf[w] = mx;
+    __syncthreads();
+    float M = -FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < DEC_WARPS; ++i) M = fmaxf(M, S.rf[i]);
+    __syncthreads();
+    float av[NC][VEC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) av[c][v] = 0.0f;
+    float ssum = 0.0f;
+    for (uint32_t rb = w; rb < nrows; rb += DEC_WARPS * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t r = rb + u * DEC_WARPS;
+            if (r < nrows) {
+                const uint32_t i = __ldcg(P.sel + r0 + r);
+                const float p = expf(lg[r] - M);
+                ssum += p;
+                const float* vr = row_ptr(sd.vpre, sd.vtail, i);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    if (c >= nchunks) break;
+                    const uint32_t e = c * 32 * VEC + ln * VEC;
+                    if (VEC == 4) {
+                        if (e < d) {
+                            const float4 vv = __ldg(reinterpret_cast<const float4*>(vr + e));
+                            av[c][0] = fmaf(p, vv.x, av[c][0]);
+                            av[c][1] = fmaf(p, vv.y, av[c][1]);
+                            av[c][2] = fmaf(p, vv.z, av[c][2]);
+                            av[c][3] = fmaf(p, vv.w, av[c][3]);
+                        }
+                    } else {
+                        if (e < d) av[c][0] = fmaf(p, __ldg(vr + e), av[c][0]);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c >= nchunks) break;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const uint32_t e = c * 32 * VEC + ln * VEC + v;
+            if (e < d) wacc[w * d + e] = av[c][v];
+        }
+    }
+    if (ln == 0) S.rf[w] = ssum;
+    __syncthreads();
+    for (uint32_t t = tid; t < d; t += blockDim.x) {
+        float a = 0.0f;
+        for (int i = 0; i < DEC_WARPS; ++i) a += wacc[i * d + t];
+        S.pacc[t] = a;
+    }
+    if (tid == 0) {
+        float s = 0.0f;
+        for (int i = 0; i < DEC_WARPS; ++i) s += S.rf[i];
+        S.x_m = nrows ? M : -FLT_MAX;
+        S.x_s = s;
+    }
+    cl.sync();  // partials published
+    if (leader) {
+        float GM = -FLT_MAX;
+        for (int c = 0; c < cs; ++c) GM = fmaxf(GM, *remote(cl, &S.x_m, c));
+        float GS = 0.0f;
+        for (int c = 0; c < cs; ++c) {
+            const float s = *remote(cl, &S.x_s, c);
+            if (s > 0.0f) GS += s * expf(*remote(cl, &S.x_m, c) - GM);
+        }
+        const float inv = 1.0f / GS;
+        for (uint32_t t = tid; t < d; t += blockDim.x) {
+            float o = 0.0f;
+            for (int c = 0; c < cs; ++c) {
+                const float s = *remote(cl, &S.x_s, c);
+                if (s > 0.0f) o += remote(cl, S.pacc, c)[t] * expf(*remote(cl, &S.x_m, c) - GM);
+            }
+            if (P.out) P.out[t] = o * inv;
+        }
+        if (tid == 0) {
+            S.x_M = GM;
+            S.x_S = GS;
+            reinterpret_cast<DecodeReport*>(P.rep)->k = K;
+        }
+    }
+    cl.sync();  // CTA 0 done reading peers; global M/S published
+    if ((P.mode & MODE_WEIGHTS) && P.weights) {
+        const float GM = *remote(cl, &S.x_M, 0);
+        const float inv = 1.0f / *remote(cl, &S.x_S, 0);
+        for (uint32_t r = tid; r < nrows; r += blockDim.x)
+            P.weights[r0 + r] = expf(lg[r] - GM) * inv;
+    }
+    cl.sync();  // nobody exits while a peer may still read its shared memory
+}
+
+size_t decode_smem_bytes(uint32_t kpc, uint32_t d) {
+    return ((sizeof(DecSmem) + 15) & ~size_t(15)) + static_cast<size_t>(kpc) * sizeof(double) +
+           static_cast<size_t>(DEC_WARPS) * d * sizeof(float);
+}
+
+template <int VEC>
+static cudaError_t launch_decode_t(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc,
+                                   uint32_t cs, uint32_t d, cudaStream_t st) {
+    const size_t smem = decode_smem_bytes(kpc, d);
+    cudaError_t e = cudaFuncSetAttribute(decode_kernel<VEC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    if (cs > 8) {
+        e = cudaFuncSetAttribute(decode_kernel<VEC>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nprob * cs, 1, 1);
+    cfg.blockDim = dim3(DEC_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, decode_kernel<VEC>, probs, kpc);
+}
+
+cudaError_t launch_decode(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
+                          uint32_t d, cudaStream_t st) {
+    if (d % 4 == 0) return launch_decode_t<4>(probs, nprob, kpc, cs, d, st);
+    return launch_decode_t<1>(probs, nprob, kpc, cs, d, st);
+}
+
+}  // namespace csa

@@ -1,0 +1,28 @@
+// kernels.h — host-callable launchers of the sm_100a kernels (csrc/*.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace csa {
+
+// decode.cu: fused route + gather + select + attend, one cluster per problem
+size_t decode_smem_bytes(uint32_t kpc, uint32_t d);
+cudaError_t launch_decode(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
+                          uint32_t d, cudaStream_t st);
+
+// insert.cu: append + streaming insert, one CTA per session
+cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st);
+
+// build.cu: exact fp64 centroid x key scores and top-L tables
+//   scores: T x P floats scratch
+cudaError_t launch_build_scores(const SessionDev* s_dev, const SessionDev& s_host, float* scores,
+                                cudaStream_t st);
+cudaError_t launch_build_lists(const SessionDev* s_dev, const SessionDev& s_host,
+                               const float* scores, cudaStream_t st);
+
+
+}  // namespace csa
