@@ -155,6 +155,12 @@ csattn_status csattn_ctx_destroy(csattn_ctx ctx);
 csattn_status csattn_ctx_synchronize(csattn_ctx ctx);
 /* Number of CUDA kernels this context has launched (driver-side evidence). */
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx);
+/* Kernel timing: when enabled, every decode / insert launch is bracketed by
+ * CUDA events on the context's stream. read returns the summed milliseconds
+ * and launch counts since the last reset (and synchronizes the stream). */
+csattn_status csattn_ctx_profile(csattn_ctx ctx, int32_t enable);
+csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* decode_ms, uint64_t* n_decode,
+                                      double* insert_ms, uint64_t* n_insert, int32_t reset);
 
 /* ---- offline build ----
  * prefill (session.cpp:25-44) = KvStore + build_index (index.cpp:145-177)

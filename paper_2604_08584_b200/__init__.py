@@ -252,6 +252,18 @@ class Context:
     def launches(self) -> int:
         return lib().csattn_ctx_launch_count(self.h)
 
+    def profile(self, enable: bool = True):
+        """Bracket every decode / insert launch with CUDA events on this stream."""
+        _check(lib().csattn_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        a, b = C.c_double(), C.c_double()
+        na, nb = C.c_uint64(), C.c_uint64()
+        _check(lib().csattn_ctx_profile_read(self.h, C.byref(a), C.byref(na), C.byref(b),
+                                             C.byref(nb), int(reset)))
+        return {"decode_ms": a.value, "n_decode": na.value, "insert_ms": b.value,
+                "n_insert": nb.value}
+
     def close(self):
         if self.h:
             lib().csattn_ctx_destroy(self.h)

@@ -120,6 +120,20 @@ struct csattn_ctx_s {
     std::vector<csa::DecodeProblem> hprobs;
     std::vector<csa::InsertProblem> hiprobs;
     std::vector<unsigned char> hrep;
+    // kernel timing (csattn_ctx_profile)
+    bool profile = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_decode, ev_insert;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t take_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        return e;
+    }
 };
 
 struct csattn_session_s {
@@ -456,12 +470,25 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     ctx->iprobs.ensure(ns * sizeof(csa::InsertProblem));
     upload(ctx, ctx->probs.p, ctx->hprobs.data(), nq * sizeof(csa::DecodeProblem), true);
     upload(ctx, ctx->iprobs.p, ctx->hiprobs.data(), ns * sizeof(csa::InsertProblem), true);
+    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    if (ctx->profile) {
+        e0 = ctx->take_event();
+        e1 = ctx->take_event();
+        e2 = ctx->take_event();
+        ck(cudaEventRecord(e0, ctx->stream), "event");
+    }
     ck(csa::launch_decode(ctx->probs.as<csa::DecodeProblem>(), static_cast<uint32_t>(nq), kpc, cs,
                           d, ctx->stream),
        "decode launch");
+    if (ctx->profile) ck(cudaEventRecord(e1, ctx->stream), "event");
     ck(csa::launch_insert(ctx->iprobs.as<csa::InsertProblem>(), static_cast<uint32_t>(ns),
                           ctx->stream),
        "insert launch");
+    if (ctx->profile) {
+        ck(cudaEventRecord(e2, ctx->stream), "event");
+        ctx->ev_decode.emplace_back(e0, e1);
+        ctx->ev_insert.emplace_back(e1, e2);
+    }
     ctx->launches += 2;
 
     // host bookkeeping: SearchState + Session counters
@@ -729,6 +756,12 @@ csattn_status csattn_ctx_destroy(csattn_ctx ctx) {
     return guard([&] {
         if (!ctx) return;
         cudaStreamSynchronize(ctx->stream);
+        for (auto& pr : ctx->ev_decode) ctx->ev_pool.push_back(pr.first);
+        for (auto& pr : ctx->ev_insert) {
+            ctx->ev_pool.push_back(pr.first);
+            ctx->ev_pool.push_back(pr.second);
+        }
+        for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
         if (ctx->own) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -739,6 +772,42 @@ csattn_status csattn_ctx_synchronize(csattn_ctx ctx) {
 }
 
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+csattn_status csattn_ctx_profile(csattn_ctx ctx, int32_t enable) {
+    return guard([&] { ctx->profile = enable != 0; });
+}
+
+csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* decode_ms, uint64_t* n_decode,
+                                      double* insert_ms, uint64_t* n_insert, int32_t reset) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(ctx->stream), "profile sync");
+        double a = 0.0, b = 0.0;
+        for (auto& pr : ctx->ev_decode) {
+            float ms = 0.0f;
+            ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "elapsed");
+            a += ms;
+        }
+        for (auto& pr : ctx->ev_insert) {
+            float ms = 0.0f;
+            ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "elapsed");
+            b += ms;
+        }
+        *decode_ms = a;
+        *insert_ms = b;
+        *n_decode = ctx->ev_decode.size();
+        *n_insert = ctx->ev_insert.size();
+        if (reset) {
+            // e1 is shared by a decode and an insert pair: return each event once
+            for (auto& pr : ctx->ev_decode) ctx->ev_pool.push_back(pr.first);
+            for (auto& pr : ctx->ev_insert) {
+                ctx->ev_pool.push_back(pr.first);
+                ctx->ev_pool.push_back(pr.second);
+            }
+            ctx->ev_decode.clear();
+            ctx->ev_insert.clear();
+        }
+    });
+}
 
 // prefill (session.cpp:25-44) -> build_index (index.cpp:145-177) on the GPU.
 csattn_status csattn_prefill(csattn_ctx ctx, const float* queries, uint64_t nq, const float* keys,
