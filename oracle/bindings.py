@@ -49,6 +49,9 @@ def ref_lib():
         L.csref_prefill_from_centroids.argtypes = [vp, u64, vp, vp, u64, u64, P(u64), u64,
                                                    P(_abi.IndexConfigC),
                                                    P(_abi.RetrievalConfigC), u64, P(vp)]
+        L.csref_import.argtypes = [vp, u64, vp, vp, vp, u64, u64, C.c_double, C.c_int32, vp,
+                                   vp, u64, u64, P(u64), u64, P(_abi.RetrievalConfigC), u64,
+                                   P(vp)]
         L.csref_free.argtypes = [vp]
         L.csref_info.argtypes = [vp, P(u64), P(u64), P(u64), P(u64)]
         L.csref_export.argtypes = [vp, vp, vp, vp, u64, vp]
@@ -180,6 +183,25 @@ class RefSession(_Base):
         return cls._wrap(h, d, group)
 
     @classmethod
+    def from_index(cls, cent, lens, idx, sc, L, alpha, keys, values, widths, rcfg, group=1,
+                   normalize_keys=False):
+        """A reference Session over a given CsIndex image (TopList order)."""
+        d = sum(widths)
+        c = _f32(cent).reshape(-1)
+        lens = np.ascontiguousarray(lens, np.uint32)
+        idx = np.ascontiguousarray(idx, np.uint32)
+        sc = _f32(sc)
+        k, v = _f32(keys), _f32(values)
+        rc, w = rcfg.c()
+        h = C.c_void_p()
+        cls._chk(ref_lib().csref_import(c.ctypes.data, c.size // d, lens.ctypes.data,
+                                        idx.ctypes.data, sc.ctypes.data, idx.shape[1], L, alpha,
+                                        int(normalize_keys), k.ctypes.data, v.ctypes.data,
+                                        k.size // d, d, _w(widths), len(widths), C.byref(rc),
+                                        group, C.byref(h)))
+        return cls._wrap(h, d, group)
+
+    @classmethod
     def _wrap(cls, h, d, group):
         n, L, c, m = u64(), u64(), u64(), u64()
         ref_lib().csref_info(h, C.byref(n), C.byref(L), C.byref(c), C.byref(m))
@@ -271,6 +293,20 @@ class OraSession(_Base):
                 self.h = None
         except Exception:
             pass
+
+
+def ref_bench(sessions, q, k, v, steps, threads):
+    """Wall seconds for `steps` decode steps of every session on `threads` host
+    threads. q: [n, steps, group, d]; k, v: [n, steps, d] (float32)."""
+    n = len(sessions)
+    hs = (C.c_void_p * n)(*[s.h.value if isinstance(s.h, C.c_void_p) else s.h for s in sessions])
+    q, k, v = _f32(q), _f32(k), _f32(v)
+    sec = C.c_double()
+    RefSession._chk(ref_lib().csref_bench(hs, n, q.ctypes.data, k.ctypes.data, v.ctypes.data,
+                                          steps, threads, C.byref(sec)))
+    for s in sessions:
+        s.n += steps
+    return sec.value
 
 
 def ref_make_synthetic(spec):

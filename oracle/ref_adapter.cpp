@@ -255,6 +255,44 @@ int csref_prefill_from_centroids(const float* cent, uint64_t c, const float* k, 
     });
 }
 
+// A reference Session over a given CsIndex image (TopList order) — used by
+// bench.py's cpu_baseline leg to run the reference's decode path on exactly
+// the tables the GPU built (tests pin them bit-identical to build_index).
+int csref_import(const float* cent, uint64_t c, const uint32_t* lens, const uint32_t* idx,
+                 const float* scores, uint64_t stride, uint64_t L, double alpha,
+                 int32_t normalize_keys, const float* k, const float* v, uint64_t p, uint64_t d,
+                 const uint64_t* widths, uint64_t m, const csattn_retrieval_config* rcfg,
+                 uint64_t group, void** out) {
+    return guarded([&] {
+        R::CsIndex ix(layout_of(widths, m));
+        const float* src = cent;
+        for (uint64_t b = 0; b < m; ++b) {
+            R::CentroidSet cs;
+            cs.subspace_id = b;
+            cs.count = c;
+            cs.dim = widths[b];
+            cs.centroids.assign(src, src + c * widths[b]);
+            src += c * widths[b];
+            ix.centroid_sets.push_back(std::move(cs));
+        }
+        for (uint64_t t = 0; t < m * c; ++t) {
+            R::TopList tl;
+            tl.capacity = static_cast<uint32_t>(L);
+            tl.indices.assign(idx + t * stride, idx + t * stride + lens[t]);
+            tl.scores.assign(scores + t * stride, scores + t * stride + lens[t]);
+            ix.tables.push_back(std::move(tl));
+        }
+        ix.alpha = alpha;
+        ix.list_capacity = static_cast<uint32_t>(L);
+        ix.prefill_len = p;
+        ix.normalize_keys = normalize_keys != 0;
+        ix.score_bits = 32;
+        R::KvStore kv(d, {k, p * d}, {v, p * d});
+        R::Session s(std::move(kv), std::move(ix), rcfg_of(rcfg));
+        *out = new Group(std::move(s), group);
+    });
+}
+
 void csref_free(void* h) { delete static_cast<Group*>(h); }
 
 int csref_info(void* h, uint64_t* n, uint64_t* l, uint64_t* c, uint64_t* m) {

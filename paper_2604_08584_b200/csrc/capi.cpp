@@ -119,6 +119,25 @@ struct csattn_ctx_s {
     DevMem probs, iprobs, stage;
     std::vector<csa::DecodeProblem> hprobs;
     std::vector<csa::InsertProblem> hiprobs;
+    // Per-step descriptor ring: pinned host staging + device copy + an event
+    // marking the step's kernels done, so the host never waits on the GPU
+    // before reusing a slot that is still in flight.
+    struct Slot {
+        void* host = nullptr;
+        DevMem dev;
+        size_t cap = 0;
+        cudaEvent_t done = nullptr;
+        bool used = false;
+    };
+    static constexpr int kSlots = 4;
+    Slot ring[kSlots];
+    int next_slot = 0;
+    ~csattn_ctx_s() {
+        for (Slot& s : ring) {
+            if (s.host) cudaFreeHost(s.host);
+            if (s.done) cudaEventDestroy(s.done);
+        }
+    }
     std::vector<unsigned char> hrep;
     // kernel timing (csattn_ctx_profile)
     bool profile = false;
@@ -466,10 +485,29 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         I.N = static_cast<uint32_t>(n);
         I.pad = 0;
     }
-    ctx->probs.ensure(nq * sizeof(csa::DecodeProblem));
-    ctx->iprobs.ensure(ns * sizeof(csa::InsertProblem));
-    upload(ctx, ctx->probs.p, ctx->hprobs.data(), nq * sizeof(csa::DecodeProblem), true);
-    upload(ctx, ctx->iprobs.p, ctx->hiprobs.data(), ns * sizeof(csa::InsertProblem), true);
+    // stage both descriptor arrays through one pinned ring slot
+    auto& slot = ctx->ring[ctx->next_slot];
+    ctx->next_slot = (ctx->next_slot + 1) % csattn_ctx_s::kSlots;
+    if (slot.used) ck(cudaEventSynchronize(slot.done), "descriptor slot");
+    const size_t dbytes = nq * sizeof(csa::DecodeProblem);
+    const size_t ibytes = ns * sizeof(csa::InsertProblem);
+    const size_t need = ((dbytes + 255) & ~size_t(255)) + ibytes;
+    if (need > slot.cap) {
+        if (slot.host) ck(cudaFreeHost(slot.host), "cudaFreeHost");
+        slot.cap = need + need / 2;
+        ck(cudaMallocHost(&slot.host, slot.cap), "cudaMallocHost");
+        slot.dev.alloc(slot.cap);
+    }
+    if (!slot.done) ck(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "event");
+    char* hb = static_cast<char*>(slot.host);
+    const size_t ioff = (dbytes + 255) & ~size_t(255);
+    std::memcpy(hb, ctx->hprobs.data(), dbytes);
+    std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
+    ck(cudaMemcpyAsync(slot.dev.p, hb, ioff + ibytes, cudaMemcpyHostToDevice, ctx->stream),
+       "descriptor upload");
+    const csa::DecodeProblem* dprobs = slot.dev.as<csa::DecodeProblem>();
+    const csa::InsertProblem* diprobs =
+        reinterpret_cast<const csa::InsertProblem*>(slot.dev.as<char>() + ioff);
     cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
     if (ctx->profile) {
         e0 = ctx->take_event();
@@ -477,13 +515,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         e2 = ctx->take_event();
         ck(cudaEventRecord(e0, ctx->stream), "event");
     }
-    ck(csa::launch_decode(ctx->probs.as<csa::DecodeProblem>(), static_cast<uint32_t>(nq), kpc, cs,
-                          d, ctx->stream),
+    ck(csa::launch_decode(dprobs, static_cast<uint32_t>(nq), kpc, cs, d, ctx->stream),
        "decode launch");
     if (ctx->profile) ck(cudaEventRecord(e1, ctx->stream), "event");
-    ck(csa::launch_insert(ctx->iprobs.as<csa::InsertProblem>(), static_cast<uint32_t>(ns),
-                          ctx->stream),
-       "insert launch");
+    ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
+    ck(cudaEventRecord(slot.done, ctx->stream), "event");
+    slot.used = true;
     if (ctx->profile) {
         ck(cudaEventRecord(e2, ctx->stream), "event");
         ctx->ev_decode.emplace_back(e0, e1);
