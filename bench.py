@@ -394,18 +394,34 @@ def main():
         t += 1
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
-    dec_ms = prof["decode_ms"] / max(1, prof["n_decode"])
-    ins_ms = prof["insert_ms"] / max(1, prof["n_insert"])
-    # algorithmic bytes of one decode launch, averaged over
-    # the profiled steps: per query head m*L*8 gathered entries + K*(2*d*4 + 4)
-    # selected K/V rows and indices + C*d*4 centroids + 2*d*4 q/out
-    bytes_l = []
+    nps = max(1, prof["steps"])
+    sel_ms = prof["select_ms"] / nps
+    att_ms = prof["attend_ms"] / nps
+    ins_ms = prof["insert_ms"] / nps
+    # algorithmic bytes per launch, averaged over the profiled
+    # steps. Per query head: select = m*L*8 gathered (u32, f32) entries +
+    # C*d*4 centroids + d*4 q + K*4 indices out; attend = K*(2*d*4) selected K/V
+    # rows + K*4 indices + 2*d*4 q/out. Their sum is the per-query-head unit.
+    sel_b, att_b = [], []
     for j in range(prof_steps):
         K = keep_count(0.05, n_prof0 + j)
-        bytes_l.append(nq * (M * L * 8 + K * (2 * D * 4 + 4) + C_CENT * D * 4 + 2 * D * 4))
-    alg_bytes = float(np.mean(bytes_l))
+        sel_b.append(nq * (M * L * 8 + C_CENT * D * 4 + D * 4 + K * 4))
+        att_b.append(nq * (K * (2 * D * 4 + 4) + 2 * D * 4))
+    sel_bytes, att_bytes = float(np.mean(sel_b)), float(np.mean(att_b))
+    alg_bytes = att_bytes  # the dominant kernel: attend
+    dec_ms = att_ms
     achieved = alg_bytes / (dec_ms * 1e-3) / 1e9
     peak, peak_src = measured_peak()
+    kernels = {
+        "select": {"ms": sel_ms, "alg_bytes": sel_bytes,
+                   "gbs": sel_bytes / (sel_ms * 1e-3) / 1e9},
+        "attend": {"ms": att_ms, "alg_bytes": att_bytes,
+                   "gbs": att_bytes / (att_ms * 1e-3) / 1e9},
+        "insert": {"ms": ins_ms},
+    }
+    for v in kernels.values():
+        if "gbs" in v:
+            v["frac"] = v["gbs"] / peak
     step_bytes = float(np.mean([nq * (M * L * 8 + keep_count(0.05, n_at_start + j) *
                                       (2 * D * 4 + 4) + C_CENT * D * 4 + 2 * D * 4)
                                 for j in range(steps)]))
@@ -457,11 +473,11 @@ def main():
             "config": dict(config, parallelism=f"kv-head shard x{world}", l2_policy=(
                 "working set (tables ~14 GB + KV 1 GB per GPU at c3) >> 126 MB L2; no flush")),
             "hbm_gbs_per_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "csa::decode_kernel", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": "csa::attend_kernel", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": ncu_traffic(args.config), "peak_source": peak_src,
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms": dec_ms,
-                         "insert_kernel_ms": ins_ms, "problems_per_launch": nq},
+                         "problems_per_launch": nq, "kernels": kernels},
             "e2e": {"value": e2e_ms * 1e3, "unit": "us",
                     "h2d_bytes_per_step": int(qh[0].nbytes + kh[0].nbytes + vh[0].nbytes),
                     "d2h_bytes_per_step": int(op[0].numel() * 4)},

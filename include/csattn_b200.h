@@ -155,12 +155,12 @@ csattn_status csattn_ctx_destroy(csattn_ctx ctx);
 csattn_status csattn_ctx_synchronize(csattn_ctx ctx);
 /* Number of CUDA kernels this context has launched (driver-side evidence). */
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx);
-/* Kernel timing: when enabled, every decode / insert launch is bracketed by
- * CUDA events on the context's stream. read returns the summed milliseconds
- * and launch counts since the last reset (and synchronizes the stream). */
+/* Kernel timing: when enabled, the three kernels of every decode step
+ * (select, attend, insert) are bracketed by CUDA events on the context's
+ * stream. read returns the summed milliseconds per kernel (ms[3]) and the
+ * number of profiled steps since the last reset (synchronizes the stream). */
 csattn_status csattn_ctx_profile(csattn_ctx ctx, int32_t enable);
-csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* decode_ms, uint64_t* n_decode,
-                                      double* insert_ms, uint64_t* n_insert, int32_t reset);
+csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* ms, uint64_t* steps, int32_t reset);
 
 /* ---- offline build ----
  * prefill (session.cpp:25-44) = KvStore + build_index (index.cpp:145-177)
@@ -216,6 +216,14 @@ csattn_status csattn_session_fork(csattn_session src, uint64_t max_decode_steps,
 csattn_status csattn_session_destroy(csattn_session s);
 csattn_status csattn_session_info_get(csattn_session s, csattn_session_info* out);
 csattn_status csattn_session_set_retrieval(csattn_session s, const csattn_retrieval_config* rcfg);
+/* SearchState::cached (retrieval.hpp:88-94): the CandidateSet of the last
+ * search of query head `head` — ascending key indices with their fp64
+ * accumulated scores (reduce_by_key, retrieval.cpp:111-148). Candidates are
+ * kept on the device only when the search period is > 1 or after
+ * keep_candidates(s, 1). Host memory; *n receives the candidate count. */
+csattn_status csattn_session_keep_candidates(csattn_session s, int32_t enable);
+csattn_status csattn_session_candidates(csattn_session s, uint64_t head, uint32_t* indices,
+                                        double* scores, uint64_t cap, uint64_t* n);
 /* KvStore rows back to the host (core.cpp:84-90): rows [first, first+count). */
 csattn_status csattn_session_read_kv(csattn_session s, uint64_t first, uint64_t count,
                                      float* keys, float* values);

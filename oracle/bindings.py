@@ -52,6 +52,7 @@ def ref_lib():
         L.csref_import.argtypes = [vp, u64, vp, vp, vp, u64, u64, C.c_double, C.c_int32, vp,
                                    vp, u64, u64, P(u64), u64, P(_abi.RetrievalConfigC), u64,
                                    P(vp)]
+        L.csref_candidates.argtypes = [vp, u64, vp, vp, u64, P(u64)]
         L.csref_free.argtypes = [vp]
         L.csref_info.argtypes = [vp, P(u64), P(u64), P(u64), P(u64)]
         L.csref_export.argtypes = [vp, vp, vp, vp, u64, vp]
@@ -209,6 +210,15 @@ class RefSession(_Base):
         s.C = c.value
         s.m = m.value
         return s
+
+    def candidates(self, head=0):
+        cap = self.n + 1
+        idx = np.zeros(cap, np.uint32)
+        sc = np.zeros(cap, np.float64)
+        n = u64()
+        self._chk(self.lib.csref_candidates(self.h, head, idx.ctypes.data, sc.ctypes.data, cap,
+                                            C.byref(n)))
+        return idx[:n.value].copy(), sc[:n.value].copy()
 
     def _step(self, q, key, value, sel, stride, out, wts, reps):
         self._chk(self.lib.csref_step(self.h, q.ctypes.data, key.ctypes.data, value.ctypes.data,

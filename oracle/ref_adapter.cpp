@@ -336,6 +336,20 @@ int csref_step(void* h, const float* q, const float* key, const float* value,
     });
 }
 
+// SearchState::cached of query head `head` (the last reduce_by_key result).
+int csref_candidates(void* h, uint64_t head, uint32_t* idx, double* scores, uint64_t cap,
+                     uint64_t* n) {
+    return guarded([&] {
+        Group& g = *static_cast<Group*>(h);
+        const R::SearchState& st = g.group == 1 ? g.session.search_state : g.states.at(head);
+        const R::CandidateSet& c = st.cached;
+        if (c.size() > cap) throw R::ParameterError("candidate buffer too small");
+        std::copy(c.indices.begin(), c.indices.end(), idx);
+        std::copy(c.scores.begin(), c.scores.end(), scores);
+        *n = c.size();
+    });
+}
+
 // decode_step with compare_dense = true (session.cpp:66-78): recall + l2 error.
 int csref_step_compare(void* h, const float* q, const float* key, const float* value,
                        uint32_t* selected, float* out, float* dense_out, double* recall,

@@ -257,12 +257,10 @@ class Context:
         _check(lib().csattn_ctx_profile(self.h, int(enable)))
 
     def profile_read(self, reset: bool = True) -> dict:
-        a, b = C.c_double(), C.c_double()
-        na, nb = C.c_uint64(), C.c_uint64()
-        _check(lib().csattn_ctx_profile_read(self.h, C.byref(a), C.byref(na), C.byref(b),
-                                             C.byref(nb), int(reset)))
-        return {"decode_ms": a.value, "n_decode": na.value, "insert_ms": b.value,
-                "n_insert": nb.value}
+        ms = (C.c_double * 3)()
+        n = C.c_uint64()
+        _check(lib().csattn_ctx_profile_read(self.h, ms, C.byref(n), int(reset)))
+        return {"select_ms": ms[0], "attend_ms": ms[1], "insert_ms": ms[2], "steps": n.value}
 
     def close(self):
         if self.h:
@@ -318,6 +316,20 @@ class Session:
         v = np.zeros_like(k)
         _check(lib().csattn_session_read_kv(self.h, first, count, k.ctypes.data, v.ctypes.data))
         return k, v
+
+    def keep_candidates(self, enable: bool = True):
+        """Keep every search's CandidateSet on the device (SearchState::cached)."""
+        _check(lib().csattn_session_keep_candidates(self.h, int(enable)))
+
+    def candidates(self, head: int = 0):
+        """(indices ascending, fp64 scores) of the last search of `head`."""
+        cap = self.info().max_context
+        idx = np.zeros(cap, np.uint32)
+        sc = np.zeros(cap, np.float64)
+        n = C.c_uint64()
+        _check(lib().csattn_session_candidates(self.h, head, idx.ctypes.data, sc.ctypes.data,
+                                               cap, C.byref(n)))
+        return idx[:n.value].copy(), sc[:n.value].copy()
 
     def fork(self, max_decode_steps: int | None = None) -> "Session":
         inf = self.info()

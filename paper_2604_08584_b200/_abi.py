@@ -82,7 +82,7 @@ SIGNATURES = {
     "csattn_ctx_synchronize": (C.c_int, [vp]),
     "csattn_ctx_launch_count": (u64, [vp]),
     "csattn_ctx_profile": (C.c_int, [vp, i32]),
-    "csattn_ctx_profile_read": (C.c_int, [vp, P(C.c_double), P(u64), P(C.c_double), P(u64), i32]),
+    "csattn_ctx_profile_read": (C.c_int, [vp, P(C.c_double), P(u64), i32]),
     "csattn_prefill": (C.c_int, [vp, vp, u64, vp, vp, u64, u64, P(u64), u64, P(IndexConfigC),
                                  P(RetrievalConfigC), u64, u64, u32, P(vp)]),
     "csattn_prefill_from_centroids": (C.c_int, [vp, vp, u64, vp, vp, u64, u64, P(u64), u64,
@@ -97,6 +97,8 @@ SIGNATURES = {
     "csattn_session_info_get": (C.c_int, [vp, P(SessionInfoC)]),
     "csattn_session_set_retrieval": (C.c_int, [vp, P(RetrievalConfigC)]),
     "csattn_session_read_kv": (C.c_int, [vp, u64, u64, vp, vp]),
+    "csattn_session_keep_candidates": (C.c_int, [vp, i32]),
+    "csattn_session_candidates": (C.c_int, [vp, u64, vp, vp, u64, P(u64)]),
     "csattn_decode_step": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, u64, P(StepReportC), P(u64),
                                      u32]),
     "csattn_decode_batch": (C.c_int, [vp, u64, P(vp), vp, vp, vp, vp, vp, u64, u32]),

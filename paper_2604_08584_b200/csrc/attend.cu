@@ -1,0 +1,217 @@
+// attend.cu — CSAttention decode, part 2: sparse attention over the selected
+// rows (masked dense_attention, core.cpp:118-169) on sm_100a.
+//
+// Split-K flash decoding: the K selected rows of every problem are cut into
+// ATT_ROWS-row chunks and every chunk is one 128-thread CTA, so a layer step
+// (512 problems x ~52 chunks at 128K) is a grid of ~27K independent CTAs with
+// high memory-level parallelism. Each warp streams 32 rows: one coalesced load
+// of its 32 row indices, then ATT_U rows at a time with one float4 per lane of
+// the K row and of the V row in flight (a 512-byte row = one warp-wide 128-bit
+// load), online softmax in fp32. The CTA reduces its 4 warps into one partial
+// (max, sum, acc[d]); the last CTA to finish a problem (device-scope counter)
+// merges the partials in chunk order — a deterministic log-sum-exp merge —
+// writes the output, the softmax weights (if requested: logits are parked in
+// the weights buffer and normalized in place) and resets the counter.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace csa {
+
+constexpr int ATT_THREADS = 128;
+constexpr int ATT_WARPS = ATT_THREADS / 32;
+constexpr int ATT_U = 4;
+
+__device__ __forceinline__ float wsum(float v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Each lane holds NC x VEC elements of the head dim: element (cc, v) is
+// cc*32*VEC + lane*VEC + v (VEC = 4 when d % 4 == 0: 128-bit loads).
+template <int VEC>
+__device__ __forceinline__ void ld_vec(float (&x)[VEC], const float* p) {
+    if constexpr (VEC == 4) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+        x[0] = t.x;
+        x[1] = t.y;
+        x[2] = t.z;
+        x[3] = t.w;
+    } else {
+        x[0] = __ldcs(p);
+    }
+}
+
+template <int NC, int VEC>
+__global__ void __launch_bounds__(ATT_THREADS)
+attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
+              const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
+              uint32_t* __restrict__ counters) {
+    __shared__ float wm[ATT_WARPS], ws[ATT_WARPS];
+    __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
+    __shared__ uint32_t is_last;
+    const uint32_t c = blockIdx.x;
+    const uint32_t p = chunk_prob[c];
+    const DecodeProblem& P = probs[p];
+    const SessionDev& sd = *P.s;
+    const uint32_t d = sd.d, K = P.K, P0 = sd.P;
+    const uint32_t j = c - chunk_base[p];
+    const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const uint32_t r0 = j * ATT_ROWS + w * 32;
+    const uint32_t nr = r0 < K ? min(32u, K - r0) : 0u;
+    const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
+
+    float q[NC][VEC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const uint32_t e = cc * 32 * VEC + ln * VEC + v;
+            q[cc][v] = e < d ? P.q[e] : 0.0f;
+        }
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
+    const uint32_t myidx = ln < nr ? __ldg(P.sel + r0 + ln) : 0u;
+
+    float m = -FLT_MAX, s = 0.0f;
+    float acc[NC][VEC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[cc][v] = 0.0f;
+
+    for (uint32_t i0 = 0; i0 < nr; i0 += ATT_U) {
+        float kv[ATT_U][NC][VEC], vv[ATT_U][NC][VEC];
+#pragma unroll
+        for (int u = 0; u < ATT_U; ++u) {
+            const uint32_t i = __shfl_sync(0xffffffffu, myidx, (i0 + u) & 31);
+            const bool ok = i0 + u < nr;
+            const float* kr = i < P0 ? sd.kpre + static_cast<size_t>(i) * d
+                                     : sd.ktail + static_cast<size_t>(i - P0) * d;
+            const float* vr = i < P0 ? sd.vpre + static_cast<size_t>(i) * d
+                                     : sd.vtail + static_cast<size_t>(i - P0) * d;
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc) {
+                const uint32_t e = cc * 32 * VEC + ln * VEC;
+                if (ok && e < d) {
+                    ld_vec<VEC>(kv[u][cc], kr + e);
+                    ld_vec<VEC>(vv[u][cc], vr + e);
+                } else {
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) kv[u][cc][v] = vv[u][cc][v] = 0.0f;
+                }
+            }
+        }
+        float lg[ATT_U];
+#pragma unroll
+        for (int u = 0; u < ATT_U; ++u) {
+            float dp = 0.0f;
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) dp = fmaf(q[cc][v], kv[u][cc][v], dp);
+            lg[u] = wsum(dp) * scale;
+        }
+        float mn = m;
+#pragma unroll
+        for (int u = 0; u < ATT_U; ++u)
+            if (i0 + u < nr) mn = fmaxf(mn, lg[u]);
+        const float f = expf(m - mn);
+        s *= f;
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[cc][v] *= f;
+#pragma unroll
+        for (int u = 0; u < ATT_U; ++u) {
+            if (i0 + u >= nr) continue;
+            const float pu = expf(lg[u] - mn);
+            s += pu;
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) acc[cc][v] = fmaf(pu, vv[u][cc][v], acc[cc][v]);
+            if (want_w && ln == 0) P.weights[r0 + i0 + u] = lg[u];  // logit, normalized later
+        }
+        m = mn;
+    }
+    // ---- CTA partial ----
+    if (ln == 0) {
+        wm[w] = nr ? m : -FLT_MAX;
+        ws[w] = nr ? s : 0.0f;
+    }
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) wacc[w][cc * 32 * VEC + ln * VEC + v] = acc[cc][v];
+    __syncthreads();
+    float M = -FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < ATT_WARPS; ++i) M = fmaxf(M, wm[i]);
+    float* pp = part + static_cast<size_t>(c) * (d + 2);
+    if (threadIdx.x == 0) {
+        float S = 0.0f;
+        for (int i = 0; i < ATT_WARPS; ++i)
+            if (ws[i] > 0.0f) S += ws[i] * expf(wm[i] - M);
+        pp[0] = M;
+        pp[1] = S;
+    }
+    for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
+        float a = 0.0f;
+        for (int i = 0; i < ATT_WARPS; ++i)
+            if (ws[i] > 0.0f) a += wacc[i][t] * expf(wm[i] - M);
+        pp[2 + t] = a;
+    }
+    // ---- last CTA of the problem merges all partials in chunk order ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(counters + p, 1u) == nch - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const float* pb = part + static_cast<size_t>(chunk_base[p]) * (d + 2);
+    float GM = -FLT_MAX;
+    for (uint32_t k = 0; k < nch; ++k) GM = fmaxf(GM, __ldcg(pb + k * (d + 2)));
+    float GS = 0.0f;
+    for (uint32_t k = 0; k < nch; ++k) {
+        const float sk = __ldcg(pb + k * (d + 2) + 1);
+        if (sk > 0.0f) GS += sk * expf(__ldcg(pb + k * (d + 2)) - GM);
+    }
+    const float inv = 1.0f / GS;
+    for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
+        float o = 0.0f;
+        for (uint32_t k = 0; k < nch; ++k) {
+            const float sk = __ldcg(pb + k * (d + 2) + 1);
+            if (sk > 0.0f) o += __ldcg(pb + k * (d + 2) + 2 + t) * expf(__ldcg(pb + k * (d + 2)) - GM);
+        }
+        if (P.out) P.out[t] = o * inv;
+    }
+    if (want_w)
+        for (uint32_t r = threadIdx.x; r < K; r += blockDim.x)
+            P.weights[r] = expf(__ldcg(P.weights + r) - GM) * inv;
+    if (threadIdx.x == 0) counters[p] = 0;  // ready for the next step
+}
+
+cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
+                          const uint32_t* chunk_base, uint32_t nchunks, float* part,
+                          uint32_t* counters, uint32_t d, cudaStream_t st) {
+#define CSA_ATT(NC, VEC) \
+    attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
+    if (d % 4 == 0) {
+        if (d <= 128) CSA_ATT(1, 4);
+        else if (d <= 256) CSA_ATT(2, 4);
+        else CSA_ATT(4, 4);
+    } else {
+        if (d <= 32) CSA_ATT(1, 1);
+        else if (d <= 128) CSA_ATT(4, 1);
+        else CSA_ATT(16, 1);
+    }
+#undef CSA_ATT
+    return cudaGetLastError();
+}
+
+}  // namespace csa

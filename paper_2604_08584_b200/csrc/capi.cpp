@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -113,6 +114,7 @@ struct HeadState {
 
 struct csattn_ctx_s {
     int device = 0;
+    int refs = 1;  // the handle + one per live session
     cudaStream_t stream = nullptr;
     bool own = false;
     uint64_t launches = 0;
@@ -141,7 +143,9 @@ struct csattn_ctx_s {
     std::vector<unsigned char> hrep;
     // kernel timing (csattn_ctx_profile)
     bool profile = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_decode, ev_insert;
+    std::vector<std::array<cudaEvent_t, 4>> ev_steps;  // select | attend | insert
+    DevMem part, counters;  // attention partials + per-problem merge counters
+    uint64_t counters_n = 0;
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t take_event() {
         if (!ev_pool.empty()) {
@@ -170,6 +174,7 @@ struct csattn_session_s {
     std::vector<HeadState> hs;
     std::vector<uint64_t> widths;
 
+    ~csattn_session_s();
     uint64_t T() const { return static_cast<uint64_t>(h.m) * h.C; }
     size_t device_bytes() const {
         return ktail.n + vtail.n + cent.n + ent.n + n_used.n + live.n + blk_off.n + low.n +
@@ -263,6 +268,7 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     if (L > 0x7fffffffull) fail(CSATTN_ERR_PARAMETER, "list capacity too large");
     auto s = std::make_unique<csattn_session_s>();
     s->ctx = ctx;
+    ctx->refs += 1;
     s->group = group;
     s->max_steps = max_steps;
     s->N = p;
@@ -489,9 +495,28 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     auto& slot = ctx->ring[ctx->next_slot];
     ctx->next_slot = (ctx->next_slot + 1) % csattn_ctx_s::kSlots;
     if (slot.used) ck(cudaEventSynchronize(slot.done), "descriptor slot");
+    // attention work list: ceil(K / ATT_ROWS) chunk-CTAs per problem
+    std::vector<uint32_t> cbase(nq + 1), cprob;
+    for (uint64_t i = 0; i < nq; ++i) {
+        cbase[i] = static_cast<uint32_t>(cprob.size());
+        const uint64_t nc = (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
+        cprob.insert(cprob.end(), nc, static_cast<uint32_t>(i));
+    }
+    cbase[nq] = static_cast<uint32_t>(cprob.size());
+    const uint64_t nchunks = cprob.size();
+    if (nq > ctx->counters_n) {
+        ctx->counters.alloc(nq * 4);
+        ck(cudaMemsetAsync(ctx->counters.p, 0, nq * 4, ctx->stream), "memset");
+        ctx->counters_n = nq;
+    }
+    ctx->part.ensure(nchunks * (d + 2) * sizeof(float));
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t dbytes = nq * sizeof(csa::DecodeProblem);
     const size_t ibytes = ns * sizeof(csa::InsertProblem);
-    const size_t need = ((dbytes + 255) & ~size_t(255)) + ibytes;
+    const size_t ioff = al(dbytes);
+    const size_t boff = ioff + al(ibytes);
+    const size_t poff = boff + al((nq + 1) * 4);
+    const size_t need = poff + nchunks * 4;
     if (need > slot.cap) {
         if (slot.host) ck(cudaFreeHost(slot.host), "cudaFreeHost");
         slot.cap = need + need / 2;
@@ -500,33 +525,37 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     if (!slot.done) ck(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "event");
     char* hb = static_cast<char*>(slot.host);
-    const size_t ioff = (dbytes + 255) & ~size_t(255);
     std::memcpy(hb, ctx->hprobs.data(), dbytes);
     std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
-    ck(cudaMemcpyAsync(slot.dev.p, hb, ioff + ibytes, cudaMemcpyHostToDevice, ctx->stream),
+    std::memcpy(hb + boff, cbase.data(), (nq + 1) * 4);
+    std::memcpy(hb + poff, cprob.data(), nchunks * 4);
+    ck(cudaMemcpyAsync(slot.dev.p, hb, need, cudaMemcpyHostToDevice, ctx->stream),
        "descriptor upload");
-    const csa::DecodeProblem* dprobs = slot.dev.as<csa::DecodeProblem>();
-    const csa::InsertProblem* diprobs =
-        reinterpret_cast<const csa::InsertProblem*>(slot.dev.as<char>() + ioff);
-    cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+    char* db = slot.dev.as<char>();
+    const csa::DecodeProblem* dprobs = reinterpret_cast<const csa::DecodeProblem*>(db);
+    const csa::InsertProblem* diprobs = reinterpret_cast<const csa::InsertProblem*>(db + ioff);
+    const uint32_t* dcbase = reinterpret_cast<const uint32_t*>(db + boff);
+    const uint32_t* dcprob = reinterpret_cast<const uint32_t*>(db + poff);
+    std::array<cudaEvent_t, 4> ev{};
     if (ctx->profile) {
-        e0 = ctx->take_event();
-        e1 = ctx->take_event();
-        e2 = ctx->take_event();
-        ck(cudaEventRecord(e0, ctx->stream), "event");
+        for (auto& e : ev) e = ctx->take_event();
+        ck(cudaEventRecord(ev[0], ctx->stream), "event");
     }
-    ck(csa::launch_decode(dprobs, static_cast<uint32_t>(nq), kpc, cs, d, ctx->stream),
-       "decode launch");
-    if (ctx->profile) ck(cudaEventRecord(e1, ctx->stream), "event");
+    ck(csa::launch_select(dprobs, static_cast<uint32_t>(nq), kpc, cs, ctx->stream),
+       "select launch");
+    if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
+    ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
+                          ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream),
+       "attend launch");
+    if (ctx->profile) ck(cudaEventRecord(ev[2], ctx->stream), "event");
     ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
     ck(cudaEventRecord(slot.done, ctx->stream), "event");
     slot.used = true;
     if (ctx->profile) {
-        ck(cudaEventRecord(e2, ctx->stream), "event");
-        ctx->ev_decode.emplace_back(e0, e1);
-        ctx->ev_insert.emplace_back(e1, e2);
+        ck(cudaEventRecord(ev[3], ctx->stream), "event");
+        ctx->ev_steps.push_back(ev);
     }
-    ctx->launches += 2;
+    ctx->launches += 3;
 
     // host bookkeeping: SearchState + Session counters
     std::vector<uint64_t> n_before(ns);
@@ -789,20 +818,39 @@ csattn_status csattn_ctx_create(int device, void* stream, csattn_ctx* out) {
     });
 }
 
+}  // extern "C"
+
+// A context lives until its handle AND every session created on it are gone
+// (sessions keep a reference), so destruction order never matters.
+static void ctx_release(csattn_ctx ctx) {
+    if (--ctx->refs > 0) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& ev : ctx->ev_steps)
+        for (cudaEvent_t e : ev) ctx->ev_pool.push_back(e);
+    for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->own) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+extern "C" {
+
 csattn_status csattn_ctx_destroy(csattn_ctx ctx) {
     return guard([&] {
         if (!ctx) return;
-        cudaStreamSynchronize(ctx->stream);
-        for (auto& pr : ctx->ev_decode) ctx->ev_pool.push_back(pr.first);
-        for (auto& pr : ctx->ev_insert) {
-            ctx->ev_pool.push_back(pr.first);
-            ctx->ev_pool.push_back(pr.second);
-        }
-        for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
-        if (ctx->own) cudaStreamDestroy(ctx->stream);
-        delete ctx;
+        ctx_release(ctx);
     });
 }
+
+}  // extern "C"
+
+csattn_session_s::~csattn_session_s() {
+    if (ctx) {
+        cudaStreamSynchronize(ctx->stream);
+        ctx_release(ctx);
+    }
+}
+
+extern "C" {
 
 csattn_status csattn_ctx_synchronize(csattn_ctx ctx) {
     return guard([&] { ck(cudaStreamSynchronize(ctx->stream), "synchronize"); });
@@ -814,34 +862,22 @@ csattn_status csattn_ctx_profile(csattn_ctx ctx, int32_t enable) {
     return guard([&] { ctx->profile = enable != 0; });
 }
 
-csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* decode_ms, uint64_t* n_decode,
-                                      double* insert_ms, uint64_t* n_insert, int32_t reset) {
+csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* ms, uint64_t* steps,
+                                      int32_t reset) {
     return guard([&] {
         ck(cudaStreamSynchronize(ctx->stream), "profile sync");
-        double a = 0.0, b = 0.0;
-        for (auto& pr : ctx->ev_decode) {
-            float ms = 0.0f;
-            ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "elapsed");
-            a += ms;
-        }
-        for (auto& pr : ctx->ev_insert) {
-            float ms = 0.0f;
-            ck(cudaEventElapsedTime(&ms, pr.first, pr.second), "elapsed");
-            b += ms;
-        }
-        *decode_ms = a;
-        *insert_ms = b;
-        *n_decode = ctx->ev_decode.size();
-        *n_insert = ctx->ev_insert.size();
-        if (reset) {
-            // e1 is shared by a decode and an insert pair: return each event once
-            for (auto& pr : ctx->ev_decode) ctx->ev_pool.push_back(pr.first);
-            for (auto& pr : ctx->ev_insert) {
-                ctx->ev_pool.push_back(pr.first);
-                ctx->ev_pool.push_back(pr.second);
+        ms[0] = ms[1] = ms[2] = 0.0;
+        for (auto& ev : ctx->ev_steps)
+            for (int k = 0; k < 3; ++k) {
+                float x = 0.0f;
+                ck(cudaEventElapsedTime(&x, ev[k], ev[k + 1]), "elapsed");
+                ms[k] += x;
             }
-            ctx->ev_decode.clear();
-            ctx->ev_insert.clear();
+        *steps = ctx->ev_steps.size();
+        if (reset) {
+            for (auto& ev : ctx->ev_steps)
+                for (cudaEvent_t e : ev) ctx->ev_pool.push_back(e);
+            ctx->ev_steps.clear();
         }
     });
 }
@@ -1101,11 +1137,7 @@ csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn
 }
 
 csattn_status csattn_session_destroy(csattn_session s) {
-    return guard([&] {
-        if (!s) return;
-        cudaStreamSynchronize(s->ctx->stream);
-        delete s;
-    });
+    return guard([&] { delete s; });
 }
 
 csattn_status csattn_session_info_get(csattn_session s, csattn_session_info* o) {
@@ -1134,6 +1166,48 @@ csattn_status csattn_session_set_retrieval(csattn_session s, const csattn_retrie
         set_retrieval(s, rc);
         push_dev(s);
         ck(cudaStreamSynchronize(s->ctx->stream), "set_retrieval");
+    });
+}
+
+csattn_status csattn_session_keep_candidates(csattn_session s, int32_t enable) {
+    return guard([&] {
+        if (enable && !s->cache.p) {
+            s->cache.alloc(s->group * s->h.max_ctx * sizeof(double));
+        } else if (!enable && s->cache.p && s->rc.search_period <= 1) {
+            cudaStreamSynchronize(s->ctx->stream);
+            cudaFree(s->cache.p);
+            s->cache.p = nullptr;
+            s->cache.n = 0;
+        }
+    });
+}
+
+csattn_status csattn_session_candidates(csattn_session s, uint64_t head, uint32_t* indices,
+                                        double* scores, uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        if (head >= s->group) fail(CSATTN_ERR_PARAMETER, "query head out of range");
+        if (!s->cache.p) fail(CSATTN_ERR_PARAMETER, "candidates are not kept (keep_candidates)");
+        *n = 0;
+        const HeadState& hs = s->hs[head];
+        if (!hs.has_cache) return;
+        std::vector<double> c(hs.n_cache);
+        ck(cudaMemcpyAsync(c.data(), s->cache.as<double>() + head * s->h.max_ctx,
+                           hs.n_cache * sizeof(double), cudaMemcpyDeviceToHost, s->ctx->stream),
+           "copy candidates");
+        ck(cudaStreamSynchronize(s->ctx->stream), "candidates");
+        uint64_t k = 0;
+        for (uint64_t i = 0; i < hs.n_cache; ++i) {
+            uint64_t bits;
+            std::memcpy(&bits, &c[i], 8);
+            if (bits == 0x7ff4deadbeef0000ull) continue;  // absent (select.cu ABSENT)
+            if (k < cap) {
+                indices[k] = static_cast<uint32_t>(i);
+                scores[k] = c[i];
+            }
+            ++k;
+        }
+        if (k > cap) fail(CSATTN_ERR_PARAMETER, "candidate buffer too small");
+        *n = k;
     });
 }
 

@@ -19,7 +19,7 @@
 
 namespace csa {
 
-constexpr int KEY_BLOCK_SHIFT = 10;  // blk_off granularity: 1024 keys
+constexpr int KEY_BLOCK_SHIFT = 8;   // blk_off granularity: 256 keys
 constexpr int KEY_BLOCK = 1 << KEY_BLOCK_SHIFT;
 constexpr int MAXM = 32;             // subspaces
 constexpr int MAXTAU = 8;            // backoff centroids per subspace

@@ -9,10 +9,16 @@
 
 namespace csa {
 
-// decode.cu: fused route + gather + select + attend, one cluster per problem
-size_t decode_smem_bytes(uint32_t kpc, uint32_t d);
-cudaError_t launch_decode(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
-                          uint32_t d, cudaStream_t st);
+// select.cu: route + gather + top-K, one cluster per problem
+size_t select_smem_bytes(uint32_t kpc);
+cudaError_t launch_select(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
+                          cudaStream_t st);
+
+// attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
+constexpr uint32_t ATT_ROWS = 128;
+cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
+                          const uint32_t* chunk_base, uint32_t nchunks, float* part,
+                          uint32_t* counters, uint32_t d, cudaStream_t st);
 
 // insert.cu: append + streaming insert, one CTA per session
 cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st);

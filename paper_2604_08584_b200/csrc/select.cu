@@ -1,26 +1,23 @@
-// decode.cu — the fused CSAttention decode step on sm_100a.
+// select.cu — CSAttention decode, part 1: route + gather + top-K on sm_100a.
 //
 // One thread-block CLUSTER per (session, query head) "problem". CTA r of the
 // cluster owns the key range [r*KPC, (r+1)*KPC) and keeps that range's fp64
-// candidate scores in its own shared memory for the whole step, so the
-// per-key scores never touch HBM. Phases (reference functions in brackets):
+// candidate scores in its own shared memory, so per-key scores never touch
+// HBM. Phases (reference functions in brackets):
 //   1. route     [select_centroids retrieval.cpp:40-87]  per-subspace cosine
-//                argmax (or top-tau backoff) of the normalized query slice —
-//                a warp-level GEMV over m*C*w centroid floats, fp64 exact.
+//                argmax (or top-tau backoff) of the normalized query slice,
+//                fp64 exact, m*C dot products spread over the CTA.
 //   2. gather    [gather_lists :95-109, reduce_by_key :111-148]  the selected
-//                index-sorted lists are read as coalesced 128-bit ranges
-//                (one range per key block) and accumulated with a
-//                conflict-free shared-memory RMW, list by list in gathered
-//                order: score(i) = sum_l w_b(l) * double(score_l(i)).
+//                index-sorted lists' key-block ranges are streamed into a
+//                shared-memory ring by TMA bulk copies (cp.async.bulk +
+//                mbarrier complete_tx, several chunks in flight) and
+//                accumulated with a conflict-free shared-memory RMW, chunk by
+//                chunk in gathered-list order:
+//                score(i) = sum_l w_b(l) * double(score_l(i)).
 //   3. select    [select_topk :150-228]  cluster-wide radix select on the
 //                orderable 64-bit image of the fp64 score, ties by lower
-//                index, recent-window passthrough and newest-first padding.
-//   4. attend    [dense_attention core.cpp:118-169, masked]  split-K flash
-//                decoding over the K selected rows (CTA r takes positions
-//                [rK/cs, (r+1)K/cs)), log-sum-exp merge across the cluster
-//                through distributed shared memory.
-// Everything stays on chip between phases; the only HBM traffic is the
-// gathered list entries, the selected K/V rows, q/out and the index output.
+//                index, recent-window passthrough and newest-first padding;
+//                the K indices are written ascending for attend.cu.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -29,12 +26,15 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace csa {
 
 constexpr int DEC_THREADS = 512;
+constexpr int RING = 4;           // TMA staging slots
+constexpr int CHUNK_E = 512;      // entries per slot (4 KB)
 constexpr int DEC_WARPS = DEC_THREADS / 32;
 constexpr int HB_BITS = 10;
 constexpr int HB = 1 << HB_BITS;  // radix histogram bins
@@ -60,7 +60,6 @@ struct DecSmem {
     // values other CTAs of the cluster read through DSMEM
     unsigned long long x_kmax, x_kmin, x_tk;
     uint32_t x_cnt, x_tx, x_slice_total, x_nsel, x_nunt;
-    float x_m, x_s, x_M, x_S;
     // block-level scratch
     unsigned long long r64a[DEC_WARPS], r64b[DEC_WARPS];
     uint32_t r32a[DEC_WARPS], r32b[DEC_WARPS];
@@ -70,7 +69,11 @@ struct DecSmem {
     uint32_t b_tx, b_rem, b_bucket, b_dsel, b_done, b_nsurv, b_use_surv, b_cabove;
     int b_pshift;
     uint32_t surv_count, wpos, nsv, b_base, b_take;
-    float pacc[DMAX];
+    // gather stream
+    unsigned long long bar[RING];
+    uint32_t c_list[RING], c_cnt[RING];
+    uint32_t l_beg[MAXL], l_cnt[MAXL], l_first[MAXL + 1];
+    uint32_t nchunk, issue_l;
 };
 
 __device__ __forceinline__ unsigned long long ordkey(double x) {
@@ -266,60 +269,94 @@ __device__ void route(DecSmem& S, const SessionDev& sd, double* csc, uint32_t* r
 }
 
 // ---------------------------------------------------------------------------
-// Phase 2: gather + fp64 accumulate of this CTA's key range
+// Phase 2: gather + fp64 accumulate of this CTA's key range.
+// The per-list key-block ranges are concatenated into a stream of <= CHUNK_E
+// entry chunks; thread 0 keeps RING chunks in flight with TMA bulk copies,
+// every thread consumes chunks in order (so each key sees its lists in
+// gathered order: the fixed accumulation order).
 // ---------------------------------------------------------------------------
-__device__ void gather(DecSmem& S, const SessionDev& sd, double* acc, uint32_t k0, uint32_t k1,
-                       uint32_t N) {
+__device__ __forceinline__ void acc_entry(double* acc, uint32_t key, uint32_t sbits, double w,
+                                          uint32_t k0, uint32_t k1) {
+    if ((key & TOMB) || key < k0 || key >= k1) return;  // tombstone / neighbour block
+    const uint32_t li = key - k0;
+    const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(sbits)));
+    const double o = acc[li];
+    acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
+}
+
+// plan the chunk stream and launch the first RING bulk copies (thread 0 issues)
+__device__ void gather_issue(DecSmem& S, const SessionDev& sd, uint2* stage, uint32_t k0,
+                             uint32_t k1, uint32_t N) {
+    const uint32_t tid = threadIdx.x;
     const uint32_t last_blk = (N - 1) >> KEY_BLOCK_SHIFT;
     const uint32_t kb0 = k0 >> KEY_BLOCK_SHIFT;
     const uint32_t kb1 = (k1 + KEY_BLOCK - 1) >> KEY_BLOCK_SHIFT;
-    for (uint32_t l = 0; l < S.nl; ++l) {
-        const uint32_t t = S.lists[l];
-        const double w = sd.weights[S.lsub[l]];
+    if (tid < S.nl) {
+        const uint32_t t = S.lists[tid];
         const uint32_t* bo = sd.blk_off + static_cast<size_t>(t) * sd.nb_stride;
         const uint32_t beg = __ldg(bo + kb0);
-        const uint32_t end = kb1 <= last_blk ? __ldg(bo + kb1) : __ldg(sd.n_used + t);
-        const uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
-        // 16-byte aligned body: two entries per 128-bit load
-        uint32_t a = beg + (beg & 1u);
-        if ((beg & 1u) && threadIdx.x == 0 && beg < end) {
-            const uint2 v = __ldg(e + beg);
-            if (!(v.x & TOMB)) {
-                const uint32_t li = v.x - k0;
-                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.y)));
-                const double o = acc[li];
-                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
-            }
+        const uint32_t end = kb1 <= last_blk ? __ldg(bo + kb1) : __ldcg(sd.n_used + t);
+        // 16-byte aligned superset [beg & ~1, (end + 1) & ~1); cap2 is even
+        const uint32_t ab = beg & ~1u;
+        const uint32_t ae = end > beg ? ((end + 1) & ~1u) : ab;
+        S.l_beg[tid] = ab;
+        S.l_cnt[tid] = ae - ab;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t nch = 0;
+        for (uint32_t l = 0; l < S.nl; ++l) {
+            S.l_first[l] = nch;
+            nch += div_up(S.l_cnt[l], CHUNK_E);
         }
-        const uint32_t npair = end > a ? (end - a) >> 1 : 0;
-        const uint4* e4 = reinterpret_cast<const uint4*>(e + a);
-#pragma unroll 4
-        for (uint32_t p = threadIdx.x; p < npair; p += blockDim.x) {
-            const uint4 v = __ldg(e4 + p);
-            if (!(v.x & TOMB)) {
-                const uint32_t li = v.x - k0;
-                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.y)));
-                const double o = acc[li];
-                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
-            }
-            if (!(v.z & TOMB)) {
-                const uint32_t li = v.z - k0;
-                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.w)));
-                const double o = acc[li];
-                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
-            }
+        S.l_first[S.nl] = nch;
+        S.nchunk = nch;
+        S.issue_l = 0;
+        for (int r = 0; r < RING; ++r) mbar_init(&S.bar[r], 1);
+        fence_mbar_init();
+        for (uint32_t c = 0; c < nch && c < static_cast<uint32_t>(RING); ++c) {
+            // locate chunk c
+            while (S.l_first[S.issue_l + 1] <= c) ++S.issue_l;
+            const uint32_t l = S.issue_l;
+            const uint32_t off = (c - S.l_first[l]) * CHUNK_E;
+            const uint32_t n = min(static_cast<uint32_t>(CHUNK_E), S.l_cnt[l] - off);
+            const uint2* src = sd.ent + static_cast<size_t>(S.lists[l]) * sd.cap2 + S.l_beg[l] + off;
+            S.c_list[c % RING] = l;
+            S.c_cnt[c % RING] = n;
+            mbar_expect_tx(&S.bar[c % RING], n * 8);
+            bulk_g2s(stage + (c % RING) * CHUNK_E, src, n * 8, &S.bar[c % RING]);
         }
-        const uint32_t tail = a + 2 * npair;
-        if (tail < end && threadIdx.x == 32) {
-            const uint2 v = __ldg(e + tail);
-            if (!(v.x & TOMB)) {
-                const uint32_t li = v.x - k0;
-                const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(v.y)));
-                const double o = acc[li];
-                acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
-            }
+    }
+}
+
+__device__ void gather_consume(DecSmem& S, const SessionDev& sd, uint2* stage, double* acc,
+                               uint32_t k0, uint32_t k1) {
+    const uint32_t nch = S.nchunk;
+    for (uint32_t c = 0; c < nch; ++c) {
+        const uint32_t slot = c % RING;
+        mbar_wait(&S.bar[slot], (c / RING) & 1u);
+        const uint32_t l = S.c_list[slot];
+        const uint32_t n = S.c_cnt[slot];
+        const double w = sd.weights[S.lsub[l]];
+        const uint4* e4 = reinterpret_cast<const uint4*>(stage + slot * CHUNK_E);
+        for (uint32_t p = threadIdx.x; p < (n >> 1); p += blockDim.x) {
+            const uint4 v = e4[p];
+            acc_entry(acc, v.x, v.y, w, k0, k1);
+            acc_entry(acc, v.z, v.w, w, k0, k1);
         }
-        __syncthreads();
+        __syncthreads();  // slot consumed; meta of chunk c no longer needed
+        if (threadIdx.x == 0 && c + RING < nch) {
+            const uint32_t cn = c + RING;
+            while (S.l_first[S.issue_l + 1] <= cn) ++S.issue_l;
+            const uint32_t ln = S.issue_l;
+            const uint32_t off = (cn - S.l_first[ln]) * CHUNK_E;
+            const uint32_t nn = min(static_cast<uint32_t>(CHUNK_E), S.l_cnt[ln] - off);
+            const uint2* src = sd.ent + static_cast<size_t>(S.lists[ln]) * sd.cap2 + S.l_beg[ln] + off;
+            S.c_list[slot] = ln;
+            S.c_cnt[slot] = nn;
+            mbar_expect_tx(&S.bar[slot], nn * 8);
+            bulk_g2s(stage + slot * CHUNK_E, src, nn * 8, &S.bar[slot]);
+        }
     }
 }
 
@@ -610,18 +647,17 @@ __device__ void select_threshold(cg::cluster_group& cl, DecSmem& S, const KeyVie
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
-template <int VEC>
-__global__ void __launch_bounds__(DEC_THREADS, 1)
-decode_kernel(const DecodeProblem* __restrict__ probs, uint32_t kpc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(DEC_THREADS, 2)
+select_kernel(const DecodeProblem* __restrict__ probs, uint32_t kpc) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     DecSmem& S = *reinterpret_cast<DecSmem*>(smem_raw);
-    double* acc = reinterpret_cast<double*>(smem_raw + ((sizeof(DecSmem) + 15) & ~size_t(15)));
+    uint2* stage = reinterpret_cast<uint2*>(smem_raw + ((sizeof(DecSmem) + 127) & ~size_t(127)));
+    double* acc = reinterpret_cast<double*>(stage + RING * CHUNK_E);
     cg::cluster_group cl = cg::this_cluster();
     const int rank = cl.block_rank(), cs = cl.num_blocks();
     const DecodeProblem& P = probs[blockIdx.x / cs];
     const SessionDev& sd = *P.s;
     const uint32_t tid = threadIdx.x, N = P.N, K = P.K, d = sd.d;
-    float* wacc = reinterpret_cast<float*>(acc + kpc);
     const bool leader = rank == 0;
 
     const uint32_t k0 = rank * kpc;
@@ -639,10 +675,11 @@ decode_kernel(const DecodeProblem* __restrict__ probs, uint32_t kpc) {
     // ---- 1+2: candidate scores of this CTA's key range ----
     if (P.mode & MODE_SEARCH) {
         route(S, sd, acc, P.rep, leader);  // acc doubles as the m*C score scratch
-        for (uint32_t l = tid; l < kpc; l += blockDim.x)
+        if (nloc) gather_issue(S, sd, stage, k0, k1, N);  // TMA copies in flight ...
+        for (uint32_t l = tid; l < kpc; l += blockDim.x)  // ... while acc is reset
             acc[l] = __longlong_as_double(static_cast<long long>(ABSENT));
         __syncthreads();
-        if (nloc) gather(S, sd, acc, k0, k1, N);
+        if (nloc) gather_consume(S, sd, stage, acc, k0, k1);
         if (P.mode & MODE_STORE_CACHE)
             for (uint32_t l = tid; l < nloc; l += blockDim.x) P.cache[k0 + l] = acc[l];
     } else {
@@ -747,181 +784,23 @@ decode_kernel(const DecodeProblem* __restrict__ probs, uint32_t kpc) {
             if (s) P.sel[pos++] = k0 + l;
         }
     }
-    cl.sync();  // selected indices visible cluster-wide
-
-    // ---- 4: split-K attention over the K selected rows ----
-    const uint32_t r0 = static_cast<uint32_t>((static_cast<unsigned long long>(K) * rank) / cs);
-    const uint32_t r1 = static_cast<uint32_t>((static_cast<unsigned long long>(K) * (rank + 1)) / cs);
-    const uint32_t nrows = r1 - r0;
-    float* lg = reinterpret_cast<float*>(acc);  // logits reuse the score region
-    const int w = tid >> 5, ln = tid & 31;
-    constexpr int NC = DMAX / (32 * VEC);
-    const int nchunks = static_cast<int>(div_up(d, 32 * VEC));
-    float qr[NC][VEC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-            const uint32_t e = c * 32 * VEC + ln * VEC + v;
-            qr[c][v] = (c < nchunks && e < d) ? S.q[e] : 0.0f;
-        }
-    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
-    const uint32_t P0 = sd.P;
-    auto row_ptr = [&](const float* pre, const float* tail, uint32_t i) {
-        return i < P0 ? pre + static_cast<size_t>(i) * d : tail + static_cast<size_t>(i - P0) * d;
-    };
-    float mx = -FLT_MAX;
-    constexpr int U = 4;
-    for (uint32_t rb = w; rb < nrows; rb += DEC_WARPS * U) {
-        float dp[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            dp[u] = 0.0f;
-            const uint32_t r = rb + u * DEC_WARPS;
-            if (r < nrows) {
-                const uint32_t i = __ldcg(P.sel + r0 + r);
-                const float* kr = row_ptr(sd.kpre, sd.ktail, i);
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    if (c >= nchunks) break;
-                    const uint32_t e = c * 32 * VEC + ln * VEC;
-                    if (VEC == 4) {
-                        if (e < d) {
-                            const float4 kk = __ldg(reinterpret_cast<const float4*>(kr + e));
-                            dp[u] = fmaf(qr[c][0], kk.x, dp[u]);
-                            dp[u] = fmaf(qr[c][1], kk.y, dp[u]);
-                            dp[u] = fmaf(qr[c][2], kk.z, dp[u]);
-                            dp[u] = fmaf(qr[c][3], kk.w, dp[u]);
-                        }
-                    } else {
-                        if (e < d) dp[u] = fmaf(qr[c][0], __ldg(kr + e), dp[u]);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const float s = warp_sumf(dp[u]) * scale;
-            const uint32_t r = rb + u * DEC_WARPS;
-            if (r < nrows) {
-                if (ln == 0) lg[r] = s;
-                mx = fmaxf(mx, s);
-            }
-        }
-    }
-    mx = warp_maxf(mx);
-    if (ln == 0) S.rf[w] = mx;
-    __syncthreads();
-    float M = -FLT_MAX;
-#pragma unroll
-    for (int i = 0; i < DEC_WARPS; ++i) M = fmaxf(M, S.rf[i]);
-    __syncthreads();
-    float av[NC][VEC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c)
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) av[c][v] = 0.0f;
-    float ssum = 0.0f;
-    for (uint32_t rb = w; rb < nrows; rb += DEC_WARPS * U) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t r = rb + u * DEC_WARPS;
-            if (r < nrows) {
-                const uint32_t i = __ldcg(P.sel + r0 + r);
-                const float p = expf(lg[r] - M);
-                ssum += p;
-                const float* vr = row_ptr(sd.vpre, sd.vtail, i);
-#pragma unroll
-                for (int c = 0; c < NC; ++c) {
-                    if (c >= nchunks) break;
-                    const uint32_t e = c * 32 * VEC + ln * VEC;
-                    if (VEC == 4) {
-                        if (e < d) {
-                            const float4 vv = __ldg(reinterpret_cast<const float4*>(vr + e));
-                            av[c][0] = fmaf(p, vv.x, av[c][0]);
-                            av[c][1] = fmaf(p, vv.y, av[c][1]);
-                            av[c][2] = fmaf(p, vv.z, av[c][2]);
-                            av[c][3] = fmaf(p, vv.w, av[c][3]);
-                        }
-                    } else {
-                        if (e < d) av[c][0] = fmaf(p, __ldg(vr + e), av[c][0]);
-                    }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c >= nchunks) break;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-            const uint32_t e = c * 32 * VEC + ln * VEC + v;
-            if (e < d) wacc[w * d + e] = av[c][v];
-        }
-    }
-    if (ln == 0) S.rf[w] = ssum;
-    __syncthreads();
-    for (uint32_t t = tid; t < d; t += blockDim.x) {
-        float a = 0.0f;
-        for (int i = 0; i < DEC_WARPS; ++i) a += wacc[i * d + t];
-        S.pacc[t] = a;
-    }
-    if (tid == 0) {
-        float s = 0.0f;
-        for (int i = 0; i < DEC_WARPS; ++i) s += S.rf[i];
-        S.x_m = nrows ? M : -FLT_MAX;
-        S.x_s = s;
-    }
-    cl.sync();  // partials published
-    if (leader) {
-        float GM = -FLT_MAX;
-        for (int c = 0; c < cs; ++c) GM = fmaxf(GM, *remote(cl, &S.x_m, c));
-        float GS = 0.0f;
-        for (int c = 0; c < cs; ++c) {
-            const float s = *remote(cl, &S.x_s, c);
-            if (s > 0.0f) GS += s * expf(*remote(cl, &S.x_m, c) - GM);
-        }
-        const float inv = 1.0f / GS;
-        for (uint32_t t = tid; t < d; t += blockDim.x) {
-            float o = 0.0f;
-            for (int c = 0; c < cs; ++c) {
-                const float s = *remote(cl, &S.x_s, c);
-                if (s > 0.0f) o += remote(cl, S.pacc, c)[t] * expf(*remote(cl, &S.x_m, c) - GM);
-            }
-            if (P.out) P.out[t] = o * inv;
-        }
-        if (tid == 0) {
-            S.x_M = GM;
-            S.x_S = GS;
-            reinterpret_cast<DecodeReport*>(P.rep)->k = K;
-        }
-    }
-    cl.sync();  // CTA 0 done reading peers; global M/S published
-    if ((P.mode & MODE_WEIGHTS) && P.weights) {
-        const float GM = *remote(cl, &S.x_M, 0);
-        const float inv = 1.0f / *remote(cl, &S.x_S, 0);
-        for (uint32_t r = tid; r < nrows; r += blockDim.x)
-            P.weights[r0 + r] = expf(lg[r] - GM) * inv;
-    }
+    if (leader && tid == 0) reinterpret_cast<DecodeReport*>(P.rep)->k = K;
     cl.sync();  // nobody exits while a peer may still read its shared memory
 }
 
-size_t decode_smem_bytes(uint32_t kpc, uint32_t d) {
-    return ((sizeof(DecSmem) + 15) & ~size_t(15)) + static_cast<size_t>(kpc) * sizeof(double) +
-           static_cast<size_t>(DEC_WARPS) * d * sizeof(float);
+size_t select_smem_bytes(uint32_t kpc) {
+    return ((sizeof(DecSmem) + 127) & ~size_t(127)) + static_cast<size_t>(RING) * CHUNK_E * 8 +
+           static_cast<size_t>(kpc) * sizeof(double);
 }
 
-template <int VEC>
-static cudaError_t launch_decode_t(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc,
-                                   uint32_t cs, uint32_t d, cudaStream_t st) {
-    const size_t smem = decode_smem_bytes(kpc, d);
-    cudaError_t e = cudaFuncSetAttribute(decode_kernel<VEC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+cudaError_t launch_select(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
+                          cudaStream_t st) {
+    const size_t smem = select_smem_bytes(kpc);
+    cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     if (cs > 8) {
-        e = cudaFuncSetAttribute(decode_kernel<VEC>,
-                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
     }
     cudaLaunchConfig_t cfg = {};
@@ -936,13 +815,7 @@ static cudaError_t launch_decode_t(const DecodeProblem* probs, uint32_t nprob, u
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, decode_kernel<VEC>, probs, kpc);
-}
-
-cudaError_t launch_decode(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
-                          uint32_t d, cudaStream_t st) {
-    if (d % 4 == 0) return launch_decode_t<4>(probs, nprob, kpc, cs, d, st);
-    return launch_decode_t<1>(probs, nprob, kpc, cs, d, st);
+    return cudaLaunchKernelEx(&cfg, select_kernel, probs, kpc);
 }
 
 }  // namespace csa

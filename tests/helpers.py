@@ -44,14 +44,28 @@ def rel_err(a, b):
 
 
 def lockstep(gpu: cs.Session, ref, q, k, v, P, T, group=1, check_tables_every=0, tol=1e-3):
-    """Drive the GPU session and a CPU checker through T identical steps."""
+    """Drive the GPU session and a CPU checker through T identical steps.
+    With the reference library as checker, the accumulated candidate sets
+    (reduce_by_key output, SearchState::cached) are compared bit-exactly too."""
     d = k.shape[1]
     worst = 0.0
+    check_cand = hasattr(ref, "candidates")
+    if check_cand:
+        gpu.keep_candidates(True)
     for t in range(T):
         qs = np.stack([q[P + t]] * group) if q.ndim == 2 else q[t]
         g = gpu.decode_step(qs, k[P + t], v[P + t], want_weights=True)
         g = g if isinstance(g, list) else [g]
         r = ref.step(qs, k[P + t], v[P + t])
+        if check_cand:
+            for h in range(group):
+                gi, gs = gpu.candidates(h)
+                ri, rs = ref.candidates(h)
+                assert np.array_equal(gi, ri), (t, h, "candidate keys",
+                                                np.setxor1d(gi, ri)[:8])
+                bad = np.nonzero(gs.view(np.uint64) != rs.view(np.uint64))[0]
+                assert bad.size == 0, (t, h, "candidate scores", gi[bad[:4]], gs[bad[:4]],
+                                       rs[bad[:4]])
         for h, (gr, (sel, out, wts, rep)) in enumerate(zip(g, r)):
             assert gr.k == len(sel), (t, h, gr.k, len(sel))
             assert np.array_equal(gr.selected, sel), (t, h, np.setdiff1d(gr.selected, sel)[:8],
