@@ -71,8 +71,8 @@ struct DecSmem {
     uint32_t surv_count, wpos, nsv, b_base, b_take;
     // gather stream
     unsigned long long bar[RING];
-    uint32_t c_list[RING], c_cnt[RING];
-    uint32_t l_beg[MAXL], l_cnt[MAXL], l_first[MAXL + 1];
+    uint32_t c_list[RING], c_cnt[RING], c_vlo[RING], c_vhi[RING];
+    uint32_t l_beg[MAXL], l_cnt[MAXL], l_first[MAXL + 1], l_lo[MAXL], l_hi[MAXL];
     uint32_t nchunk, issue_l;
 };
 
@@ -301,6 +301,8 @@ __device__ void gather_issue(DecSmem& S, const SessionDev& sd, uint2* stage, uin
         const uint32_t ae = end > beg ? ((end + 1) & ~1u) : ab;
         S.l_beg[tid] = ab;
         S.l_cnt[tid] = ae - ab;
+        S.l_lo[tid] = beg;  // the aligned superset may include one entry of a
+        S.l_hi[tid] = end;  // neighbour block or one slot past n_used: masked
     }
     __syncthreads();
     if (tid == 0) {
@@ -323,6 +325,8 @@ __device__ void gather_issue(DecSmem& S, const SessionDev& sd, uint2* stage, uin
             const uint2* src = sd.ent + static_cast<size_t>(S.lists[l]) * sd.cap2 + S.l_beg[l] + off;
             S.c_list[c % RING] = l;
             S.c_cnt[c % RING] = n;
+            S.c_vlo[c % RING] = S.l_lo[l] > S.l_beg[l] + off ? S.l_lo[l] - S.l_beg[l] - off : 0u;
+            S.c_vhi[c % RING] = min(n, S.l_hi[l] - S.l_beg[l] - off);
             mbar_expect_tx(&S.bar[c % RING], n * 8);
             bulk_g2s(stage + (c % RING) * CHUNK_E, src, n * 8, &S.bar[c % RING]);
         }
@@ -337,12 +341,13 @@ __device__ void gather_consume(DecSmem& S, const SessionDev& sd, uint2* stage, d
         mbar_wait(&S.bar[slot], (c / RING) & 1u);
         const uint32_t l = S.c_list[slot];
         const uint32_t n = S.c_cnt[slot];
+        const uint32_t vlo = S.c_vlo[slot], vhi = S.c_vhi[slot];
         const double w = sd.weights[S.lsub[l]];
         const uint4* e4 = reinterpret_cast<const uint4*>(stage + slot * CHUNK_E);
         for (uint32_t p = threadIdx.x; p < (n >> 1); p += blockDim.x) {
             const uint4 v = e4[p];
-            acc_entry(acc, v.x, v.y, w, k0, k1);
-            acc_entry(acc, v.z, v.w, w, k0, k1);
+            if (2 * p >= vlo && 2 * p < vhi) acc_entry(acc, v.x, v.y, w, k0, k1);
+            if (2 * p + 1 >= vlo && 2 * p + 1 < vhi) acc_entry(acc, v.z, v.w, w, k0, k1);
         }
         __syncthreads();  // slot consumed; meta of chunk c no longer needed
         if (threadIdx.x == 0 && c + RING < nch) {
@@ -354,6 +359,8 @@ __device__ void gather_consume(DecSmem& S, const SessionDev& sd, uint2* stage, d
             const uint2* src = sd.ent + static_cast<size_t>(S.lists[ln]) * sd.cap2 + S.l_beg[ln] + off;
             S.c_list[slot] = ln;
             S.c_cnt[slot] = nn;
+            S.c_vlo[slot] = S.l_lo[ln] > S.l_beg[ln] + off ? S.l_lo[ln] - S.l_beg[ln] - off : 0u;
+            S.c_vhi[slot] = min(nn, S.l_hi[ln] - S.l_beg[ln] - off);
             mbar_expect_tx(&S.bar[slot], nn * 8);
             bulk_g2s(stage + slot * CHUNK_E, src, nn * 8, &S.bar[slot]);
         }
