@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -145,7 +146,13 @@ struct csattn_ctx_s {
     bool profile = false;
     std::vector<std::array<cudaEvent_t, 4>> ev_steps;  // select | attend | insert
     DevMem part, counters;  // attention partials + per-problem merge counters
+    DevMem plans;           // route.cu -> select.cu routing plans
     uint64_t counters_n = 0;
+    // select-kernel phase timestamps (env CSATTN_PHASE_PROF=1; diagnostics only)
+    bool phase_prof = std::getenv("CSATTN_PHASE_PROF") != nullptr;
+    DevMem phase;
+    double phase_sum[6] = {0, 0, 0, 0, 0, 0};
+    uint64_t phase_n = 0;
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t take_event() {
         if (!ev_pool.empty()) {
@@ -416,7 +423,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
         nq += s->group;
         maxN = std::max<uint64_t>(maxN, s->N);
-        maxmc = std::max<uint64_t>(maxmc, static_cast<uint64_t>(s->h.m) * s->h.C);
+        // the score array doubles as routing scratch: m*C fp64 dots + C*d centroids
+        const uint64_t mc = static_cast<uint64_t>(s->h.m) * s->h.C;
+        maxmc = std::max<uint64_t>(maxmc, 0 * mc);  // scores only (routing is route.cu)
     }
     if ((selected || weights) && sel_stride < maxK)
         fail(CSATTN_ERR_PARAMETER, "selected/weights stride " + std::to_string(sel_stride) +
@@ -458,6 +467,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         dw = weights ? reinterpret_cast<float*>(base + o_w) : nullptr;
     }
     ctx->hprobs.resize(nq);
+    if (ctx->phase_prof) {
+        ctx->phase.ensure(nq * 16 * 8 * sizeof(unsigned long long));
+        ck(cudaMemsetAsync(ctx->phase.p, 0, nq * 16 * 8 * 8, ctx->stream), "memset");
+    }
     ctx->hiprobs.resize(ns);
     uint64_t qi = 0;
     std::vector<uint32_t> searched(nq);
@@ -482,6 +495,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             P.mode = (srch ? csa::MODE_SEARCH : 0u) |
                      ((srch && P.cache) ? csa::MODE_STORE_CACHE : 0u) |
                      (dw ? csa::MODE_WEIGHTS : 0u);
+            P.prof = ctx->phase_prof ? ctx->phase.as<unsigned long long>() + qi * 16 * 8 : nullptr;
         }
         csa::InsertProblem& I = ctx->hiprobs[i];
         I.s = s->dev.as<csa::SessionDev>();
@@ -541,7 +555,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         for (auto& e : ev) e = ctx->take_event();
         ck(cudaEventRecord(ev[0], ctx->stream), "event");
     }
-    ck(csa::launch_select(dprobs, static_cast<uint32_t>(nq), kpc, cs, ctx->stream),
+    ctx->plans.ensure(nq * sizeof(csa::RoutePlan));
+    ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), cs,
+                         kpc, ctx->stream),
+       "route launch");
+    ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), kpc,
+                          cs, ctx->stream),
        "select launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
@@ -555,7 +574,27 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaEventRecord(ev[3], ctx->stream), "event");
         ctx->ev_steps.push_back(ev);
     }
-    ctx->launches += 3;
+    ctx->launches += 4;
+    if (ctx->phase_prof) {
+        // mean per-CTA duration of each select phase (route, issue, consume,
+        // keys, select, emit); prints at context teardown
+        std::vector<unsigned long long> ph(nq * 16 * 8);
+        ck(cudaMemcpyAsync(ph.data(), ctx->phase.p, ph.size() * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream), "phase copy");
+        ck(cudaStreamSynchronize(ctx->stream), "phase sync");
+        double sum[6] = {0, 0, 0, 0, 0, 0};
+        uint64_t n = 0;
+        for (uint64_t i = 0; i < nq * 16; ++i) {
+            const unsigned long long* t = &ph[i * 8];
+            if (!t[0] || !t[6]) continue;
+            for (int k = 0; k < 6; ++k) sum[k] += (t[k + 1] && t[k]) ? double(t[k + 1] - t[k]) : 0.0;
+            ++n;
+        }
+        if (n) {
+            for (int k = 0; k < 6; ++k) ctx->phase_sum[k] += sum[k] / n;
+            ctx->phase_n += 1;
+        }
+    }
 
     // host bookkeeping: SearchState + Session counters
     std::vector<uint64_t> n_before(ns);
@@ -824,6 +863,14 @@ csattn_status csattn_ctx_create(int device, void* stream, csattn_ctx* out) {
 // (sessions keep a reference), so destruction order never matters.
 static void ctx_release(csattn_ctx ctx) {
     if (--ctx->refs > 0) return;
+    if (ctx->phase_n) {
+        const char* nm[6] = {"route", "issue", "consume", "keys", "select", "emit"};
+        std::fprintf(stderr, "[csattn] select phases (mean per CTA over %llu steps, us):",
+                     static_cast<unsigned long long>(ctx->phase_n));
+        for (int k = 0; k < 6; ++k)
+            std::fprintf(stderr, " %s=%.2f", nm[k], ctx->phase_sum[k] / ctx->phase_n / 1e3);
+        std::fprintf(stderr, "\n");
+    }
     cudaStreamSynchronize(ctx->stream);
     for (auto& ev : ctx->ev_steps)
         for (cudaEvent_t e : ev) ctx->ev_pool.push_back(e);

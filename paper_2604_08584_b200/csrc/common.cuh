@@ -80,6 +80,7 @@ struct DecodeProblem {
     uint32_t K;        // selected-set size
     uint32_t n_cache;  // context length when the cache was filled
     uint32_t mode;     // MODE_* bits
+    unsigned long long* prof;  // phase timestamps [cs][8] (CSATTN_PHASE_PROF) or null
 };
 constexpr uint32_t MODE_SEARCH = 1u;       // route + gather + accumulate
 constexpr uint32_t MODE_STORE_CACHE = 2u;  // persist candidate scores
@@ -94,6 +95,16 @@ struct DecodeReport {
     uint32_t pad[2];
     double best_cos[MAXM];
     uint32_t lists[MAXL];        // table ids gathered, in order
+};
+
+// Routing result + gather plan of one problem (route.cu -> select.cu).
+constexpr int MAX_CLUSTER = 16;
+struct RoutePlan {
+    uint32_t nl;
+    uint32_t pad[3];
+    uint32_t lists[MAXL];               // table ids, gathered order
+    uint32_t lsub[MAXL];                // their subspaces
+    uint2 bounds[MAX_CLUSTER * MAXL];   // [rank][list]: entry range [x, y)
 };
 
 // Per-session append + insert descriptor.

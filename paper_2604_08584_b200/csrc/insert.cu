@@ -1,16 +1,20 @@
 // insert.cu — KvStore::append (core.cpp:71-79) + streaming_insert
 // (retrieval.cpp:272-301, TopList::try_insert index.cpp:22-44) on sm_100a.
 //
-// One CTA per session, one thread per (subspace b, centroid j) table.
-// The new key's index N is larger than every stored key, so in the
-// index-sorted layout an admitted entry is a plain append at n_used[t].
-// Eviction removes the TopList back = the live entry that is first in
-// eviction order (score asc, key desc); it is found in O(1) at the tail of
-// the per-table low buffer (stored in DESCENDING eviction order, so the next
-// victim is low[cnt-1]) and tombstoned in place. When a buffer runs dry the
-// CTA compacts that table (dropping its <= LOW_Q tombstones, rebuilding the
-// key-block offsets) and refills the buffer with the LOW_Q lowest live entries
-// via a radix select over the 64-bit eviction key.
+// One CTA per session. The new key's index N is larger than every stored key,
+// so in the index-sorted layout an admitted entry is a plain append at
+// n_used[t]. Eviction removes the TopList back = the live entry first in
+// eviction order (score asc, key desc), found in O(1) at the tail of the
+// per-table low buffer (kept in DESCENDING eviction order: the next victim is
+// low[cnt-1]) and tombstoned in place.
+//   A. one thread per (subspace b, centroid j) table: fp64 score of the new key
+//      slice, strict-win admission against the victim, tombstone + append;
+//   B. one warp per table whose new entry belongs in its low buffer: the
+//      buffer is loaded into registers, ranked by ballot and written back
+//      shifted by one (two memory round trips, no serial shifting);
+//   C. the whole CTA compacts any table whose buffer ran dry or whose slack is
+//      used up, rebuilds its key-block offsets and refills the buffer (radix
+//      select of the LOW_Q lowest eviction keys).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -22,13 +26,23 @@
 namespace csa {
 
 constexpr int INS_THREADS = 512;
+constexpr int INS_WARPS = INS_THREADS / 32;
+constexpr int LQ_PER_LANE = LOW_Q / 32;
+
+struct BufEnt {
+    float score;
+    uint32_t pos;
+    uint32_t cnt;
+};
 
 struct InsSmem {
     float ks[DMAX];
     uint32_t zero_mask;
-    uint32_t nref;
+    uint32_t nref, nbuf;
     uint32_t applied;
     uint32_t reflist[MAX_TABLES];  // tables needing compaction + refill
+    uint32_t buflist[MAX_TABLES];  // tables whose new entry enters the low buffer
+    BufEnt bufent[MAX_TABLES];     // that entry (key = N) + the buffer count
     RefillSmem r;
 };
 
@@ -40,13 +54,15 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
     const uint32_t d = sd.d, m = sd.m, C = sd.C, T = m * C, N = P.N;
     // KvStore::append: row N lands at tail row N - P
     for (uint32_t x = threadIdx.x; x < d; x += blockDim.x) {
-        sd.ktail[static_cast<size_t>(N - sd.P) * d + x] = P.key[x];
+        const float kx = P.key[x];
+        sd.ktail[static_cast<size_t>(N - sd.P) * d + x] = kx;
         sd.vtail[static_cast<size_t>(N - sd.P) * d + x] = P.value[x];
-        S.ks[x] = P.key[x];
+        S.ks[x] = kx;
     }
     if (threadIdx.x == 0) {
         S.zero_mask = 0;
         S.nref = 0;
+        S.nbuf = 0;
         S.applied = 0;
     }
     __syncthreads();
@@ -64,6 +80,7 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
         }
     }
     __syncthreads();
+    // ---- A: admission, tombstone, append ----
     uint8_t* mask = reinterpret_cast<uint8_t*>(P.rep + 1);
     const uint32_t new_blk = (N & (KEY_BLOCK - 1)) == 0;
     for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
@@ -78,18 +95,18 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
         uint32_t nu = sd.n_used[t];
         if (new_blk) sd.blk_off[static_cast<size_t>(t) * sd.nb_stride + (N >> KEY_BLOCK_SHIFT)] = nu;
         uint32_t applied = 0;
-        const uint32_t live = sd.live[t];
-        uint32_t cnt = sd.low_cnt[t];
-        LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
-        uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
         if (sd.L != 0) {
+            const uint32_t live = sd.live[t];
+            uint32_t cnt = sd.low_cnt[t];
+            LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
+            uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
             const bool full = live >= sd.L;
+            const bool complete = cnt == live;  // buffer holds every live entry
             bool ok = true;
-            bool complete = (cnt == live);
             if (full) {
                 const LowEnt victim = lo[cnt - 1];
                 if (!(sc > victim.score)) {
-                    ok = false;
+                    ok = false;  // strict win required (index.cpp:25)
                 } else {
                     e[victim.pos].x = victim.key | TOMB;
                     cnt -= 1;
@@ -101,41 +118,71 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
                 const uint32_t pos = nu;
                 nu += 1;
                 if (!full) sd.live[t] = live + 1;
-                // keep low buffer = the cnt lowest live entries
+                sd.n_used[t] = nu;
+                // does the new entry belong among the cnt lowest live entries?
                 bool ins;
                 if (cnt == 0)
-                    ins = complete;  // empty: only a complete buffer may take it
+                    ins = complete;  // an empty, incomplete buffer is refilled instead
                 else if (complete && cnt < static_cast<uint32_t>(LOW_Q))
                     ins = true;
                 else
                     ins = ev_before(sc, N, lo[0].score, lo[0].key);
                 if (ins) {
-                    // descending eviction order: skip entries evicted after new
-                    uint32_t p = 0;
-                    while (p < cnt && !ev_before(lo[p].score, lo[p].key, sc, N)) ++p;
-                    const bool drop_first = cnt == static_cast<uint32_t>(LOW_Q);
-                    if (drop_first) {
-                        // drop lo[0] (the largest), insert at p-1
-                        for (uint32_t x = 0; x + 1 < p; ++x) lo[x] = lo[x + 1];
-                        LowEnt le{sc, N, pos, 0};
-                        lo[p - 1] = le;
-                    } else {
-                        for (uint32_t x = cnt; x > p; --x) lo[x] = lo[x - 1];
-                        LowEnt le{sc, N, pos, 0};
-                        lo[p] = le;
-                        cnt += 1;
-                    }
+                    const uint32_t k = atomicAdd(&S.nbuf, 1u);
+                    S.buflist[k] = t;
+                    S.bufent[k] = BufEnt{sc, pos, cnt};
+                } else {
+                    sd.low_cnt[t] = cnt;
+                    if (cnt == 0 || nu == sd.cap2) S.reflist[atomicAdd(&S.nref, 1u)] = t;
                 }
-                sd.n_used[t] = nu;
-                sd.low_cnt[t] = cnt;
-                if (cnt == 0 || nu == sd.cap2) S.reflist[atomicAdd(&S.nref, 1u)] = t;
             }
         }
         mask[t] = static_cast<uint8_t>(applied);
         if (applied) atomicAdd(&S.applied, 1u);
     }
     __syncthreads();
+    // ---- B: warp-cooperative low-buffer insertion ----
+    const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    for (uint32_t k = wid; k < S.nbuf; k += INS_WARPS) {
+        const uint32_t t = S.buflist[k];
+        const BufEnt be = S.bufent[k];
+        const LowEnt ne{be.score, N, be.pos, 0};
+        const uint32_t cnt = be.cnt;
+        LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
+        LowEnt v[LQ_PER_LANE];
+        uint32_t after = 0;  // entries evicted after the new one precede it
+#pragma unroll
+        for (int i = 0; i < LQ_PER_LANE; ++i) {
+            const uint32_t e = i * 32 + ln;
+            if (e < cnt) {
+                v[i] = lo[e];
+                after += ev_before(v[i].score, v[i].key, ne.score, ne.key) ? 0u : 1u;
+            }
+        }
+        for (int o = 16; o; o >>= 1) after += __shfl_xor_sync(0xffffffffu, after, o);
+        const uint32_t p = after;  // sorted buffer: entries [0, p) go before new
+        const bool drop_first = cnt == static_cast<uint32_t>(LOW_Q);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < LQ_PER_LANE; ++i) {
+            const uint32_t e = i * 32 + ln;
+            if (e >= cnt) continue;
+            if (drop_first) {
+                if (e >= 1 && e < p) lo[e - 1] = v[i];  // drop lo[0], shift down
+            } else {
+                if (e >= p) lo[e + 1] = v[i];  // shift up
+            }
+        }
+        if (ln == 0) {
+            lo[drop_first ? p - 1 : p] = ne;
+            const uint32_t nc = drop_first ? cnt : cnt + 1;
+            sd.low_cnt[t] = nc;
+            if (sd.n_used[t] == sd.cap2) S.reflist[atomicAdd(&S.nref, 1u)] = t;
+        }
+    }
+    __syncthreads();
     if (threadIdx.x == 0) P.rep[0] = S.applied;
+    // ---- C: compaction + refill ----
     const uint32_t last_blk = N >> KEY_BLOCK_SHIFT;  // block of the newest key
     for (uint32_t r = 0; r < S.nref; ++r) refill_table(S.r, sd, S.reflist[r], last_blk);
 }

@@ -9,10 +9,14 @@
 
 namespace csa {
 
-// select.cu: route + gather + top-K, one cluster per problem
+// route.cu: centroid routing + per-rank gather plan, one CTA per problem
+cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob, uint32_t cs,
+                         uint32_t kpc, cudaStream_t st);
+
+// select.cu: gather + top-K, one cluster per problem
 size_t select_smem_bytes(uint32_t kpc);
-cudaError_t launch_select(const DecodeProblem* probs, uint32_t nprob, uint32_t kpc, uint32_t cs,
-                          cudaStream_t st);
+cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                          uint32_t kpc, uint32_t cs, cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
 constexpr uint32_t ATT_ROWS = 128;

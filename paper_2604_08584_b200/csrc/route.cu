@@ -1,0 +1,169 @@
+// route.cu — CSAttention decode, part 0: centroid routing (select_centroids,
+// retrieval.cpp:40-87) + gather planning, one CTA per (session, query head).
+//
+// Per subspace b: normalize the query slice (fp64 sum of squares, f32 store,
+// l2_normalize core.cpp:109-116), m*C sequential-fp64 centroid dots, argmax
+// with strict > (lower j wins) or the top-tau backoff below the threshold.
+// The gathered lists (b-major, selection order — gather_lists :95-109) and,
+// for every cluster rank of the select kernel, each list's [beg, end) entry
+// range over that rank's key range (from the key-block offsets) are written
+// to a per-problem plan, so select.cu starts streaming after one load.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace csa {
+
+constexpr int RT_THREADS = 256;
+constexpr int RT_WARPS = RT_THREADS / 32;
+
+__global__ void __launch_bounds__(RT_THREADS)
+route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ plans, uint32_t cs,
+             uint32_t kpc) {
+    __shared__ float q[DMAX], qn[DMAX];
+    __shared__ double csc[MAX_TABLES];
+    __shared__ uint32_t ids[MAXM * MAXTAU], nids[MAXM], zero_mask;
+    __shared__ uint32_t lists[MAXL], lsub[MAXL], nl;
+    const DecodeProblem& P = probs[blockIdx.x];
+    if (!(P.mode & MODE_SEARCH)) return;
+    const SessionDev& sd = *P.s;
+    const uint32_t m = sd.m, C = sd.C, d = sd.d, tid = threadIdx.x, N = P.N;
+    RoutePlan& plan = plans[blockIdx.x];
+    DecodeReport* Rp = reinterpret_cast<DecodeReport*>(P.rep);
+    for (uint32_t t = tid; t < d; t += blockDim.x) q[t] = P.q[t];
+    if (tid == 0) zero_mask = 0;
+    __syncthreads();
+    if (tid < m) {
+        const uint32_t off = sd.offs[tid], w = sd.widths[tid];
+        double n2 = 0.0;
+        for (uint32_t t = 0; t < w; ++t) {
+            const double x = q[off + t];
+            n2 = __fma_rn(x, x, n2);  // x*x is exact in fp64
+        }
+        if (n2 == 0.0) {
+            atomicOr(&zero_mask, 1u << tid);
+        } else {
+            const double inv = 1.0 / sqrt(n2);
+            for (uint32_t t = 0; t < w; ++t)
+                qn[off + t] = __double2float_rn(__dmul_rn(static_cast<double>(q[off + t]), inv));
+        }
+    }
+    __syncthreads();
+    for (uint32_t x = tid; x < m * C; x += blockDim.x) {
+        const uint32_t b = x / C, j = x - b * C;
+        if (zero_mask & (1u << b)) continue;
+        const uint32_t off = sd.offs[b], w = sd.widths[b];
+        const float* c = sd.cent + static_cast<size_t>(C) * off + static_cast<size_t>(j) * w;
+        double acc = 0.0;
+        for (uint32_t t = 0; t < w; ++t) acc = __fma_rn((double)qn[off + t], (double)__ldg(c + t), acc);
+        csc[x] = acc;
+    }
+    __syncthreads();
+    const int wid = tid >> 5, ln = tid & 31;
+    for (uint32_t b = wid; b < m; b += RT_WARPS) {
+        if (zero_mask & (1u << b)) {  // degenerate slice: centroid 0, no backoff
+            if (ln == 0) {
+                ids[b * MAXTAU] = 0;
+                nids[b] = 1;
+                Rp->best_cos[b] = 1.0;
+            }
+            continue;
+        }
+        const double* sc = csc + b * C;
+        const uint32_t take = sd.tau < C ? sd.tau : C;
+        for (uint32_t r = 0; r < take; ++r) {
+            double bv = -DBL_MAX;
+            uint32_t bj = 0xffffffffu;
+            for (uint32_t j = ln; j < C; j += 32) {
+                bool used = false;
+                for (uint32_t u = 0; u < r; ++u) used |= (ids[b * MAXTAU + u] == j);
+                if (used) continue;
+                const double v = sc[j];
+                if (bj == 0xffffffffu || v > bv) {
+                    bv = v;
+                    bj = j;
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                if (oj != 0xffffffffu && (bj == 0xffffffffu || ov > bv || (ov == bv && oj < bj))) {
+                    bv = ov;
+                    bj = oj;
+                }
+            }
+            if (ln == 0) ids[b * MAXTAU + r] = bj;
+            __syncwarp();
+            if (r == 0) {
+                if (ln == 0) Rp->best_cos[b] = bv;
+                if (bv >= sd.threshold) {
+                    if (ln == 0) nids[b] = 1;
+                    break;
+                }
+            }
+            if (ln == 0) nids[b] = r + 1;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t n = 0;
+        unsigned long long dots = 0;
+        for (uint32_t b = 0; b < m; ++b) {
+            if (!(zero_mask & (1u << b))) dots += static_cast<unsigned long long>(C) * sd.widths[b];
+            for (uint32_t r = 0; r < nids[b]; ++r) {
+                lists[n] = b * C + ids[b * MAXTAU + r];
+                lsub[n] = b;
+                ++n;
+            }
+        }
+        nl = n;
+        plan.nl = n;
+        Rp->nl = n;
+        Rp->dot_ops_lo = static_cast<uint32_t>(dots);
+        Rp->dot_ops_hi = static_cast<uint32_t>(dots >> 32);
+    }
+    __syncthreads();
+    if (tid < nl) {
+        plan.lists[tid] = lists[tid];
+        plan.lsub[tid] = lsub[tid];
+        Rp->lists[tid] = lists[tid];
+    }
+    // per-rank entry ranges: [blk_off(kb0), blk_off(kb1) or n_used)
+    const uint32_t last_blk = (N - 1) >> KEY_BLOCK_SHIFT;
+    for (uint32_t x = tid; x < cs * nl; x += blockDim.x) {
+        const uint32_t r = x / nl, l = x - r * nl;
+        const uint32_t k0 = r * kpc, k1 = min(N, k0 + kpc);
+        uint2 be = make_uint2(0, 0);
+        if (k1 > k0) {
+            const uint32_t t = lists[l];
+            const uint32_t* bo = sd.blk_off + static_cast<size_t>(t) * sd.nb_stride;
+            const uint32_t kb0 = k0 >> KEY_BLOCK_SHIFT;
+            const uint32_t kb1 = (k1 + KEY_BLOCK - 1) >> KEY_BLOCK_SHIFT;
+            be.x = __ldcg(bo + kb0);
+            be.y = kb1 <= last_blk ? __ldcg(bo + kb1) : __ldcg(sd.n_used + t);
+        }
+        plan.bounds[r * MAXL + l] = be;
+    }
+    if (wid == 0) {  // gathered_entries (CostCounters): live lengths of the lists
+        uint32_t g = 0;
+        for (uint32_t l = ln; l < nl; l += 32) g += __ldcg(sd.live + lists[l]);
+        for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+        if (ln == 0) {
+            Rp->gathered_lo = g;
+            Rp->gathered_hi = 0;
+        }
+    }
+}
+
+cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob, uint32_t cs,
+                         uint32_t kpc, cudaStream_t st) {
+    route_kernel<<<nprob, RT_THREADS, 0, st>>>(probs, plans, cs, kpc);
+    return cudaGetLastError();
+}
+
+}  // namespace csa

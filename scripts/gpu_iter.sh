@@ -1,0 +1,8 @@
+# one optimisation iteration: parity suite, phase breakdown, benches (c2, c3)
+timeout 700 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 240 -rf > gpurun_out/gpu_tests.log 2>&1
+tail -3 gpurun_out/gpu_tests.log
+CSATTN_PHASE_PROF=1 timeout 900 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/phase_c3.json 2> gpurun_out/phase_c3.err
+grep csattn gpurun_out/phase_c3.err
+timeout 600 python bench.py --config c2 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+tail -n 2 gpurun_out/bench_c2.err gpurun_out/bench_c3.err
