@@ -76,6 +76,7 @@ __device__ __forceinline__ unsigned long long sel_key(float s, uint32_t i) {
 
 struct BuildSmem {
     RefillSmem r;
+    float rmin[BL_THREADS / 32], rmax[BL_THREADS / 32];
 };
 
 __global__ void __launch_bounds__(BL_THREADS)
@@ -90,6 +91,7 @@ build_lists_kernel(const SessionDev* __restrict__ sp, const float* __restrict__ 
         thr = cta_kth_largest(S.r, P, keep, [&](uint32_t i) { return sel_key(sc[i], i); });
     uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
     uint32_t out = 0;
+    float smin = INFINITY, smax = -INFINITY;  // live score bounds (SessionDev::tmm)
     for (uint32_t c0 = 0; c0 < P; c0 += blockDim.x) {
         const uint32_t i = c0 + threadIdx.x;
         float s = 0.0f;
@@ -100,12 +102,30 @@ build_lists_kernel(const SessionDev* __restrict__ sp, const float* __restrict__ 
         }
         uint32_t tot;
         const uint32_t ex = tbl_block_excl_scan(S.r, keepi, tot);
-        if (keepi) e[out + ex] = make_uint2(i, __float_as_uint(s));
+        if (keepi) {
+            e[out + ex] = make_uint2(i, __float_as_uint(s));
+            smin = fminf(smin, s);
+            smax = fmaxf(smax, s);
+        }
         out += tot;
     }
+    for (int o = 16; o; o >>= 1) {
+        smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+        smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        S.rmin[threadIdx.x >> 5] = smin;
+        S.rmax[threadIdx.x >> 5] = smax;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
+        for (int i = 0; i < BL_THREADS / 32; ++i) {
+            smin = fminf(smin, S.rmin[i]);
+            smax = fmaxf(smax, S.rmax[i]);
+        }
         sd.n_used[t] = out;
         sd.live[t] = out;
+        sd.tmm[t] = make_float2(smin, smax);
     }
     __syncthreads();
     refill_table(S.r, sd, t, (P - 1) >> KEY_BLOCK_SHIFT);

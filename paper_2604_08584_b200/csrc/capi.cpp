@@ -147,11 +147,15 @@ struct csattn_ctx_s {
     std::vector<std::array<cudaEvent_t, 4>> ev_steps;  // select | attend | insert
     DevMem part, counters;  // attention partials + per-problem merge counters
     DevMem plans;           // route.cu -> select.cu routing plans
+    DevMem log_idx, log_sc; // select.cu candidate logs: log_rows x log_cap
+    uint64_t log_cap = 0, log_rows = 0;
+    int num_sms = 148;
     uint64_t counters_n = 0;
     // select-kernel phase timestamps (env CSATTN_PHASE_PROF=1; diagnostics only)
     bool phase_prof = std::getenv("CSATTN_PHASE_PROF") != nullptr;
     DevMem phase;
     double phase_sum[6] = {0, 0, 0, 0, 0, 0};
+    double phase_dbg[3] = {0, 0, 0};
     uint64_t phase_n = 0;
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t take_event() {
@@ -171,8 +175,8 @@ struct csattn_session_s {
     csa::SessionDev h{};
     DevMem dev;
     std::shared_ptr<SharedRows> pre;
-    DevMem ktail, vtail, cent, ent, n_used, live, blk_off, low, low_cnt, refill;
-    DevMem cache, sel, drep, irep;
+    DevMem ktail, vtail, cent, ent, n_used, live, blk_off, low, low_cnt, refill, tmm;
+    DevMem cache, cbounds, sel, drep, irep;
     uint64_t group = 1, N = 0, step = 0, max_steps = 0;
     double alpha = 0.0;
     int32_t score_bits = 32;
@@ -185,7 +189,7 @@ struct csattn_session_s {
     uint64_t T() const { return static_cast<uint64_t>(h.m) * h.C; }
     size_t device_bytes() const {
         return ktail.n + vtail.n + cent.n + ent.n + n_used.n + live.n + blk_off.n + low.n +
-               low_cnt.n + refill.n + cache.n + sel.n + drep.n + irep.n +
+               low_cnt.n + refill.n + tmm.n + cache.n + cbounds.n + sel.n + drep.n + irep.n +
                (pre ? pre->k.n + pre->v.n : 0);
     }
 };
@@ -310,8 +314,10 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     s->low.alloc(T * csa::LOW_Q * sizeof(csa::LowEnt));
     s->low_cnt.alloc(T * 4);
     s->refill.alloc(T * 4);
+    s->tmm.alloc(T * sizeof(float2));
     s->sel.alloc(group * (p + max_steps) * 4);
     if (rc->search_period > 1) s->cache.alloc(group * (p + max_steps) * sizeof(double));
+    s->cbounds.alloc(group * 2 * sizeof(double));
     s->drep.alloc(group * sizeof(csa::DecodeReport));
     s->irep.alloc(4 + ((T + 15) & ~15ull));
     s->dev.alloc(sizeof(csa::SessionDev));
@@ -325,6 +331,7 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     h.low = s->low.as<csa::LowEnt>();
     h.low_cnt = s->low_cnt.as<uint32_t>();
     h.refill = s->refill.as<uint32_t>();
+    h.tmm = s->tmm.as<float2>();
     s->hs.assign(group, HeadState{});
     return s;
 }
@@ -376,22 +383,6 @@ void check_rows(const float* keys, const float* values, uint64_t p, uint64_t d, 
     }
 }
 
-// choose cluster size and keys per CTA for a context of n keys
-void cluster_shape(uint64_t n, uint64_t mc, uint32_t& cs, uint32_t& kpc) {
-    uint64_t c = (n + 4095) / 4096;
-    if (c < 1) c = 1;
-    if (c > 16) c = 16;
-    uint64_t k = (n + c - 1) / c;
-    k = (k + csa::KEY_BLOCK - 1) / csa::KEY_BLOCK * csa::KEY_BLOCK;
-    if (k < mc) k = (mc + csa::KEY_BLOCK - 1) / csa::KEY_BLOCK * csa::KEY_BLOCK;
-    if (k > 16384)
-        fail(CSATTN_ERR_CAPACITY,
-             "context of " + std::to_string(n) +
-                 " keys exceeds one GPU's decode cluster (262144); shard the sequence");
-    cs = static_cast<uint32_t>(c);
-    kpc = static_cast<uint32_t>(k);
-}
-
 struct Outs {
     float* out;
     uint32_t* sel;
@@ -406,7 +397,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const bool host = flags & CSATTN_HOST_BUFFERS;
     if (ns == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
     const uint32_t d = ss[0]->h.d;
-    uint64_t nq = 0, maxN = 0, maxmc = 0, maxK = 0;
+    uint64_t nq = 0, maxN = 0, maxK = 0;
     std::vector<uint64_t> Ks;
     for (uint64_t i = 0; i < ns; ++i) {
         csattn_session s = ss[i];
@@ -423,9 +414,6 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
         nq += s->group;
         maxN = std::max<uint64_t>(maxN, s->N);
-        // the score array doubles as routing scratch: m*C fp64 dots + C*d centroids
-        const uint64_t mc = static_cast<uint64_t>(s->h.m) * s->h.C;
-        maxmc = std::max<uint64_t>(maxmc, 0 * mc);  // scores only (routing is route.cu)
     }
     if ((selected || weights) && sel_stride < maxK)
         fail(CSATTN_ERR_PARAMETER, "selected/weights stride " + std::to_string(sel_stride) +
@@ -434,8 +422,11 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         require_finite(keys, ns * d, "appended key");
         require_finite(values, ns * d, "appended value");
     }
-    uint32_t cs, kpc;
-    cluster_shape(maxN, maxmc, cs, kpc);
+    if (maxN > csa::SELECT_MAX_CONTEXT)
+        fail(CSATTN_ERR_CAPACITY, "context of " + std::to_string(maxN) +
+                                      " keys exceeds one GPU's decode search (" +
+                                      std::to_string(csa::SELECT_MAX_CONTEXT) +
+                                      "); shard the sequence");
 
     // device views of inputs / outputs
     const float *dq = q, *dk = keys, *dv = values;
@@ -468,8 +459,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     ctx->hprobs.resize(nq);
     if (ctx->phase_prof) {
-        ctx->phase.ensure(nq * 16 * 8 * sizeof(unsigned long long));
-        ck(cudaMemsetAsync(ctx->phase.p, 0, nq * 16 * 8 * 8, ctx->stream), "memset");
+        ctx->phase.ensure(nq * 8 * sizeof(unsigned long long));
+        ck(cudaMemsetAsync(ctx->phase.p, 0, nq * 8 * 8, ctx->stream), "memset");
     }
     ctx->hiprobs.resize(ns);
     uint64_t qi = 0;
@@ -495,7 +486,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             P.mode = (srch ? csa::MODE_SEARCH : 0u) |
                      ((srch && P.cache) ? csa::MODE_STORE_CACHE : 0u) |
                      (dw ? csa::MODE_WEIGHTS : 0u);
-            P.prof = ctx->phase_prof ? ctx->phase.as<unsigned long long>() + qi * 16 * 8 : nullptr;
+            P.cbounds = s->cbounds.as<double>() + h * 2;
+            P.prof = ctx->phase_prof ? ctx->phase.as<unsigned long long>() + qi * 8 : nullptr;
         }
         csa::InsertProblem& I = ctx->hiprobs[i];
         I.s = s->dev.as<csa::SessionDev>();
@@ -556,11 +548,23 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaEventRecord(ev[0], ctx->stream), "event");
     }
     ctx->plans.ensure(nq * sizeof(csa::RoutePlan));
-    ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), cs,
-                         kpc, ctx->stream),
+    ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
+                         ctx->stream),
        "route launch");
-    ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), kpc,
-                          cs, ctx->stream),
+    const uint32_t sgrid = csa::select_grid(static_cast<uint32_t>(nq), ctx->num_sms);
+    if (maxN > ctx->log_cap || sgrid > ctx->log_rows) {
+        // sized for the sessions' full capacity, so it is not re-grown every step
+        uint64_t cap = maxN;
+        for (uint64_t i = 0; i < ns; ++i) cap = std::max<uint64_t>(cap, ss[i]->h.max_ctx);
+        cap = (cap + csa::SELECT_LOG_ALIGN - 1) / csa::SELECT_LOG_ALIGN * csa::SELECT_LOG_ALIGN;
+        ctx->log_cap = std::max<uint64_t>(cap, ctx->log_cap);
+        ctx->log_rows = std::max<uint64_t>(sgrid, ctx->log_rows);
+        ctx->log_idx.alloc(ctx->log_rows * ctx->log_cap * 4);
+        ctx->log_sc.alloc(ctx->log_rows * ctx->log_cap * 8);
+    }
+    ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
+                          ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
+                          static_cast<uint32_t>(ctx->log_cap), ctx->stream),
        "select launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
@@ -576,22 +580,35 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     ctx->launches += 4;
     if (ctx->phase_prof) {
-        // mean per-CTA duration of each select phase (route, issue, consume,
-        // keys, select, emit); prints at context teardown
-        std::vector<unsigned long long> ph(nq * 16 * 8);
+        // per problem: streaming (gather + log) and final-selection time,
+        // logged candidates, threshold-bin size; printed at context teardown
+        std::vector<unsigned long long> ph(nq * 8);
         ck(cudaMemcpyAsync(ph.data(), ctx->phase.p, ph.size() * 8, cudaMemcpyDeviceToHost,
                            ctx->stream), "phase copy");
         ck(cudaStreamSynchronize(ctx->stream), "phase sync");
         double sum[6] = {0, 0, 0, 0, 0, 0};
         uint64_t n = 0;
-        for (uint64_t i = 0; i < nq * 16; ++i) {
+        for (uint64_t i = 0; i < nq; ++i) {
             const unsigned long long* t = &ph[i * 8];
-            if (!t[0] || !t[6]) continue;
-            for (int k = 0; k < 6; ++k) sum[k] += (t[k + 1] && t[k]) ? double(t[k + 1] - t[k]) : 0.0;
+            if (!t[0] || !t[2]) continue;
+            sum[0] += double(t[1] - t[0]);
+            sum[1] += double(t[2] - t[1]);
+            sum[2] += double(t[3]);
+            sum[3] += double(t[4]);
+            sum[4] = std::max(sum[4], double(t[4]));
             ++n;
         }
+        if (nq) {
+            double lo, hi;
+            std::memcpy(&lo, &ph[5], 8);
+            std::memcpy(&hi, &ph[6], 8);
+            ctx->phase_dbg[0] = lo;
+            ctx->phase_dbg[1] = hi;
+            ctx->phase_dbg[2] = static_cast<double>(ph[7]);
+        }
         if (n) {
-            for (int k = 0; k < 6; ++k) ctx->phase_sum[k] += sum[k] / n;
+            for (int k = 0; k < 4; ++k) ctx->phase_sum[k] += sum[k] / n;
+            ctx->phase_sum[4] = std::max(ctx->phase_sum[4], sum[4]);
             ctx->phase_n += 1;
         }
     }
@@ -678,6 +695,7 @@ void import_tables(csattn_session_s* s, const uint32_t* lens, const uint32_t* in
     std::vector<uint2> ent(T * cap2, make_uint2(0, 0));
     std::vector<uint32_t> nused(T), live(T), bo(T * nb, 0), lcnt(T);
     std::vector<csa::LowEnt> low(T * csa::LOW_Q);
+    std::vector<float2> tmm(T, make_float2(0.0f, 0.0f));
     std::vector<uint32_t> order;
     for (uint64_t t = 0; t < T; ++t) {
         const uint32_t n = lens[t];
@@ -695,7 +713,10 @@ void import_tables(csattn_session_s* s, const uint32_t* lens, const uint32_t* in
         std::vector<uint32_t> pos_of(n);
         for (uint32_t p = 0; p < n; ++p) {
             ent[t * cap2 + p] = make_uint2(ix[order[p]], 0);
-            std::memcpy(&ent[t * cap2 + p].y, &sc[order[p]], 4);
+            // -0.0f -> +0.0f: equal in every comparison, and select.cu uses
+            // -0.0 as its "not gathered" marker
+            const float f = sc[order[p]] == 0.0f ? 0.0f : sc[order[p]];
+            std::memcpy(&ent[t * cap2 + p].y, &f, 4);
             pos_of[order[p]] = p;
         }
         nused[t] = n;
@@ -715,6 +736,10 @@ void import_tables(csattn_session_s* s, const uint32_t* lens, const uint32_t* in
             low[t * csa::LOW_Q + r] = le;
         }
         lcnt[t] = q;
+        for (uint32_t r = 0; r < n; ++r) {
+            tmm[t].x = r ? std::min(tmm[t].x, sc[r]) : sc[r];
+            tmm[t].y = r ? std::max(tmm[t].y, sc[r]) : sc[r];
+        }
     }
     cudaStream_t st = s->ctx->stream;
     ck(cudaMemcpyAsync(s->ent.p, ent.data(), ent.size() * sizeof(uint2), cudaMemcpyHostToDevice, st), "import");
@@ -723,6 +748,7 @@ void import_tables(csattn_session_s* s, const uint32_t* lens, const uint32_t* in
     ck(cudaMemcpyAsync(s->blk_off.p, bo.data(), bo.size() * 4, cudaMemcpyHostToDevice, st), "import");
     ck(cudaMemcpyAsync(s->low.p, low.data(), low.size() * sizeof(csa::LowEnt), cudaMemcpyHostToDevice, st), "import");
     ck(cudaMemcpyAsync(s->low_cnt.p, lcnt.data(), T * 4, cudaMemcpyHostToDevice, st), "import");
+    ck(cudaMemcpyAsync(s->tmm.p, tmm.data(), T * sizeof(float2), cudaMemcpyHostToDevice, st), "import");
     ck(cudaStreamSynchronize(st), "import");
 }
 
@@ -847,6 +873,7 @@ csattn_status csattn_ctx_create(int device, void* stream, csattn_ctx* out) {
                                       std::to_string(major) + std::to_string(minor));
         auto c = std::make_unique<csattn_ctx_s>();
         c->device = device;
+        ck(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
         if (stream) {
             c->stream = static_cast<cudaStream_t>(stream);
         } else {
@@ -864,12 +891,15 @@ csattn_status csattn_ctx_create(int device, void* stream, csattn_ctx* out) {
 static void ctx_release(csattn_ctx ctx) {
     if (--ctx->refs > 0) return;
     if (ctx->phase_n) {
-        const char* nm[6] = {"route", "issue", "consume", "keys", "select", "emit"};
-        std::fprintf(stderr, "[csattn] select phases (mean per CTA over %llu steps, us):",
-                     static_cast<unsigned long long>(ctx->phase_n));
-        for (int k = 0; k < 6; ++k)
-            std::fprintf(stderr, " %s=%.2f", nm[k], ctx->phase_sum[k] / ctx->phase_n / 1e3);
-        std::fprintf(stderr, "\n");
+        const double n = static_cast<double>(ctx->phase_n);
+        std::fprintf(stderr,
+                     "[csattn] select per problem (mean over %llu steps): stream=%.2fus "
+                     "final=%.2fus logged=%.0f bin_members=%.1f (max %.0f)\n",
+                     static_cast<unsigned long long>(ctx->phase_n), ctx->phase_sum[0] / n / 1e3,
+                     ctx->phase_sum[1] / n / 1e3, ctx->phase_sum[2] / n, ctx->phase_sum[3] / n,
+                     ctx->phase_sum[4]);
+        std::fprintf(stderr, "[csattn] problem 0 of the last step: bounds [%g, %g] take_all|bin<<1=%g\n",
+                     ctx->phase_dbg[0], ctx->phase_dbg[1], ctx->phase_dbg[2]);
     }
     cudaStreamSynchronize(ctx->stream);
     for (auto& ev : ctx->ev_steps)
@@ -1171,6 +1201,8 @@ csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn
            "fork blk_off");
         d2d(s->low, src->low, T * csa::LOW_Q * sizeof(csa::LowEnt));
         d2d(s->low_cnt, src->low_cnt, T * 4);
+        d2d(s->tmm, src->tmm, T * sizeof(float2));
+        d2d(s->cbounds, src->cbounds, s->group * 2 * sizeof(double));
         if (s->cache.p && src->cache.p)
             for (uint64_t h = 0; h < s->group; ++h)
                 ck(cudaMemcpyAsync(s->cache.as<double>() + h * s->h.max_ctx,

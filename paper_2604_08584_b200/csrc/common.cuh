@@ -12,6 +12,9 @@
 //                               (score asc, key desc) = the TopList tail
 //                               reversed; eviction pops low[t][0]
 //   live[t]                     live entries (= TopList::indices.size())
+//   tmm[t]                      (lower bound, upper bound) of the live scores:
+//                               the min at build time (evictions only raise
+//                               the min) and the running max (inserts raise it)
 // A list holds at most L live entries plus LOW_Q tombstones: when the low
 // buffer runs dry the list is compacted and the buffer refilled.
 #pragma once
@@ -65,6 +68,7 @@ struct SessionDev {
     LowEnt* low;        // [T][LOW_Q]
     uint32_t* low_cnt;  // [T]
     uint32_t* refill;   // [T] scratch flags for the insert kernel
+    float2* tmm;        // [T] live score bounds (min lower bound, max)
 };
 
 // Per-(session, query head) decode-step descriptor.
@@ -75,6 +79,7 @@ struct DecodeProblem {
     float* weights;    // K floats (nullable)
     uint32_t* sel;     // K entries (scratch or caller buffer)
     double* cache;     // candidate-score cache for search_period > 1 (nullable)
+    double* cbounds;   // score bounds of the cached search (2 doubles, with cache)
     uint32_t* rep;     // DecodeReport (device)
     uint32_t N;        // context this step attends to (pre-append)
     uint32_t K;        // selected-set size
@@ -97,14 +102,15 @@ struct DecodeReport {
     uint32_t lists[MAXL];        // table ids gathered, in order
 };
 
-// Routing result + gather plan of one problem (route.cu -> select.cu).
-constexpr int MAX_CLUSTER = 16;
+// Routing result of one problem (route.cu -> select.cu): the gathered lists
+// and bounds [lo, hi] on every accumulated candidate score (from the lists'
+// score bounds), which fix the selection histogram before the gather starts.
 struct RoutePlan {
     uint32_t nl;
     uint32_t pad[3];
+    double lo, hi;
     uint32_t lists[MAXL];               // table ids, gathered order
     uint32_t lsub[MAXL];                // their subspaces
-    uint2 bounds[MAX_CLUSTER * MAXL];   // [rank][list]: entry range [x, y)
 };
 
 // Per-session append + insert descriptor.

@@ -115,6 +115,12 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
             if (ok) {
                 applied = 1;
                 e[nu] = make_uint2(N, __float_as_uint(sc));
+                {  // live score bounds (evictions only raise the min: kept as a bound)
+                    float2 mm = sd.tmm[t];
+                    mm = live == 0 ? make_float2(sc, sc)
+                                   : make_float2(fminf(mm.x, sc), fmaxf(mm.y, sc));
+                    sd.tmm[t] = mm;
+                }
                 const uint32_t pos = nu;
                 nu += 1;
                 if (!full) sd.live[t] = live + 1;

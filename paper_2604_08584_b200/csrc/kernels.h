@@ -9,14 +9,18 @@
 
 namespace csa {
 
-// route.cu: centroid routing + per-rank gather plan, one CTA per problem
-cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob, uint32_t cs,
-                         uint32_t kpc, cudaStream_t st);
+// route.cu: centroid routing + score bounds, one CTA per problem
+cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob,
+                         cudaStream_t st);
 
-// select.cu: gather + top-K, one cluster per problem
-size_t select_smem_bytes(uint32_t kpc);
+// select.cu: streaming gather + top-K, persistent (one CTA per SM, problems
+// strided over the grid). log_idx/log_sc: grid x log_cap candidate-log slots.
+constexpr uint32_t SELECT_MAX_CONTEXT = 8192u * 32u;  // bitmap aliases the tile accumulator
+constexpr uint32_t SELECT_LOG_ALIGN = 8192u;           // log_cap multiple (per-warp regions)
+uint32_t select_grid(uint32_t nprob, int num_sms);
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
-                          uint32_t kpc, uint32_t cs, cudaStream_t st);
+                          uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
+                          cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
 constexpr uint32_t ATT_ROWS = 128;

@@ -4,10 +4,9 @@
 // Per subspace b: normalize the query slice (fp64 sum of squares, f32 store,
 // l2_normalize core.cpp:109-116), m*C sequential-fp64 centroid dots, argmax
 // with strict > (lower j wins) or the top-tau backoff below the threshold.
-// The gathered lists (b-major, selection order — gather_lists :95-109) and,
-// for every cluster rank of the select kernel, each list's [beg, end) entry
-// range over that rank's key range (from the key-block offsets) are written
-// to a per-problem plan, so select.cu starts streaming after one load.
+// The gathered lists (b-major, selection order — gather_lists :95-109) and
+// bounds on the accumulated scores are written to a per-problem plan that
+// select.cu streams from.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -22,8 +21,7 @@ constexpr int RT_THREADS = 256;
 constexpr int RT_WARPS = RT_THREADS / 32;
 
 __global__ void __launch_bounds__(RT_THREADS)
-route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ plans, uint32_t cs,
-             uint32_t kpc) {
+route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ plans) {
     __shared__ float q[DMAX], qn[DMAX];
     __shared__ double csc[MAX_TABLES];
     __shared__ uint32_t ids[MAXM * MAXTAU], nids[MAXM], zero_mask;
@@ -31,7 +29,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     const DecodeProblem& P = probs[blockIdx.x];
     if (!(P.mode & MODE_SEARCH)) return;
     const SessionDev& sd = *P.s;
-    const uint32_t m = sd.m, C = sd.C, d = sd.d, tid = threadIdx.x, N = P.N;
+    const uint32_t m = sd.m, C = sd.C, d = sd.d, tid = threadIdx.x;
     RoutePlan& plan = plans[blockIdx.x];
     DecodeReport* Rp = reinterpret_cast<DecodeReport*>(P.rep);
     for (uint32_t t = tid; t < d; t += blockDim.x) q[t] = P.q[t];
@@ -133,21 +131,32 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
         plan.lsub[tid] = lsub[tid];
         Rp->lists[tid] = lists[tid];
     }
-    // per-rank entry ranges: [blk_off(kb0), blk_off(kb1) or n_used)
-    const uint32_t last_blk = (N - 1) >> KEY_BLOCK_SHIFT;
-    for (uint32_t x = tid; x < cs * nl; x += blockDim.x) {
-        const uint32_t r = x / nl, l = x - r * nl;
-        const uint32_t k0 = r * kpc, k1 = min(N, k0 + kpc);
-        uint2 be = make_uint2(0, 0);
-        if (k1 > k0) {
+    // bounds on every accumulated score: a pool key's score is a sum of
+    // w_l * score over a non-empty subset of the gathered lists, each score in
+    // [tmin_l, tmax_l] (the lists' live score bounds)
+    if (tid == 0) {
+        double neg = 0.0, pos = 0.0, amin = DBL_MAX, bmax = -DBL_MAX;
+        bool any = false, any_neg = false, any_pos = false;
+        for (uint32_t l = 0; l < nl; ++l) {
             const uint32_t t = lists[l];
-            const uint32_t* bo = sd.blk_off + static_cast<size_t>(t) * sd.nb_stride;
-            const uint32_t kb0 = k0 >> KEY_BLOCK_SHIFT;
-            const uint32_t kb1 = (k1 + KEY_BLOCK - 1) >> KEY_BLOCK_SHIFT;
-            be.x = __ldcg(bo + kb0);
-            be.y = kb1 <= last_blk ? __ldcg(bo + kb1) : __ldcg(sd.n_used + t);
+            if (__ldcg(sd.live + t) == 0) continue;
+            const float2 mm = __ldcg(sd.tmm + t);
+            const double w = sd.weights[lsub[l]];
+            const double a = w * static_cast<double>(mm.x), b = w * static_cast<double>(mm.y);
+            any = true;
+            if (a < 0.0) { neg += a; any_neg = true; }
+            if (b > 0.0) { pos += b; any_pos = true; }
+            amin = fmin(amin, a);
+            bmax = fmax(bmax, b);
         }
-        plan.bounds[r * MAXL + l] = be;
+        double lo = any ? (any_neg ? neg : amin) : 0.0;
+        double hi = any ? (any_pos ? pos : bmax) : 0.0;
+        if (!sd.passthrough) {  // window keys compete at score 0 when absent
+            lo = fmin(lo, 0.0);
+            hi = fmax(hi, 0.0);
+        }
+        plan.lo = lo;
+        plan.hi = hi;
     }
     if (wid == 0) {  // gathered_entries (CostCounters): live lengths of the lists
         uint32_t g = 0;
@@ -160,9 +169,9 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     }
 }
 
-cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob, uint32_t cs,
-                         uint32_t kpc, cudaStream_t st) {
-    route_kernel<<<nprob, RT_THREADS, 0, st>>>(probs, plans, cs, kpc);
+cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob,
+                         cudaStream_t st) {
+    route_kernel<<<nprob, RT_THREADS, 0, st>>>(probs, plans);
     return cudaGetLastError();
 }
 

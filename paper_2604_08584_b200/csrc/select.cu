@@ -1,28 +1,39 @@
-// select.cu — CSAttention decode, part 1: route + gather + top-K on sm_100a.
+// select.cu — CSAttention decode, part 1: gather + accumulate + top-K on sm_100a.
 //
-// One thread-block CLUSTER per (session, query head) "problem". CTA r of the
-// cluster owns the key range [r*KPC, (r+1)*KPC) and keeps that range's fp64
-// candidate scores in its own shared memory, so per-key scores never touch
-// HBM. Phases (reference functions in brackets):
-//   1. plan      routing (select_centroids) is done by route.cu, which also
-//                writes every rank's entry range of each gathered list.
-//   2. gather    [gather_lists :95-109, reduce_by_key :111-148]  the selected
-//                index-sorted lists' key-block ranges are streamed into an
-//                8-slot shared-memory ring by TMA bulk copies (cp.async.bulk +
-//                mbarrier complete_tx) and accumulated with a conflict-free
-//                shared-memory RMW, chunk by chunk in gathered-list order:
-//                score(i) = sum_l w_b(l) * double(score_l(i)).
-//   3. select    [select_topk :150-228]  the `need`-th best pool key by
-//                (score desc, index asc), cluster-wide: one 1024-bin
-//                linear-bucket pass in the fp64 domain (monotone, so the
-//                threshold bucket is exact), then the bucket's members are
-//                ranked on CTA 0. Degenerate inputs (huge buckets, exact ties)
-//                fall back to 64-bit radix passes and index-order tie breaks.
-//   4. emit      window passthrough + newest-first padding; the K indices are
-//                written ascending for attend.cu.
-// Shared memory: a small header, one 32 KB region reused as (query slices |
-// TMA ring | selection scratch) across phases, and KPC fp64 scores.
-#include <cooperative_groups.h>
+// Persistent kernel, one 544-thread CTA per SM; CTA b takes problems
+// b, b + grid, ... (a problem = one (session, query head) decode search).
+//
+//   producer warp   streams the gathered lists (route.cu's plan) tile by tile:
+//                   for each 8192-key tile and each list, the list's entries
+//                   with keys in the tile ([blk_off(tile), blk_off(tile+1)),
+//                   the tables are index-sorted) are copied by TMA bulk copies
+//                   (cp.async.bulk, L2 evict_first, mbarrier complete_tx) into
+//                   a 7-slot ring. It runs ahead across tile and problem
+//                   boundaries, so the next problem's lists are in flight while
+//                   the current one is being selected.
+//   16 consumer     accumulate list by list in gathered-list order (the
+//   warps           reference's per-key order [gather_lists :95-109,
+//                   reduce_by_key :111-148]): each warp takes an equal slice of
+//                   the list's segment (keys are unique within a list, so the
+//                   fp64 shared-memory RMWs never collide) and a named barrier
+//                   separates lists: score(i) = sum_l w_b(l) * double(score_l(i)).
+//                   At the end of a tile each warp turns its 512 keys into pool
+//                   candidates [select_topk :150-228 pool rules]: a cheap
+//                   compare against the current cut compacts the survivors in
+//                   place, then only those are binned into a 4096-bin linear
+//                   histogram fixed up front by route.cu's score bounds (a
+//                   monotone map, so bins never split equal scores) and
+//                   appended to the warp's candidate log. The cut is the highest
+//                   bin whose suffix count already reaches `need`; it only
+//                   rises, so every candidate that can still be selected is
+//                   logged.
+//   final phase     the exact bin of the need-th best candidate comes from the
+//                   histogram; candidates above it are selected, the bin's
+//                   members are ranked by (score desc, index asc) in shared
+//                   memory (64-bit radix passes for large bins), then window
+//                   passthrough and newest-first padding are applied on a key
+//                   bitmap that is emitted in ascending order.
+// The per-key scores never leave the SM except as logged candidates.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -32,868 +43,886 @@
 #include "kernels.h"
 #include "tma.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace csa {
 
-constexpr int SEL_THREADS = 256;
-constexpr int SEL_WARPS = SEL_THREADS / 32;
-constexpr int RING = 4;           // TMA staging slots
-constexpr int CHUNK_E = 1024;     // entries per slot (8 KB)
-constexpr int HB_BITS = 10;
-constexpr int HB = 1 << HB_BITS;  // histogram bins
-constexpr int SURV_LOCAL = 2048;  // compacted local survivors (fallback radix)
-constexpr int SURV_MAX = 256;     // bucket size finished on CTA 0
+constexpr int SEL_CW = 16;                   // consumer warps
+constexpr int SEL_CT = SEL_CW * 32;          // consumer threads
+constexpr int SEL_THREADS = SEL_CT + 32;     // + producer warp
+constexpr uint32_t TILE = 8192;              // keys per tile (fp64 accumulator: 64 KB)
+constexpr uint32_t TILE_BLKS = TILE / KEY_BLOCK;
+constexpr uint32_t WKEYS = TILE / SEL_CW;    // keys per warp in the tile-end filter
+constexpr int NSLOT = 7;                     // ring slots
+constexpr uint32_t SLOT_E = 2048;            // entries per slot (16 KB)
+constexpr uint32_t CACHE_LIST = 127;         // chunk "list" id of a cached-score tile
+constexpr int NB = 4096;                     // histogram bins
+constexpr int NCB = NB / 32;                 // coarse bins (32 fine bins each)
+constexpr int BKT = 1024;                    // threshold-bin members ranked in smem
+constexpr int RANK_DIRECT = 384;             // O(n^2) ranking up to this size
+constexpr uint32_t F_LIST_END = 1, F_TILE_END = 2, F_PROB_END = 4;
 constexpr unsigned long long ABSENT = 0x7ff4deadbeef0000ull;  // NaN box: key not gathered
+static_assert(TILE * 32 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bits");
+static_assert(SELECT_MAX_CONTEXT / TILE <= 128 && MAXL < 127, "chunk info fields");
+
+// One ring chunk: info = list | flags << 7 | tile << 10; entries at table
+// positions [lo, hi), staged from position `base` (even, 16-byte aligned).
+struct SlotMeta {
+    uint32_t info, base, lo, hi;
+};
 
 struct SelHdr {
-    uint32_t lists[MAXL];
-    uint32_t lsub[MAXL];
-    uint32_t nids[MAXM];
-    uint32_t ids[MAXM * MAXTAU];
-    uint32_t zero_mask, nl;
-    // gather stream
-    unsigned long long bar[RING];    // full: TMA bytes landed
-    unsigned long long empty[RING];  // all warps done with the slot
-    uint32_t c_list[RING], c_cnt[RING], c_vlo[RING], c_vhi[RING];
-    uint32_t l_beg[MAXL], l_cnt[MAXL], l_first[MAXL + 1], l_lo[MAXL], l_hi[MAXL];
-    uint32_t nchunk, issue_l;
-    // values other CTAs of the cluster read through DSMEM
-    unsigned long long x_kmax, x_kmin, x_tk, x_bmax, x_bmin;
-    uint32_t x_cnt, x_tx, x_slice_total, x_nsel, x_nunt;
-    // block scratch / broadcasts
-    unsigned long long r64a[SEL_WARPS], r64b[SEL_WARPS];
-    uint32_t r32a[SEL_WARPS], r32b[SEL_WARPS];
-    unsigned long long b_tk, b_gmax, b_gmin;
-    uint32_t b_tx, b_dsel, b_cabove, b_bucket, b_base, b_take, b_total, b_off;
-    uint32_t surv_count, wpos, nsv;
+    unsigned long long full[NSLOT], empty[NSLOT];
+    SlotMeta meta[NSLOT];
+    uint32_t plist[MAXL];  // producer: table ids of its current problem
+    double cw[MAXL];       // consumers: weight of each gathered list
+    uint32_t cut, nbkt;
+    uint32_t wlog[SEL_CW + 1];  // per-warp candidate-log lengths, then prefix
+    uint32_t wsum[SEL_CW];
+    // final-phase broadcasts
+    uint32_t f_bin, f_above, f_count, f_take_all;
+    unsigned long long tk;
+    uint32_t tx;
 };
-
-// the 32 KB multi-use region
-struct SelectView {
-    uint32_t hist[2][HB];
-    uint32_t ghist[HB];
-    uint32_t gcopy[HB];
-    unsigned long long skey[SURV_MAX];
-    uint32_t sidx[SURV_MAX];
-    uint16_t surv[SURV_LOCAL];
-};
-constexpr size_t REGION_BYTES = static_cast<size_t>(RING) * CHUNK_E * sizeof(uint2);
-static_assert(sizeof(SelectView) <= REGION_BYTES, "select view exceeds region");
 
 __device__ __forceinline__ unsigned long long ordkey(double x) {
     if (x == 0.0) x = 0.0;  // -0.0 == +0.0 (retrieval.cpp:168-171)
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
-__device__ __forceinline__ double key_double(unsigned long long k) {
-    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-    return __longlong_as_double(static_cast<long long>(b));
-}
 __device__ __forceinline__ bool is_absent(double v) {
     return static_cast<unsigned long long>(__double_as_longlong(v)) == ABSENT;
 }
-
-template <class T>
-__device__ __forceinline__ T* remote(cg::cluster_group& cl, T* p, int rank) {
-    return cl.map_shared_rank(p, rank);
+__device__ __forceinline__ double absent_d() {
+    return __longlong_as_double(static_cast<long long>(ABSENT));
+}
+// The tile accumulator marks "not gathered" with -0.0: a gathered key's sum
+// starts as 0.0 + w*s (reduce_by_key) and table scores are never -0.0f (they
+// are fp64 dot sums from +0.0; imports canonicalise), so no sum is -0.0 and
+// -0.0 + w*s == 0.0 + w*s.
+constexpr unsigned long long NEG0 = 0x8000000000000000ull;
+__device__ __forceinline__ double neg0_d() { return __longlong_as_double(static_cast<long long>(NEG0)); }
+__device__ __forceinline__ bool is_neg0(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) == NEG0;
+}
+// monotone non-decreasing score -> bin map (IEEE sub/mul preserve <=)
+__device__ __forceinline__ uint32_t bin_of(double s, double lo, double scale) {
+    const double f = __dmul_rn(__dsub_rn(s, lo), scale);
+    return f >= static_cast<double>(NB - 1) ? static_cast<uint32_t>(NB - 1)
+                                            : (f > 0.0 ? static_cast<uint32_t>(f) : 0u);
 }
 
-__device__ __forceinline__ uint32_t warp_sum(uint32_t v) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
+__device__ __forceinline__ void cbar() {  // consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(SEL_CT) : "memory");
 }
 
-__device__ uint32_t block_sum(SelHdr& S, uint32_t v) {
+// exclusive scan over the consumer threads in thread order; total = sum
+__device__ uint32_t cscan(SelHdr& S, uint32_t v, uint32_t& total) {
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    v = warp_sum(v);
-    __syncthreads();
-    if (ln == 0) S.r32a[w] = v;
-    __syncthreads();
-    uint32_t t = 0;
-#pragma unroll
-    for (int i = 0; i < SEL_WARPS; ++i) t += S.r32a[i];
-    return t;
-}
-
-// Block-wide exclusive scan of two counters (thread order) + totals.
-__device__ void block_scan2(SelHdr& S, uint32_t a, uint32_t b, uint32_t& ea, uint32_t& eb,
-                            uint32_t& ta, uint32_t& tb) {
-    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    uint32_t ia = a, ib = b;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t xa = __shfl_up_sync(0xffffffffu, ia, o);
-        const uint32_t xb = __shfl_up_sync(0xffffffffu, ib, o);
-        if (ln >= o) {
-            ia += xa;
-            ib += xb;
-        }
-    }
-    __syncthreads();
-    if (ln == 31) {
-        S.r32a[w] = ia;
-        S.r32b[w] = ib;
-    }
-    __syncthreads();
-    uint32_t pa = 0, pb = 0;
-    ta = tb = 0;
-#pragma unroll
-    for (int i = 0; i < SEL_WARPS; ++i) {
-        if (i < w) {
-            pa += S.r32a[i];
-            pb += S.r32b[i];
-        }
-        ta += S.r32a[i];
-        tb += S.r32b[i];
-    }
-    ea = pa + ia - a;
-    eb = pb + ib - b;
-}
-
-// lane c of the calling warp gets f(c) for c < cs; returns the exclusive prefix
-// over ranks < `rank` and the total (warp-uniform).
-template <class F>
-__device__ __forceinline__ void warp_rank_scan(int cs, int rank, F f, uint32_t& before,
-                                               uint32_t& total) {
-    const int ln = threadIdx.x & 31;
-    const uint32_t v = ln < cs ? f(ln) : 0u;
     uint32_t inc = v;
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
         if (ln >= o) inc += x;
     }
-    total = __shfl_sync(0xffffffffu, inc, 31);
-    before = rank > 0 ? __shfl_sync(0xffffffffu, inc, rank - 1) : 0u;
-}
-
-// ---------------------------------------------------------------------------
-// Phase 1: the routing plan written by route.cu (lists, subspaces, and this
-// rank's entry range of every list) — one round trip.
-// ---------------------------------------------------------------------------
-__device__ void load_plan(SelHdr& S, const RoutePlan& plan, int rank) {
-    const uint32_t nl = __ldcg(&plan.nl);
-    if (threadIdx.x < MAXL) {  // all slots at once (one round trip); slots >= nl unused
-        const uint32_t l = threadIdx.x;
-        S.lists[l] = __ldcg(plan.lists + l);
-        S.lsub[l] = __ldcg(plan.lsub + l);
-        const uint2 be = plan.bounds[rank * MAXL + l];
-        S.l_lo[l] = be.x;
-        S.l_hi[l] = be.y;
+    if (ln == 31) S.wsum[w] = inc;
+    cbar();
+    uint32_t pre = 0;
+    total = 0;
+#pragma unroll
+    for (int i = 0; i < SEL_CW; ++i) {
+        const uint32_t x = S.wsum[i];
+        pre += i < w ? x : 0u;
+        total += x;
     }
-    if (threadIdx.x == 0) S.nl = nl;
-    __syncthreads();
+    cbar();
+    return pre + inc - v;
 }
 
-// ---------------------------------------------------------------------------
-// Phase 2: gather + fp64 accumulate of this CTA's key range.
-// The per-list key-block ranges are concatenated into a stream of <= CHUNK_E
-// entry chunks; thread 0 keeps RING chunks in flight with TMA bulk copies,
-// every thread consumes chunks in order (so each key sees its lists in
-// gathered order: the fixed accumulation order).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void acc_entry(double* acc, uint32_t key, uint32_t sbits, double w,
-                                          uint32_t k0) {
-    if (key & TOMB) return;  // evicted entry
-    const uint32_t li = key - k0;
-    const double val = __dmul_rn(w, static_cast<double>(__uint_as_float(sbits)));
-    const double o = acc[li];
-    acc[li] = is_absent(o) ? __dadd_rn(0.0, val) : __dadd_rn(o, val);
-}
-
-__device__ __forceinline__ void issue_chunk(SelHdr& S, const SessionDev& sd, uint2* stage,
-                                            uint32_t c) {
-    while (S.l_first[S.issue_l + 1] <= c) ++S.issue_l;
-    const uint32_t l = S.issue_l, slot = c % RING;
-    const uint32_t off = (c - S.l_first[l]) * CHUNK_E;
-    const uint32_t n = min(static_cast<uint32_t>(CHUNK_E), S.l_cnt[l] - off);
-    const uint2* src = sd.ent + static_cast<size_t>(S.lists[l]) * sd.cap2 + S.l_beg[l] + off;
-    S.c_list[slot] = l;
-    S.c_cnt[slot] = n;
-    // the 16-byte aligned superset may include one entry of a neighbour block
-    // or one slot past n_used: only positions inside [lo, hi) are accumulated
-    const uint32_t pos = S.l_beg[l] + off;
-    S.c_vlo[slot] = S.l_lo[l] > pos ? S.l_lo[l] - pos : 0u;
-    S.c_vhi[slot] = min(n, S.l_hi[l] - pos);
-    mbar_expect_tx(&S.bar[slot], n * 8);
-    bulk_g2s(stage + slot * CHUNK_E, src, n * 8, &S.bar[slot]);
-}
-
-// plan the chunk stream (bounds prefetched by route) and launch the first RING
-// bulk copies; thread 0 is the producer. Called right after route's barrier.
-__device__ void gather_issue(SelHdr& S, const SessionDev& sd, uint2* stage) {
-    if (threadIdx.x != 0) return;
-    uint32_t nch = 0;
-    for (uint32_t l = 0; l < S.nl; ++l) {
-        const uint32_t beg = S.l_lo[l], end = S.l_hi[l];
-        const uint32_t ab = beg & ~1u;
-        const uint32_t ae = end > beg ? ((end + 1) & ~1u) : ab;  // cap2 is even
-        S.l_beg[l] = ab;
-        S.l_cnt[l] = ae - ab;
-        S.l_first[l] = nch;
-        nch += div_up(ae - ab, CHUNK_E);
+// Top-down crossing over a warp-held group of 32 counts: lane l holds count of
+// bin (base + l); `above` = count above the group. Returns the highest lane
+// whose suffix (bins >= it, plus above) reaches `need`, or -1; sets the count
+// strictly above that lane.
+__device__ __forceinline__ int warp_cross(uint32_t v, uint32_t above, uint32_t need,
+                                          uint32_t& above_out) {
+    const int ln = threadIdx.x & 31;
+    uint32_t suf = v;  // inclusive suffix over lanes >= ln
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_down_sync(0xffffffffu, suf, o);
+        if (ln + o < 32) suf += x;
     }
-    S.l_first[S.nl] = nch;
-    S.nchunk = nch;
-    S.issue_l = 0;
-    for (int r = 0; r < RING; ++r) {
-        mbar_init(&S.bar[r], 1);
-        mbar_init(&S.empty[r], SEL_WARPS);
-    }
-    fence_mbar_init();
-    fence_proxy_async();  // the ring reuses bytes the generic proxy just wrote
-    for (uint32_t c = 0; c < nch && c < static_cast<uint32_t>(RING); ++c) issue_chunk(S, sd, stage, c);
+    const unsigned hit = __ballot_sync(0xffffffffu, above + suf >= need);
+    if (!hit) return -1;
+    const int l = 31 - __clz(hit);
+    above_out = above + __shfl_sync(0xffffffffu, suf - v, l);
+    return l;
 }
 
-// Consumers: chunks of one list touch distinct keys, so warps only need a
-// block barrier where a new list starts (fixed per-key accumulation order);
-// slot reuse is tracked per slot by an `empty` mbarrier (one arrival per warp),
-// which the producer waits on before refilling the slot.
-__device__ void gather_consume(SelHdr& S, const SessionDev& sd, uint2* stage, double* acc,
-                               uint32_t k0) {
-    const uint32_t nch = S.nchunk;
-    uint32_t cur = 0;  // list of chunk c
-    for (uint32_t c = 0; c < nch; ++c) {
-        const uint32_t slot = c % RING, par = (c / RING) & 1u;
-        if (S.l_first[cur + 1] <= c) {  // chunk c opens a new list (skip empty ones)
-            while (S.l_first[cur + 1] <= c) ++cur;
-            if (c > 0) __syncthreads();  // previous list fully accumulated
+// Highest fine bin whose suffix count reaches `need`, from the two-level
+// histogram, by one warp (counts at and above the answer must be exact).
+// Returns -1 if the total is below need; `above` = count strictly above.
+__device__ int warp_find_bin(const uint32_t* hist, const uint32_t* coarse, uint32_t need,
+                             uint32_t& above) {
+    const int ln = threadIdx.x & 31;
+    uint32_t run = 0;
+    for (int g = NCB / 32 - 1; g >= 0; --g) {
+        const uint32_t v = coarse[g * 32 + ln];
+        uint32_t ab;
+        const int l = warp_cross(v, run, need, ab);
+        if (l >= 0) {
+            const int cb = g * 32 + l;
+            uint32_t ab2;
+            const int f = warp_cross(hist[cb * 32 + ln], ab, need, ab2);
+            above = ab2;
+            // f < 0 only while other warps are mid-update (coarse counted
+            // before fine): report no crossing, the caller keeps its cut
+            return f < 0 ? -1 : cb * 32 + f;
         }
-        mbar_wait(&S.bar[slot], par);
-        const uint32_t n = S.c_cnt[slot];
-        const uint32_t vlo = S.c_vlo[slot], vhi = S.c_vhi[slot];
-        const double w = sd.weights[S.lsub[cur]];
-        const uint4* e4 = reinterpret_cast<const uint4*>(stage + slot * CHUNK_E);
-        for (uint32_t p = threadIdx.x; p < (n >> 1); p += blockDim.x) {
-            const uint4 v = e4[p];
-            if (2 * p >= vlo && 2 * p < vhi) acc_entry(acc, v.x, v.y, w, k0);
-            if (2 * p + 1 >= vlo && 2 * p + 1 < vhi) acc_entry(acc, v.z, v.w, w, k0);
-        }
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(&S.empty[slot]);
-        if (threadIdx.x == 0 && c + RING < nch) {
-            mbar_wait(&S.empty[slot], par);  // every warp is done with chunk c
-            issue_chunk(S, sd, stage, c + RING);
-        }
+        uint32_t s = v;
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        run += s;
     }
-    __syncthreads();
+    above = run;
+    return -1;
 }
 
-// ---------------------------------------------------------------------------
-// Phase 3: cluster-wide selection of the `need` best pool keys.
-// Result (on every CTA): S.b_tk / S.b_tx such that a pool key is selected iff
-// key > tk || (key == tk && index < tx).
-// ---------------------------------------------------------------------------
-struct Keys {
-    unsigned long long* k;  // local pool keys (0 = not in pool)
-    uint32_t n;
-};
-
-// Finish on CTA 0: the bucket's members (pred) from every CTA are copied to
-// CTA 0, which finds the rem-th by (key desc, index asc). cnt_of(c) = members
-// on CTA c. Publishes b_tk / b_tx on every CTA.
-template <class Pred, class CountOf>
-__device__ void rank_on_leader(cg::cluster_group& cl, SelHdr& S, SelectView& V, const Keys& kv,
-                               uint32_t k0, uint32_t rem, uint32_t bucket, Pred pred,
-                               CountOf cnt_of) {
-    const int rank = cl.block_rank(), cs = cl.num_blocks();
+// Exact rem-th best member (key desc, index asc) by radix passes; members are
+// get(e, key, idx) == true for e < n. Leaves S.tk / S.tx such that a member is
+// selected iff key > tk || (key == tk && idx < tx). Uses hist as scratch.
+template <class Get>
+__device__ void radix_kth(SelHdr& S, uint32_t* hist, uint32_t n, uint32_t rem, Get get) {
     const uint32_t tid = threadIdx.x;
-    if (tid < 32) {
-        uint32_t before, total;
-        warp_rank_scan(cs, rank, cnt_of, before, total);
-        if (tid == 0) {
-            S.b_off = before;
-            S.wpos = 0;
+    unsigned long long prefix = 0;
+    int pshift = 64;
+    bool ties = false;
+    for (;;) {  // stage 1: the score key
+        const int shift = pshift > 11 ? pshift - 11 : 0;
+        const uint32_t nbins = 1u << (pshift - shift);
+        for (uint32_t i = tid; i < nbins; i += SEL_CT) hist[i] = 0;
+        cbar();
+        for (uint32_t e = tid; e < n; e += SEL_CT) {
+            unsigned long long k;
+            uint32_t ix;
+            if (!get(e, k, ix)) continue;
+            if (pshift < 64 && (k >> pshift) != prefix) continue;
+            atomicAdd(&hist[(k >> shift) & (nbins - 1)], 1u);
         }
-    }
-    __syncthreads();
-    unsigned long long* dk = remote(cl, V.skey, 0);
-    uint32_t* di = remote(cl, V.sidx, 0);
-    const uint32_t off = S.b_off;
-    for (uint32_t l = tid; l < kv.n; l += blockDim.x) {
-        const unsigned long long k = kv.k[l];
-        if (k && pred(l, k)) {
-            const uint32_t p = off + atomicAdd(&S.wpos, 1u);
-            dk[p] = k;
-            di[p] = k0 + l;
-        }
-    }
-    cl.sync();  // bucket gathered on CTA 0
-    if (rank == 0) {
-        for (uint32_t e = tid; e < bucket; e += blockDim.x) {
-            const unsigned long long ke = V.skey[e];
-            const uint32_t ie = V.sidx[e];
-            uint32_t r = 0;
-            for (uint32_t f = 0; f < bucket; ++f) {
-                const unsigned long long kf = V.skey[f];
-                r += (kf > ke) || (kf == ke && V.sidx[f] < ie);
-            }
-            if (r == rem - 1) {
-                S.x_tk = ke;
-                S.x_tx = ie + 1;
-            }
-        }
-    }
-    cl.sync();  // threshold published by CTA 0
-    if (tid == 0) {
-        S.b_tk = *remote(cl, &S.x_tk, 0);
-        S.b_tx = *remote(cl, &S.x_tx, 0);
-    }
-    __syncthreads();
-}
-
-// Exact ties at key == tk: the rem-th smallest index among them, cluster-wide.
-template <class Pred, class CountOf>
-__device__ void resolve_ties(cg::cluster_group& cl, SelHdr& S, const Keys& kv, uint32_t k0,
-                             unsigned long long tk, uint32_t rem, Pred pred, CountOf cnt_of) {
-    const int rank = cl.block_rank(), cs = cl.num_blocks();
-    if (threadIdx.x < 32) {
-        uint32_t before, total;
-        warp_rank_scan(cs, rank, cnt_of, before, total);
-        if (threadIdx.x == 0) S.b_off = before;
-    }
-    __syncthreads();
-    const uint32_t before = S.b_off;
-    const uint32_t mine = cnt_of(rank);
-    if (rem > before && rem <= before + mine) {
-        const uint32_t want = rem - before;  // 1-based among local ties
-        const uint32_t chunk = div_up(kv.n, blockDim.x);
-        const uint32_t c0 = min(kv.n, threadIdx.x * chunk), c1 = min(kv.n, c0 + chunk);
-        uint32_t n = 0;
-        for (uint32_t l = c0; l < c1; ++l) n += (kv.k[l] == tk && pred(l, tk));
-        uint32_t ex, dummy, tot, tot2;
-        block_scan2(S, n, 0, ex, dummy, tot, tot2);
-        if (want > ex && want <= ex + n) {
-            uint32_t seen = ex;
-            for (uint32_t l = c0; l < c1; ++l)
-                if (kv.k[l] == tk && pred(l, tk) && ++seen == want) {
-                    *remote(cl, &S.x_tx, 0) = k0 + l + 1;
+        cbar();
+        if (tid < 32) {
+            uint32_t run = 0;
+            for (int g = static_cast<int>(nbins / 32) - 1; g >= 0; --g) {
+                const uint32_t v = hist[g * 32 + tid];
+                uint32_t ab;
+                const int l = warp_cross(v, run, rem, ab);
+                if (l >= 0) {
+                    if (tid == 0) {
+                        S.f_bin = g * 32 + l;
+                        S.f_above = ab;
+                        S.f_count = hist[g * 32 + l];
+                    }
                     break;
                 }
-        }
-    }
-    cl.sync();
-    if (threadIdx.x == 0) {
-        S.b_tk = tk;
-        S.b_tx = *remote(cl, &S.x_tx, 0);
-    }
-    __syncthreads();
-}
-
-// Distributed histogram: local hist (nb bins, already filled) -> CTA r reduces
-// slice r across the cluster -> every CTA locates the bin holding the rem-th
-// largest. Leaves b_dsel / b_cabove / b_bucket. Two cluster barriers.
-__device__ void cluster_hist_pick(cg::cluster_group& cl, SelHdr& S, SelectView& V, uint32_t* hist,
-                                  uint32_t nb, uint32_t rem) {
-    const int rank = cl.block_rank(), cs = cl.num_blocks();
-    const uint32_t tid = threadIdx.x;
-    cl.sync();  // local histograms complete
-    const uint32_t sl = div_up(nb, cs);
-    const uint32_t lo = min(nb, rank * sl), hi = min(nb, lo + sl);
-    uint32_t part = 0;
-    for (uint32_t i = lo + tid; i < hi; i += blockDim.x) {
-        uint32_t v = 0;
-        for (int c = 0; c < cs; ++c) v += remote(cl, hist, c)[i];
-        V.ghist[i] = v;
-        part += v;
-    }
-    part = block_sum(S, part);
-    if (tid == 0) S.x_slice_total = part;
-    cl.sync();  // reduced slices + slice totals published
-    if (tid < 32) {
-        const int ln = tid;
-        const uint32_t st = ln < cs ? *remote(cl, &S.x_slice_total, ln) : 0;
-        uint32_t suf = st;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_down_sync(0xffffffffu, suf, o);
-            if (ln + o < 32) suf += x;
-        }
-        const uint32_t above = suf - st;
-        const bool hit = (ln < cs) && st > 0 && above < rem && suf >= rem;
-        const unsigned hm = __ballot_sync(0xffffffffu, hit);
-        const int sstar = __ffs(hm) - 1;
-        const uint32_t cab = __shfl_sync(0xffffffffu, above, sstar);
-        const uint32_t slo = min(nb, sstar * sl), shi = min(nb, slo + sl);
-        const uint32_t* src = remote(cl, V.ghist, sstar);
-        for (uint32_t i = slo + ln; i < shi; i += 32) V.gcopy[i] = src[i];
-        __syncwarp();
-        if (ln == 0) {
-            uint32_t c = cab, dd = shi;
-            while (dd > slo) {
-                --dd;
-                const uint32_t h = V.gcopy[dd];
-                if (c + h >= rem) break;
-                c += h;
-            }
-            S.b_dsel = dd;
-            S.b_cabove = c;
-            S.b_bucket = V.gcopy[dd];
-        }
-    }
-    __syncthreads();
-}
-
-// 64-bit radix refinement restricted to keys with pred(l, k) (fallback path).
-template <class Pred>
-__device__ void radix_refine(cg::cluster_group& cl, SelHdr& S, SelectView& V, const Keys& kv,
-                             uint32_t k0, uint32_t rem, unsigned long long gmin,
-                             unsigned long long gmax, Pred pred) {
-    const uint32_t tid = threadIdx.x;
-    if (gmin == gmax) {
-        resolve_ties(cl, S, kv, k0, gmax, rem, pred, [&](int c) { return *remote(cl, &S.x_cnt, c); });
-        return;
-    }
-    int pshift = 64 - __clzll(static_cast<long long>(gmax ^ gmin));
-    unsigned long long prefix = pshift == 64 ? 0ull : (gmax >> pshift);
-    bool use_surv = false;
-    for (int pass = 0;; ++pass) {
-        const int shift = pshift > HB_BITS ? pshift - HB_BITS : 0;
-        const int nbits = pshift - shift;
-        const uint32_t nb = 1u << nbits;
-        uint32_t* hist = V.hist[pass & 1];
-        for (uint32_t i = tid; i < nb; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        auto cand = [&](uint32_t l, unsigned long long k) {
-            return k && pred(l, k) && (pshift == 64 || (k >> pshift) == prefix);
-        };
-        if (use_surv) {
-            for (uint32_t s = tid; s < S.surv_count; s += blockDim.x) {
-                const unsigned long long k = kv.k[V.surv[s]];
-                atomicAdd(&hist[(k >> shift) & (nb - 1)], 1u);
-            }
-        } else {
-            for (uint32_t l = tid; l < kv.n; l += blockDim.x) {
-                const unsigned long long k = kv.k[l];
-                if (cand(l, k)) atomicAdd(&hist[(k >> shift) & (nb - 1)], 1u);
+                uint32_t s = v;
+                for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                run += s;
             }
         }
-        cluster_hist_pick(cl, S, V, hist, nb, rem);
-        const uint32_t dsel = S.b_dsel;
-        rem -= S.b_cabove;
-        const uint32_t bucket = S.b_bucket;
-        prefix = (pshift == 64 ? 0ull : (prefix << nbits)) | dsel;
+        cbar();
+        rem -= S.f_above;
+        prefix = (pshift == 64 ? 0ull : (prefix << (pshift - shift))) | S.f_bin;
         pshift = shift;
-        auto member = [&](uint32_t l, unsigned long long k) {
-            return pred(l, k) && (k >> pshift) == prefix;
-        };
-        auto cnt_of = [&](int c) { return remote(cl, hist, c)[dsel]; };
-        if (bucket == rem) {  // the whole bucket is taken
+        if (S.f_count == rem) {  // the whole digit bucket is taken
+            const unsigned long long T = prefix << pshift;
             if (tid == 0) {
-                S.b_tk = (prefix << pshift) - 1;
-                S.b_tx = 0;
+                S.tk = T ? T - 1 : 0ull;
+                S.tx = 0;
             }
-            __syncthreads();
+            cbar();
             return;
         }
-        if (pshift == 0) {  // exact ties at key == prefix
-            resolve_ties(cl, S, kv, k0, prefix, rem, member, cnt_of);
-            return;
-        }
-        if (bucket <= static_cast<uint32_t>(SURV_MAX)) {
-            rank_on_leader(cl, S, V, kv, k0, rem, bucket, member, cnt_of);
-            return;
-        }
-        const uint32_t mine = hist[dsel];
-        if (mine <= static_cast<uint32_t>(SURV_LOCAL)) {
-            if (tid == 0) S.nsv = 0;
-            __syncthreads();
-            if (use_surv) {
-                const uint32_t n0 = S.surv_count;
-                uint16_t keep[SURV_LOCAL / SEL_THREADS];
-                uint32_t nk = 0;
-                for (uint32_t s = tid, u = 0; s < n0 && u < SURV_LOCAL / SEL_THREADS;
-                     s += blockDim.x, ++u) {
-                    const unsigned long long k = kv.k[V.surv[s]];
-                    if ((k >> pshift) == prefix) keep[nk++] = V.surv[s];
-                }
-                __syncthreads();
-                for (uint32_t u = 0; u < nk; ++u) V.surv[atomicAdd(&S.nsv, 1u)] = keep[u];
-            } else {
-                for (uint32_t l = tid; l < kv.n; l += blockDim.x) {
-                    const unsigned long long k = kv.k[l];
-                    if (k && member(l, k)) V.surv[atomicAdd(&S.nsv, 1u)] = static_cast<uint16_t>(l);
-                }
-            }
-            __syncthreads();
-            if (tid == 0) S.surv_count = S.nsv;
-            use_surv = true;
-            __syncthreads();
-        } else {
-            use_surv = false;
+        if (pshift == 0) {
+            ties = true;
+            break;
         }
     }
+    // stage 2: rem lowest indices among the members tied at key == prefix
+    const unsigned long long tk = prefix;
+    uint32_t ipre = 0;
+    int ishift = 32;
+    if (ties) {
+        for (;;) {
+            const int shift = ishift > 11 ? ishift - 11 : 0;
+            const uint32_t nbins = 1u << (ishift - shift);
+            for (uint32_t i = tid; i < nbins; i += SEL_CT) hist[i] = 0;
+            cbar();
+            for (uint32_t e = tid; e < n; e += SEL_CT) {
+                unsigned long long k;
+                uint32_t ix;
+                if (!get(e, k, ix) || k != tk) continue;
+                const uint32_t r = ~ix;  // largest r = smallest index
+                if (ishift < 32 && (r >> ishift) != ipre) continue;
+                atomicAdd(&hist[(r >> shift) & (nbins - 1)], 1u);
+            }
+            cbar();
+            if (tid < 32) {
+                uint32_t run = 0;
+                for (int g = static_cast<int>(nbins / 32) - 1; g >= 0; --g) {
+                    const uint32_t v = hist[g * 32 + tid];
+                    uint32_t ab;
+                    const int l = warp_cross(v, run, rem, ab);
+                    if (l >= 0) {
+                        if (tid == 0) {
+                            S.f_bin = g * 32 + l;
+                            S.f_above = ab;
+                            S.f_count = hist[g * 32 + l];
+                        }
+                        break;
+                    }
+                    uint32_t s = v;
+                    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                    run += s;
+                }
+            }
+            cbar();
+            rem -= S.f_above;
+            ipre = (ishift == 32 ? 0u : (ipre << (ishift - shift))) | S.f_bin;
+            ishift = shift;
+            if (S.f_count == rem || ishift == 0) break;  // indices are unique
+        }
+    }
+    // selected ties: ~idx >= (ipre << ishift)  <=>  idx <= ~(ipre << ishift)
+    if (tid == 0) {
+        S.tk = tk;
+        S.tx = ~(ipre << ishift) + 1u;  // idx < tx
+    }
+    cbar();
 }
 
-// (cnt, kmax, kmin): this thread's pool statistics from the key transform
-__device__ void select_threshold(cg::cluster_group& cl, SelHdr& S, SelectView& V, const Keys& kv,
-                                 uint32_t k0, uint32_t need, uint32_t cnt,
-                                 unsigned long long kmax, unsigned long long kmin) {
-    const int cs = cl.num_blocks();
+__device__ __forceinline__ void set_bit(uint32_t* bm, uint32_t i) {
+    atomicOr(bm + (i >> 5), 1u << (i & 31));
+}
+
+
+// Per-problem state of the consumer warps (registers).
+struct ProbState {
+    uint32_t N, K, need, f_lo, wlo;
+    uint32_t n_cache;
+    bool pt, store_cache;
+    double lo, scale;
+    double* cache;
+    uint32_t* sel;
+    uint32_t* rep;
+    unsigned long long* prof;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// consumer warps: load problem p's descriptor, list weights, score bounds
+__device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const RoutePlan* plans,
+                              uint32_t p, ProbState& st) {
     const uint32_t tid = threadIdx.x;
-    // ---- pool statistics: count, max, min key ----
-    for (int o = 16; o; o >>= 1) {
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        const unsigned long long a = __shfl_xor_sync(0xffffffffu, kmax, o);
-        const unsigned long long b = __shfl_xor_sync(0xffffffffu, kmin, o);
-        kmax = a > kmax ? a : kmax;
-        kmin = b < kmin ? b : kmin;
+    const DecodeProblem* Pp = probs + p;
+    const SessionDev* sdp = Pp->s;
+    st.N = Pp->N;
+    st.K = Pp->K;
+    const uint32_t mode = Pp->mode;
+    st.n_cache = Pp->n_cache;
+    st.cache = Pp->cache;
+    double* const cbounds = Pp->cbounds;
+    st.sel = Pp->sel;
+    st.rep = Pp->rep;
+    st.prof = Pp->prof;
+    const uint32_t window = sdp->window;
+    st.pt = sdp->passthrough != 0;
+    const bool search = mode & MODE_SEARCH;
+    st.store_cache = (mode & MODE_STORE_CACHE) && st.cache;
+    if (search) {
+        const uint32_t nl = __ldcg(&plans[p].nl);
+        for (uint32_t l = tid; l < nl; l += SEL_CT) S.cw[l] = sdp->weights[__ldcg(plans[p].lsub + l)];
     }
-    const int w = tid >> 5, ln = tid & 31;
-    if (ln == 0) {
-        S.r32a[w] = cnt;
-        S.r64a[w] = kmax;
-        S.r64b[w] = kmin;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t c = 0;
-        unsigned long long a = 0, b = ~0ull;
-        for (int i = 0; i < SEL_WARPS; ++i) {
-            c += S.r32a[i];
-            a = S.r64a[i] > a ? S.r64a[i] : a;
-            b = S.r64b[i] < b ? S.r64b[i] : b;
+    double lo, hi;
+    if (search) {
+        lo = __ldcg(&plans[p].lo);
+        hi = __ldcg(&plans[p].hi);
+        if (st.store_cache && tid == 0) {
+            cbounds[0] = lo;
+            cbounds[1] = hi;
         }
-        S.x_cnt = c;
-        S.x_kmax = a;
-        S.x_kmin = b;
+    } else {
+        lo = __ldcg(cbounds);
+        hi = __ldcg(cbounds + 1);
     }
-    cl.sync();
-    if (tid < 32) {
-        uint32_t c = 0;
-        unsigned long long a = 0, b = ~0ull;
-        if (ln < cs) {
-            c = *remote(cl, &S.x_cnt, ln);
-            a = *remote(cl, &S.x_kmax, ln);
-            b = *remote(cl, &S.x_kmin, ln);
-        }
-        c = warp_sum(c);
-        for (int o = 16; o; o >>= 1) {
-            const unsigned long long x = __shfl_xor_sync(0xffffffffu, a, o);
-            const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
-            a = x > a ? x : a;
-            b = y < b ? y : b;
-        }
-        if (ln == 0) {
-            S.b_total = c;
-            S.b_gmax = a;
-            S.b_gmin = b;
-        }
+    st.lo = lo;
+    st.scale = hi > lo ? static_cast<double>(NB) / (hi - lo) : 0.0;
+    const uint32_t N = st.N, K = st.K;
+    const uint32_t r_eff = window < N ? window : N;
+    st.wlo = N - r_eff;
+    if (st.pt) {
+        st.need = K > r_eff ? K - r_eff : 0;
+        st.f_lo = K > r_eff ? st.wlo : N - K;
+    } else {
+        st.need = K;
+        st.f_lo = N;
     }
-    __syncthreads();
-    const uint32_t total = S.b_total;
-    const unsigned long long gmax = S.b_gmax, gmin = S.b_gmin;
-    if (need == 0 || total <= need) {  // nothing / everything from the pool
-        if (tid == 0) {
-            S.b_tk = need == 0 ? ~0ull : 0ull;
-            S.b_tx = 0;
-        }
-        __syncthreads();
-        return;
-    }
-    auto any = [](uint32_t, unsigned long long) { return true; };
-    if (gmax == gmin) {  // all pool keys tie: lowest indices win
-        resolve_ties(cl, S, kv, k0, gmax, need, any, [&](int c) { return *remote(cl, &S.x_cnt, c); });
-        return;
-    }
-    // ---- one linear-bucket pass in the fp64 domain ----
-    // bucket(s) = min(HB-1, floor((s - smin) * HB/(smax - smin))) is monotone
-    // non-decreasing in s under IEEE rounding, so the bucket holding the
-    // need-th largest key is exact; equal keys share a bucket.
-    const double smin = key_double(gmin), smax = key_double(gmax);
-    const double scale = static_cast<double>(HB) / (smax - smin);
-    auto bucket_of = [&](unsigned long long k) {
-        const double f = (key_double(k) - smin) * scale;
-        return f >= static_cast<double>(HB - 1) ? static_cast<uint32_t>(HB - 1)
-                                                : static_cast<uint32_t>(f);
-    };
-    uint32_t* hist = V.hist[0];
-    for (uint32_t i = tid; i < static_cast<uint32_t>(HB); i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (uint32_t l = tid; l < kv.n; l += blockDim.x) {
-        const unsigned long long k = kv.k[l];
-        if (k) atomicAdd(&hist[bucket_of(k)], 1u);
-    }
-    cluster_hist_pick(cl, S, V, hist, HB, need);
-    const uint32_t dsel = S.b_dsel;
-    const uint32_t rem = need - S.b_cabove;
-    const uint32_t bucket = S.b_bucket;
-    auto member = [&](uint32_t, unsigned long long k) { return bucket_of(k) == dsel; };
-    auto cnt_of = [&](int c) { return remote(cl, hist, c)[dsel]; };
-    if (bucket <= static_cast<uint32_t>(SURV_MAX)) {
-        rank_on_leader(cl, S, V, kv, k0, rem, bucket, member, cnt_of);
-        return;
-    }
-    // ---- fallback: 64-bit radix within the (large) bucket ----
-    unsigned long long bmax = 0, bmin = ~0ull;
-    uint32_t bc = 0;
-    for (uint32_t l = tid; l < kv.n; l += blockDim.x) {
-        const unsigned long long k = kv.k[l];
-        if (k && member(l, k)) {
-            bmax = k > bmax ? k : bmax;
-            bmin = k < bmin ? k : bmin;
-            ++bc;
-        }
-    }
-    for (int o = 16; o; o >>= 1) {
-        bc += __shfl_xor_sync(0xffffffffu, bc, o);
-        const unsigned long long a = __shfl_xor_sync(0xffffffffu, bmax, o);
-        const unsigned long long b = __shfl_xor_sync(0xffffffffu, bmin, o);
-        bmax = a > bmax ? a : bmax;
-        bmin = b < bmin ? b : bmin;
-    }
-    if (ln == 0) {
-        S.r32a[w] = bc;
-        S.r64a[w] = bmax;
-        S.r64b[w] = bmin;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t c = 0;
-        unsigned long long a = 0, b = ~0ull;
-        for (int i = 0; i < SEL_WARPS; ++i) {
-            c += S.r32a[i];
-            a = S.r64a[i] > a ? S.r64a[i] : a;
-            b = S.r64b[i] < b ? S.r64b[i] : b;
-        }
-        S.x_cnt = c;  // per-CTA member count (tie path)
-        S.x_bmax = a;
-        S.x_bmin = b;
-    }
-    cl.sync();
-    if (tid < 32) {
-        unsigned long long a = 0, b = ~0ull;
-        if (ln < cs) {
-            a = *remote(cl, &S.x_bmax, ln);
-            b = *remote(cl, &S.x_bmin, ln);
-        }
-        for (int o = 16; o; o >>= 1) {
-            const unsigned long long x = __shfl_xor_sync(0xffffffffu, a, o);
-            const unsigned long long y = __shfl_xor_sync(0xffffffffu, b, o);
-            a = x > a ? x : a;
-            b = y < b ? y : b;
-        }
-        if (ln == 0) {
-            S.b_gmax = a;
-            S.b_gmin = b;
-        }
-    }
-    __syncthreads();
-    radix_refine(cl, S, V, kv, k0, rem, S.b_gmin, S.b_gmax, member);
+    cbar();  // weights visible
+    if (st.prof && tid == 0) st.prof[0] = gtimer();
 }
 
-// ---------------------------------------------------------------------------
-// the kernel
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(SEL_THREADS, 2)
+__global__ void __launch_bounds__(SEL_THREADS, 1)
 select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
-              uint32_t kpc) {
+              uint32_t nprob, uint32_t* __restrict__ log_idx_all, double* __restrict__ log_sc_all,
+              uint32_t log_cap) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
-    unsigned char* region = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
-    uint2* stage = reinterpret_cast<uint2*>(region);
-    SelectView& V = *reinterpret_cast<SelectView*>(region);
-    double* acc = reinterpret_cast<double*>(region + REGION_BYTES);
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = cl.block_rank(), cs = cl.num_blocks();
-    const DecodeProblem& P = probs[blockIdx.x / cs];
-    const SessionDev& sd = *P.s;
-    const uint32_t tid = threadIdx.x, N = P.N, K = P.K;
-    const bool leader = rank == 0;
-    const uint32_t k0 = rank * kpc;
-    const uint32_t k1 = min(N, k0 + kpc);
-    const uint32_t nloc = k1 > k0 ? k1 - k0 : 0;
+    unsigned char* p0 = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
+    double* acc = reinterpret_cast<double*>(p0);                    // TILE fp64
+    uint32_t* bm = reinterpret_cast<uint32_t*>(p0);                 // bitmap (aliases acc)
+    uint32_t* hist = reinterpret_cast<uint32_t*>(p0 + TILE * 8);    // NB
+    uint32_t* coarse = hist + NB;                                   // NCB
+    unsigned long long* bkey = reinterpret_cast<unsigned long long*>(coarse + NCB);  // BKT
+    uint32_t* bidx = reinterpret_cast<uint32_t*>(bkey + BKT);       // BKT
+    uint16_t* cidx = reinterpret_cast<uint16_t*>(bidx + BKT);       // SEL_CW * WKEYS
+    uint2* ring = reinterpret_cast<uint2*>(cidx + SEL_CW * WKEYS);  // NSLOT * SLOT_E
+    const uint32_t tid = threadIdx.x;
+    const int wid = tid >> 5, ln = tid & 31;
+    uint32_t* log_idx = log_idx_all + static_cast<size_t>(blockIdx.x) * log_cap;
+    double* log_sc = log_sc_all + static_cast<size_t>(blockIdx.x) * log_cap;
 
     if (tid == 0) {
-        S.zero_mask = 0;
-        S.nl = 0;
-        S.surv_count = 0;
-    }
-    __syncthreads();
-    unsigned long long* prof = P.prof ? P.prof + rank * 8 : nullptr;
-    auto phase = [&](int i) {
-        if (prof && tid == 0) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            prof[i] = t;
+        for (int s = 0; s < NSLOT; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], SEL_CW);
         }
-    };
-    phase(0);
-
-    // ---- 1+2: candidate scores of this CTA's key range ----
-    if (P.mode & MODE_SEARCH) {
-        load_plan(S, plans[blockIdx.x / cs], rank);
-        phase(1);
-        if (nloc) gather_issue(S, sd, stage);  // TMA copies in flight ...
-        for (uint32_t l = tid; l < kpc; l += blockDim.x)  // ... while acc is reset
-            acc[l] = __longlong_as_double(static_cast<long long>(ABSENT));
-        __syncthreads();
-        phase(2);
-        if (nloc) gather_consume(S, sd, stage, acc, k0);
-        phase(3);
-        if (P.mode & MODE_STORE_CACHE)
-            for (uint32_t l = tid; l < nloc; l += blockDim.x) P.cache[k0 + l] = acc[l];
-    } else {
-        for (uint32_t l = tid; l < kpc; l += blockDim.x)
-            acc[l] = (l < nloc && k0 + l < P.n_cache)
-                         ? P.cache[k0 + l]
-                         : __longlong_as_double(static_cast<long long>(ABSENT));
+        fence_mbar_init();
+        S.cut = 0;
+        S.nbkt = 0;
     }
+    for (uint32_t i = tid; i < TILE; i += SEL_THREADS) acc[i] = neg0_d();
+    for (uint32_t i = tid; i < NB + NCB; i += SEL_THREADS) hist[i] = 0;
     __syncthreads();
 
-    // ---- 3: pool keys, selection threshold ----
-    const uint32_t r_eff = sd.window < N ? sd.window : N;
-    const uint32_t wlo = N - r_eff;
-    const bool pt = sd.passthrough != 0;
-    uint32_t need, f_lo;
-    if (pt) {
-        need = K > r_eff ? K - r_eff : 0;
-        f_lo = K > r_eff ? wlo : N - K;
-    } else {
-        need = K;
-        f_lo = N;
-    }
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(acc);
-    uint32_t pcnt = 0;
-    unsigned long long pmax = 0, pmin = ~0ull;
-    for (uint32_t l = tid; l < nloc; l += blockDim.x) {
-        const uint32_t i = k0 + l;
-        const double v = acc[l];
-        unsigned long long key = 0;
-        if (i < wlo)
-            key = is_absent(v) ? 0ull : ordkey(v);
-        else if (!pt)
-            key = ordkey(is_absent(v) ? 0.0 : v);
-        keys[l] = key;
-        if (key) {
-            ++pcnt;
-            pmax = key > pmax ? key : pmax;
-            pmin = key < pmin ? key : pmin;
+    // ======================= producer warp =======================
+    if (wid == SEL_CW) {
+        const unsigned long long pol = l2_evict_first_policy();
+        uint32_t c = 0;
+        auto publish = [&](uint32_t info, uint32_t base, uint32_t lo, uint32_t hi,
+                           const uint2* src, uint32_t bytes) {
+            const uint32_t slot = c % NSLOT;
+            if (c >= static_cast<uint32_t>(NSLOT))
+                mbar_wait_sleep(&S.empty[slot], ((c / NSLOT) - 1) & 1u);
+            if (ln == 0) {
+                S.meta[slot] = SlotMeta{info, base, lo, hi};
+                if (bytes) {
+                    mbar_expect_tx(&S.full[slot], bytes);
+                    bulk_g2s_hint(ring + static_cast<size_t>(slot) * SLOT_E, src, bytes,
+                                  &S.full[slot], pol);
+                } else {
+                    mbar_arrive(&S.full[slot]);
+                }
+            }
+            __syncwarp();
+            ++c;
+        };
+        for (uint32_t p = blockIdx.x; p < nprob; p += gridDim.x) {
+            const DecodeProblem& P = probs[p];
+            const SessionDev& sd = *P.s;
+            const uint32_t N = P.N;
+            const uint32_t ntile = div_up(N, TILE);
+            uint32_t nl = 0;
+            if (P.mode & MODE_SEARCH) {
+                nl = __ldcg(&plans[p].nl);
+                for (uint32_t l = ln; l < nl; l += 32) S.plist[l] = __ldcg(plans[p].lists + l);
+                __syncwarp();
+            }
+            const uint32_t last_blk = (N - 1) >> KEY_BLOCK_SHIFT;
+            const uint32_t* const blk_off = sd.blk_off;
+            const uint32_t* const n_used = sd.n_used;
+            const uint2* const ent = sd.ent;
+            const uint32_t nb_stride = sd.nb_stride, cap2 = sd.cap2;
+            // first table position of tile `tile` in list l (lanes l and l+32);
+            // tile t+2's bounds are loaded while tile t is published
+            auto bound = [&](uint32_t tile, uint32_t l) -> uint32_t {
+                if (l >= nl) return 0u;
+                const uint32_t t = S.plist[l];
+                const uint32_t kb = tile * TILE_BLKS;
+                return kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
+                                      : __ldcg(n_used + t);
+            };
+            uint32_t a0 = bound(0, ln), a1 = bound(0, ln + 32);
+            uint32_t b0 = bound(1, ln), b1 = bound(1, ln + 32);
+            for (uint32_t tile = 0; tile < ntile; ++tile) {
+                const uint32_t tflag = F_TILE_END | (tile + 1 == ntile ? F_PROB_END : 0u);
+                if (nl == 0) {  // cached scores: one data-less chunk per tile
+                    publish(CACHE_LIST | ((F_LIST_END | tflag) << 7) | (tile << 10), 0, 0, 0,
+                            nullptr, 0);
+                    continue;
+                }
+                const uint32_t c0 = bound(tile + 2, ln), c1 = bound(tile + 2, ln + 32);
+                for (uint32_t l = 0; l < nl; ++l) {
+                    const uint32_t e0 = __shfl_sync(0xffffffffu, l < 32 ? a0 : a1, l & 31);
+                    const uint32_t e1 = __shfl_sync(0xffffffffu, l < 32 ? b0 : b1, l & 31);
+                    const uint32_t lflag = F_LIST_END | (l + 1 == nl ? tflag : 0u);
+                    const uint2* tbl = ent + static_cast<size_t>(S.plist[l]) * cap2;
+                    if (e0 == e1) {  // nothing in this tile: only the flags travel
+                        publish(l | (lflag << 7) | (tile << 10), 0, 0, 0, nullptr, 0);
+                        continue;
+                    }
+                    uint32_t pos = e0;
+                    for (;;) {
+                        const uint32_t ab = pos & ~1u;
+                        const uint32_t pe = min(e1, ab + SLOT_E);
+                        const uint32_t ae = (pe + 1) & ~1u;  // <= cap2 (even)
+                        const bool last = pe == e1;
+                        publish(l | ((last ? lflag : 0u) << 7) | (tile << 10), ab, pos, pe,
+                                tbl + ab, (ae - ab) * 8u);
+                        if (last) break;
+                        pos = pe;
+                    }
+                }
+                a0 = b0;
+                a1 = b1;
+                b0 = c0;
+                b1 = c1;
+            }
         }
+        return;
     }
-    __syncthreads();
-    Keys kv{keys, nloc};
-    phase(4);
-    select_threshold(cl, S, V, kv, k0, need, pcnt, pmax, pmin);
-    phase(5);
-    const unsigned long long tk = S.b_tk;
-    const uint32_t tx = S.b_tx;
 
-    // ---- 4: emit the selected set in ascending order (+ newest-first padding) ----
-    // Warp w owns keys [w*span, (w+1)*span), 32 at a time: ballots give each
-    // key's rank among the selected / untaken keys, so index writes coalesce.
-    const int w = tid >> 5, ln = tid & 31;
-    const uint32_t span = div_up(div_up(nloc, SEL_WARPS), 32) * 32;
-    const uint32_t wb = min(nloc, w * span), we = min(nloc, wb + span);
-    auto picked = [&](uint32_t l) {
-        const uint32_t i = k0 + l;
-        const unsigned long long k = keys[l];
-        return i >= f_lo || (k && (k > tk || (k == tk && i < tx)));
-    };
-    uint32_t wsel = 0, wunt = 0;
-    for (uint32_t g = wb; g < we; g += 32) {
-        const uint32_t l = g + ln;
-        const bool in = l < we;
-        const unsigned ms = __ballot_sync(0xffffffffu, in && picked(l));
-        const unsigned mu = __ballot_sync(0xffffffffu, in) & ~ms;
-        wsel += __popc(ms);
-        wunt += __popc(mu);
-    }
-    if (ln == 0) {
-        S.r32a[w] = wsel;
-        S.r32b[w] = wunt;
-    }
-    __syncthreads();
-    uint32_t esel = 0, eunt = 0, tsel = 0, tunt = 0;
+    // ======================= consumer warps =======================
+    uint32_t p = blockIdx.x;
+    if (p >= nprob) return;
+    ProbState st;
+    setup_problem(S, probs, plans, p, st);
+    // warp w logs into its own region (it owns 1/16 of every tile's keys)
+    uint32_t wlog_n = 0;
+    uint32_t* const wlog_idx = log_idx + static_cast<size_t>(wid) * (log_cap / SEL_CW);
+    double* const wlog_sc = log_sc + static_cast<size_t>(wid) * (log_cap / SEL_CW);
+    uint16_t* const wcidx = cidx + wid * WKEYS;
+    double* const wacc = acc + wid * WKEYS;
+    uint32_t c = 0;
+    while (p < nprob) {
+        const uint32_t slot = c % NSLOT;
+        mbar_wait_sleep(&S.full[slot], (c / NSLOT) & 1u);
+        const SlotMeta M = S.meta[slot];
+        const uint32_t list = M.info & 127u, flags = (M.info >> 7) & 7u, tile = M.info >> 10;
+        const uint32_t kbase = tile * TILE;
+        if (list != CACHE_LIST) {
+            if (M.hi > M.lo) {
+                // this warp's equal share of the chunk's entry pairs
+                const uint32_t qa = (M.lo - M.base) >> 1, qb = (M.hi - M.base + 1) >> 1;
+                const uint32_t np = qb - qa;
+                const uint32_t q0 = qa + (np * wid) / SEL_CW, q1 = qa + (np * (wid + 1)) / SEL_CW;
+                const uint4* st4 = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * SLOT_E);
+                const double w = S.cw[list];
+                const uint32_t plo = M.lo - M.base, phi = M.hi - M.base;  // valid [plo, phi)
+                // two pairs (four entries) per lane per step, all loads issued
+                // before the adds: keys are unique within a list, so the four
+                // read-modify-writes are independent
+                for (uint32_t q = q0 + ln; q < q1; q += 64) {
+                    const bool h2 = q + 32 < q1;
+                    const uint4 e = st4[q];
+                    const uint4 f = h2 ? st4[q + 32] : make_uint4(TOMB, 0, TOMB, 0);
+                    const bool v0 = 2 * q >= plo && !(e.x & TOMB);
+                    const bool v1 = 2 * q + 1 < phi && !(e.z & TOMB);
+                    const bool v2 = !(f.x & TOMB);
+                    const bool v3 = 2 * q + 65 < phi && !(f.z & TOMB);
+                    double* const a0 = acc + ((v0 ? e.x : kbase) - kbase);
+                    double* const a1 = acc + ((v1 ? e.z : kbase) - kbase);
+                    double* const a2 = acc + ((v2 ? f.x : kbase) - kbase);
+                    double* const a3 = acc + ((v3 ? f.z : kbase) - kbase);
+                    const double o0 = *a0, o1 = *a1, o2 = *a2, o3 = *a3;
+                    double x0 = static_cast<double>(__uint_as_float(e.y));
+                    double x1 = static_cast<double>(__uint_as_float(e.w));
+                    double x2 = static_cast<double>(__uint_as_float(f.y));
+                    double x3 = static_cast<double>(__uint_as_float(f.w));
+                    if (w != 1.0) {  // w * double(s) (exact when w == 1)
+                        x0 = __dmul_rn(w, x0);
+                        x1 = __dmul_rn(w, x1);
+                        x2 = __dmul_rn(w, x2);
+                        x3 = __dmul_rn(w, x3);
+                    }
+                    if (v0) *a0 = __dadd_rn(o0, x0);
+                    if (v1) *a1 = __dadd_rn(o1, x1);
+                    if (v2) *a2 = __dadd_rn(o2, x2);
+                    if (v3) *a3 = __dadd_rn(o3, x3);
+                }
+            }
+        } else {  // cached candidate scores (search_period > 1): this warp's keys
+            for (uint32_t u = 0; u < WKEYS / 32; ++u) {
+                const uint32_t li = wid * WKEYS + u * 32 + ln, i = kbase + li;
+                if (i >= st.N) continue;
+                double v = neg0_d();
+                if (st.cache && i < st.n_cache) {
+                    v = __ldcg(st.cache + i);
+                    if (is_absent(v)) v = neg0_d();
+                }
+                acc[li] = v;
+            }
+        }
+        __syncwarp();
+        if (ln == 0) mbar_arrive(&S.empty[slot]);
+        ++c;
+        if (!(flags & F_LIST_END)) continue;
+        cbar();  // the list is fully accumulated before the next one (or the filter)
+        if (!(flags & F_TILE_END)) continue;
+
+        // ---- tile end: this warp's 512 keys -> pool candidates ----
+        {
+            const uint32_t N = st.N, need = st.need, wlo = st.wlo;
+            const double lo = st.lo, scale = st.scale;
+            const uint32_t cut = *reinterpret_cast<volatile uint32_t*>(&S.cut);
+            const double cut_lo = (cut > 1 && scale > 0.0)
+                                      ? lo + static_cast<double>(cut - 1) / scale
+                                      : -DBL_MAX;  // s < cut_lo  =>  bin(s) < cut
+            const uint32_t kw = kbase + wid * WKEYS;  // this warp's first key
+            const bool tile_win = kbase + TILE > wlo;  // holds window keys
+            double2* const a2 = reinterpret_cast<double2*>(wacc);
+            // pass 1: cheap compare, survivors compacted to the front of the
+            // warp's accumulator slice (positions never pass the read front)
+            uint32_t nadm = 0;
+            if (!tile_win && !st.store_cache) {
+                // common case: every key below the window, nothing cached —
+                // four keys per lane per step
+                if (need) {
+#pragma unroll 2
+                    for (uint32_t u = 0; u < WKEYS / 128; ++u) {
+                        const uint32_t lp = u * 64 + ln;
+                        const double2 v = a2[lp], x = a2[lp + 32];
+                        const bool k0 = !is_neg0(v.x) && v.x >= cut_lo;
+                        const bool k1 = !is_neg0(v.y) && v.y >= cut_lo;
+                        const bool k2 = !is_neg0(x.x) && x.x >= cut_lo;
+                        const bool k3 = !is_neg0(x.y) && x.y >= cut_lo;
+                        const unsigned m0 = __ballot_sync(0xffffffffu, k0);
+                        const unsigned m1 = __ballot_sync(0xffffffffu, k1);
+                        const unsigned m2 = __ballot_sync(0xffffffffu, k2);
+                        const unsigned m3 = __ballot_sync(0xffffffffu, k3);
+                        if (m0 | m1 | m2 | m3) {
+                            const unsigned lt = (1u << ln) - 1u;
+                            const uint32_t n0 = __popc(m0), n1 = n0 + __popc(m1), n2 = n1 + __popc(m2);
+                            __syncwarp();  // every lane has read its keys
+                            if (k0) {
+                                const uint32_t pos = nadm + __popc(m0 & lt);
+                                wacc[pos] = v.x;
+                                wcidx[pos] = static_cast<uint16_t>(2 * lp);
+                            }
+                            if (k1) {
+                                const uint32_t pos = nadm + n0 + __popc(m1 & lt);
+                                wacc[pos] = v.y;
+                                wcidx[pos] = static_cast<uint16_t>(2 * lp + 1);
+                            }
+                            if (k2) {
+                                const uint32_t pos = nadm + n1 + __popc(m2 & lt);
+                                wacc[pos] = x.x;
+                                wcidx[pos] = static_cast<uint16_t>(2 * lp + 64);
+                            }
+                            if (k3) {
+                                const uint32_t pos = nadm + n2 + __popc(m3 & lt);
+                                wacc[pos] = x.y;
+                                wcidx[pos] = static_cast<uint16_t>(2 * lp + 65);
+                            }
+                            nadm += n2 + __popc(m3);
+                        }
+                    }
+                }
+            } else {
+    #pragma unroll 2
+                for (uint32_t u = 0; u < WKEYS / 64; ++u) {
+                    const uint32_t lp = u * 32 + ln;
+                    const uint32_t i0 = kw + 2 * lp;
+                    const double2 v = a2[lp];
+                    double s0 = v.x, s1 = v.y;
+                    const bool p0 = !is_neg0(s0), p1 = !is_neg0(s1);  // gathered
+                    if (st.store_cache) {
+                        if (i0 < N) st.cache[i0] = p0 ? s0 : absent_d();
+                        if (i0 + 1 < N) st.cache[i0 + 1] = p1 ? s1 : absent_d();
+                    }
+                    bool in0 = p0, in1 = p1;
+                    if (tile_win) {  // window: passthrough keeps them out of the pool;
+                                     // otherwise they compete, at 0 when absent
+                        if (i0 >= wlo) {
+                            in0 = !st.pt && i0 < N;
+                            s0 = p0 ? s0 : 0.0;
+                        }
+                        if (i0 + 1 >= wlo) {
+                            in1 = !st.pt && i0 + 1 < N;
+                            s1 = p1 ? s1 : 0.0;
+                        }
+                    }
+                    const bool k0 = need && in0 && s0 >= cut_lo, k1 = need && in1 && s1 >= cut_lo;
+                    const unsigned m0 = __ballot_sync(0xffffffffu, k0);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, k1);
+                    if (m0 | m1) {
+                        const unsigned lt = (1u << ln) - 1u;
+                        const uint32_t n0 = __popc(m0);
+                        __syncwarp();  // every lane has read its pair
+                        if (k0) {
+                            const uint32_t pos = nadm + __popc(m0 & lt);
+                            wacc[pos] = s0;
+                            wcidx[pos] = static_cast<uint16_t>(2 * lp);
+                        }
+                        if (k1) {
+                            const uint32_t pos = nadm + n0 + __popc(m1 & lt);
+                            wacc[pos] = s1;
+                            wcidx[pos] = static_cast<uint16_t>(2 * lp + 1);
+                        }
+                        nadm += n0 + __popc(m1);
+                    }
+                }
+            }
+            __syncwarp();
+            // pass 2: bin the survivors, count and log those at or above the cut
+            for (uint32_t j0 = 0; j0 < nadm; j0 += 32) {
+                const uint32_t j = j0 + ln;
+                bool a = false;
+                uint32_t b = 0;
+                double sc = 0.0;
+                uint32_t off = 0;
+                if (j < nadm) {
+                    sc = wacc[j];
+                    off = wcidx[j];
+                    b = bin_of(sc, lo, scale);
+                    a = b >= cut;
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, a);
+                if (a) {
+                    const uint32_t pos = wlog_n + __popc(m & ((1u << ln) - 1u));
+                    wlog_idx[pos] = kw + off;
+                    wlog_sc[pos] = sc;
+                    atomicAdd(&hist[b], 1u);
+                    atomicAdd(&coarse[b >> 5], 1u);
+                }
+                wlog_n += __popc(m);
+            }
+            __syncwarp();
 #pragma unroll
-    for (int i = 0; i < SEL_WARPS; ++i) {
-        if (i < w) {
-            esel += S.r32a[i];
-            eunt += S.r32b[i];
+            for (uint32_t u = 0; u < WKEYS / 64; ++u)
+                a2[u * 32 + ln] = make_double2(neg0_d(), neg0_d());
+            // raise the cut (stale counts only under-estimate: still safe)
+            if (need && (tile % SEL_CW) == static_cast<uint32_t>(wid)) {
+                uint32_t ab;
+                const int b = warp_find_bin(hist, coarse, need, ab);
+                if (ln == 0 && b > static_cast<int>(*reinterpret_cast<volatile uint32_t*>(&S.cut)))
+                    atomicMax(&S.cut, static_cast<uint32_t>(b));
+            }
         }
-        tsel += S.r32a[i];
-        tunt += S.r32b[i];
+        cbar();  // accumulator clear before the next tile's first list
+        if (!(flags & F_PROB_END)) continue;
+
+        // ======================= final selection =======================
+        {
+            const uint32_t N = st.N, K = st.K, need = st.need, f_lo = st.f_lo;
+            const double lo = st.lo, scale = st.scale;
+            unsigned long long* const prof = st.prof;
+            uint32_t* const sel = st.sel;
+            uint32_t* const rep = st.rep;
+            if (ln == 0) S.wlog[wid] = wlog_n;
+            cbar();  // every warp has logged its keys
+            if (tid == 0) {  // exclusive prefix of the per-warp log lengths
+                uint32_t run = 0;
+                for (int w = 0; w <= SEL_CW; ++w) {
+                    const uint32_t x = w < SEL_CW ? S.wlog[w] : 0u;
+                    S.wlog[w] = run;
+                    run += x;
+                }
+            }
+            if (prof && tid == 0) prof[1] = gtimer();
+            const uint32_t nw = div_up(N, 32);
+            if (tid < 32) {
+                uint32_t ab = 0;
+                int b = -1;
+                if (need) b = warp_find_bin(hist, coarse, need, ab);
+                if (tid == 0) {
+                    // b < 0: fewer than `need` pool keys (then the cut never rose
+                    // and the log holds the whole pool): take them all
+                    S.f_take_all = (need && b < 0) ? 1u : 0u;
+                    S.f_bin = b < 0 ? 0u : static_cast<uint32_t>(b);
+                    S.f_above = ab;
+                    S.f_count = b < 0 ? 0u : hist[b];
+                }
+            }
+            for (uint32_t x = tid; x < nw; x += SEL_CT) bm[x] = 0;
+            cbar();
+            const uint32_t take_all = S.f_take_all, dsel = S.f_bin;
+            const uint32_t rem = need - (take_all ? 0u : min(need, S.f_above));
+            const uint32_t nlog = S.wlog[SEL_CW];
+            const uint32_t wstride = log_cap / SEL_CW;
+            // flat log index -> slot in the per-warp regions (search from `w`,
+            // indices visited by one thread only grow)
+            auto lpos = [&](uint32_t e, uint32_t& w) {
+                while (S.wlog[w + 1] <= e) ++w;
+                return w * wstride + (e - S.wlog[w]);
+            };
+            if (need) {
+                constexpr int LOGU = 8;  // entries per thread in flight (the log lives in L2)
+                uint32_t w = 0;
+                for (uint32_t e0 = tid; e0 < nlog; e0 += SEL_CT * LOGU) {
+                    uint32_t ii[LOGU];
+                    double sv[LOGU];
+#pragma unroll
+                    for (int u = 0; u < LOGU; ++u) {
+                        const uint32_t e = e0 + u * SEL_CT;
+                        const uint32_t x = e < nlog ? lpos(e, w) : 0u;
+                        ii[u] = e < nlog ? __ldcg(log_idx + x) : 0u;
+                        sv[u] = e < nlog ? __ldcg(log_sc + x) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < LOGU; ++u) {
+                        if (e0 + u * SEL_CT >= nlog) break;
+                        const uint32_t b = bin_of(sv[u], lo, scale);
+                        if (take_all || b > dsel) {
+                            set_bit(bm, ii[u]);
+                        } else if (b == dsel) {
+                            const uint32_t k = atomicAdd(&S.nbkt, 1u);
+                            if (k < static_cast<uint32_t>(BKT)) {
+                                bkey[k] = ordkey(sv[u]);
+                                bidx[k] = ii[u];
+                            }
+                        }
+                    }
+                }
+            }
+            cbar();
+            const uint32_t nb = S.nbkt;
+            if (need && !take_all && rem) {
+                if (nb <= static_cast<uint32_t>(RANK_DIRECT)) {
+                    // direct ranking: member e is selected iff fewer than rem beat it
+                    for (uint32_t e = tid; e < nb; e += SEL_CT) {
+                        const unsigned long long ke = bkey[e];
+                        const uint32_t ie = bidx[e];
+                        uint32_t r = 0;
+                        for (uint32_t f = 0; f < nb; ++f) {
+                            const unsigned long long kf = bkey[f];
+                            r += (kf > ke) || (kf == ke && bidx[f] < ie);
+                        }
+                        if (r < rem) set_bit(bm, ie);
+                    }
+                } else if (nb <= static_cast<uint32_t>(BKT)) {
+                    radix_kth(S, hist, nb, rem, [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+                        k = bkey[e];
+                        ix = bidx[e];
+                        return true;
+                    });
+                    const unsigned long long tk = S.tk;
+                    const uint32_t tx = S.tx;
+                    for (uint32_t e = tid; e < nb; e += SEL_CT) {
+                        const unsigned long long k = bkey[e];
+                        if (k > tk || (k == tk && bidx[e] < tx)) set_bit(bm, bidx[e]);
+                    }
+                } else {  // huge threshold bin: rank straight from the log
+                    auto member = [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+                        uint32_t w = 0;
+                        const uint32_t x = lpos(e, w);
+                        const double s = __ldcg(log_sc + x);
+                        if (bin_of(s, lo, scale) != dsel) return false;
+                        k = ordkey(s);
+                        ix = __ldcg(log_idx + x);
+                        return true;
+                    };
+                    radix_kth(S, hist, nlog, rem, member);
+                    const unsigned long long tk = S.tk;
+                    const uint32_t tx = S.tx;
+                    for (uint32_t e = tid; e < nlog; e += SEL_CT) {
+                        unsigned long long k;
+                        uint32_t ix;
+                        if (member(e, k, ix) && (k > tk || (k == tk && ix < tx))) set_bit(bm, ix);
+                    }
+                }
+            }
+            // window passthrough (or the newest K when K <= R)
+            for (uint32_t i = f_lo + tid; i < N; i += SEL_CT) set_bit(bm, i);
+            cbar();
+            // ---- count, newest-first padding, ascending emit ----
+            const uint32_t wpt = div_up(nw, SEL_CT);
+            const uint32_t w0 = min(nw, tid * wpt), w1 = min(nw, w0 + wpt);
+            auto valid = [&](uint32_t x) {
+                return x + 1 < nw || (N & 31) == 0 ? 0xffffffffu : ((1u << (N & 31)) - 1u);
+            };
+            uint32_t cnt = 0, zeros = 0;
+            for (uint32_t x = w0; x < w1; ++x) {
+                const uint32_t b = bm[x];
+                cnt += __popc(b);
+                zeros += __popc(~b & valid(x));
+            }
+            uint32_t total;
+            cscan(S, cnt, total);
+            if (total < K) {  // pad with the newest untaken keys (retrieval.cpp:218-225)
+                const uint32_t pad = K - total;
+                uint32_t zt;
+                const uint32_t zbelow = cscan(S, zeros, zt);
+                const uint32_t zabove = zt - zbelow - zeros;  // zeros in higher threads
+                uint32_t take = pad > zabove ? min(pad - zabove, zeros) : 0u;
+                for (uint32_t x = w1; x > w0 && take;) {
+                    --x;
+                    uint32_t z = ~bm[x] & valid(x);
+                    while (z && take) {
+                        const int hb = 31 - __clz(z);
+                        bm[x] |= 1u << hb;
+                        z &= ~(1u << hb);
+                        --take;
+                        ++cnt;
+                    }
+                }
+            }
+            const uint32_t at = cscan(S, cnt, total);
+            {
+                uint32_t pos = at;
+                for (uint32_t x = w0; x < w1; ++x) {
+                    uint32_t b = bm[x];
+                    while (b) {
+                        const int lb = __ffs(b) - 1;
+                        sel[pos++] = x * 32 + lb;
+                        b &= b - 1;
+                    }
+                }
+            }
+            if (tid == 0) {
+                reinterpret_cast<DecodeReport*>(rep)->k = K;
+                if (prof) {
+                    prof[2] = gtimer();
+                    prof[3] = nlog;
+                    prof[4] = nb;
+                    prof[5] = static_cast<unsigned long long>(__double_as_longlong(lo));
+                    prof[6] = static_cast<unsigned long long>(
+                        __double_as_longlong(scale > 0.0 ? lo + NB / scale : lo));
+                    prof[7] = S.f_take_all | (dsel << 1);
+                }
+            }
+            cbar();  // bitmap emitted, scratch free
+            // ---- reset for the next problem ----
+            for (uint32_t x = tid; x < div_up(nw, 2); x += SEL_CT) acc[x] = neg0_d();
+            for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) hist[x] = 0;
+            if (tid == 0) {
+                S.cut = 0;
+                S.nbkt = 0;
+            }
+            wlog_n = 0;
+            p += gridDim.x;
+            if (p < nprob) setup_problem(S, probs, plans, p, st);  // ends with a barrier
+            else cbar();
+        }
     }
-    if (tid == 0) {
-        S.x_nsel = tsel;
-        S.x_nunt = tunt;
-    }
-    cl.sync();
-    if (tid < 32) {
-        // per-CTA padding share and output base, one lane per cluster rank
-        const uint32_t ns = ln < cs ? *remote(cl, &S.x_nsel, ln) : 0;
-        const uint32_t nu = ln < cs ? *remote(cl, &S.x_nunt, ln) : 0;
-        const uint32_t all_sel = warp_sum(ns);
-        uint32_t suf = nu;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_down_sync(0xffffffffu, suf, o);
-            if (ln + o < 32) suf += x;
-        }
-        const uint32_t above = suf - nu;
-        const uint32_t pad = K > all_sel ? K - all_sel : 0;
-        const uint32_t tk_l = pad > above ? min(pad - above, nu) : 0;
-        const uint32_t cnt = ns + tk_l;
-        uint32_t inc = cnt;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-            if (ln >= o) inc += x;
-        }
-        if (ln == rank) {
-            S.b_base = inc - cnt;
-            S.b_take = tk_l;
-        }
-    }
-    __syncthreads();
-    {
-        // padded keys: the `take` highest-index untaken keys of this CTA
-        const uint32_t pad_from = tunt - S.b_take;  // untaken rank >= pad_from is padded
-        uint32_t pos = S.b_base + esel + (eunt > pad_from ? eunt - pad_from : 0);
-        uint32_t u = eunt;
-        const unsigned lt = (1u << ln) - 1u;
-        for (uint32_t g = wb; g < we; g += 32) {
-            const uint32_t l = g + ln;
-            const bool in = l < we;
-            const bool ps = in && picked(l);
-            const unsigned mu = __ballot_sync(0xffffffffu, in && !ps);
-            const uint32_t urank = u + __popc(mu & lt);  // this key's untaken rank
-            const bool out = ps || (in && !ps && urank >= pad_from);
-            const unsigned mo = __ballot_sync(0xffffffffu, out);
-            if (out) P.sel[pos + __popc(mo & lt)] = k0 + l;
-            pos += __popc(mo);
-            u += __popc(mu);
-        }
-    }
-    if (leader && tid == 0) reinterpret_cast<DecodeReport*>(P.rep)->k = K;
-    phase(6);
-    cl.sync();  // nobody exits while a peer may still read its shared memory
 }
 
-size_t select_smem_bytes(uint32_t kpc) {
-    return ((sizeof(SelHdr) + 127) & ~size_t(127)) + REGION_BYTES +
-           static_cast<size_t>(kpc) * sizeof(double);
+static size_t select_smem() {
+    return ((sizeof(SelHdr) + 127) & ~size_t(127)) + TILE * 8 + (NB + NCB) * 4 + BKT * 12 +
+           SEL_CW * WKEYS * 2 + static_cast<size_t>(NSLOT) * SLOT_E * 8;
+}
+
+uint32_t select_grid(uint32_t nprob, int num_sms) {
+    const uint32_t g = static_cast<uint32_t>(num_sms > 0 ? num_sms : 1);
+    return nprob < g ? nprob : g;
 }
 
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
-                          uint32_t kpc, uint32_t cs, cudaStream_t st) {
-    const size_t smem = select_smem_bytes(kpc);
+                          uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
+                          cudaStream_t st) {
+    const size_t smem = select_smem();
     cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    if (cs > 8) {
-        e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nprob * cs, 1, 1);
-    cfg.blockDim = dim3(SEL_THREADS, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, select_kernel, probs, plans, kpc);
+    select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap);
+    return cudaGetLastError();
 }
 
 }  // namespace csa
