@@ -209,6 +209,10 @@ csattn_status csattn_session_import(csattn_ctx ctx, const float* centroids, uint
 csattn_status csattn_session_export(csattn_session s, uint32_t* lens, uint32_t* indices,
                                     float* scores, uint64_t stride, float* centroids);
 
+/* The per-subspace unit centroids (CsIndex::centroid_sets, index.hpp:46-68),
+ * packed per subspace as for csattn_prefill_from_centroids: C*d floats, host. */
+csattn_status csattn_session_centroids(csattn_session s, float* centroids);
+
 /* Independent copy (Session is a value type, session.hpp:19-31): tables are
  * copied, the immutable prefill KV rows are shared. */
 csattn_status csattn_session_fork(csattn_session src, uint64_t max_decode_steps,

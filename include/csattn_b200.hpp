@@ -1,0 +1,571 @@
+// csattn_b200.hpp — C++ drop-in facade of the B200 decode hot path.
+//
+// Mirrors the reference API in proj/include/csattn/ (same type names, field
+// names, function names and exception classes) on top of the C ABI in
+// csattn_b200.h, so reference call sites compile against it with
+//
+//     namespace csattn = csattn_b200;
+//
+// Covered (the hot path):
+//   errors.hpp:8-52        Error, DimensionError, ParameterError, DataError (+4),
+//                          PropertyError, StreamExhaustedError
+//   core.hpp:23-39         SubspaceLayout (uniform, dim, count, slice)
+//   core.hpp:74-79         AttentionOutput
+//   clustering.hpp:17-28   ClusterConfig
+//   index.hpp:19-42        TopList (host image), IndexConfig
+//   index.hpp:46-68        CsIndex (host image: export of the device tables)
+//   retrieval.hpp:17-38    RetrievalConfig (incl. k_bump), parse_schedule, keep_count
+//   metrics.hpp:15-37      CostCounters
+//   metrics.cpp:32-38      h2d_bytes
+//   session.hpp:19-66      Session, DecodeStepReport, prefill, decode_step, run_decode
+// Differences a caller can observe (documented in INTEGRATION.md):
+//   * Session owns device state; `index` is materialised on demand by
+//     Session::export_index() instead of being a public value member, and
+//     KvStore rows live in HBM (Session::read_kv()).
+//   * decode_step's compare_dense runs the dense oracle on the GPU
+//     (csattn_dense_attention); recall/l2 are computed on the host from it.
+//   * k_bump is honoured: the callback's input (worst best-cosine of the
+//     step's own routing) is evaluated on the host from the exported
+//     centroids before the step is launched, exactly as decode_search
+//     (retrieval.cpp:259-265) feeds it.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdint>
+#include <functional>
+#include <limits>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "csattn_b200.h"
+
+namespace csattn_b200 {
+
+// ---- errors.hpp:8-52 ----
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct DimensionError : Error {
+    using Error::Error;
+};
+struct ParameterError : Error {
+    using Error::Error;
+};
+struct DataError : Error {
+    using Error::Error;
+};
+struct BadMagicError : DataError {
+    using DataError::DataError;
+};
+struct VersionError : DataError {
+    using DataError::DataError;
+};
+struct TruncatedError : DataError {
+    using DataError::DataError;
+};
+struct CorruptError : DataError {
+    using DataError::DataError;
+};
+struct PropertyError : Error {
+    using Error::Error;
+};
+struct StreamExhaustedError : Error {
+    using Error::Error;
+};
+// B200-only failure classes (no reference counterpart)
+struct CudaError : Error {
+    using Error::Error;
+};
+struct CapacityError : ParameterError {
+    using ParameterError::ParameterError;
+};
+
+// status -> the same exception class and message the reference throws
+inline void check(csattn_status s) {
+    if (s == CSATTN_OK) return;
+    const std::string m = csattn_last_error();
+    switch (s) {
+        case CSATTN_ERR_DIMENSION: throw DimensionError(m);
+        case CSATTN_ERR_PARAMETER: throw ParameterError(m);
+        case CSATTN_ERR_DATA: throw DataError(m);
+        case CSATTN_ERR_BAD_MAGIC: throw BadMagicError(m);
+        case CSATTN_ERR_VERSION: throw VersionError(m);
+        case CSATTN_ERR_TRUNCATED: throw TruncatedError(m);
+        case CSATTN_ERR_CORRUPT: throw CorruptError(m);
+        case CSATTN_ERR_PROPERTY: throw PropertyError(m);
+        case CSATTN_ERR_STREAM_EXHAUSTED: throw StreamExhaustedError(m);
+        case CSATTN_ERR_CUDA: throw CudaError(m);
+        case CSATTN_ERR_CAPACITY: throw CapacityError(m);
+        default: throw Error(m);
+    }
+}
+
+using HeadVector = std::vector<float>;
+
+// ---- core.hpp:23-39 / core.cpp:35-50 ----
+struct SubspaceLayout {
+    std::vector<std::size_t> sizes;
+    std::vector<std::size_t> offsets;
+
+    SubspaceLayout() = default;
+    explicit SubspaceLayout(std::vector<std::size_t> subspace_sizes) : sizes(std::move(subspace_sizes)) {
+        if (sizes.empty()) throw ParameterError("subspace layout needs m >= 1");
+        std::size_t off = 0;
+        for (std::size_t b = 0; b < sizes.size(); ++b) {
+            if (sizes[b] == 0)
+                throw ParameterError("subspace width must be >= 1 (subspace " + std::to_string(b) + ")");
+            offsets.push_back(off);
+            off += sizes[b];
+        }
+    }
+    static SubspaceLayout uniform(std::size_t dim, std::size_t subspaces) {
+        if (subspaces == 0 || subspaces > dim)
+            throw ParameterError("uniform layout needs 1 <= m <= d");
+        std::vector<std::size_t> s(subspaces, dim / subspaces);
+        for (std::size_t b = 0; b < dim % subspaces; ++b) s[b] += 1;
+        return SubspaceLayout(std::move(s));
+    }
+    std::size_t dim() const {
+        std::size_t d = 0;
+        for (std::size_t x : sizes) d += x;
+        return d;
+    }
+    std::size_t count() const { return sizes.size(); }
+    std::span<const float> slice(std::span<const float> v, std::size_t b) const {
+        return v.subspan(offsets[b], sizes[b]);
+    }
+};
+
+// ---- core.hpp:74-79 ----
+struct AttentionOutput {
+    std::vector<float> weights;
+    HeadVector output;
+};
+
+// ---- clustering.hpp:17-28, index.hpp:19-68 ----
+struct ClusterConfig {
+    std::size_t centroids = 64;
+    std::size_t iterations = 10;
+    std::size_t batch_size = 0;
+    std::uint64_t seed = 0;
+    double tolerance = 1e-7;
+};
+
+struct IndexConfig {
+    double alpha = 0.2;
+    std::size_t list_capacity = 0;
+    bool normalize_keys = false;
+    int score_bits = 16;
+    ClusterConfig cluster;
+
+    csattn_index_config c() const {
+        csattn_index_config x{};
+        x.alpha = alpha;
+        x.list_capacity = list_capacity;
+        x.normalize_keys = normalize_keys ? 1 : 0;
+        x.score_bits = score_bits;
+        x.centroids = cluster.centroids;
+        x.iterations = cluster.iterations;
+        x.batch_size = cluster.batch_size;
+        x.seed = cluster.seed;
+        x.tolerance = cluster.tolerance;
+        return x;
+    }
+};
+
+struct TopList {
+    std::uint32_t capacity = 0;
+    std::vector<std::uint32_t> indices;  // score desc, index asc
+    std::vector<float> scores;
+    bool full() const { return indices.size() >= capacity; }
+    float min_score() const {
+        return scores.empty() ? -std::numeric_limits<float>::infinity() : scores.back();
+    }
+};
+
+struct CentroidSet {
+    std::size_t subspace_id = 0;
+    std::vector<float> centroids;  // count x dim, unit rows
+    std::size_t count = 0;
+    std::size_t dim = 0;
+};
+
+// Host image of the device tables (Session::export_index).
+struct CsIndex {
+    SubspaceLayout layout;
+    std::vector<CentroidSet> centroid_sets;
+    std::vector<TopList> tables;  // m x C, subspace-major
+    double alpha = 0.0;
+    std::uint32_t list_capacity = 0;
+    std::uint64_t prefill_len = 0;
+    bool normalize_keys = false;
+    int score_bits = 16;
+
+    explicit CsIndex(SubspaceLayout l) : layout(std::move(l)) {}
+    std::size_t subspaces() const { return layout.count(); }
+    std::size_t centroids_per_subspace() const {
+        return centroid_sets.empty() ? 0 : centroid_sets[0].count;
+    }
+    TopList& table(std::size_t b, std::size_t j) { return tables[b * centroids_per_subspace() + j]; }
+    const TopList& table(std::size_t b, std::size_t j) const {
+        return tables[b * centroids_per_subspace() + j];
+    }
+};
+
+// ---- retrieval.hpp:17-38 ----
+struct RetrievalConfig {
+    double keep_ratio = 0.05;
+    std::size_t search_period = 1;
+    std::size_t recent_window = 32;
+    std::vector<double> weights;
+    std::size_t backoff_tau = 1;
+    double backoff_threshold = -std::numeric_limits<double>::infinity();
+    bool recent_passthrough = true;
+    std::function<std::size_t(std::size_t, double)> k_bump;
+
+    csattn_retrieval_config c() const {
+        csattn_retrieval_config x{};
+        x.keep_ratio = keep_ratio;
+        x.search_period = search_period;
+        x.recent_window = recent_window;
+        x.weights = weights.empty() ? nullptr : weights.data();
+        x.n_weights = weights.size();
+        x.backoff_tau = backoff_tau;
+        x.backoff_threshold = backoff_threshold;
+        x.recent_passthrough = recent_passthrough ? 1 : 0;
+        return x;
+    }
+};
+
+inline std::size_t keep_count(double rho, std::size_t n) {
+    uint64_t k = 0;
+    check(csattn_keep_count(rho, n, &k));
+    return static_cast<std::size_t>(k);
+}
+
+inline std::pair<double, std::size_t> parse_schedule(const std::string& name) {
+    double rho = 0.0;
+    uint64_t period = 0;
+    check(csattn_parse_schedule(name.c_str(), &rho, &period));
+    return {rho, static_cast<std::size_t>(period)};
+}
+
+// ---- metrics.hpp:15-37, metrics.cpp:32-38 ----
+struct CostCounters {
+    std::size_t centroid_dot_ops = 0;
+    std::size_t gathered_entries = 0;
+    std::size_t reduce_ops = 0;
+    std::size_t attention_key_ops = 0;
+    double h2d_bytes_model = 0.0;
+    std::size_t searches = 0;
+    std::size_t inserts_attempted = 0;
+    std::size_t inserts_applied = 0;
+    std::size_t insert_dot_ops = 0;
+
+    void add(const CostCounters& o) {
+        centroid_dot_ops += o.centroid_dot_ops;
+        gathered_entries += o.gathered_entries;
+        reduce_ops += o.reduce_ops;
+        attention_key_ops += o.attention_key_ops;
+        h2d_bytes_model += o.h2d_bytes_model;
+        searches += o.searches;
+        inserts_attempted += o.inserts_attempted;
+        inserts_applied += o.inserts_applied;
+        insert_dot_ops += o.insert_dot_ops;
+    }
+};
+
+inline double h2d_bytes(double rho, std::size_t n, std::size_t d, std::size_t b, std::size_t period) {
+    double out = 0.0;
+    check(csattn_h2d_bytes(rho, n, d, b, period, &out));
+    return out;
+}
+
+// ---- one device + stream (no reference counterpart: the CPU path has none) ----
+class Context {
+   public:
+    explicit Context(int device = 0, void* cuda_stream = nullptr) {
+        check(csattn_ctx_create(device, cuda_stream, &h_));
+    }
+    ~Context() {
+        if (h_) csattn_ctx_destroy(h_);
+    }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+    csattn_ctx handle() const { return h_; }
+    uint64_t launches() const { return csattn_ctx_launch_count(h_); }
+    static Context& default_context() {
+        static Context c(0);
+        return c;
+    }
+
+   private:
+    csattn_ctx h_ = nullptr;
+};
+
+// ---- session.hpp:19-42 ----
+struct DecodeStepReport {
+    std::vector<std::uint32_t> selected;  // ascending, size K
+    std::size_t k = 0;
+    bool searched = false;
+    AttentionOutput attention;
+    std::optional<AttentionOutput> dense_reference;
+    std::optional<double> recall;
+    std::optional<double> l2_error;
+    CostCounters counters;
+};
+
+class Session {
+   public:
+    Session(csattn_session h, SubspaceLayout layout, RetrievalConfig cfg)
+        : cfg(std::move(cfg)), h_(h), layout_(std::move(layout)) {
+        csattn_session_info info{};
+        check(csattn_session_info_get(h_, &info));
+        dim_ = info.dim;
+    }
+    ~Session() {
+        if (h_) csattn_session_destroy(h_);
+    }
+    Session(Session&& o) noexcept
+        : cfg(std::move(o.cfg)), step(o.step), h2d_elem_bytes(o.h2d_elem_bytes), totals(o.totals),
+          h_(std::exchange(o.h_, nullptr)), layout_(std::move(o.layout_)),
+          centroids_(std::move(o.centroids_)), dim_(o.dim_) {}
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+
+    // Session is a value type in the reference: copy = fork the device tables.
+    Session fork(std::size_t max_decode_steps) const {
+        csattn_session out = nullptr;
+        check(csattn_session_fork(h_, max_decode_steps, &out));
+        Session s(out, layout_, cfg);
+        s.step = step;
+        s.totals = totals;
+        return s;
+    }
+
+    csattn_session handle() const { return h_; }
+    const SubspaceLayout& layout() const { return layout_; }
+    std::size_t dim() const { return dim_; }
+    csattn_session_info info() const {
+        csattn_session_info i{};
+        check(csattn_session_info_get(h_, &i));
+        return i;
+    }
+    std::size_t size() const { return info().context_len; }  // kv.size()
+
+    // CsIndex image of the current device tables (index.hpp:46-68)
+    CsIndex export_index() const {
+        const csattn_session_info in = info();
+        const std::size_t T = in.subspaces * in.centroids;
+        const std::size_t stride = std::max<std::size_t>(in.list_capacity, 1);
+        std::vector<uint32_t> lens(T), idx(T * stride);
+        std::vector<float> sc(T * stride), cent(in.centroids * in.dim);
+        check(csattn_session_export(h_, lens.data(), idx.data(), sc.data(), stride, cent.data()));
+        CsIndex ix(layout_);
+        ix.alpha = in.alpha;
+        ix.list_capacity = static_cast<uint32_t>(in.list_capacity);
+        ix.prefill_len = in.prefill_len;
+        ix.normalize_keys = in.normalize_keys != 0;
+        ix.score_bits = in.score_bits;
+        for (std::size_t b = 0; b < layout_.count(); ++b) {
+            CentroidSet cs;
+            cs.subspace_id = b;
+            cs.count = in.centroids;
+            cs.dim = layout_.sizes[b];
+            const float* src = cent.data() + in.centroids * layout_.offsets[b];
+            cs.centroids.assign(src, src + cs.count * cs.dim);
+            ix.centroid_sets.push_back(std::move(cs));
+        }
+        for (std::size_t t = 0; t < T; ++t) {
+            TopList l;
+            l.capacity = static_cast<uint32_t>(in.list_capacity);
+            l.indices.assign(idx.begin() + t * stride, idx.begin() + t * stride + lens[t]);
+            l.scores.assign(sc.begin() + t * stride, sc.begin() + t * stride + lens[t]);
+            ix.tables.push_back(std::move(l));
+        }
+        return ix;
+    }
+
+    // KvStore rows [first, first + count) (core.hpp:47-68)
+    void read_kv(std::size_t first, std::size_t count, std::vector<float>& keys,
+                 std::vector<float>& values) const {
+        keys.resize(count * dim_);
+        values.resize(count * dim_);
+        check(csattn_session_read_kv(h_, first, count, keys.data(), values.data()));
+    }
+
+    // select_centroids' worst best-cosine (retrieval.cpp:40-87) for k_bump:
+    // fp64 dots of the normalised query slice with the unit centroids.
+    double worst_best_cosine(std::span<const float> q) const {
+        const std::vector<float>& cent = centroids();
+        const std::size_t C = cent.size() / std::max<std::size_t>(dim_, 1);
+        double worst = 1.0;
+        for (std::size_t b = 0; b < layout_.count(); ++b) {
+            const std::size_t off = layout_.offsets[b], w = layout_.sizes[b];
+            double n2 = 0.0;
+            for (std::size_t t = 0; t < w; ++t) n2 += static_cast<double>(q[off + t]) * q[off + t];
+            if (n2 == 0.0) continue;  // zero slice: best cosine 1.0
+            const double inv = 1.0 / std::sqrt(n2);
+            std::vector<float> qn(w);
+            for (std::size_t t = 0; t < w; ++t) qn[t] = static_cast<float>(q[off + t] * inv);
+            double best = -std::numeric_limits<double>::infinity();
+            for (std::size_t j = 0; j < C; ++j) {
+                const float* c = cent.data() + C * off + j * w;
+                double s = 0.0;
+                for (std::size_t t = 0; t < w; ++t) s += static_cast<double>(qn[t]) * c[t];
+                best = std::max(best, s);
+            }
+            worst = std::min(worst, best);
+        }
+        return worst;
+    }
+
+    RetrievalConfig cfg;
+    std::size_t step = 0;
+    std::size_t h2d_elem_bytes = 2;
+    CostCounters totals;
+
+   private:
+    const std::vector<float>& centroids() const {  // immutable after the build
+        if (centroids_.empty()) {
+            const csattn_session_info in = info();
+            centroids_.resize(in.centroids * in.dim);
+            check(csattn_session_centroids(h_, centroids_.data()));
+        }
+        return centroids_;
+    }
+
+    csattn_session h_ = nullptr;
+    SubspaceLayout layout_;
+    mutable std::vector<float> centroids_;
+    std::size_t dim_ = 0;
+};
+
+// ---- session.hpp:44-66 ----
+// prefill (session.cpp:25-44): KvStore + build_index on the GPU. `group`
+// query heads may share the index (GQA): queries then hold their pooled rows.
+inline Session prefill(std::span<const float> queries, std::span<const float> keys,
+                       std::span<const float> values, const SubspaceLayout& layout,
+                       const IndexConfig& index_cfg, const RetrievalConfig& cfg,
+                       std::size_t max_decode_steps = 4096, std::size_t group = 1,
+                       Context& ctx = Context::default_context()) {
+    const std::size_t d = layout.dim();
+    if (queries.size() % d != 0 || keys.size() % d != 0 || values.size() % d != 0)
+        throw DimensionError("prefill rows are not a multiple of d");
+    if (queries.size() / d == 0) throw ParameterError("prefill must be non-empty");
+    if (keys.size() * group != queries.size() || values.size() != keys.size())
+        throw ParameterError("prefill query/key/value counts must be equal");
+    const std::size_t p = keys.size() / d;
+    std::vector<uint64_t> widths(layout.sizes.begin(), layout.sizes.end());
+    const csattn_index_config ic = index_cfg.c();
+    const csattn_retrieval_config rc = cfg.c();
+    csattn_session s = nullptr;
+    check(csattn_prefill(ctx.handle(), queries.data(), queries.size() / d, keys.data(), values.data(),
+                         p, d, widths.data(), widths.size(), &ic, &rc, group, max_decode_steps,
+                         CSATTN_HOST_BUFFERS, &s));
+    return Session(s, layout, cfg);
+}
+
+// decode_step (session.cpp:46-99) for a single-head session.
+inline DecodeStepReport decode_step(Session& session, std::span<const float> q,
+                                    std::span<const float> new_key,
+                                    std::span<const float> new_value, bool compare_dense) {
+    const std::size_t d = session.dim();
+    if (q.size() != d || new_key.size() != d || new_value.size() != d)
+        throw DimensionError("decode step inputs must have width d");
+    const std::size_t n = session.size();
+    uint64_t k_override = 0;
+    if (session.cfg.k_bump)
+        k_override = session.cfg.k_bump(keep_count(session.cfg.keep_ratio, n),
+                                         session.worst_best_cosine(q));
+    DecodeStepReport r;
+    std::vector<uint32_t> sel(n);
+    std::vector<float> out(d), w(n);
+    csattn_step_report rep{};
+    std::optional<AttentionOutput> dense;
+    if (compare_dense) {  // the dense oracle sees the same pre-append context
+        AttentionOutput full;
+        full.output.resize(d);
+        full.weights.resize(n);
+        check(csattn_dense_attention(session.handle(), q.data(), nullptr, 0, full.output.data(),
+                                     full.weights.data(), CSATTN_HOST_BUFFERS));
+        dense = std::move(full);
+    }
+    check(csattn_decode_step(session.handle(), q.data(), new_key.data(), new_value.data(),
+                             out.data(), sel.data(), w.data(), n, &rep,
+                             k_override ? &k_override : nullptr, CSATTN_HOST_BUFFERS));
+    r.k = rep.k;
+    r.searched = rep.searched != 0;
+    r.selected.assign(sel.begin(), sel.begin() + rep.k);
+    r.attention.output = std::move(out);
+    r.attention.weights.assign(w.begin(), w.begin() + rep.k);
+    r.counters.centroid_dot_ops = rep.centroid_dot_ops;
+    r.counters.gathered_entries = rep.gathered_entries;
+    r.counters.reduce_ops = rep.reduce_ops;
+    r.counters.attention_key_ops = rep.attention_key_ops;
+    r.counters.h2d_bytes_model =
+        h2d_bytes(session.cfg.keep_ratio, n, d, session.h2d_elem_bytes, session.cfg.search_period);
+    r.counters.searches = rep.searches;
+    r.counters.inserts_attempted = rep.inserts_attempted;
+    r.counters.inserts_applied = rep.inserts_applied;
+    r.counters.insert_dot_ops = rep.insert_dot_ops;
+    if (dense) {
+        // recall_at_k (metrics.cpp:9-30) against dense_topk (core.cpp:171-192):
+        // the K best sequential-fp64 dot scores, index ascending on ties
+        std::vector<float> kk, vv;
+        session.read_kv(0, n, kk, vv);
+        std::vector<double> sc(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            double a = 0.0;
+            for (std::size_t t = 0; t < d; ++t) a += static_cast<double>(q[t]) * kk[i * d + t];
+            sc[i] = a;
+        }
+        std::vector<uint32_t> order(n);
+        for (uint32_t i = 0; i < n; ++i) order[i] = i;
+        std::partial_sort(order.begin(), order.begin() + static_cast<std::ptrdiff_t>(r.k), order.end(),
+                          [&](uint32_t a, uint32_t b) { return sc[a] != sc[b] ? sc[a] > sc[b] : a < b; });
+        std::vector<uint32_t> truth(order.begin(), order.begin() + static_cast<std::ptrdiff_t>(r.k));
+        std::sort(truth.begin(), truth.end());
+        std::size_t hit = 0;
+        for (uint32_t x : r.selected) hit += std::binary_search(truth.begin(), truth.end(), x) ? 1 : 0;
+        r.recall = truth.empty() ? 1.0 : static_cast<double>(hit) / static_cast<double>(truth.size());
+        double e2 = 0.0;
+        for (std::size_t t = 0; t < d; ++t) {
+            const double x = static_cast<double>(r.attention.output[t]) - dense->output[t];
+            e2 += x * x;
+        }
+        r.l2_error = std::sqrt(e2);
+        r.dense_reference = std::move(dense);
+    }
+    session.step += 1;
+    session.totals.add(r.counters);
+    return r;
+}
+
+// run_decode (session.cpp:101-126): validates stream lengths up front.
+inline std::vector<DecodeStepReport> run_decode(Session& session, std::span<const float> queries,
+                                                std::span<const float> keys,
+                                                std::span<const float> values, std::size_t steps,
+                                                bool compare_dense) {
+    const std::size_t d = session.dim();
+    if (queries.size() % d != 0 || keys.size() % d != 0 || values.size() % d != 0)
+        throw DimensionError("decode rows are not a multiple of d");
+    const std::size_t available = std::min({queries.size() / d, keys.size() / d, values.size() / d});
+    if (available < steps)
+        throw StreamExhaustedError("decode streams run out at step " + std::to_string(available) +
+                                   " of " + std::to_string(steps));
+    std::vector<DecodeStepReport> out;
+    out.reserve(steps);
+    for (std::size_t t = 0; t < steps; ++t)
+        out.push_back(decode_step(session, queries.subspan(t * d, d), keys.subspan(t * d, d),
+                                  values.subspan(t * d, d), compare_dense));
+    return out;
+}
+
+}  // namespace csattn_b200

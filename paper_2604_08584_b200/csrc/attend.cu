@@ -196,12 +196,178 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     if (threadIdx.x == 0) counters[p] = 0;  // ready for the next step
 }
 
+// Fast path, d == 128: lane l owns elements [4l, 4l+4) of every row. Rows go
+// in groups of 8: eight 128-bit K loads and eight V loads per lane in flight,
+// partial dots reduced across the warp by a transposed butterfly (9 shuffles
+// for 8 rows: after it, lane l holds the logit of row ((l>>4)&1)*4 +
+// ((l>>3)&1)*2 + ((l>>2)&1)), so exp / max / sum run lane-parallel.
+constexpr int GR = 8;
+__device__ __forceinline__ float4 ld_row4(const float* p) {
+    return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+__global__ void __launch_bounds__(ATT_THREADS)
+attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
+                 const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
+                 uint32_t* __restrict__ counters) {
+    constexpr int NC = 1, VEC = 4;
+    __shared__ float wm[ATT_WARPS], ws[ATT_WARPS];
+    __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
+    __shared__ uint32_t is_last;
+    const uint32_t c = blockIdx.x;
+    const uint32_t p = chunk_prob[c];
+    const DecodeProblem& P = probs[p];
+    const SessionDev& sd = *P.s;
+    const uint32_t d = 128, K = P.K, P0 = sd.P;
+    const uint32_t j = c - chunk_base[p];
+    const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const uint32_t r0 = j * ATT_ROWS + w * 32;
+    const uint32_t nr = r0 < K ? min(32u, K - r0) : 0u;
+    const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
+    const float* const kpre = sd.kpre;
+    const float* const vpre = sd.vpre;
+    const float* const ktail = sd.ktail;
+    const float* const vtail = sd.vtail;
+    const float4 q4 = ld_row4(P.q + 4 * ln);
+    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
+    const uint32_t myidx = ln < nr ? __ldg(P.sel + r0 + ln) : 0u;
+    // this lane's row slot within a group of 8 after the butterfly
+    const int myrow = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+    const bool up16 = ln & 16, up8 = ln & 8, up4 = ln & 4;
+
+    float m = -FLT_MAX, s = 0.0f;
+    float acc[NC][VEC] = {{0.0f, 0.0f, 0.0f, 0.0f}};
+    for (uint32_t g0 = 0; g0 < nr; g0 += GR) {
+        float4 kk[GR], vv[GR];
+#pragma unroll
+        for (int u = 0; u < GR; ++u) {
+            const uint32_t i = __shfl_sync(0xffffffffu, myidx, (g0 + u) & 31);
+            const bool ok = g0 + u < nr;
+            const float* kr = i < P0 ? kpre + static_cast<size_t>(i) * d : ktail + static_cast<size_t>(i - P0) * d;
+            const float* vr = i < P0 ? vpre + static_cast<size_t>(i) * d : vtail + static_cast<size_t>(i - P0) * d;
+            kk[u] = ok ? ld_row4(kr + 4 * ln) : make_float4(0.f, 0.f, 0.f, 0.f);
+            vv[u] = ok ? ld_row4(vr + 4 * ln) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float pd[GR];
+#pragma unroll
+        for (int u = 0; u < GR; ++u)
+            pd[u] = fmaf(q4.w, kk[u].w, fmaf(q4.z, kk[u].z, fmaf(q4.y, kk[u].y, q4.x * kk[u].x)));
+        // transposed butterfly: 8 -> 4 -> 2 -> 1 partials, then a plain sum
+        float h4[4], h2[2];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const float send = up16 ? pd[t] : pd[t + 4];
+            const float keep = up16 ? pd[t + 4] : pd[t];
+            h4[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const float send = up8 ? h4[t] : h4[t + 2];
+            const float keep = up8 ? h4[t + 2] : h4[t];
+            h2[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        float lg;
+        {
+            const float send = up4 ? h2[0] : h2[1];
+            const float keep = up4 ? h2[1] : h2[0];
+            lg = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        lg += __shfl_xor_sync(0xffffffffu, lg, 2);
+        lg += __shfl_xor_sync(0xffffffffu, lg, 1);
+        lg *= scale;
+        const bool valid = g0 + myrow < nr;
+        float gm = valid ? lg : -FLT_MAX;
+        gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 4));
+        gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 8));
+        gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 16));
+        const float mn = fmaxf(m, gm);
+        const float f = expf(m - mn);
+        const float pr = valid ? expf(lg - mn) : 0.0f;
+        float ps = pr;  // rows are replicated over lane bits 0-1: sum bits 2-4
+        ps += __shfl_xor_sync(0xffffffffu, ps, 4);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+        s = s * f + ps;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[0][v] *= f;
+#pragma unroll
+        for (int u = 0; u < GR; ++u) {
+            const int src = ((u >> 2) & 1) * 16 + ((u >> 1) & 1) * 8 + (u & 1) * 4;
+            const float pu = __shfl_sync(0xffffffffu, pr, src);
+            acc[0][0] = fmaf(pu, vv[u].x, acc[0][0]);
+            acc[0][1] = fmaf(pu, vv[u].y, acc[0][1]);
+            acc[0][2] = fmaf(pu, vv[u].z, acc[0][2]);
+            acc[0][3] = fmaf(pu, vv[u].w, acc[0][3]);
+        }
+        if (want_w && valid && (ln & 3) == 0) P.weights[r0 + g0 + myrow] = lg;  // normalized later
+        m = mn;
+    }
+    // ---- CTA partial ----
+    if (ln == 0) {
+        wm[w] = nr ? m : -FLT_MAX;
+        ws[w] = nr ? s : 0.0f;
+    }
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) wacc[w][cc * 32 * VEC + ln * VEC + v] = acc[cc][v];
+    __syncthreads();
+    float M = -FLT_MAX;
+#pragma unroll
+    for (int i = 0; i < ATT_WARPS; ++i) M = fmaxf(M, wm[i]);
+    float* pp = part + static_cast<size_t>(c) * (d + 2);
+    if (threadIdx.x == 0) {
+        float S = 0.0f;
+        for (int i = 0; i < ATT_WARPS; ++i)
+            if (ws[i] > 0.0f) S += ws[i] * expf(wm[i] - M);
+        pp[0] = M;
+        pp[1] = S;
+    }
+    for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
+        float a = 0.0f;
+        for (int i = 0; i < ATT_WARPS; ++i)
+            if (ws[i] > 0.0f) a += wacc[i][t] * expf(wm[i] - M);
+        pp[2 + t] = a;
+    }
+    // ---- last CTA of the problem merges all partials in chunk order ----
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) is_last = (atomicAdd(counters + p, 1u) == nch - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const float* pb = part + static_cast<size_t>(chunk_base[p]) * (d + 2);
+    float GM = -FLT_MAX;
+    for (uint32_t k = 0; k < nch; ++k) GM = fmaxf(GM, __ldcg(pb + k * (d + 2)));
+    float GS = 0.0f;
+    for (uint32_t k = 0; k < nch; ++k) {
+        const float sk = __ldcg(pb + k * (d + 2) + 1);
+        if (sk > 0.0f) GS += sk * expf(__ldcg(pb + k * (d + 2)) - GM);
+    }
+    const float inv = 1.0f / GS;
+    for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
+        float o = 0.0f;
+        for (uint32_t k = 0; k < nch; ++k) {
+            const float sk = __ldcg(pb + k * (d + 2) + 1);
+            if (sk > 0.0f) o += __ldcg(pb + k * (d + 2) + 2 + t) * expf(__ldcg(pb + k * (d + 2)) - GM);
+        }
+        if (P.out) P.out[t] = o * inv;
+    }
+    if (want_w)
+        for (uint32_t r = threadIdx.x; r < K; r += blockDim.x)
+            P.weights[r] = expf(__ldcg(P.weights + r) - GM) * inv;
+    if (threadIdx.x == 0) counters[p] = 0;  // ready for the next step
+}
+
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
-    if (d % 4 == 0) {
+    if (d == 128) {
+        attend128_kernel<<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+    } else if (d % 4 == 0) {
         if (d <= 128) CSA_ATT(1, 4);
         else if (d <= 256) CSA_ATT(2, 4);
         else CSA_ATT(4, 4);

@@ -1163,6 +1163,16 @@ csattn_status csattn_session_export(csattn_session s, uint32_t* lens, uint32_t* 
     });
 }
 
+csattn_status csattn_session_centroids(csattn_session s, float* centroids) {
+    return guard([&] {
+        if (!centroids) fail(CSATTN_ERR_PARAMETER, "null output");
+        ck(cudaMemcpyAsync(centroids, s->cent.p, static_cast<size_t>(s->h.C) * s->h.d * 4,
+                           cudaMemcpyDeviceToHost, s->ctx->stream),
+           "copy centroids");
+        ck(cudaStreamSynchronize(s->ctx->stream), "centroids");
+    });
+}
+
 csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn_session* out) {
     return guard([&] {
         if (max_steps < src->step) fail(CSATTN_ERR_PARAMETER, "fork capacity below steps taken");

@@ -1,0 +1,185 @@
+// test_facade.cpp — the reference's own session-level checks, run twice with
+// the same calls: once through the UNMODIFIED reference library (namespace
+// csattn_ref, oracle/_ref) and once through the B200 drop-in facade
+// (include/csattn_b200.hpp -> C ABI -> sm_100a kernels). TEST INFRASTRUCTURE:
+// it links the checker; it is built by tests/cpp/Makefile where
+// /root/reference exists and run by tests/test_cpp_facade.py on a B200.
+//
+// Mirrors test_session.cpp: prefill validation (:222-267), full lifecycle vs
+// reference with exact selected sets and output agreement (:113-151),
+// counters (:66-82, :153-168), stream exhaustion message (:179-196), and
+// table equality after streaming inserts (acceptance.cpp:229-267).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "csattn/session.hpp"    // reference (compiled with -Dcsattn=csattn_ref)
+#include "csattn/synthetic.hpp"
+#include "csattn_b200.hpp"       // B200 facade
+
+namespace R = csattn_ref;
+namespace B = csattn_b200;
+
+static int failures = 0;
+#define CHECK(cond, ...)                                   \
+    do {                                                   \
+        if (!(cond)) {                                     \
+            std::printf("FAIL %s:%d: ", __FILE__, __LINE__); \
+            std::printf(__VA_ARGS__);                      \
+            std::printf("\n");                             \
+            ++failures;                                    \
+        }                                                  \
+    } while (0)
+
+template <class E, class F>
+static std::string thrown(F&& f) {
+    try {
+        f();
+    } catch (const E& e) {
+        return e.what();
+    } catch (...) {
+        return "<other exception>";
+    }
+    return "<none>";
+}
+
+static void lifecycle(std::size_t P, std::size_t T, std::size_t d, std::size_t m, std::uint64_t seed,
+                      const char* schedule, bool passthrough) {
+    R::SyntheticSpec spec;
+    spec.rows = P + T;
+    spec.dim = d;
+    spec.seed = seed;
+    const R::SyntheticWorkload w = R::make_synthetic(spec);
+    const std::span<const float> q(w.queries), k(w.keys), v(w.values);
+    auto pre = [&](std::span<const float> x) { return x.subspan(0, P * d); };
+    auto tail = [&](std::span<const float> x) { return x.subspan(P * d, T * d); };
+
+    R::IndexConfig ric;
+    ric.cluster.seed = 1;
+    ric.score_bits = 32;
+    B::IndexConfig bic;
+    bic.cluster.seed = 1;
+    bic.score_bits = 32;
+    const auto [rho, period] = R::parse_schedule(schedule);
+    const auto [brho, bperiod] = B::parse_schedule(schedule);
+    CHECK(rho == brho && period == bperiod, "parse_schedule(%s)", schedule);
+    R::RetrievalConfig rrc;
+    rrc.keep_ratio = rho;
+    rrc.search_period = period;
+    rrc.recent_passthrough = passthrough;
+    B::RetrievalConfig brc;
+    brc.keep_ratio = brho;
+    brc.search_period = bperiod;
+    brc.recent_passthrough = passthrough;
+
+    R::Session rs = R::prefill(pre(q), pre(k), pre(v), R::SubspaceLayout::uniform(d, m), ric, rrc);
+    B::Session bs = B::prefill(pre(q), pre(k), pre(v), B::SubspaceLayout::uniform(d, m), bic, brc, T);
+
+    // offline build: identical tables (membership, order, scores)
+    {
+        const B::CsIndex bi = bs.export_index();
+        CHECK(bi.tables.size() == rs.index.tables.size(), "table count");
+        std::size_t diff = 0;
+        for (std::size_t t = 0; t < bi.tables.size(); ++t)
+            diff += (bi.tables[t].indices != rs.index.tables[t].indices ||
+                     bi.tables[t].scores != rs.index.tables[t].scores);
+        CHECK(diff == 0, "P=%zu: %zu of %zu prefill tables differ", P, diff, bi.tables.size());
+        CHECK(bi.list_capacity == rs.index.list_capacity, "L");
+    }
+
+    const auto rr = R::run_decode(rs, tail(q), tail(k), tail(v), T, false);
+    const auto br = B::run_decode(bs, tail(q), tail(k), tail(v), T, false);
+    std::size_t sel_diff = 0;
+    double worst = 0.0;
+    for (std::size_t t = 0; t < T; ++t) {
+        sel_diff += rr[t].selected != br[t].selected;
+        double e2 = 0.0, n2 = 0.0;
+        for (std::size_t x = 0; x < d; ++x) {
+            const double a = rr[t].attention.output[x], b = br[t].attention.output[x];
+            e2 += (a - b) * (a - b);
+            n2 += a * a;
+        }
+        worst = std::max(worst, std::sqrt(e2 / n2));
+        CHECK(rr[t].k == br[t].k && rr[t].searched == br[t].searched, "step %zu k/searched", t);
+        const auto& a = rr[t].counters;
+        const auto& b = br[t].counters;
+        CHECK(a.centroid_dot_ops == b.centroid_dot_ops && a.gathered_entries == b.gathered_entries &&
+                  a.reduce_ops == b.reduce_ops && a.attention_key_ops == b.attention_key_ops &&
+                  a.searches == b.searches && a.inserts_attempted == b.inserts_attempted &&
+                  a.inserts_applied == b.inserts_applied && a.insert_dot_ops == b.insert_dot_ops &&
+                  a.h2d_bytes_model == b.h2d_bytes_model,
+              "step %zu counters differ", t);
+    }
+    CHECK(sel_diff == 0, "P=%zu %s: %zu of %zu selected sets differ", P, schedule, sel_diff, T);
+    CHECK(worst <= 1e-3, "P=%zu %s: output rel err %.3g", P, schedule, worst);
+    CHECK(rs.totals.inserts_applied == bs.totals.inserts_applied, "totals");
+
+    // streaming inserts: tables still identical (acceptance.cpp:229-267)
+    {
+        const B::CsIndex bi = bs.export_index();
+        std::size_t diff = 0;
+        for (std::size_t t = 0; t < bi.tables.size(); ++t)
+            diff += (bi.tables[t].indices != rs.index.tables[t].indices ||
+                     bi.tables[t].scores != rs.index.tables[t].scores);
+        CHECK(diff == 0, "P=%zu: %zu tables differ after %zu inserts", P, diff, T);
+    }
+    std::printf("lifecycle P=%zu T=%zu d=%zu m=%zu %s pt=%d: sets equal %zu/%zu, rel err %.2e\n", P,
+                T, d, m, schedule, passthrough ? 1 : 0, T - sel_diff, T, worst);
+}
+
+static void errors() {
+    const std::size_t d = 16, P = 64;
+    std::vector<float> q(P * d, 0.5f), k(P * d, 0.25f), v(P * d, 1.0f);
+    // prefill validation (session.cpp:25-44): same class, same message
+    {
+        std::vector<float> bad(P * d + 3, 0.0f);
+        auto a = thrown<R::DimensionError>([&] {
+            R::prefill(bad, k, v, R::SubspaceLayout::uniform(d, 4), R::IndexConfig{}, R::RetrievalConfig{});
+        });
+        auto b = thrown<B::DimensionError>([&] {
+            B::prefill(bad, k, v, B::SubspaceLayout::uniform(d, 4), B::IndexConfig{}, B::RetrievalConfig{});
+        });
+        CHECK(a == b, "prefill width: ref '%s' vs b200 '%s'", a.c_str(), b.c_str());
+        std::vector<float> half(P / 2 * d, 0.0f);
+        a = thrown<R::ParameterError>([&] {
+            R::prefill(q, half, v, R::SubspaceLayout::uniform(d, 4), R::IndexConfig{}, R::RetrievalConfig{});
+        });
+        b = thrown<B::ParameterError>([&] {
+            B::prefill(q, half, v, B::SubspaceLayout::uniform(d, 4), B::IndexConfig{}, B::RetrievalConfig{});
+        });
+        CHECK(a == b, "prefill counts: ref '%s' vs b200 '%s'", a.c_str(), b.c_str());
+    }
+    // stream exhaustion (session.cpp:111-116)
+    {
+        R::IndexConfig ric;
+        ric.cluster.centroids = 4;
+        B::IndexConfig bic;
+        bic.cluster.centroids = 4;
+        R::Session rs = R::prefill(q, k, v, R::SubspaceLayout::uniform(d, 4), ric, R::RetrievalConfig{});
+        B::Session bs = B::prefill(q, k, v, B::SubspaceLayout::uniform(d, 4), bic, B::RetrievalConfig{}, 8);
+        std::vector<float> s3(3 * d, 0.1f);
+        const auto a = thrown<R::StreamExhaustedError>([&] { R::run_decode(rs, s3, s3, s3, 5, false); });
+        const auto b = thrown<B::StreamExhaustedError>([&] { B::run_decode(bs, s3, s3, s3, 5, false); });
+        CHECK(a == b && a.find("step 3 of 5") != std::string::npos, "exhaustion: '%s' vs '%s'",
+              a.c_str(), b.c_str());
+    }
+    // keep_count / h2d closed forms
+    CHECK(R::keep_count(0.05, 8192) == B::keep_count(0.05, 8192), "keep_count");
+    CHECK(R::h2d_bytes(0.05, 4096, 128, 2, 1) == B::h2d_bytes(0.05, 4096, 128, 2, 1), "h2d_bytes");
+    std::printf("errors: done\n");
+}
+
+int main() {
+    errors();
+    lifecycle(4096, 12, 128, 8, 2026, "0.05-step-1", true);   // BASELINE config 1
+    lifecycle(2000, 10, 64, 8, 7, "0.15-step-4", true);       // period reuse
+    lifecycle(1500, 6, 64, 4, 11, "0.05-step-1", false);      // window competes
+    if (failures) {
+        std::printf("%d FAILURES\n", failures);
+        return 1;
+    }
+    std::printf("ALL OK\n");
+    return 0;
+}

@@ -1,0 +1,31 @@
+"""The C++ drop-in facade (include/csattn_b200.hpp) against the unmodified
+reference library, driven by the same calls (tests/cpp/test_facade.cpp):
+identical tables, selected sets, counters, error classes and messages."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "test_facade")
+
+
+@pytest.mark.gpu
+def test_cpp_facade_matches_reference_library():
+    if not os.path.exists(BIN):
+        pytest.skip("tests/cpp/test_facade not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_cpp_facade_header_compiles_standalone(tmp_path):
+    """The facade header is self-contained C++20 over the C ABI (no CUDA, no torch)."""
+    root = os.path.dirname(HERE)
+    src = tmp_path / "t.cpp"
+    src.write_text('#include "csattn_b200.hpp"\n'
+                   'int main() { csattn_b200::RetrievalConfig c; '
+                   'return csattn_b200::SubspaceLayout::uniform(128, 8).count() == 8 ? 0 : 1; }\n')
+    r = subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-I", os.path.join(root, "include"),
+                        str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
