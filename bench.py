@@ -153,9 +153,10 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config: str):
-    """Per-launch DRAM bytes of the decode kernel from the committed ncu capture."""
-    p = os.path.join(ROOT, "profiles", f"ncu_decode_{config}.json")
+def ncu_traffic(kernel: str, config: str):
+    """Per-launch DRAM bytes (read + write) of `kernel` from the committed ncu
+    capture (profiles/ncu_<kernel>_<config>.json, one `ncu --set full` launch)."""
+    p = os.path.join(ROOT, "profiles", f"ncu_{kernel}_{config}.json")
     try:
         with open(p) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -304,8 +305,9 @@ def main():
     steps, warm = args.steps, args.warmup
     prof_steps = min(steps, 10)
     e2e_steps = min(steps, 10)
-    T = warm + steps + prof_steps + e2e_steps + 1
-    my_heads = [g for g in range(N_KV) if g % world == rank]
+    T = warm + steps + prof_steps + e2e_steps + 2
+    from paper_2604_08584_b200.sharding import kv_head_shard
+    my_heads = kv_head_shard(N_KV, world, rank)
     widths = [D // M] * M
     rc = cs.RetrievalConfig()
 
@@ -398,33 +400,61 @@ def main():
     sel_ms = prof["select_ms"] / nps
     att_ms = prof["attend_ms"] / nps
     ins_ms = prof["insert_ms"] / nps
-    # algorithmic bytes per launch, averaged over the profiled
-    # steps. Per query head: select = m*L*8 gathered (u32, f32) entries +
-    # C*d*4 centroids + d*4 q + K*4 indices out; attend = K*(2*d*4) selected K/V
-    # rows + K*4 indices + 2*d*4 q/out. Their sum is the per-query-head unit.
-    sel_b, att_b = [], []
-    for j in range(prof_steps):
-        K = keep_count(0.05, n_prof0 + j)
-        sel_b.append(nq * (M * L * 8 + C_CENT * D * 4 + D * 4 + K * 4))
-        att_b.append(nq * (K * (2 * D * 4 + 4) + 2 * D * 4))
-    sel_bytes, att_bytes = float(np.mean(sel_b)), float(np.mean(att_b))
-    alg_bytes = att_bytes  # the dominant kernel: attend
-    dec_ms = att_ms
-    achieved = alg_bytes / (dec_ms * 1e-3) / 1e9
+    # ---- algorithmic bytes ----
+    # per query head ("per-query"): m*L gathered (u32, f32) entries + C*d*4
+    # centroids + d*4 q + K*4 indices (select); K*(2*d*4 + 4) selected K/V rows
+    # and indices + 2*d*4 q/out (attend). Unique (what one pass over HBM must
+    # move): the union of the tables a session's query heads gather, and per KV
+    # head the union of the selected prefill rows over its 64 (sequence, head)
+    # problems (the 16 sequences share the prefill rows) plus each session's
+    # own appended rows. Measured on the last profiled step (gather) and on one
+    # extra step with the selected sets read back (attend).
+    u_ent = C.c_uint64()
+    t_ent = C.c_uint64()
+    uniq_entries = tot_entries = 0
+    for sh in sessions:
+        cs._check(lib.csattn_session_gather_stats(sh.h, C.byref(u_ent), C.byref(t_ent)))
+        uniq_entries += u_ent.value
+        tot_entries += t_ent.value
+    Kp = keep_count(0.05, n_prof0 + prof_steps - 1)
+    sel_unique = (uniq_entries * 8 + ns * C_CENT * D * 4 + nq * (D * 4 + Kp * 4))
+    sel_perq = (tot_entries * 8 + nq * (C_CENT * D * 4 + D * 4 + Kp * 4))
+    maxK = keep_count(0.05, P + t)
+    seld = torch.zeros((nq, maxK), dtype=torch.int32, device="cuda")
+    st_ = lib.csattn_decode_batch(ctx.h, ns, handles, C.c_void_p(qd[t].data_ptr()),
+                                  C.c_void_p(kd[t].data_ptr()), C.c_void_p(vd[t].data_ptr()),
+                                  C.c_void_p(outd[t].data_ptr()), C.c_void_p(seld.data_ptr()),
+                                  maxK, 0)
+    cs._check(st_)
+    Ka = keep_count(0.05, P + t)
+    t += 1
+    selh = seld.cpu().numpy().astype(np.int64)[:, :Ka]
+    uniq_rows = 0
+    for gi, g in enumerate(my_heads):
+        rows_g = selh[gi * n_seq * GROUP:(gi + 1) * n_seq * GROUP]
+        pre_rows = np.unique(rows_g[rows_g < P])
+        uniq_rows += pre_rows.size
+        for sidx in range(n_seq):  # appended rows are per session
+            r = rows_g[sidx * GROUP:(sidx + 1) * GROUP]
+            uniq_rows += np.unique(r[r >= P]).size
+    att_unique = uniq_rows * 2 * D * 4 + nq * (Ka * 4 + 2 * D * 4)
+    att_perq = nq * (Ka * (2 * D * 4 + 4) + 2 * D * 4)
     peak, peak_src = measured_peak()
     kernels = {
-        "select": {"ms": sel_ms, "alg_bytes": sel_bytes,
-                   "gbs": sel_bytes / (sel_ms * 1e-3) / 1e9},
-        "attend": {"ms": att_ms, "alg_bytes": att_bytes,
-                   "gbs": att_bytes / (att_ms * 1e-3) / 1e9},
+        "select": {"ms": sel_ms, "alg_bytes_unique": sel_unique, "alg_bytes_per_query": sel_perq,
+                   "gbs": sel_unique / (sel_ms * 1e-3) / 1e9},
+        "attend": {"ms": att_ms, "alg_bytes_unique": att_unique, "alg_bytes_per_query": att_perq,
+                   "gbs": att_unique / (att_ms * 1e-3) / 1e9},
         "insert": {"ms": ins_ms},
     }
     for v in kernels.values():
         if "gbs" in v:
             v["frac"] = v["gbs"] / peak
-    step_bytes = float(np.mean([nq * (M * L * 8 + keep_count(0.05, n_at_start + j) *
-                                      (2 * D * 4 + 4) + C_CENT * D * 4 + 2 * D * 4)
-                                for j in range(steps)]))
+    dom = "select" if sel_ms >= att_ms else "attend"
+    dec_ms = kernels[dom]["ms"]
+    alg_bytes = kernels[dom]["alg_bytes_unique"]
+    achieved = kernels[dom]["gbs"]
+    step_bytes = sel_unique + att_unique
     # ---- e2e: public API with pinned host buffers, copies inside the timed region ----
     qp = torch.from_numpy(qh).pin_memory()
     kp = torch.from_numpy(kh).pin_memory()
@@ -473,11 +503,11 @@ def main():
             "config": dict(config, parallelism=f"kv-head shard x{world}", l2_policy=(
                 "working set (tables ~14 GB + KV 1 GB per GPU at c3) >> 126 MB L2; no flush")),
             "hbm_gbs_per_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "csa::attend_kernel", "achieved": achieved,
+            "roofline": {"bound": "hbm", "kernel": f"csa::{dom}_kernel", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(args.config), "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg_bytes, "kernel_ms": dec_ms,
-                         "problems_per_launch": nq, "kernels": kernels},
+                         "traffic": ncu_traffic(dom, args.config), "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg_bytes, "alg_bytes": "unique (SURVEY 8(d))",
+                         "kernel_ms": dec_ms, "problems_per_launch": nq, "kernels": kernels},
             "e2e": {"value": e2e_ms * 1e3, "unit": "us",
                     "h2d_bytes_per_step": int(qh[0].nbytes + kh[0].nbytes + vh[0].nbytes),
                     "d2h_bytes_per_step": int(op[0].numel() * 4)},

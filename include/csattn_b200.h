@@ -228,6 +228,13 @@ csattn_status csattn_session_set_retrieval(csattn_session s, const csattn_retrie
 csattn_status csattn_session_keep_candidates(csattn_session s, int32_t enable);
 csattn_status csattn_session_candidates(csattn_session s, uint64_t head, uint32_t* indices,
                                         double* scores, uint64_t cap, uint64_t* n);
+/* Gather accounting of the last search of every query head (bench/roofline):
+ * total = sum over heads of the gathered lists' live entries
+ * (CostCounters::gathered_entries), unique = live entries of the union of the
+ * heads' gathered tables (what one pass over HBM must read). */
+csattn_status csattn_session_gather_stats(csattn_session s, uint64_t* unique_entries,
+                                          uint64_t* total_entries);
+
 /* KvStore rows back to the host (core.cpp:84-90): rows [first, first+count). */
 csattn_status csattn_session_read_kv(csattn_session s, uint64_t first, uint64_t count,
                                      float* keys, float* values);

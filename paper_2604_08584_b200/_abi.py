@@ -93,6 +93,7 @@ SIGNATURES = {
                                         u64, P(vp)]),
     "csattn_session_export": (C.c_int, [vp, vp, vp, vp, u64, vp]),
     "csattn_session_centroids": (C.c_int, [vp, vp]),
+    "csattn_session_gather_stats": (C.c_int, [vp, P(u64), P(u64)]),
     "csattn_session_fork": (C.c_int, [vp, u64, P(vp)]),
     "csattn_session_destroy": (C.c_int, [vp]),
     "csattn_session_info_get": (C.c_int, [vp, P(SessionInfoC)]),

@@ -1163,6 +1163,35 @@ csattn_status csattn_session_export(csattn_session s, uint32_t* lens, uint32_t* 
     });
 }
 
+csattn_status csattn_session_gather_stats(csattn_session s, uint64_t* unique_entries,
+                                          uint64_t* total_entries) {
+    return guard([&] {
+        std::vector<csa::DecodeReport> dr(s->group);
+        std::vector<uint32_t> live(s->T());
+        ck(cudaMemcpyAsync(dr.data(), s->drep.p, s->group * sizeof(csa::DecodeReport),
+                           cudaMemcpyDeviceToHost, s->ctx->stream),
+           "copy report");
+        ck(cudaMemcpyAsync(live.data(), s->live.p, live.size() * 4, cudaMemcpyDeviceToHost,
+                           s->ctx->stream),
+           "copy live");
+        ck(cudaStreamSynchronize(s->ctx->stream), "gather stats");
+        std::vector<char> seen(s->T(), 0);
+        uint64_t u = 0, t = 0;
+        for (uint64_t h = 0; h < s->group; ++h)
+            for (uint32_t l = 0; l < dr[h].nl && l < static_cast<uint32_t>(csa::MAXL); ++l) {
+                const uint32_t tb = dr[h].lists[l];
+                if (tb >= s->T()) continue;
+                t += live[tb];
+                if (!seen[tb]) {
+                    seen[tb] = 1;
+                    u += live[tb];
+                }
+            }
+        *unique_entries = u;
+        *total_entries = t;
+    });
+}
+
 csattn_status csattn_session_centroids(csattn_session s, float* centroids) {
     return guard([&] {
         if (!centroids) fail(CSATTN_ERR_PARAMETER, "null output");
