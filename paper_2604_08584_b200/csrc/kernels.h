@@ -15,8 +15,8 @@ cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t 
 
 // select.cu: streaming gather + top-K, persistent (one CTA per SM, problems
 // strided over the grid). log_idx/log_sc: grid x log_cap candidate-log slots.
-constexpr uint32_t SELECT_MAX_CONTEXT = 8192u * 32u;  // bitmap aliases the tile accumulator
-constexpr uint32_t SELECT_LOG_ALIGN = 8192u;           // log_cap multiple (per-warp regions)
+constexpr uint32_t SELECT_MAX_CONTEXT = 4096u * 64u;  // bitmap aliases the tile accumulator
+constexpr uint32_t SELECT_LOG_ALIGN = 4096u;           // log_cap multiple (per-warp regions)
 uint32_t select_grid(uint32_t nprob, int num_sms);
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,

@@ -45,22 +45,22 @@
 
 namespace csa {
 
-constexpr int SEL_CW = 16;                   // consumer warps
+constexpr int SEL_CW = 8;                    // consumer warps (2 CTAs per SM)
 constexpr int SEL_CT = SEL_CW * 32;          // consumer threads
 constexpr int SEL_THREADS = SEL_CT + 32;     // + producer warp
-constexpr uint32_t TILE = 8192;              // keys per tile (fp64 accumulator: 64 KB)
+constexpr uint32_t TILE = 4096;              // keys per tile (fp64 accumulator: 32 KB)
 constexpr uint32_t TILE_BLKS = TILE / KEY_BLOCK;
 constexpr uint32_t WKEYS = TILE / SEL_CW;    // keys per warp in the tile-end filter
-constexpr int NSLOT = 7;                     // ring slots
-constexpr uint32_t SLOT_E = 2048;            // entries per slot (16 KB)
+constexpr int NSLOT = 6;                     // ring slots
+constexpr uint32_t SLOT_E = 1024;            // entries per slot (8 KB)
 constexpr uint32_t CACHE_LIST = 127;         // chunk "list" id of a cached-score tile
-constexpr int NB = 4096;                     // histogram bins
+constexpr int NB = 2048;                     // histogram bins
 constexpr int NCB = NB / 32;                 // coarse bins (32 fine bins each)
-constexpr int BKT = 1024;                    // threshold-bin members ranked in smem
+constexpr int BKT = 512;                     // threshold-bin members ranked in smem
 constexpr int RANK_DIRECT = 384;             // O(n^2) ranking up to this size
 constexpr uint32_t F_LIST_END = 1, F_TILE_END = 2, F_PROB_END = 4;
 constexpr unsigned long long ABSENT = 0x7ff4deadbeef0000ull;  // NaN box: key not gathered
-static_assert(TILE * 32 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bits");
+static_assert(TILE * 64 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bits");
 static_assert(SELECT_MAX_CONTEXT / TILE <= 128 && MAXL < 127, "chunk info fields");
 
 // One ring chunk: info = list | flags << 7 | tile << 10; entries at table
@@ -369,7 +369,7 @@ __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const Route
     if (st.prof && tid == 0) st.prof[0] = gtimer();
 }
 
-__global__ void __launch_bounds__(SEL_THREADS, 1)
+__global__ void __launch_bounds__(SEL_THREADS, 2)
 select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
               uint32_t nprob, uint32_t* __restrict__ log_idx_all, double* __restrict__ log_sc_all,
               uint32_t log_cap) {
@@ -910,7 +910,7 @@ static size_t select_smem() {
 }
 
 uint32_t select_grid(uint32_t nprob, int num_sms) {
-    const uint32_t g = static_cast<uint32_t>(num_sms > 0 ? num_sms : 1);
+    const uint32_t g = 2u * static_cast<uint32_t>(num_sms > 0 ? num_sms : 1);  // 2 CTAs per SM
     return nprob < g ? nprob : g;
 }
 
