@@ -62,8 +62,8 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const uint32_t r0 = j * ATT_ROWS + w * 32;
-    const uint32_t nr = r0 < K ? min(32u, K - r0) : 0u;
+    const uint32_t rw = j * ATT_ROWS + w * (ATT_ROWS / ATT_WARPS);  // this warp's first row
+    const uint32_t nrw = rw < K ? min(ATT_ROWS / ATT_WARPS, K - rw) : 0u;
     const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
 
     float q[NC][VEC];
@@ -75,7 +75,6 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
             q[cc][v] = e < d ? P.q[e] : 0.0f;
         }
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
-    const uint32_t myidx = ln < nr ? __ldg(P.sel + r0 + ln) : 0u;
 
     float m = -FLT_MAX, s = 0.0f;
     float acc[NC][VEC];
@@ -84,6 +83,10 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc[cc][v] = 0.0f;
 
+    for (uint32_t b0 = 0; b0 < nrw; b0 += 32) {  // 32-row index batches
+    const uint32_t r0 = rw + b0;
+    const uint32_t nr = min(32u, nrw - b0);
+    const uint32_t myidx = ln < nr ? __ldg(P.sel + r0 + ln) : 0u;
     for (uint32_t i0 = 0; i0 < nr; i0 += ATT_U) {
         float kv[ATT_U][NC][VEC], vv[ATT_U][NC][VEC];
 #pragma unroll
@@ -139,10 +142,11 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
         }
         m = mn;
     }
+    }
     // ---- CTA partial ----
     if (ln == 0) {
-        wm[w] = nr ? m : -FLT_MAX;
-        ws[w] = nr ? s : 0.0f;
+        wm[w] = nrw ? m : -FLT_MAX;
+        ws[w] = nrw ? s : 0.0f;
     }
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)
@@ -222,8 +226,8 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const uint32_t r0 = j * ATT_ROWS + w * 32;
-    const uint32_t nr = r0 < K ? min(32u, K - r0) : 0u;
+    const uint32_t rw = j * ATT_ROWS + w * (ATT_ROWS / ATT_WARPS);  // this warp's first row
+    const uint32_t nrw = rw < K ? min(ATT_ROWS / ATT_WARPS, K - rw) : 0u;
     const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
     const float* const kpre = sd.kpre;
     const float* const vpre = sd.vpre;
@@ -231,23 +235,34 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const float* const vtail = sd.vtail;
     const float4 q4 = ld_row4(P.q + 4 * ln);
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
-    const uint32_t myidx = ln < nr ? __ldg(P.sel + r0 + ln) : 0u;
     // this lane's row slot within a group of 8 after the butterfly
     const int myrow = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
     const bool up16 = ln & 16, up8 = ln & 8, up4 = ln & 4;
 
     float m = -FLT_MAX, s = 0.0f;
     float acc[NC][VEC] = {{0.0f, 0.0f, 0.0f, 0.0f}};
+    for (uint32_t b0 = 0; b0 < nrw; b0 += 32) {  // 32-row index batches
+    const uint32_t r0 = rw + b0;
+    const uint32_t nr = min(32u, nrw - b0);
+    // each lane resolves one row: element offset within its store (32-bit),
+    // top bit = appended row (tail store); K and V share the offset
+    uint32_t myoff = 0;
+    if (ln < nr) {
+        const uint32_t i = __ldg(P.sel + r0 + ln);
+        myoff = i < P0 ? i * d : ((i - P0) * d) | 0x80000000u;
+    }
     for (uint32_t g0 = 0; g0 < nr; g0 += GR) {
         float4 kk[GR], vv[GR];
 #pragma unroll
         for (int u = 0; u < GR; ++u) {
-            const uint32_t i = __shfl_sync(0xffffffffu, myidx, (g0 + u) & 31);
+            const uint32_t o = __shfl_sync(0xffffffffu, myoff, (g0 + u) & 31);
             const bool ok = g0 + u < nr;
-            const float* kr = i < P0 ? kpre + static_cast<size_t>(i) * d : ktail + static_cast<size_t>(i - P0) * d;
-            const float* vr = i < P0 ? vpre + static_cast<size_t>(i) * d : vtail + static_cast<size_t>(i - P0) * d;
-            kk[u] = ok ? ld_row4(kr + 4 * ln) : make_float4(0.f, 0.f, 0.f, 0.f);
-            vv[u] = ok ? ld_row4(vr + 4 * ln) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const bool tl = o & 0x80000000u;
+            const uint32_t e = (o & 0x7fffffffu) + 4 * ln;
+            const float* kr = (tl ? ktail : kpre) + e;
+            const float* vr = (tl ? vtail : vpre) + e;
+            kk[u] = ok ? ld_row4(kr) : make_float4(0.f, 0.f, 0.f, 0.f);
+            vv[u] = ok ? ld_row4(vr) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         float pd[GR];
 #pragma unroll
@@ -303,10 +318,11 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         if (want_w && valid && (ln & 3) == 0) P.weights[r0 + g0 + myrow] = lg;  // normalized later
         m = mn;
     }
+    }
     // ---- CTA partial ----
     if (ln == 0) {
-        wm[w] = nr ? m : -FLT_MAX;
-        ws[w] = nr ? s : 0.0f;
+        wm[w] = nrw ? m : -FLT_MAX;
+        ws[w] = nrw ? s : 0.0f;
     }
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc)

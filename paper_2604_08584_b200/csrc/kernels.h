@@ -23,7 +23,7 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
                           cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
-constexpr uint32_t ATT_ROWS = 128;
+constexpr uint32_t ATT_ROWS = 256;
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st);
