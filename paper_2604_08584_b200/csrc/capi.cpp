@@ -148,14 +148,19 @@ struct csattn_ctx_s {
     DevMem part, counters;  // attention partials + per-problem merge counters
     DevMem plans;           // route.cu -> select.cu routing plans
     DevMem log_idx, log_sc; // select.cu candidate logs: log_rows x log_cap
+    DevMem retry;           // select.cu retry list (speculative cut too high)
     uint64_t log_cap = 0, log_rows = 0;
     int num_sms = 148;
+    // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
+    // retry pass — used by the tests to exercise it)
+    double spec_keep = std::getenv("CSATTN_SPEC_KEEP") ? std::atof(std::getenv("CSATTN_SPEC_KEEP")) : 0.7;
     uint64_t counters_n = 0;
     // select-kernel phase timestamps (env CSATTN_PHASE_PROF=1; diagnostics only)
     bool phase_prof = std::getenv("CSATTN_PHASE_PROF") != nullptr;
     DevMem phase;
     double phase_sum[6] = {0, 0, 0, 0, 0, 0};
     double phase_dbg[3] = {0, 0, 0};
+    uint64_t phase_retry = 0, phase_probs = 0;
     uint64_t phase_n = 0;
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t take_event() {
@@ -317,7 +322,8 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     s->tmm.alloc(T * sizeof(float2));
     s->sel.alloc(group * (p + max_steps) * 4);
     if (rc->search_period > 1) s->cache.alloc(group * (p + max_steps) * sizeof(double));
-    s->cbounds.alloc(group * 2 * sizeof(double));
+    s->cbounds.alloc(group * 4 * sizeof(double));
+    ck(cudaMemsetAsync(s->cbounds.p, 0, group * 4 * sizeof(double), ctx->stream), "memset");
     s->drep.alloc(group * sizeof(csa::DecodeReport));
     s->irep.alloc(4 + ((T + 15) & ~15ull));
     s->dev.alloc(sizeof(csa::SessionDev));
@@ -486,7 +492,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             P.mode = (srch ? csa::MODE_SEARCH : 0u) |
                      ((srch && P.cache) ? csa::MODE_STORE_CACHE : 0u) |
                      (dw ? csa::MODE_WEIGHTS : 0u);
-            P.cbounds = s->cbounds.as<double>() + h * 2;
+            P.cbounds = s->cbounds.as<double>() + h * 4;
             P.prof = ctx->phase_prof ? ctx->phase.as<unsigned long long>() + qi * 8 : nullptr;
         }
         csa::InsertProblem& I = ctx->hiprobs[i];
@@ -562,10 +568,20 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->log_idx.alloc(ctx->log_rows * ctx->log_cap * 4);
         ctx->log_sc.alloc(ctx->log_rows * ctx->log_cap * 8);
     }
+    // retry list of problems whose speculative cut proved too high: [count, ids...]
+    ctx->retry.ensure((nq + 1) * 4);
+    ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
+    uint32_t* const rcount = ctx->retry.as<uint32_t>();
     ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
                           ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
-                          static_cast<uint32_t>(ctx->log_cap), ctx->stream),
+                          static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
+                          rcount, ctx->spec_keep, ctx->stream),
        "select launch");
+    ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
+                          ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
+                          static_cast<uint32_t>(ctx->log_cap), rcount + 1, rcount, nullptr,
+                          nullptr, 0.0, ctx->stream),
+       "select retry launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
                           ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream),
@@ -578,7 +594,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaEventRecord(ev[3], ctx->stream), "event");
         ctx->ev_steps.push_back(ev);
     }
-    ctx->launches += 4;
+    ctx->launches += 5;
     if (ctx->phase_prof) {
         // per problem: streaming (gather + log) and final-selection time,
         // logged candidates, threshold-bin size; printed at context teardown
@@ -597,6 +613,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             sum[3] += double(t[4]);
             sum[4] = std::max(sum[4], double(t[4]));
             ++n;
+        }
+        {
+            uint32_t nretry = 0;
+            ck(cudaMemcpy(&nretry, ctx->retry.p, 4, cudaMemcpyDeviceToHost), "retry count");
+            ctx->phase_retry += nretry;
+            ctx->phase_probs += nq;
         }
         if (nq) {
             double lo, hi;
@@ -900,6 +922,9 @@ static void ctx_release(csattn_ctx ctx) {
                      ctx->phase_sum[4]);
         std::fprintf(stderr, "[csattn] problem 0 of the last step: bounds [%g, %g] take_all|bin<<1=%g\n",
                      ctx->phase_dbg[0], ctx->phase_dbg[1], ctx->phase_dbg[2]);
+        std::fprintf(stderr, "[csattn] speculative cut: %llu of %llu problems retried\n",
+                     static_cast<unsigned long long>(ctx->phase_retry),
+                     static_cast<unsigned long long>(ctx->phase_probs));
     }
     cudaStreamSynchronize(ctx->stream);
     for (auto& ev : ctx->ev_steps)
@@ -1241,7 +1266,7 @@ csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn
         d2d(s->low, src->low, T * csa::LOW_Q * sizeof(csa::LowEnt));
         d2d(s->low_cnt, src->low_cnt, T * 4);
         d2d(s->tmm, src->tmm, T * sizeof(float2));
-        d2d(s->cbounds, src->cbounds, s->group * 2 * sizeof(double));
+        d2d(s->cbounds, src->cbounds, s->group * 4 * sizeof(double));
         if (s->cache.p && src->cache.p)
             for (uint64_t h = 0; h < s->group; ++h)
                 ck(cudaMemcpyAsync(s->cache.as<double>() + h * s->h.max_ctx,

@@ -79,7 +79,7 @@ struct DecodeProblem {
     float* weights;    // K floats (nullable)
     uint32_t* sel;     // K entries (scratch or caller buffer)
     double* cache;     // candidate-score cache for search_period > 1 (nullable)
-    double* cbounds;   // score bounds of the cached search (2 doubles, with cache)
+    double* cbounds;   // [lo, hi] of the cached search, [threshold hint, hint valid]
     uint32_t* rep;     // DecodeReport (device)
     uint32_t N;        // context this step attends to (pre-append)
     uint32_t K;        // selected-set size

@@ -18,8 +18,13 @@ cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t 
 constexpr uint32_t SELECT_MAX_CONTEXT = 4096u * 64u;  // bitmap aliases the tile accumulator
 constexpr uint32_t SELECT_LOG_ALIGN = 4096u;           // log_cap multiple (per-warp regions)
 uint32_t select_grid(uint32_t nprob, int num_sms);
+//   retry_in/retry_in_count: when non-null, process only the listed problems,
+//   without speculation (the second pass); retry_out/retry_out_count: where the
+//   first pass lists problems whose speculative cut proved too high.
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
+                          const uint32_t* retry_in, const uint32_t* retry_in_count,
+                          uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
                           cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA

@@ -38,6 +38,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -78,7 +79,7 @@ struct SelHdr {
     uint32_t wlog[SEL_CW + 1];  // per-warp candidate-log lengths, then prefix
     uint32_t wsum[SEL_CW];
     // final-phase broadcasts
-    uint32_t f_bin, f_above, f_count, f_take_all;
+    uint32_t f_bin, f_above, f_count, f_take_all, f_fail;
     unsigned long long tk;
     uint32_t tx;
 };
@@ -304,6 +305,8 @@ __device__ __forceinline__ void set_bit(uint32_t* bm, uint32_t i) {
 struct ProbState {
     uint32_t N, K, need, f_lo, wlo;
     uint32_t n_cache;
+    uint32_t cut_init;  // speculative cut from the previous step's threshold (0 = none)
+    double* hint;       // [threshold score, valid] of this (session, head)
     bool pt, store_cache;
     double lo, scale;
     double* cache;
@@ -319,8 +322,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // consumer warps: load problem p's descriptor, list weights, score bounds
+// Speculation: the previous search's threshold score t of this (session, head)
+// seeds the cut at lo + spec_keep * (t - lo) (spec_keep = 0.7 by default,
+// 0 disables). The final phase verifies that the threshold bin is at or above
+// it; otherwise the problem is redone without speculation by the retry pass,
+// so the result never depends on the guess.
+
 __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const RoutePlan* plans,
-                              uint32_t p, ProbState& st) {
+                              uint32_t p, ProbState& st, bool speculate, double spec_keep) {
     const uint32_t tid = threadIdx.x;
     const DecodeProblem* Pp = probs + p;
     const SessionDev* sdp = Pp->s;
@@ -355,6 +364,14 @@ __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const Route
     }
     st.lo = lo;
     st.scale = hi > lo ? static_cast<double>(NB) / (hi - lo) : 0.0;
+    st.hint = cbounds + 2;
+    st.cut_init = 0;
+    if (speculate && spec_keep > 0.0 && search && !st.store_cache && __ldcg(cbounds + 3) != 0.0 &&
+        st.scale > 0.0) {
+        const double t = __ldcg(cbounds + 2);
+        const double g = lo + spec_keep * (t - lo);
+        st.cut_init = bin_of(g, lo, st.scale);
+    }
     const uint32_t N = st.N, K = st.K;
     const uint32_t r_eff = window < N ? window : N;
     st.wlo = N - r_eff;
@@ -365,15 +382,24 @@ __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const Route
         st.need = K;
         st.f_lo = N;
     }
-    cbar();  // weights visible
+    if (tid == 0) S.cut = st.cut_init;
+    cbar();  // weights + cut visible
     if (st.prof && tid == 0) st.prof[0] = gtimer();
 }
 
 __global__ void __launch_bounds__(SEL_THREADS, 2)
 select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
               uint32_t nprob, uint32_t* __restrict__ log_idx_all, double* __restrict__ log_sc_all,
-              uint32_t log_cap) {
+              uint32_t log_cap, const uint32_t* __restrict__ retry_in,
+              const uint32_t* __restrict__ retry_in_count, uint32_t* __restrict__ retry_out,
+              uint32_t* __restrict__ retry_out_count, double spec_keep) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    // the problem sequence of this CTA: b, b + grid, ... over all problems, or
+    // over the retry list (second pass)
+    const uint32_t nwork = retry_in ? __ldcg(retry_in_count) : nprob;
+    if (blockIdx.x >= nwork) return;
+    auto prob_of = [&](uint32_t k) { return retry_in ? __ldcg(retry_in + k) : k; };
+    const bool speculate = retry_out != nullptr;
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
     unsigned char* p0 = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
     double* acc = reinterpret_cast<double*>(p0);                    // TILE fp64
@@ -424,7 +450,8 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             __syncwarp();
             ++c;
         };
-        for (uint32_t p = blockIdx.x; p < nprob; p += gridDim.x) {
+        for (uint32_t k = blockIdx.x; k < nwork; k += gridDim.x) {
+            const uint32_t p = prob_of(k);
             const DecodeProblem& P = probs[p];
             const SessionDev& sd = *P.s;
             const uint32_t N = P.N;
@@ -490,20 +517,21 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     }
 
     // ======================= consumer warps =======================
-    uint32_t p = blockIdx.x;
-    if (p >= nprob) return;
+    uint32_t kk = blockIdx.x;
+    uint32_t p = prob_of(kk);
     ProbState st;
-    setup_problem(S, probs, plans, p, st);
+    setup_problem(S, probs, plans, p, st, speculate, spec_keep);
     // warp w logs into its own region (it owns 1/16 of every tile's keys)
     uint32_t wlog_n = 0;
     uint32_t* const wlog_idx = log_idx + static_cast<size_t>(wid) * (log_cap / SEL_CW);
     double* const wlog_sc = log_sc + static_cast<size_t>(wid) * (log_cap / SEL_CW);
     uint16_t* const wcidx = cidx + wid * WKEYS;
     double* const wacc = acc + wid * WKEYS;
-    uint32_t c = 0;
-    while (p < nprob) {
-        const uint32_t slot = c % NSLOT;
-        mbar_wait_sleep(&S.full[slot], (c / NSLOT) & 1u);
+    uint32_t slot = 0, phase = 0;  // ring position of the next chunk
+    const uint32_t full0 = smem_u32(&S.full[0]), empty0 = smem_u32(&S.empty[0]);
+    const uint2* const ring0 = ring;
+    while (kk < nwork) {
+        mbar_wait_sleep_u32(full0 + 8 * slot, phase);
         const SlotMeta M = S.meta[slot];
         const uint32_t list = M.info & 127u, flags = (M.info >> 7) & 7u, tile = M.info >> 10;
         const uint32_t kbase = tile * TILE;
@@ -513,12 +541,13 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 const uint32_t qa = (M.lo - M.base) >> 1, qb = (M.hi - M.base + 1) >> 1;
                 const uint32_t np = qb - qa;
                 const uint32_t q0 = qa + (np * wid) / SEL_CW, q1 = qa + (np * (wid + 1)) / SEL_CW;
-                const uint4* st4 = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * SLOT_E);
+                const uint4* st4 = reinterpret_cast<const uint4*>(ring0 + slot * SLOT_E);
                 const double w = S.cw[list];
                 const uint32_t plo = M.lo - M.base, phi = M.hi - M.base;  // valid [plo, phi)
                 // two pairs (four entries) per lane per step, all loads issued
                 // before the adds: keys are unique within a list, so the four
                 // read-modify-writes are independent
+                auto run = [&](auto unit_weight) {
                 for (uint32_t q = q0 + ln; q < q1; q += 64) {
                     const bool h2 = q + 32 < q1;
                     const uint4 e = st4[q];
@@ -536,7 +565,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     double x1 = static_cast<double>(__uint_as_float(e.w));
                     double x2 = static_cast<double>(__uint_as_float(f.y));
                     double x3 = static_cast<double>(__uint_as_float(f.w));
-                    if (w != 1.0) {  // w * double(s) (exact when w == 1)
+                    if constexpr (!decltype(unit_weight)::value) {  // w * double(s)
                         x0 = __dmul_rn(w, x0);
                         x1 = __dmul_rn(w, x1);
                         x2 = __dmul_rn(w, x2);
@@ -547,6 +576,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     if (v2) *a2 = __dadd_rn(o2, x2);
                     if (v3) *a3 = __dadd_rn(o3, x3);
                 }
+                };
+                if (w == 1.0) run(std::true_type{});  // w * double(s) == double(s)
+                else run(std::false_type{});
             }
         } else {  // cached candidate scores (search_period > 1): this warp's keys
             for (uint32_t u = 0; u < WKEYS / 32; ++u) {
@@ -561,8 +593,11 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             }
         }
         __syncwarp();
-        if (ln == 0) mbar_arrive(&S.empty[slot]);
-        ++c;
+        if (ln == 0) mbar_arrive_u32(empty0 + 8 * slot);
+        if (++slot == NSLOT) {
+            slot = 0;
+            phase ^= 1u;
+        }
         if (!(flags & F_LIST_END)) continue;
         cbar();  // the list is fully accumulated before the next one (or the filter)
         if (!(flags & F_TILE_END)) continue;
@@ -626,7 +661,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     }
                 }
             } else {
-    #pragma unroll 2
+#pragma unroll 2
                 for (uint32_t u = 0; u < WKEYS / 64; ++u) {
                     const uint32_t lp = u * 32 + ln;
                     const uint32_t i0 = kw + 2 * lp;
@@ -733,6 +768,12 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 int b = -1;
                 if (need) b = warp_find_bin(hist, coarse, need, ab);
                 if (tid == 0) {
+                    // the speculative cut must not exceed the threshold bin: every
+                    // key at or above the threshold bin was then counted and logged
+                    const bool fail = need && st.cut_init &&
+                                      (b < 0 || static_cast<uint32_t>(b) < st.cut_init);
+                    S.f_fail = fail ? 1u : 0u;
+                    if (fail) retry_out[atomicAdd(retry_out_count, 1u)] = p;
                     // b < 0: fewer than `need` pool keys (then the cut never rose
                     // and the log holds the whole pool): take them all
                     S.f_take_all = (need && b < 0) ? 1u : 0u;
@@ -743,6 +784,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             }
             for (uint32_t x = tid; x < nw; x += SEL_CT) bm[x] = 0;
             cbar();
+            const bool failed = S.f_fail != 0;
             const uint32_t take_all = S.f_take_all, dsel = S.f_bin;
             const uint32_t rem = need - (take_all ? 0u : min(need, S.f_above));
             const uint32_t nlog = S.wlog[SEL_CW];
@@ -753,139 +795,145 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 while (S.wlog[w + 1] <= e) ++w;
                 return w * wstride + (e - S.wlog[w]);
             };
-            if (need) {
-                constexpr int LOGU = 8;  // entries per thread in flight (the log lives in L2)
-                uint32_t w = 0;
-                for (uint32_t e0 = tid; e0 < nlog; e0 += SEL_CT * LOGU) {
-                    uint32_t ii[LOGU];
-                    double sv[LOGU];
+            if (!failed) {  // (a failed speculation is redone by the retry pass)
+                if (need) {
+                    constexpr int LOGU = 8;  // entries per thread in flight (the log lives in L2)
+                    uint32_t w = 0;
+                    for (uint32_t e0 = tid; e0 < nlog; e0 += SEL_CT * LOGU) {
+                        uint32_t ii[LOGU];
+                        double sv[LOGU];
 #pragma unroll
-                    for (int u = 0; u < LOGU; ++u) {
-                        const uint32_t e = e0 + u * SEL_CT;
-                        const uint32_t x = e < nlog ? lpos(e, w) : 0u;
-                        ii[u] = e < nlog ? __ldcg(log_idx + x) : 0u;
-                        sv[u] = e < nlog ? __ldcg(log_sc + x) : 0.0;
-                    }
+                        for (int u = 0; u < LOGU; ++u) {
+                            const uint32_t e = e0 + u * SEL_CT;
+                            const uint32_t x = e < nlog ? lpos(e, w) : 0u;
+                            ii[u] = e < nlog ? __ldcg(log_idx + x) : 0u;
+                            sv[u] = e < nlog ? __ldcg(log_sc + x) : 0.0;
+                        }
 #pragma unroll
-                    for (int u = 0; u < LOGU; ++u) {
-                        if (e0 + u * SEL_CT >= nlog) break;
-                        const uint32_t b = bin_of(sv[u], lo, scale);
-                        if (take_all || b > dsel) {
-                            set_bit(bm, ii[u]);
-                        } else if (b == dsel) {
-                            const uint32_t k = atomicAdd(&S.nbkt, 1u);
-                            if (k < static_cast<uint32_t>(BKT)) {
-                                bkey[k] = ordkey(sv[u]);
-                                bidx[k] = ii[u];
+                        for (int u = 0; u < LOGU; ++u) {
+                            if (e0 + u * SEL_CT >= nlog) break;
+                            const uint32_t b = bin_of(sv[u], lo, scale);
+                            if (take_all || b > dsel) {
+                                set_bit(bm, ii[u]);
+                            } else if (b == dsel) {
+                                const uint32_t k = atomicAdd(&S.nbkt, 1u);
+                                if (k < static_cast<uint32_t>(BKT)) {
+                                    bkey[k] = ordkey(sv[u]);
+                                    bidx[k] = ii[u];
+                                }
                             }
                         }
                     }
                 }
-            }
-            cbar();
-            const uint32_t nb = S.nbkt;
-            if (need && !take_all && rem) {
-                if (nb <= static_cast<uint32_t>(RANK_DIRECT)) {
-                    // direct ranking: member e is selected iff fewer than rem beat it
-                    for (uint32_t e = tid; e < nb; e += SEL_CT) {
-                        const unsigned long long ke = bkey[e];
-                        const uint32_t ie = bidx[e];
-                        uint32_t r = 0;
-                        for (uint32_t f = 0; f < nb; ++f) {
-                            const unsigned long long kf = bkey[f];
-                            r += (kf > ke) || (kf == ke && bidx[f] < ie);
+                cbar();
+                const uint32_t nb = S.nbkt;
+                if (need && !take_all && rem) {
+                    if (nb <= static_cast<uint32_t>(RANK_DIRECT)) {
+                        // direct ranking: member e is selected iff fewer than rem beat it
+                        for (uint32_t e = tid; e < nb; e += SEL_CT) {
+                            const unsigned long long ke = bkey[e];
+                            const uint32_t ie = bidx[e];
+                            uint32_t r = 0;
+                            for (uint32_t f = 0; f < nb; ++f) {
+                                const unsigned long long kf = bkey[f];
+                                r += (kf > ke) || (kf == ke && bidx[f] < ie);
+                            }
+                            if (r < rem) set_bit(bm, ie);
                         }
-                        if (r < rem) set_bit(bm, ie);
-                    }
-                } else if (nb <= static_cast<uint32_t>(BKT)) {
-                    radix_kth(S, hist, nb, rem, [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
-                        k = bkey[e];
-                        ix = bidx[e];
-                        return true;
-                    });
-                    const unsigned long long tk = S.tk;
-                    const uint32_t tx = S.tx;
-                    for (uint32_t e = tid; e < nb; e += SEL_CT) {
-                        const unsigned long long k = bkey[e];
-                        if (k > tk || (k == tk && bidx[e] < tx)) set_bit(bm, bidx[e]);
-                    }
-                } else {  // huge threshold bin: rank straight from the log
-                    auto member = [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
-                        uint32_t w = 0;
-                        const uint32_t x = lpos(e, w);
-                        const double s = __ldcg(log_sc + x);
-                        if (bin_of(s, lo, scale) != dsel) return false;
-                        k = ordkey(s);
-                        ix = __ldcg(log_idx + x);
-                        return true;
-                    };
-                    radix_kth(S, hist, nlog, rem, member);
-                    const unsigned long long tk = S.tk;
-                    const uint32_t tx = S.tx;
-                    for (uint32_t e = tid; e < nlog; e += SEL_CT) {
-                        unsigned long long k;
-                        uint32_t ix;
-                        if (member(e, k, ix) && (k > tk || (k == tk && ix < tx))) set_bit(bm, ix);
-                    }
-                }
-            }
-            // window passthrough (or the newest K when K <= R)
-            for (uint32_t i = f_lo + tid; i < N; i += SEL_CT) set_bit(bm, i);
-            cbar();
-            // ---- count, newest-first padding, ascending emit ----
-            const uint32_t wpt = div_up(nw, SEL_CT);
-            const uint32_t w0 = min(nw, tid * wpt), w1 = min(nw, w0 + wpt);
-            auto valid = [&](uint32_t x) {
-                return x + 1 < nw || (N & 31) == 0 ? 0xffffffffu : ((1u << (N & 31)) - 1u);
-            };
-            uint32_t cnt = 0, zeros = 0;
-            for (uint32_t x = w0; x < w1; ++x) {
-                const uint32_t b = bm[x];
-                cnt += __popc(b);
-                zeros += __popc(~b & valid(x));
-            }
-            uint32_t total;
-            cscan(S, cnt, total);
-            if (total < K) {  // pad with the newest untaken keys (retrieval.cpp:218-225)
-                const uint32_t pad = K - total;
-                uint32_t zt;
-                const uint32_t zbelow = cscan(S, zeros, zt);
-                const uint32_t zabove = zt - zbelow - zeros;  // zeros in higher threads
-                uint32_t take = pad > zabove ? min(pad - zabove, zeros) : 0u;
-                for (uint32_t x = w1; x > w0 && take;) {
-                    --x;
-                    uint32_t z = ~bm[x] & valid(x);
-                    while (z && take) {
-                        const int hb = 31 - __clz(z);
-                        bm[x] |= 1u << hb;
-                        z &= ~(1u << hb);
-                        --take;
-                        ++cnt;
+                    } else if (nb <= static_cast<uint32_t>(BKT)) {
+                        radix_kth(S, hist, nb, rem, [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+                            k = bkey[e];
+                            ix = bidx[e];
+                            return true;
+                        });
+                        const unsigned long long tk = S.tk;
+                        const uint32_t tx = S.tx;
+                        for (uint32_t e = tid; e < nb; e += SEL_CT) {
+                            const unsigned long long k = bkey[e];
+                            if (k > tk || (k == tk && bidx[e] < tx)) set_bit(bm, bidx[e]);
+                        }
+                    } else {  // huge threshold bin: rank straight from the log
+                        auto member = [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+                            uint32_t w = 0;
+                            const uint32_t x = lpos(e, w);
+                            const double s = __ldcg(log_sc + x);
+                            if (bin_of(s, lo, scale) != dsel) return false;
+                            k = ordkey(s);
+                            ix = __ldcg(log_idx + x);
+                            return true;
+                        };
+                        radix_kth(S, hist, nlog, rem, member);
+                        const unsigned long long tk = S.tk;
+                        const uint32_t tx = S.tx;
+                        for (uint32_t e = tid; e < nlog; e += SEL_CT) {
+                            unsigned long long k;
+                            uint32_t ix;
+                            if (member(e, k, ix) && (k > tk || (k == tk && ix < tx))) set_bit(bm, ix);
+                        }
                     }
                 }
-            }
-            const uint32_t at = cscan(S, cnt, total);
-            {
-                uint32_t pos = at;
+                // window passthrough (or the newest K when K <= R)
+                for (uint32_t i = f_lo + tid; i < N; i += SEL_CT) set_bit(bm, i);
+                cbar();
+                // ---- count, newest-first padding, ascending emit ----
+                const uint32_t wpt = div_up(nw, SEL_CT);
+                const uint32_t w0 = min(nw, tid * wpt), w1 = min(nw, w0 + wpt);
+                auto valid = [&](uint32_t x) {
+                    return x + 1 < nw || (N & 31) == 0 ? 0xffffffffu : ((1u << (N & 31)) - 1u);
+                };
+                uint32_t cnt = 0, zeros = 0;
                 for (uint32_t x = w0; x < w1; ++x) {
-                    uint32_t b = bm[x];
-                    while (b) {
-                        const int lb = __ffs(b) - 1;
-                        sel[pos++] = x * 32 + lb;
-                        b &= b - 1;
+                    const uint32_t b = bm[x];
+                    cnt += __popc(b);
+                    zeros += __popc(~b & valid(x));
+                }
+                uint32_t total;
+                cscan(S, cnt, total);
+                if (total < K) {  // pad with the newest untaken keys (retrieval.cpp:218-225)
+                    const uint32_t pad = K - total;
+                    uint32_t zt;
+                    const uint32_t zbelow = cscan(S, zeros, zt);
+                    const uint32_t zabove = zt - zbelow - zeros;  // zeros in higher threads
+                    uint32_t take = pad > zabove ? min(pad - zabove, zeros) : 0u;
+                    for (uint32_t x = w1; x > w0 && take;) {
+                        --x;
+                        uint32_t z = ~bm[x] & valid(x);
+                        while (z && take) {
+                            const int hb = 31 - __clz(z);
+                            bm[x] |= 1u << hb;
+                            z &= ~(1u << hb);
+                            --take;
+                            ++cnt;
+                        }
                     }
                 }
-            }
-            if (tid == 0) {
-                reinterpret_cast<DecodeReport*>(rep)->k = K;
-                if (prof) {
-                    prof[2] = gtimer();
-                    prof[3] = nlog;
-                    prof[4] = nb;
-                    prof[5] = static_cast<unsigned long long>(__double_as_longlong(lo));
-                    prof[6] = static_cast<unsigned long long>(
-                        __double_as_longlong(scale > 0.0 ? lo + NB / scale : lo));
-                    prof[7] = S.f_take_all | (dsel << 1);
+                const uint32_t at = cscan(S, cnt, total);
+                {
+                    uint32_t pos = at;
+                    for (uint32_t x = w0; x < w1; ++x) {
+                        uint32_t b = bm[x];
+                        while (b) {
+                            const int lb = __ffs(b) - 1;
+                            sel[pos++] = x * 32 + lb;
+                            b &= b - 1;
+                        }
+                    }
+                }
+                if (tid == 0) {
+                    reinterpret_cast<DecodeReport*>(rep)->k = K;
+                    if (prof) {
+                        prof[2] = gtimer();
+                        prof[3] = nlog;
+                        prof[4] = nb;
+                        prof[5] = static_cast<unsigned long long>(__double_as_longlong(lo));
+                        prof[6] = static_cast<unsigned long long>(
+                            __double_as_longlong(scale > 0.0 ? lo + NB / scale : lo));
+                        prof[7] = S.f_take_all | (dsel << 1);
+                    }
+                }
+                if (tid == 0) {  // next step's speculative cut: this threshold bin's lower edge
+                    st.hint[0] = scale > 0.0 ? lo + static_cast<double>(dsel) / scale : lo;
+                    st.hint[1] = (need && !take_all) ? 1.0 : 0.0;
                 }
             }
             cbar();  // bitmap emitted, scratch free
@@ -897,9 +945,13 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 S.nbkt = 0;
             }
             wlog_n = 0;
-            p += gridDim.x;
-            if (p < nprob) setup_problem(S, probs, plans, p, st);  // ends with a barrier
-            else cbar();
+            kk += gridDim.x;
+            if (kk < nwork) {
+                p = prob_of(kk);
+                setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
+            } else {
+                cbar();
+            }
         }
     }
 }
@@ -916,12 +968,16 @@ uint32_t select_grid(uint32_t nprob, int num_sms) {
 
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
+                          const uint32_t* retry_in, const uint32_t* retry_in_count,
+                          uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
                           cudaStream_t st) {
     const size_t smem = select_smem();
     cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap);
+    select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap,
+                                                   retry_in, retry_in_count, retry_out,
+                                                   retry_out_count, spec_keep);
     return cudaGetLastError();
 }
 

@@ -79,6 +79,22 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, uint32_
         : "memory");
 }
 
+// variants on precomputed 32-bit shared addresses (hot loops)
+__device__ __forceinline__ void mbar_wait_sleep_u32(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITU_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITU_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
     asm volatile(
         "{\n"
