@@ -149,6 +149,8 @@ struct csattn_ctx_s {
     DevMem plans;           // route.cu -> select.cu routing plans
     DevMem log_idx, log_sc; // select.cu candidate logs: log_rows x log_cap
     DevMem retry;           // select.cu retry list (speculative cut too high)
+    DevMem ulog_idx, ulog_sc, umeta;  // split select: per part-unit logs + histograms
+    bool no_split = std::getenv("CSATTN_NO_SPLIT") != nullptr;
     uint64_t log_cap = 0, log_rows = 0;
     int num_sms = 148;
     // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
@@ -558,7 +560,28 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                          ctx->stream),
        "route launch");
     const uint32_t sgrid = csa::select_grid(static_cast<uint32_t>(nq), ctx->num_sms);
-    if (maxN > ctx->log_cap || sgrid > ctx->log_rows) {
+    // Split select for small batches: with fewer problems than CTA slots, each
+    // problem's key range is cut into `split` part units (>= one tile each)
+    // that run in parallel, then merged (select_merge_kernel).
+    const uint64_t tile = csa::select_tile_keys();
+    uint64_t min_tiles = ~0ull, max_tiles = 0;
+    for (uint64_t i = 0; i < ns; ++i) {
+        const uint64_t nt = (ss[i]->N + tile - 1) / tile;
+        min_tiles = std::min(min_tiles, nt);
+        max_tiles = std::max(max_tiles, nt);
+    }
+    uint32_t split = 1;
+    const uint64_t slots = 2ull * static_cast<uint64_t>(ctx->num_sms);  // select CTAs resident
+    if (nq < slots && !ctx->no_split) {
+        split = static_cast<uint32_t>((2ull * ctx->num_sms + nq - 1) / nq);
+        split = static_cast<uint32_t>(std::min<uint64_t>(std::min<uint64_t>(split, 16), min_tiles));
+        split = std::max<uint32_t>(split, 1);
+    }
+    // retry list of problems whose speculative cut proved too high: [count, ids...]
+    ctx->retry.ensure((nq + 1) * 4);
+    ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
+    uint32_t* const rcount = ctx->retry.as<uint32_t>();
+    if (maxN > ctx->log_cap || sgrid > ctx->log_rows) {  // non-split / retry-pass logs
         // sized for the sessions' full capacity, so it is not re-grown every step
         uint64_t cap = maxN;
         for (uint64_t i = 0; i < ns; ++i) cap = std::max<uint64_t>(cap, ss[i]->h.max_ctx);
@@ -568,19 +591,37 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->log_idx.alloc(ctx->log_rows * ctx->log_cap * 4);
         ctx->log_sc.alloc(ctx->log_rows * ctx->log_cap * 8);
     }
-    // retry list of problems whose speculative cut proved too high: [count, ids...]
-    ctx->retry.ensure((nq + 1) * 4);
-    ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
-    uint32_t* const rcount = ctx->retry.as<uint32_t>();
+    if (split == 1) {
+        ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
+                              sgrid, ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
+                              static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
+                              rcount, ctx->spec_keep, 1, nullptr, ctx->stream),
+           "select launch");
+    } else {
+        // per-unit logs: a unit has at most ceil(max_tiles / split) tiles
+        const uint64_t ucap = (max_tiles + split - 1) / split * tile;
+        const uint64_t units = nq * split;
+        ctx->ulog_idx.ensure(units * ucap * 4);
+        ctx->ulog_sc.ensure(units * ucap * 8);
+        ctx->umeta.ensure(units * csa::select_unit_meta_words() * 4);
+        const uint32_t ugrid = static_cast<uint32_t>(std::min<uint64_t>(units, slots));
+        ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
+                              ugrid, ctx->ulog_idx.as<uint32_t>(), ctx->ulog_sc.as<double>(),
+                              static_cast<uint32_t>(ucap), nullptr, nullptr, nullptr, nullptr,
+                              ctx->spec_keep, split, ctx->umeta.as<uint32_t>(), ctx->stream),
+           "select (split) launch");
+        ck(csa::launch_select_merge(dprobs, ctx->plans.as<csa::RoutePlan>(),
+                                    static_cast<uint32_t>(nq), split, ctx->umeta.as<uint32_t>(),
+                                    ctx->ulog_idx.as<uint32_t>(), ctx->ulog_sc.as<double>(),
+                                    static_cast<uint32_t>(ucap), ctx->spec_keep, rcount + 1,
+                                    rcount, ctx->stream),
+           "select merge launch");
+    }
+    // second pass over the (usually empty) retry list, without speculation
     ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
                           ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
-                          static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
-                          rcount, ctx->spec_keep, ctx->stream),
-       "select launch");
-    ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
-                          ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
-                          static_cast<uint32_t>(ctx->log_cap), rcount + 1, rcount, nullptr,
-                          nullptr, 0.0, ctx->stream),
+                          static_cast<uint32_t>(ctx->log_cap), rcount + 1, rcount, nullptr, nullptr,
+                          0.0, 1, nullptr, ctx->stream),
        "select retry launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),

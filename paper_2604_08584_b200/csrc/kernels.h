@@ -25,7 +25,16 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
                           const uint32_t* retry_in, const uint32_t* retry_in_count,
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
-                          cudaStream_t st);
+                          uint32_t split, uint32_t* unit_meta, cudaStream_t st);
+// split > 1: each problem's tiles are cut into `split` part units (logs of
+// log_cap entries each, unit_meta: select_unit_meta_words() per unit) and
+// finalised by the merge kernel (one CTA per problem).
+uint32_t select_unit_meta_words();
+uint32_t select_tile_keys();
+cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                                uint32_t split, const uint32_t* unit_meta, const uint32_t* log_idx,
+                                const double* log_sc, uint32_t log_cap, double spec_keep,
+                                uint32_t* retry_out, uint32_t* retry_out_count, cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
 constexpr uint32_t ATT_ROWS = 256;

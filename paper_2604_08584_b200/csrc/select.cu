@@ -60,9 +60,13 @@ constexpr int NCB = NB / 32;                 // coarse bins (32 fine bins each)
 constexpr int BKT = 512;                     // threshold-bin members ranked in smem
 constexpr int RANK_DIRECT = 384;             // O(n^2) ranking up to this size
 constexpr uint32_t F_LIST_END = 1, F_TILE_END = 2, F_PROB_END = 4;
+constexpr int MAXPART = 16;                  // key-range parts of a split problem
+constexpr uint32_t MAXSEG = MAXPART * 8;     // log segments (parts x warps)
+constexpr uint32_t UNIT_META = 2048 + 64 + 8;  // per part unit: hist, coarse, per-warp log lengths
 constexpr unsigned long long ABSENT = 0x7ff4deadbeef0000ull;  // NaN box: key not gathered
 static_assert(TILE * 64 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bits");
 static_assert(SELECT_MAX_CONTEXT / TILE <= 128 && MAXL < 127, "chunk info fields");
+static_assert(UNIT_META == NB + NCB + SEL_CW && SEL_CW == 8, "unit metadata layout");
 
 // One ring chunk: info = list | flags << 7 | tile << 10; entries at table
 // positions [lo, hi), staged from position `base` (even, 16-byte aligned).
@@ -76,7 +80,8 @@ struct SelHdr {
     uint32_t plist[MAXL];  // producer: table ids of its current problem
     double cw[MAXL];       // consumers: weight of each gathered list
     uint32_t cut, nbkt;
-    uint32_t wlog[SEL_CW + 1];  // per-warp candidate-log lengths, then prefix
+    // candidate-log segments of the problem being finalised
+    uint32_t seg_len[MAXSEG], seg_off[MAXSEG], seg_pre[MAXSEG + 1];
     uint32_t wsum[SEL_CW];
     // final-phase broadcasts
     uint32_t f_bin, f_above, f_count, f_take_all, f_fail;
@@ -387,19 +392,227 @@ __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const Route
     if (st.prof && tid == 0) st.prof[0] = gtimer();
 }
 
+
+// The final selection of one problem from its histogram (hist/coarse, complete
+// at and above every cut used) and its candidate log, given as nseg segments
+// (S.seg_off[k], S.seg_len[k]) of log_idx/log_sc. Consumer threads only (named
+// barrier 1). Leaves the bitmap region dirty; the caller resets its scratch.
+__device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_t* hist,
+                             uint32_t* coarse, uint32_t* bm, unsigned long long* bkey,
+                             uint32_t* bidx, const uint32_t* log_idx, const double* log_sc,
+                             uint32_t nseg, uint32_t* retry_out, uint32_t* retry_out_count) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t N = st.N, K = st.K, need = st.need, f_lo = st.f_lo;
+    const double lo = st.lo, scale = st.scale;
+    unsigned long long* const prof = st.prof;
+    uint32_t* const sel = st.sel;
+    uint32_t* const rep = st.rep;
+    if (tid == 0) {  // exclusive prefix of the segment lengths
+        uint32_t run = 0;
+        for (uint32_t k = 0; k <= nseg; ++k) {
+            const uint32_t x = k < nseg ? S.seg_len[k] : 0u;
+            S.seg_pre[k] = run;
+            run += x;
+        }
+    }
+    if (prof && tid == 0) prof[1] = gtimer();
+    const uint32_t nw = div_up(N, 32);
+    if (tid < 32) {
+        uint32_t ab = 0;
+        int b = -1;
+        if (need) b = warp_find_bin(hist, coarse, need, ab);
+        if (tid == 0) {
+            // the speculative cut must not exceed the threshold bin: every
+            // key at or above the threshold bin was then counted and logged
+            const bool fail = need && st.cut_init &&
+                              (b < 0 || static_cast<uint32_t>(b) < st.cut_init);
+            S.f_fail = fail ? 1u : 0u;
+            if (fail) retry_out[atomicAdd(retry_out_count, 1u)] = p;
+            // b < 0: fewer than `need` pool keys (then the cut never rose
+            // and the log holds the whole pool): take them all
+            S.f_take_all = (need && b < 0) ? 1u : 0u;
+            S.f_bin = b < 0 ? 0u : static_cast<uint32_t>(b);
+            S.f_above = ab;
+            S.f_count = b < 0 ? 0u : hist[b];
+        }
+    }
+    for (uint32_t x = tid; x < nw; x += SEL_CT) bm[x] = 0;
+    cbar();
+    const bool failed = S.f_fail != 0;
+    const uint32_t take_all = S.f_take_all, dsel = S.f_bin;
+    const uint32_t rem = need - (take_all ? 0u : min(need, S.f_above));
+    const uint32_t nlog = S.seg_pre[nseg];
+    // flat log index -> log position through the segment table (search from
+    // `w`: the indices one thread visits only grow)
+    auto lpos = [&](uint32_t e, uint32_t& w) {
+        while (S.seg_pre[w + 1] <= e) ++w;
+        return S.seg_off[w] + (e - S.seg_pre[w]);
+    };
+    if (!failed) {  // (a failed speculation is redone by the retry pass)
+        if (need) {
+            constexpr int LOGU = 8;  // entries per thread in flight (the log lives in L2)
+            uint32_t w = 0;
+            for (uint32_t e0 = tid; e0 < nlog; e0 += SEL_CT * LOGU) {
+                uint32_t ii[LOGU];
+                double sv[LOGU];
+#pragma unroll
+                for (int u = 0; u < LOGU; ++u) {
+                    const uint32_t e = e0 + u * SEL_CT;
+                    const uint32_t x = e < nlog ? lpos(e, w) : 0u;
+                    ii[u] = e < nlog ? __ldcg(log_idx + x) : 0u;
+                    sv[u] = e < nlog ? __ldcg(log_sc + x) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < LOGU; ++u) {
+                    if (e0 + u * SEL_CT >= nlog) break;
+                    const uint32_t b = bin_of(sv[u], lo, scale);
+                    if (take_all || b > dsel) {
+                        set_bit(bm, ii[u]);
+                    } else if (b == dsel) {
+                        const uint32_t k = atomicAdd(&S.nbkt, 1u);
+                        if (k < static_cast<uint32_t>(BKT)) {
+                            bkey[k] = ordkey(sv[u]);
+                            bidx[k] = ii[u];
+                        }
+                    }
+                }
+            }
+        }
+        cbar();
+        const uint32_t nb = S.nbkt;
+        if (need && !take_all && rem) {
+            if (nb <= static_cast<uint32_t>(RANK_DIRECT)) {
+                // direct ranking: member e is selected iff fewer than rem beat it
+                for (uint32_t e = tid; e < nb; e += SEL_CT) {
+                    const unsigned long long ke = bkey[e];
+                    const uint32_t ie = bidx[e];
+                    uint32_t r = 0;
+                    for (uint32_t f = 0; f < nb; ++f) {
+                        const unsigned long long kf = bkey[f];
+                        r += (kf > ke) || (kf == ke && bidx[f] < ie);
+                    }
+                    if (r < rem) set_bit(bm, ie);
+                }
+            } else if (nb <= static_cast<uint32_t>(BKT)) {
+                radix_kth(S, hist, nb, rem, [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+                    k = bkey[e];
+                    ix = bidx[e];
+                    return true;
+                });
+                const unsigned long long tk = S.tk;
+                const uint32_t tx = S.tx;
+                for (uint32_t e = tid; e < nb; e += SEL_CT) {
+                    const unsigned long long k = bkey[e];
+                    if (k > tk || (k == tk && bidx[e] < tx)) set_bit(bm, bidx[e]);
+                }
+            } else {  // huge threshold bin: rank straight from the log
+                auto member = [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+                    uint32_t w = 0;
+                    const uint32_t x = lpos(e, w);
+                    const double s = __ldcg(log_sc + x);
+                    if (bin_of(s, lo, scale) != dsel) return false;
+                    k = ordkey(s);
+                    ix = __ldcg(log_idx + x);
+                    return true;
+                };
+                radix_kth(S, hist, nlog, rem, member);
+                const unsigned long long tk = S.tk;
+                const uint32_t tx = S.tx;
+                for (uint32_t e = tid; e < nlog; e += SEL_CT) {
+                    unsigned long long k;
+                    uint32_t ix;
+                    if (member(e, k, ix) && (k > tk || (k == tk && ix < tx))) set_bit(bm, ix);
+                }
+            }
+        }
+        // window passthrough (or the newest K when K <= R)
+        for (uint32_t i = f_lo + tid; i < N; i += SEL_CT) set_bit(bm, i);
+        cbar();
+        // ---- count, newest-first padding, ascending emit ----
+        const uint32_t wpt = div_up(nw, SEL_CT);
+        const uint32_t w0 = min(nw, tid * wpt), w1 = min(nw, w0 + wpt);
+        auto valid = [&](uint32_t x) {
+            return x + 1 < nw || (N & 31) == 0 ? 0xffffffffu : ((1u << (N & 31)) - 1u);
+        };
+        uint32_t cnt = 0, zeros = 0;
+        for (uint32_t x = w0; x < w1; ++x) {
+            const uint32_t b = bm[x];
+            cnt += __popc(b);
+            zeros += __popc(~b & valid(x));
+        }
+        uint32_t total;
+        cscan(S, cnt, total);
+        if (total < K) {  // pad with the newest untaken keys (retrieval.cpp:218-225)
+            const uint32_t pad = K - total;
+            uint32_t zt;
+            const uint32_t zbelow = cscan(S, zeros, zt);
+            const uint32_t zabove = zt - zbelow - zeros;  // zeros in higher threads
+            uint32_t take = pad > zabove ? min(pad - zabove, zeros) : 0u;
+            for (uint32_t x = w1; x > w0 && take;) {
+                --x;
+                uint32_t z = ~bm[x] & valid(x);
+                while (z && take) {
+                    const int hb = 31 - __clz(z);
+                    bm[x] |= 1u << hb;
+                    z &= ~(1u << hb);
+                    --take;
+                    ++cnt;
+                }
+            }
+        }
+        const uint32_t at = cscan(S, cnt, total);
+        {
+            uint32_t pos = at;
+            for (uint32_t x = w0; x < w1; ++x) {
+                uint32_t b = bm[x];
+                while (b) {
+                    const int lb = __ffs(b) - 1;
+                    sel[pos++] = x * 32 + lb;
+                    b &= b - 1;
+                }
+            }
+        }
+        if (tid == 0) {
+            reinterpret_cast<DecodeReport*>(rep)->k = K;
+            if (prof) {
+                prof[2] = gtimer();
+                prof[3] = nlog;
+                prof[4] = nb;
+                prof[5] = static_cast<unsigned long long>(__double_as_longlong(lo));
+                prof[6] = static_cast<unsigned long long>(
+                    __double_as_longlong(scale > 0.0 ? lo + NB / scale : lo));
+                prof[7] = S.f_take_all | (dsel << 1);
+            }
+        }
+        if (tid == 0) {  // next step's speculative cut: this threshold bin's lower edge
+            st.hint[0] = scale > 0.0 ? lo + static_cast<double>(dsel) / scale : lo;
+            st.hint[1] = (need && !take_all) ? 1.0 : 0.0;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(SEL_THREADS, 2)
 select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
               uint32_t nprob, uint32_t* __restrict__ log_idx_all, double* __restrict__ log_sc_all,
               uint32_t log_cap, const uint32_t* __restrict__ retry_in,
               const uint32_t* __restrict__ retry_in_count, uint32_t* __restrict__ retry_out,
-              uint32_t* __restrict__ retry_out_count, double spec_keep) {
+              uint32_t* __restrict__ retry_out_count, double spec_keep, uint32_t split,
+              uint32_t* __restrict__ unit_meta) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    // the problem sequence of this CTA: b, b + grid, ... over all problems, or
-    // over the retry list (second pass)
-    const uint32_t nwork = retry_in ? __ldcg(retry_in_count) : nprob;
+    // The work sequence of this CTA: units b, b + grid, ... A unit is problem
+    // u / split, tiles [part u % split] of its key range; split == 1 (one unit
+    // per problem, finalised here) or split > 1 (part units dump histogram and
+    // log lengths to unit_meta; select_merge_kernel finalises). The retry pass
+    // walks the retry list (split == 1 only).
+    const uint32_t nwork = retry_in ? __ldcg(retry_in_count) : nprob * split;
     if (blockIdx.x >= nwork) return;
-    auto prob_of = [&](uint32_t k) { return retry_in ? __ldcg(retry_in + k) : k; };
-    const bool speculate = retry_out != nullptr;
+    auto prob_of = [&](uint32_t k) { return retry_in ? __ldcg(retry_in + k) : k / split; };
+    auto tiles_of = [&](uint32_t k, uint32_t N, uint32_t& tl, uint32_t& th) {
+        const uint32_t nt = div_up(N, TILE), j = retry_in ? 0u : k % split;
+        tl = (nt * j) / split;
+        th = (nt * (j + 1)) / split;
+    };
+    const bool speculate = (retry_out != nullptr || split > 1) && !retry_in;
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
     unsigned char* p0 = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
     double* acc = reinterpret_cast<double*>(p0);                    // TILE fp64
@@ -455,7 +668,8 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             const DecodeProblem& P = probs[p];
             const SessionDev& sd = *P.s;
             const uint32_t N = P.N;
-            const uint32_t ntile = div_up(N, TILE);
+            uint32_t tl, ntile;
+            tiles_of(k, N, tl, ntile);  // this unit's tiles [tl, ntile)
             uint32_t nl = 0;
             if (P.mode & MODE_SEARCH) {
                 nl = __ldcg(&plans[p].nl);
@@ -476,9 +690,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 return kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
                                       : __ldcg(n_used + t);
             };
-            uint32_t a0 = bound(0, ln), a1 = bound(0, ln + 32);
-            uint32_t b0 = bound(1, ln), b1 = bound(1, ln + 32);
-            for (uint32_t tile = 0; tile < ntile; ++tile) {
+            uint32_t a0 = bound(tl, ln), a1 = bound(tl, ln + 32);
+            uint32_t b0 = bound(tl + 1, ln), b1 = bound(tl + 1, ln + 32);
+            for (uint32_t tile = tl; tile < ntile; ++tile) {
                 const uint32_t tflag = F_TILE_END | (tile + 1 == ntile ? F_PROB_END : 0u);
                 if (nl == 0) {  // cached scores: one data-less chunk per tile
                     publish(CACHE_LIST | ((F_LIST_END | tflag) << 7) | (tile << 10), 0, 0, 0,
@@ -521,10 +735,16 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     uint32_t p = prob_of(kk);
     ProbState st;
     setup_problem(S, probs, plans, p, st, speculate, spec_keep);
-    // warp w logs into its own region (it owns 1/16 of every tile's keys)
+    // warp w logs into its own region (it owns 1/8 of every tile's keys): the
+    // CTA's log (split == 1) or the unit's (split > 1, log_cap per unit)
     uint32_t wlog_n = 0;
-    uint32_t* const wlog_idx = log_idx + static_cast<size_t>(wid) * (log_cap / SEL_CW);
-    double* const wlog_sc = log_sc + static_cast<size_t>(wid) * (log_cap / SEL_CW);
+    auto log_base = [&](uint32_t k) -> size_t {
+        return (split == 1 ? static_cast<size_t>(0) : static_cast<size_t>(k) * log_cap -
+                                                          static_cast<size_t>(blockIdx.x) * log_cap) +
+               static_cast<size_t>(wid) * (log_cap / SEL_CW);
+    };
+    uint32_t* wlog_idx = log_idx + log_base(kk);
+    double* wlog_sc = log_sc + log_base(kk);
     uint16_t* const wcidx = cidx + wid * WKEYS;
     double* const wacc = acc + wid * WKEYS;
     uint32_t slot = 0, phase = 0;  // ring position of the next chunk
@@ -744,198 +964,40 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
         cbar();  // accumulator clear before the next tile's first list
         if (!(flags & F_PROB_END)) continue;
 
+        if (split > 1) {  // part unit: hand histogram + log lengths to the merge kernel
+            uint32_t* const um = unit_meta + static_cast<size_t>(kk) * UNIT_META;
+            if (ln == 0) um[NB + NCB + wid] = wlog_n;
+            cbar();
+            for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) {
+                um[x] = hist[x];
+                hist[x] = 0;
+            }
+            if (tid == 0) {
+                S.cut = 0;
+                S.nbkt = 0;
+            }
+            wlog_n = 0;
+            kk += gridDim.x;
+            if (kk < nwork) {
+                p = prob_of(kk);
+                wlog_idx = log_idx + log_base(kk);
+                wlog_sc = log_sc + log_base(kk);
+                setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
+            } else {
+                cbar();
+            }
+            continue;
+        }
         // ======================= final selection =======================
         {
-            const uint32_t N = st.N, K = st.K, need = st.need, f_lo = st.f_lo;
-            const double lo = st.lo, scale = st.scale;
-            unsigned long long* const prof = st.prof;
-            uint32_t* const sel = st.sel;
-            uint32_t* const rep = st.rep;
-            if (ln == 0) S.wlog[wid] = wlog_n;
+            if (ln == 0) {  // this CTA's log: one segment per warp
+                S.seg_len[wid] = wlog_n;
+                S.seg_off[wid] = wid * (log_cap / SEL_CW);
+            }
             cbar();  // every warp has logged its keys
-            if (tid == 0) {  // exclusive prefix of the per-warp log lengths
-                uint32_t run = 0;
-                for (int w = 0; w <= SEL_CW; ++w) {
-                    const uint32_t x = w < SEL_CW ? S.wlog[w] : 0u;
-                    S.wlog[w] = run;
-                    run += x;
-                }
-            }
-            if (prof && tid == 0) prof[1] = gtimer();
-            const uint32_t nw = div_up(N, 32);
-            if (tid < 32) {
-                uint32_t ab = 0;
-                int b = -1;
-                if (need) b = warp_find_bin(hist, coarse, need, ab);
-                if (tid == 0) {
-                    // the speculative cut must not exceed the threshold bin: every
-                    // key at or above the threshold bin was then counted and logged
-                    const bool fail = need && st.cut_init &&
-                                      (b < 0 || static_cast<uint32_t>(b) < st.cut_init);
-                    S.f_fail = fail ? 1u : 0u;
-                    if (fail) retry_out[atomicAdd(retry_out_count, 1u)] = p;
-                    // b < 0: fewer than `need` pool keys (then the cut never rose
-                    // and the log holds the whole pool): take them all
-                    S.f_take_all = (need && b < 0) ? 1u : 0u;
-                    S.f_bin = b < 0 ? 0u : static_cast<uint32_t>(b);
-                    S.f_above = ab;
-                    S.f_count = b < 0 ? 0u : hist[b];
-                }
-            }
-            for (uint32_t x = tid; x < nw; x += SEL_CT) bm[x] = 0;
-            cbar();
-            const bool failed = S.f_fail != 0;
-            const uint32_t take_all = S.f_take_all, dsel = S.f_bin;
-            const uint32_t rem = need - (take_all ? 0u : min(need, S.f_above));
-            const uint32_t nlog = S.wlog[SEL_CW];
-            const uint32_t wstride = log_cap / SEL_CW;
-            // flat log index -> slot in the per-warp regions (search from `w`,
-            // indices visited by one thread only grow)
-            auto lpos = [&](uint32_t e, uint32_t& w) {
-                while (S.wlog[w + 1] <= e) ++w;
-                return w * wstride + (e - S.wlog[w]);
-            };
-            if (!failed) {  // (a failed speculation is redone by the retry pass)
-                if (need) {
-                    constexpr int LOGU = 8;  // entries per thread in flight (the log lives in L2)
-                    uint32_t w = 0;
-                    for (uint32_t e0 = tid; e0 < nlog; e0 += SEL_CT * LOGU) {
-                        uint32_t ii[LOGU];
-                        double sv[LOGU];
-#pragma unroll
-                        for (int u = 0; u < LOGU; ++u) {
-                            const uint32_t e = e0 + u * SEL_CT;
-                            const uint32_t x = e < nlog ? lpos(e, w) : 0u;
-                            ii[u] = e < nlog ? __ldcg(log_idx + x) : 0u;
-                            sv[u] = e < nlog ? __ldcg(log_sc + x) : 0.0;
-                        }
-#pragma unroll
-                        for (int u = 0; u < LOGU; ++u) {
-                            if (e0 + u * SEL_CT >= nlog) break;
-                            const uint32_t b = bin_of(sv[u], lo, scale);
-                            if (take_all || b > dsel) {
-                                set_bit(bm, ii[u]);
-                            } else if (b == dsel) {
-                                const uint32_t k = atomicAdd(&S.nbkt, 1u);
-                                if (k < static_cast<uint32_t>(BKT)) {
-                                    bkey[k] = ordkey(sv[u]);
-                                    bidx[k] = ii[u];
-                                }
-                            }
-                        }
-                    }
-                }
-                cbar();
-                const uint32_t nb = S.nbkt;
-                if (need && !take_all && rem) {
-                    if (nb <= static_cast<uint32_t>(RANK_DIRECT)) {
-                        // direct ranking: member e is selected iff fewer than rem beat it
-                        for (uint32_t e = tid; e < nb; e += SEL_CT) {
-                            const unsigned long long ke = bkey[e];
-                            const uint32_t ie = bidx[e];
-                            uint32_t r = 0;
-                            for (uint32_t f = 0; f < nb; ++f) {
-                                const unsigned long long kf = bkey[f];
-                                r += (kf > ke) || (kf == ke && bidx[f] < ie);
-                            }
-                            if (r < rem) set_bit(bm, ie);
-                        }
-                    } else if (nb <= static_cast<uint32_t>(BKT)) {
-                        radix_kth(S, hist, nb, rem, [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
-                            k = bkey[e];
-                            ix = bidx[e];
-                            return true;
-                        });
-                        const unsigned long long tk = S.tk;
-                        const uint32_t tx = S.tx;
-                        for (uint32_t e = tid; e < nb; e += SEL_CT) {
-                            const unsigned long long k = bkey[e];
-                            if (k > tk || (k == tk && bidx[e] < tx)) set_bit(bm, bidx[e]);
-                        }
-                    } else {  // huge threshold bin: rank straight from the log
-                        auto member = [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
-                            uint32_t w = 0;
-                            const uint32_t x = lpos(e, w);
-                            const double s = __ldcg(log_sc + x);
-                            if (bin_of(s, lo, scale) != dsel) return false;
-                            k = ordkey(s);
-                            ix = __ldcg(log_idx + x);
-                            return true;
-                        };
-                        radix_kth(S, hist, nlog, rem, member);
-                        const unsigned long long tk = S.tk;
-                        const uint32_t tx = S.tx;
-                        for (uint32_t e = tid; e < nlog; e += SEL_CT) {
-                            unsigned long long k;
-                            uint32_t ix;
-                            if (member(e, k, ix) && (k > tk || (k == tk && ix < tx))) set_bit(bm, ix);
-                        }
-                    }
-                }
-                // window passthrough (or the newest K when K <= R)
-                for (uint32_t i = f_lo + tid; i < N; i += SEL_CT) set_bit(bm, i);
-                cbar();
-                // ---- count, newest-first padding, ascending emit ----
-                const uint32_t wpt = div_up(nw, SEL_CT);
-                const uint32_t w0 = min(nw, tid * wpt), w1 = min(nw, w0 + wpt);
-                auto valid = [&](uint32_t x) {
-                    return x + 1 < nw || (N & 31) == 0 ? 0xffffffffu : ((1u << (N & 31)) - 1u);
-                };
-                uint32_t cnt = 0, zeros = 0;
-                for (uint32_t x = w0; x < w1; ++x) {
-                    const uint32_t b = bm[x];
-                    cnt += __popc(b);
-                    zeros += __popc(~b & valid(x));
-                }
-                uint32_t total;
-                cscan(S, cnt, total);
-                if (total < K) {  // pad with the newest untaken keys (retrieval.cpp:218-225)
-                    const uint32_t pad = K - total;
-                    uint32_t zt;
-                    const uint32_t zbelow = cscan(S, zeros, zt);
-                    const uint32_t zabove = zt - zbelow - zeros;  // zeros in higher threads
-                    uint32_t take = pad > zabove ? min(pad - zabove, zeros) : 0u;
-                    for (uint32_t x = w1; x > w0 && take;) {
-                        --x;
-                        uint32_t z = ~bm[x] & valid(x);
-                        while (z && take) {
-                            const int hb = 31 - __clz(z);
-                            bm[x] |= 1u << hb;
-                            z &= ~(1u << hb);
-                            --take;
-                            ++cnt;
-                        }
-                    }
-                }
-                const uint32_t at = cscan(S, cnt, total);
-                {
-                    uint32_t pos = at;
-                    for (uint32_t x = w0; x < w1; ++x) {
-                        uint32_t b = bm[x];
-                        while (b) {
-                            const int lb = __ffs(b) - 1;
-                            sel[pos++] = x * 32 + lb;
-                            b &= b - 1;
-                        }
-                    }
-                }
-                if (tid == 0) {
-                    reinterpret_cast<DecodeReport*>(rep)->k = K;
-                    if (prof) {
-                        prof[2] = gtimer();
-                        prof[3] = nlog;
-                        prof[4] = nb;
-                        prof[5] = static_cast<unsigned long long>(__double_as_longlong(lo));
-                        prof[6] = static_cast<unsigned long long>(
-                            __double_as_longlong(scale > 0.0 ? lo + NB / scale : lo));
-                        prof[7] = S.f_take_all | (dsel << 1);
-                    }
-                }
-                if (tid == 0) {  // next step's speculative cut: this threshold bin's lower edge
-                    st.hint[0] = scale > 0.0 ? lo + static_cast<double>(dsel) / scale : lo;
-                    st.hint[1] = (need && !take_all) ? 1.0 : 0.0;
-                }
-            }
+            final_select(S, st, p, hist, coarse, bm, bkey, bidx, log_idx, log_sc, SEL_CW, retry_out,
+                         retry_out_count);
+            const uint32_t nw = div_up(st.N, 32);
             cbar();  // bitmap emitted, scratch free
             // ---- reset for the next problem ----
             for (uint32_t x = tid; x < div_up(nw, 2); x += SEL_CT) acc[x] = neg0_d();
@@ -948,12 +1010,53 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             kk += gridDim.x;
             if (kk < nwork) {
                 p = prob_of(kk);
+                wlog_idx = log_idx + log_base(kk);
+                wlog_sc = log_sc + log_base(kk);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
             } else {
                 cbar();
             }
         }
     }
+}
+
+// Finalise split problems (split > 1): sum the parts' histograms (each part's
+// cut is a lower bound of the global threshold bin, so the sum is complete at
+// and above it), take the parts' warp logs as segments, run the final
+// selection. One 256-thread CTA per problem.
+__global__ void __launch_bounds__(SEL_CT)
+select_merge_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
+                    uint32_t split, const uint32_t* __restrict__ unit_meta,
+                    const uint32_t* __restrict__ log_idx, const double* __restrict__ log_sc,
+                    uint32_t log_cap, double spec_keep, uint32_t* __restrict__ retry_out,
+                    uint32_t* __restrict__ retry_out_count) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
+    unsigned char* p0 = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
+    uint32_t* bm = reinterpret_cast<uint32_t*>(p0);                 // SELECT_MAX_CONTEXT bits
+    uint32_t* hist = bm + SELECT_MAX_CONTEXT / 32;                  // NB
+    uint32_t* coarse = hist + NB;                                   // NCB
+    unsigned long long* bkey = reinterpret_cast<unsigned long long*>(coarse + NCB);  // BKT
+    uint32_t* bidx = reinterpret_cast<uint32_t*>(bkey + BKT);       // BKT
+    const uint32_t tid = threadIdx.x, p = blockIdx.x;
+    if (tid == 0) S.nbkt = 0;
+    ProbState st;
+    // the parts' speculative cut (same hint, read before any part finished)
+    setup_problem(S, probs, plans, p, st, true, spec_keep);  // ends with a barrier
+    const uint32_t* um = unit_meta + static_cast<size_t>(p) * split * UNIT_META;
+    for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) {
+        uint32_t v = 0;
+        for (uint32_t j = 0; j < split; ++j) v += __ldcg(um + static_cast<size_t>(j) * UNIT_META + x);
+        hist[x] = v;
+    }
+    if (tid < split * SEL_CW) {
+        const uint32_t j = tid / SEL_CW, w = tid % SEL_CW;
+        S.seg_len[tid] = __ldcg(um + static_cast<size_t>(j) * UNIT_META + NB + NCB + w);
+        S.seg_off[tid] = (p * split + j) * log_cap + w * (log_cap / SEL_CW);
+    }
+    cbar();
+    final_select(S, st, p, hist, coarse, bm, bkey, bidx, log_idx, log_sc, split * SEL_CW, retry_out,
+                 retry_out_count);
 }
 
 static size_t select_smem() {
@@ -966,18 +1069,36 @@ uint32_t select_grid(uint32_t nprob, int num_sms) {
     return nprob < g ? nprob : g;
 }
 
+uint32_t select_unit_meta_words() { return UNIT_META; }
+uint32_t select_tile_keys() { return TILE; }
+
+cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                                uint32_t split, const uint32_t* unit_meta, const uint32_t* log_idx,
+                                const double* log_sc, uint32_t log_cap, double spec_keep,
+                                uint32_t* retry_out, uint32_t* retry_out_count, cudaStream_t st) {
+    const size_t smem = ((sizeof(SelHdr) + 127) & ~size_t(127)) + SELECT_MAX_CONTEXT / 8 +
+                        (NB + NCB) * 4 + BKT * 12;
+    cudaError_t e = cudaFuncSetAttribute(select_merge_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    select_merge_kernel<<<nprob, SEL_CT, smem, st>>>(probs, plans, split, unit_meta, log_idx, log_sc,
+                                                     log_cap, spec_keep, retry_out, retry_out_count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
                           const uint32_t* retry_in, const uint32_t* retry_in_count,
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
-                          cudaStream_t st) {
+                          uint32_t split, uint32_t* unit_meta, cudaStream_t st) {
     const size_t smem = select_smem();
     cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap,
                                                    retry_in, retry_in_count, retry_out,
-                                                   retry_out_count, spec_keep);
+                                                   retry_out_count, spec_keep, split, unit_meta);
     return cudaGetLastError();
 }
 
