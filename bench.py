@@ -46,11 +46,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (prefill P, sequences, description)
-    "c2": (32768, 1, "Llama-3.1-8B-shaped attention layer (32 q / 8 KV heads, d=128) at 32K "
-                     "context, 1 B200"),
-    "c3": (131072, 16, "Llama-3.1-8B-shaped layer at 128K context, batch-16 decode sharing one "
-                       "prefilled context"),
+    # name: (prefill P, sequences, layers, description)
+    "c2": (32768, 1, 1, "Llama-3.1-8B-shaped attention layer (32 q / 8 KV heads, d=128) at 32K "
+                        "context, 1 B200"),
+    "c3": (131072, 16, 1, "Llama-3.1-8B-shaped layer at 128K context, batch-16 decode sharing one "
+                          "prefilled context"),
+    "c4": (131072, 1, 32, "full 32-layer Llama-3.1-8B-shaped decode at 128K, KV heads sharded "
+                          "across the GPUs of the run"),
 }
 N_KV, GROUP, D, M, C_CENT = 8, 4, 128, 8, 64
 DWELLS = (32, 16, 64, 8)
@@ -265,13 +267,14 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    P, n_seq, desc = CONFIGS[args.config]
+    P, n_seq, n_layers, desc = CONFIGS[args.config]
     config = {"workload": f"{args.config}: {desc}", "prefill": P, "sequences": n_seq,
+              "layers": n_layers,
               "kv_heads": N_KV, "q_heads": N_KV * GROUP, "d": D, "m": M, "C": C_CENT,
               "alpha": 0.2, "rho": 0.05, "window": 32, "tau": 1}
 
     if args.impl == "reference":
-        res = run_reference(args, P, n_seq, rank)
+        res = run_reference(args, P, n_seq * n_layers, rank)
         if rank != 0:
             return
         if "unavailable" in res:
@@ -312,7 +315,7 @@ def main():
     rc = cs.RetrievalConfig()
 
     t0 = time.perf_counter()
-    data = dict(zip(my_heads, gen_heads(cs, my_heads, P + n_seq * T + args.cpu_steps)))
+    data = dict(zip(my_heads, gen_heads(cs, my_heads, P + n_layers * n_seq * T + args.cpu_steps)))
     t_gen = time.perf_counter() - t0
     base_sessions = {}
     t0 = time.perf_counter()
@@ -323,15 +326,25 @@ def main():
         base_sessions[g] = cs.prefill(ctx, pooled, k[:P], v[:P], widths, ic, rc, group=GROUP,
                                       max_decode_steps=T)
     t_build = time.perf_counter() - t0
-    # session order: head-major, sequence-minor; sequence 0 is the prefilled session
+    # Session order: layer-major, then KV head, then sequence. Sequence 0 of
+    # layer 0 is the prefilled session; every other (layer, sequence) is a fork
+    # of it (tables copied, prefill rows shared: c3's 16 sequences share one
+    # prefill; c4's layers start from layer 0's tables, build time only), and
+    # decodes its own rows of the head's stream, [P + (l*n_seq + s)*T, +T).
+    t0 = time.perf_counter()
     sessions, rows = [], []
-    for g in my_heads:
-        for s in range(n_seq):
-            sessions.append(base_sessions[g] if s == 0 else base_sessions[g].fork(T))
-            rows.append((g, s))
+    for layer in range(n_layers):
+        for g in my_heads:
+            for s in range(n_seq):
+                first = layer == 0 and s == 0
+                sessions.append(base_sessions[g] if first else base_sessions[g].fork(T))
+                rows.append((g, layer * n_seq + s))
+    t_fork = time.perf_counter() - t0
     ns = len(sessions)
     nq = ns * GROUP
-    handles = (C.c_void_p * ns)(*[s.h.value for s in sessions])
+    ns_l = ns // n_layers  # sessions per layer (a layer = one decode_batch call)
+    handles = [(C.c_void_p * ns_l)(*[s.h.value for s in sessions[l * ns_l:(l + 1) * ns_l]])
+               for l in range(n_layers)]
     # per-step inputs for every session: q [T, ns*4, d], k/v [T, ns, d]
     qh = np.empty((T, nq, D), np.float32)
     kh = np.empty((T, ns, D), np.float32)
@@ -350,11 +363,17 @@ def main():
     torch.cuda.synchronize()
     lib = cs.lib()
 
-    def step(t, flags=_abi.NO_SYNC):
-        st = lib.csattn_decode_batch(ctx.h, ns, handles, C.c_void_p(qd[t].data_ptr()),
-                                     C.c_void_p(kd[t].data_ptr()), C.c_void_p(vd[t].data_ptr()),
-                                     C.c_void_p(outd[t].data_ptr()), None, 0, flags)
-        cs._check(st)
+    def step(t, flags=_abi.NO_SYNC, sel=None, sel_stride=0):
+        # one decode step of the model slice: the layers in order, each one
+        # csattn_decode_batch over its (KV head x sequence) sessions
+        for l in range(n_layers):
+            qs, ks = l * ns_l * GROUP, l * ns_l
+            st = lib.csattn_decode_batch(
+                ctx.h, ns_l, handles[l], C.c_void_p(qd[t, qs].data_ptr()),
+                C.c_void_p(kd[t, ks].data_ptr()), C.c_void_p(vd[t, ks].data_ptr()),
+                C.c_void_p(outd[t, qs].data_ptr()),
+                None if sel is None else C.c_void_p(sel[qs].data_ptr()), sel_stride, flags)
+            cs._check(st)
 
     # ---- warmup ----
     t = 0
@@ -396,8 +415,8 @@ def main():
         t += 1
     prof = ctx.profile_read(reset=True)
     ctx.profile(False)
-    nps = max(1, prof["steps"])
-    sel_ms = prof["select_ms"] / nps
+    nps = max(1, prof["steps"]) / n_layers  # profiled model steps (one call per layer)
+    sel_ms = prof["select_ms"] / nps          # per model step: all layers' launches
     att_ms = prof["attend_ms"] / nps
     ins_ms = prof["insert_ms"] / nps
     # ---- algorithmic bytes ----
@@ -421,22 +440,19 @@ def main():
     sel_perq = (tot_entries * 8 + nq * (C_CENT * D * 4 + D * 4 + Kp * 4))
     maxK = keep_count(0.05, P + t)
     seld = torch.zeros((nq, maxK), dtype=torch.int32, device="cuda")
-    st_ = lib.csattn_decode_batch(ctx.h, ns, handles, C.c_void_p(qd[t].data_ptr()),
-                                  C.c_void_p(kd[t].data_ptr()), C.c_void_p(vd[t].data_ptr()),
-                                  C.c_void_p(outd[t].data_ptr()), C.c_void_p(seld.data_ptr()),
-                                  maxK, 0)
-    cs._check(st_)
+    step(t, flags=0, sel=seld, sel_stride=maxK)
     Ka = keep_count(0.05, P + t)
     t += 1
     selh = seld.cpu().numpy().astype(np.int64)[:, :Ka]
     uniq_rows = 0
-    for gi, g in enumerate(my_heads):
-        rows_g = selh[gi * n_seq * GROUP:(gi + 1) * n_seq * GROUP]
-        pre_rows = np.unique(rows_g[rows_g < P])
-        uniq_rows += pre_rows.size
-        for sidx in range(n_seq):  # appended rows are per session
-            r = rows_g[sidx * GROUP:(sidx + 1) * GROUP]
-            uniq_rows += np.unique(r[r >= P]).size
+    for l in range(n_layers):  # every layer's KV is its own memory in a real model
+        for gi, g in enumerate(my_heads):
+            b = (l * len(my_heads) + gi) * n_seq * GROUP
+            rows_g = selh[b:b + n_seq * GROUP]
+            uniq_rows += np.unique(rows_g[rows_g < P]).size
+            for sidx in range(n_seq):  # appended rows are per session
+                r = rows_g[sidx * GROUP:(sidx + 1) * GROUP]
+                uniq_rows += np.unique(r[r >= P]).size
     att_unique = uniq_rows * 2 * D * 4 + nq * (Ka * 4 + 2 * D * 4)
     att_perq = nq * (Ka * (2 * D * 4 + 4) + 2 * D * 4)
     peak, peak_src = measured_peak()
@@ -465,10 +481,14 @@ def main():
         dist.barrier()
     te0 = time.perf_counter()
     for _ in range(e2e_steps):
-        st = lib.csattn_decode_batch(ctx.h, ns, handles, C.c_void_p(qp[t].data_ptr()),
-                                     C.c_void_p(kp[t].data_ptr()), C.c_void_p(vp_[t].data_ptr()),
-                                     C.c_void_p(op[t].data_ptr()), None, 0, _abi.HOST_BUFFERS)
-        cs._check(st)
+        for l in range(n_layers):
+            qs, ks = l * ns_l * GROUP, l * ns_l
+            st = lib.csattn_decode_batch(ctx.h, ns_l, handles[l], C.c_void_p(qp[t, qs].data_ptr()),
+                                         C.c_void_p(kp[t, ks].data_ptr()),
+                                         C.c_void_p(vp_[t, ks].data_ptr()),
+                                         C.c_void_p(op[t, qs].data_ptr()), None, 0,
+                                         _abi.HOST_BUFFERS)
+            cs._check(st)
         t += 1
     e2e_ms = (time.perf_counter() - te0) * 1e3 / e2e_steps
     if dist:
@@ -482,7 +502,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import bindings as ob
-            cpu = cpu_baseline_from_gpu(cs, ob, base_sessions, data, P, n_seq, args.cpu_steps, t)
+            cpu = cpu_baseline_from_gpu(cs, ob, base_sessions, data, P, n_seq * n_layers,
+                                        args.cpu_steps, t)
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "error": str(e)[:200]}
 
@@ -513,7 +534,8 @@ def main():
                     "d2h_bytes_per_step": int(op[0].numel() * 4)},
             "gpu_launches": int(gpu_launches),
             "clocks": clk.summary(),
-            "setup_s": {"synthetic": round(t_gen, 2), "gpu_build": round(t_build, 2)},
+            "setup_s": {"synthetic": round(t_gen, 2), "gpu_build": round(t_build, 2),
+                        "fork": round(t_fork, 2)},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
