@@ -273,6 +273,79 @@ csattn_status csattn_dense_attention(csattn_session s, const float* q, const uin
                                      uint64_t n_mask, float* out, float* weights,
                                      uint32_t flags);
 
+/* ---- sequence sharding ----
+ * A logical session (one KV head, P prefill keys) is split by key range over
+ * shards. Shard s holds keys [key_lo, key_hi) of every global TopList (global
+ * indices kept), their KV rows, and (owner shard only) the appended keys.
+ * Boundaries are multiples of 4096 keys (the select tile). The global list
+ * sizes and score bounds are replicated on every shard.
+ *
+ * A decode step runs as phases on every shard, in order, with the caller's
+ * collectives between them (NCCL across GPUs, or plain device ops when the
+ * shards share a GPU); the union of the shards' selections is exactly the
+ * unsharded selection and the merged output agrees within 1e-3:
+ *   SCAN    route + per-shard gather/accumulate/histogram -> io.ghist
+ *           caller: all-reduce(sum, uint32) io.ghist over shards
+ *   BUCKET  threshold bin; this shard's members of it -> io.bucket
+ *           caller: all-gather io.bucket -> io.bucket_all (shard order)
+ *   MARK    global rank of the bucket; local selection -> io.counts (2/problem)
+ *           caller: all-gather io.counts -> io.counts_all
+ *   EMIT    newest-first padding across shards, local selection (ascending
+ *           global indices -> io.selected / io.n_selected), sparse attention
+ *           partials (max, sum, acc[d]) -> io.partial
+ *           caller: all-gather io.partial -> io.partial_all
+ *   MERGE   log-sum-exp merge -> io.out (every shard may run it)
+ *   VICTIM  per table, this shard's next eviction key -> io.victim
+ *           caller: all-reduce(min, uint64) io.victim
+ *   INSERT  KvStore::append on the owner + global strict-win streaming insert
+ * All io pointers are device pointers on the context's device. */
+typedef enum csattn_shard_phase {
+    CSATTN_SHARD_SCAN = 0,
+    CSATTN_SHARD_BUCKET = 1,
+    CSATTN_SHARD_MARK = 2,
+    CSATTN_SHARD_EMIT = 3,
+    CSATTN_SHARD_MERGE = 4,
+    CSATTN_SHARD_VICTIM = 5,
+    CSATTN_SHARD_INSERT = 6
+} csattn_shard_phase;
+
+typedef struct csattn_shard_io {
+    const float* q;                  /* sum of groups x d */
+    const float* new_keys;           /* n x d */
+    const float* new_values;         /* n x d */
+    uint32_t* ghist;                 /* nq x hist_words */
+    uint32_t* bucket;                /* nq x bucket_words */
+    const uint32_t* bucket_all;      /* n_shards x nq x bucket_words */
+    uint32_t* counts;                /* nq x 2 */
+    const uint32_t* counts_all;      /* n_shards x nq x 2 */
+    float* partial;                  /* nq x (d + 2) */
+    const float* partial_all;        /* n_shards x nq x (d + 2) */
+    float* out;                      /* nq x d */
+    uint32_t* selected;              /* nq x sel_stride (nullable) */
+    uint32_t* n_selected;            /* nq (nullable) */
+    uint64_t sel_stride;
+    unsigned long long* victim;      /* n x m*C */
+    uint32_t shard_index;
+    uint32_t n_shards;
+} csattn_shard_io;
+
+/* Shard [key_lo, key_hi) of a freshly prefilled session (no decode steps
+ * yet), created on context `ctx` (one context per shard: a context runs one
+ * sharded step at a time). owner != 0: this shard also receives the appended
+ * keys. */
+csattn_status csattn_shard_create(csattn_ctx ctx, csattn_session full, uint64_t key_lo,
+                                  uint64_t key_hi, int32_t owner, uint64_t max_decode_steps,
+                                  csattn_session* out);
+/* Buffer sizes per problem (hist, bucket: uint32 words; partial: floats) and
+ * per session (victim: uint64 words). */
+csattn_status csattn_shard_buffer_words(csattn_session shard, uint64_t* hist_words,
+                                        uint64_t* bucket_words, uint64_t* partial_floats,
+                                        uint64_t* victim_words);
+/* One phase of a sharded decode step for n shard sessions of this shard
+ * (one per KV head, groups as in csattn_decode_batch). */
+csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t n, const csattn_session* shards,
+                                int32_t phase, const csattn_shard_io* io);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,17 @@ i32 = C.c_int32
 P = C.POINTER
 
 # name -> (restype, argtypes); every symbol include/csattn_b200.h declares
+class ShardIoC(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("new_keys", C.c_void_p), ("new_values", C.c_void_p),
+                ("ghist", C.c_void_p), ("bucket", C.c_void_p), ("bucket_all", C.c_void_p),
+                ("counts", C.c_void_p), ("counts_all", C.c_void_p),
+                ("partial", C.c_void_p), ("partial_all", C.c_void_p), ("out", C.c_void_p),
+                ("selected", C.c_void_p), ("n_selected", C.c_void_p), ("sel_stride", C.c_uint64),
+                ("victim", C.c_void_p), ("shard_index", C.c_uint32), ("n_shards", C.c_uint32)]
+
+
+SHARD_SCAN, SHARD_BUCKET, SHARD_MARK, SHARD_EMIT, SHARD_MERGE, SHARD_VICTIM, SHARD_INSERT = range(7)
+
 SIGNATURES = {
     "csattn_index_config_default": (None, [P(IndexConfigC)]),
     "csattn_retrieval_config_default": (None, [P(RetrievalConfigC)]),
@@ -93,6 +104,9 @@ SIGNATURES = {
                                         u64, P(vp)]),
     "csattn_session_export": (C.c_int, [vp, vp, vp, vp, u64, vp]),
     "csattn_session_centroids": (C.c_int, [vp, vp]),
+    "csattn_shard_create": (C.c_int, [vp, vp, u64, u64, C.c_int32, u64, P(vp)]),
+    "csattn_shard_buffer_words": (C.c_int, [vp, P(u64), P(u64), P(u64), P(u64)]),
+    "csattn_shard_step": (C.c_int, [vp, u64, P(vp), C.c_int32, P(ShardIoC)]),
     "csattn_session_gather_stats": (C.c_int, [vp, P(u64), P(u64)]),
     "csattn_session_fork": (C.c_int, [vp, u64, P(vp)]),
     "csattn_session_destroy": (C.c_int, [vp]),

@@ -58,7 +58,7 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     const uint32_t p = chunk_prob[c];
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
-    const uint32_t d = sd.d, K = P.K, P0 = sd.P;
+    const uint32_t d = sd.d, K = P.kdev ? __ldcg(P.kdev + p) : P.K, P0 = sd.P;
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -186,13 +186,20 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
         if (sk > 0.0f) GS += sk * expf(__ldcg(pb + k * (d + 2)) - GM);
     }
     const float inv = 1.0f / GS;
+    if ((P.mode & MODE_PARTIAL) && P.out && threadIdx.x == 0) {
+        P.out[0] = GM;  // (max, sum, acc[d]) for the cross-shard merge
+        P.out[1] = GS;
+    }
     for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
         float o = 0.0f;
         for (uint32_t k = 0; k < nch; ++k) {
             const float sk = __ldcg(pb + k * (d + 2) + 1);
             if (sk > 0.0f) o += __ldcg(pb + k * (d + 2) + 2 + t) * expf(__ldcg(pb + k * (d + 2)) - GM);
         }
-        if (P.out) P.out[t] = o * inv;
+        if (P.out) {
+            if (P.mode & MODE_PARTIAL) P.out[2 + t] = o;  // shard partial: unnormalised
+            else P.out[t] = o * inv;
+        }
     }
     if (want_w)
         for (uint32_t r = threadIdx.x; r < K; r += blockDim.x)
@@ -222,7 +229,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const uint32_t p = chunk_prob[c];
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
-    const uint32_t d = 128, K = P.K, P0 = sd.P;
+    const uint32_t d = 128, K = P.kdev ? __ldcg(P.kdev + p) : P.K, P0 = sd.P;
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -362,18 +369,60 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         if (sk > 0.0f) GS += sk * expf(__ldcg(pb + k * (d + 2)) - GM);
     }
     const float inv = 1.0f / GS;
+    if ((P.mode & MODE_PARTIAL) && P.out && threadIdx.x == 0) {
+        P.out[0] = GM;  // (max, sum, acc[d]) for the cross-shard merge
+        P.out[1] = GS;
+    }
     for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
         float o = 0.0f;
         for (uint32_t k = 0; k < nch; ++k) {
             const float sk = __ldcg(pb + k * (d + 2) + 1);
             if (sk > 0.0f) o += __ldcg(pb + k * (d + 2) + 2 + t) * expf(__ldcg(pb + k * (d + 2)) - GM);
         }
-        if (P.out) P.out[t] = o * inv;
+        if (P.out) {
+            if (P.mode & MODE_PARTIAL) P.out[2 + t] = o;  // shard partial: unnormalised
+            else P.out[t] = o * inv;
+        }
     }
     if (want_w)
         for (uint32_t r = threadIdx.x; r < K; r += blockDim.x)
             P.weights[r] = expf(__ldcg(P.weights + r) - GM) * inv;
     if (threadIdx.x == 0) counters[p] = 0;  // ready for the next step
+}
+
+// Cross-shard log-sum-exp merge of the shards' (max, sum, acc[d]) partials
+// (all-gathered: shard j's partial of problem p at parts[(j*nprob + p)*(d+2)]),
+// in shard order: the sharded step's output.
+__global__ void shard_merge_kernel(const float* __restrict__ parts, uint32_t nshard, uint32_t nprob,
+                                   uint32_t d, float* __restrict__ out, size_t out_stride) {
+    const uint32_t p = blockIdx.x;
+    float GM = -FLT_MAX;
+    for (uint32_t j = 0; j < nshard; ++j) {
+        const float* pp = parts + (static_cast<size_t>(j) * nprob + p) * (d + 2);
+        if (__ldcg(pp + 1) > 0.0f) GM = fmaxf(GM, __ldcg(pp));
+    }
+    float GS = 0.0f;
+    for (uint32_t j = 0; j < nshard; ++j) {
+        const float* pp = parts + (static_cast<size_t>(j) * nprob + p) * (d + 2);
+        const float sj = __ldcg(pp + 1);
+        if (sj > 0.0f) GS += sj * expf(__ldcg(pp) - GM);
+    }
+    const float inv = 1.0f / GS;
+    for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
+        float o = 0.0f;
+        for (uint32_t j = 0; j < nshard; ++j) {
+            const float* pp = parts + (static_cast<size_t>(j) * nprob + p) * (d + 2);
+            const float sj = __ldcg(pp + 1);
+            if (sj > 0.0f) o += __ldcg(pp + 2 + t) * expf(__ldcg(pp) - GM);
+        }
+        out[p * out_stride + t] = o * inv;
+    }
+}
+
+cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t nprob, uint32_t d,
+                               float* out, cudaStream_t st) {
+    shard_merge_kernel<<<nprob, 128, 0, st>>>(parts, nshard, nprob, d, out, d);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,

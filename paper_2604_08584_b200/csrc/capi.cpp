@@ -35,6 +35,11 @@ struct Fail {
 
 [[noreturn]] void fail(csattn_status c, std::string m) { throw Fail{c, std::move(m)}; }
 
+// a nested C-ABI call's failure, re-raised with its status and message
+void check_status(csattn_status st) {
+    if (st != CSATTN_OK) fail(st, g_err);
+}
+
 void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(CSATTN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -150,6 +155,14 @@ struct csattn_ctx_s {
     DevMem log_idx, log_sc; // select.cu candidate logs: log_rows x log_cap
     DevMem retry;           // select.cu retry list (speculative cut too high)
     DevMem ulog_idx, ulog_sc, umeta;  // split select: per part-unit logs + histograms
+    // sharded steps (csattn_shard_step): descriptors + scratch kept across phases
+    DevMem sh_desc, sh_pstate, sh_bitmap, sh_kdev, sh_ulog_idx, sh_ulog_sc, sh_umeta, sh_chunks;
+    std::vector<csa::DecodeProblem> sh_hprobs;
+    std::vector<csa::InsertProblem> sh_hiprobs;
+    std::vector<uint32_t> sh_chunk_host;
+    std::vector<uint64_t> sh_Ks;
+    uint64_t sh_nq = 0, sh_ns = 0, sh_ucap = 0, sh_bm_words = 0, sh_nchunks = 0;
+    bool sh_scanned = false;
     bool no_split = std::getenv("CSATTN_NO_SPLIT") != nullptr;
     uint64_t log_cap = 0, log_rows = 0;
     int num_sms = 148;
@@ -183,7 +196,7 @@ struct csattn_session_s {
     DevMem dev;
     std::shared_ptr<SharedRows> pre;
     DevMem ktail, vtail, cent, ent, n_used, live, blk_off, low, low_cnt, refill, tmm;
-    DevMem cache, cbounds, sel, drep, irep;
+    DevMem cache, cbounds, sel, drep, irep, live_g;
     uint64_t group = 1, N = 0, step = 0, max_steps = 0;
     double alpha = 0.0;
     int32_t score_bits = 32;
@@ -340,6 +353,11 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     h.low_cnt = s->low_cnt.as<uint32_t>();
     h.refill = s->refill.as<uint32_t>();
     h.tmm = s->tmm.as<float2>();
+    h.key_lo = 0;
+    h.key_hi = h.P;
+    h.owner = 1;
+    h.sharded = 0;
+    h.live_g = h.live;  // unsharded: the global count is the local one
     s->hs.assign(group, HeadState{});
     return s;
 }
@@ -1255,6 +1273,280 @@ csattn_status csattn_session_gather_stats(csattn_session s, uint64_t* unique_ent
             }
         *unique_entries = u;
         *total_entries = t;
+    });
+}
+
+
+// ---------------------------------------------------------------------------
+// sequence sharding
+// ---------------------------------------------------------------------------
+csattn_status csattn_shard_create(csattn_ctx ctx, csattn_session full, uint64_t key_lo,
+                                  uint64_t key_hi, int32_t owner, uint64_t max_steps,
+                                  csattn_session* out) {
+    return guard([&] {
+        const uint64_t P = full->h.P, d = full->h.d, tile = csa::select_tile_keys();
+        if (full->step != 0) fail(CSATTN_ERR_PARAMETER, "shard a session before its first decode step");
+        if (key_lo % tile || (!owner && key_hi % tile) || key_lo >= key_hi || key_hi > P)
+            fail(CSATTN_ERR_PARAMETER, "shard bounds must be multiples of " + std::to_string(tile) +
+                                           " keys inside the prefill");
+        if (full->rc.search_period != 1)
+            fail(CSATTN_ERR_PARAMETER, "sharded decoding needs search period 1");
+        const csattn_session_info in = [&] {
+            csattn_session_info x{};
+            check_status(csattn_session_info_get(full, &x));
+            return x;
+        }();
+        const uint64_t T = full->T(), L = full->h.L, stride = std::max<uint64_t>(L, 1);
+        std::vector<uint32_t> lens(T), idx(T * stride);
+        std::vector<float> sc(T * stride), cent(static_cast<size_t>(full->h.C) * d);
+        check_status(csattn_session_export(full, lens.data(), idx.data(), sc.data(), stride, cent.data()));
+        // global bounds + sizes (replicated), then the shard's part of every list
+        std::vector<float2> tmm(T);
+        ck(cudaMemcpy(tmm.data(), full->tmm.p, T * sizeof(float2), cudaMemcpyDeviceToHost), "tmm");
+        std::vector<uint32_t> slens(T), sidx(T * stride), gl(T);
+        std::vector<float> ssc(T * stride);
+        for (uint64_t t = 0; t < T; ++t) {
+            gl[t] = lens[t];
+            uint32_t n = 0;
+            for (uint32_t r = 0; r < lens[t]; ++r) {
+                const uint32_t i = idx[t * stride + r];
+                if (i >= key_lo && i < key_hi) {
+                    sidx[t * stride + n] = i;
+                    ssc[t * stride + n] = sc[t * stride + r];
+                    ++n;
+                }
+            }
+            slens[t] = n;
+        }
+        csattn_retrieval_config rc = full->rc;
+        rc.weights = full->weights.data();
+        rc.n_weights = full->weights.size();
+        ck(cudaStreamSynchronize(full->ctx->stream), "shard source");
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        auto s = new_session(ctx, d, full->widths.data(), full->h.m, full->h.C, L, P, full->group,
+                             max_steps, &rc);
+        s->alpha = full->alpha;
+        s->score_bits = full->score_bits;
+        s->h.normalize_keys = full->h.normalize_keys;
+        // KV rows [key_lo, key_hi); kpre/vpre offset so that row i is at kpre[i*d]
+        s->pre = std::make_shared<SharedRows>();
+        const size_t rows = (key_hi - key_lo) * d * sizeof(float);
+        s->pre->k.alloc(rows);
+        s->pre->v.alloc(rows);
+        ck(cudaMemcpy(s->pre->k.p, full->h.kpre + key_lo * d, rows, cudaMemcpyDefault), "shard rows");
+        ck(cudaMemcpy(s->pre->v.p, full->h.vpre + key_lo * d, rows, cudaMemcpyDefault), "shard rows");
+        s->h.kpre = s->pre->k.as<float>() - key_lo * d;
+        s->h.vpre = s->pre->v.as<float>() - key_lo * d;
+        ck(cudaMemcpy(s->cent.p, full->cent.p, cent.size() * 4, cudaMemcpyDefault), "shard centroids");
+        s->live_g.alloc(T * 4);
+        s->h.live_g = s->live_g.as<uint32_t>();
+        s->h.key_lo = static_cast<uint32_t>(key_lo);
+        s->h.key_hi = static_cast<uint32_t>(key_hi);
+        s->h.owner = owner ? 1u : 0u;
+        s->h.sharded = 1;
+        push_dev(s.get());
+        import_tables(s.get(), slens.data(), sidx.data(), ssc.data(), stride);
+        ck(cudaMemcpy(s->tmm.p, tmm.data(), T * sizeof(float2), cudaMemcpyHostToDevice), "tmm");
+        ck(cudaMemcpy(s->live_g.p, gl.data(), T * 4, cudaMemcpyHostToDevice), "live_g");
+        (void)in;
+        *out = s.release();
+    });
+}
+
+csattn_status csattn_shard_buffer_words(csattn_session s, uint64_t* hist_words,
+                                        uint64_t* bucket_words, uint64_t* partial_floats,
+                                        uint64_t* victim_words) {
+    return guard([&] {
+        *hist_words = csa::shard_hist_words();
+        *bucket_words = csa::shard_bucket_words();
+        *partial_floats = s->h.d + 2;
+        *victim_words = s->T();
+    });
+}
+
+csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss,
+                                int32_t phase, const csattn_shard_io* io) {
+    return guard([&] {
+        if (ns == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
+        if (!io) fail(CSATTN_ERR_PARAMETER, "null io");
+        for (uint64_t i = 0; i < ns; ++i)
+            if (!ss[i]->h.sharded) fail(CSATTN_ERR_PARAMETER, "not a shard session (csattn_shard_create)");
+        const uint32_t d = ss[0]->h.d;
+        cudaStream_t st = ctx->stream;
+        const uint64_t tile = csa::select_tile_keys();
+        if (phase == CSATTN_SHARD_SCAN) {
+            uint64_t nq = 0, maxtiles = 0, maxrange = 0;
+            ctx->sh_Ks.clear();
+            for (uint64_t i = 0; i < ns; ++i) {
+                csattn_session s = ss[i];
+                if (s->ctx != ctx) fail(CSATTN_ERR_PARAMETER, "sessions belong to another context");
+                if (s->h.d != d) fail(CSATTN_ERR_DIMENSION, "sessions differ in head dimension");
+                if (s->step >= s->max_steps)
+                    fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
+                                                  std::to_string(s->max_steps));
+                for (uint64_t h = 0; h < s->group; ++h) ctx->sh_Ks.push_back(keep_count(s->rc.keep_ratio, s->N));
+                nq += s->group;
+                const uint64_t khi = s->h.owner ? s->N : s->h.key_hi;
+                maxtiles = std::max(maxtiles, (khi - s->h.key_lo + tile - 1) / tile);
+                maxrange = std::max<uint64_t>(maxrange, (s->h.owner ? s->h.max_ctx : s->h.key_hi) - s->h.key_lo);
+            }
+            if (io->selected && io->sel_stride < *std::max_element(ctx->sh_Ks.begin(), ctx->sh_Ks.end()))
+                fail(CSATTN_ERR_PARAMETER, "selected stride is below K");
+            ctx->sh_nq = nq;
+            ctx->sh_ns = ns;
+            ctx->sh_ucap = maxtiles * tile;
+            ctx->sh_bm_words = (maxrange + 31) / 32;
+            ctx->sh_umeta.ensure(nq * csa::select_unit_meta_words() * 4);
+            ctx->sh_ulog_idx.ensure(nq * ctx->sh_ucap * 4);
+            ctx->sh_ulog_sc.ensure(nq * ctx->sh_ucap * 8);
+            ctx->sh_pstate.ensure(nq * csa::shard_pstate_bytes());
+            ctx->sh_bitmap.ensure(nq * ctx->sh_bm_words * 4);
+            ctx->sh_kdev.ensure(nq * 4);
+            ctx->sh_hprobs.resize(nq);
+            ctx->sh_hiprobs.resize(ns);
+            uint64_t qi = 0;
+            for (uint64_t i = 0; i < ns; ++i) {
+                csattn_session s = ss[i];
+                const uint64_t khi = s->h.owner ? s->N : s->h.key_hi;
+                for (uint64_t h = 0; h < s->group; ++h, ++qi) {
+                    csa::DecodeProblem& P = ctx->sh_hprobs[qi];
+                    P = csa::DecodeProblem{};
+                    P.s = s->dev.as<csa::SessionDev>();
+                    P.q = io->q + qi * d;
+                    P.out = io->partial + qi * (d + 2);
+                    P.weights = nullptr;
+                    P.sel = io->selected ? io->selected + qi * io->sel_stride
+                                         : s->sel.as<uint32_t>() + h * s->h.max_ctx;
+                    P.cache = nullptr;
+                    P.cbounds = s->cbounds.as<double>() + h * 4;
+                    P.rep = reinterpret_cast<uint32_t*>(s->drep.as<csa::DecodeReport>() + h);
+                    P.N = static_cast<uint32_t>(s->N);
+                    P.K = static_cast<uint32_t>(ctx->sh_Ks[qi]);
+                    P.mode = csa::MODE_SEARCH | csa::MODE_PARTIAL;
+                    P.tile_lo = static_cast<uint32_t>(s->h.key_lo / tile);
+                    P.tile_hi = static_cast<uint32_t>((khi + tile - 1) / tile);
+                    P.kdev = ctx->sh_kdev.as<uint32_t>();
+                }
+                csa::InsertProblem& I = ctx->sh_hiprobs[i];
+                I.s = s->dev.as<csa::SessionDev>();
+                I.key = io->new_keys + i * d;
+                I.value = io->new_values + i * d;
+                I.rep = s->irep.as<uint32_t>();
+                I.N = static_cast<uint32_t>(s->N);
+                I.pad = 0;
+            }
+            // attention work list: ceil(K / ATT_ROWS) chunk-CTAs per problem (global K:
+            // the shard's own share is read on the device, excess chunks idle)
+            std::vector<uint32_t> cbase(nq + 1), cprob;
+            for (uint64_t i = 0; i < nq; ++i) {
+                cbase[i] = static_cast<uint32_t>(cprob.size());
+                cprob.insert(cprob.end(), (ctx->sh_Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS,
+                             static_cast<uint32_t>(i));
+            }
+            cbase[nq] = static_cast<uint32_t>(cprob.size());
+            ctx->sh_nchunks = cprob.size();
+            ctx->sh_chunk_host.assign(cbase.begin(), cbase.end());
+            ctx->sh_chunk_host.insert(ctx->sh_chunk_host.end(), cprob.begin(), cprob.end());
+            const size_t dbytes = nq * sizeof(csa::DecodeProblem), ibytes = ns * sizeof(csa::InsertProblem);
+            const size_t ioff = (dbytes + 255) & ~size_t(255);
+            ctx->sh_desc.ensure(ioff + ibytes);
+            ck(cudaMemcpyAsync(ctx->sh_desc.p, ctx->sh_hprobs.data(), dbytes, cudaMemcpyHostToDevice, st), "desc");
+            ck(cudaMemcpyAsync(ctx->sh_desc.as<char>() + ioff, ctx->sh_hiprobs.data(), ibytes,
+                               cudaMemcpyHostToDevice, st), "desc");
+            ctx->sh_chunks.ensure(ctx->sh_chunk_host.size() * 4);
+            ck(cudaMemcpyAsync(ctx->sh_chunks.p, ctx->sh_chunk_host.data(), ctx->sh_chunk_host.size() * 4,
+                               cudaMemcpyHostToDevice, st), "chunks");
+            if (nq > ctx->counters_n) {
+                ctx->counters.alloc(nq * 4);
+                ck(cudaMemsetAsync(ctx->counters.p, 0, nq * 4, st), "memset");
+                ctx->counters_n = nq;
+            }
+            ctx->part.ensure(ctx->sh_nchunks * (d + 2) * sizeof(float));
+            ctx->plans.ensure(nq * sizeof(csa::RoutePlan));
+            const csa::DecodeProblem* dprobs = ctx->sh_desc.as<csa::DecodeProblem>();
+            ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), st),
+               "route launch");
+            const uint32_t grid = csa::select_grid(static_cast<uint32_t>(nq), ctx->num_sms);
+            ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), grid,
+                                  ctx->sh_ulog_idx.as<uint32_t>(), ctx->sh_ulog_sc.as<double>(),
+                                  static_cast<uint32_t>(ctx->sh_ucap), nullptr, nullptr, nullptr,
+                                  nullptr, 0.0, 1, ctx->sh_umeta.as<uint32_t>(), st),
+               "select (shard scan) launch");
+            const uint64_t hw = csa::shard_hist_words();
+            ck(cudaMemcpy2DAsync(io->ghist, hw * 4, ctx->sh_umeta.p, csa::select_unit_meta_words() * 4,
+                                 hw * 4, nq, cudaMemcpyDeviceToDevice, st),
+               "histograms");
+            ctx->launches += 2;
+            ctx->sh_scanned = true;
+            return;
+        }
+        if (!ctx->sh_scanned || ns != ctx->sh_ns) fail(CSATTN_ERR_PARAMETER, "shard phases out of order");
+        const uint64_t nq = ctx->sh_nq;
+        const csa::DecodeProblem* dprobs = ctx->sh_desc.as<csa::DecodeProblem>();
+        const size_t ioff = (nq * sizeof(csa::DecodeProblem) + 255) & ~size_t(255);
+        const csa::InsertProblem* diprobs =
+            reinterpret_cast<const csa::InsertProblem*>(ctx->sh_desc.as<char>() + ioff);
+        switch (phase) {
+            case CSATTN_SHARD_BUCKET:
+                ck(csa::launch_shard_bucket(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
+                                            io->ghist, ctx->sh_umeta.as<uint32_t>(),
+                                            ctx->sh_ulog_idx.as<uint32_t>(), ctx->sh_ulog_sc.as<double>(),
+                                            static_cast<uint32_t>(ctx->sh_ucap), io->bucket,
+                                            ctx->sh_pstate.p, st),
+                   "shard bucket launch");
+                break;
+            case CSATTN_SHARD_MARK:
+                ck(csa::launch_shard_mark(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
+                                          ctx->sh_pstate.p, io->bucket_all, io->n_shards,
+                                          ctx->sh_umeta.as<uint32_t>(), ctx->sh_ulog_idx.as<uint32_t>(),
+                                          ctx->sh_ulog_sc.as<double>(), static_cast<uint32_t>(ctx->sh_ucap),
+                                          ctx->sh_bitmap.as<uint32_t>(),
+                                          static_cast<uint32_t>(ctx->sh_bm_words), io->counts, st),
+                   "shard mark launch");
+                break;
+            case CSATTN_SHARD_EMIT: {
+                ck(csa::launch_shard_emit(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
+                                          io->counts_all, io->n_shards, io->shard_index,
+                                          ctx->sh_bitmap.as<uint32_t>(),
+                                          static_cast<uint32_t>(ctx->sh_bm_words), ctx->sh_kdev.as<uint32_t>(), st),
+                   "shard emit launch");
+                if (io->n_selected)
+                    ck(cudaMemcpyAsync(io->n_selected, ctx->sh_kdev.p, nq * 4, cudaMemcpyDeviceToDevice, st),
+                       "n_selected");
+                const uint32_t* ch = ctx->sh_chunks.as<uint32_t>();
+                ck(csa::launch_attend(dprobs, ch + nq + 1, ch, static_cast<uint32_t>(ctx->sh_nchunks),
+                                      ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, st),
+                   "attend launch");
+                ctx->launches += 2;
+                break;
+            }
+            case CSATTN_SHARD_MERGE:
+                ck(csa::launch_shard_merge(io->partial_all, io->n_shards, static_cast<uint32_t>(nq), d,
+                                           io->out, st),
+                   "shard merge launch");
+                break;
+            case CSATTN_SHARD_VICTIM:
+                ck(csa::launch_shard_victim(diprobs, static_cast<uint32_t>(ns), io->victim, st),
+                   "shard victim launch");
+                break;
+            case CSATTN_SHARD_INSERT:
+                ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), st, io->victim), "insert launch");
+                for (uint64_t i = 0; i < ns; ++i) {
+                    csattn_session s = ss[i];
+                    for (uint64_t h = 0; h < s->group; ++h) {
+                        s->hs[h].has_cache = true;
+                        s->hs[h].n_cache = s->N;
+                    }
+                    s->N += 1;
+                    s->step += 1;
+                }
+                ctx->sh_scanned = false;
+                ck(cudaStreamSynchronize(st), "shard step");
+                break;
+            default:
+                fail(CSATTN_ERR_PARAMETER, "unknown shard phase");
+        }
+        ctx->launches += 1;
     });
 }
 

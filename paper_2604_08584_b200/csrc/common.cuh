@@ -68,7 +68,14 @@ struct SessionDev {
     LowEnt* low;        // [T][LOW_Q]
     uint32_t* low_cnt;  // [T]
     uint32_t* refill;   // [T] scratch flags for the insert kernel
-    float2* tmm;        // [T] live score bounds (min lower bound, max)
+    float2* tmm;        // [T] live score bounds (min lower bound, max) of the GLOBAL list
+    // Sequence sharding: a shard holds the keys [key_lo, key_hi)
+    // of the global lists (global indices kept) and of the prefill KV rows;
+    // `owner` shards also hold appended keys (index >= P). live_g[t] is the
+    // global live count of list t, replicated on every shard (== live when the
+    // session is not sharded). kpre/vpre are offset so row i is kpre[i*d].
+    uint32_t key_lo, key_hi, owner, sharded;
+    uint32_t* live_g;   // [T]
 };
 
 // Per-(session, query head) decode-step descriptor.
@@ -86,10 +93,13 @@ struct DecodeProblem {
     uint32_t n_cache;  // context length when the cache was filled
     uint32_t mode;     // MODE_* bits
     unsigned long long* prof;  // phase timestamps [cs][8] (CSATTN_PHASE_PROF) or null
+    uint32_t tile_lo, tile_hi;  // select tiles of this shard (tile_hi == 0: all)
+    const uint32_t* kdev;       // device-side K (sharded steps: this shard's share) or null
 };
 constexpr uint32_t MODE_SEARCH = 1u;       // route + gather + accumulate
 constexpr uint32_t MODE_STORE_CACHE = 2u;  // persist candidate scores
 constexpr uint32_t MODE_WEIGHTS = 4u;      // emit softmax weights
+constexpr uint32_t MODE_PARTIAL = 8u;      // attend writes (max, sum, acc[d]) unnormalised
 
 // Device report written by CTA 0 of a problem (uint32 words).
 struct DecodeReport {

@@ -46,17 +46,44 @@ struct InsSmem {
     RefillSmem r;
 };
 
+// score of an eviction key (inverse of evkey's order-preserving map)
+__device__ __forceinline__ float ev_score(unsigned long long k) {
+    const uint32_t o = static_cast<uint32_t>(k >> 32);
+    return __uint_as_float((o >> 31) ? (o & 0x7fffffffu) : ~o);
+}
+
+// Sharded sessions: the first entry of each table in eviction order on this
+// shard (low[cnt-1]); the caller all-reduces (min) over the shards to get the
+// global TopList back (score asc, key desc).
+__global__ void shard_victim_kernel(const InsertProblem* __restrict__ probs,
+                                    unsigned long long* __restrict__ vk) {
+    const InsertProblem& P = probs[blockIdx.x];
+    const SessionDev& sd = *P.s;
+    const uint32_t T = sd.m * sd.C;
+    for (uint32_t t = threadIdx.x; t < T; t += blockDim.x) {
+        const uint32_t cnt = sd.low_cnt[t];
+        unsigned long long k = ~0ull;
+        if (cnt) {
+            const LowEnt v = sd.low[static_cast<size_t>(t) * LOW_Q + cnt - 1];
+            k = evkey(v.score, v.key);
+        }
+        vk[static_cast<size_t>(blockIdx.x) * T + t] = k;
+    }
+}
+
 __global__ void __launch_bounds__(INS_THREADS)
-insert_kernel(const InsertProblem* __restrict__ probs) {
+insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long* __restrict__ gvk) {
     __shared__ InsSmem S;
     const InsertProblem& P = probs[blockIdx.x];
     const SessionDev& sd = *P.s;
     const uint32_t d = sd.d, m = sd.m, C = sd.C, T = m * C, N = P.N;
-    // KvStore::append: row N lands at tail row N - P
+    // KvStore::append: row N lands at tail row N - P (on the owner shard)
     for (uint32_t x = threadIdx.x; x < d; x += blockDim.x) {
         const float kx = P.key[x];
-        sd.ktail[static_cast<size_t>(N - sd.P) * d + x] = kx;
-        sd.vtail[static_cast<size_t>(N - sd.P) * d + x] = P.value[x];
+        if (sd.owner) {
+            sd.ktail[static_cast<size_t>(N - sd.P) * d + x] = kx;
+            sd.vtail[static_cast<size_t>(N - sd.P) * d + x] = P.value[x];
+        }
         S.ks[x] = kx;
     }
     if (threadIdx.x == 0) {
@@ -95,7 +122,64 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
         uint32_t nu = sd.n_used[t];
         if (new_blk) sd.blk_off[static_cast<size_t>(t) * sd.nb_stride + (N >> KEY_BLOCK_SHIFT)] = nu;
         uint32_t applied = 0;
-        if (sd.L != 0) {
+        if (sd.L != 0 && sd.sharded) {
+            // global TopList semantics over the shards: the list is full when the
+            // GLOBAL live count reaches L; a full list admits only a strict win
+            // over the global back (gvk, all-reduced); the shard holding it
+            // tombstones it, the owner shard appends the new entry
+            const uint32_t live_g = sd.live_g[t];
+            uint32_t live = sd.live[t];
+            uint32_t cnt = sd.low_cnt[t];
+            LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
+            uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
+            const bool full = live_g >= sd.L;
+            const bool complete = cnt == live;
+            bool ok = true, evicted = false;
+            if (full) {
+                const unsigned long long gv = gvk[static_cast<size_t>(blockIdx.x) * T + t];
+                if (!(sc > ev_score(gv))) {
+                    ok = false;
+                } else if (cnt && evkey(lo[cnt - 1].score, lo[cnt - 1].key) == gv) {
+                    e[lo[cnt - 1].pos].x = lo[cnt - 1].key | TOMB;
+                    cnt -= 1;
+                    live -= 1;
+                    evicted = true;
+                }
+            }
+            if (ok) {
+                applied = 1;
+                float2 mm = sd.tmm[t];  // global bounds, replicated on every shard
+                mm = live_g == 0 ? make_float2(sc, sc) : make_float2(fminf(mm.x, sc), fmaxf(mm.y, sc));
+                sd.tmm[t] = mm;
+                if (!full) sd.live_g[t] = live_g + 1;
+                if (sd.owner) {
+                    e[nu] = make_uint2(N, __float_as_uint(sc));
+                    const uint32_t pos = nu;
+                    nu += 1;
+                    live += 1;
+                    sd.n_used[t] = nu;
+                    bool ins;
+                    if (cnt == 0)
+                        ins = complete;
+                    else if (complete && cnt < static_cast<uint32_t>(LOW_Q))
+                        ins = true;
+                    else
+                        ins = ev_before(sc, N, lo[0].score, lo[0].key);
+                    if (ins) {
+                        const uint32_t k = atomicAdd(&S.nbuf, 1u);
+                        S.buflist[k] = t;
+                        S.bufent[k] = BufEnt{sc, pos, cnt};
+                    } else {
+                        sd.low_cnt[t] = cnt;
+                        if (cnt == 0 || nu == sd.cap2) S.reflist[atomicAdd(&S.nref, 1u)] = t;
+                    }
+                } else if (evicted) {
+                    sd.low_cnt[t] = cnt;
+                    if (cnt == 0 && live > 0) S.reflist[atomicAdd(&S.nref, 1u)] = t;
+                }
+                sd.live[t] = live;
+            }
+        } else if (sd.L != 0) {
             const uint32_t live = sd.live[t];
             uint32_t cnt = sd.low_cnt[t];
             LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
@@ -193,8 +277,15 @@ insert_kernel(const InsertProblem* __restrict__ probs) {
     for (uint32_t r = 0; r < S.nref; ++r) refill_table(S.r, sd, S.reflist[r], last_blk);
 }
 
-cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st) {
-    insert_kernel<<<nprob, INS_THREADS, 0, st>>>(probs);
+cudaError_t launch_shard_victim(const InsertProblem* probs, uint32_t nprob,
+                                unsigned long long* vk, cudaStream_t st) {
+    shard_victim_kernel<<<nprob, 256, 0, st>>>(probs, vk);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st,
+                          const unsigned long long* gvk) {
+    insert_kernel<<<nprob, INS_THREADS, 0, st>>>(probs, gvk);
     return cudaGetLastError();
 }
 

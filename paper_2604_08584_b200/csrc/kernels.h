@@ -36,14 +36,38 @@ cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* pla
                                 const double* log_sc, uint32_t log_cap, double spec_keep,
                                 uint32_t* retry_out, uint32_t* retry_out_count, cudaStream_t st);
 
+// select.cu, sequence-sharded decode phases (see select.cu)
+uint32_t shard_bucket_words();  // per problem, uint32 words of a bucket record
+uint32_t shard_hist_words();    // per problem histogram words (all-reduced)
+uint32_t shard_pstate_bytes();
+cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                                const uint32_t* ghist, const uint32_t* unit_meta,
+                                const uint32_t* log_idx, const double* log_sc, uint32_t log_cap,
+                                void* bucket, void* pstate, cudaStream_t st);
+cudaError_t launch_shard_mark(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                              const void* pstate, const void* bucket_all, uint32_t nshard,
+                              const uint32_t* unit_meta, const uint32_t* log_idx,
+                              const double* log_sc, uint32_t log_cap, uint32_t* bitmap,
+                              uint32_t bm_words, uint32_t* counts, cudaStream_t st);
+cudaError_t launch_shard_emit(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                              const uint32_t* counts_all, uint32_t nshard, uint32_t shard,
+                              uint32_t* bitmap, uint32_t bm_words, uint32_t* kdev, cudaStream_t st);
+
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
 constexpr uint32_t ATT_ROWS = 256;
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st);
 
+cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t nprob, uint32_t d,
+                               float* out, cudaStream_t st);
+
 // insert.cu: append + streaming insert, one CTA per session
-cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st);
+//   gvk: sharded sessions only, per session x table the global victim key
+cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st,
+                          const unsigned long long* gvk = nullptr);
+cudaError_t launch_shard_victim(const InsertProblem* probs, uint32_t nprob,
+                                unsigned long long* vk, cudaStream_t st);
 
 // build.cu: exact fp64 centroid x key scores and top-L tables
 //   scores: T x P floats scratch

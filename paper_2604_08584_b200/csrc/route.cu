@@ -139,7 +139,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
         bool any = false, any_neg = false, any_pos = false;
         for (uint32_t l = 0; l < nl; ++l) {
             const uint32_t t = lists[l];
-            if (__ldcg(sd.live + t) == 0) continue;
+            if (__ldcg(sd.live_g + t) == 0) continue;
             const float2 mm = __ldcg(sd.tmm + t);
             const double w = sd.weights[lsub[l]];
             const double a = w * static_cast<double>(mm.x), b = w * static_cast<double>(mm.y);
@@ -160,7 +160,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     }
     if (wid == 0) {  // gathered_entries (CostCounters): live lengths of the lists
         uint32_t g = 0;
-        for (uint32_t l = ln; l < nl; l += 32) g += __ldcg(sd.live + lists[l]);
+        for (uint32_t l = ln; l < nl; l += 32) g += __ldcg(sd.live_g + lists[l]);
         for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
         if (ln == 0) {
             Rp->gathered_lo = g;

@@ -607,10 +607,14 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     const uint32_t nwork = retry_in ? __ldcg(retry_in_count) : nprob * split;
     if (blockIdx.x >= nwork) return;
     auto prob_of = [&](uint32_t k) { return retry_in ? __ldcg(retry_in + k) : k / split; };
-    auto tiles_of = [&](uint32_t k, uint32_t N, uint32_t& tl, uint32_t& th) {
-        const uint32_t nt = div_up(N, TILE), j = retry_in ? 0u : k % split;
-        tl = (nt * j) / split;
-        th = (nt * (j + 1)) / split;
+    // unit k's tiles: part k % split of the problem's tile range (a shard's
+    // range [tile_lo, tile_hi), else all tiles of its N keys)
+    auto tiles_of = [&](uint32_t k, const DecodeProblem& P, uint32_t& tl, uint32_t& th) {
+        const uint32_t t0 = P.tile_hi ? P.tile_lo : 0u;
+        const uint32_t t1 = P.tile_hi ? P.tile_hi : div_up(P.N, TILE);
+        const uint32_t nt = t1 - t0, j = retry_in ? 0u : k % split;
+        tl = t0 + (nt * j) / split;
+        th = t0 + (nt * (j + 1)) / split;
     };
     const bool speculate = (retry_out != nullptr || split > 1) && !retry_in;
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
@@ -669,7 +673,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             const SessionDev& sd = *P.s;
             const uint32_t N = P.N;
             uint32_t tl, ntile;
-            tiles_of(k, N, tl, ntile);  // this unit's tiles [tl, ntile)
+            tiles_of(k, P, tl, ntile);  // this unit's tiles [tl, ntile)
             uint32_t nl = 0;
             if (P.mode & MODE_SEARCH) {
                 nl = __ldcg(&plans[p].nl);
@@ -964,7 +968,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
         cbar();  // accumulator clear before the next tile's first list
         if (!(flags & F_PROB_END)) continue;
 
-        if (split > 1) {  // part unit: hand histogram + log lengths to the merge kernel
+        if (unit_meta) {  // part unit / shard: hand histogram + log lengths on
             uint32_t* const um = unit_meta + static_cast<size_t>(kk) * UNIT_META;
             if (ln == 0) um[NB + NCB + wid] = wlog_n;
             cbar();
@@ -1058,6 +1062,272 @@ select_merge_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __
     final_select(S, st, p, hist, coarse, bm, bkey, bidx, log_idx, log_sc, split * SEL_CW, retry_out,
                  retry_out_count);
 }
+
+// ===========================================================================
+// Sequence-sharded decode. Shard s holds keys
+// [key_lo, key_hi) of every global list (+ appended keys on the owner shard).
+// After the per-shard scan (select_kernel in dump mode over the shard's tiles)
+// the caller all-reduces the histograms; then:
+//   shard_bucket_kernel  threshold bin from the global histogram; this shard's
+//                        members of that bin -> bucket (caller all-gathers)
+//   shard_mark_kernel    rank the gathered bucket globally (score desc, index
+//                        asc) -> local selection bitmap; per-shard (selected,
+//                        untaken) counts (caller all-gathers)
+//   shard_emit_kernel    newest-first padding across shards (higher shards hold
+//                        newer keys) and the ascending local selection + its
+//                        size for attend
+// Every shard computes the same global threshold, so the union of the local
+// selections is exactly the unsharded selection.
+// ===========================================================================
+struct ShardPState {
+    uint32_t dsel, above, take_all, nbkt;
+};
+constexpr uint32_t SHARD_BCAP = 2048;  // bucket members per problem per shard
+
+// flat log index -> (segment) for a problem's dump-mode log (one unit per problem)
+struct LogView {
+    const uint32_t* idx;
+    const double* sc;
+    const uint32_t* wl;  // per-warp lengths (unit_meta tail)
+    size_t base;         // p * log_cap
+    uint32_t stride;     // log_cap / SEL_CW
+};
+
+__global__ void __launch_bounds__(SEL_CT)
+shard_bucket_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
+                    const uint32_t* __restrict__ ghist, const uint32_t* __restrict__ unit_meta,
+                    const uint32_t* __restrict__ log_idx, const double* __restrict__ log_sc,
+                    uint32_t log_cap, uint4* __restrict__ bucket, ShardPState* __restrict__ pstate) {
+    __shared__ SelHdr S;
+    const uint32_t tid = threadIdx.x, p = blockIdx.x;
+    ProbState st;
+    setup_problem(S, probs, plans, p, st, false, 0.0);
+    const uint32_t* gh = ghist + static_cast<size_t>(p) * (NB + NCB);
+    if (tid < 32) {
+        uint32_t ab = 0;
+        int b = -1;
+        if (st.need) b = warp_find_bin(gh, gh + NB, st.need, ab);
+        if (tid == 0) {
+            S.f_take_all = (st.need && b < 0) ? 1u : 0u;
+            S.f_bin = b < 0 ? 0u : static_cast<uint32_t>(b);
+            S.f_above = ab;
+            S.nbkt = 0;
+        }
+    }
+    cbar();
+    const uint32_t dsel = S.f_bin;
+    const bool collect = st.need && !S.f_take_all;
+    const uint32_t* wl = unit_meta + static_cast<size_t>(p) * UNIT_META + NB + NCB;
+    uint4* bk = bucket + static_cast<size_t>(p) * (SHARD_BCAP + 1);
+    if (collect) {
+        for (uint32_t w = 0; w < SEL_CW; ++w) {
+            const size_t base = static_cast<size_t>(p) * log_cap + w * (log_cap / SEL_CW);
+            const uint32_t n = __ldcg(wl + w);
+            for (uint32_t e = tid; e < n; e += SEL_CT) {
+                const double sv = __ldcg(log_sc + base + e);
+                if (bin_of(sv, st.lo, st.scale) != dsel) continue;
+                const uint32_t k = atomicAdd(&S.nbkt, 1u);
+                if (k < SHARD_BCAP) {
+                    const unsigned long long key = ordkey(sv);
+                    bk[1 + k] = make_uint4(static_cast<uint32_t>(key), static_cast<uint32_t>(key >> 32),
+                                           __ldcg(log_idx + base + e), 0u);
+                }
+            }
+        }
+    }
+    cbar();
+    if (tid == 0) {
+        bk[0] = make_uint4(min(S.nbkt, SHARD_BCAP), S.nbkt > SHARD_BCAP ? 1u : 0u, 0u, 0u);
+        pstate[p] = ShardPState{dsel, S.f_above, S.f_take_all, S.nbkt};
+    }
+}
+
+__global__ void __launch_bounds__(SEL_CT)
+shard_mark_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
+                  const ShardPState* __restrict__ pstate, const uint4* __restrict__ bucket_all,
+                  uint32_t nshard, uint32_t nprob, const uint32_t* __restrict__ unit_meta,
+                  const uint32_t* __restrict__ log_idx, const double* __restrict__ log_sc,
+                  uint32_t log_cap, uint32_t* __restrict__ bitmap, uint32_t bm_words,
+                  uint32_t* __restrict__ counts) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127)));
+    const uint32_t tid = threadIdx.x, p = blockIdx.x;
+    ProbState st;
+    setup_problem(S, probs, plans, p, st, false, 0.0);
+    const SessionDev& sd = *probs[p].s;
+    const ShardPState ps = pstate[p];
+    const uint32_t need = st.need, N = st.N;
+    const uint32_t rem = need - (ps.take_all ? 0u : min(need, ps.above));
+    // gathered bucket: shard j's members at bucket_all[(j*nprob + p)*(BCAP+1) + 1 ..]
+    if (tid == 0) {
+        uint32_t run = 0;
+        for (uint32_t j = 0; j <= nshard; ++j) {
+            S.seg_pre[j] = run;
+            if (j < nshard)
+                run += __ldcg(&bucket_all[(static_cast<size_t>(j) * nprob + p) * (SHARD_BCAP + 1)].x);
+        }
+    }
+    cbar();
+    const uint32_t nb = S.seg_pre[nshard];
+    auto member = [&](uint32_t e, unsigned long long& k, uint32_t& ix) {
+        uint32_t j = 0;
+        while (S.seg_pre[j + 1] <= e) ++j;
+        const uint4 v = __ldcg(&bucket_all[(static_cast<size_t>(j) * nprob + p) * (SHARD_BCAP + 1) + 1 +
+                                           (e - S.seg_pre[j])]);
+        k = (static_cast<unsigned long long>(v.y) << 32) | v.x;
+        ix = v.z;
+        return true;
+    };
+    unsigned long long tk = ~0ull;
+    uint32_t tx = 0;
+    if (need && !ps.take_all && rem) {
+        radix_kth(S, hist, nb, rem, member);
+        tk = S.tk;
+        tx = S.tx;
+    }
+    // local selection bitmap over this shard's key range
+    const uint32_t klo = sd.key_lo;
+    const uint32_t khi = sd.owner ? N : min(sd.key_hi, N);
+    const uint32_t nwb = khi > klo ? div_up(khi - klo, 32) : 0u;
+    uint32_t* bm = bitmap + static_cast<size_t>(p) * bm_words;
+    for (uint32_t x = tid; x < nwb; x += SEL_CT) bm[x] = 0;
+    cbar();
+    if (need) {
+        const uint32_t* wl = unit_meta + static_cast<size_t>(p) * UNIT_META + NB + NCB;
+        for (uint32_t w = 0; w < SEL_CW; ++w) {
+            const size_t base = static_cast<size_t>(p) * log_cap + w * (log_cap / SEL_CW);
+            const uint32_t n = __ldcg(wl + w);
+            for (uint32_t e = tid; e < n; e += SEL_CT) {
+                const double sv = __ldcg(log_sc + base + e);
+                const uint32_t b = bin_of(sv, st.lo, st.scale);
+                bool on = ps.take_all || b > ps.dsel;
+                if (!on && b == ps.dsel) {
+                    const unsigned long long k = ordkey(sv);
+                    on = k > tk || (k == tk && __ldcg(log_idx + base + e) < tx);
+                }
+                if (on) {
+                    const uint32_t i = __ldcg(log_idx + base + e);
+                    atomicOr(bm + ((i - klo) >> 5), 1u << ((i - klo) & 31));
+                }
+            }
+        }
+    }
+    // window passthrough (or the newest K when K <= R) within this shard
+    for (uint32_t i = max(st.f_lo, klo) + tid; i < khi; i += SEL_CT)
+        atomicOr(bm + ((i - klo) >> 5), 1u << ((i - klo) & 31));
+    cbar();
+    uint32_t cnt = 0;
+    for (uint32_t x = tid; x < nwb; x += SEL_CT) cnt += __popc(bm[x]);
+    uint32_t total;
+    cscan(S, cnt, total);
+    if (tid == 0) {
+        counts[2 * p] = total;
+        counts[2 * p + 1] = (khi > klo ? khi - klo : 0u) - total;  // untaken keys of the range
+    }
+}
+
+__global__ void __launch_bounds__(SEL_CT)
+shard_emit_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
+                  const uint32_t* __restrict__ counts_all, uint32_t nshard, uint32_t shard,
+                  uint32_t nprob, uint32_t* __restrict__ bitmap, uint32_t bm_words,
+                  uint32_t* __restrict__ kdev) {
+    __shared__ SelHdr S;
+    const uint32_t tid = threadIdx.x, p = blockIdx.x;
+    ProbState st;
+    setup_problem(S, probs, plans, p, st, false, 0.0);
+    const SessionDev& sd = *probs[p].s;
+    const uint32_t N = st.N, K = st.K;
+    uint32_t total = 0, above = 0;
+    for (uint32_t j = 0; j < nshard; ++j) {
+        total += __ldcg(counts_all + (static_cast<size_t>(j) * nprob + p) * 2);
+        if (j > shard) above += __ldcg(counts_all + (static_cast<size_t>(j) * nprob + p) * 2 + 1);
+    }
+    const uint32_t klo = sd.key_lo;
+    const uint32_t khi = sd.owner ? N : min(sd.key_hi, N);
+    const uint32_t nwb = khi > klo ? div_up(khi - klo, 32) : 0u;
+    uint32_t* bm = bitmap + static_cast<size_t>(p) * bm_words;
+    const uint32_t wpt = div_up(nwb, SEL_CT);
+    const uint32_t w0 = min(nwb, tid * wpt), w1 = min(nwb, w0 + wpt);
+    auto valid = [&](uint32_t x) {
+        const uint32_t r = khi - klo;
+        return x + 1 < nwb || (r & 31) == 0 ? 0xffffffffu : ((1u << (r & 31)) - 1u);
+    };
+    uint32_t cnt = 0, zeros = 0;
+    for (uint32_t x = w0; x < w1; ++x) {
+        cnt += __popc(bm[x]);
+        zeros += __popc(~bm[x] & valid(x));
+    }
+    if (total < K) {  // newest untaken keys first: higher shards, then this one's top
+        const uint32_t pad = K - total;
+        uint32_t zt;
+        const uint32_t zbelow = cscan(S, zeros, zt);
+        const uint32_t mine = pad > above ? min(pad - above, zt) : 0u;  // this shard's share
+        const uint32_t zabove = zt - zbelow - zeros;
+        uint32_t take = mine > zabove ? min(mine - zabove, zeros) : 0u;
+        for (uint32_t x = w1; x > w0 && take;) {
+            --x;
+            uint32_t z = ~bm[x] & valid(x);
+            while (z && take) {
+                const int hb = 31 - __clz(z);
+                bm[x] |= 1u << hb;
+                z &= ~(1u << hb);
+                --take;
+                ++cnt;
+            }
+        }
+    }
+    uint32_t n_local;
+    const uint32_t at = cscan(S, cnt, n_local);
+    uint32_t pos = at;
+    for (uint32_t x = w0; x < w1; ++x) {
+        uint32_t b = bm[x];
+        while (b) {
+            const int lb = __ffs(b) - 1;
+            st.sel[pos++] = klo + x * 32 + lb;
+            b &= b - 1;
+        }
+    }
+    if (tid == 0) {
+        kdev[p] = n_local;
+        reinterpret_cast<DecodeReport*>(st.rep)->k = K;
+    }
+}
+
+uint32_t shard_bucket_words() { return (SHARD_BCAP + 1) * 4; }
+uint32_t shard_hist_words() { return NB + NCB; }
+
+cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                                const uint32_t* ghist, const uint32_t* unit_meta,
+                                const uint32_t* log_idx, const double* log_sc, uint32_t log_cap,
+                                void* bucket, void* pstate, cudaStream_t st) {
+    shard_bucket_kernel<<<nprob, SEL_CT, 0, st>>>(probs, plans, ghist, unit_meta, log_idx, log_sc,
+                                                   log_cap, static_cast<uint4*>(bucket),
+                                                   static_cast<ShardPState*>(pstate));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_mark(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                              const void* pstate, const void* bucket_all, uint32_t nshard,
+                              const uint32_t* unit_meta, const uint32_t* log_idx,
+                              const double* log_sc, uint32_t log_cap, uint32_t* bitmap,
+                              uint32_t bm_words, uint32_t* counts, cudaStream_t st) {
+    const size_t smem = ((sizeof(SelHdr) + 127) & ~size_t(127)) + NB * 4;
+    shard_mark_kernel<<<nprob, SEL_CT, smem, st>>>(
+        probs, plans, static_cast<const ShardPState*>(pstate), static_cast<const uint4*>(bucket_all),
+        nshard, nprob, unit_meta, log_idx, log_sc, log_cap, bitmap, bm_words, counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shard_emit(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
+                              const uint32_t* counts_all, uint32_t nshard, uint32_t shard,
+                              uint32_t* bitmap, uint32_t bm_words, uint32_t* kdev, cudaStream_t st) {
+    shard_emit_kernel<<<nprob, SEL_CT, 0, st>>>(probs, plans, counts_all, nshard, shard, nprob,
+                                                bitmap, bm_words, kdev);
+    return cudaGetLastError();
+}
+
+uint32_t shard_pstate_bytes() { return sizeof(ShardPState); }
 
 static size_t select_smem() {
     return ((sizeof(SelHdr) + 127) & ~size_t(127)) + TILE * 8 + (NB + NCB) * 4 + BKT * 12 +

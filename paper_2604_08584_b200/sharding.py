@@ -6,6 +6,8 @@ layer step), done here with one all_gather over the process group.
 """
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
 
@@ -46,3 +48,193 @@ def gather_layer_output(local_out, n_kv_heads: int, group: int, world: int, rank
 def shard_table(n_kv_heads: int, world: int) -> np.ndarray:
     """owner[g] = rank owning KV head g."""
     return np.array([g % world for g in range(n_kv_heads)], np.int64)
+
+
+# ---------------------------------------------------------------------------
+# Sequence sharding (SURVEY.md §8(e), config c5): one logical KV-head session
+# split by key range over shards; the decode step runs the C ABI's phases
+# (csattn_shard_step) with the collectives between them. Two transports:
+#   local  all shards in this process (one context each, same device or
+#          several): collectives are plain tensor ops;
+#   dist   one shard per rank (torch.distributed, NCCL): all_reduce /
+#          all_gather on the same buffers.
+# The union of the shards' selections equals the unsharded selection (tests).
+# ---------------------------------------------------------------------------
+SHARD_ALIGN = 4096  # select tile: shard boundaries are multiples of it
+
+_U64_FLIP = -(1 << 63)  # uint64 <-> order-preserving int64 (XOR the sign bit)
+
+
+def shard_bounds(P: int, n_shards: int) -> list[tuple[int, int]]:
+    """Key ranges [lo, hi) of the shards: tile-aligned, ascending; the last
+    shard (the owner of appended keys) ends at P."""
+    tiles = -(-P // SHARD_ALIGN)
+    if n_shards < 1 or n_shards > tiles:
+        raise ValueError(f"{n_shards} shards for {tiles} tiles")
+    cuts = [(tiles * j) // n_shards * SHARD_ALIGN for j in range(n_shards)] + [P]
+    return [(cuts[j], cuts[j + 1]) for j in range(n_shards)]
+
+
+class ShardGroup:
+    """Sharded decode of a set of KV-head sessions.
+
+    local: ShardGroup.local(contexts, full_sessions, max_decode_steps) —
+           contexts[j] holds shard j of every session.
+    dist:  ShardGroup.distributed(ctx, full_sessions, rank, world, ...) —
+           this rank holds shard `rank`; collectives over the default group.
+    decode_step(q, new_keys, new_values) takes device tensors (sum of groups
+    x d, n x d, n x d) and returns the output (sum of groups x d) and, if
+    asked, each query head's selected key indices (ascending).
+    """
+
+    def __init__(self, ctxs, shard_sessions, bounds, dist=None, rank=0):
+        import torch
+        from . import _abi, lib
+        self.torch, self._abi, self.lib = torch, _abi, lib()
+        self.ctxs = ctxs                # per local shard
+        self.shards = shard_sessions    # [local shard][session]
+        self.bounds = bounds
+        self.dist, self.rank = dist, rank
+        self.n_shards = len(bounds)
+        s0 = shard_sessions[0][0]
+        info = s0.info()
+        self.d, self.groups = info.dim, [s.info().group for s in shard_sessions[0]]
+        self.nq, self.ns = sum(self.groups), len(shard_sessions[0])
+        hw, bw, pf, vw = (C.c_uint64() for _ in range(4))
+        from . import _check
+        self._check = _check
+        _check(self.lib.csattn_shard_buffer_words(s0.h, C.byref(hw), C.byref(bw), C.byref(pf),
+                                                  C.byref(vw)))
+        self.hw, self.bw, self.pf, self.vw = hw.value, bw.value, pf.value, vw.value
+
+    # -- construction --
+    @classmethod
+    def local(cls, ctxs, full_sessions, max_decode_steps):
+        from . import Session, _check, lib
+        P = full_sessions[0].info().prefill_len
+        bounds = shard_bounds(P, len(ctxs))
+        shards = []
+        for j, (c, (lo, hi)) in enumerate(zip(ctxs, bounds)):
+            row = []
+            for fs in full_sessions:
+                h = C.c_void_p()
+                _check(lib().csattn_shard_create(c.h, fs.h, lo, hi, int(j == len(bounds) - 1),
+                                                 max_decode_steps, C.byref(h)))
+                row.append(Session(c, h))
+            shards.append(row)
+        return cls(ctxs, shards, bounds)
+
+    @classmethod
+    def distributed(cls, ctx, full_sessions, rank, world, max_decode_steps, dist):
+        from . import Session, _check, lib
+        P = full_sessions[0].info().prefill_len
+        bounds = shard_bounds(P, world)
+        lo, hi = bounds[rank]
+        row = []
+        for fs in full_sessions:
+            h = C.c_void_p()
+            _check(lib().csattn_shard_create(ctx.h, fs.h, lo, hi, int(rank == world - 1),
+                                             max_decode_steps, C.byref(h)))
+            row.append(Session(ctx, h))
+        return cls([ctx], [row], bounds, dist=dist, rank=rank)
+
+    # -- one decode step --
+    def decode_step(self, q, new_keys, new_values, want_selected=False, k_max=None):
+        torch = self.torch
+        dev = q.device
+        L = len(self.shards)  # shards held by this process
+        nq, d = self.nq, self.d
+        io = []
+        bufs = []
+        for j in range(L):
+            b = {
+                "ghist": torch.zeros((nq, self.hw), dtype=torch.int32, device=dev),
+                "bucket": torch.zeros((nq, self.bw), dtype=torch.int32, device=dev),
+                "counts": torch.zeros((nq, 2), dtype=torch.int32, device=dev),
+                "partial": torch.zeros((nq, self.pf), dtype=torch.float32, device=dev),
+                "victim": torch.zeros((self.ns, self.vw), dtype=torch.int64, device=dev),
+                "out": torch.empty((nq, d), dtype=torch.float32, device=dev),
+                "nsel": torch.zeros((nq,), dtype=torch.int32, device=dev),
+            }
+            if want_selected:
+                b["sel"] = torch.zeros((nq, k_max), dtype=torch.int32, device=dev)
+            bufs.append(b)
+            x = self._abi.ShardIoC()
+            x.q, x.new_keys, x.new_values = q.data_ptr(), new_keys.data_ptr(), new_values.data_ptr()
+            x.ghist, x.bucket = b["ghist"].data_ptr(), b["bucket"].data_ptr()
+            x.counts, x.partial = b["counts"].data_ptr(), b["partial"].data_ptr()
+            x.out, x.victim = b["out"].data_ptr(), b["victim"].data_ptr()
+            x.n_selected = b["nsel"].data_ptr()
+            if want_selected:
+                x.selected, x.sel_stride = b["sel"].data_ptr(), k_max
+            x.shard_index = self.rank if self.dist else j
+            x.n_shards = self.n_shards
+            io.append(x)
+
+        def run(phase):
+            for j in range(L):
+                hs = (C.c_void_p * self.ns)(*[s.h.value for s in self.shards[j]])
+                self._check(self.lib.csattn_shard_step(self.ctxs[j].h, self.ns, hs, phase,
+                                                       C.byref(io[j])))
+
+        def all_reduce_sum(key):
+            if self.dist:
+                self.dist.all_reduce(bufs[0][key])
+            else:
+                tot = torch.stack([b[key] for b in bufs]).sum(0)
+                for b in bufs:
+                    b[key].copy_(tot)
+
+        def all_gather(key, all_key):
+            if self.dist:
+                parts = [torch.empty_like(bufs[0][key]) for _ in range(self.n_shards)]
+                self.dist.all_gather(parts, bufs[0][key])
+                g = torch.stack(parts).contiguous()
+            else:
+                g = torch.stack([b[key] for b in bufs]).contiguous()
+            for j in range(L):
+                bufs[j][all_key] = g
+                setattr(io[j], all_key, g.data_ptr())
+
+        def all_reduce_min_u64(key):
+            if self.dist:
+                t = bufs[0][key] ^ _U64_FLIP
+                self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+                bufs[0][key].copy_(t ^ _U64_FLIP)
+            else:
+                m = (torch.stack([b[key] for b in bufs]) ^ _U64_FLIP).min(0).values ^ _U64_FLIP
+                for b in bufs:
+                    b[key].copy_(m)
+
+        A = self._abi
+        run(A.SHARD_SCAN)
+        all_reduce_sum("ghist")
+        run(A.SHARD_BUCKET)
+        all_gather("bucket", "bucket_all")
+        run(A.SHARD_MARK)
+        all_gather("counts", "counts_all")
+        run(A.SHARD_EMIT)
+        all_gather("partial", "partial_all")
+        run(A.SHARD_MERGE)
+        run(A.SHARD_VICTIM)
+        all_reduce_min_u64("victim")
+        run(A.SHARD_INSERT)
+        out = bufs[0]["out"]
+        if not want_selected:
+            return out, None
+        # every shard's ascending local selection, concatenated in shard order
+        sels = []
+        if self.dist:
+            n_all = [torch.empty_like(bufs[0]["nsel"]) for _ in range(self.n_shards)]
+            self.dist.all_gather(n_all, bufs[0]["nsel"])
+            s_all = [torch.empty_like(bufs[0]["sel"]) for _ in range(self.n_shards)]
+            self.dist.all_gather(s_all, bufs[0]["sel"])
+        else:
+            n_all = [b["nsel"] for b in bufs]
+            s_all = [b["sel"] for b in bufs]
+        n_all = [x.cpu().numpy() for x in n_all]
+        s_all = [x.cpu().numpy() for x in s_all]
+        for p in range(nq):
+            sels.append(np.concatenate([s_all[j][p, :n_all[j][p]] for j in range(self.n_shards)])
+                        .astype(np.uint32))
+        return out, sels
