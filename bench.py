@@ -53,6 +53,9 @@ CONFIGS = {
                           "prefilled context"),
     "c4": (131072, 1, 32, "full 32-layer Llama-3.1-8B-shaped decode at 128K, KV heads sharded "
                           "across the GPUs of the run"),
+    "c5": (1048576, 1, 1, "1M-token context, Llama-3.1-8B-shaped layer, sequence-sharded (>= 4 "
+                          "shards, spread over the GPUs of the run) with the histogram / bucket / "
+                          "LSE / victim collectives"),
 }
 N_KV, GROUP, D, M, C_CENT = 8, 4, 128, 8, 64
 DWELLS = (32, 16, 64, 8)
@@ -251,6 +254,144 @@ def cpu_baseline_from_gpu(cs, ob, sessions_by_head, data, P, n_seq, steps, T_use
 # our arm
 # --------------------------------------------------------------------------
 
+def run_c5(args, config, P, rank, world, local):
+    """Config c5: a 1M-token layer (8 KV heads x GQA 4), sequence-sharded.
+    Shards are tile-aligned key ranges of <= 256K keys; there are
+    max(4, world) of them, world/ranks each holding the same number. Every
+    rank builds the 8 full sessions (deterministic: identical everywhere),
+    keeps its shards and drops the rest. A step = one sharded decode step of
+    the layer (ShardGroup.decode_step): per-shard scan, then the histogram
+    all-reduce, bucket all-gather, count all-gather, attention-partial
+    all-gather + LSE merge, victim all-reduce and the insert."""
+    import torch
+    import paper_2604_08584_b200 as cs
+    from paper_2604_08584_b200.sharding import ShardGroup
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    n_total = max(4, world)
+    L = n_total // world
+    if L * world != n_total:
+        raise SystemExit(f"c5 needs a world size dividing {n_total}")
+    ctxs = [cs.Context(local, stream.cuda_stream) for _ in range(L)]
+    steps, warm = args.steps, args.warmup
+    e2e_steps = min(steps, 5)
+    T = warm + steps + e2e_steps + 1
+    widths = [D // M] * M
+    rc = cs.RetrievalConfig()
+    heads = list(range(N_KV))
+    t0 = time.perf_counter()
+    data = dict(zip(heads, gen_heads(cs, heads, P + T)))
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    full = []
+    for g in heads:
+        q, k, v = data[g]
+        pooled = np.ascontiguousarray(np.concatenate([q[:P, r] for r in range(GROUP)]))
+        ic = cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
+        full.append(cs.prefill(ctxs[0], pooled, k[:P], v[:P], widths, ic, rc, group=GROUP,
+                               max_decode_steps=1))
+        del pooled
+    t_build = time.perf_counter() - t0
+    if world == 1:
+        grp = ShardGroup.local(ctxs, full, max_decode_steps=T)
+    else:
+        grp = ShardGroup.distributed(ctxs, full, rank, world, T, dist)
+    for f in full:
+        f.close()
+    nq = N_KV * GROUP
+    qh = np.stack([np.concatenate([data[g][0][P + t] for g in heads]) for t in range(T)])
+    kh = np.stack([np.stack([data[g][1][P + t] for g in heads]) for t in range(T)])
+    vh = np.stack([np.stack([data[g][2][P + t] for g in heads]) for t in range(T)])
+    qd, kd, vd = (torch.from_numpy(x).cuda() for x in (qh, kh, vh))
+    torch.cuda.synchronize()
+
+    def step(t):
+        with torch.cuda.stream(stream):
+            return grp.decode_step(qd[t], kd[t], vd[t])
+
+    t = 0
+    for _ in range(warm):
+        step(t)
+        t += 1
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = P + t
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+        for _ in range(steps):
+            step(t)
+            t += 1
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        tm = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ms = float(tm.item())
+    ms_per_step = ms / steps
+    # e2e: host inputs copied in, output copied out, inside the timed region
+    qp = torch.from_numpy(qh).pin_memory()
+    kp = torch.from_numpy(kh).pin_memory()
+    vp_ = torch.from_numpy(vh).pin_memory()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    te0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        with torch.cuda.stream(stream):
+            out, _ = grp.decode_step(qp[t].cuda(non_blocking=True), kp[t].cuda(non_blocking=True),
+                                     vp_[t].cuda(non_blocking=True))
+            host_out = out.cpu()
+        t += 1
+    e2e_ms = (time.perf_counter() - te0) * 1e3 / e2e_steps
+    if dist:
+        tm = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tm.item())
+    assert np.isfinite(host_out.numpy()).all()
+    L_list = 209716
+    Kmean = keep_count(0.05, n0 + steps // 2)
+    per_query = nq * (M * L_list * 8 + Kmean * (2 * D * 4 + 4) + C_CENT * D * 4 + 2 * D * 4)
+    peak, peak_src = measured_peak()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": ms_per_step * 1e3, "unit": "us", "n_gpus": world,
+            "steps": steps, "warmup": warm, "ms_per_step": ms_per_step, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference make_synthetic, prefix-stable rows)",
+            "config": dict(config, parallelism=f"sequence shards x{n_total} over {world} GPU(s)",
+                           l2_policy="working set >> L2; no flush"),
+            "hbm_gbs_per_step": per_query / (ms_per_step * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "layer step (all sharded phases)",
+                         "achieved": per_query / (ms_per_step * 1e-3) / 1e9, "peak": peak * world,
+                         "unit": "GB/s", "frac": per_query / (ms_per_step * 1e-3) / 1e9 / (peak * world),
+                         "traffic": None, "peak_source": peak_src,
+                         "alg_bytes_per_launch": per_query, "alg_bytes": "per query head (8(d))"},
+            "e2e": {"value": e2e_ms * 1e3, "unit": "us",
+                    "h2d_bytes_per_step": int(qh[0].nbytes + kh[0].nbytes + vh[0].nbytes),
+                    "d2h_bytes_per_step": int(nq * D * 4)},
+            "gpu_launches": int(sum(c.launches for c in ctxs)),
+            "clocks": clk.summary(),
+            "setup_s": {"synthetic": round(t_gen, 2), "gpu_build": round(t_build, 2)},
+            "cpu_baseline": None,
+        }))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -297,6 +438,8 @@ def main():
     from paper_2604_08584_b200 import _abi
     import ctypes as C
 
+    if args.config == "c5":
+        return run_c5(args, config, P, rank, world, local)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:

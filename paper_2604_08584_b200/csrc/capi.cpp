@@ -162,6 +162,7 @@ struct csattn_ctx_s {
     std::vector<uint32_t> sh_chunk_host;
     std::vector<uint64_t> sh_Ks;
     uint64_t sh_nq = 0, sh_ns = 0, sh_ucap = 0, sh_bm_words = 0, sh_nchunks = 0;
+    uint32_t sh_split = 1;
     bool sh_scanned = false;
     bool no_split = std::getenv("CSATTN_NO_SPLIT") != nullptr;
     uint64_t log_cap = 0, log_rows = 0;
@@ -1392,13 +1393,23 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
             }
             if (io->selected && io->sel_stride < *std::max_element(ctx->sh_Ks.begin(), ctx->sh_Ks.end()))
                 fail(CSATTN_ERR_PARAMETER, "selected stride is below K");
+            // part units over the shard's tiles so a small batch fills the GPU
+            uint64_t mintiles = ~0ull;
+            for (uint64_t i = 0; i < ns; ++i) {
+                const uint64_t khi = ss[i]->h.owner ? ss[i]->N : ss[i]->h.key_hi;
+                mintiles = std::min(mintiles, (khi - ss[i]->h.key_lo + tile - 1) / tile);
+            }
+            const uint64_t slots = 2ull * static_cast<uint64_t>(ctx->num_sms);
+            uint64_t split = (nq < slots && !ctx->no_split) ? (slots + nq - 1) / nq : 1;
+            split = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(split, 16), mintiles));
+            ctx->sh_split = static_cast<uint32_t>(split);
             ctx->sh_nq = nq;
             ctx->sh_ns = ns;
-            ctx->sh_ucap = maxtiles * tile;
+            ctx->sh_ucap = (maxtiles + split - 1) / split * tile;
             ctx->sh_bm_words = (maxrange + 31) / 32;
-            ctx->sh_umeta.ensure(nq * csa::select_unit_meta_words() * 4);
-            ctx->sh_ulog_idx.ensure(nq * ctx->sh_ucap * 4);
-            ctx->sh_ulog_sc.ensure(nq * ctx->sh_ucap * 8);
+            ctx->sh_umeta.ensure(nq * split * csa::select_unit_meta_words() * 4);
+            ctx->sh_ulog_idx.ensure(nq * split * ctx->sh_ucap * 4);
+            ctx->sh_ulog_sc.ensure(nq * split * ctx->sh_ucap * 8);
             ctx->sh_pstate.ensure(nq * csa::shard_pstate_bytes());
             ctx->sh_bitmap.ensure(nq * ctx->sh_bm_words * 4);
             ctx->sh_kdev.ensure(nq * 4);
@@ -1466,15 +1477,15 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
             const csa::DecodeProblem* dprobs = ctx->sh_desc.as<csa::DecodeProblem>();
             ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), st),
                "route launch");
-            const uint32_t grid = csa::select_grid(static_cast<uint32_t>(nq), ctx->num_sms);
+            const uint32_t grid = static_cast<uint32_t>(std::min<uint64_t>(nq * split, slots));
             ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), grid,
                                   ctx->sh_ulog_idx.as<uint32_t>(), ctx->sh_ulog_sc.as<double>(),
                                   static_cast<uint32_t>(ctx->sh_ucap), nullptr, nullptr, nullptr,
-                                  nullptr, 0.0, 1, ctx->sh_umeta.as<uint32_t>(), st),
+                                  nullptr, 0.0, static_cast<uint32_t>(split),
+                                  ctx->sh_umeta.as<uint32_t>(), st),
                "select (shard scan) launch");
-            const uint64_t hw = csa::shard_hist_words();
-            ck(cudaMemcpy2DAsync(io->ghist, hw * 4, ctx->sh_umeta.p, csa::select_unit_meta_words() * 4,
-                                 hw * 4, nq, cudaMemcpyDeviceToDevice, st),
+            ck(csa::launch_shard_hist_sum(ctx->sh_umeta.as<uint32_t>(), static_cast<uint32_t>(nq),
+                                          static_cast<uint32_t>(split), io->ghist, st),
                "histograms");
             ctx->launches += 2;
             ctx->sh_scanned = true;
@@ -1491,8 +1502,8 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                 ck(csa::launch_shard_bucket(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
                                             io->ghist, ctx->sh_umeta.as<uint32_t>(),
                                             ctx->sh_ulog_idx.as<uint32_t>(), ctx->sh_ulog_sc.as<double>(),
-                                            static_cast<uint32_t>(ctx->sh_ucap), io->bucket,
-                                            ctx->sh_pstate.p, st),
+                                            static_cast<uint32_t>(ctx->sh_ucap), ctx->sh_split,
+                                            io->bucket, ctx->sh_pstate.p, st),
                    "shard bucket launch");
                 break;
             case CSATTN_SHARD_MARK:
@@ -1500,7 +1511,7 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                                           ctx->sh_pstate.p, io->bucket_all, io->n_shards,
                                           ctx->sh_umeta.as<uint32_t>(), ctx->sh_ulog_idx.as<uint32_t>(),
                                           ctx->sh_ulog_sc.as<double>(), static_cast<uint32_t>(ctx->sh_ucap),
-                                          ctx->sh_bitmap.as<uint32_t>(),
+                                          ctx->sh_split, ctx->sh_bitmap.as<uint32_t>(),
                                           static_cast<uint32_t>(ctx->sh_bm_words), io->counts, st),
                    "shard mark launch");
                 break;

@@ -40,15 +40,18 @@ cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* pla
 uint32_t shard_bucket_words();  // per problem, uint32 words of a bucket record
 uint32_t shard_hist_words();    // per problem histogram words (all-reduced)
 uint32_t shard_pstate_bytes();
+cudaError_t launch_shard_hist_sum(const uint32_t* unit_meta, uint32_t nprob, uint32_t split,
+                                  uint32_t* ghist, cudaStream_t st);
 cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 const uint32_t* ghist, const uint32_t* unit_meta,
                                 const uint32_t* log_idx, const double* log_sc, uint32_t log_cap,
-                                void* bucket, void* pstate, cudaStream_t st);
+                                uint32_t split, void* bucket, void* pstate, cudaStream_t st);
 cudaError_t launch_shard_mark(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                               const void* pstate, const void* bucket_all, uint32_t nshard,
                               const uint32_t* unit_meta, const uint32_t* log_idx,
-                              const double* log_sc, uint32_t log_cap, uint32_t* bitmap,
-                              uint32_t bm_words, uint32_t* counts, cudaStream_t st);
+                              const double* log_sc, uint32_t log_cap, uint32_t split,
+                              uint32_t* bitmap, uint32_t bm_words, uint32_t* counts,
+                              cudaStream_t st);
 cudaError_t launch_shard_emit(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                               const uint32_t* counts_all, uint32_t nshard, uint32_t shard,
                               uint32_t* bitmap, uint32_t bm_words, uint32_t* kdev, cudaStream_t st);

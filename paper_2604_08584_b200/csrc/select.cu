@@ -1097,7 +1097,8 @@ __global__ void __launch_bounds__(SEL_CT)
 shard_bucket_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restrict__ plans,
                     const uint32_t* __restrict__ ghist, const uint32_t* __restrict__ unit_meta,
                     const uint32_t* __restrict__ log_idx, const double* __restrict__ log_sc,
-                    uint32_t log_cap, uint4* __restrict__ bucket, ShardPState* __restrict__ pstate) {
+                    uint32_t log_cap, uint32_t split, uint4* __restrict__ bucket,
+                    ShardPState* __restrict__ pstate) {
     __shared__ SelHdr S;
     const uint32_t tid = threadIdx.x, p = blockIdx.x;
     ProbState st;
@@ -1117,12 +1118,12 @@ shard_bucket_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __
     cbar();
     const uint32_t dsel = S.f_bin;
     const bool collect = st.need && !S.f_take_all;
-    const uint32_t* wl = unit_meta + static_cast<size_t>(p) * UNIT_META + NB + NCB;
     uint4* bk = bucket + static_cast<size_t>(p) * (SHARD_BCAP + 1);
     if (collect) {
-        for (uint32_t w = 0; w < SEL_CW; ++w) {
-            const size_t base = static_cast<size_t>(p) * log_cap + w * (log_cap / SEL_CW);
-            const uint32_t n = __ldcg(wl + w);
+        for (uint32_t sg = 0; sg < split * SEL_CW; ++sg) {  // (part unit, warp) log segments
+            const uint32_t u = p * split + sg / SEL_CW, w = sg % SEL_CW;
+            const size_t base = static_cast<size_t>(u) * log_cap + w * (log_cap / SEL_CW);
+            const uint32_t n = __ldcg(unit_meta + static_cast<size_t>(u) * UNIT_META + NB + NCB + w);
             for (uint32_t e = tid; e < n; e += SEL_CT) {
                 const double sv = __ldcg(log_sc + base + e);
                 if (bin_of(sv, st.lo, st.scale) != dsel) continue;
@@ -1147,8 +1148,8 @@ shard_mark_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __re
                   const ShardPState* __restrict__ pstate, const uint4* __restrict__ bucket_all,
                   uint32_t nshard, uint32_t nprob, const uint32_t* __restrict__ unit_meta,
                   const uint32_t* __restrict__ log_idx, const double* __restrict__ log_sc,
-                  uint32_t log_cap, uint32_t* __restrict__ bitmap, uint32_t bm_words,
-                  uint32_t* __restrict__ counts) {
+                  uint32_t log_cap, uint32_t split, uint32_t* __restrict__ bitmap,
+                  uint32_t bm_words, uint32_t* __restrict__ counts) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127)));
@@ -1194,10 +1195,10 @@ shard_mark_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __re
     for (uint32_t x = tid; x < nwb; x += SEL_CT) bm[x] = 0;
     cbar();
     if (need) {
-        const uint32_t* wl = unit_meta + static_cast<size_t>(p) * UNIT_META + NB + NCB;
-        for (uint32_t w = 0; w < SEL_CW; ++w) {
-            const size_t base = static_cast<size_t>(p) * log_cap + w * (log_cap / SEL_CW);
-            const uint32_t n = __ldcg(wl + w);
+        for (uint32_t sg = 0; sg < split * SEL_CW; ++sg) {  // (part unit, warp) log segments
+            const uint32_t u = p * split + sg / SEL_CW, w = sg % SEL_CW;
+            const size_t base = static_cast<size_t>(u) * log_cap + w * (log_cap / SEL_CW);
+            const uint32_t n = __ldcg(unit_meta + static_cast<size_t>(u) * UNIT_META + NB + NCB + w);
             for (uint32_t e = tid; e < n; e += SEL_CT) {
                 const double sv = __ldcg(log_sc + base + e);
                 const uint32_t b = bin_of(sv, st.lo, st.scale);
@@ -1297,12 +1298,31 @@ shard_emit_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __re
 uint32_t shard_bucket_words() { return (SHARD_BCAP + 1) * 4; }
 uint32_t shard_hist_words() { return NB + NCB; }
 
+// per problem: sum of its `split` part units' histograms -> ghist (the shard's
+// histogram, all-reduced over the shards by the caller)
+__global__ void shard_hist_sum_kernel(const uint32_t* __restrict__ unit_meta, uint32_t split,
+                                      uint32_t* __restrict__ ghist) {
+    const uint32_t p = blockIdx.x;
+    for (uint32_t x = threadIdx.x; x < NB + NCB; x += blockDim.x) {
+        uint32_t v = 0;
+        for (uint32_t j = 0; j < split; ++j)
+            v += __ldcg(unit_meta + (static_cast<size_t>(p) * split + j) * UNIT_META + x);
+        ghist[static_cast<size_t>(p) * (NB + NCB) + x] = v;
+    }
+}
+
+cudaError_t launch_shard_hist_sum(const uint32_t* unit_meta, uint32_t nprob, uint32_t split,
+                                  uint32_t* ghist, cudaStream_t st) {
+    shard_hist_sum_kernel<<<nprob, 256, 0, st>>>(unit_meta, split, ghist);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 const uint32_t* ghist, const uint32_t* unit_meta,
                                 const uint32_t* log_idx, const double* log_sc, uint32_t log_cap,
-                                void* bucket, void* pstate, cudaStream_t st) {
+                                uint32_t split, void* bucket, void* pstate, cudaStream_t st) {
     shard_bucket_kernel<<<nprob, SEL_CT, 0, st>>>(probs, plans, ghist, unit_meta, log_idx, log_sc,
-                                                   log_cap, static_cast<uint4*>(bucket),
+                                                   log_cap, split, static_cast<uint4*>(bucket),
                                                    static_cast<ShardPState*>(pstate));
     return cudaGetLastError();
 }
@@ -1310,12 +1330,13 @@ cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* pla
 cudaError_t launch_shard_mark(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                               const void* pstate, const void* bucket_all, uint32_t nshard,
                               const uint32_t* unit_meta, const uint32_t* log_idx,
-                              const double* log_sc, uint32_t log_cap, uint32_t* bitmap,
-                              uint32_t bm_words, uint32_t* counts, cudaStream_t st) {
+                              const double* log_sc, uint32_t log_cap, uint32_t split,
+                              uint32_t* bitmap, uint32_t bm_words, uint32_t* counts,
+                              cudaStream_t st) {
     const size_t smem = ((sizeof(SelHdr) + 127) & ~size_t(127)) + NB * 4;
     shard_mark_kernel<<<nprob, SEL_CT, smem, st>>>(
         probs, plans, static_cast<const ShardPState*>(pstate), static_cast<const uint4*>(bucket_all),
-        nshard, nprob, unit_meta, log_idx, log_sc, log_cap, bitmap, bm_words, counts);
+        nshard, nprob, unit_meta, log_idx, log_sc, log_cap, split, bitmap, bm_words, counts);
     return cudaGetLastError();
 }
 

@@ -75,6 +75,41 @@ def shard_bounds(P: int, n_shards: int) -> list[tuple[int, int]]:
     return [(cuts[j], cuts[j + 1]) for j in range(n_shards)]
 
 
+def coll_all_reduce_sum(bufs, dist=None):
+    """In place: every local buffer becomes the sum over all shards (local
+    ones, then across ranks)."""
+    import torch
+    tot = torch.stack(bufs).sum(0) if len(bufs) > 1 else bufs[0].clone()
+    if dist is not None:
+        dist.all_reduce(tot)
+    for b in bufs:
+        b.copy_(tot)
+
+
+def coll_all_gather(bufs, dist=None, world=1):
+    """[n_shards, ...]: every shard's buffer in global shard order (rank-major,
+    then local order)."""
+    import torch
+    mine = torch.stack(bufs).contiguous()
+    if dist is None:
+        return mine
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    return torch.cat(parts).contiguous()
+
+
+def coll_all_reduce_min_u64(bufs, dist=None):
+    """In place: elementwise min of uint64 values stored in int64 tensors
+    (sign bit flipped so that signed order equals unsigned order)."""
+    import torch
+    m = (torch.stack(bufs) ^ _U64_FLIP).min(0).values
+    if dist is not None:
+        dist.all_reduce(m, op=dist.ReduceOp.MIN)
+    m = m ^ _U64_FLIP
+    for b in bufs:
+        b.copy_(m)
+
+
 class ShardGroup:
     """Sharded decode of a set of KV-head sessions.
 
@@ -87,15 +122,16 @@ class ShardGroup:
     asked, each query head's selected key indices (ascending).
     """
 
-    def __init__(self, ctxs, shard_sessions, bounds, dist=None, rank=0):
+    def __init__(self, ctxs, shard_sessions, bounds, dist=None, rank=0, world=1):
         import torch
         from . import _abi, lib
         self.torch, self._abi, self.lib = torch, _abi, lib()
         self.ctxs = ctxs                # per local shard
         self.shards = shard_sessions    # [local shard][session]
-        self.bounds = bounds
-        self.dist, self.rank = dist, rank
+        self.bounds = bounds            # all shards, global order
+        self.dist, self.rank, self.world = dist, rank, world
         self.n_shards = len(bounds)
+        self.first = rank * len(shard_sessions)  # global index of local shard 0
         s0 = shard_sessions[0][0]
         info = s0.info()
         self.d, self.groups = info.dim, [s.info().group for s in shard_sessions[0]]
@@ -125,28 +161,37 @@ class ShardGroup:
         return cls(ctxs, shards, bounds)
 
     @classmethod
-    def distributed(cls, ctx, full_sessions, rank, world, max_decode_steps, dist):
+    def distributed(cls, ctxs, full_sessions, rank, world, max_decode_steps, dist):
+        """This rank holds shards [rank*len(ctxs), (rank+1)*len(ctxs)) of
+        world*len(ctxs) shards (one context each, on this rank's GPU)."""
         from . import Session, _check, lib
         P = full_sessions[0].info().prefill_len
-        bounds = shard_bounds(P, world)
-        lo, hi = bounds[rank]
-        row = []
-        for fs in full_sessions:
-            h = C.c_void_p()
-            _check(lib().csattn_shard_create(ctx.h, fs.h, lo, hi, int(rank == world - 1),
-                                             max_decode_steps, C.byref(h)))
-            row.append(Session(ctx, h))
-        return cls([ctx], [row], bounds, dist=dist, rank=rank)
+        L = len(ctxs)
+        bounds = shard_bounds(P, world * L)
+        shards = []
+        for j, c in enumerate(ctxs):
+            g = rank * L + j
+            lo, hi = bounds[g]
+            row = []
+            for fs in full_sessions:
+                h = C.c_void_p()
+                _check(lib().csattn_shard_create(c.h, fs.h, lo, hi, int(g == len(bounds) - 1),
+                                                 max_decode_steps, C.byref(h)))
+                row.append(Session(c, h))
+            shards.append(row)
+        return cls(ctxs, shards, bounds, dist=dist, rank=rank, world=world)
 
     # -- one decode step --
-    def decode_step(self, q, new_keys, new_values, want_selected=False, k_max=None):
+    def _buffers(self, dev, want_selected, k_max):
+        """Per-local-shard I/O buffers and ShardIoC structs, cached across steps
+        (re-made only when the selected-set capacity grows)."""
         torch = self.torch
-        dev = q.device
-        L = len(self.shards)  # shards held by this process
+        key = (str(dev), bool(want_selected), int(k_max or 0))
+        if getattr(self, "_cache_key", None) == key:
+            return self._bufs, self._io
         nq, d = self.nq, self.d
-        io = []
-        bufs = []
-        for j in range(L):
+        bufs, io = [], []
+        for j in range(len(self.shards)):
             b = {
                 "ghist": torch.zeros((nq, self.hw), dtype=torch.int32, device=dev),
                 "bucket": torch.zeros((nq, self.bw), dtype=torch.int32, device=dev),
@@ -160,51 +205,44 @@ class ShardGroup:
                 b["sel"] = torch.zeros((nq, k_max), dtype=torch.int32, device=dev)
             bufs.append(b)
             x = self._abi.ShardIoC()
-            x.q, x.new_keys, x.new_values = q.data_ptr(), new_keys.data_ptr(), new_values.data_ptr()
             x.ghist, x.bucket = b["ghist"].data_ptr(), b["bucket"].data_ptr()
             x.counts, x.partial = b["counts"].data_ptr(), b["partial"].data_ptr()
             x.out, x.victim = b["out"].data_ptr(), b["victim"].data_ptr()
             x.n_selected = b["nsel"].data_ptr()
             if want_selected:
                 x.selected, x.sel_stride = b["sel"].data_ptr(), k_max
-            x.shard_index = self.rank if self.dist else j
+            x.shard_index = self.first + j
             x.n_shards = self.n_shards
             io.append(x)
+        self._hs = [(C.c_void_p * self.ns)(*[s.h.value for s in row]) for row in self.shards]
+        self._cache_key, self._bufs, self._io = key, bufs, io
+        return bufs, io
+
+    def decode_step(self, q, new_keys, new_values, want_selected=False, k_max=None):
+        torch = self.torch
+        dev = q.device
+        L = len(self.shards)  # shards held by this process
+        nq = self.nq
+        bufs, io = self._buffers(dev, want_selected, k_max)
+        for x in io:
+            x.q, x.new_keys, x.new_values = q.data_ptr(), new_keys.data_ptr(), new_values.data_ptr()
 
         def run(phase):
             for j in range(L):
-                hs = (C.c_void_p * self.ns)(*[s.h.value for s in self.shards[j]])
-                self._check(self.lib.csattn_shard_step(self.ctxs[j].h, self.ns, hs, phase,
+                self._check(self.lib.csattn_shard_step(self.ctxs[j].h, self.ns, self._hs[j], phase,
                                                        C.byref(io[j])))
 
         def all_reduce_sum(key):
-            if self.dist:
-                self.dist.all_reduce(bufs[0][key])
-            else:
-                tot = torch.stack([b[key] for b in bufs]).sum(0)
-                for b in bufs:
-                    b[key].copy_(tot)
+            coll_all_reduce_sum([bb[key] for bb in bufs], self.dist)
 
         def all_gather(key, all_key):
-            if self.dist:
-                parts = [torch.empty_like(bufs[0][key]) for _ in range(self.n_shards)]
-                self.dist.all_gather(parts, bufs[0][key])
-                g = torch.stack(parts).contiguous()
-            else:
-                g = torch.stack([b[key] for b in bufs]).contiguous()
+            g = coll_all_gather([bb[key] for bb in bufs], self.dist, self.world)
             for j in range(L):
                 bufs[j][all_key] = g
                 setattr(io[j], all_key, g.data_ptr())
 
         def all_reduce_min_u64(key):
-            if self.dist:
-                t = bufs[0][key] ^ _U64_FLIP
-                self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
-                bufs[0][key].copy_(t ^ _U64_FLIP)
-            else:
-                m = (torch.stack([b[key] for b in bufs]) ^ _U64_FLIP).min(0).values ^ _U64_FLIP
-                for b in bufs:
-                    b[key].copy_(m)
+            coll_all_reduce_min_u64([bb[key] for bb in bufs], self.dist)
 
         A = self._abi
         run(A.SHARD_SCAN)
@@ -223,17 +261,9 @@ class ShardGroup:
         if not want_selected:
             return out, None
         # every shard's ascending local selection, concatenated in shard order
+        n_all = coll_all_gather([bb["nsel"] for bb in bufs], self.dist, self.world).cpu().numpy()
+        s_all = coll_all_gather([bb["sel"] for bb in bufs], self.dist, self.world).cpu().numpy()
         sels = []
-        if self.dist:
-            n_all = [torch.empty_like(bufs[0]["nsel"]) for _ in range(self.n_shards)]
-            self.dist.all_gather(n_all, bufs[0]["nsel"])
-            s_all = [torch.empty_like(bufs[0]["sel"]) for _ in range(self.n_shards)]
-            self.dist.all_gather(s_all, bufs[0]["sel"])
-        else:
-            n_all = [b["nsel"] for b in bufs]
-            s_all = [b["sel"] for b in bufs]
-        n_all = [x.cpu().numpy() for x in n_all]
-        s_all = [x.cpu().numpy() for x in s_all]
         for p in range(nq):
             sels.append(np.concatenate([s_all[j][p, :n_all[j][p]] for j in range(self.n_shards)])
                         .astype(np.uint32))

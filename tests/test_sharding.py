@@ -79,3 +79,42 @@ def test_gloo_world2_output_gather_matches_single_process():
         assert p.exitcode == 0
     ref = _layer_outputs(list(range(N_KV)))
     assert np.array_equal(full, ref)
+
+
+def _coll_worker(rank, world, port, q):
+    import paper_2604_08584_b200.sharding as sh
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    L = 2  # local shards per rank
+    g = [torch.full((3, 4), 10 * rank + j, dtype=torch.int32) for j in range(L)]
+    sh.coll_all_reduce_sum(g, dist)
+    gathered = sh.coll_all_gather([torch.full((2,), 10 * rank + j) for j in range(L)], dist, world)
+    big = (1 << 63) + 5  # uint64 values above 2^63, stored as int64
+    v = [torch.tensor([(big + 100 * rank + 7 * j) - (1 << 64), rank + j], dtype=torch.int64)
+         for j in range(L)]
+    sh.coll_all_reduce_min_u64(v, dist)
+    if rank == 0:
+        q.put((g[0].tolist(), g[1].tolist(), gathered.tolist(), v[0].tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_shard_collectives():
+    """The sequence-sharding collectives over ranks x local shards equal their
+    single-process meaning: sum over all shards, gather in global shard order
+    (rank-major), unsigned-64-bit min."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coll_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    g0, g1, gathered, vmin = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    total = 0 + 1 + 10 + 11
+    assert g0 == g1 == [[total] * 4] * 3
+    assert gathered == [[0, 0], [1, 1], [10, 10], [11, 11]]
+    assert vmin[0] == ((1 << 63) + 5) - (1 << 64) and vmin[1] == 0
