@@ -286,7 +286,9 @@ csattn_status csattn_dense_attention(csattn_session s, const float* q, const uin
  * unsharded selection and the merged output agrees within 1e-3:
  *   SCAN    route + per-shard gather/accumulate/histogram -> io.ghist
  *           caller: all-reduce(sum, uint32) io.ghist over shards
- *   BUCKET  threshold bin; this shard's members of it -> io.bucket
+ *   BUCKET  threshold bin; this shard's members of it -> io.bucket. If
+ *           *io.spec_fail became non-zero the speculative cut missed: RESCAN,
+ *           all-reduce, BUCKET again (every shard sees the same flag)
  *           caller: all-gather io.bucket -> io.bucket_all (shard order)
  *   MARK    global rank of the bucket; local selection -> io.counts (2/problem)
  *           caller: all-gather io.counts -> io.counts_all
@@ -306,7 +308,8 @@ typedef enum csattn_shard_phase {
     CSATTN_SHARD_EMIT = 3,
     CSATTN_SHARD_MERGE = 4,
     CSATTN_SHARD_VICTIM = 5,
-    CSATTN_SHARD_INSERT = 6
+    CSATTN_SHARD_INSERT = 6,
+    CSATTN_SHARD_RESCAN = 7   /* SCAN without the speculative cut (after *io.spec_fail) */
 } csattn_shard_phase;
 
 typedef struct csattn_shard_io {
@@ -325,6 +328,9 @@ typedef struct csattn_shard_io {
     uint32_t* n_selected;            /* nq (nullable) */
     uint64_t sel_stride;
     unsigned long long* victim;      /* n x m*C */
+    uint32_t* spec_fail;             /* 1 word, set by BUCKET when the scan's speculative
+                                        cut (the previous step's threshold) was too high:
+                                        zero it, RESCAN, all-reduce, BUCKET again */
     uint32_t shard_index;
     uint32_t n_shards;
 } csattn_shard_io;

@@ -73,10 +73,12 @@ class ShardIoC(C.Structure):
                 ("counts", C.c_void_p), ("counts_all", C.c_void_p),
                 ("partial", C.c_void_p), ("partial_all", C.c_void_p), ("out", C.c_void_p),
                 ("selected", C.c_void_p), ("n_selected", C.c_void_p), ("sel_stride", C.c_uint64),
-                ("victim", C.c_void_p), ("shard_index", C.c_uint32), ("n_shards", C.c_uint32)]
+                ("victim", C.c_void_p), ("spec_fail", C.c_void_p), ("shard_index", C.c_uint32),
+                ("n_shards", C.c_uint32)]
 
 
-SHARD_SCAN, SHARD_BUCKET, SHARD_MARK, SHARD_EMIT, SHARD_MERGE, SHARD_VICTIM, SHARD_INSERT = range(7)
+SHARD_SCAN, SHARD_BUCKET, SHARD_MARK, SHARD_EMIT, SHARD_MERGE, SHARD_VICTIM, SHARD_INSERT, \
+    SHARD_RESCAN = range(8)
 
 SIGNATURES = {
     "csattn_index_config_default": (None, [P(IndexConfigC)]),

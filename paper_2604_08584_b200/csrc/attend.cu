@@ -58,7 +58,7 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     const uint32_t p = chunk_prob[c];
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
-    const uint32_t d = sd.d, K = P.kdev ? __ldcg(P.kdev + p) : P.K, P0 = sd.P;
+    const uint32_t d = sd.d, K = P.K, P0 = sd.P;
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -217,6 +217,7 @@ __device__ __forceinline__ float4 ld_row4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+template <bool PARTIAL>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
 __global__ void __launch_bounds__(ATT_THREADS)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
@@ -229,7 +230,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const uint32_t p = chunk_prob[c];
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
-    const uint32_t d = 128, K = P.kdev ? __ldcg(P.kdev + p) : P.K, P0 = sd.P;
+    const uint32_t d = 128, K = P.K, P0 = sd.P;
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -369,7 +370,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         if (sk > 0.0f) GS += sk * expf(__ldcg(pb + k * (d + 2)) - GM);
     }
     const float inv = 1.0f / GS;
-    if ((P.mode & MODE_PARTIAL) && P.out && threadIdx.x == 0) {
+    if (PARTIAL && P.out && threadIdx.x == 0) {
         P.out[0] = GM;  // (max, sum, acc[d]) for the cross-shard merge
         P.out[1] = GS;
     }
@@ -380,7 +381,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
             if (sk > 0.0f) o += __ldcg(pb + k * (d + 2) + 2 + t) * expf(__ldcg(pb + k * (d + 2)) - GM);
         }
         if (P.out) {
-            if (P.mode & MODE_PARTIAL) P.out[2 + t] = o;  // shard partial: unnormalised
+            if (PARTIAL) P.out[2 + t] = o;  // shard partial: unnormalised
             else P.out[t] = o * inv;
         }
     }
@@ -427,11 +428,13 @@ cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t npr
 
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
-                          uint32_t* counters, uint32_t d, cudaStream_t st) {
+                          uint32_t* counters, uint32_t d, cudaStream_t st, bool partial) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
-    if (d == 128) {
-        attend128_kernel<<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+    if (d == 128 && partial) {
+        attend128_kernel<true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+    } else if (d == 128) {
+        attend128_kernel<false><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
     } else if (d % 4 == 0) {
         if (d <= 128) CSA_ATT(1, 4);
         else if (d <= 256) CSA_ATT(2, 4);

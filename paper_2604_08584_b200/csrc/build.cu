@@ -131,6 +131,41 @@ build_lists_kernel(const SessionDev* __restrict__ sp, const float* __restrict__ 
     refill_table(S.r, sd, t, (P - 1) >> KEY_BLOCK_SHIFT);
 }
 
+// Shard extraction (sequence sharding): table t of the shard = the entries of
+// the full session's table t with keys in [key_lo, key_hi) — one contiguous
+// run of the index-sorted list of a freshly built session — then key-block
+// offsets and the low buffer are rebuilt over them (refill_table).
+__global__ void __launch_bounds__(BL_THREADS)
+shard_extract_kernel(const SessionDev* __restrict__ fp, const SessionDev* __restrict__ sp,
+                     uint32_t key_lo, uint32_t key_hi) {
+    __shared__ BuildSmem S;
+    const SessionDev& f = *fp;
+    const SessionDev& sd = *sp;
+    const uint32_t t = blockIdx.x;
+    const uint32_t* fbo = f.blk_off + static_cast<size_t>(t) * f.nb_stride;
+    const uint32_t last_f = (f.P - 1) >> KEY_BLOCK_SHIFT;
+    const uint32_t kb0 = key_lo >> KEY_BLOCK_SHIFT, kb1 = (key_hi + KEY_BLOCK - 1) >> KEY_BLOCK_SHIFT;
+    const uint32_t p0 = fbo[kb0];
+    const uint32_t p1 = kb1 <= last_f ? fbo[kb1] : f.n_used[t];
+    const uint2* src = f.ent + static_cast<size_t>(t) * f.cap2;
+    uint2* dst = sd.ent + static_cast<size_t>(t) * sd.cap2;
+    for (uint32_t i = threadIdx.x; i < p1 - p0; i += blockDim.x) dst[i] = src[p0 + i];
+    if (threadIdx.x == 0) {
+        sd.n_used[t] = p1 - p0;
+        sd.live[t] = p1 - p0;
+        sd.live_g[t] = f.live[t];
+        sd.tmm[t] = f.tmm[t];
+    }
+    __syncthreads();
+    refill_table(S.r, sd, t, (sd.P - 1) >> KEY_BLOCK_SHIFT);
+}
+
+cudaError_t launch_shard_extract(const SessionDev* full_dev, const SessionDev* shard_dev,
+                                 uint32_t tables, uint32_t key_lo, uint32_t key_hi, cudaStream_t st) {
+    shard_extract_kernel<<<tables, BL_THREADS, 0, st>>>(full_dev, shard_dev, key_lo, key_hi);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_build_scores(const SessionDev* s_dev, const SessionDev& sh, float* scores,
                                 cudaStream_t st) {
     uint32_t wmax = 0;

@@ -163,8 +163,10 @@ struct csattn_ctx_s {
     std::vector<uint64_t> sh_Ks;
     uint64_t sh_nq = 0, sh_ns = 0, sh_ucap = 0, sh_bm_words = 0, sh_nchunks = 0;
     uint32_t sh_split = 1;
+    double sh_spec = 0.0;
     bool sh_scanned = false;
     bool no_split = std::getenv("CSATTN_NO_SPLIT") != nullptr;
+    bool shard_split = std::getenv("CSATTN_SHARD_SPLIT") != nullptr;
     uint64_t log_cap = 0, log_rows = 0;
     int num_sms = 148;
     // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
@@ -1292,33 +1294,9 @@ csattn_status csattn_shard_create(csattn_ctx ctx, csattn_session full, uint64_t 
                                            " keys inside the prefill");
         if (full->rc.search_period != 1)
             fail(CSATTN_ERR_PARAMETER, "sharded decoding needs search period 1");
-        const csattn_session_info in = [&] {
-            csattn_session_info x{};
-            check_status(csattn_session_info_get(full, &x));
-            return x;
-        }();
-        const uint64_t T = full->T(), L = full->h.L, stride = std::max<uint64_t>(L, 1);
-        std::vector<uint32_t> lens(T), idx(T * stride);
-        std::vector<float> sc(T * stride), cent(static_cast<size_t>(full->h.C) * d);
-        check_status(csattn_session_export(full, lens.data(), idx.data(), sc.data(), stride, cent.data()));
-        // global bounds + sizes (replicated), then the shard's part of every list
-        std::vector<float2> tmm(T);
-        ck(cudaMemcpy(tmm.data(), full->tmm.p, T * sizeof(float2), cudaMemcpyDeviceToHost), "tmm");
-        std::vector<uint32_t> slens(T), sidx(T * stride), gl(T);
-        std::vector<float> ssc(T * stride);
-        for (uint64_t t = 0; t < T; ++t) {
-            gl[t] = lens[t];
-            uint32_t n = 0;
-            for (uint32_t r = 0; r < lens[t]; ++r) {
-                const uint32_t i = idx[t * stride + r];
-                if (i >= key_lo && i < key_hi) {
-                    sidx[t * stride + n] = i;
-                    ssc[t * stride + n] = sc[t * stride + r];
-                    ++n;
-                }
-            }
-            slens[t] = n;
-        }
+        const uint64_t T = full->T(), L = full->h.L;
+        if (full->ctx->device != ctx->device)
+            fail(CSATTN_ERR_PARAMETER, "shard and source session must share a device");
         csattn_retrieval_config rc = full->rc;
         rc.weights = full->weights.data();
         rc.n_weights = full->weights.size();
@@ -1338,7 +1316,8 @@ csattn_status csattn_shard_create(csattn_ctx ctx, csattn_session full, uint64_t 
         ck(cudaMemcpy(s->pre->v.p, full->h.vpre + key_lo * d, rows, cudaMemcpyDefault), "shard rows");
         s->h.kpre = s->pre->k.as<float>() - key_lo * d;
         s->h.vpre = s->pre->v.as<float>() - key_lo * d;
-        ck(cudaMemcpy(s->cent.p, full->cent.p, cent.size() * 4, cudaMemcpyDefault), "shard centroids");
+        ck(cudaMemcpy(s->cent.p, full->cent.p, static_cast<size_t>(full->h.C) * d * 4, cudaMemcpyDefault),
+           "shard centroids");
         s->live_g.alloc(T * 4);
         s->h.live_g = s->live_g.as<uint32_t>();
         s->h.key_lo = static_cast<uint32_t>(key_lo);
@@ -1346,10 +1325,13 @@ csattn_status csattn_shard_create(csattn_ctx ctx, csattn_session full, uint64_t 
         s->h.owner = owner ? 1u : 0u;
         s->h.sharded = 1;
         push_dev(s.get());
-        import_tables(s.get(), slens.data(), sidx.data(), ssc.data(), stride);
-        ck(cudaMemcpy(s->tmm.p, tmm.data(), T * sizeof(float2), cudaMemcpyHostToDevice), "tmm");
-        ck(cudaMemcpy(s->live_g.p, gl.data(), T * 4, cudaMemcpyHostToDevice), "live_g");
-        (void)in;
+        // the shard's part of every list, extracted and re-indexed on the device
+        ck(cudaStreamSynchronize(ctx->stream), "shard setup");
+        ck(csa::launch_shard_extract(full->dev.as<csa::SessionDev>(), s->dev.as<csa::SessionDev>(),
+                                     static_cast<uint32_t>(T), static_cast<uint32_t>(key_lo),
+                                     static_cast<uint32_t>(key_hi), ctx->stream),
+           "shard extract launch");
+        ck(cudaStreamSynchronize(ctx->stream), "shard extract");
         *out = s.release();
     });
 }
@@ -1375,7 +1357,8 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
         const uint32_t d = ss[0]->h.d;
         cudaStream_t st = ctx->stream;
         const uint64_t tile = csa::select_tile_keys();
-        if (phase == CSATTN_SHARD_SCAN) {
+        if (phase == CSATTN_SHARD_SCAN || phase == CSATTN_SHARD_RESCAN) {
+            ctx->sh_spec = phase == CSATTN_SHARD_SCAN ? ctx->spec_keep : 0.0;
             uint64_t nq = 0, maxtiles = 0, maxrange = 0;
             ctx->sh_Ks.clear();
             for (uint64_t i = 0; i < ns; ++i) {
@@ -1400,7 +1383,9 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                 mintiles = std::min(mintiles, (khi - ss[i]->h.key_lo + tile - 1) / tile);
             }
             const uint64_t slots = 2ull * static_cast<uint64_t>(ctx->num_sms);
-            uint64_t split = (nq < slots && !ctx->no_split) ? (slots + nq - 1) / nq : 1;
+            // (default 1: the shard phases after the scan walk every part's log;
+            // CSATTN_SHARD_SPLIT=1 enables part units here)
+            uint64_t split = (nq < slots && ctx->shard_split) ? (slots + nq - 1) / nq : 1;
             split = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(split, 16), mintiles));
             ctx->sh_split = static_cast<uint32_t>(split);
             ctx->sh_nq = nq;
@@ -1481,7 +1466,7 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
             ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), grid,
                                   ctx->sh_ulog_idx.as<uint32_t>(), ctx->sh_ulog_sc.as<double>(),
                                   static_cast<uint32_t>(ctx->sh_ucap), nullptr, nullptr, nullptr,
-                                  nullptr, 0.0, static_cast<uint32_t>(split),
+                                  nullptr, ctx->sh_spec, static_cast<uint32_t>(split),
                                   ctx->sh_umeta.as<uint32_t>(), st),
                "select (shard scan) launch");
             ck(csa::launch_shard_hist_sum(ctx->sh_umeta.as<uint32_t>(), static_cast<uint32_t>(nq),
@@ -1503,7 +1488,8 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                                             io->ghist, ctx->sh_umeta.as<uint32_t>(),
                                             ctx->sh_ulog_idx.as<uint32_t>(), ctx->sh_ulog_sc.as<double>(),
                                             static_cast<uint32_t>(ctx->sh_ucap), ctx->sh_split,
-                                            io->bucket, ctx->sh_pstate.p, st),
+                                            io->bucket, ctx->sh_pstate.p, ctx->sh_spec,
+                                            io->spec_fail, st),
                    "shard bucket launch");
                 break;
             case CSATTN_SHARD_MARK:
@@ -1526,7 +1512,7 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                        "n_selected");
                 const uint32_t* ch = ctx->sh_chunks.as<uint32_t>();
                 ck(csa::launch_attend(dprobs, ch + nq + 1, ch, static_cast<uint32_t>(ctx->sh_nchunks),
-                                      ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, st),
+                                      ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, st, true),
                    "attend launch");
                 ctx->launches += 2;
                 break;

@@ -94,7 +94,7 @@ struct DecodeProblem {
     uint32_t mode;     // MODE_* bits
     unsigned long long* prof;  // phase timestamps [cs][8] (CSATTN_PHASE_PROF) or null
     uint32_t tile_lo, tile_hi;  // select tiles of this shard (tile_hi == 0: all)
-    const uint32_t* kdev;       // device-side K (sharded steps: this shard's share) or null
+    const uint32_t* kdev;       // sharded steps: this shard's selection sizes (emit output)
 };
 constexpr uint32_t MODE_SEARCH = 1u;       // route + gather + accumulate
 constexpr uint32_t MODE_STORE_CACHE = 2u;  // persist candidate scores

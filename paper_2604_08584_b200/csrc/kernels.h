@@ -45,7 +45,8 @@ cudaError_t launch_shard_hist_sum(const uint32_t* unit_meta, uint32_t nprob, uin
 cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 const uint32_t* ghist, const uint32_t* unit_meta,
                                 const uint32_t* log_idx, const double* log_sc, uint32_t log_cap,
-                                uint32_t split, void* bucket, void* pstate, cudaStream_t st);
+                                uint32_t split, void* bucket, void* pstate, double spec_keep,
+                                uint32_t* spec_fail, cudaStream_t st);
 cudaError_t launch_shard_mark(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                               const void* pstate, const void* bucket_all, uint32_t nshard,
                               const uint32_t* unit_meta, const uint32_t* log_idx,
@@ -60,7 +61,7 @@ cudaError_t launch_shard_emit(const DecodeProblem* probs, const RoutePlan* plans
 constexpr uint32_t ATT_ROWS = 256;
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
-                          uint32_t* counters, uint32_t d, cudaStream_t st);
+                          uint32_t* counters, uint32_t d, cudaStream_t st, bool partial = false);
 
 cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t nprob, uint32_t d,
                                float* out, cudaStream_t st);
@@ -76,6 +77,8 @@ cudaError_t launch_shard_victim(const InsertProblem* probs, uint32_t nprob,
 //   scores: T x P floats scratch
 cudaError_t launch_build_scores(const SessionDev* s_dev, const SessionDev& s_host, float* scores,
                                 cudaStream_t st);
+cudaError_t launch_shard_extract(const SessionDev* full_dev, const SessionDev* shard_dev,
+                                 uint32_t tables, uint32_t key_lo, uint32_t key_hi, cudaStream_t st);
 cudaError_t launch_build_lists(const SessionDev* s_dev, const SessionDev& s_host,
                                const float* scores, cudaStream_t st);
 

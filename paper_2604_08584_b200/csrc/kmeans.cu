@@ -30,8 +30,11 @@ namespace csa {
 constexpr int KM_THREADS = 512;
 constexpr int KM_MAXKW = KM_MAX_KW;  // k * w floats of centroid state in shared memory
 
+constexpr int KM_CHUNK = 3072;  // seeding-prefix staging (24 KB)
+
 struct KmSmem {
     float cen[KM_MAXKW];
+    double chunk[KM_CHUNK];
     uint32_t wsum[KM_THREADS / 32];
     uint32_t n;
     uint32_t cursor;
@@ -161,21 +164,31 @@ __global__ void __launch_bounds__(KM_THREADS) kmeans_kernel(const KmeansJob* __r
     __syncthreads();
     uint32_t dup = 0;
     for (uint32_t j = 1; j < k; ++j) {
-        for (uint32_t i = tid; i < n; i += blockDim.x) {
-            double dd = 1.0 - best[i];
-            if (dd < 0.0) dd = 0.0;
-            run[i] = __dmul_rn(dd, dd);
-        }
-        __syncthreads();
-        if (tid == 0) {
-            double r = 0.0;
-#pragma unroll 8
-            for (uint32_t i = 0; i < n; ++i) {
-                r = __dadd_rn(r, run[i]);
-                run[i] = r;
+        // seeding weights w_i = max(0, 1 - best_i)^2 and their SEQUENTIAL fp64
+        // prefix (the reference's `total` and inverse-CDF order): chunks are
+        // staged in shared memory by the whole CTA, one thread runs the
+        // dependent add chain (latency of DADD, not of global memory)
+        double r = 0.0;
+        for (uint32_t c0 = 0; c0 < n; c0 += KM_CHUNK) {
+            const uint32_t cn = min(static_cast<uint32_t>(KM_CHUNK), n - c0);
+            for (uint32_t i = tid; i < cn; i += blockDim.x) {
+                double dd = 1.0 - best[c0 + i];
+                if (dd < 0.0) dd = 0.0;
+                S.chunk[i] = __dmul_rn(dd, dd);
             }
-            S.total = r;
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll 8
+                for (uint32_t i = 0; i < cn; ++i) {
+                    r = __dadd_rn(r, S.chunk[i]);
+                    S.chunk[i] = r;
+                }
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < cn; i += blockDim.x) run[c0 + i] = S.chunk[i];
+            __syncthreads();
         }
+        if (tid == 0) S.total = r;
         __syncthreads();
         const double total = S.total;
         if (total > 0.0) {

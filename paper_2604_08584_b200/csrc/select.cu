@@ -616,7 +616,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
         tl = t0 + (nt * j) / split;
         th = t0 + (nt * (j + 1)) / split;
     };
-    const bool speculate = (retry_out != nullptr || split > 1) && !retry_in;
+    const bool speculate = (retry_out != nullptr || unit_meta != nullptr) && !retry_in;
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
     unsigned char* p0 = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
     double* acc = reinterpret_cast<double*>(p0);                    // TILE fp64
@@ -1098,11 +1098,13 @@ shard_bucket_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __
                     const uint32_t* __restrict__ ghist, const uint32_t* __restrict__ unit_meta,
                     const uint32_t* __restrict__ log_idx, const double* __restrict__ log_sc,
                     uint32_t log_cap, uint32_t split, uint4* __restrict__ bucket,
-                    ShardPState* __restrict__ pstate) {
+                    ShardPState* __restrict__ pstate, double spec_keep,
+                    uint32_t* __restrict__ spec_fail) {
     __shared__ SelHdr S;
     const uint32_t tid = threadIdx.x, p = blockIdx.x;
     ProbState st;
-    setup_problem(S, probs, plans, p, st, false, 0.0);
+    // the scan's speculative cut (same hint, same margin) for the verification
+    setup_problem(S, probs, plans, p, st, spec_keep > 0.0, spec_keep);
     const uint32_t* gh = ghist + static_cast<size_t>(p) * (NB + NCB);
     if (tid < 32) {
         uint32_t ab = 0;
@@ -1113,6 +1115,11 @@ shard_bucket_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __
             S.f_bin = b < 0 ? 0u : static_cast<uint32_t>(b);
             S.f_above = ab;
             S.nbkt = 0;
+            // a speculative cut above the global threshold bin lost candidates:
+            // the caller rescans without speculation (every shard sees the same
+            // global histogram, so they agree)
+            if (st.need && st.cut_init && (b < 0 || static_cast<uint32_t>(b) < st.cut_init))
+                atomicOr(spec_fail, 1u);
         }
     }
     cbar();
@@ -1223,6 +1230,9 @@ shard_mark_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __re
     uint32_t total;
     cscan(S, cnt, total);
     if (tid == 0) {
+        // next step's speculative cut: the global threshold bin's lower edge
+        st.hint[0] = st.scale > 0.0 ? st.lo + static_cast<double>(ps.dsel) / st.scale : st.lo;
+        st.hint[1] = (need && !ps.take_all) ? 1.0 : 0.0;
         counts[2 * p] = total;
         counts[2 * p + 1] = (khi > klo ? khi - klo : 0u) - total;  // untaken keys of the range
     }
@@ -1291,6 +1301,8 @@ shard_emit_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __re
     }
     if (tid == 0) {
         kdev[p] = n_local;
+        // attend reads K from the (device) descriptor: this shard's share
+        const_cast<DecodeProblem*>(probs)[p].K = n_local;
         reinterpret_cast<DecodeReport*>(st.rep)->k = K;
     }
 }
@@ -1320,10 +1332,12 @@ cudaError_t launch_shard_hist_sum(const uint32_t* unit_meta, uint32_t nprob, uin
 cudaError_t launch_shard_bucket(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 const uint32_t* ghist, const uint32_t* unit_meta,
                                 const uint32_t* log_idx, const double* log_sc, uint32_t log_cap,
-                                uint32_t split, void* bucket, void* pstate, cudaStream_t st) {
+                                uint32_t split, void* bucket, void* pstate, double spec_keep,
+                                uint32_t* spec_fail, cudaStream_t st) {
     shard_bucket_kernel<<<nprob, SEL_CT, 0, st>>>(probs, plans, ghist, unit_meta, log_idx, log_sc,
                                                    log_cap, split, static_cast<uint4*>(bucket),
-                                                   static_cast<ShardPState*>(pstate));
+                                                   static_cast<ShardPState*>(pstate), spec_keep,
+                                                   spec_fail);
     return cudaGetLastError();
 }
 

@@ -200,6 +200,7 @@ class ShardGroup:
                 "victim": torch.zeros((self.ns, self.vw), dtype=torch.int64, device=dev),
                 "out": torch.empty((nq, d), dtype=torch.float32, device=dev),
                 "nsel": torch.zeros((nq,), dtype=torch.int32, device=dev),
+                "fail": torch.zeros((1,), dtype=torch.int32, device=dev),
             }
             if want_selected:
                 b["sel"] = torch.zeros((nq, k_max), dtype=torch.int32, device=dev)
@@ -209,6 +210,7 @@ class ShardGroup:
             x.counts, x.partial = b["counts"].data_ptr(), b["partial"].data_ptr()
             x.out, x.victim = b["out"].data_ptr(), b["victim"].data_ptr()
             x.n_selected = b["nsel"].data_ptr()
+            x.spec_fail = b["fail"].data_ptr()
             if want_selected:
                 x.selected, x.sel_stride = b["sel"].data_ptr(), k_max
             x.shard_index = self.first + j
@@ -245,9 +247,23 @@ class ShardGroup:
             coll_all_reduce_min_u64([bb[key] for bb in bufs], self.dist)
 
         A = self._abi
+        for bb in bufs:
+            bb["fail"].zero_()
         run(A.SHARD_SCAN)
         all_reduce_sum("ghist")
         run(A.SHARD_BUCKET)
+        # the speculative cut (previous step's threshold) missed on some query
+        # head: every shard saw the same global histogram; rescan without it
+        fail = torch.stack([bb["fail"] for bb in bufs]).max()
+        if self.dist is not None:
+            self.dist.all_reduce(fail, op=self.dist.ReduceOp.MAX)
+        if int(fail.item()):
+            self.rescans = getattr(self, "rescans", 0) + 1
+            for bb in bufs:
+                bb["fail"].zero_()
+            run(A.SHARD_RESCAN)
+            all_reduce_sum("ghist")
+            run(A.SHARD_BUCKET)
         all_gather("bucket", "bucket_all")
         run(A.SHARD_MARK)
         all_gather("counts", "counts_all")

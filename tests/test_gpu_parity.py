@@ -102,6 +102,26 @@ def test_decode_lockstep(ctx, name):
     lockstep(g, r, q, k, v, P, T, group=grp, check_tables_every=10, tol=TOL)
 
 
+MT_CASES = ["default", "no_passthrough", "period4", "backoff", "weights", "gqa4"]
+
+
+@pytest.mark.parametrize("name", MT_CASES)
+def test_decode_lockstep_multitile(ctx, name):
+    """Several 4096-key select tiles per problem: split part units + merge (few
+    problems), the speculative cut from step 2 on, list boundaries across tiles."""
+    case = DECODE_CASES[name]
+    P, T, d = 12288, 12, 64
+    q, k, v = workload(P, T, d, seed=77)
+    widths = cs.uniform_widths(d, 8)
+    ic = cs.IndexConfig(alpha=0.2, centroids=16, seed=1, score_bits=32, **case.get("ic", {}))
+    rc = cs.RetrievalConfig(**case.get("rc", {}))
+    grp = case.get("group", 1)
+    qq = np.concatenate([q[:P]] * grp) if grp > 1 else q[:P]
+    g = cs.prefill(ctx, qq, k[:P], v[:P], widths, ic, rc, group=grp, max_decode_steps=T)
+    r = _checker("ref").prefill(qq, k[:P], v[:P], widths, ic, rc, grp)
+    lockstep(g, r, q, k, v, P, T, group=grp, check_tables_every=6, tol=TOL)
+
+
 def test_c1_config_matches_reference(ctx):
     """BASELINE config 1: one head, d=128, 4K context, 95% sparsity, full defaults."""
     P, T, d = 4096, 16, 128
