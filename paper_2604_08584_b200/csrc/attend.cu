@@ -16,6 +16,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -212,13 +213,13 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
 // partial dots reduced across the warp by a transposed butterfly (9 shuffles
 // for 8 rows: after it, lane l holds the logit of row ((l>>4)&1)*4 +
 // ((l>>3)&1)*2 + ((l>>2)&1)), so exp / max / sum run lane-parallel.
-constexpr int GR = 8;
+// GR rows per group: 8 (96 regs, 5 CTAs/SM) or 4 (<= 64 regs, 8 CTAs/SM)
 __device__ __forceinline__ float4 ld_row4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-template <bool PARTIAL>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
-__global__ void __launch_bounds__(ATT_THREADS)
+template <bool PARTIAL, int GR>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
+__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 6 : 5)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
                  uint32_t* __restrict__ counters) {
@@ -243,8 +244,9 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const float* const vtail = sd.vtail;
     const float4 q4 = ld_row4(P.q + 4 * ln);
     const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
-    // this lane's row slot within a group of 8 after the butterfly
-    const int myrow = ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1);
+    // this lane's row slot within a group after the butterfly
+    const int myrow = GR == 8 ? ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1)
+                              : ((ln >> 4) & 1) * 2 + ((ln >> 3) & 1);
     const bool up16 = ln & 16, up8 = ln & 8, up4 = ln & 4;
 
     float m = -FLT_MAX, s = 0.0f;
@@ -276,39 +278,51 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
 #pragma unroll
         for (int u = 0; u < GR; ++u)
             pd[u] = fmaf(q4.w, kk[u].w, fmaf(q4.z, kk[u].z, fmaf(q4.y, kk[u].y, q4.x * kk[u].x)));
-        // transposed butterfly: 8 -> 4 -> 2 -> 1 partials, then a plain sum
-        float h4[4], h2[2];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const float send = up16 ? pd[t] : pd[t + 4];
-            const float keep = up16 ? pd[t + 4] : pd[t];
-            h4[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const float send = up8 ? h4[t] : h4[t + 2];
-            const float keep = up8 ? h4[t + 2] : h4[t];
-            h2[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
+        // transposed butterfly: GR -> ... -> 1 partials, then a plain sum
         float lg;
-        {
+        if constexpr (GR == 8) {
+            float h4[4], h2[2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float send = up16 ? pd[t] : pd[t + 4];
+                const float keep = up16 ? pd[t + 4] : pd[t];
+                h4[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const float send = up8 ? h4[t] : h4[t + 2];
+                const float keep = up8 ? h4[t + 2] : h4[t];
+                h2[t] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
             const float send = up4 ? h2[0] : h2[1];
             const float keep = up4 ? h2[1] : h2[0];
             lg = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        } else {
+            float h2[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const float send = up16 ? pd[t] : pd[t + 2];
+                const float keep = up16 ? pd[t + 2] : pd[t];
+                h2[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+            const float send = up8 ? h2[0] : h2[1];
+            const float keep = up8 ? h2[1] : h2[0];
+            lg = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            lg += __shfl_xor_sync(0xffffffffu, lg, 4);
         }
         lg += __shfl_xor_sync(0xffffffffu, lg, 2);
         lg += __shfl_xor_sync(0xffffffffu, lg, 1);
         lg *= scale;
         const bool valid = g0 + myrow < nr;
         float gm = valid ? lg : -FLT_MAX;
-        gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 4));
+        if constexpr (GR == 8) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 4));
         gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 8));
         gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 16));
         const float mn = fmaxf(m, gm);
         const float f = expf(m - mn);
         const float pr = valid ? expf(lg - mn) : 0.0f;
-        float ps = pr;  // rows are replicated over lane bits 0-1: sum bits 2-4
-        ps += __shfl_xor_sync(0xffffffffu, ps, 4);
+        float ps = pr;  // rows replicated over the low lane bits: sum the row bits
+        if constexpr (GR == 8) ps += __shfl_xor_sync(0xffffffffu, ps, 4);
         ps += __shfl_xor_sync(0xffffffffu, ps, 8);
         ps += __shfl_xor_sync(0xffffffffu, ps, 16);
         s = s * f + ps;
@@ -316,14 +330,16 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         for (int v = 0; v < VEC; ++v) acc[0][v] *= f;
 #pragma unroll
         for (int u = 0; u < GR; ++u) {
-            const int src = ((u >> 2) & 1) * 16 + ((u >> 1) & 1) * 8 + (u & 1) * 4;
+            const int src = GR == 8 ? ((u >> 2) & 1) * 16 + ((u >> 1) & 1) * 8 + (u & 1) * 4
+                                    : ((u >> 1) & 1) * 16 + (u & 1) * 8;
             const float pu = __shfl_sync(0xffffffffu, pr, src);
             acc[0][0] = fmaf(pu, vv[u].x, acc[0][0]);
             acc[0][1] = fmaf(pu, vv[u].y, acc[0][1]);
             acc[0][2] = fmaf(pu, vv[u].z, acc[0][2]);
             acc[0][3] = fmaf(pu, vv[u].w, acc[0][3]);
         }
-        if (want_w && valid && (ln & 3) == 0) P.weights[r0 + g0 + myrow] = lg;  // normalized later
+        if (want_w && valid && (ln & (GR == 8 ? 3 : 7)) == 0)
+            P.weights[r0 + g0 + myrow] = lg;  // normalized later
         m = mn;
     }
     }
@@ -431,10 +447,13 @@ cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
+    static const int gr = std::getenv("CSATTN_ATT_GR8") ? 8 : 4;  // 4: 75 regs, 6 CTAs/SM
     if (d == 128 && partial) {
-        attend128_kernel<true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+        if (gr == 4) attend128_kernel<true, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+        else attend128_kernel<true, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
     } else if (d == 128) {
-        attend128_kernel<false><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+        if (gr == 4) attend128_kernel<false, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+        else attend128_kernel<false, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
     } else if (d % 4 == 0) {
         if (d <= 128) CSA_ATT(1, 4);
         else if (d <= 256) CSA_ATT(2, 4);
