@@ -389,6 +389,29 @@ class Session:
             pass
 
 
+def decode_batch(sessions, q, new_keys, new_values):
+    """One decode step for a batch of sessions on one context (csattn_decode_batch):
+    q holds sum(group) query rows in session order, new_keys/new_values one row
+    per session. Returns (out [rows, d], selected [rows, max context]); row r's
+    selected set is selected[r, :k] with k = keep_count(keep_ratio, context)."""
+    if not sessions:
+        raise ParameterError("no sessions")
+    ctx = sessions[0].ctx
+    d = sessions[0].info().dim
+    rows = sum(s.group for s in sessions)
+    stride = max(s.context_len for s in sessions)
+    q = _f32(q).reshape(rows, d)
+    nk = _f32(new_keys).reshape(len(sessions), d)
+    nv = _f32(new_values).reshape(len(sessions), d)
+    out = np.zeros((rows, d), np.float32)
+    sel = np.zeros((rows, stride), np.uint32)
+    hs = (C.c_void_p * len(sessions))(*[s.h for s in sessions])
+    _check(lib().csattn_decode_batch(ctx.h, len(sessions), hs, q.ctypes.data, nk.ctypes.data,
+                                     nv.ctypes.data, out.ctypes.data, sel.ctypes.data, stride,
+                                     _abi.HOST_BUFFERS))
+    return out, sel
+
+
 def _widths_arr(widths):
     return (C.c_uint64 * len(widths))(*[int(w) for w in widths])
 

@@ -167,6 +167,17 @@ struct csattn_ctx_s {
     bool sh_scanned = false;
     bool no_split = std::getenv("CSATTN_NO_SPLIT") != nullptr;
     bool shard_split = std::getenv("CSATTN_SHARD_SPLIT") != nullptr;
+    // union attend (attend_union.cu) for problems sharing a prefill: opt-in
+    // with CSATTN_UNION=1 (read every step); CSATTN_UNION_MIN sets the minimum
+    // number of problems on one prefill for it to engage (default 16)
+    uint64_t union_min = std::getenv("CSATTN_UNION_MIN") ? std::strtoull(std::getenv("CSATTN_UNION_MIN"), nullptr, 10) : 16;
+    DevMem un_bnd, un_parts, un_tails;
+    // union-kernel timeline (CSATTN_UNION_PROF=1; diagnostics only): per CTA
+    // [16 items][4 stamps] + [16] tile counts, summarised at teardown
+    bool union_prof = std::getenv("CSATTN_UNION_PROF") != nullptr;
+    DevMem un_prof;
+    double un_sum[4] = {0, 0, 0, 0};
+    uint64_t un_items = 0, un_tiles = 0, un_launches = 0;
     uint64_t log_cap = 0, log_rows = 0;
     int num_sms = 148;
     // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
@@ -530,10 +541,60 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     auto& slot = ctx->ring[ctx->next_slot];
     ctx->next_slot = (ctx->next_slot + 1) % csattn_ctx_s::kSlots;
     if (slot.used) ck(cudaEventSynchronize(slot.done), "descriptor slot");
+    // union attend groups: problems on one prefill, in first-appearance order,
+    // cut into groups of <= UN_GROUP (attend_union.cu)
+    std::vector<uint32_t> ugP, ugmem, umem, umgrp;
+    std::vector<char> in_union(nq, 0);
+    uint32_t u_maxP = 0;
+    const char* uenv = std::getenv("CSATTN_UNION");
+    if (uenv && uenv[0] == '1' && !dw && d == 128) {
+        std::vector<std::pair<const float*, std::vector<uint32_t>>> by_pre;
+        std::vector<uint32_t> prob_sess(nq);
+        qi = 0;
+        for (uint64_t i = 0; i < ns; ++i)
+            for (uint64_t h = 0; h < ss[i]->group; ++h, ++qi) {
+                prob_sess[qi] = static_cast<uint32_t>(i);
+                const float* key = ss[i]->h.kpre;
+                auto it = std::find_if(by_pre.begin(), by_pre.end(),
+                                       [&](const auto& e) { return e.first == key; });
+                if (it == by_pre.end()) {
+                    by_pre.emplace_back(key, std::vector<uint32_t>{});
+                    it = by_pre.end() - 1;
+                }
+                it->second.push_back(static_cast<uint32_t>(qi));
+            }
+        for (auto& [key, list] : by_pre) {
+            if (list.size() < std::max<uint64_t>(ctx->union_min, 1)) continue;
+            const uint64_t ng = (list.size() + csa::UN_GROUP - 1) / csa::UN_GROUP;
+            const uint64_t per = (list.size() + ng - 1) / ng;
+            for (uint64_t g0 = 0; g0 < list.size(); g0 += per) {
+                const uint32_t g = static_cast<uint32_t>(ugP.size());
+                const uint32_t Pg = static_cast<uint32_t>(ss[prob_sess[list[g0]]]->h.P);
+                ugP.push_back(Pg);
+                u_maxP = std::max(u_maxP, Pg);
+                ugmem.resize(ugmem.size() + csa::UN_GROUP, 0xffffffffu);
+                for (uint64_t b = 0; g0 + b < list.size() && b < per; ++b) {
+                    const uint32_t p = list[g0 + b];
+                    ugmem[g * csa::UN_GROUP + b] = static_cast<uint32_t>(umem.size());
+                    umem.push_back(p);
+                    umgrp.push_back(g);
+                    in_union[p] = 1;
+                }
+            }
+        }
+    }
+    const uint64_t ngroups = ugP.size(), nmem = umem.size();
+    const uint32_t u_nrange = (u_maxP + csa::UN_RANGE - 1) / csa::UN_RANGE;
+    if (ngroups) {
+        ctx->un_bnd.ensure(nmem * (u_nrange + 1) * 4);
+        ctx->un_parts.ensure(nmem * u_nrange * csa::UN_PART_WORDS * 4);
+        ctx->un_tails.ensure(nmem * csa::UN_PART_WORDS * 4);
+    }
     // attention work list: ceil(K / ATT_ROWS) chunk-CTAs per problem
     std::vector<uint32_t> cbase(nq + 1), cprob;
     for (uint64_t i = 0; i < nq; ++i) {
         cbase[i] = static_cast<uint32_t>(cprob.size());
+        if (in_union[i]) continue;
         const uint64_t nc = (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
         cprob.insert(cprob.end(), nc, static_cast<uint32_t>(i));
     }
@@ -551,7 +612,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const size_t ioff = al(dbytes);
     const size_t boff = ioff + al(ibytes);
     const size_t poff = boff + al((nq + 1) * 4);
-    const size_t need = poff + nchunks * 4;
+    const size_t uoff = poff + al(nchunks * 4);  // union tables: gP | gmember | members | mgroup
+    const size_t u_gm = uoff + al(ngroups * 4), u_m = u_gm + al(ugmem.size() * 4);
+    const size_t u_mg = u_m + al(nmem * 4);
+    const size_t need = u_mg + nmem * 4;
     if (need > slot.cap) {
         if (slot.host) ck(cudaFreeHost(slot.host), "cudaFreeHost");
         slot.cap = need + need / 2;
@@ -564,6 +628,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
     std::memcpy(hb + boff, cbase.data(), (nq + 1) * 4);
     std::memcpy(hb + poff, cprob.data(), nchunks * 4);
+    if (ngroups) {
+        std::memcpy(hb + uoff, ugP.data(), ngroups * 4);
+        std::memcpy(hb + u_gm, ugmem.data(), ugmem.size() * 4);
+        std::memcpy(hb + u_m, umem.data(), nmem * 4);
+        std::memcpy(hb + u_mg, umgrp.data(), nmem * 4);
+    }
     ck(cudaMemcpyAsync(slot.dev.p, hb, need, cudaMemcpyHostToDevice, ctx->stream),
        "descriptor upload");
     char* db = slot.dev.as<char>();
@@ -645,9 +715,55 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                           0.0, 1, nullptr, ctx->stream),
        "select retry launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
-    ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
-                          ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream),
-       "attend launch");
+    if (nchunks)
+        ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
+                              ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream),
+           "attend launch");
+    if (ngroups) {
+        auto u32 = [&](size_t off) { return reinterpret_cast<const uint32_t*>(db + off); };
+        if (ctx->union_prof) {
+            ctx->un_prof.ensure(static_cast<size_t>(ctx->num_sms) * 160 * 8);
+            ck(cudaMemsetAsync(ctx->un_prof.p, 0, static_cast<size_t>(ctx->num_sms) * 160 * 8, ctx->stream), "memset");
+        }
+        ck(csa::launch_attend_union(dprobs, static_cast<uint32_t>(ngroups), u32(uoff), u32(u_gm),
+                                    u32(u_m), u32(u_mg), static_cast<uint32_t>(nmem), u_nrange,
+                                    ctx->un_bnd.as<uint32_t>(), ctx->un_parts.as<float>(),
+                                    ctx->un_tails.as<float>(), ctx->num_sms,
+                                    ctx->union_prof ? ctx->un_prof.as<unsigned long long>() : nullptr,
+                                    ctx->stream),
+           "union attend launch");
+        ctx->launches += 4;
+        if (ctx->union_prof) {
+            std::vector<unsigned long long> h(static_cast<size_t>(ctx->num_sms) * 160);
+            ck(cudaMemcpyAsync(h.data(), ctx->un_prof.p, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream), "prof");
+            ck(cudaStreamSynchronize(ctx->stream), "prof");
+            unsigned long long t0 = ~0ull, t1 = 0;
+            for (int c = 0; c < ctx->num_sms; ++c)
+                for (int i = 0; i < 16; ++i) {
+                    const unsigned long long* q = &h[static_cast<size_t>(c) * 160 + i * 4];
+                    if (!q[0] || !q[3]) continue;
+                    t0 = std::min(t0, q[0]);
+                    t1 = std::max(t1, q[3]);
+                    ctx->un_sum[0] += double(q[1] - q[0]);
+                    if (q[2]) ctx->un_sum[1] += double(q[2] - q[1]);
+                    ctx->un_sum[2] += double(q[3] - (q[2] ? q[2] : q[1]));
+                    ctx->un_items += 1;
+                    ctx->un_tiles += h[static_cast<size_t>(c) * 160 + 64 + i];
+                }
+            if (t1 > t0) ctx->un_sum[3] += double(t1 - t0);
+            if (ctx->un_launches == 3) {  // CTA 0, first item, per tile: relative to item prologue end
+                const unsigned long long* q = &h[0];
+                const unsigned long long b = q[1];
+                for (int t = 0; t < 10 && q[80 + t * 8 + 4]; ++t) {
+                    const unsigned long long* z = q + 80 + t * 8;
+                    std::fprintf(stderr, "[csattn] tile %d: QK issued %.2f  S seen %.2f  P done %.2f  PV issued %.2f | K stored %.2f  V stored %.2f us\n", t,
+                                 (double)(z[0] - b) / 1e3, (double)(z[1] - b) / 1e3, (double)(z[2] - b) / 1e3,
+                                 (double)(z[3] - b) / 1e3, (double)(z[4] - b) / 1e3, (double)(z[5] - b) / 1e3);
+                }
+            }
+            ctx->un_launches += 1;
+        }
+    }
     if (ctx->profile) ck(cudaEventRecord(ev[2], ctx->stream), "event");
     ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
     ck(cudaEventRecord(slot.done, ctx->stream), "event");
@@ -656,7 +772,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaEventRecord(ev[3], ctx->stream), "event");
         ctx->ev_steps.push_back(ev);
     }
-    ctx->launches += 5;
+    ctx->launches += nchunks ? 5 : 4;
     if (ctx->phase_prof) {
         // per problem: streaming (gather + log) and final-selection time,
         // logged candidates, threshold-bin size; printed at context teardown
@@ -987,6 +1103,16 @@ static void ctx_release(csattn_ctx ctx) {
         std::fprintf(stderr, "[csattn] speculative cut: %llu of %llu problems retried\n",
                      static_cast<unsigned long long>(ctx->phase_retry),
                      static_cast<unsigned long long>(ctx->phase_probs));
+    }
+    if (ctx->un_items) {
+        const double n = static_cast<double>(ctx->un_items);
+        std::fprintf(stderr,
+                     "[csattn] union kernel: %llu launches, %.1f items/launch, %.1f tiles/item; per item "
+                     "prologue=%.2fus tiles=%.2fus epilogue=%.2fus; kernel span %.1fus\n",
+                     static_cast<unsigned long long>(ctx->un_launches), n / ctx->un_launches,
+                     static_cast<double>(ctx->un_tiles) / n, ctx->un_sum[0] / n / 1e3,
+                     ctx->un_sum[1] / n / 1e3, ctx->un_sum[2] / n / 1e3,
+                     ctx->un_sum[3] / ctx->un_launches / 1e3);
     }
     cudaStreamSynchronize(ctx->stream);
     for (auto& ev : ctx->ev_steps)

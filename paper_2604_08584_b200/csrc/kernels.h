@@ -63,6 +63,18 @@ cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial = false);
 
+// attend_union.cu: problems sharing a prefill (groups of <= UN_GROUP
+// members), by prefill row range: each union row is read once per group
+constexpr uint32_t UN_GROUP = 64;
+constexpr uint32_t UN_RANGE = 2048;
+constexpr uint32_t UN_MAX_RANGES = SELECT_MAX_CONTEXT / UN_RANGE;
+constexpr uint32_t UN_PART_WORDS = 132;  // max, sum, 2 pad, acc[128] (16-byte aligned)
+cudaError_t launch_attend_union(const DecodeProblem* probs, uint32_t ngroups, const uint32_t* gP,
+                                const uint32_t* gmember, const uint32_t* members,
+                                const uint32_t* mgroup, uint32_t nmembers, uint32_t nrange,
+                                uint32_t* bnd, float* parts, float* tails, int num_sms,
+                                unsigned long long* tprof, cudaStream_t st);
+
 cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t nprob, uint32_t d,
                                float* out, cudaStream_t st);
 

@@ -1,9 +1,10 @@
 """Per-CUDA-source-line instruction and stall totals from an ncu report.
-usage: python scripts/ncu_lines.py report.ncu-rep [top]"""
+usage: python scripts/ncu_lines.py report.ncu-rep [top] [kernel-regex]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kf = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 res = []

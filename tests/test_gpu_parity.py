@@ -317,3 +317,45 @@ def test_c2_scale_selected_sets(ctx):
     assert tables_equal(g.export_index(), r.export())
     qstep = np.stack([np.stack([x[0][P + t] for x in qs]) for t in range(T)])
     lockstep(g, r, qstep, k, v, P, T, group=4)
+
+
+@pytest.mark.parametrize("ctas", ["", "1"])
+def test_union_attend_fork_batch(ctx, monkeypatch, ctas):
+    """Batch decode of forks that share one prefill (config c3's shape): the
+    union attend path (attend_union.cu, CSATTN_UNION=1) must give every
+    (sequence, head) the same selected set and output as decoding that fork
+    alone. 20 forks x GQA 4 = 80 problems on one prefill -> two union groups of
+    40; a second prefill with 2 forks (8 problems) in the same batch stays on
+    the per-problem path. ctas="1": every work item on one persistent CTA."""
+    monkeypatch.setenv("CSATTN_UNION", "1")
+    if ctas:
+        monkeypatch.setenv("CSATTN_UNION_CTAS", ctas)
+    P, T, d, F = 8192, 5, 128, 20
+    q, k, v = workload(P, 64, d, seed=31)
+    widths = cs.uniform_widths(d, 8)
+    ic = cs.IndexConfig(alpha=0.2, centroids=32, seed=1, score_bits=32)
+    rc = cs.RetrievalConfig()
+    qq = np.concatenate([q[:P]] * 4)
+    base = cs.prefill(ctx, qq, k[:P], v[:P], widths, ic, rc, group=4, max_decode_steps=T)
+    q2, k2, v2 = workload(4096, 8, d, seed=32)
+    base2 = cs.prefill(ctx, np.concatenate([q2[:4096]] * 4), k2[:4096], v2[:4096], widths, ic, rc,
+                       group=4, max_decode_steps=T)
+    batch = [base.fork() for _ in range(F)] + [base2.fork() for _ in range(2)]
+    alone = [base.fork() for _ in range(F)] + [base2.fork() for _ in range(2)]
+    rng = np.random.default_rng(5)
+    worst = 0.0
+    for t in range(T):
+        # fork f queries with prefill rows near its own offset; its own appended rows
+        Q = np.stack([q[(P + 3 * f + t + 8 * h) % (P + 64)] for f in range(F) for h in range(4)] +
+                     [q2[4096 + t]] * 8).astype(np.float32)
+        Q *= (1.0 + 0.1 * rng.standard_normal((len(Q), 1))).astype(np.float32)
+        Kn = np.stack([k[P + (f + t) % 64] for f in range(F)] + [k2[4096 + t]] * 2)
+        Vn = np.stack([v[P + (f + 2 * t) % 64] for f in range(F)] + [v2[4096 + t]] * 2)
+        out, sel = cs.decode_batch(batch, Q, Kn, Vn)
+        for f, s in enumerate(alone):
+            reps = s.decode_step(Q[4 * f:4 * f + 4], Kn[f], Vn[f])
+            for h, r in enumerate(reps):
+                row = 4 * f + h
+                assert np.array_equal(sel[row, :r.k], r.selected), (t, f, h)
+                worst = max(worst, rel_err(out[row], r.output))
+    assert worst < 1e-4, worst
