@@ -1,37 +1,35 @@
 // attend_union.cu — sparse attention for problems that share one prefill
-// (masked dense_attention, core.cpp:118-169), on sm_100a.
+// (masked dense_attention, core.cpp:118-169), on sm_100a tensor cores.
 //
 // The batch-decode case (config c3: 16 sequences forked from one prefill, GQA
 // groups of 4 -> 64 (sequence, head) problems per KV head) selects each prefill
-// row ~6x on average. The per-problem path (attend.cu) gathers a row once per
-// problem that selected it; here a group of <= 64 problems ("members") on one
-// prefill is processed by prefill ROW RANGE, so a row crosses HBM/L2 once per
-// group:
-//   union_bounds_kernel  per member: where each row range starts in its
-//                        (ascending) selected list, and where its appended
-//                        rows (index >= P) start
-//   attend_range_kernel  per (group, range of UN_RANGE prefill rows): the
-//                        members' selected rows in the range are marked in a
-//                        shared-memory bitmask (bit b = member b), the union is
-//                        compacted and streamed through a cp.async double
-//                        buffer; warp w owns members 8w..8w+7 (q and the
-//                        online-softmax state in registers) and runs each
-//                        member over ITS rows of the batch in groups of four
-//                        -> partial (max, sum, acc[128]) per (member, range)
-//   attend_tail_kernel   per member: its appended rows (private to its
-//                        session), one warp -> a partial
-//   union_merge_kernel   per member: log-sum-exp of its range partials in
-//                        range order, then the tail -> output
-// Every problem attends exactly its own selected rows in a fixed order, so the
-// result is deterministic and independent of how problems are grouped.
+// row ~6x on average. The per-problem path (attend.cu) handles every
+// (problem, selected row) pair on CUDA cores. Here a group of <= 64 problems
+// ("members") on one prefill is processed by prefill ROW RANGE as a small dense
+// attention over the UNION of their selected rows, masked per member:
+//   union_build_kernel  per (group, range of UN_RANGE prefill rows): each
+//                       member's selected rows in the range (binary search in
+//                       its ascending list) are marked in a shared-memory
+//                       bitmask (bit b = member b) and compacted -> global
+//                       union list (row offsets, member masks, count)
+//   attend_tc_kernel    persistent, one CTA per SM over the (group, range)
+//                       items: tiles of 64 union rows, S = Q K^T and O += P V
+//                       on tcgen05 (operands in swizzled smem, accumulators in
+//                       TMEM), masked online softmax in between
+//                       -> partial (max, sum, acc[128]) per (member, range)
+//   attend_tail_kernel  per member: its appended rows (index >= P, private to
+//                       its session), one warp -> a partial
+//   union_merge_kernel  per member: log-sum-exp of its range partials in range
+//                       order, then the tail -> output
+// Every problem attends exactly its own selected rows (its mask bit) in a fixed
+// order, so results are deterministic and independent of how problems are
+// grouped.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cfloat>
-#include <cstdint>
-
-#include <cuda_bf16.h>
-
 #include <climits>
+#include <cstdint>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -42,31 +40,99 @@ namespace csa {
 
 constexpr uint32_t UN_PART = UN_PART_WORDS;  // max, sum, 2 pad, acc[128]
 constexpr uint32_t UN_NONE = 0xffffffffu;
+// attend_tc_kernel shared-memory operand offsets (see TcSmem)
+constexpr uint32_t TcSmem_K0 = 0, TcSmem_KSZ = 32768, TcSmem_V0 = 65536, TcSmem_VSZ = 32768;
+constexpr uint32_t TcSmem_QHI = 131072, TcSmem_QLO = 147456, TcSmem_P0 = 163840, TcSmem_PSZ = 16384;
 
-// ---- per member: range starts in its selected list ----
-// bnd[k][r] = lower_bound(sel, r * UN_RANGE) for r < nr = ceil(P / UN_RANGE),
-// bnd[k][nr] = lower_bound(sel, P): the first appended row.
-__global__ void __launch_bounds__(256)
-union_bounds_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ members,
-                    const uint32_t* __restrict__ mgroup, const uint32_t* __restrict__ gP,
-                    uint32_t nrange, uint32_t* __restrict__ bnd) {
-    const uint32_t k = blockIdx.x;
-    const DecodeProblem& Pb = probs[members[k]];
-    const uint32_t* sel = Pb.sel;
-    const uint32_t K = Pb.K, P0 = gP[mgroup[k]];
-    const uint32_t nr = div_up(P0, UN_RANGE);
-    uint32_t* b = bnd + static_cast<size_t>(k) * (nrange + 1);
-    // entry i (i == K: +infinity) starts every boundary e with sel[i-1] < e <= sel[i]
-    for (uint32_t i = threadIdx.x; i <= K; i += blockDim.x) {
-        const long long prev = i ? static_cast<long long>(sel[i - 1]) : -1ll;
-        const long long x = i < K ? static_cast<long long>(sel[i]) : (1ll << 40);
-        for (uint32_t r = prev < 0 ? 0u : min(nr, static_cast<uint32_t>(prev / UN_RANGE) + 1u); r <= nr;
-             ++r) {
-            const long long e = r < nr ? static_cast<long long>(r) * UN_RANGE : P0;
-            if (e > x) break;
-            if (e > prev) b[r] = i;
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t n, uint32_t key) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// ---- union lists: one CTA per (group, range) ----
+constexpr int UB_THREADS = 256;
+__global__ void __launch_bounds__(UB_THREADS)
+union_build_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ members,
+                   const uint32_t* __restrict__ gmember, const uint32_t* __restrict__ gP,
+                   uint32_t nrange, uint16_t* __restrict__ urow, unsigned long long* __restrict__ umask,
+                   uint32_t* __restrict__ ucount) {
+    __shared__ unsigned long long mask[UN_RANGE];
+    __shared__ uint32_t lo_s[64], hi_s[64], wcount[UB_THREADS / 32];
+    __shared__ const uint32_t* sel_s[64];
+    const uint32_t item = blockIdx.x, g = item / nrange, r = item % nrange;
+    const uint32_t tid = threadIdx.x;
+    const int w = tid >> 5, ln = tid & 31;
+    const uint32_t P0 = gP[g], r0 = r * UN_RANGE;
+    if (r0 >= P0) return;
+    const uint32_t r1 = min(P0, r0 + UN_RANGE);
+    for (uint32_t i = tid; i < UN_RANGE; i += UB_THREADS) mask[i] = 0ull;
+    if (tid < 128) {  // member tid >> 1: bound tid & 1
+        const uint32_t b = tid >> 1, kk = gmember[g * UN_GROUP + b];
+        uint32_t v = 0;
+        const uint32_t* sel = nullptr;
+        if (kk != UN_NONE) {
+            const DecodeProblem& Pb = probs[members[kk]];
+            sel = Pb.sel;
+            v = lower_bound_u32(sel, Pb.K, (tid & 1) ? r1 : r0);
+        }
+        if (tid & 1)
+            hi_s[b] = v;
+        else {
+            lo_s[b] = v;
+            sel_s[b] = sel;
         }
     }
+    __syncthreads();
+    // warp w marks members 8w..8w+7 (32-bit halves: native shared atomics)
+    uint32_t* m32 = reinterpret_cast<uint32_t*>(mask) + (w >= 4 ? 1 : 0);
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t b = 8 * w + j;
+        const uint32_t* sel = sel_s[b];
+        if (!sel) continue;
+        const uint32_t bit = 1u << (b & 31);
+        for (uint32_t e = lo_s[b] + ln; e < hi_s[b]; e += 32) atomicOr(m32 + 2 * (__ldg(sel + e) - r0), bit);
+    }
+    __syncthreads();
+    // compaction (thread order = row order)
+    constexpr int PER = UN_RANGE / UB_THREADS;
+    unsigned long long v[PER];
+    uint32_t n = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        v[i] = mask[tid * PER + i];
+        n += v[i] != 0ull;
+    }
+    uint32_t inc = n;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (ln >= o) inc += y;
+    }
+    if (ln == 31) wcount[w] = inc;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < UB_THREADS / 32; ++i) {
+        pre += i < w ? wcount[i] : 0u;
+        tot += wcount[i];
+    }
+    uint32_t pos = pre + inc - n;
+    uint16_t* ur = urow + static_cast<size_t>(item) * UN_RANGE;
+    unsigned long long* um = umask + static_cast<size_t>(item) * UN_RANGE;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+        if (v[i]) {
+            ur[pos] = static_cast<uint16_t>(tid * PER + i);
+            um[pos] = v[i];
+            ++pos;
+        }
+    if (tid == 0) ucount[item] = tot;
 }
 
 __device__ __forceinline__ float4 ld4(const float* p, int ln) {
@@ -139,49 +205,96 @@ __device__ __forceinline__ float4 load_q2(const float* q, int ln) {
 }
 
 // ---- tensor-core union attention: one persistent CTA per SM ----
-// Work item = (group g, prefill range r of UN_RANGE rows); its union rows are
-// processed in tiles of 64 (FlashAttention-4 orientation, member = TMEM lane):
+// Item = (group g, range r); its union rows in tiles of 64, FlashAttention-4
+// orientation (member = TMEM lane):
 //   S[member][row] = Q . K_tile^T   (tcgen05 M = 128: 64 members + padding, N = 64)
-//   P[member][row] = mask ? 2^(S - m_member) : 0     (thread = member)
+//   P[member][row] = mask ? 2^(S - m_member) : 0
 //   O[member][dim] += P . V_tile    (tcgen05 M = 128, N = 128)
-// fp32 operands are split into bf16 hi + lo, each product takes three terms
-// (hi.hi + lo.hi + hi.lo): ~2^-16 relative, fp32-grade. Q is pre-scaled by
-// log2(e)/sqrt(d) (base-2 logits). A member's running max is raised only when
-// a tile exceeds it by more than UN_TAU (lazy rescale of its O row), so
-// P <= 2^UN_TAU. Lanes 64-127 of every MMA read padding (their rows are never
-// used). K, V, P and S are double-buffered; mbarrier rings connect the roles:
-//   warps 0-1   math: softmax of member lane (tid), epilogue
-//   warp 2      MMA issuer (one thread)
-//   warps 3-10  K loaders, warps 11-18 V loaders (global -> regs -> bf16 hi/lo
-//               -> swizzled smem), one tile ahead in registers + L2 prefetch
-constexpr int TC_MATH = 64, TC_LOAD = 256;
-constexpr int TC_THREADS = TC_MATH + 32 + 2 * TC_LOAD;  // 608
-constexpr int TC_KW0 = (TC_MATH + 32) / 32;             // first K-loader warp
+// fp32 operands are split into bf16 hi + lo; each product is three MMAs
+// (hi.hi + lo.hi + hi.lo, ~2^-16 relative: fp32-grade). Consecutive MMAs into
+// one accumulator serialise (~128 cycles each on B200 whatever N is), so S and
+// O each use two accumulators that the MMAs alternate between (summed when
+// read). Q is pre-scaled by log2(e)/sqrt(d): base-2 logits. A member's
+// running max is raised only when a tile exceeds it by more than UN_TAU (lazy
+// rescale of its O row), so P <= 2^UN_TAU. MMA lanes 64-127 read padding.
+// Roles (warps 0-17; warp w runs on SM sub-partition w % 4, which also fixes
+// its TMEM lane quadrant): w % 4 in {0, 1}, w < 16 (8 warps): softmax, member
+// (w & 1) * 32 + lane over tile rows 16 (w >> 2) .. +15; warp 2: QK issuer,
+// warp 6: PV issuer (one thread each: issuing a tcgen05.mma costs ~70 cycles
+// on B200, so at N = 64 / 128 the issue streams, not the tensor core, pace a
+// tile and two streams overlap); warps 3, 7, 11, 15: K loaders; 10, 14, 16,
+// 17: V loaders (global -> regs -> bf16 hi/lo -> swizzled smem).
+// K, V, P and S are double-buffered; mbarrier rings connect the roles.
+constexpr int TC_LOAD = 128;
+constexpr int TC_THREADS = 18 * 32;  // 576
+__device__ __forceinline__ int loader_slot(int w) {  // 0-3 K, 4-7 V, -1 other
+    switch (w) {
+        case 3: return 0;
+        case 7: return 1;
+        case 11: return 2;
+        case 15: return 3;
+        case 10: return 4;
+        case 14: return 5;
+        case 16: return 6;
+        case 17: return 7;
+        default: return -1;
+    }
+}
+// MMA issue with every descriptor a compile-time offset from uniform bases
+template <int B>
+__device__ __forceinline__ void issue_qk(uint32_t sbase, uint32_t tS, uint32_t id_qk) {
+    const uint32_t kb = sbase + TcSmem_K0 + B * TcSmem_KSZ;
+    const uint32_t d0 = tS + B * 128, d1 = d0 + 64;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const uint32_t o = (s >> 2) * 64 * 128 + (s & 3) * 32;
+        const uint64_t qhi = tc::desc_sw128(sbase + TcSmem_QHI + o, 16, 1024);
+        const uint64_t qlo = tc::desc_sw128(sbase + TcSmem_QLO + o, 16, 1024);
+        const uint64_t khi = tc::desc_sw128(kb + o, 16, 1024);
+        const uint64_t klo = tc::desc_sw128(kb + 16384 + o, 16, 1024);
+        // MMA i = 3s + term -> accumulator i & 1 (independent chains)
+        tc::mma_bf16((3 * s) & 1 ? d1 : d0, qhi, khi, id_qk, s > 0);
+        tc::mma_bf16((3 * s + 1) & 1 ? d1 : d0, qlo, khi, id_qk, s > 0 || (3 * s + 1) > 1);
+        tc::mma_bf16((3 * s + 2) & 1 ? d1 : d0, qhi, klo, id_qk, 1);
+    }
+}
+template <int B>
+__device__ __forceinline__ void issue_pv(uint32_t sbase, uint32_t tO, uint32_t id_pv, bool first) {
+    const uint32_t vb = sbase + TcSmem_V0 + B * TcSmem_VSZ;
+    const uint32_t pb = sbase + TcSmem_P0 + B * TcSmem_PSZ;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const uint64_t phi = tc::desc_sw128(pb + s * 32, 16, 1024);
+        const uint64_t plo = tc::desc_sw128(pb + 8192 + s * 32, 16, 1024);
+        const uint64_t vhi = tc::desc_sw128(vb + s * 2048, 8192, 1024);
+        const uint64_t vlo = tc::desc_sw128(vb + 16384 + s * 2048, 8192, 1024);
+        const int i0 = 3 * s;
+        tc::mma_bf16(tO + 128 * (i0 & 1), phi, vhi, id_pv, (!first || i0 > 1) ? 1u : 0u);
+        tc::mma_bf16(tO + 128 * ((i0 + 1) & 1), plo, vhi, id_pv, (!first || i0 + 1 > 1) ? 1u : 0u);
+        tc::mma_bf16(tO + 128 * ((i0 + 2) & 1), phi, vlo, id_pv, 1);
+    }
+}
 constexpr uint32_t TC_TILE = 64;
 constexpr float UN_TAU = 8.0f;
 struct TcSmem {  // 1024-byte aligned operand buffers
-    // K tile (B of QK, K-major, 64 rows x 128 dims): hi | lo, 16 KB each; x2
-    static constexpr uint32_t K0 = 0, KSZ = 32768;
-    // V tile (B of PV, MN-major, 64 rows x 128 dims): hi | lo; x2
-    static constexpr uint32_t V0 = 65536, VSZ = 32768;
-    // Q (A of QK, K-major, 64 member rows x 128 dims): hi | lo
-    static constexpr uint32_t QHI = 131072, QLO = 147456;
-    // P (A of PV, K-major, 64 member rows x 64 tile rows): hi | lo, 8 KB each; x2
-    static constexpr uint32_t P0 = 163840, PSZ = 16384;
-    static constexpr uint32_t MASK = 196608;               // u64[UN_RANGE]: marks, then compacted
-    static constexpr uint32_t CROW = MASK + UN_RANGE * 8;  // u16[UN_RANGE]
-    static constexpr uint32_t MISC = CROW + UN_RANGE * 2;
-    static constexpr uint32_t BYTES = MISC + 1024;
+    static constexpr uint32_t K0 = 0, KSZ = 32768;        // K tile (B of QK, K-major): hi | lo; x2
+    static constexpr uint32_t V0 = 65536, VSZ = 32768;    // V tile (B of PV, MN-major): hi | lo; x2
+    static constexpr uint32_t QHI = 131072, QLO = 147456; // Q (A of QK, K-major, 64 rows)
+    static constexpr uint32_t P0 = 163840, PSZ = 16384;   // P (A of PV, K-major, 64 rows): hi | lo; x2
+    static constexpr uint32_t MISC = 196608;
+    // MMA lanes 64-127 of the last P slot read up to 8 KB past it: keep it in bounds
+    static constexpr uint32_t BYTES = MISC + 8192;
 };
 static_assert(TcSmem::BYTES + 1024 <= 232448, "shared memory budget");
 struct TcMisc {
     uint64_t kfull[2], vfull[2], kempty[2], vempty[2], sfull[2], pfull[2], odone;
     const float* kv[2];
-    uint32_t wcount[TC_THREADS / 32];
     uint32_t nu, tbase;
     uint32_t kidx[64];
+    float hmax[4][64];  // [row quarter][member]
+    float hsum[4][64];
 };
-static_assert(sizeof(TcMisc) <= 1024, "misc");
+static_assert(sizeof(TcMisc) <= 4096, "misc");
 
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
@@ -194,6 +307,7 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(b)) : "memory");
 }
+__device__ __forceinline__ void math_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 // x = hi + lo with hi = bf16(x), lo = bf16(x - hi): 16 significant bits
 __device__ __forceinline__ void split2(float x, float y, uint32_t& hi, uint32_t& lo) {
     const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
@@ -220,32 +334,28 @@ __device__ __forceinline__ void store4_split(uint32_t hi_addr, uint32_t lo_addr,
 
 // K (PASS 0) or V (PASS 1) loader warps: tile t of the item into slot T & 1
 template <int PASS>
-__device__ __forceinline__ void tc_loader(TcMisc& X, uint32_t sbase, const float* src,
-                                          const uint16_t* crow, uint32_t nu, uint32_t ntile,
-                                          uint32_t lt, uint32_t& T, unsigned long long* tstamp) {
+__device__ __forceinline__ void tc_loader(TcMisc& X, uint32_t sbase, const float* src, const uint16_t* urow,
+                                          uint32_t nu, uint32_t ntile, uint32_t lt, uint32_t& T,
+                                          unsigned long long* ts) {
     constexpr int NV = TC_TILE * 32 / TC_LOAD;  // float4 per thread per tile (8)
     constexpr uint32_t PF = 4;                  // L2 prefetch distance (tiles)
     auto prefetch_tile = [&](uint32_t tt) {
         if (lt < TC_TILE && tt < ntile) {
             const uint32_t u = tt * TC_TILE + lt;
-            if (u < nu) prefetch_l2(src + static_cast<size_t>(crow[u]) * 128, 512);
-        }
-    };
-    auto load = [&](uint32_t tt, float4 (&v)[NV]) {
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const uint32_t x = lt + TC_LOAD * i;
-            const uint32_t row = x >> 5, e = x & 31, u = tt * TC_TILE + row;
-            v[i] = (tt < ntile && u < nu)
-                       ? __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(crow[u]) * 128) + e)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (u < nu) prefetch_l2(src + static_cast<size_t>(__ldg(urow + u)) * 128, 512);
         }
     };
     for (uint32_t tt = 0; tt < PF; ++tt) prefetch_tile(tt);
     for (uint32_t t = 0; t < ntile; ++t, ++T) {
         prefetch_tile(t + PF);
         float4 cur[NV];
-        load(t, cur);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const uint32_t x = lt + TC_LOAD * i;
+            const uint32_t row = x >> 5, e = x & 31, u = t * TC_TILE + row;
+            cur[i] = u < nu ? __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(__ldg(urow + u)) * 128) + e)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         const uint32_t b = T & 1u;
         if (T >= 2) tc::mbar_wait(PASS ? &X.vempty[b] : &X.kempty[b], ((T >> 1) - 1) & 1u);
         const uint32_t base = sbase + (PASS ? TcSmem::V0 + b * TcSmem::VSZ : TcSmem::K0 + b * TcSmem::KSZ);
@@ -258,25 +368,25 @@ __device__ __forceinline__ void tc_loader(TcMisc& X, uint32_t sbase, const float
         }
         tc::fence_smem_async();
         mbar_arrive(PASS ? &X.vfull[b] : &X.kfull[b]);
-        if (tstamp && lt == 0 && t < 10) tstamp[t * 8 + 4 + PASS] = gtime();
+        if (ts && lt == 0 && t < 10) ts[t * 8 + 4 + PASS] = gtime();
     }
 }
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ members,
                  const uint32_t* __restrict__ gmember, const uint32_t* __restrict__ gP,
-                 const uint32_t* __restrict__ bnd, uint32_t ngroups, uint32_t nrange,
+                 const uint16_t* __restrict__ urow_all, const unsigned long long* __restrict__ umask_all,
+                 const uint32_t* __restrict__ ucount, uint32_t ngroups, uint32_t nrange,
                  float* __restrict__ parts, unsigned long long* __restrict__ tprof) {
     // tprof (diagnostics, CSATTN_UNION_PROF): per CTA [16 items][4] globaltimer
     // stamps (item start, prologue done, tiles done, item done), [16] tile counts
     extern __shared__ unsigned char smem_raw[];
     unsigned char* sm = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays shared
     TcMisc& X = *reinterpret_cast<TcMisc*>(sm + TcSmem::MISC);
-    unsigned long long* mask = reinterpret_cast<unsigned long long*>(sm + TcSmem::MASK);
-    uint16_t* crow = reinterpret_cast<uint16_t*>(sm + TcSmem::CROW);
     const uint32_t tid = threadIdx.x;
     const int w = tid >> 5, ln = tid & 31;
     const uint32_t sbase = tc::smem_u32(sm);
+    const bool math = (w & 3) < 2 && w < 16;
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&X.kfull[b], TC_LOAD);
@@ -284,16 +394,17 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
             tc::mbar_init(&X.kempty[b], 1);
             tc::mbar_init(&X.vempty[b], 1);
             tc::mbar_init(&X.sfull[b], 1);
-            tc::mbar_init(&X.pfull[b], TC_MATH);
+            tc::mbar_init(&X.pfull[b], 256);
         }
         tc::mbar_init(&X.odone, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (w == 0) tc::tmem_alloc<256>(&X.tbase);
+    if (w == 0) tc::tmem_alloc<512>(&X.tbase);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    const uint32_t tS = X.tbase, tO = X.tbase + 128;  // S[2] (64 cols each) | O (128 cols)
+    // TMEM: S[slot][acc] at 64 (2 slot + acc) | O[acc] at 256 + 128 acc
+    const uint32_t tS = X.tbase, tO = X.tbase + 256;
     const uint32_t id_qk = tc::idesc_bf16(128, TC_TILE, false, false);
     const uint32_t id_pv = tc::idesc_bf16(128, 128, false, true);
     uint32_t T = 0;      // tiles processed by this CTA (ring positions)
@@ -303,49 +414,27 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const uint32_t nitems = ngroups * nrange;
     for (uint32_t item = blockIdx.x; item < nitems; item += gridDim.x) {
         const uint32_t g = item / nrange, r = item % nrange;
-        const uint32_t P0 = gP[g];
-        const uint32_t r0 = r * UN_RANGE;
-        if (r0 >= P0) continue;  // uniform across the CTA
+        if (r * UN_RANGE >= gP[g]) continue;  // uniform across the CTA
+        const uint32_t nu = __ldg(ucount + item);
+        const uint32_t ntile = div_up(nu, TC_TILE);
         const bool rec = tp && tid == 0 && it_no < 16;
         if (rec) tp[it_no * 4] = gtime();
-        // ---- item prologue (all threads): members, marks, compaction, Q ----
-        for (uint32_t i = tid; i < UN_RANGE; i += TC_THREADS) mask[i] = 0ull;
+        const uint16_t* urow = urow_all + static_cast<size_t>(item) * UN_RANGE;
+        const unsigned long long* umask = umask_all + static_cast<size_t>(item) * UN_RANGE;
+        // ---- prologue (all threads): members, Q (pre-scaled, split) -> A operand ----
         if (tid < 64) X.kidx[tid] = gmember[g * UN_GROUP + tid];
         if (tid == 0) {
             const DecodeProblem& Pf = probs[members[gmember[g * UN_GROUP]]];  // member 0 exists
-            X.kv[0] = Pf.s->kpre;
-            X.kv[1] = Pf.s->vpre;
+            X.kv[0] = Pf.s->kpre + static_cast<size_t>(r) * UN_RANGE * 128;
+            X.kv[1] = Pf.s->vpre + static_cast<size_t>(r) * UN_RANGE * 128;
         }
-        __syncthreads();
-        if (w < 8) {  // warp w marks members 8w..8w+7 (32-bit halves: native shared atomics)
-            const uint32_t* selp = nullptr;
-            uint32_t lo = 0, hi = 0;
-            if (ln < 8) {
-                const uint32_t kk = X.kidx[8 * w + ln];
-                if (kk != UN_NONE) {
-                    const uint32_t* b = bnd + static_cast<size_t>(kk) * (nrange + 1);
-                    lo = b[r];
-                    hi = b[r + 1];
-                    selp = probs[members[kk]].sel;
-                }
-            }
-            uint32_t* m32 = reinterpret_cast<uint32_t*>(mask) + (w >= 4 ? 1 : 0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t* sp = reinterpret_cast<const uint32_t*>(
-                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(selp), j));
-                const uint32_t elo = __shfl_sync(0xffffffffu, lo, j), ehi = __shfl_sync(0xffffffffu, hi, j);
-                const uint32_t bit = 1u << ((8 * w + j) & 31);
-                for (uint32_t e = elo + ln; e < ehi; e += 32) atomicOr(m32 + 2 * (__ldg(sp + e) - r0), bit);
-            }
-        }
-        {   // Q (pre-scaled by log2(e)/sqrt(d), split) -> A operand, K-major, 64 rows
+        {
             const float c = static_cast<float>(1.4426950408889634 / sqrt(128.0));
             for (uint32_t x = tid; x < 64 * 32; x += TC_THREADS) {
                 const uint32_t j = x >> 5, e = x & 31;
-                const uint32_t kk = X.kidx[j];
+                const uint32_t kk = gmember[g * UN_GROUP + j];
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (kk != UN_NONE) {
+                if (kk != UN_NONE && ntile) {
                     v = __ldg(reinterpret_cast<const float4*>(probs[members[kk]].q) + e);
                     v.x *= c;
                     v.y *= c;
@@ -356,43 +445,8 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
                 store4_split(sbase + TcSmem::QHI + off, sbase + TcSmem::QLO + off, v);
             }
         }
+        tc::fence_smem_async();
         __syncthreads();
-        {   // in-place compaction (thread order = row order)
-            constexpr int PER = (UN_RANGE + TC_THREADS - 1) / TC_THREADS;
-            unsigned long long v[PER];
-            uint32_t n = 0;
-#pragma unroll
-            for (int i = 0; i < PER; ++i) {
-                v[i] = tid * PER + i < UN_RANGE ? mask[tid * PER + i] : 0ull;
-                n += v[i] != 0ull;
-            }
-            uint32_t inc = n;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (ln >= o) inc += y;
-            }
-            if (ln == 31) X.wcount[w] = inc;
-            __syncthreads();
-            uint32_t pre = 0, tot = 0;
-#pragma unroll
-            for (int i = 0; i < TC_THREADS / 32; ++i) {
-                pre += i < w ? X.wcount[i] : 0u;
-                tot += X.wcount[i];
-            }
-            uint32_t pos = pre + inc - n;
-#pragma unroll
-            for (int i = 0; i < PER; ++i)
-                if (v[i]) {
-                    crow[pos] = static_cast<uint16_t>(tid * PER + i);
-                    mask[pos] = v[i];
-                    ++pos;
-                }
-            if (tid == 0) X.nu = tot;
-            tc::fence_smem_async();  // Q operand
-            __syncthreads();
-        }
-        const uint32_t nu = X.nu;
-        const uint32_t ntile = div_up(nu, TC_TILE);
         if (rec) {
             tp[it_no * 4 + 1] = gtime();
             tp[64 + it_no] = ntile;
@@ -408,99 +462,84 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
             ++it_no;
             continue;
         }
-        const float* kpre = X.kv[0] + static_cast<size_t>(r0) * 128;
-        const float* vpre = X.kv[1] + static_cast<size_t>(r0) * 128;
-        if (w >= TC_KW0) {
+        if (loader_slot(w) >= 0) {
             // ================= loaders =================
-            const uint32_t lw = tid - (TC_MATH + 32);
-            if (lw < TC_LOAD)
-                tc_loader<0>(X, sbase, kpre, crow, nu, ntile, lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
+            const int sl = loader_slot(w);
+            const uint32_t lw = static_cast<uint32_t>(sl & 3) * 32 + ln;
+            if (sl < 4)
+                tc_loader<0>(X, sbase, X.kv[0], urow, nu, ntile, lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
             else
-                tc_loader<1>(X, sbase, vpre, crow, nu, ntile, lw - TC_LOAD, T, (tp && it_no == 0) ? tp + 80 : nullptr);
+                tc_loader<1>(X, sbase, X.kv[1], urow, nu, ntile, lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
         } else if (w == 2) {
-            // ================= MMA issuer =================
-            const uint32_t T0 = T;
-            auto qk = [&](uint32_t t) {  // S[slot] = Q . K^T
-                const uint32_t TT = T0 + t, b = TT & 1u;
-                tc::mbar_wait(&X.kfull[b], (TT >> 1) & 1u);
+            // ================= QK issuer: S[slot] = Q . K^T =================
+            for (uint32_t t = 0; t < ntile; ++t, ++T) {
+                const uint32_t b = T & 1u;
+                if (T >= 2) tc::mbar_wait(&X.pfull[b], ((T >> 1) - 1) & 1u);  // S slot read (tile T-2)
+                tc::mbar_wait(&X.kfull[b], (T >> 1) & 1u);
                 tc::fence_after();
+                if (tp && it_no == 0 && t < 10 && ln == 0) tp[80 + t * 8 + 7] = gtime();
                 if (ln == 0) {
-                    const uint32_t kb = sbase + TcSmem::K0 + b * TcSmem::KSZ;
-#pragma unroll
-                    for (int s = 0; s < 8; ++s) {
-                        const uint32_t o = (s >> 2) * 64 * 128 + (s & 3) * 32;
-                        const uint64_t qhi = tc::desc_sw128(sbase + TcSmem::QHI + o, 16, 1024);
-                        const uint64_t qlo = tc::desc_sw128(sbase + TcSmem::QLO + o, 16, 1024);
-                        const uint64_t khi = tc::desc_sw128(kb + o, 16, 1024);
-                        const uint64_t klo = tc::desc_sw128(kb + 16384 + o, 16, 1024);
-                        tc::mma_bf16(tS + b * 64, qhi, khi, id_qk, s > 0);
-                        tc::mma_bf16(tS + b * 64, qlo, khi, id_qk, 1);
-                        tc::mma_bf16(tS + b * 64, qhi, klo, id_qk, 1);
-                    }
+                    if (b)
+                        issue_qk<1>(sbase, tS, id_qk);
+                    else
+                        issue_qk<0>(sbase, tS, id_qk);
                     tc::commit(&X.sfull[b]);
                     tc::commit(&X.kempty[b]);
                     if (tp && it_no == 0 && t < 10) tp[80 + t * 8 + 0] = gtime();
                 }
                 __syncwarp();
-            };
-            qk(0);
-            if (ntile > 1) qk(1);
-            for (uint32_t t = 0; t < ntile; ++t) {
-                const uint32_t TT = T0 + t, b = TT & 1u;
-                tc::mbar_wait(&X.pfull[b], (TT >> 1) & 1u);
-                tc::mbar_wait(&X.vfull[b], (TT >> 1) & 1u);
+            }
+        } else if (w == 6) {
+            // ================= PV issuer: O += P . V =================
+            for (uint32_t t = 0; t < ntile; ++t, ++T) {
+                const uint32_t b = T & 1u;
+                tc::mbar_wait(&X.pfull[b], (T >> 1) & 1u);
+                tc::mbar_wait(&X.vfull[b], (T >> 1) & 1u);
                 tc::fence_after();
-                if (ln == 0) {  // O += P . V
-                    const uint32_t vb = sbase + TcSmem::V0 + b * TcSmem::VSZ;
-                    const uint32_t pb = sbase + TcSmem::P0 + b * TcSmem::PSZ;
-#pragma unroll
-                    for (int s = 0; s < 4; ++s) {
-                        const uint64_t phi = tc::desc_sw128(pb + s * 32, 16, 1024);
-                        const uint64_t plo = tc::desc_sw128(pb + 8192 + s * 32, 16, 1024);
-                        const uint64_t vhi = tc::desc_sw128(vb + s * 2048, 8192, 1024);
-                        const uint64_t vlo = tc::desc_sw128(vb + 16384 + s * 2048, 8192, 1024);
-                        tc::mma_bf16(tO, phi, vhi, id_pv, (t > 0 || s > 0) ? 1u : 0u);
-                        tc::mma_bf16(tO, plo, vhi, id_pv, 1);
-                        tc::mma_bf16(tO, phi, vlo, id_pv, 1);
-                    }
+                if (tp && it_no == 0 && t < 10 && ln == 0) tp[80 + t * 8 + 6] = gtime();
+                if (ln == 0) {
+                    if (b)
+                        issue_pv<1>(sbase, tO, id_pv, t == 0);
+                    else
+                        issue_pv<0>(sbase, tO, id_pv, t == 0);
                     tc::commit(&X.vempty[b]);  // V and P slots free; O stable up to tile t
-                    if (tp && it_no == 0 && t < 10) tp[80 + t * 8 + 3] = gtime();
                     if (t + 1 == ntile) tc::commit(&X.odone);
+                    if (tp && it_no == 0 && t < 10) tp[80 + t * 8 + 3] = gtime();
                 }
                 __syncwarp();
-                if (t + 2 < ntile) qk(t + 2);
             }
-            T += ntile;
-        } else {
-            // ================= math (thread = member = TMEM lane) =================
-            const uint32_t j = tid;  // member
-            const uint32_t lane_off = (static_cast<uint32_t>(w) * 32u) << 16;
+        } else if (math) {
+            // ================= softmax (math) =================
+            const uint32_t j = (w & 1) * 32 + ln;  // member = TMEM lane
+            const uint32_t qt = w >> 2;            // tile rows 16 qt .. 16 qt + 15
+            const uint32_t lane_off = (static_cast<uint32_t>(w & 3) * 32u) << 16;
             float m = -FLT_MAX, s = 0.0f;
             for (uint32_t t = 0; t < ntile; ++t, ++T) {
-                const uint32_t b = T & 1u, u0 = t * TC_TILE;
-                // selection bits of this member over the tile's rows
-                uint32_t bits0 = 0, bits1 = 0;
-#pragma unroll 8
-                for (int rr = 0; rr < 32; ++rr) {
-                    const uint32_t u = u0 + rr, u2 = u0 + 32 + rr;
-                    bits0 |= (u < nu ? static_cast<uint32_t>(mask[u] >> j) & 1u : 0u) << rr;
-                    bits1 |= (u2 < nu ? static_cast<uint32_t>(mask[u2] >> j) & 1u : 0u) << rr;
+                const uint32_t b = T & 1u;
+                // this member's selection bits over its 16 rows (loads issued before the wait)
+                uint32_t bits = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const uint32_t u = t * TC_TILE + 16 * qt + i;
+                    const unsigned long long mk = u < nu ? __ldg(umask + u) : 0ull;
+                    bits |= static_cast<uint32_t>((mk >> j) & 1ull) << i;
                 }
                 tc::mbar_wait(&X.sfull[b], (T >> 1) & 1u);
                 tc::fence_after();
                 if (tp && it_no == 0 && t < 10 && tid == 0) tp[80 + t * 8 + 1] = gtime();
+                float a[16], a2[16];
+                tc::tmem_ld16(tS + b * 128 + 16 * qt + lane_off, a);
+                tc::tmem_ld16(tS + b * 128 + 64 + 16 * qt + lane_off, a2);
                 float mx = -FLT_MAX;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    float a[32];
-                    tc::tmem_ld32(tS + b * 64 + 32 * h + lane_off, a);
-                    const uint32_t bits = h ? bits1 : bits0;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if ((bits >> i) & 1u) mx = fmaxf(mx, a[i]);
+                for (int i = 0; i < 16; ++i) {
+                    a[i] += a2[i];
+                    if ((bits >> i) & 1u) mx = fmaxf(mx, a[i]);
                 }
-                // lazy rescale of this member's O row and sum; the TMEM accesses
-                // are warp-collective, so a warp rescales together (f = 1 elsewhere)
+                X.hmax[qt][j] = mx;
+                math_sync();
+                mx = fmaxf(fmaxf(X.hmax[0][j], X.hmax[1][j]), fmaxf(X.hmax[2][j], X.hmax[3][j]));
+                // lazy rescale; TMEM accesses are warp-collective (f = 1 elsewhere)
                 const bool up = mx > m + UN_TAU;
                 float f = 1.0f;
                 if (up) {
@@ -513,80 +552,77 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
                     tc::fence_after();
                     float o[32];
 #pragma unroll
-                    for (int c = 0; c < 128; c += 32) {
-                        tc::tmem_ld32(tO + c + lane_off, o);
+                    for (int q = 0; q < 2; ++q) {  // O accumulators 0,1 x columns 32 qt .. +31
+                        const uint32_t col = tO + 128 * q + 32 * qt + lane_off;
+                        tc::tmem_ld32(col, o);
 #pragma unroll
                         for (int i = 0; i < 32; ++i) o[i] *= f;
-                        tc::tmem_st32(tO + c + lane_off, o);
+                        tc::tmem_st32(col, o);
                     }
                 }
-                // P row: 64 tile rows, 8 per 16-byte store (hi and lo)
                 if (T >= 2) tc::mbar_wait(&X.vempty[b], ((T >> 1) - 1) & 1u);  // PV(T-2) read this P slot
                 const uint32_t pb = sbase + TcSmem::P0 + b * TcSmem::PSZ;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    float a[32];
-                    tc::tmem_ld32(tS + b * 64 + 32 * h + lane_off, a);
-                    const uint32_t bits = h ? bits1 : bits0;
+                for (int c = 0; c < 16; c += 8) {
+                    float p[8];
 #pragma unroll
-                    for (int c = 0; c < 32; c += 8) {
-                        float p[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            p[u] = ((bits >> (c + u)) & 1u) ? ex2(a[c + u] - m) : 0.0f;
-                            s += p[u];
-                        }
-                        uint4 hh, ll;
-                        split2(p[0], p[1], hh.x, ll.x);
-                        split2(p[2], p[3], hh.y, ll.y);
-                        split2(p[4], p[5], hh.z, ll.z);
-                        split2(p[6], p[7], hh.w, ll.w);
-                        const uint32_t off = tc::kmaj_off(j, 32 * h + c, 64);
-                        sts128(pb + off, hh);
-                        sts128(pb + 8192 + off, ll);
+                    for (int u = 0; u < 8; ++u) {
+                        p[u] = ((bits >> (c + u)) & 1u) ? ex2(a[c + u] - m) : 0.0f;
+                        s += p[u];
                     }
+                    uint4 hh, ll;
+                    split2(p[0], p[1], hh.x, ll.x);
+                    split2(p[2], p[3], hh.y, ll.y);
+                    split2(p[4], p[5], hh.z, ll.z);
+                    split2(p[6], p[7], hh.w, ll.w);
+                    const uint32_t off = tc::kmaj_off(j, 16 * qt + c, 64);
+                    sts128(pb + off, hh);
+                    sts128(pb + 8192 + off, ll);
                 }
                 tc::fence_smem_async();
                 tc::fence_before();
                 mbar_arrive(&X.pfull[b]);
                 if (tp && it_no == 0 && t < 10 && tid == 0) tp[80 + t * 8 + 2] = gtime();
             }
-            // ---- item epilogue: O row of this member -> partial ----
+            // ---- item epilogue: O row of this member (columns 32 qt ..) -> partial ----
             tc::mbar_wait(&X.odone, items & 1u);
             tc::fence_after();
             if (rec) tp[it_no * 4 + 2] = gtime();
             const uint32_t kk = X.kidx[j];
             float* pp = kk != UN_NONE ? parts + (static_cast<size_t>(kk) * nrange + r) * UN_PART : nullptr;
-            float o[32];
-#pragma unroll
-            for (int c = 0; c < 128; c += 32) {
-                tc::tmem_ld32(tO + c + lane_off, o);
+            {
+                float o[32], o2[32];
+                tc::tmem_ld32(tO + 32 * qt + lane_off, o);
+                tc::tmem_ld32(tO + 128 + 32 * qt + lane_off, o2);
                 if (pp)
 #pragma unroll
                     for (int i = 0; i < 32; i += 4)
-                        *reinterpret_cast<float4*>(pp + 4 + c + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+                        *reinterpret_cast<float4*>(pp + 4 + 32 * qt + i) =
+                            make_float4(o[i] + o2[i], o[i + 1] + o2[i + 1], o[i + 2] + o2[i + 2], o[i + 3] + o2[i + 3]);
             }
-            if (pp) {
-                pp[0] = s > 0.0f ? m : -FLT_MAX;
-                pp[1] = s;
+            X.hsum[qt][j] = s;
+            math_sync();
+            if (pp && qt == 0) {
+                const float st = (s + X.hsum[1][j]) + (X.hsum[2][j] + X.hsum[3][j]);
+                pp[0] = st > 0.0f ? m : -FLT_MAX;
+                pp[1] = st;
             }
         }
         ++items;
         tc::fence_before();
-        __syncthreads();  // item done: marks, rows, Q and O may be rewritten
+        __syncthreads();  // item done: Q, bitmaps and O may be rewritten
         tc::fence_after();
         if (rec) tp[it_no * 4 + 3] = gtime();
         ++it_no;
     }
     tc::fence_before();
     __syncthreads();
-    if (w == 0) tc::tmem_free<256>(X.tbase);
+    if (w == 0) tc::tmem_free<512>(X.tbase);
 }
 
 // ---- appended rows (>= P) of every member: one warp each ----
 __global__ void attend_tail_kernel(const DecodeProblem* __restrict__ probs,
                                    const uint32_t* __restrict__ members, uint32_t n,
-                                   const uint32_t* __restrict__ bnd, uint32_t nrange,
                                    float* __restrict__ tails) {
     const uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int ln = threadIdx.x & 31;
@@ -594,7 +630,7 @@ __global__ void attend_tail_kernel(const DecodeProblem* __restrict__ probs,
     const DecodeProblem& Pb = probs[members[k]];
     const SessionDev& sd = *Pb.s;
     const uint32_t K = Pb.K, P0 = sd.P;
-    const uint32_t first = bnd[static_cast<size_t>(k) * (nrange + 1) + div_up(P0, UN_RANGE)];
+    const uint32_t first = lower_bound_u32(Pb.sel, K, P0);
     const float4 q = load_q2(Pb.q, ln);
     float m = -FLT_MAX, s = 0.0f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -618,70 +654,71 @@ __global__ void attend_tail_kernel(const DecodeProblem* __restrict__ probs,
     reinterpret_cast<float4*>(pp + 4)[ln] = acc;
 }
 
-// ---- per member (one warp): range partials in range order, then the tail ----
+// ---- per member (one CTA of 4 warps): range partials in range order, then the tail ----
 __global__ void __launch_bounds__(128)
 union_merge_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ members,
-                   const uint32_t* __restrict__ mgroup, const uint32_t* __restrict__ gP, uint32_t n,
-                   uint32_t nrange, const float* __restrict__ parts, const float* __restrict__ tails) {
-    __shared__ float wsh[4][UN_MAX_RANGES + 1];
-    const uint32_t k = blockIdx.x * 4 + (threadIdx.x >> 5);
+                   const uint32_t* __restrict__ mgroup, const uint32_t* __restrict__ gP, uint32_t nrange,
+                   const float* __restrict__ parts, const float* __restrict__ tails) {
+    __shared__ float wsh[UN_MAX_RANGES + 1];
+    __shared__ float red[4];
+    __shared__ float4 acc_s[4][32];
+    const uint32_t k = blockIdx.x;
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    if (k >= n) return;
     const DecodeProblem& Pb = probs[members[k]];
     const uint32_t nr = div_up(gP[mgroup[k]], UN_RANGE);
     auto part = [&](uint32_t r) {
         return r < nr ? parts + (static_cast<size_t>(k) * nrange + r) * UN_PART
                       : tails + static_cast<size_t>(k) * UN_PART;
     };
+    // global max over non-empty partials
     float gm = -FLT_MAX;
-    for (uint32_t r = ln; r <= nr; r += 32) {
+    for (uint32_t r = threadIdx.x; r <= nr; r += 128) {
         const float* pp = part(r);
         if (pp[1] > 0.0f) gm = fmaxf(gm, pp[0]);
     }
     for (int o = 16; o; o >>= 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (ln == 0) red[w] = gm;
+    __syncthreads();
+    gm = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    __syncthreads();
     float gs = 0.0f;
-    for (uint32_t r = ln; r <= nr; r += 32) {
+    for (uint32_t r = threadIdx.x; r <= nr; r += 128) {
         const float* pp = part(r);
         const float f = pp[1] > 0.0f ? ex2(pp[0] - gm) : 0.0f;
-        wsh[w][r] = f;
+        wsh[r] = f;
         gs = fmaf(pp[1], f, gs);
     }
     for (int o = 16; o; o >>= 1) gs += __shfl_xor_sync(0xffffffffu, gs, o);
-    __syncwarp();
+    if (ln == 0) red[w] = gs;
+    __syncthreads();
+    gs = (red[0] + red[1]) + (red[2] + red[3]);
+    // warp w accumulates partials r = w, w + 4, ... (fixed order), lanes own 4 dims
     float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t r = 0;
-    for (; r + 4 <= nr + 1; r += 4) {  // 4 partials in flight
-        float4 a[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = reinterpret_cast<const float4*>(part(r + u) + 4)[ln];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const float f = wsh[w][r + u];  // 0 for empty partials (their acc is 0)
-            o4.x = fmaf(f, a[u].x, o4.x);
-            o4.y = fmaf(f, a[u].y, o4.y);
-            o4.z = fmaf(f, a[u].z, o4.z);
-            o4.w = fmaf(f, a[u].w, o4.w);
-        }
-    }
-    for (; r <= nr; ++r) {
-        const float f = wsh[w][r];
+    for (uint32_t r = w; r <= nr; r += 4) {
+        const float f = wsh[r];  // 0 for empty partials (their acc is 0)
         const float4 a = reinterpret_cast<const float4*>(part(r) + 4)[ln];
         o4.x = fmaf(f, a.x, o4.x);
         o4.y = fmaf(f, a.y, o4.y);
         o4.z = fmaf(f, a.z, o4.z);
         o4.w = fmaf(f, a.w, o4.w);
     }
-    const float inv = 1.0f / gs;
-    if (Pb.out)
+    acc_s[w][ln] = o4;
+    __syncthreads();
+    if (w == 0 && Pb.out) {
+        const float4 x0 = acc_s[0][ln], x1 = acc_s[1][ln], x2 = acc_s[2][ln], x3 = acc_s[3][ln];
+        const float inv = 1.0f / gs;
         reinterpret_cast<float4*>(Pb.out)[ln] =
-            make_float4(o4.x * inv, o4.y * inv, o4.z * inv, o4.w * inv);
+            make_float4(((x0.x + x1.x) + (x2.x + x3.x)) * inv, ((x0.y + x1.y) + (x2.y + x3.y)) * inv,
+                        ((x0.z + x1.z) + (x2.z + x3.z)) * inv, ((x0.w + x1.w) + (x2.w + x3.w)) * inv);
+    }
 }
 
 cudaError_t launch_attend_union(const DecodeProblem* probs, uint32_t ngroups, const uint32_t* gP,
                                 const uint32_t* gmember, const uint32_t* members,
                                 const uint32_t* mgroup, uint32_t nmembers, uint32_t nrange,
-                                uint32_t* bnd, float* parts, float* tails, int num_sms,
-                                unsigned long long* tprof, cudaStream_t st) {
+                                uint16_t* urow, unsigned long long* umask, uint32_t* ucount,
+                                float* parts, float* tails, int num_sms, unsigned long long* tprof,
+                                cudaStream_t st) {
     if (nrange > UN_MAX_RANGES) return cudaErrorInvalidValue;
     static bool attr = false;
     const int smem = static_cast<int>(TcSmem::BYTES + 1024);
@@ -691,19 +728,17 @@ cudaError_t launch_attend_union(const DecodeProblem* probs, uint32_t ngroups, co
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    union_bounds_kernel<<<nmembers, 256, 0, st>>>(probs, members, mgroup, gP, nrange, bnd);
     const uint32_t items = ngroups * nrange;
+    union_build_kernel<<<items, UB_THREADS, 0, st>>>(probs, members, gmember, gP, nrange, urow, umask, ucount);
     // CSATTN_UNION_CTAS caps the persistent grid (tests: many items per CTA)
     const char* cenv = std::getenv("CSATTN_UNION_CTAS");
     const uint32_t cap = cenv ? static_cast<uint32_t>(std::atoi(cenv)) : 0u;
     uint32_t grid = items < static_cast<uint32_t>(num_sms) ? items : static_cast<uint32_t>(num_sms);
     if (cap && cap < grid) grid = cap;
-    attend_tc_kernel<<<grid, TC_THREADS, smem, st>>>(
-        probs, members, gmember, gP, bnd, ngroups, nrange, parts, tprof);
-    attend_tail_kernel<<<div_up(nmembers, 8), 256, 0, st>>>(probs, members, nmembers, bnd, nrange,
-                                                            tails);
-    union_merge_kernel<<<div_up(nmembers, 4), 128, 0, st>>>(probs, members, mgroup, gP, nmembers,
-                                                            nrange, parts, tails);
+    attend_tc_kernel<<<grid, TC_THREADS, smem, st>>>(probs, members, gmember, gP, urow, umask, ucount, ngroups,
+                                                     nrange, parts, tprof);
+    attend_tail_kernel<<<div_up(nmembers, 8), 256, 0, st>>>(probs, members, nmembers, tails);
+    union_merge_kernel<<<nmembers, 128, 0, st>>>(probs, members, mgroup, gP, nrange, parts, tails);
     return cudaGetLastError();
 }
 

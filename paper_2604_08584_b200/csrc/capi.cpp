@@ -171,7 +171,7 @@ struct csattn_ctx_s {
     // with CSATTN_UNION=1 (read every step); CSATTN_UNION_MIN sets the minimum
     // number of problems on one prefill for it to engage (default 16)
     uint64_t union_min = std::getenv("CSATTN_UNION_MIN") ? std::strtoull(std::getenv("CSATTN_UNION_MIN"), nullptr, 10) : 16;
-    DevMem un_bnd, un_parts, un_tails;
+    DevMem un_row, un_mask, un_count, un_parts, un_tails;
     // union-kernel timeline (CSATTN_UNION_PROF=1; diagnostics only): per CTA
     // [16 items][4 stamps] + [16] tile counts, summarised at teardown
     bool union_prof = std::getenv("CSATTN_UNION_PROF") != nullptr;
@@ -586,7 +586,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const uint64_t ngroups = ugP.size(), nmem = umem.size();
     const uint32_t u_nrange = (u_maxP + csa::UN_RANGE - 1) / csa::UN_RANGE;
     if (ngroups) {
-        ctx->un_bnd.ensure(nmem * (u_nrange + 1) * 4);
+        ctx->un_row.ensure(ngroups * u_nrange * csa::UN_RANGE * 2);
+        ctx->un_mask.ensure(ngroups * u_nrange * csa::UN_RANGE * 8);
+        ctx->un_count.ensure(ngroups * u_nrange * 4);
         ctx->un_parts.ensure(nmem * u_nrange * csa::UN_PART_WORDS * 4);
         ctx->un_tails.ensure(nmem * csa::UN_PART_WORDS * 4);
     }
@@ -727,7 +729,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
         ck(csa::launch_attend_union(dprobs, static_cast<uint32_t>(ngroups), u32(uoff), u32(u_gm),
                                     u32(u_m), u32(u_mg), static_cast<uint32_t>(nmem), u_nrange,
-                                    ctx->un_bnd.as<uint32_t>(), ctx->un_parts.as<float>(),
+                                    ctx->un_row.as<uint16_t>(), ctx->un_mask.as<unsigned long long>(),
+                                    ctx->un_count.as<uint32_t>(), ctx->un_parts.as<float>(),
                                     ctx->un_tails.as<float>(), ctx->num_sms,
                                     ctx->union_prof ? ctx->un_prof.as<unsigned long long>() : nullptr,
                                     ctx->stream),
@@ -756,9 +759,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                 const unsigned long long b = q[1];
                 for (int t = 0; t < 10 && q[80 + t * 8 + 4]; ++t) {
                     const unsigned long long* z = q + 80 + t * 8;
-                    std::fprintf(stderr, "[csattn] tile %d: QK issued %.2f  S seen %.2f  P done %.2f  PV issued %.2f | K stored %.2f  V stored %.2f us\n", t,
+                    std::fprintf(stderr, "[csattn] tile %d: QK start %.2f issued %.2f  S seen %.2f  P done %.2f  PV start %.2f issued %.2f | K stored %.2f  V stored %.2f us\n", t, (double)(z[7] - b) / 1e3,
                                  (double)(z[0] - b) / 1e3, (double)(z[1] - b) / 1e3, (double)(z[2] - b) / 1e3,
-                                 (double)(z[3] - b) / 1e3, (double)(z[4] - b) / 1e3, (double)(z[5] - b) / 1e3);
+                                 (double)(z[6] - b) / 1e3, (double)(z[3] - b) / 1e3, (double)(z[4] - b) / 1e3,
+                                 (double)(z[5] - b) / 1e3);
                 }
             }
             ctx->un_launches += 1;

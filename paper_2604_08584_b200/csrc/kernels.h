@@ -72,8 +72,9 @@ constexpr uint32_t UN_PART_WORDS = 132;  // max, sum, 2 pad, acc[128] (16-byte a
 cudaError_t launch_attend_union(const DecodeProblem* probs, uint32_t ngroups, const uint32_t* gP,
                                 const uint32_t* gmember, const uint32_t* members,
                                 const uint32_t* mgroup, uint32_t nmembers, uint32_t nrange,
-                                uint32_t* bnd, float* parts, float* tails, int num_sms,
-                                unsigned long long* tprof, cudaStream_t st);
+                                uint16_t* urow, unsigned long long* umask, uint32_t* ucount,
+                                float* parts, float* tails, int num_sms, unsigned long long* tprof,
+                                cudaStream_t st);
 
 cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t nprob, uint32_t d,
                                float* out, cudaStream_t st);

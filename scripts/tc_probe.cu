@@ -104,9 +104,21 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int n, int kind, unsigned lon
             else if (kind == 1)
                 tc::mma_bf16(tbase + 128, tc::desc_sw128(b + (it & 3) * 32, 16, 1024),
                              tc::desc_sw128(b + 32768 + (it & 3) * 2048, 8192, 1024), idp, 1);
-            else
+            else if (kind == 2)
                 tc::mma_bf16(tbase, tc::desc_sw128(b + (it & 3) * 32, 16, 1024),
                              tc::desc_sw128(b + 16384 + (it & 3) * 32, 16, 1024), idm, 1);
+            else if (kind == 3)  // QK shape, 2 alternating accumulators
+                tc::mma_bf16(tbase + 64 * (it & 1), tc::desc_sw128(b + (it & 3) * 32, 16, 1024),
+                             tc::desc_sw128(b + 32768 + (it & 3) * 32, 16, 1024), idq, 1);
+            else if (kind == 4)  // QK shape, 4 alternating accumulators
+                tc::mma_bf16(tbase + 64 * (it & 3), tc::desc_sw128(b + (it & 3) * 32, 16, 1024),
+                             tc::desc_sw128(b + 32768 + (it & 3) * 32, 16, 1024), idq, 1);
+            else if (kind == 5)  // PV shape, 2 alternating accumulators
+                tc::mma_bf16(tbase + 128 * (it & 1), tc::desc_sw128(b + (it & 3) * 32, 16, 1024),
+                             tc::desc_sw128(b + 32768 + (it & 3) * 2048, 8192, 1024), idp, 1);
+            else  // QK shape, A operand in no-swizzle... same as 0 but enable=0 each time (no accumulate)
+                tc::mma_bf16(tbase, tc::desc_sw128(b + (it & 3) * 32, 16, 1024),
+                             tc::desc_sw128(b + 32768 + (it & 3) * 32, 16, 1024), idq, 0);
         }
         tc::commit(&bar);
         tc::mbar_wait(&bar, 0);
@@ -168,16 +180,17 @@ int main() {
         }
     printf("max |S err| %.3g  max |O err| %.3g  %s\n", es, eo, (es < 1e-3 && eo < 1e-3) ? "OK" : "FAIL");
     unsigned long long* dc;
-    cudaMalloc(&dc, 32);
+    cudaMalloc(&dc, 64);
     cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-    const char* names[3] = {"QK  M128 N64  K16 (A,B K-major)", "PV  M128 N128 K16 (B MN-major)", "ref M128 N256 K16 (K-major)"};
-    for (int kind = 0; kind < 3; ++kind) {
+    const char* names[7] = {"QK  M128 N64  K16 (A,B K-major)", "PV  M128 N128 K16 (B MN-major)", "ref M128 N256 K16 (K-major)",
+                            "QK  2 accumulators", "QK  4 accumulators", "PV  2 accumulators", "QK  no accumulate"};
+    for (int kind = 0; kind < 7; ++kind) {
         const int n = 4096;
         mma_rate<<<1, 128, 65536>>>(n, kind, dc);
-        unsigned long long c[3] = {0, 0, 0};
+        unsigned long long c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         cudaDeviceSynchronize();
-        cudaMemcpy(c, dc, 24, cudaMemcpyDeviceToHost);
-        const int N = kind == 0 ? 64 : kind == 1 ? 128 : 256;
+        cudaMemcpy(c, dc, 64, cudaMemcpyDeviceToHost);
+        const int N = (kind == 1 || kind == 5) ? 128 : kind == 2 ? 256 : 64;
         printf("%s: %.1f cycles/MMA (pacing-law floor %d)\n", names[kind], (double)c[kind] / n, 128 * N / 256);
     }
     return 0;
