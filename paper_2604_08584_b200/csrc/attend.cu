@@ -23,6 +23,12 @@
 
 namespace csa {
 
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 constexpr int ATT_THREADS = 128;
 constexpr int ATT_WARPS = ATT_THREADS / 32;
 constexpr int ATT_U = 4;
@@ -242,8 +248,17 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const float* const vpre = sd.vpre;
     const float* const ktail = sd.ktail;
     const float* const vtail = sd.vtail;
-    const float4 q4 = ld_row4(P.q + 4 * ln);
-    const float scale = static_cast<float>(1.0 / sqrt(static_cast<double>(d)));
+    // base-2 logits: q pre-scaled by log2(e)/sqrt(d), exp2 = one MUFU op;
+    // partials leave the kernel in natural-log units (x ln 2)
+    float4 q4 = ld_row4(P.q + 4 * ln);
+    {
+        const float c2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(d)));
+        q4.x *= c2;
+        q4.y *= c2;
+        q4.z *= c2;
+        q4.w *= c2;
+    }
+    constexpr float LN2 = 0.6931471805599453f;
     // this lane's row slot within a group after the butterfly
     const int myrow = GR == 8 ? ((ln >> 4) & 1) * 4 + ((ln >> 3) & 1) * 2 + ((ln >> 2) & 1)
                               : ((ln >> 4) & 1) * 2 + ((ln >> 3) & 1);
@@ -312,22 +327,24 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         }
         lg += __shfl_xor_sync(0xffffffffu, lg, 2);
         lg += __shfl_xor_sync(0xffffffffu, lg, 1);
-        lg *= scale;
         const bool valid = g0 + myrow < nr;
         float gm = valid ? lg : -FLT_MAX;
         if constexpr (GR == 8) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 4));
         gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 8));
         gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 16));
-        const float mn = fmaxf(m, gm);
-        const float f = expf(m - mn);
-        const float pr = valid ? expf(lg - mn) : 0.0f;
+        if (gm > m) {  // warp-uniform: rescale only when the running max grows
+            const float f = ex2f(m - gm);
+            s *= f;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[0][v] *= f;
+            m = gm;
+        }
+        const float pr = valid ? ex2f(lg - m) : 0.0f;
         float ps = pr;  // rows replicated over the low lane bits: sum the row bits
         if constexpr (GR == 8) ps += __shfl_xor_sync(0xffffffffu, ps, 4);
         ps += __shfl_xor_sync(0xffffffffu, ps, 8);
         ps += __shfl_xor_sync(0xffffffffu, ps, 16);
-        s = s * f + ps;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[0][v] *= f;
+        s += ps;
 #pragma unroll
         for (int u = 0; u < GR; ++u) {
             const int src = GR == 8 ? ((u >> 2) & 1) * 16 + ((u >> 1) & 1) * 8 + (u & 1) * 4
@@ -339,8 +356,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
             acc[0][3] = fmaf(pu, vv[u].w, acc[0][3]);
         }
         if (want_w && valid && (ln & (GR == 8 ? 3 : 7)) == 0)
-            P.weights[r0 + g0 + myrow] = lg;  // normalized later
-        m = mn;
+            P.weights[r0 + g0 + myrow] = lg * LN2;  // natural-log logit, normalized later
     }
     }
     // ---- CTA partial ----
@@ -360,14 +376,14 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     if (threadIdx.x == 0) {
         float S = 0.0f;
         for (int i = 0; i < ATT_WARPS; ++i)
-            if (ws[i] > 0.0f) S += ws[i] * expf(wm[i] - M);
-        pp[0] = M;
+            if (ws[i] > 0.0f) S += ws[i] * ex2f(wm[i] - M);
+        pp[0] = M * LN2;  // natural-log units for the chunk / shard merges
         pp[1] = S;
     }
     for (uint32_t t = threadIdx.x; t < d; t += blockDim.x) {
         float a = 0.0f;
         for (int i = 0; i < ATT_WARPS; ++i)
-            if (ws[i] > 0.0f) a += wacc[i][t] * expf(wm[i] - M);
+            if (ws[i] > 0.0f) a += wacc[i][t] * ex2f(wm[i] - M);
         pp[2 + t] = a;
     }
     // ---- last CTA of the problem merges all partials in chunk order ----
