@@ -273,6 +273,55 @@ csattn_status csattn_dense_attention(csattn_session s, const float* q, const uin
                                      uint64_t n_mask, float* out, float* weights,
                                      uint32_t flags);
 
+/* ---- CSAT v1 index image (index.hpp:98-121) ----
+ * Little-endian image written by serialize_index (index.cpp:289-318) and
+ * validated by deserialize_index (:320-396): "CSAT" | version u16 | flags u16 |
+ * m u32 | C u32 | L u32 | d u32 | prefill u64 | widths u32 x m | centroid rows |
+ * per table: len u32, indices u32 x len, scores x len. Flag bit 0 stores
+ * scores AND centroid elements as IEEE half (RNE), bit 1 marks normalized keys.
+ * The codec below is host-only (no GPU needed); the session calls run the
+ * table ordering and byte writing on the device. */
+#define CSATTN_CSAT_MAX_SUBSPACES 32
+typedef struct csattn_csat_header {
+    uint64_t m, centroids, list_capacity, dim, prefill_len;
+    int32_t score_bits;     /* 16 or 32 */
+    int32_t normalize_keys; /* 0 / 1 */
+    uint64_t widths[CSATTN_CSAT_MAX_SUBSPACES];
+} csattn_csat_header;
+
+/* f32_to_f16 / f16_to_f32 (util.cpp:8-74) */
+uint16_t csattn_f32_to_f16(float value);
+float csattn_f16_to_f32(uint16_t bits);
+/* The header of an image (errors as deserialize_index through the widths). */
+csattn_status csattn_csat_read_header(const uint8_t* bytes, uint64_t n, csattn_csat_header* header);
+/* index_footprint (index.cpp:419-431): header (incl. widths and length
+ * prefixes), centroid and entry bytes for the given list lengths. */
+csattn_status csattn_csat_footprint(const csattn_csat_header* header, const uint32_t* lens,
+                                    uint64_t* header_bytes, uint64_t* centroid_bytes,
+                                    uint64_t* entry_bytes);
+/* serialize_index over host tables in TopList order (lists of `stride`).
+ * out == NULL: *size = bytes needed. */
+csattn_status csattn_csat_encode(const csattn_csat_header* header, const float* centroids,
+                                 const uint32_t* lens, const uint32_t* indices, const float* scores,
+                                 uint64_t stride, uint8_t* out, uint64_t capacity, uint64_t* size);
+/* deserialize_index: same check order, error classes and messages. Tables
+ * land at `stride` >= list_capacity; centroids hold C x d floats. */
+csattn_status csattn_csat_decode(const uint8_t* bytes, uint64_t n, csattn_csat_header* header,
+                                 float* centroids, uint32_t* lens, uint32_t* indices,
+                                 float* scores, uint64_t stride);
+/* The session's current index (tables after any streaming inserts) as a CSAT
+ * image: tables sorted into TopList order and encoded on the device, header
+ * and centroids prepended on the host. out == NULL: *size = bytes needed. */
+csattn_status csattn_session_serialize(csattn_session s, uint8_t* out, uint64_t capacity,
+                                       uint64_t* size);
+/* A session from a CSAT image plus the prefill KV rows it indexes
+ * (load_index + KvStore + Session, session.hpp:19-31); n_rows must equal the
+ * image's prefill length. */
+csattn_status csattn_session_deserialize(csattn_ctx ctx, const uint8_t* bytes, uint64_t n,
+                                         const float* keys, const float* values, uint64_t n_rows,
+                                         const csattn_retrieval_config* rcfg, uint64_t group,
+                                         uint64_t max_decode_steps, csattn_session* out);
+
 /* ---- sequence sharding ----
  * A logical session (one KV head, P prefill keys) is split by key range over
  * shards. Shard s holds keys [key_lo, key_hi) of every global TopList (global

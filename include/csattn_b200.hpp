@@ -39,6 +39,7 @@
 #include <optional>
 #include <span>
 #include <stdexcept>
+#include <fstream>
 #include <string>
 #include <utility>
 #include <vector>
@@ -392,6 +393,16 @@ class Session {
         return ix;
     }
 
+    // CSAT v1 image of the current tables (serialize_index, index.cpp:289-318),
+    // ordered and encoded on the device
+    std::vector<std::uint8_t> serialize() const {
+        uint64_t n = 0;
+        check(csattn_session_serialize(h_, nullptr, 0, &n));
+        std::vector<std::uint8_t> out(n);
+        check(csattn_session_serialize(h_, out.data(), out.size(), &n));
+        return out;
+    }
+
     // KvStore rows [first, first + count) (core.hpp:47-68)
     void read_kv(std::size_t first, std::size_t count, std::vector<float>& keys,
                  std::vector<float>& values) const {
@@ -446,6 +457,140 @@ class Session {
     mutable std::vector<float> centroids_;
     std::size_t dim_ = 0;
 };
+
+// ---- index.hpp:98-121: the CSAT v1 image of a host CsIndex ----
+struct IndexFootprint {
+    std::size_t header_bytes = 0;
+    std::size_t centroid_bytes = 0;
+    std::size_t entry_bytes = 0;
+    std::size_t payload() const { return centroid_bytes + entry_bytes; }
+    std::size_t total() const { return header_bytes + payload(); }
+};
+
+namespace detail {
+inline csattn_csat_header csat_header_of(const CsIndex& ix) {
+    csattn_csat_header h{};
+    h.m = ix.subspaces();
+    h.centroids = ix.centroids_per_subspace();
+    h.list_capacity = ix.list_capacity;
+    h.dim = ix.layout.dim();
+    h.prefill_len = ix.prefill_len;
+    h.score_bits = ix.score_bits == 16 ? 16 : 32;
+    h.normalize_keys = ix.normalize_keys ? 1 : 0;
+    if (h.m > CSATTN_CSAT_MAX_SUBSPACES) throw ParameterError("too many subspaces for a CSAT image");
+    for (std::size_t b = 0; b < h.m; ++b) h.widths[b] = ix.layout.sizes[b];
+    return h;
+}
+struct FlatTables {
+    std::vector<float> cent, sc;
+    std::vector<std::uint32_t> lens, idx;
+    std::size_t stride = 1;
+};
+inline FlatTables flatten(const CsIndex& ix) {
+    FlatTables f;
+    for (const TopList& l : ix.tables) f.stride = std::max(f.stride, l.indices.size());
+    for (const CentroidSet& cs : ix.centroid_sets) f.cent.insert(f.cent.end(), cs.centroids.begin(), cs.centroids.end());
+    f.lens.resize(ix.tables.size());
+    f.idx.assign(ix.tables.size() * f.stride, 0);
+    f.sc.assign(ix.tables.size() * f.stride, 0.0f);
+    for (std::size_t t = 0; t < ix.tables.size(); ++t) {
+        const TopList& l = ix.tables[t];
+        f.lens[t] = static_cast<std::uint32_t>(l.indices.size());
+        std::copy(l.indices.begin(), l.indices.end(), f.idx.begin() + t * f.stride);
+        std::copy(l.scores.begin(), l.scores.end(), f.sc.begin() + t * f.stride);
+    }
+    return f;
+}
+}  // namespace detail
+
+inline std::vector<std::uint8_t> serialize_index(const CsIndex& index) {
+    const csattn_csat_header h = detail::csat_header_of(index);
+    const detail::FlatTables f = detail::flatten(index);
+    uint64_t n = 0;
+    check(csattn_csat_encode(&h, f.cent.data(), f.lens.data(), f.idx.data(), f.sc.data(), f.stride, nullptr, 0, &n));
+    std::vector<std::uint8_t> out(n);
+    check(csattn_csat_encode(&h, f.cent.data(), f.lens.data(), f.idx.data(), f.sc.data(), f.stride, out.data(),
+                             out.size(), &n));
+    return out;
+}
+
+inline CsIndex deserialize_index(std::span<const std::uint8_t> bytes) {
+    csattn_csat_header h{};
+    check(csattn_csat_read_header(bytes.data(), bytes.size(), &h));
+    const std::size_t T = h.m * h.centroids, L = h.list_capacity;
+    std::vector<float> cent(h.centroids * h.dim), sc(T * L);
+    std::vector<std::uint32_t> lens(T), idx(T * L);
+    check(csattn_csat_decode(bytes.data(), bytes.size(), &h, cent.data(), lens.data(), idx.data(), sc.data(), L));
+    CsIndex ix(SubspaceLayout(std::vector<std::size_t>(h.widths, h.widths + h.m)));
+    ix.alpha = static_cast<double>(L) / static_cast<double>(h.prefill_len);
+    ix.list_capacity = static_cast<std::uint32_t>(L);
+    ix.prefill_len = h.prefill_len;
+    ix.normalize_keys = h.normalize_keys != 0;
+    ix.score_bits = h.score_bits;
+    const float* src = cent.data();
+    for (std::size_t b = 0; b < h.m; ++b) {
+        CentroidSet cs;
+        cs.subspace_id = b;
+        cs.count = h.centroids;
+        cs.dim = h.widths[b];
+        cs.centroids.assign(src, src + cs.count * cs.dim);
+        src += cs.count * cs.dim;
+        ix.centroid_sets.push_back(std::move(cs));
+    }
+    for (std::size_t t = 0; t < T; ++t) {
+        TopList l;
+        l.capacity = static_cast<std::uint32_t>(L);
+        l.indices.assign(idx.begin() + t * L, idx.begin() + t * L + lens[t]);
+        l.scores.assign(sc.begin() + t * L, sc.begin() + t * L + lens[t]);
+        ix.tables.push_back(std::move(l));
+    }
+    return ix;
+}
+
+inline void save_index(const CsIndex& index, const std::string& path) {
+    const auto bytes = serialize_index(index);
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw DataError("cannot open for writing: " + path);
+    out.write(reinterpret_cast<const char*>(bytes.data()), static_cast<std::streamsize>(bytes.size()));
+    if (!out) throw DataError("short write to " + path);
+}
+
+inline CsIndex load_index(const std::string& path) {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) throw DataError("cannot open: " + path);
+    const std::streamsize size = in.tellg();
+    in.seekg(0);
+    std::vector<std::uint8_t> bytes(static_cast<std::size_t>(size));
+    in.read(reinterpret_cast<char*>(bytes.data()), size);
+    if (!in) throw DataError("short read from " + path);
+    return deserialize_index(bytes);
+}
+
+inline IndexFootprint index_footprint(const CsIndex& index) {
+    const csattn_csat_header h = detail::csat_header_of(index);
+    std::vector<std::uint32_t> lens(index.tables.size());
+    for (std::size_t t = 0; t < lens.size(); ++t) lens[t] = static_cast<std::uint32_t>(index.tables[t].indices.size());
+    uint64_t a = 0, b = 0, c = 0;
+    check(csattn_csat_footprint(&h, lens.data(), &a, &b, &c));
+    return IndexFootprint{a, b, c};
+}
+
+// A device session from a CSAT image and the prefill rows it indexes
+// (load_index + KvStore + Session, session.hpp:19-31).
+inline Session load_session(std::span<const std::uint8_t> bytes, std::span<const float> keys,
+                            std::span<const float> values, const RetrievalConfig& cfg,
+                            std::size_t max_decode_steps = 4096, std::size_t group = 1,
+                            Context& ctx = Context::default_context()) {
+    csattn_csat_header h{};
+    check(csattn_csat_read_header(bytes.data(), bytes.size(), &h));
+    SubspaceLayout layout(std::vector<std::size_t>(h.widths, h.widths + h.m));
+    const csattn_retrieval_config rc = cfg.c();
+    csattn_session s = nullptr;
+    check(csattn_session_deserialize(ctx.handle(), bytes.data(), bytes.size(), keys.data(), values.data(),
+                                     keys.size() / std::max<std::size_t>(h.dim, 1), &rc, group,
+                                     max_decode_steps, &s));
+    return Session(s, layout, cfg);
+}
 
 // ---- session.hpp:44-66 ----
 // prefill (session.cpp:25-44): KvStore + build_index on the GPU. `group`

@@ -62,6 +62,16 @@ def ref_lib():
         L.csref_bench.argtypes = [P(vp), u64, vp, vp, vp, u64, u64, P(C.c_double)]
         L.csref_dense_attention.argtypes = [vp, vp, vp, u64, u64, vp, u64, vp, vp]
         L.csref_dense_topk.argtypes = [vp, vp, u64, u64, u64, vp]
+        L.csref_f32_to_f16.restype = C.c_uint16
+        L.csref_f32_to_f16.argtypes = [C.c_float]
+        L.csref_f16_to_f32.restype = C.c_float
+        L.csref_f16_to_f32.argtypes = [C.c_uint16]
+        L.csref_encode.argtypes = [vp, u64, vp, vp, vp, u64, u64, u64, C.c_int32, C.c_int32, vp, u64,
+                                   vp, u64, P(u64)]
+        L.csref_serialize.argtypes = [vp, C.c_int32, vp, u64, P(u64)]
+        L.csref_roundtrip.argtypes = [vp, u64, vp, u64, P(u64)]
+        L.csref_footprint.argtypes = [vp, u64, P(u64), P(u64), P(u64)]
+        L.csref_load.argtypes = [vp, u64, vp, vp, u64, vp, u64, P(vp)]
         _ref = L
     return _ref
 
@@ -182,6 +192,25 @@ class RefSession(_Base):
                                             C.byref(h))
         cls._chk(st)
         return cls._wrap(h, d, group)
+
+    @classmethod
+    def load(cls, data, keys, values, d, rcfg, group=1):
+        """load_index (deserialize_index) + KvStore + Session over the image."""
+        a = np.frombuffer(bytes(data), np.uint8)
+        k, v = _f32(keys), _f32(values)
+        rc, w = rcfg.c()
+        h = C.c_void_p()
+        cls._chk(ref_lib().csref_load(a.ctypes.data, a.size, k.ctypes.data, v.ctypes.data, d,
+                                      C.byref(rc), group, C.byref(h)))
+        return cls._wrap(h, d, group)
+
+    def serialize(self, score_bits=32):
+        """serialize_index of the current index at the given score width."""
+        n = C.c_uint64()
+        self._chk(ref_lib().csref_serialize(self.h, score_bits, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        self._chk(ref_lib().csref_serialize(self.h, score_bits, buf, n.value, C.byref(n)))
+        return bytes(buf)
 
     @classmethod
     def from_index(cls, cent, lens, idx, sc, L, alpha, keys, values, widths, rcfg, group=1,

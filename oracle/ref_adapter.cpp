@@ -409,6 +409,111 @@ int csref_bench(void** hs, uint64_t n, const float* q, const float* k, const flo
 }
 
 // Dense oracle helpers (core.cpp:118-192) on an arbitrary store.
+// ---- CSAT v1 (serialize_index / deserialize_index, index.cpp:289-396) ----
+
+uint16_t csref_f32_to_f16(float x) { return R::f32_to_f16(x); }
+float csref_f16_to_f32(uint16_t h) { return R::f16_to_f32(h); }
+
+namespace {
+R::CsIndex index_of(const float* cent, uint64_t c, const uint32_t* lens, const uint32_t* idx,
+                    const float* scores, uint64_t stride, uint64_t L, uint64_t prefill,
+                    int32_t normalize_keys, int32_t score_bits, const uint64_t* widths, uint64_t m) {
+    R::CsIndex ix(layout_of(widths, m));
+    const float* src = cent;
+    for (uint64_t b = 0; b < m; ++b) {
+        R::CentroidSet cs;
+        cs.subspace_id = b;
+        cs.count = c;
+        cs.dim = widths[b];
+        cs.centroids.assign(src, src + c * widths[b]);
+        src += c * widths[b];
+        ix.centroid_sets.push_back(std::move(cs));
+    }
+    for (uint64_t t = 0; t < m * c; ++t) {
+        R::TopList tl;
+        tl.capacity = static_cast<uint32_t>(L);
+        tl.indices.assign(idx + t * stride, idx + t * stride + lens[t]);
+        tl.scores.assign(scores + t * stride, scores + t * stride + lens[t]);
+        ix.tables.push_back(std::move(tl));
+    }
+    ix.alpha = static_cast<double>(L) / static_cast<double>(prefill);
+    ix.list_capacity = static_cast<uint32_t>(L);
+    ix.prefill_len = prefill;
+    ix.normalize_keys = normalize_keys != 0;
+    ix.score_bits = score_bits;
+    return ix;
+}
+int copy_bytes(const std::vector<std::uint8_t>& b, uint8_t* out, uint64_t cap, uint64_t* size) {
+    *size = b.size();
+    if (out) {
+        if (cap < b.size()) return CSATTN_ERR_PARAMETER;
+        std::memcpy(out, b.data(), b.size());
+    }
+    return CSATTN_OK;
+}
+}  // namespace
+
+// serialize_index of a host index given as arrays (TopList order)
+int csref_encode(const float* cent, uint64_t c, const uint32_t* lens, const uint32_t* idx,
+                 const float* scores, uint64_t stride, uint64_t L, uint64_t prefill,
+                 int32_t normalize_keys, int32_t score_bits, const uint64_t* widths, uint64_t m,
+                 uint8_t* out, uint64_t cap, uint64_t* size) {
+    int st = CSATTN_OK;
+    const int g = guarded([&] {
+        const auto b = R::serialize_index(index_of(cent, c, lens, idx, scores, stride, L, prefill,
+                                                   normalize_keys, score_bits, widths, m));
+        st = copy_bytes(b, out, cap, size);
+    });
+    return g != CSATTN_OK ? g : st;
+}
+
+// serialize_index of a reference session's current index
+int csref_serialize(void* h, int32_t score_bits, uint8_t* out, uint64_t cap, uint64_t* size) {
+    int st = CSATTN_OK;
+    const int g = guarded([&] {
+        R::CsIndex& ix = static_cast<Group*>(h)->session.index;
+        const int keep = ix.score_bits;
+        ix.score_bits = score_bits;
+        const auto b = R::serialize_index(ix);
+        ix.score_bits = keep;
+        st = copy_bytes(b, out, cap, size);
+    });
+    return g != CSATTN_OK ? g : st;
+}
+
+// deserialize_index -> status (+ csref_last_error) and the re-serialized image
+int csref_roundtrip(const uint8_t* bytes, uint64_t n, uint8_t* out, uint64_t cap, uint64_t* size) {
+    int st = CSATTN_OK;
+    const int g = guarded([&] {
+        const R::CsIndex ix = R::deserialize_index({bytes, n});
+        st = copy_bytes(R::serialize_index(ix), out, cap, size);
+    });
+    return g != CSATTN_OK ? g : st;
+}
+
+// index_footprint of a deserialized image
+int csref_footprint(const uint8_t* bytes, uint64_t n, uint64_t* header, uint64_t* centroid,
+                    uint64_t* entry) {
+    return guarded([&] {
+        const auto fp = R::index_footprint(R::deserialize_index({bytes, n}));
+        *header = fp.header_bytes;
+        *centroid = fp.centroid_bytes;
+        *entry = fp.entry_bytes;
+    });
+}
+
+// load_index + KvStore + Session over the image's prefill rows
+int csref_load(const uint8_t* bytes, uint64_t n, const float* k, const float* v, uint64_t d,
+               const csattn_retrieval_config* rcfg, uint64_t group, void** out) {
+    return guarded([&] {
+        R::CsIndex ix = R::deserialize_index({bytes, n});
+        const uint64_t p = ix.prefill_len;
+        R::KvStore kv(d, {k, p * d}, {v, p * d});
+        R::Session s(std::move(kv), std::move(ix), rcfg_of(rcfg));
+        *out = new Group(std::move(s), group);
+    });
+}
+
 int csref_dense_attention(const float* q, const float* keys, const float* values, uint64_t n,
                           uint64_t d, const uint32_t* mask, uint64_t n_mask, float* out,
                           float* weights) {

@@ -377,6 +377,16 @@ class Session:
                 worst_best_cosine=r.worst_best_cosine))
         return res[0] if g == 1 else res
 
+    # -- CSAT v1 image (serialize_index, index.cpp:289-318) --
+    def serialize(self) -> bytes:
+        """The session's current index as a CSAT v1 image (tables ordered and
+        encoded on the device)."""
+        n = C.c_uint64()
+        _check(lib().csattn_session_serialize(self.h, None, 0, C.byref(n)))
+        buf = (C.c_uint8 * n.value)()
+        _check(lib().csattn_session_serialize(self.h, buf, n.value, C.byref(n)))
+        return bytes(buf)
+
     def close(self):
         if self.h:
             lib().csattn_session_destroy(self.h)
@@ -483,6 +493,99 @@ def import_index(ctx: Context, centroids, lens, indices, scores, list_capacity: 
         sc.ctypes.data, idx.shape[1], list_capacity, alpha, int(normalize_keys), score_bits,
         keys.ctypes.data, values.ctypes.data, keys.size // d, d, _widths_arr(widths),
         len(widths), C.byref(rc), group, max_decode_steps, C.byref(h)))
+    return Session(ctx, h)
+
+
+# ---- CSAT v1 index images (index.hpp:98-121) ----
+
+def f32_to_f16(x: float) -> int:
+    return int(lib().csattn_f32_to_f16(float(x)))
+
+
+def f16_to_f32(h: int) -> float:
+    return float(lib().csattn_f16_to_f32(int(h)))
+
+
+def _u8(data):
+    a = np.frombuffer(bytes(data), dtype=np.uint8)
+    return a, (a.ctypes.data if a.size else None)
+
+
+def csat_header(data) -> dict:
+    """Header fields of a CSAT image (deserialize_index's checks through the widths)."""
+    a, p = _u8(data)
+    h = _abi.CsatHeaderC()
+    _check(lib().csattn_csat_read_header(p, a.size, C.byref(h)))
+    return dict(m=h.m, centroids=h.centroids, list_capacity=h.list_capacity, dim=h.dim,
+                prefill_len=h.prefill_len, score_bits=h.score_bits,
+                normalize_keys=bool(h.normalize_keys), widths=list(h.widths[:h.m]))
+
+
+def _header_c(hd: dict):
+    h = _abi.CsatHeaderC()
+    h.m, h.centroids, h.list_capacity = hd["m"], hd["centroids"], hd["list_capacity"]
+    h.dim, h.prefill_len, h.score_bits = hd["dim"], hd["prefill_len"], hd["score_bits"]
+    h.normalize_keys = int(hd["normalize_keys"])
+    for b, w in enumerate(hd["widths"]):
+        h.widths[b] = w
+    return h
+
+
+def csat_decode(data):
+    """deserialize_index on the host: (header dict, centroids, lens, indices, scores)."""
+    a, p = _u8(data)
+    hd = csat_header(data)
+    T, L = hd["m"] * hd["centroids"], hd["list_capacity"]
+    cent = np.zeros(hd["centroids"] * hd["dim"], np.float32)
+    lens = np.zeros(T, np.uint32)
+    ix = np.zeros((T, L), np.uint32)
+    sc = np.zeros((T, L), np.float32)
+    h = _abi.CsatHeaderC()
+    _check(lib().csattn_csat_decode(p, a.size, C.byref(h), cent.ctypes.data, lens.ctypes.data,
+                                    ix.ctypes.data, sc.ctypes.data, L))
+    return hd, cent, lens, ix, sc
+
+
+def csat_encode(header: dict, centroids, lens, indices, scores) -> bytes:
+    """serialize_index of host tables in TopList order (rows of `indices`/`scores`)."""
+    h = _header_c(header)
+    cent = _f32(centroids).ravel()
+    lens = np.ascontiguousarray(lens, np.uint32)
+    ix = np.ascontiguousarray(indices, np.uint32)
+    sc = np.ascontiguousarray(scores, np.float32)
+    stride = ix.shape[1] if ix.ndim == 2 else ix.size
+    n = C.c_uint64()
+    _check(lib().csattn_csat_encode(C.byref(h), cent.ctypes.data, lens.ctypes.data, ix.ctypes.data,
+                                    sc.ctypes.data, stride, None, 0, C.byref(n)))
+    buf = (C.c_uint8 * n.value)()
+    _check(lib().csattn_csat_encode(C.byref(h), cent.ctypes.data, lens.ctypes.data, ix.ctypes.data,
+                                    sc.ctypes.data, stride, buf, n.value, C.byref(n)))
+    return bytes(buf)
+
+
+def csat_footprint(header: dict, lens) -> dict:
+    """index_footprint (index.cpp:419-431)."""
+    h = _header_c(header)
+    lens = np.ascontiguousarray(lens, np.uint32)
+    a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    _check(lib().csattn_csat_footprint(C.byref(h), lens.ctypes.data, C.byref(a), C.byref(b), C.byref(c)))
+    return dict(header_bytes=a.value, centroid_bytes=b.value, entry_bytes=c.value,
+                payload=b.value + c.value, total=a.value + b.value + c.value)
+
+
+def deserialize(ctx: Context, data, keys, values, cfg: RetrievalConfig, group: int = 1,
+                max_decode_steps: int = 4096) -> Session:
+    """A session from a CSAT image and the prefill KV rows it indexes
+    (load_index + KvStore + Session, session.hpp:19-31)."""
+    a, p = _u8(data)
+    k = _f32(keys)
+    v = _f32(values)
+    hd = csat_header(data)
+    rows = k.size // hd["dim"] if hd["dim"] else 0
+    rc, w = cfg.c()
+    h = C.c_void_p()
+    _check(lib().csattn_session_deserialize(ctx.h, p, a.size, k.ctypes.data, v.ctypes.data, rows,
+                                            C.byref(rc), group, max_decode_steps, C.byref(h)))
     return Session(ctx, h)
 
 

@@ -80,6 +80,15 @@ class ShardIoC(C.Structure):
 SHARD_SCAN, SHARD_BUCKET, SHARD_MARK, SHARD_EMIT, SHARD_MERGE, SHARD_VICTIM, SHARD_INSERT, \
     SHARD_RESCAN = range(8)
 
+CSAT_MAX_SUBSPACES = 32
+
+
+class CsatHeaderC(C.Structure):
+    _fields_ = [("m", C.c_uint64), ("centroids", C.c_uint64), ("list_capacity", C.c_uint64),
+                ("dim", C.c_uint64), ("prefill_len", C.c_uint64), ("score_bits", C.c_int32),
+                ("normalize_keys", C.c_int32), ("widths", C.c_uint64 * CSAT_MAX_SUBSPACES)]
+
+
 SIGNATURES = {
     "csattn_index_config_default": (None, [P(IndexConfigC)]),
     "csattn_retrieval_config_default": (None, [P(RetrievalConfigC)]),
@@ -109,6 +118,15 @@ SIGNATURES = {
     "csattn_shard_create": (C.c_int, [vp, vp, u64, u64, C.c_int32, u64, P(vp)]),
     "csattn_shard_buffer_words": (C.c_int, [vp, P(u64), P(u64), P(u64), P(u64)]),
     "csattn_shard_step": (C.c_int, [vp, u64, P(vp), C.c_int32, P(ShardIoC)]),
+    "csattn_f32_to_f16": (C.c_uint16, [C.c_float]),
+    "csattn_f16_to_f32": (C.c_float, [C.c_uint16]),
+    "csattn_csat_read_header": (C.c_int, [vp, u64, P(CsatHeaderC)]),
+    "csattn_csat_footprint": (C.c_int, [P(CsatHeaderC), vp, P(u64), P(u64), P(u64)]),
+    "csattn_csat_encode": (C.c_int, [P(CsatHeaderC), vp, vp, vp, vp, u64, vp, u64, P(u64)]),
+    "csattn_csat_decode": (C.c_int, [vp, u64, P(CsatHeaderC), vp, vp, vp, vp, u64]),
+    "csattn_session_serialize": (C.c_int, [vp, vp, u64, P(u64)]),
+    "csattn_session_deserialize": (C.c_int, [vp, vp, u64, vp, vp, u64, P(RetrievalConfigC), u64, u64,
+                                             P(vp)]),
     "csattn_session_gather_stats": (C.c_int, [vp, P(u64), P(u64)]),
     "csattn_session_fork": (C.c_int, [vp, u64, P(vp)]),
     "csattn_session_destroy": (C.c_int, [vp]),

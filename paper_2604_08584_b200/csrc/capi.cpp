@@ -22,18 +22,20 @@
 #include "csattn_b200.h"
 #include "kernels.h"
 #include "kmeans.h"
+#include "errors.hpp"
+#include "csat.h"
 #include <random>
+
+namespace csa_host {
+thread_local std::string g_err;
+}  // namespace csa_host
 
 namespace {
 
-thread_local std::string g_err;
-
-struct Fail {
-    csattn_status code;
-    std::string msg;
-};
-
-[[noreturn]] void fail(csattn_status c, std::string m) { throw Fail{c, std::move(m)}; }
+using csa_host::Fail;
+using csa_host::fail;
+using csa_host::g_err;
+using csa_host::guard;
 
 // a nested C-ABI call's failure, re-raised with its status and message
 void check_status(csattn_status st) {
@@ -44,22 +46,6 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(CSATTN_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-template <class F>
-csattn_status guard(F&& f) {
-    try {
-        f();
-        return CSATTN_OK;
-    } catch (const Fail& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return CSATTN_ERR_GENERIC;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return CSATTN_ERR_GENERIC;
-    }
-}
 
 struct DevMem {
     void* p = nullptr;
@@ -212,6 +198,7 @@ struct csattn_session_s {
     DevMem ktail, vtail, cent, ent, n_used, live, blk_off, low, low_cnt, refill, tmm;
     DevMem cache, cbounds, sel, drep, irep, live_g;
     uint64_t group = 1, N = 0, step = 0, max_steps = 0;
+    uint64_t index_prefill = 0;  // CsIndex::prefill_len (0: = h.P); differs after loading an image with appended keys
     double alpha = 0.0;
     int32_t score_bits = 32;
     csattn_retrieval_config rc{};
@@ -1380,6 +1367,100 @@ csattn_status csattn_session_export(csattn_session s, uint32_t* lens, uint32_t* 
     });
 }
 
+// ---- CSAT v1 image of a session (serialize_index / load_index, index.cpp:289-433) ----
+
+csattn_status csattn_session_serialize(csattn_session s, uint8_t* out, uint64_t capacity,
+                                       uint64_t* size) {
+    return guard([&] {
+        if (!size) fail(CSATTN_ERR_PARAMETER, "size must not be null");
+        const uint64_t T = s->T();
+        const uint32_t cap2 = s->h.cap2;
+        cudaStream_t st = s->ctx->stream;
+        csattn_csat_header h{};
+        h.m = s->h.m;
+        h.centroids = s->h.C;
+        h.list_capacity = s->h.L;
+        h.dim = s->h.d;
+        h.prefill_len = s->index_prefill ? s->index_prefill : s->h.P;
+        h.score_bits = s->score_bits == 16 ? 16 : 32;
+        h.normalize_keys = s->h.normalize_keys ? 1 : 0;
+        for (uint64_t b = 0; b < h.m; ++b) h.widths[b] = s->h.widths[b];
+        std::vector<float> cent(static_cast<size_t>(h.centroids) * h.dim);
+        std::vector<uint32_t> live(T);
+        ck(cudaMemcpyAsync(cent.data(), s->cent.p, cent.size() * 4, cudaMemcpyDeviceToHost, st), "serialize");
+        ck(cudaMemcpyAsync(live.data(), s->live.p, T * 4, cudaMemcpyDeviceToHost, st), "serialize");
+        ck(cudaStreamSynchronize(st), "serialize");
+        const uint64_t pre = csa_host::csat_prefix(&h, cent.data(), nullptr);
+        const uint64_t sb = h.score_bits == 16 ? 2 : 4;
+        std::vector<unsigned long long> off(T);
+        std::vector<int> seg_b(T), seg_e(T);
+        uint64_t tb = 0;
+        std::vector<uint32_t> nused(T);
+        ck(cudaMemcpy(nused.data(), s->n_used.p, T * 4, cudaMemcpyDeviceToHost), "serialize");
+        for (uint64_t t = 0; t < T; ++t) {
+            off[t] = tb;
+            tb += 4 + static_cast<uint64_t>(live[t]) * (4 + sb);
+            seg_b[t] = static_cast<int>(t * cap2);
+            seg_e[t] = static_cast<int>(t * cap2 + nused[t]);
+        }
+        *size = pre + tb;
+        if (!out) return;
+        if (capacity < *size)
+            fail(CSATTN_ERR_PARAMETER, "serialize: buffer holds " + std::to_string(capacity) +
+                                           " bytes, image needs " + std::to_string(*size));
+        if (T * cap2 > static_cast<uint64_t>(std::numeric_limits<int>::max()))
+            fail(CSATTN_ERR_CAPACITY, "serialize: table image too large for one sort");
+        csa_host::csat_prefix(&h, cent.data(), out);
+        DevMem keys, sorted, temp, segs, offs, img;
+        keys.alloc(T * cap2 * 8);
+        sorted.alloc(T * cap2 * 8);
+        const size_t tbytes = csa::csat_sort_temp_bytes(static_cast<uint32_t>(T), cap2);
+        temp.alloc(tbytes);
+        segs.alloc(T * 8);
+        offs.alloc(T * 8);
+        img.alloc(tb);
+        ck(cudaMemcpyAsync(segs.p, seg_b.data(), T * 4, cudaMemcpyHostToDevice, st), "serialize");
+        ck(cudaMemcpyAsync(segs.as<int>() + T, seg_e.data(), T * 4, cudaMemcpyHostToDevice, st), "serialize");
+        ck(cudaMemcpyAsync(offs.p, off.data(), T * 8, cudaMemcpyHostToDevice, st), "serialize");
+        ck(csa::launch_csat_tables(s->ent.as<uint2>(), s->n_used.as<uint32_t>(), s->live.as<uint32_t>(),
+                                   static_cast<uint32_t>(T), cap2, segs.as<int>(), segs.as<int>() + T,
+                                   offs.as<unsigned long long>(), h.score_bits == 16 ? 1 : 0,
+                                   keys.as<unsigned long long>(), sorted.as<unsigned long long>(), temp.p,
+                                   tbytes, img.as<unsigned char>(), st),
+           "serialize launch");
+        ck(cudaMemcpyAsync(out + pre, img.p, tb, cudaMemcpyDeviceToHost, st), "serialize");
+        ck(cudaStreamSynchronize(st), "serialize");
+        s->ctx->launches += 3;
+    });
+}
+
+csattn_status csattn_session_deserialize(csattn_ctx ctx, const uint8_t* bytes, uint64_t n,
+                                         const float* keys, const float* values, uint64_t n_rows,
+                                         const csattn_retrieval_config* rcfg, uint64_t group,
+                                         uint64_t max_decode_steps, csattn_session* out) {
+    return guard([&] {
+        csattn_csat_header h{};
+        check_status(csattn_csat_read_header(bytes, n, &h));
+        const uint64_t T = h.m * h.centroids, L = h.list_capacity;
+        std::vector<float> cent(h.centroids * h.dim), sc(T * L);
+        std::vector<uint32_t> lens(T), ix(T * L);
+        check_status(csattn_csat_decode(bytes, n, &h, cent.data(), lens.data(), ix.data(), sc.data(), L));
+        // A session's image can index keys appended after the prefill
+        // (streaming inserts); the KV rows must cover every indexed key. All
+        // n_rows rows become the session's resident rows; prefill_len stays the
+        // index's metadata (written back by serialize).
+        if (n_rows < h.prefill_len)
+            fail(CSATTN_ERR_PARAMETER, "the image indexes " + std::to_string(h.prefill_len) +
+                                           " prefill rows, got " + std::to_string(n_rows) + " KV rows");
+        const double alpha = static_cast<double>(L) / static_cast<double>(h.prefill_len);
+        check_status(csattn_session_import(ctx, cent.data(), h.centroids, lens.data(), ix.data(), sc.data(), L, L,
+                                           alpha, h.normalize_keys, h.score_bits, keys, values,
+                                           n_rows, h.dim, h.widths, h.m, rcfg, group,
+                                           max_decode_steps, out));
+        (*out)->index_prefill = h.prefill_len;
+    });
+}
+
 csattn_status csattn_session_gather_stats(csattn_session s, uint64_t* unique_entries,
                                           uint64_t* total_entries) {
     return guard([&] {
@@ -1697,6 +1778,7 @@ csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn
                              src->h.P, src->group, max_steps, &rc);
         s->alpha = src->alpha;
         s->score_bits = src->score_bits;
+        s->index_prefill = src->index_prefill;
         s->h.normalize_keys = src->h.normalize_keys;
         s->pre = src->pre;
         s->h.kpre = src->h.kpre;
@@ -1749,7 +1831,7 @@ csattn_status csattn_session_info_get(csattn_session s, csattn_session_info* o) 
         o->subspaces = s->h.m;
         o->centroids = s->h.C;
         o->list_capacity = s->h.L;
-        o->prefill_len = s->h.P;
+        o->prefill_len = s->index_prefill ? s->index_prefill : s->h.P;
         o->context_len = s->N;
         o->steps = s->step;
         o->max_context = s->h.max_ctx;

@@ -76,6 +76,14 @@ cudaError_t launch_attend_union(const DecodeProblem* probs, uint32_t ngroups, co
                                 float* parts, float* tails, int num_sms, unsigned long long* tprof,
                                 cudaStream_t st);
 
+// csat_dev.cu: the tables section of a CSAT v1 image, written on the device
+size_t csat_sort_temp_bytes(uint32_t ntables, uint32_t cap2);
+cudaError_t launch_csat_tables(const uint2* ent, const uint32_t* n_used, const uint32_t* live,
+                               uint32_t ntables, uint32_t cap2, const int* seg_begin, const int* seg_end,
+                               const unsigned long long* off, int half, unsigned long long* keys,
+                               unsigned long long* sorted, void* temp, size_t temp_bytes,
+                               unsigned char* out, cudaStream_t st);
+
 cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t nprob, uint32_t d,
                                float* out, cudaStream_t st);
 

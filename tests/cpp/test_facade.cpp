@@ -125,6 +125,45 @@ static void lifecycle(std::size_t P, std::size_t T, std::size_t d, std::size_t m
                      bi.tables[t].scores != rs.index.tables[t].scores);
         CHECK(diff == 0, "P=%zu: %zu tables differ after %zu inserts", P, diff, T);
     }
+    // CSAT v1 images (index.cpp:289-433): host codec and device writer against
+    // serialize_index; load -> decode identical (acceptance.cpp:425-468)
+    {
+        const auto ref_img = R::serialize_index(rs.index);
+        CHECK(B::serialize_index(bs.export_index()) == ref_img, "P=%zu: host CSAT image differs", P);
+        CHECK(bs.serialize() == ref_img, "P=%zu: device CSAT image differs", P);
+        const B::CsIndex back = B::deserialize_index(ref_img);
+        CHECK(B::serialize_index(back) == ref_img, "P=%zu: CSAT decode/encode round trip", P);
+        const auto fp_r = R::index_footprint(rs.index);
+        const auto fp_b = B::index_footprint(back);
+        CHECK(fp_r.header_bytes == fp_b.header_bytes && fp_r.centroid_bytes == fp_b.centroid_bytes &&
+                  fp_r.entry_bytes == fp_b.entry_bytes,
+              "P=%zu: footprint", P);
+        // load the image into fresh sessions on both sides and decode two more steps
+        // the image indexes appended keys too: load with all P + T rows
+        std::vector<float> kk, vv;
+        bs.read_kv(0, P + T, kk, vv);
+        B::Session bl = B::load_session(ref_img, kk, vv, brc, 4);
+        R::Session rl(R::KvStore(d, k.subspan(0, (P + T) * d), v.subspan(0, (P + T) * d)),
+                      R::deserialize_index(ref_img), rrc);
+        const auto rr2 = R::run_decode(rl, pre(q).subspan(0, 2 * d), pre(k).subspan(0, 2 * d),
+                                       pre(v).subspan(0, 2 * d), 2, false);
+        const auto br2 = B::run_decode(bl, pre(q).subspan(0, 2 * d), pre(k).subspan(0, 2 * d),
+                                       pre(v).subspan(0, 2 * d), 2, false);
+        for (std::size_t t = 0; t < 2; ++t)
+            CHECK(rr2[t].selected == br2[t].selected, "P=%zu: loaded-session step %zu differs", P, t);
+        CHECK(bl.serialize() == R::serialize_index(rl.index), "P=%zu: loaded session image after inserts", P);
+        // load errors: same class and message (test_index.cpp:361-390)
+        auto bad = ref_img;
+        bad[4] = 9;
+        const std::string a = thrown<R::VersionError>([&] { R::deserialize_index(bad); });
+        const std::string b = thrown<B::VersionError>([&] { B::deserialize_index(bad); });
+        CHECK(a == b, "version error: '%s' vs '%s'", a.c_str(), b.c_str());
+        bad = ref_img;
+        bad.resize(bad.size() / 3);
+        const std::string c = thrown<R::TruncatedError>([&] { R::deserialize_index(bad); });
+        const std::string e = thrown<B::TruncatedError>([&] { B::deserialize_index(bad); });
+        CHECK(c == e, "truncation error: '%s' vs '%s'", c.c_str(), e.c_str());
+    }
     std::printf("lifecycle P=%zu T=%zu d=%zu m=%zu %s pt=%d: sets equal %zu/%zu, rel err %.2e\n", P,
                 T, d, m, schedule, passthrough ? 1 : 0, T - sel_diff, T, worst);
 }
