@@ -267,11 +267,18 @@ csattn_status csattn_decode_batch(csattn_ctx ctx, uint64_t n_sessions,
                                   const float* new_keys, const float* new_values, float* out,
                                   uint32_t* selected, uint64_t sel_stride, uint32_t flags);
 
-/* Masked (or full, mask == NULL) dense attention on the GPU over the session's
- * current KV rows (core.cpp:118-169). Used for compare_dense and recall. */
+/* The dense oracle on the GPU, over the session's current
+ * KV rows: masked (mask = n_mask row indices) or full (mask == NULL)
+ * dense_attention (core.cpp:118-169): fp64 logits from the reference's
+ * sequential dot, fp64 softmax, f32 weights in mask order, f32 output. Used for
+ * compare_dense and recall at scale. Not on the decode hot path. */
 csattn_status csattn_dense_attention(csattn_session s, const float* q, const uint32_t* mask,
                                      uint64_t n_mask, float* out, float* weights,
                                      uint32_t flags);
+/* dense_topk (core.cpp:171-192): the k rows with the largest sequential-fp64
+ * dot q.k (lower index first on equal scores), returned ascending. */
+csattn_status csattn_dense_topk(csattn_session s, const float* q, uint64_t k, uint32_t* out,
+                                uint32_t flags);
 
 /* ---- CSAT v1 index image (index.hpp:98-121) ----
  * Little-endian image written by serialize_index (index.cpp:289-318) and

@@ -23,7 +23,7 @@
 //     Session::export_index() instead of being a public value member, and
 //     KvStore rows live in HBM (Session::read_kv()).
 //   * decode_step's compare_dense runs the dense oracle on the GPU
-//     (csattn_dense_attention); recall/l2 are computed on the host from it.
+//     (csattn_dense_attention, csattn_dense_topk); recall/l2 follow on the host.
 //   * k_bump is honoured: the callback's input (worst best-cosine of the
 //     step's own routing) is evaluated on the host from the exported
 //     centroids before the step is launched, exactly as decode_search
@@ -634,6 +634,7 @@ inline DecodeStepReport decode_step(Session& session, std::span<const float> q,
     std::vector<float> out(d), w(n);
     csattn_step_report rep{};
     std::optional<AttentionOutput> dense;
+    std::vector<uint32_t> truth;
     if (compare_dense) {  // the dense oracle sees the same pre-append context
         AttentionOutput full;
         full.output.resize(d);
@@ -641,6 +642,11 @@ inline DecodeStepReport decode_step(Session& session, std::span<const float> q,
         check(csattn_dense_attention(session.handle(), q.data(), nullptr, 0, full.output.data(),
                                      full.weights.data(), CSATTN_HOST_BUFFERS));
         dense = std::move(full);
+        // dense_topk (core.cpp:171-192) at this step's K, on the device
+        const std::size_t kk = k_override ? std::min<std::size_t>(k_override, n)
+                                          : keep_count(session.cfg.keep_ratio, n);
+        truth.resize(kk);
+        check(csattn_dense_topk(session.handle(), q.data(), kk, truth.data(), CSATTN_HOST_BUFFERS));
     }
     check(csattn_decode_step(session.handle(), q.data(), new_key.data(), new_value.data(),
                              out.data(), sel.data(), w.data(), n, &rep,
@@ -661,22 +667,7 @@ inline DecodeStepReport decode_step(Session& session, std::span<const float> q,
     r.counters.inserts_applied = rep.inserts_applied;
     r.counters.insert_dot_ops = rep.insert_dot_ops;
     if (dense) {
-        // recall_at_k (metrics.cpp:9-30) against dense_topk (core.cpp:171-192):
-        // the K best sequential-fp64 dot scores, index ascending on ties
-        std::vector<float> kk, vv;
-        session.read_kv(0, n, kk, vv);
-        std::vector<double> sc(n);
-        for (std::size_t i = 0; i < n; ++i) {
-            double a = 0.0;
-            for (std::size_t t = 0; t < d; ++t) a += static_cast<double>(q[t]) * kk[i * d + t];
-            sc[i] = a;
-        }
-        std::vector<uint32_t> order(n);
-        for (uint32_t i = 0; i < n; ++i) order[i] = i;
-        std::partial_sort(order.begin(), order.begin() + static_cast<std::ptrdiff_t>(r.k), order.end(),
-                          [&](uint32_t a, uint32_t b) { return sc[a] != sc[b] ? sc[a] > sc[b] : a < b; });
-        std::vector<uint32_t> truth(order.begin(), order.begin() + static_cast<std::ptrdiff_t>(r.k));
-        std::sort(truth.begin(), truth.end());
+        // recall_at_k (metrics.cpp:9-30) against the dense top-K
         std::size_t hit = 0;
         for (uint32_t x : r.selected) hit += std::binary_search(truth.begin(), truth.end(), x) ? 1 : 0;
         r.recall = truth.empty() ? 1.0 : static_cast<double>(hit) / static_cast<double>(truth.size());

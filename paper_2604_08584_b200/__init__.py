@@ -377,6 +377,28 @@ class Session:
                 worst_best_cosine=r.worst_best_cosine))
         return res[0] if g == 1 else res
 
+    # -- the dense oracle on the device (core.cpp:118-192) --
+    def dense_attention(self, q, mask=None):
+        """Masked (mask = row indices) or full dense_attention over the current
+        KV rows: (output[d], weights[len(mask) or N])."""
+        inf = self.info()
+        qv = _f32(q).reshape(inf.dim)
+        n = inf.context_len if mask is None else len(mask)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint32)
+        out = np.zeros(inf.dim, np.float32)
+        w = np.zeros(max(n, 1), np.float32)
+        _check(lib().csattn_dense_attention(self.h, qv.ctypes.data, None if m is None else m.ctypes.data,
+                                            0 if m is None else m.size, out.ctypes.data, w.ctypes.data,
+                                            _abi.HOST_BUFFERS))
+        return out, w[:n]
+
+    def dense_topk(self, q, k: int) -> np.ndarray:
+        """dense_topk: the k best rows by sequential-fp64 q.k, ascending."""
+        qv = _f32(q).reshape(self.info().dim)
+        out = np.zeros(max(int(k), 1), np.uint32)
+        _check(lib().csattn_dense_topk(self.h, qv.ctypes.data, int(k), out.ctypes.data, _abi.HOST_BUFFERS))
+        return out[:int(k)]
+
     # -- CSAT v1 image (serialize_index, index.cpp:289-318) --
     def serialize(self) -> bytes:
         """The session's current index as a CSAT v1 image (tables ordered and
@@ -494,6 +516,14 @@ def import_index(ctx: Context, centroids, lens, indices, scores, list_capacity: 
         keys.ctypes.data, values.ctypes.data, keys.size // d, d, _widths_arr(widths),
         len(widths), C.byref(rc), group, max_decode_steps, C.byref(h)))
     return Session(ctx, h)
+
+
+def recall_at_k(selected, truth) -> float:
+    """recall_at_k (metrics.cpp:9-30): |selected & truth| / |truth|."""
+    truth = np.asarray(truth)
+    if truth.size == 0:
+        raise ParameterError("recall is undefined against an empty truth set")
+    return float(np.intersect1d(np.asarray(selected), truth).size) / float(truth.size)
 
 
 # ---- CSAT v1 index images (index.hpp:98-121) ----

@@ -158,6 +158,7 @@ struct csattn_ctx_s {
     // number of problems on one prefill for it to engage (default 16)
     uint64_t union_min = std::getenv("CSATTN_UNION_MIN") ? std::strtoull(std::getenv("CSATTN_UNION_MIN"), nullptr, 10) : 16;
     DevMem un_row, un_mask, un_count, un_parts, un_tails;
+    DevMem dense;  // dense oracle scratch (dense.cu)
     // union-kernel timeline (CSATTN_UNION_PROF=1; diagnostics only): per CTA
     // [16 items][4 stamps] + [16] tile counts, summarised at teardown
     bool union_prof = std::getenv("CSATTN_UNION_PROF") != nullptr;
@@ -1941,18 +1942,73 @@ csattn_status csattn_decode_batch(csattn_ctx ctx, uint64_t n, const csattn_sessi
     });
 }
 
+// ---- the dense oracle on the device (core.cpp:118-192) ----
+
 csattn_status csattn_dense_attention(csattn_session s, const float* q, const uint32_t* mask,
                                      uint64_t n_mask, float* out, float* weights,
                                      uint32_t flags) {
     return guard([&] {
-        (void)s;
-        (void)q;
-        (void)mask;
-        (void)n_mask;
-        (void)out;
-        (void)weights;
-        (void)flags;
-        fail(CSATTN_ERR_GENERIC, "dense attention is not built yet");
+        const bool host = flags & CSATTN_HOST_BUFFERS;
+        const uint64_t N = s->N, d = s->h.d;
+        if (N == 0) fail(CSATTN_ERR_PARAMETER, "attention over an empty KV store");
+        uint64_t n = N;
+        std::vector<uint32_t> hm;
+        if (mask) {
+            if (n_mask == 0) fail(CSATTN_ERR_PARAMETER, "attention over an empty index set");
+            hm.resize(n_mask);
+            if (host)
+                std::memcpy(hm.data(), mask, n_mask * 4);
+            else
+                ck(cudaMemcpy(hm.data(), mask, n_mask * 4, cudaMemcpyDeviceToHost), "dense mask");
+            for (uint32_t i : hm)
+                if (i >= N) fail(CSATTN_ERR_PARAMETER, "mask index " + std::to_string(i) + " out of range");
+            n = n_mask;
+        }
+        csattn_ctx ctx = s->ctx;
+        cudaStream_t st = ctx->stream;
+        ctx->dense.ensure(csa::dense_scratch_bytes(static_cast<uint32_t>(n), static_cast<uint32_t>(d)) +
+                          n * 8 + d * 8 + n * 4 + 1024);
+        char* base = ctx->dense.as<char>();
+        const size_t scratch = csa::dense_scratch_bytes(static_cast<uint32_t>(n), static_cast<uint32_t>(d));
+        float* dq = reinterpret_cast<float*>(base + scratch);
+        uint32_t* dmask = reinterpret_cast<uint32_t*>(base + scratch + ((d * 4 + 255) & ~size_t(255)));
+        float* dout = reinterpret_cast<float*>(reinterpret_cast<char*>(dmask) + ((n * 4 + 255) & ~size_t(255)));
+        float* dw = dout + ((d + 63) & ~uint64_t(63));
+        ck(cudaMemcpyAsync(dq, q, d * 4, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st), "dense q");
+        if (mask) ck(cudaMemcpyAsync(dmask, hm.data(), n * 4, cudaMemcpyHostToDevice, st), "dense mask");
+        ck(csa::launch_dense_attention(dq, s->h.kpre, s->h.ktail, s->h.vpre, s->h.vtail, s->h.P,
+                                       mask ? dmask : nullptr, static_cast<uint32_t>(n),
+                                       static_cast<uint32_t>(d), dout, weights ? dw : nullptr, base, st),
+           "dense attention launch");
+        const cudaMemcpyKind kind = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (out) ck(cudaMemcpyAsync(out, dout, d * 4, kind, st), "dense out");
+        if (weights) ck(cudaMemcpyAsync(weights, dw, n * 4, kind, st), "dense weights");
+        ck(cudaStreamSynchronize(st), "dense attention");
+        ctx->launches += 5;
+    });
+}
+
+csattn_status csattn_dense_topk(csattn_session s, const float* q, uint64_t k, uint32_t* out,
+                                uint32_t flags) {
+    return guard([&] {
+        const bool host = flags & CSATTN_HOST_BUFFERS;
+        const uint64_t N = s->N, d = s->h.d;
+        if (k < 1 || k > N) fail(CSATTN_ERR_PARAMETER, "top-k count out of range: " + std::to_string(k));
+        csattn_ctx ctx = s->ctx;
+        cudaStream_t st = ctx->stream;
+        const size_t scratch = csa::dense_scratch_bytes(static_cast<uint32_t>(N), static_cast<uint32_t>(d));
+        ctx->dense.ensure(scratch + d * 4 + k * 4 + 1024);
+        char* base = ctx->dense.as<char>();
+        float* dq = reinterpret_cast<float*>(base + scratch);
+        uint32_t* dout = reinterpret_cast<uint32_t*>(base + scratch + ((d * 4 + 255) & ~size_t(255)));
+        ck(cudaMemcpyAsync(dq, q, d * 4, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st), "topk q");
+        ck(csa::launch_dense_topk(dq, s->h.kpre, s->h.ktail, s->h.P, static_cast<uint32_t>(N),
+                                  static_cast<uint32_t>(d), static_cast<uint32_t>(k), dout, base, scratch, st),
+           "dense topk launch");
+        ck(cudaMemcpyAsync(out, dout, k * 4, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, st),
+           "topk out");
+        ck(cudaStreamSynchronize(st), "dense topk");
+        ctx->launches += 4;
     });
 }
 

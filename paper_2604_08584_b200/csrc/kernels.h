@@ -76,6 +76,15 @@ cudaError_t launch_attend_union(const DecodeProblem* probs, uint32_t ngroups, co
                                 float* parts, float* tails, int num_sms, unsigned long long* tprof,
                                 cudaStream_t st);
 
+// dense.cu: the dense oracle (masked/full dense_attention, dense_topk)
+size_t dense_scratch_bytes(uint32_t n, uint32_t d);
+cudaError_t launch_dense_attention(const float* q, const float* kpre, const float* ktail, const float* vpre,
+                                   const float* vtail, uint32_t P, const uint32_t* mask, uint32_t n,
+                                   uint32_t d, float* out, float* weights, void* scratch, cudaStream_t st);
+cudaError_t launch_dense_topk(const float* q, const float* kpre, const float* ktail, uint32_t P, uint32_t n,
+                              uint32_t d, uint32_t k, uint32_t* out, void* scratch, size_t scratch_bytes,
+                              cudaStream_t st);
+
 // csat_dev.cu: the tables section of a CSAT v1 image, written on the device
 size_t csat_sort_temp_bytes(uint32_t ntables, uint32_t cap2);
 cudaError_t launch_csat_tables(const uint2* ent, const uint32_t* n_used, const uint32_t* live,

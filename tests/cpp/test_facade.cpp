@@ -168,6 +168,44 @@ static void lifecycle(std::size_t P, std::size_t T, std::size_t d, std::size_t m
                 T, d, m, schedule, passthrough ? 1 : 0, T - sel_diff, T, worst);
 }
 
+// compare_dense (session.cpp:66-78): the dense reference, recall@K against
+// dense_topk and the l2 error, with the dense oracle on the GPU
+static void dense_compare() {
+    const std::size_t P = 4096, T = 4, d = 128;
+    R::SyntheticSpec spec;
+    spec.rows = P + T;
+    spec.dim = d;
+    spec.seed = 77;
+    const R::SyntheticWorkload w = R::make_synthetic(spec);
+    const std::span<const float> q(w.queries), k(w.keys), v(w.values);
+    R::IndexConfig ric;
+    ric.cluster.seed = 1;
+    ric.score_bits = 32;
+    B::IndexConfig bic;
+    bic.cluster.seed = 1;
+    bic.score_bits = 32;
+    R::Session rs = R::prefill(q.subspan(0, P * d), k.subspan(0, P * d), v.subspan(0, P * d),
+                               R::SubspaceLayout::uniform(d, 8), ric, R::RetrievalConfig{});
+    B::Session bs = B::prefill(q.subspan(0, P * d), k.subspan(0, P * d), v.subspan(0, P * d),
+                               B::SubspaceLayout::uniform(d, 8), bic, B::RetrievalConfig{}, T);
+    const auto rr = R::run_decode(rs, q.subspan(P * d), k.subspan(P * d), v.subspan(P * d), T, true);
+    const auto br = B::run_decode(bs, q.subspan(P * d), k.subspan(P * d), v.subspan(P * d), T, true);
+    for (std::size_t t = 0; t < T; ++t) {
+        CHECK(rr[t].recall && br[t].recall && *rr[t].recall == *br[t].recall, "step %zu recall %.6f vs %.6f", t,
+              rr[t].recall.value_or(-1), br[t].recall.value_or(-1));
+        double e2 = 0.0, n2 = 0.0;
+        for (std::size_t x = 0; x < d; ++x) {
+            const double a = rr[t].dense_reference->output[x], b = br[t].dense_reference->output[x];
+            e2 += (a - b) * (a - b);
+            n2 += a * a;
+        }
+        CHECK(std::sqrt(e2 / n2) < 1e-6, "step %zu dense output rel err %.3g", t, std::sqrt(e2 / n2));
+        CHECK(std::fabs(*rr[t].l2_error - *br[t].l2_error) < 1e-4, "step %zu l2 %.6g vs %.6g", t,
+              *rr[t].l2_error, *br[t].l2_error);
+    }
+    std::printf("dense compare: recall %.4f (step 0), l2 %.3g: done\n", *br[0].recall, *br[0].l2_error);
+}
+
 static void errors() {
     const std::size_t d = 16, P = 64;
     std::vector<float> q(P * d, 0.5f), k(P * d, 0.25f), v(P * d, 1.0f);
@@ -212,6 +250,7 @@ static void errors() {
 
 int main() {
     errors();
+    dense_compare();
     lifecycle(4096, 12, 128, 8, 2026, "0.05-step-1", true);   // BASELINE config 1
     lifecycle(2000, 10, 64, 8, 7, "0.15-step-4", true);       // period reuse
     lifecycle(1500, 6, 64, 4, 11, "0.05-step-1", false);      // window competes
