@@ -49,6 +49,8 @@ CONFIGS = {
     # name: (prefill P, sequences, layers, description)
     "c2": (32768, 1, 1, "Llama-3.1-8B-shaped attention layer (32 q / 8 KV heads, d=128) at 32K "
                         "context, 1 B200"),
+    "c2o": (32768, 1, 1, "c2 in the CPU<->GPU offload mode: KV rows in pinned host memory, tables "
+                         "in HBM; a step moves only the selected K/V rows over the host link"),
     "c3": (131072, 16, 1, "Llama-3.1-8B-shaped layer at 128K context, batch-16 decode sharing one "
                           "prefilled context"),
     "c4": (131072, 1, 32, "full 32-layer Llama-3.1-8B-shaped decode at 128K, KV heads sharded "
@@ -447,6 +449,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
     ctx = cs.Context(local, stream.cuda_stream)
+    if args.config == "c2o":  # offload mode
+        ctx.set_kv_placement("host")
+        config["kv_placement"] = "pinned host memory (mapped), tables in HBM"
 
     steps, warm = args.steps, args.warmup
     prof_steps = min(steps, 10)

@@ -153,6 +153,15 @@ const char* csattn_status_name(csattn_status s);
 csattn_status csattn_ctx_create(int device, void* cuda_stream, csattn_ctx* out);
 csattn_status csattn_ctx_destroy(csattn_ctx ctx);
 csattn_status csattn_ctx_synchronize(csattn_ctx ctx);
+/* KV placement of sessions created on this context from now on (the paper's
+ * CPU<->GPU offload mode; the reference has only its byte
+ * model, metrics.cpp:32-38). CSATTN_KV_HOST keeps every KV row (prefill and
+ * appended) in mapped pinned host memory: the tables stay in HBM, and a
+ * decode step moves only the selected K/V rows (and the appended row) across
+ * the host link. */
+#define CSATTN_KV_DEVICE 0
+#define CSATTN_KV_HOST 1
+csattn_status csattn_ctx_set_kv_placement(csattn_ctx ctx, int32_t placement);
 /* Number of CUDA kernels this context has launched (driver-side evidence). */
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx);
 /* Kernel timing: when enabled, the three kernels of every decode step

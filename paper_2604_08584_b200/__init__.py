@@ -245,6 +245,11 @@ class Context:
         self.h = h
         self.device = device
 
+    def set_kv_placement(self, placement: str):
+        """'device' (HBM, default) or 'host': sessions created afterwards keep
+        their KV rows in mapped pinned host memory (offload mode)."""
+        _check(lib().csattn_ctx_set_kv_placement(self.h, {"device": 0, "host": 1}[placement]))
+
     def synchronize(self):
         _check(lib().csattn_ctx_synchronize(self.h))
 

@@ -119,6 +119,7 @@ SIGNATURES = {
     "csattn_shard_buffer_words": (C.c_int, [vp, P(u64), P(u64), P(u64), P(u64)]),
     "csattn_shard_step": (C.c_int, [vp, u64, P(vp), C.c_int32, P(ShardIoC)]),
     "csattn_dense_topk": (C.c_int, [vp, vp, u64, vp, u32]),
+    "csattn_ctx_set_kv_placement": (C.c_int, [vp, C.c_int32]),
     "csattn_f32_to_f16": (C.c_uint16, [C.c_float]),
     "csattn_f16_to_f32": (C.c_float, [C.c_uint16]),
     "csattn_csat_read_header": (C.c_int, [vp, u64, P(CsatHeaderC)]),

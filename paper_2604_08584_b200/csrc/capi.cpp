@@ -50,20 +50,32 @@ void ck(cudaError_t e, const char* what) {
 struct DevMem {
     void* p = nullptr;
     size_t n = 0;
+    bool host = false;  // mapped pinned host memory (KV offload), device-addressable through UVA
     DevMem() = default;
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
-    ~DevMem() {
-        if (p) cudaFree(p);
-    }
-    void alloc(size_t bytes) {
-        if (p) cudaFree(p);
+    ~DevMem() { release(); }
+    void release() {
+        if (p) host ? cudaFreeHost(p) : cudaFree(p);
         p = nullptr;
         n = 0;
+    }
+    void alloc(size_t bytes) {
+        release();
+        host = false;
         if (bytes == 0) bytes = 16;
         ck(cudaMalloc(&p, bytes), "cudaMalloc");
         n = bytes;
     }
+    // pinned host memory the kernels read and write over the host link
+    void alloc_host(size_t bytes) {
+        release();
+        host = true;
+        if (bytes == 0) bytes = 16;
+        ck(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+        n = bytes;
+    }
+    void alloc_on(bool on_host, size_t bytes) { on_host ? alloc_host(bytes) : alloc(bytes); }
     void ensure(size_t bytes) {
         if (bytes > n) alloc(bytes + bytes / 2);
     }
@@ -159,6 +171,8 @@ struct csattn_ctx_s {
     uint64_t union_min = std::getenv("CSATTN_UNION_MIN") ? std::strtoull(std::getenv("CSATTN_UNION_MIN"), nullptr, 10) : 16;
     DevMem un_row, un_mask, un_count, un_parts, un_tails;
     DevMem dense;  // dense oracle scratch (dense.cu)
+    // KV placement of sessions created from now on (csattn_ctx_set_kv_placement)
+    bool kv_host = false;
     // union-kernel timeline (CSATTN_UNION_PROF=1; diagnostics only): per CTA
     // [16 items][4 stamps] + [16] tile counts, summarised at teardown
     bool union_prof = std::getenv("CSATTN_UNION_PROF") != nullptr;
@@ -326,8 +340,8 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     }
     set_retrieval(s.get(), rc);
     const uint64_t T = m * c;
-    s->ktail.alloc(std::max<uint64_t>(max_steps, 1) * d * sizeof(float));
-    s->vtail.alloc(std::max<uint64_t>(max_steps, 1) * d * sizeof(float));
+    s->ktail.alloc_on(s->ctx->kv_host, std::max<uint64_t>(max_steps, 1) * d * sizeof(float));
+    s->vtail.alloc_on(s->ctx->kv_host, std::max<uint64_t>(max_steps, 1) * d * sizeof(float));
     s->cent.alloc(c * d * sizeof(float));
     s->ent.alloc(T * cap2 * sizeof(uint2));
     s->n_used.alloc(T * 4);
@@ -365,16 +379,15 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
 }
 
 void upload(csattn_ctx ctx, void* dst, const void* src, size_t bytes, bool host) {
-    ck(cudaMemcpyAsync(dst, src, bytes, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                       ctx->stream),
-       "copy in");
+    (void)host;  // UVA: the runtime resolves device, mapped-host and pageable pointers
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream), "copy in");
 }
 
 void attach_rows(csattn_session_s* s, const float* keys, const float* values, bool host) {
     s->pre = std::make_shared<SharedRows>();
     const size_t bytes = static_cast<size_t>(s->h.P) * s->h.d * sizeof(float);
-    s->pre->k.alloc(bytes);
-    s->pre->v.alloc(bytes);
+    s->pre->k.alloc_on(s->ctx->kv_host, bytes);
+    s->pre->v.alloc_on(s->ctx->kv_host, bytes);
     upload(s->ctx, s->pre->k.p, keys, bytes, host);
     upload(s->ctx, s->pre->v.p, values, bytes, host);
     s->h.kpre = s->pre->k.as<float>();
@@ -1134,6 +1147,14 @@ csattn_session_s::~csattn_session_s() {
 
 extern "C" {
 
+csattn_status csattn_ctx_set_kv_placement(csattn_ctx ctx, int32_t placement) {
+    return guard([&] {
+        if (placement != CSATTN_KV_DEVICE && placement != CSATTN_KV_HOST)
+            fail(CSATTN_ERR_PARAMETER, "KV placement must be CSATTN_KV_DEVICE or CSATTN_KV_HOST");
+        ctx->kv_host = placement == CSATTN_KV_HOST;
+    });
+}
+
 csattn_status csattn_ctx_synchronize(csattn_ctx ctx) {
     return guard([&] { ck(cudaStreamSynchronize(ctx->stream), "synchronize"); });
 }
@@ -1790,7 +1811,7 @@ csattn_status csattn_session_fork(csattn_session src, uint64_t max_steps, csattn
         cudaStream_t st = src->ctx->stream;
         const uint64_t T = s->T();
         auto d2d = [&](DevMem& dst, const DevMem& from, size_t bytes) {
-            ck(cudaMemcpyAsync(dst.p, from.p, bytes, cudaMemcpyDeviceToDevice, st), "fork copy");
+            ck(cudaMemcpyAsync(dst.p, from.p, bytes, cudaMemcpyDefault, st), "fork copy");
         };
         const size_t rows = (src->N - src->h.P) * src->h.d * 4;
         if (rows) {
@@ -1910,9 +1931,9 @@ csattn_status csattn_session_read_kv(csattn_session s, uint64_t first, uint64_t 
             const float* kb = pre ? s->h.kpre + i * d : s->h.ktail + (i - P) * d;
             const float* vb = pre ? s->h.vpre + i * d : s->h.vtail + (i - P) * d;
             if (keys)
-                ck(cudaMemcpyAsync(keys + (i - first) * d, kb, n * d * 4, cudaMemcpyDeviceToHost, st), "read kv");
+                ck(cudaMemcpyAsync(keys + (i - first) * d, kb, n * d * 4, cudaMemcpyDefault, st), "read kv");
             if (values)
-                ck(cudaMemcpyAsync(values + (i - first) * d, vb, n * d * 4, cudaMemcpyDeviceToHost, st), "read kv");
+                ck(cudaMemcpyAsync(values + (i - first) * d, vb, n * d * 4, cudaMemcpyDefault, st), "read kv");
             i = lim;
         }
         ck(cudaStreamSynchronize(st), "read kv");
