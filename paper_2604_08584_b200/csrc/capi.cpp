@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -99,9 +100,14 @@ uint64_t keep_count(double rho, uint64_t n) {
 }
 
 void require_finite(const float* v, size_t n, const char* what) {
-    for (size_t i = 0; i < n; ++i)
-        if (!std::isfinite(v[i]))
-            fail(CSATTN_ERR_DATA, std::string(what) + " contains a non-finite value");
+    // exponent all ones = inf or nan; branch-free so the scan vectorizes
+    uint32_t bad = 0;
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t b;
+        std::memcpy(&b, v + i, 4);
+        bad |= static_cast<uint32_t>((b & 0x7f800000u) == 0x7f800000u);
+    }
+    if (bad) fail(CSATTN_ERR_DATA, std::string(what) + " contains a non-finite value");
 }
 
 struct SharedRows {
@@ -173,6 +179,9 @@ struct csattn_ctx_s {
     DevMem dense;  // dense oracle scratch (dense.cu)
     // KV placement of sessions created from now on (csattn_ctx_set_kv_placement)
     bool kv_host = false;
+    bool host_prof = std::getenv("CSATTN_HOST_PROF") != nullptr;
+    double host_sum[4] = {0, 0, 0, 0}, host_sub[4] = {0, 0, 0, 0}, host_sub2[3] = {0, 0, 0};
+    uint64_t host_n = 0;
     // union-kernel timeline (CSATTN_UNION_PROF=1; diagnostics only): per CTA
     // [16 items][4 stamps] + [16] tile counts, summarised at teardown
     bool union_prof = std::getenv("CSATTN_UNION_PROF") != nullptr;
@@ -435,6 +444,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
               const float* keys, const float* values, float* out, uint32_t* selected,
               float* weights, uint64_t sel_stride, csattn_step_report* reports,
               const uint64_t* k_override, uint32_t flags) {
+    const auto ht0 = std::chrono::steady_clock::now();
     const bool host = flags & CSATTN_HOST_BUFFERS;
     if (ns == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
     const uint32_t d = ss[0]->h.d;
@@ -459,10 +469,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     if ((selected || weights) && sel_stride < maxK)
         fail(CSATTN_ERR_PARAMETER, "selected/weights stride " + std::to_string(sel_stride) +
                                        " is below K = " + std::to_string(maxK));
+    const auto hta = std::chrono::steady_clock::now();
     if (host) {
         require_finite(keys, ns * d, "appended key");
         require_finite(values, ns * d, "appended value");
     }
+    const auto htb = std::chrono::steady_clock::now();
     if (maxN > csa::SELECT_MAX_CONTEXT)
         fail(CSATTN_ERR_CAPACITY, "context of " + std::to_string(maxN) +
                                       " keys exceeds one GPU's decode search (" +
@@ -498,6 +510,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         dsel = selected ? reinterpret_cast<uint32_t*>(base + o_sel) : nullptr;
         dw = weights ? reinterpret_cast<float*>(base + o_w) : nullptr;
     }
+    const auto htc = std::chrono::steady_clock::now();
     ctx->hprobs.resize(nq);
     if (ctx->phase_prof) {
         ctx->phase.ensure(nq * 8 * sizeof(unsigned long long));
@@ -538,6 +551,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         I.N = static_cast<uint32_t>(n);
         I.pad = 0;
     }
+    const auto ht1 = std::chrono::steady_clock::now();
     // stage both descriptor arrays through one pinned ring slot
     auto& slot = ctx->ring[ctx->next_slot];
     ctx->next_slot = (ctx->next_slot + 1) % csattn_ctx_s::kSlots;
@@ -593,6 +607,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->un_parts.ensure(nmem * u_nrange * csa::UN_PART_WORDS * 4);
         ctx->un_tails.ensure(nmem * csa::UN_PART_WORDS * 4);
     }
+    const auto htd = std::chrono::steady_clock::now();
     // attention work list: ceil(K / ATT_ROWS) chunk-CTAs per problem
     std::vector<uint32_t> cbase(nq + 1), cprob;
     for (uint64_t i = 0; i < nq; ++i) {
@@ -644,6 +659,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const csa::InsertProblem* diprobs = reinterpret_cast<const csa::InsertProblem*>(db + ioff);
     const uint32_t* dcbase = reinterpret_cast<const uint32_t*>(db + boff);
     const uint32_t* dcprob = reinterpret_cast<const uint32_t*>(db + poff);
+    const auto hte = std::chrono::steady_clock::now();
     std::array<cudaEvent_t, 4> ev{};
     if (ctx->profile) {
         for (auto& e : ev) e = ctx->take_event();
@@ -778,6 +794,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->ev_steps.push_back(ev);
     }
     ctx->launches += nchunks ? 5 : 4;
+    const auto ht2 = std::chrono::steady_clock::now();
     if (ctx->phase_prof) {
         // per problem: streaming (gather + log) and final-selection time,
         // logged candidates, threshold-bin size; printed at context teardown
@@ -887,7 +904,24 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             }
         }
     }
+    const auto ht3 = std::chrono::steady_clock::now();
     if (host || !(flags & CSATTN_NO_SYNC)) ck(cudaStreamSynchronize(ctx->stream), "decode step");
+    if (ctx->host_prof && host) {  // host-buffer calls: phases (CSATTN_HOST_PROF=1; diagnostics only)
+        const auto ht4 = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        ctx->host_sum[0] += us(ht0, ht1);
+        ctx->host_sum[1] += us(ht1, ht2);
+        ctx->host_sum[2] += us(ht2, ht3);
+        ctx->host_sum[3] += us(ht3, ht4);
+        ctx->host_sub[0] += us(ht0, hta);
+        ctx->host_sub[1] += us(hta, htb);
+        ctx->host_sub[2] += us(htb, htc);
+        ctx->host_sub[3] += us(htc, ht1);
+        ctx->host_sub2[0] += us(ht1, htd);
+        ctx->host_sub2[1] += us(htd, hte);
+        ctx->host_sub2[2] += us(hte, ht2);
+        ctx->host_n += 1;
+    }
 }
 
 // ---- host <-> device table images ----
@@ -1108,6 +1142,18 @@ static void ctx_release(csattn_ctx ctx) {
         std::fprintf(stderr, "[csattn] speculative cut: %llu of %llu problems retried\n",
                      static_cast<unsigned long long>(ctx->phase_retry),
                      static_cast<unsigned long long>(ctx->phase_probs));
+    }
+    if (ctx->host_n) {
+        const double n = static_cast<double>(ctx->host_n);
+        std::fprintf(stderr,
+                     "[csattn] run_step host (mean over %llu calls): prepare %.1f us, stage+launch %.1f us, "
+                     "bookkeeping+copies %.1f us, sync wait %.1f us\n",
+                     static_cast<unsigned long long>(ctx->host_n), ctx->host_sum[0] / n, ctx->host_sum[1] / n,
+                     ctx->host_sum[2] / n, ctx->host_sum[3] / n);
+        std::fprintf(stderr, "[csattn]   prepare = sizes %.1f + finite checks %.1f + uploads %.1f + descriptors %.1f us\n",
+                     ctx->host_sub[0] / n, ctx->host_sub[1] / n, ctx->host_sub[2] / n, ctx->host_sub[3] / n);
+        std::fprintf(stderr, "[csattn]   stage+launch = slot wait %.1f + work list/staging %.1f + launches %.1f us\n",
+                     ctx->host_sub2[0] / n, ctx->host_sub2[1] / n, ctx->host_sub2[2] / n);
     }
     if (ctx->un_items) {
         const double n = static_cast<double>(ctx->un_items);
