@@ -228,13 +228,13 @@ __device__ __forceinline__ float4 load_q2(const float* q, int ln) {
 constexpr int TC_LOAD = 128;
 constexpr int TC_THREADS = 18 * 32;  // 576
 __device__ __forceinline__ int loader_slot(int w) {  // 0-3 K, 4-7 V, -1 other
-    switch (w) {
+    switch (w) {  // K and V loaders alternate over sub-partitions 2 and 3
         case 3: return 0;
-        case 7: return 1;
-        case 11: return 2;
-        case 15: return 3;
-        case 10: return 4;
-        case 14: return 5;
+        case 10: return 1;
+        case 7: return 2;
+        case 14: return 3;
+        case 11: return 4;
+        case 15: return 5;
         case 16: return 6;
         case 17: return 7;
         default: return -1;
@@ -283,7 +283,8 @@ struct TcSmem {  // 1024-byte aligned operand buffers
     static constexpr uint32_t P0 = 163840, PSZ = 16384;   // P (A of PV, K-major, 64 rows): hi | lo; x2
     static constexpr uint32_t MISC = 196608;
     // MMA lanes 64-127 of the last P slot read up to 8 KB past it: keep it in bounds
-    static constexpr uint32_t BYTES = MISC + 8192;
+    static constexpr uint32_t CROW = MISC + 8192;       // u16[UN_RANGE]: the item's union rows
+    static constexpr uint32_t BYTES = CROW + UN_RANGE * 2;
 };
 static_assert(TcSmem::BYTES + 1024 <= 232448, "shared memory budget");
 struct TcMisc {
@@ -342,33 +343,48 @@ __device__ __forceinline__ void tc_loader(TcMisc& X, uint32_t sbase, const float
     auto prefetch_tile = [&](uint32_t tt) {
         if (lt < TC_TILE && tt < ntile) {
             const uint32_t u = tt * TC_TILE + lt;
-            if (u < nu) prefetch_l2(src + static_cast<size_t>(__ldg(urow + u)) * 128, 512);
+            if (u < nu) prefetch_l2(src + static_cast<size_t>(urow[u]) * 128, 512);
+        }
+    };
+    // software pipeline over half tiles: the loads of item j + 1 are in
+    // flight while item j waits for its slot, converts and stores
+    constexpr int NH = NV / 2;
+    auto load_half = [&](uint32_t item, float4 (&v)[NH]) {
+        const uint32_t tt = item >> 1, hh = item & 1u;
+#pragma unroll
+        for (int i = 0; i < NH; ++i) {
+            const uint32_t x = lt + TC_LOAD * (i + NH * hh);
+            const uint32_t row = x >> 5, e = x & 31, u = tt * TC_TILE + row;
+            v[i] = (tt < ntile && u < nu)
+                       ? __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(urow[u]) * 128) + e)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     };
     for (uint32_t tt = 0; tt < PF; ++tt) prefetch_tile(tt);
-    for (uint32_t t = 0; t < ntile; ++t, ++T) {
-        prefetch_tile(t + PF);
-        float4 cur[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const uint32_t x = lt + TC_LOAD * i;
-            const uint32_t row = x >> 5, e = x & 31, u = t * TC_TILE + row;
-            cur[i] = u < nu ? __ldg(reinterpret_cast<const float4*>(src + static_cast<size_t>(__ldg(urow + u)) * 128) + e)
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+    float4 cur[NH], nxt[NH];
+    load_half(0, cur);
+    for (uint32_t item = 0; item < 2 * ntile; ++item) {
+        const uint32_t t = item >> 1, hh = item & 1u;
+        if (hh == 0) prefetch_tile(t + PF);
+        load_half(item + 1, nxt);
         const uint32_t b = T & 1u;
-        if (T >= 2) tc::mbar_wait(PASS ? &X.vempty[b] : &X.kempty[b], ((T >> 1) - 1) & 1u);
+        if (hh == 0 && T >= 2) tc::mbar_wait(PASS ? &X.vempty[b] : &X.kempty[b], ((T >> 1) - 1) & 1u);
         const uint32_t base = sbase + (PASS ? TcSmem::V0 + b * TcSmem::VSZ : TcSmem::K0 + b * TcSmem::KSZ);
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const uint32_t x = lt + TC_LOAD * i;
+        for (int i = 0; i < NH; ++i) {
+            const uint32_t x = lt + TC_LOAD * (i + NH * hh);
             const uint32_t row = x >> 5, e = x & 31;
             const uint32_t off = PASS ? tc::mnmaj_off(4 * e, row, TC_TILE) : tc::kmaj_off(row, 4 * e, TC_TILE);
             store4_split(base + off, base + 16384 + off, cur[i]);
         }
-        tc::fence_smem_async();
-        mbar_arrive(PASS ? &X.vfull[b] : &X.kfull[b]);
-        if (ts && lt == 0 && t < 10) ts[t * 8 + 4 + PASS] = gtime();
+        if (hh == 1) {
+            tc::fence_smem_async();
+            mbar_arrive(PASS ? &X.vfull[b] : &X.kfull[b]);
+            if (ts && lt == 0 && t < 10) ts[t * 8 + 4 + PASS] = gtime();
+            ++T;
+        }
+#pragma unroll
+        for (int i = 0; i < NH; ++i) cur[i] = nxt[i];
     }
 }
 
@@ -445,6 +461,10 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
                 store4_split(sbase + TcSmem::QHI + off, sbase + TcSmem::QLO + off, v);
             }
         }
+        {   // the item's union rows -> shared memory (the loaders' index lookups)
+            uint16_t* crow = reinterpret_cast<uint16_t*>(sm + TcSmem::CROW);
+            for (uint32_t u = tid; u < nu; u += TC_THREADS) crow[u] = __ldg(urow + u);
+        }
         tc::fence_smem_async();
         __syncthreads();
         if (rec) {
@@ -467,9 +487,11 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
             const int sl = loader_slot(w);
             const uint32_t lw = static_cast<uint32_t>(sl & 3) * 32 + ln;
             if (sl < 4)
-                tc_loader<0>(X, sbase, X.kv[0], urow, nu, ntile, lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
+                tc_loader<0>(X, sbase, X.kv[0], reinterpret_cast<const uint16_t*>(sm + TcSmem::CROW), nu, ntile,
+                             lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
             else
-                tc_loader<1>(X, sbase, X.kv[1], urow, nu, ntile, lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
+                tc_loader<1>(X, sbase, X.kv[1], reinterpret_cast<const uint16_t*>(sm + TcSmem::CROW), nu, ntile,
+                             lw, T, (tp && it_no == 0) ? tp + 80 : nullptr);
         } else if (w == 2) {
             // ================= QK issuer: S[slot] = Q . K^T =================
             for (uint32_t t = 0; t < ntile; ++t, ++T) {
@@ -610,7 +632,7 @@ attend_tc_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         }
         ++items;
         tc::fence_before();
-        __syncthreads();  // item done: Q, bitmaps and O may be rewritten
+        __syncthreads();  // item done: Q, rows and O may be rewritten
         tc::fence_after();
         if (rec) tp[it_no * 4 + 3] = gtime();
         ++it_no;
