@@ -129,6 +129,56 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int n, int kind, unsigned lon
     if (tid < 32) tc::tmem_free<256>(tbase);
 }
 
+// O[128][128] = P[128 x 64] . V[64 x 128]: P from TMEM (tcgen05.st), V MN-major B
+__global__ void __launch_bounds__(128, 1) probe_ts(const float* Pm, const float* V, float* O_out) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    unsigned char* sV = sm;  // V as MN-major B (N = dims 128, K = rows 64): 16 KB
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < 64 * 128; i += 128) {
+        const int r = i / 128, c = i % 128;
+        *reinterpret_cast<__nv_bfloat16*>(sV + tc::mnmaj_off(c, r, 64)) = __float2bfloat16(V[i]);
+    }
+    if (tid == 0) tc::mbar_init(&bar, 1);
+    if (tid < 32) tc::tmem_alloc<256>(&tbase);
+    tc::fence_smem_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const int w = tid >> 5;
+    const uint32_t lane = static_cast<uint32_t>(w * 32) << 16;
+    const uint32_t tP = tbase, tO = tbase + 128;
+    for (int s = 0; s < 4; ++s) {  // k-step s: P[tid][16s .. 16s+15] -> columns 8s .. 8s+7
+        uint32_t v[8];
+        for (int i = 0; i < 8; ++i) {
+            const __nv_bfloat162 h = __floats2bfloat162_rn(Pm[tid * 64 + 16 * s + 2 * i], Pm[tid * 64 + 16 * s + 2 * i + 1]);
+            v[i] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        tc::tmem_st8(tP + lane + 8 * s, v);
+    }
+    tc::tmem_st_wait();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+        const uint32_t id = tc::idesc_bf16(128, 128, false, true);
+        for (int s = 0; s < 4; ++s)
+            tc::mma_bf16_ts(tO, tP + 8 * s, tc::desc_sw128(tc::smem_u32(sV) + s * 2048, 64 * 128, 1024), id, s > 0);
+        tc::commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after();
+    for (int c = 0; c < 128; c += 32) {
+        float v[32];
+        tc::tmem_ld32(tO + lane + c, v);
+        for (int i = 0; i < 32; ++i) O_out[tid * 128 + c + i] = v[i];
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (tid < 32) tc::tmem_free<256>(tbase);
+}
+
 static float bf(float x) {
     return __bfloat162float(__float2bfloat16(x));
 }
@@ -179,6 +229,29 @@ int main() {
                        O[r * 64 + j], o);
         }
     printf("max |S err| %.3g  max |O err| %.3g  %s\n", es, eo, (es < 1e-3 && eo < 1e-3) ? "OK" : "FAIL");
+    {  // A from TMEM
+        std::vector<float> Pm(128 * 64), V2(64 * 128), O2(128 * 128);
+        for (auto& x : Pm) x = rnd();
+        for (auto& x : V2) x = rnd();
+        float *dPm, *dV2, *dO2;
+        cudaMalloc(&dPm, Pm.size() * 4);
+        cudaMalloc(&dV2, V2.size() * 4);
+        cudaMalloc(&dO2, O2.size() * 4);
+        cudaMemcpy(dPm, Pm.data(), Pm.size() * 4, cudaMemcpyHostToDevice);
+        cudaMemcpy(dV2, V2.data(), V2.size() * 4, cudaMemcpyHostToDevice);
+        cudaFuncSetAttribute(probe_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768);
+        probe_ts<<<1, 128, 32768>>>(dPm, dV2, dO2);
+        cudaError_t e2 = cudaDeviceSynchronize();
+        cudaMemcpy(O2.data(), dO2, O2.size() * 4, cudaMemcpyDeviceToHost);
+        double err = 0;
+        for (int m = 0; m < 128; ++m)
+            for (int j = 0; j < 128; ++j) {
+                double o = 0;
+                for (int k = 0; k < 64; ++k) o += (double)bf(Pm[m * 64 + k]) * bf(V2[k * 128 + j]);
+                err = fmax(err, fabs(o - O2[m * 128 + j]));
+            }
+        printf("A-from-TMEM PV: %s max |err| %.3g %s\n", cudaGetErrorString(e2), err, err < 1e-3 ? "OK" : "FAIL");
+    }
     unsigned long long* dc;
     cudaMalloc(&dc, 64);
     cudaFuncSetAttribute(mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
