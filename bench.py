@@ -456,7 +456,8 @@ def main():
     steps, warm = args.steps, args.warmup
     prof_steps = min(steps, 10)
     e2e_steps = min(steps, 10)
-    T = warm + steps + prof_steps + e2e_steps + 2
+    graph_steps = min(steps, 10)
+    T = warm + steps + prof_steps + e2e_steps + 3 * graph_steps + 2
     from paper_2604_08584_b200.sharding import kv_head_shard
     my_heads = kv_head_shard(N_KV, world, rank)
     widths = [D // M] * M
@@ -645,6 +646,44 @@ def main():
         e2e_ms = float(tm.item())
     assert np.isfinite(op[t - 1].numpy()).all()
     assert torch.isfinite(outd[warm:warm + steps]).all()
+    # ---- whole-run CUDA graph (csattn_decode_run): graph_steps
+    # steps per call, capture + instantiate + launch + sync inside the clock;
+    # once from device buffers, once from pinned host buffers (all steps' inputs
+    # copied in and outputs out inside the call) ----
+    graph = {"steps_per_call": graph_steps}
+    for mode in ("warmup", "device", "e2e"):  # warmup: first-call arena / staging growth
+        hostb = mode != "device"
+        src = (qp, kp, vp_) if hostb else (qd, kd, vd)
+        bufs = []
+        for l in range(n_layers):
+            qs, ks = l * ns_l * GROUP, l * ns_l
+            sl = [x[t:t + graph_steps, a:a + n].contiguous() for x, a, n in
+                  zip(src, (qs, ks, ks), (ns_l * GROUP, ns_l, ns_l))]
+            if hostb:
+                sl = [x.pin_memory() for x in sl]
+            o = torch.empty((graph_steps, ns_l * GROUP, D), dtype=torch.float32,
+                            device="cpu" if hostb else "cuda")
+            bufs.append(sl + [o.pin_memory() if hostb else o])
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        if dist:
+            dist.barrier()
+        tg0 = time.perf_counter()
+        for l in range(n_layers):
+            gq, gk, gv, go = bufs[l]
+            cs._check(lib.csattn_decode_run(
+                ctx.h, ns_l, handles[l], graph_steps, C.c_void_p(gq.data_ptr()),
+                C.c_void_p(gk.data_ptr()), C.c_void_p(gv.data_ptr()), C.c_void_p(go.data_ptr()),
+                None, 0, None, _abi.HOST_BUFFERS if hostb else 0))
+        g_ms = (time.perf_counter() - tg0) * 1e3 / graph_steps
+        if dist:
+            tm = torch.tensor([g_ms], device="cuda")
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            g_ms = float(tm.item())
+        if mode != "warmup":
+            graph[f"{mode}_us_per_step"] = g_ms * 1e3
+        assert all(torch.isfinite(b[3]).all() for b in bufs)
+        t += graph_steps
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -680,6 +719,7 @@ def main():
             "e2e": {"value": e2e_ms * 1e3, "unit": "us",
                     "h2d_bytes_per_step": int(qh[0].nbytes + kh[0].nbytes + vh[0].nbytes),
                     "d2h_bytes_per_step": int(op[0].numel() * 4)},
+            "graph": graph,
             "gpu_launches": int(gpu_launches),
             "clocks": clk.summary(),
             "setup_s": {"synthetic": round(t_gen, 2), "gpu_build": round(t_build, 2),

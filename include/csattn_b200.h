@@ -276,6 +276,18 @@ csattn_status csattn_decode_batch(csattn_ctx ctx, uint64_t n_sessions,
                                   const float* new_keys, const float* new_values, float* out,
                                   uint32_t* selected, uint64_t sel_stride, uint32_t flags);
 
+/* run_decode over n_steps steps of a session set as ONE CUDA graph (SURVEY
+ * §8(f) row 2; session.cpp:101-126 without the per-step reports): step t reads
+ * q + t*nq*d, new_keys/new_values + t*n*d and writes out + t*nq*d and selected +
+ * t*nq*sel_stride (either may be NULL); k_override, when given, is n_steps x nq
+ * (0 = keep_count). The steps and their results equal n_steps calls of
+ * csattn_decode_batch. Every session needs n_steps free decode steps (else
+ * CSATTN_ERR_CAPACITY with no state changed). Synchronous. */
+csattn_status csattn_decode_run(csattn_ctx ctx, uint64_t n_sessions, const csattn_session* sessions,
+                                uint64_t n_steps, const float* q, const float* new_keys,
+                                const float* new_values, float* out, uint32_t* selected,
+                                uint64_t sel_stride, const uint64_t* k_override, uint32_t flags);
+
 /* The dense oracle on the GPU, over the session's current
  * KV rows: masked (mask = n_mask row indices) or full (mask == NULL)
  * dense_attention (core.cpp:118-169): fp64 logits from the reference's

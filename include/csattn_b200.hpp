@@ -704,4 +704,42 @@ inline std::vector<DecodeStepReport> run_decode(Session& session, std::span<cons
     return out;
 }
 
+// run_decode as ONE CUDA graph (csattn_decode_run): the same
+// steps, the same selected sets and outputs, without per-step reports. The
+// session's step count advances; its totals are not accumulated (no counters
+// are read back).
+struct GraphRun {
+    std::vector<std::vector<std::uint32_t>> selected;  // per step, ascending
+    std::vector<float> outputs;                         // steps x d
+};
+
+inline GraphRun run_decode_graph(Session& session, std::span<const float> queries,
+                                 std::span<const float> keys, std::span<const float> values,
+                                 std::size_t steps,
+                                 Context& ctx = Context::default_context()) {
+    const std::size_t d = session.dim();
+    if (queries.size() % d != 0 || keys.size() % d != 0 || values.size() % d != 0)
+        throw DimensionError("decode rows are not a multiple of d");
+    const std::size_t available = std::min({queries.size() / d, keys.size() / d, values.size() / d});
+    if (available < steps)
+        throw StreamExhaustedError("decode streams run out at step " + std::to_string(available) +
+                                   " of " + std::to_string(steps));
+    GraphRun r;
+    if (steps == 0) return r;
+    const std::size_t n0 = session.size();
+    const std::size_t stride = n0 + steps;
+    r.outputs.assign(steps * d, 0.0f);
+    std::vector<std::uint32_t> sel(steps * stride);
+    csattn_session h = session.handle();
+    check(csattn_decode_run(ctx.handle(), 1, &h, steps, queries.data(), keys.data(),
+                            values.data(), r.outputs.data(), sel.data(), stride, nullptr,
+                            CSATTN_HOST_BUFFERS));
+    for (std::size_t t = 0; t < steps; ++t) {
+        const std::size_t k = keep_count(session.cfg.keep_ratio, n0 + t);
+        r.selected.emplace_back(sel.begin() + t * stride, sel.begin() + t * stride + k);
+    }
+    session.step += steps;
+    return r;
+}
+
 }  // namespace csattn_b200

@@ -449,6 +449,52 @@ def decode_batch(sessions, q, new_keys, new_values):
     return out, sel
 
 
+def decode_run(sessions, q, new_keys, new_values, k_override=None):
+    """run_decode over T steps of a session set as ONE CUDA graph
+    (csattn_decode_run; session.cpp:101-126 without the per-step reports):
+    q is [T, rows, d], new_keys/new_values [T, len(sessions), d] — numpy arrays
+    (host) or CUDA tensors (device, outputs returned as CUDA tensors).
+    k_override, if given, is [T, rows] (0 = keep_count). Returns (out [T, rows,
+    d], selected [T, rows, stride]); step t's row r set is selected[t, r, :k]
+    with k its keep count. Equal to T calls of decode_batch."""
+    if not sessions:
+        raise ParameterError("no sessions")
+    ctx = sessions[0].ctx
+    d = sessions[0].info().dim
+    rows = sum(s.group for s in sessions)
+    ns = len(sessions)
+    T = int(q.shape[0])
+    stride = max(s.context_len for s in sessions) + T
+    ko = None
+    if k_override is not None:
+        ko = np.ascontiguousarray(np.asarray(k_override, dtype=np.uint64).reshape(T, rows))
+    hs = (C.c_void_p * ns)(*[s.h for s in sessions])
+    if _is_cuda(q):
+        import torch
+        q = q.contiguous().float()
+        nk = new_keys.contiguous().float()
+        nv = new_values.contiguous().float()
+        if tuple(q.shape) != (T, rows, d) or nk.numel() != T * ns * d or nv.numel() != T * ns * d:
+            raise DimensionError("decode_run: q [T, rows, d], keys/values [T, sessions, d]")
+        out = torch.empty((T, rows, d), dtype=torch.float32, device=q.device)
+        sel = torch.empty((T, rows, stride), dtype=torch.int32, device=q.device)
+        torch.cuda.current_stream(q.device).synchronize()  # inputs ready for the context's stream
+        _check(lib().csattn_decode_run(ctx.h, ns, hs, T, q.data_ptr(), nk.data_ptr(),
+                                       nv.data_ptr(), out.data_ptr(), sel.data_ptr(), stride,
+                                       ko.ctypes.data if ko is not None else None, 0))
+        return out, sel
+    q = _f32(q).reshape(T, rows, d)
+    nk = _f32(new_keys).reshape(T, ns, d)
+    nv = _f32(new_values).reshape(T, ns, d)
+    out = np.zeros((T, rows, d), np.float32)
+    sel = np.zeros((T, rows, stride), np.uint32)
+    _check(lib().csattn_decode_run(ctx.h, ns, hs, T, q.ctypes.data, nk.ctypes.data,
+                                   nv.ctypes.data, out.ctypes.data, sel.ctypes.data, stride,
+                                   ko.ctypes.data if ko is not None else None,
+                                   _abi.HOST_BUFFERS))
+    return out, sel
+
+
 def _widths_arr(widths):
     return (C.c_uint64 * len(widths))(*[int(w) for w in widths])
 

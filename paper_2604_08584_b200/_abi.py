@@ -140,6 +140,7 @@ SIGNATURES = {
     "csattn_decode_step": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, u64, P(StepReportC), P(u64),
                                      u32]),
     "csattn_decode_batch": (C.c_int, [vp, u64, P(vp), vp, vp, vp, vp, vp, u64, u32]),
+    "csattn_decode_run": (C.c_int, [vp, u64, P(vp), u64, vp, vp, vp, vp, vp, u64, vp, u32]),
     "csattn_dense_attention": (C.c_int, [vp, vp, vp, u64, vp, vp, u32]),
 }
 

@@ -48,6 +48,11 @@ void ck(cudaError_t e, const char* what) {
 }
 
 
+// set while a decode graph is being captured (run_graph): every buffer was sized
+// by the preceding sizing pass, so a growth here would leave the graph pointing
+// at freed memory
+thread_local bool g_no_alloc = false;
+
 struct DevMem {
     void* p = nullptr;
     size_t n = 0;
@@ -62,14 +67,22 @@ struct DevMem {
         n = 0;
     }
     void alloc(size_t bytes) {
+        if (g_no_alloc) fail(CSATTN_ERR_GENERIC, "internal: buffer growth while capturing a decode graph");
+        static const bool prof = std::getenv("CSATTN_HOST_PROF") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         release();
         host = false;
         if (bytes == 0) bytes = 16;
         ck(cudaMalloc(&p, bytes), "cudaMalloc");
         n = bytes;
+        if (prof) {
+            const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+            if (us > 1000.0) std::fprintf(stderr, "[csattn] slow device alloc: %zu bytes in %.1f us\n", bytes, us);
+        }
     }
     // pinned host memory the kernels read and write over the host link
     void alloc_host(size_t bytes) {
+        if (g_no_alloc) fail(CSATTN_ERR_GENERIC, "internal: buffer growth while capturing a decode graph");
         release();
         host = true;
         if (bytes == 0) bytes = 16;
@@ -144,11 +157,21 @@ struct csattn_ctx_s {
     static constexpr int kSlots = 4;
     Slot ring[kSlots];
     int next_slot = 0;
+    // whole-run decode graphs (csattn_decode_run): 0 = off, 1 = sizing pass
+    // (buffers grown, no stream work), 2 = capturing. Each captured step gets its
+    // own descriptor copy in one arena (a ring slot would be overwritten before
+    // the graph runs).
+    int capture = 0;
+    std::vector<size_t> cap_need, cap_off;
+    size_t cap_step = 0, cap_bytes = 0;
+    void* cap_host = nullptr;
+    DevMem cap_dev, run_stage;
     ~csattn_ctx_s() {
         for (Slot& s : ring) {
             if (s.host) cudaFreeHost(s.host);
             if (s.done) cudaEventDestroy(s.done);
         }
+        if (cap_host) cudaFreeHost(cap_host);
     }
     std::vector<unsigned char> hrep;
     // kernel timing (csattn_ctx_profile)
@@ -552,17 +575,23 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         I.pad = 0;
     }
     const auto ht1 = std::chrono::steady_clock::now();
-    // stage both descriptor arrays through one pinned ring slot
-    auto& slot = ctx->ring[ctx->next_slot];
-    ctx->next_slot = (ctx->next_slot + 1) % csattn_ctx_s::kSlots;
-    if (slot.used) ck(cudaEventSynchronize(slot.done), "descriptor slot");
+    // stage both descriptor arrays through one pinned ring slot (a graph
+    // capture stages through its own arena instead; see run_graph)
+    const int cap = ctx->capture;
+    const bool live = cap != 1;  // sizing pass: no stream work
+    csattn_ctx_s::Slot* slot = nullptr;
+    if (!cap) {
+        slot = &ctx->ring[ctx->next_slot];
+        ctx->next_slot = (ctx->next_slot + 1) % csattn_ctx_s::kSlots;
+        if (slot->used) ck(cudaEventSynchronize(slot->done), "descriptor slot");
+    }
     // union attend groups: problems on one prefill, in first-appearance order,
     // cut into groups of <= UN_GROUP (attend_union.cu)
     std::vector<uint32_t> ugP, ugmem, umem, umgrp;
     std::vector<char> in_union(nq, 0);
     uint32_t u_maxP = 0;
     const char* uenv = std::getenv("CSATTN_UNION");
-    if (uenv && uenv[0] == '1' && !dw && d == 128) {
+    if (!cap && uenv && uenv[0] == '1' && !dw && d == 128) {
         std::vector<std::pair<const float*, std::vector<uint32_t>>> by_pre;
         std::vector<uint32_t> prob_sess(nq);
         qi = 0;
@@ -634,14 +663,27 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const size_t u_gm = uoff + al(ngroups * 4), u_m = u_gm + al(ugmem.size() * 4);
     const size_t u_mg = u_m + al(nmem * 4);
     const size_t need = u_mg + nmem * 4;
-    if (need > slot.cap) {
-        if (slot.host) ck(cudaFreeHost(slot.host), "cudaFreeHost");
-        slot.cap = need + need / 2;
-        ck(cudaMallocHost(&slot.host, slot.cap), "cudaMallocHost");
-        slot.dev.alloc(slot.cap);
+    char *hb = nullptr, *db = nullptr;
+    if (slot) {
+        if (need > slot->cap) {
+            if (slot->host) ck(cudaFreeHost(slot->host), "cudaFreeHost");
+            slot->cap = need + need / 2;
+            ck(cudaMallocHost(&slot->host, slot->cap), "cudaMallocHost");
+            slot->dev.alloc(slot->cap);
+        }
+        if (!slot->done) ck(cudaEventCreateWithFlags(&slot->done, cudaEventDisableTiming), "event");
+        hb = static_cast<char*>(slot->host);
+        db = slot->dev.as<char>();
+    } else if (cap == 1) {
+        ctx->cap_need.push_back(need);
+    } else {
+        const size_t t = ctx->cap_step++;
+        if (t >= ctx->cap_need.size() || need > ctx->cap_need[t])
+            fail(CSATTN_ERR_GENERIC, "internal: decode graph step differs from its sizing pass");
+        hb = static_cast<char*>(ctx->cap_host) + ctx->cap_off[t];
+        db = ctx->cap_dev.as<char>() + ctx->cap_off[t];
     }
-    if (!slot.done) ck(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "event");
-    char* hb = static_cast<char*>(slot.host);
+    if (live) {
     std::memcpy(hb, ctx->hprobs.data(), dbytes);
     std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
     std::memcpy(hb + boff, cbase.data(), (nq + 1) * 4);
@@ -652,9 +694,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         std::memcpy(hb + u_m, umem.data(), nmem * 4);
         std::memcpy(hb + u_mg, umgrp.data(), nmem * 4);
     }
-    ck(cudaMemcpyAsync(slot.dev.p, hb, need, cudaMemcpyHostToDevice, ctx->stream),
-       "descriptor upload");
-    char* db = slot.dev.as<char>();
+    if (!cap)  // a captured step's descriptors go up with its chunk (run_graph)
+        ck(cudaMemcpyAsync(db, hb, need, cudaMemcpyHostToDevice, ctx->stream),
+           "descriptor upload");
+    }
     const csa::DecodeProblem* dprobs = reinterpret_cast<const csa::DecodeProblem*>(db);
     const csa::InsertProblem* diprobs = reinterpret_cast<const csa::InsertProblem*>(db + ioff);
     const uint32_t* dcbase = reinterpret_cast<const uint32_t*>(db + boff);
@@ -666,6 +709,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaEventRecord(ev[0], ctx->stream), "event");
     }
     ctx->plans.ensure(nq * sizeof(csa::RoutePlan));
+    if (live)
     ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
                          ctx->stream),
        "route launch");
@@ -689,7 +733,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     // retry list of problems whose speculative cut proved too high: [count, ids...]
     ctx->retry.ensure((nq + 1) * 4);
-    ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
+    if (live) ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
     uint32_t* const rcount = ctx->retry.as<uint32_t>();
     if (maxN > ctx->log_cap || sgrid > ctx->log_rows) {  // non-split / retry-pass logs
         // sized for the sessions' full capacity, so it is not re-grown every step
@@ -701,7 +745,15 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->log_idx.alloc(ctx->log_rows * ctx->log_cap * 4);
         ctx->log_sc.alloc(ctx->log_rows * ctx->log_cap * 8);
     }
-    if (split == 1) {
+    if (!live) {
+        if (split > 1) {  // grow the split buffers only
+            const uint64_t ucap = (max_tiles + split - 1) / split * tile;
+            const uint64_t units = nq * split;
+            ctx->ulog_idx.ensure(units * ucap * 4);
+            ctx->ulog_sc.ensure(units * ucap * 8);
+            ctx->umeta.ensure(units * csa::select_unit_meta_words() * 4);
+        }
+    } else if (split == 1) {
         ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
                               sgrid, ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
                               static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
@@ -728,13 +780,14 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
            "select merge launch");
     }
     // second pass over the (usually empty) retry list, without speculation
+    if (live)
     ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
                           ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
                           static_cast<uint32_t>(ctx->log_cap), rcount + 1, rcount, nullptr, nullptr,
                           0.0, 1, nullptr, ctx->stream),
        "select retry launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
-    if (nchunks)
+    if (nchunks && live)
         ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
                               ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream),
            "attend launch");
@@ -786,9 +839,11 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
     }
     if (ctx->profile) ck(cudaEventRecord(ev[2], ctx->stream), "event");
-    ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
-    ck(cudaEventRecord(slot.done, ctx->stream), "event");
-    slot.used = true;
+    if (live) ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
+    if (slot) {
+        ck(cudaEventRecord(slot->done, ctx->stream), "event");
+        slot->used = true;
+    }
     if (ctx->profile) {
         ck(cudaEventRecord(ev[3], ctx->stream), "event");
         ctx->ev_steps.push_back(ev);
@@ -2006,6 +2061,209 @@ csattn_status csattn_decode_batch(csattn_ctx ctx, uint64_t n, const csattn_sessi
     return guard([&] {
         run_step(ctx, n, ss, q, keys, values, out, selected, nullptr, sel_stride, nullptr,
                  nullptr, flags);
+    });
+}
+
+}  // extern "C"
+
+// ---- whole-run decode as one CUDA graph ----
+
+namespace {
+
+// T consecutive decode steps of a session set (run_decode, session.cpp:101-126,
+// without the per-step reports) captured into one CUDA graph and launched once:
+// no per-step host round trip, launch or descriptor wait. Pass 1 runs the host
+// side of every step without stream work, so every buffer reaches its final
+// size and each step's descriptor bytes are known; the session counters are
+// then rewound and pass 2 captures the same steps, each staging its descriptors
+// in its own slice of one pinned arena.
+void run_graph(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, uint64_t T, const float* q,
+               const float* keys, const float* values, float* out, uint32_t* selected,
+               uint64_t sel_stride, const uint64_t* k_override, uint32_t flags) {
+    if (ns == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
+    if (T == 0) return;
+    const bool host = flags & CSATTN_HOST_BUFFERS;
+    const uint64_t d = ss[0]->h.d;
+    uint64_t nq = 0;
+    for (uint64_t i = 0; i < ns; ++i) {
+        if (ss[i]->ctx != ctx) fail(CSATTN_ERR_PARAMETER, "sessions belong to another context");
+        if (ss[i]->step + T > ss[i]->max_steps)
+            fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
+                                          std::to_string(ss[i]->max_steps));
+        nq += ss[i]->group;
+    }
+    const auto hs0 = std::chrono::steady_clock::now();
+    const float *dq = q, *dk = keys, *dv = values;
+    float* dout = out;
+    uint32_t* dsel = selected;
+    size_t o_out = 0, o_sel = 0;
+    if (host) {
+        require_finite(keys, T * ns * d, "appended key");
+        require_finite(values, T * ns * d, "appended value");
+        auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+        const size_t o_k = al(T * nq * d * 4), o_v = o_k + al(T * ns * d * 4);
+        o_out = o_v + al(T * ns * d * 4);
+        o_sel = o_out + (out ? al(T * nq * d * 4) : 0);
+        const size_t total = o_sel + (selected ? T * nq * sel_stride * 4 : 0);
+        ctx->run_stage.ensure(total);
+        char* b = ctx->run_stage.as<char>();
+        upload(ctx, b, q, T * nq * d * 4, true);
+        upload(ctx, b + o_k, keys, T * ns * d * 4, true);
+        upload(ctx, b + o_v, values, T * ns * d * 4, true);
+        dq = reinterpret_cast<const float*>(b);
+        dk = reinterpret_cast<const float*>(b + o_k);
+        dv = reinterpret_cast<const float*>(b + o_v);
+        dout = out ? reinterpret_cast<float*>(b + o_out) : nullptr;
+        dsel = selected ? reinterpret_cast<uint32_t*>(b + o_sel) : nullptr;
+    }
+    struct Saved {
+        uint64_t N, step;
+        std::vector<HeadState> hs;
+    };
+    std::vector<Saved> saved;
+    for (uint64_t i = 0; i < ns; ++i) saved.push_back({ss[i]->N, ss[i]->step, ss[i]->hs});
+    const uint64_t launches0 = ctx->launches;
+    const bool prof[3] = {ctx->profile, ctx->phase_prof, ctx->union_prof};
+    auto reset = [&] {
+        for (uint64_t i = 0; i < ns; ++i) {
+            ss[i]->N = saved[i].N;
+            ss[i]->step = saved[i].step;
+            ss[i]->hs = saved[i].hs;
+        }
+        ctx->launches = launches0;
+    };
+    auto leave = [&] {
+        g_no_alloc = false;
+        ctx->capture = 0;
+        ctx->profile = prof[0];
+        ctx->phase_prof = prof[1];
+        ctx->union_prof = prof[2];
+    };
+    auto steps = [&](uint64_t t0, uint64_t t1) {
+        for (uint64_t t = t0; t < t1; ++t)
+            run_step(ctx, ns, ss, dq + t * nq * d, dk + t * ns * d, dv + t * ns * d,
+                     dout ? dout + t * nq * d : nullptr,
+                     dsel ? dsel + t * nq * sel_stride : nullptr, nullptr, sel_stride, nullptr,
+                     k_override ? k_override + t * nq : nullptr, CSATTN_NO_SYNC);
+    };
+    const auto h0 = std::chrono::steady_clock::now();
+    ctx->profile = ctx->phase_prof = ctx->union_prof = false;
+    // chunks of kChunk steps: chunk c+1 is captured and instantiated while
+    // chunk c runs, so only the sizing pass and the first capture are exposed
+    constexpr uint64_t kChunk = 4;
+    std::vector<cudaGraph_t> graphs;
+    std::vector<cudaGraphExec_t> execs;
+    auto release = [&] {
+        for (auto x : execs) cudaGraphExecDestroy(x);
+        for (auto g : graphs) cudaGraphDestroy(g);
+    };
+    uint64_t launched = 0;  // steps whose graph was launched
+    std::chrono::steady_clock::time_point h1, h2;
+    try {
+        ctx->capture = 1;  // pass 1: sizes
+        ctx->cap_need.clear();
+        steps(0, T);
+        reset();
+        ctx->cap_off.assign(T, 0);
+        size_t total = 0;
+        for (uint64_t t = 0; t < T; ++t) {
+            ctx->cap_off[t] = total;
+            total += (ctx->cap_need[t] + 255) & ~size_t(255);
+        }
+        if (total > ctx->cap_bytes) {
+            // the previous run (if any) finished: run_graph synchronizes
+            if (ctx->cap_host) ck(cudaFreeHost(ctx->cap_host), "cudaFreeHost");
+            ctx->cap_host = nullptr;
+            ctx->cap_bytes = 0;
+            ck(cudaMallocHost(&ctx->cap_host, total + total / 4), "cudaMallocHost");
+            ctx->cap_dev.alloc(total + total / 4);
+            ctx->cap_bytes = total + total / 4;
+        }
+        h1 = std::chrono::steady_clock::now();
+        ctx->capture = 2;  // pass 2: capture chunk by chunk
+        ctx->cap_step = 0;
+        for (uint64_t c0 = 0; c0 < T; c0 += kChunk) {
+            const uint64_t c1 = std::min(T, c0 + kChunk);
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+            g_no_alloc = true;
+            try {
+                steps(c0, c1);
+            } catch (...) {
+                g_no_alloc = false;
+                cudaStreamEndCapture(ctx->stream, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            g_no_alloc = false;
+            ck(cudaStreamEndCapture(ctx->stream, &g), "end capture");
+            graphs.push_back(g);
+            cudaGraphExec_t x = nullptr;
+            ck(cudaGraphInstantiate(&x, g, 0), "graph instantiate");
+            execs.push_back(x);
+            // the chunk's descriptors in one copy, then its kernels
+            const size_t a = ctx->cap_off[c0], z = ctx->cap_off[c1 - 1] + ctx->cap_need[c1 - 1];
+            ck(cudaMemcpyAsync(ctx->cap_dev.as<char>() + a, static_cast<char*>(ctx->cap_host) + a, z - a,
+                               cudaMemcpyHostToDevice, ctx->stream),
+               "descriptor upload");
+            ck(cudaGraphLaunch(x, ctx->stream), "graph launch");
+            launched = c1;
+            if (c0 == 0) h2 = std::chrono::steady_clock::now();
+        }
+        leave();
+    } catch (...) {
+        leave();
+        // host counters back to the last launched step: rewind, then replay the
+        // host side of the launched steps without stream work
+        reset();
+        if (launched) {
+            ctx->capture = 1;
+            ctx->cap_need.clear();
+            try {
+                steps(0, launched);
+            } catch (...) {
+            }
+            ctx->capture = 0;
+        }
+        cudaStreamSynchronize(ctx->stream);
+        release();
+        throw;
+    }
+    if (host) {
+        const char* b = ctx->run_stage.as<char>();
+        if (out)
+            ck(cudaMemcpyAsync(out, b + o_out, T * nq * d * 4, cudaMemcpyDeviceToHost, ctx->stream),
+               "copy out");
+        if (selected)
+            ck(cudaMemcpyAsync(selected, b + o_sel, T * nq * sel_stride * 4,
+                               cudaMemcpyDeviceToHost, ctx->stream),
+               "copy selected");
+    }
+    const auto h3 = std::chrono::steady_clock::now();
+    // the arena and the graphs are released once the run is done
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    release();
+    if (ctx->host_prof) {
+        const auto h4 = std::chrono::steady_clock::now();
+        auto us = [](auto x, auto y) { return std::chrono::duration<double, std::micro>(y - x).count(); };
+        std::fprintf(stderr, "[csattn] decode_run %llu steps: inputs %.1f us, sizing %.1f, first chunk capture+launch %.1f, "
+                     "remaining captures %.1f, wait %.1f us\n", static_cast<unsigned long long>(T),
+                     us(hs0, h0), us(h0, h1), us(h1, h2), us(h2, h3), us(h3, h4));
+    }
+    ck(e, "decode run");
+}
+
+}  // namespace
+
+extern "C" {
+
+csattn_status csattn_decode_run(csattn_ctx ctx, uint64_t n_sessions, const csattn_session* sessions,
+                                uint64_t n_steps, const float* q, const float* new_keys,
+                                const float* new_values, float* out, uint32_t* selected,
+                                uint64_t sel_stride, const uint64_t* k_override, uint32_t flags) {
+    return guard([&] {
+        run_graph(ctx, n_sessions, sessions, n_steps, q, new_keys, new_values, out, selected,
+                  sel_stride, k_override, flags);
     });
 }
 

@@ -76,6 +76,7 @@ static void lifecycle(std::size_t P, std::size_t T, std::size_t d, std::size_t m
 
     R::Session rs = R::prefill(pre(q), pre(k), pre(v), R::SubspaceLayout::uniform(d, m), ric, rrc);
     B::Session bs = B::prefill(pre(q), pre(k), pre(v), B::SubspaceLayout::uniform(d, m), bic, brc, T);
+    B::Session bg = bs.fork(T);  // decoded below as one CUDA graph (run_decode_graph)
 
     // offline build: identical tables (membership, order, scores)
     {
@@ -113,6 +114,16 @@ static void lifecycle(std::size_t P, std::size_t T, std::size_t d, std::size_t m
               "step %zu counters differ", t);
     }
     CHECK(sel_diff == 0, "P=%zu %s: %zu of %zu selected sets differ", P, schedule, sel_diff, T);
+    {
+        const B::GraphRun gr = B::run_decode_graph(bg, tail(q), tail(k), tail(v), T);
+        std::size_t gdiff = 0;
+        for (std::size_t t = 0; t < T; ++t)
+            gdiff += gr.selected[t] != br[t].selected ||
+                     !std::equal(br[t].attention.output.begin(), br[t].attention.output.end(),
+                                 gr.outputs.begin() + t * d);
+        CHECK(gdiff == 0, "P=%zu %s: %zu of %zu graph-run steps differ", P, schedule, gdiff, T);
+        CHECK(bg.serialize() == bs.serialize(), "P=%zu: graph-run tables differ", P);
+    }
     CHECK(worst <= 1e-3, "P=%zu %s: output rel err %.3g", P, schedule, worst);
     CHECK(rs.totals.inserts_applied == bs.totals.inserts_applied, "totals");
 
