@@ -276,18 +276,23 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         const uint32_t i = __ldg(P.sel + r0 + ln);
         myoff = i < P0 ? i * d : ((i - P0) * d) | 0x80000000u;
     }
+    // lanes past the batch repeat row r0 (always present): every load is
+    // unconditional, and those rows drop out through their zero probability
+    {
+        const uint32_t o0 = __shfl_sync(0xffffffffu, myoff, 0);
+        if (ln >= nr) myoff = o0;
+    }
     for (uint32_t g0 = 0; g0 < nr; g0 += GR) {
         float4 kk[GR], vv[GR];
 #pragma unroll
         for (int u = 0; u < GR; ++u) {
             const uint32_t o = __shfl_sync(0xffffffffu, myoff, (g0 + u) & 31);
-            const bool ok = g0 + u < nr;
             const bool tl = o & 0x80000000u;
             const uint32_t e = (o & 0x7fffffffu) + 4 * ln;
             const float* kr = (tl ? ktail : kpre) + e;
             const float* vr = (tl ? vtail : vpre) + e;
-            kk[u] = ok ? ld_row4(kr) : make_float4(0.f, 0.f, 0.f, 0.f);
-            vv[u] = ok ? ld_row4(vr) : make_float4(0.f, 0.f, 0.f, 0.f);
+            kk[u] = ld_row4(kr);
+            vv[u] = ld_row4(vr);
         }
         float pd[GR];
 #pragma unroll
