@@ -14,6 +14,8 @@
 // the weights buffer and normalized in place) and resets the counter.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <cfloat>
 #include <cstdint>
 #include <cstdlib>
@@ -225,7 +227,7 @@ __device__ __forceinline__ float4 ld_row4(const float* p) {
 }
 
 template <bool PARTIAL, int GR>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
-__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 6 : 5)
+__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 7 : 5)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
                  uint32_t* __restrict__ counters) {
@@ -282,17 +284,26 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         const uint32_t o0 = __shfl_sync(0xffffffffu, myoff, 0);
         if (ln >= nr) myoff = o0;
     }
+    // sel is ascending, so appended rows form a suffix: nearly every batch is
+    // prefill-only and takes the loop without per-row store selection
+    const bool mixed = __any_sync(0xffffffffu, (myoff & 0x80000000u) != 0u);
+    auto groups = [&](auto mixed_c, auto weights_c) {
+    constexpr bool MIXED = decltype(mixed_c)::value;
+    constexpr bool WTS = decltype(weights_c)::value;
     for (uint32_t g0 = 0; g0 < nr; g0 += GR) {
         float4 kk[GR], vv[GR];
 #pragma unroll
         for (int u = 0; u < GR; ++u) {
             const uint32_t o = __shfl_sync(0xffffffffu, myoff, (g0 + u) & 31);
-            const bool tl = o & 0x80000000u;
-            const uint32_t e = (o & 0x7fffffffu) + 4 * ln;
-            const float* kr = (tl ? ktail : kpre) + e;
-            const float* vr = (tl ? vtail : vpre) + e;
-            kk[u] = ld_row4(kr);
-            vv[u] = ld_row4(vr);
+            if constexpr (MIXED) {
+                const bool tl = o & 0x80000000u;
+                const uint32_t e = (o & 0x7fffffffu) + 4 * ln;
+                kk[u] = ld_row4((tl ? ktail : kpre) + e);
+                vv[u] = ld_row4((tl ? vtail : vpre) + e);
+            } else {
+                kk[u] = ld_row4(kpre + (o + 4 * ln));
+                vv[u] = ld_row4(vpre + (o + 4 * ln));
+            }
         }
         float pd[GR];
 #pragma unroll
@@ -337,7 +348,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
         if constexpr (GR == 8) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 4));
         gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 8));
         gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 16));
-        if (gm > m) {  // warp-uniform: rescale only when the running max grows
+        if (__builtin_expect(gm > m, 0)) {  // warp-uniform: rescale only when the running max grows
             const float f = ex2f(m - gm);
             s *= f;
 #pragma unroll
@@ -360,9 +371,17 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
             acc[0][2] = fmaf(pu, vv[u].z, acc[0][2]);
             acc[0][3] = fmaf(pu, vv[u].w, acc[0][3]);
         }
-        if (want_w && valid && (ln & (GR == 8 ? 3 : 7)) == 0)
-            P.weights[r0 + g0 + myrow] = lg * LN2;  // natural-log logit, normalized later
+        if constexpr (WTS)
+            if (valid && (ln & (GR == 8 ? 3 : 7)) == 0)
+                P.weights[r0 + g0 + myrow] = lg * LN2;  // natural-log logit, normalized later
     }
+    };
+    if (want_w)
+        groups(std::true_type{}, std::true_type{});
+    else if (mixed)
+        groups(std::true_type{}, std::false_type{});
+    else
+        groups(std::false_type{}, std::false_type{});
     }
     // ---- CTA partial ----
     if (ln == 0) {
@@ -468,7 +487,11 @@ cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
-    static const int gr = std::getenv("CSATTN_ATT_GR8") ? 8 : 4;  // 4: 75 regs, 6 CTAs/SM
+    // GR=4 (72 regs, 7 CTAs/SM) for large launches; GR=8 (more rows in flight
+    // per warp) for small ones: c2's 224 chunks 29 -> 23 us, while c4's 832 per
+    // layer and c3's 13312 are faster with GR=4. CSATTN_ATT_GR=4|8 forces.
+    const int gr_env = std::getenv("CSATTN_ATT_GR") ? std::atoi(std::getenv("CSATTN_ATT_GR")) : 0;
+    const int gr = gr_env == 4 || gr_env == 8 ? gr_env : (nchunks < 148u * 3u ? 8 : 4);
     if (d == 128 && partial) {
         if (gr == 4) attend128_kernel<true, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
         else attend128_kernel<true, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);

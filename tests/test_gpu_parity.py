@@ -359,3 +359,31 @@ def test_union_attend_fork_batch(ctx, monkeypatch, ctas):
                 assert np.array_equal(sel[row, :r.k], r.selected), (t, f, h)
                 worst = max(worst, rel_err(out[row], r.output))
     assert worst < 1e-4, worst
+
+
+@pytest.mark.parametrize("gr", ["4", "8"])
+@pytest.mark.parametrize("group", [1, 4])
+def test_attend128_no_weights_path(ctx, monkeypatch, gr, group):
+    """attend128 (d = 128) as decode_batch runs it: no weights, prefill-only
+    batches on the specialised loop, batches holding appended rows (the recent
+    window keeps them selected) on the mixed loop. Both row-group sizes.
+    Selected sets exact, outputs within 1e-3 of the reference."""
+    monkeypatch.setenv("CSATTN_ATT_GR", gr)
+    P, T, d = 4096, 24, 128
+    q, k, v = workload(P, T, d, seed=81)
+    widths = cs.uniform_widths(d, 8)
+    ic = cs.IndexConfig(alpha=0.2, centroids=32, seed=1, score_bits=32)
+    rc = cs.RetrievalConfig(keep_ratio=0.1)
+    qq = np.concatenate([q[:P]] * group) if group > 1 else q[:P]
+    g = cs.prefill(ctx, qq, k[:P], v[:P], widths, ic, rc, group=group, max_decode_steps=T)
+    r = _checker("ref").prefill(qq, k[:P], v[:P], widths, ic, rc, group)
+    worst = 0.0
+    for t in range(T):
+        Q = np.stack([q[P + t] * (1 + 0.05 * h) for h in range(group)]).astype(np.float32)
+        out, sel = cs.decode_batch([g], Q, k[P + t][None], v[P + t][None])
+        for h, (rs, ro, _, _) in enumerate(r.step(Q, k[P + t], v[P + t])):
+            assert np.array_equal(sel[h, :len(rs)], rs), (t, h)
+            if t > 0:
+                assert (rs >= P).any()  # appended rows are in the set: mixed batches run
+            worst = max(worst, rel_err(out[h], ro))
+    assert worst <= 1e-3, worst
