@@ -72,12 +72,16 @@ static_assert(UNIT_META == NB + NCB + SEL_CW && SEL_CW == 8, "unit metadata layo
 // positions [lo, hi), staged from position `base` (even, 16-byte aligned).
 struct SlotMeta {
     uint32_t info, base, lo, hi;
+    uint32_t wb[SEL_CW + 1];  // table position of consumer warp w's first key: warp w owns [wb[w], wb[w+1])
 };
+static_assert(WKEYS % KEY_BLOCK == 0, "warp key ranges are whole key blocks");
+constexpr uint32_t WBLKS = WKEYS / KEY_BLOCK;  // key blocks per warp range
 
 struct SelHdr {
     unsigned long long full[NSLOT], empty[NSLOT];
     SlotMeta meta[NSLOT];
     uint32_t plist[MAXL];  // producer: table ids of its current problem
+    uint32_t wbs[2][MAXL][SEL_CW + 1];  // producer: per-warp bounds of tiles t, t+1 per list
     double cw[MAXL];       // consumers: weight of each gathered list
     uint32_t cut, nbkt;
     // candidate-log segments of the problem being finalised
@@ -650,12 +654,17 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
         const unsigned long long pol = l2_evict_first_policy();
         uint32_t c = 0;
         auto publish = [&](uint32_t info, uint32_t base, uint32_t lo, uint32_t hi,
-                           const uint2* src, uint32_t bytes) {
+                           const uint2* src, uint32_t bytes, const uint32_t* wb = nullptr) {
             const uint32_t slot = c % NSLOT;
             if (c >= static_cast<uint32_t>(NSLOT))
                 mbar_wait_sleep(&S.empty[slot], ((c / NSLOT) - 1) & 1u);
+            if (wb && ln <= SEL_CW) S.meta[slot].wb[ln] = wb[ln];
+            __syncwarp();  // lane 0's arrive below releases the other lanes' writes too
             if (ln == 0) {
-                S.meta[slot] = SlotMeta{info, base, lo, hi};
+                S.meta[slot].info = info;
+                S.meta[slot].base = base;
+                S.meta[slot].lo = lo;
+                S.meta[slot].hi = hi;
                 if (bytes) {
                     mbar_expect_tx(&S.full[slot], bytes);
                     bulk_g2s_hint(ring + static_cast<size_t>(slot) * SLOT_E, src, bytes,
@@ -694,6 +703,34 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 return kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
                                       : __ldcg(n_used + t);
             };
+            // per-warp key-range bounds of every list in tile `tile` (the
+            // consumer warps own fixed 512-key ranges: no per-list barrier)
+            auto warp_bounds = [&](uint32_t tile) {
+                const uint32_t n = nl * (SEL_CW + 1);
+                uint32_t* const dst = &S.wbs[tile & 1][0][0];
+                for (uint32_t b0_ = 0; b0_ < n; b0_ += 96) {
+                    uint32_t v[3];
+#pragma unroll
+                    for (int u = 0; u < 3; ++u) {
+                        const uint32_t idx = b0_ + u * 32 + ln;
+                        v[u] = 0;
+                        if (idx < n) {
+                            const uint32_t l = idx / (SEL_CW + 1), j = idx - l * (SEL_CW + 1);
+                            const uint32_t t = S.plist[l];
+                            const uint32_t kb = tile * TILE_BLKS + j * WBLKS;
+                            v[u] = kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
+                                                  : __ldcg(n_used + t);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 3; ++u) {
+                        const uint32_t idx = b0_ + u * 32 + ln;
+                        if (idx < n) dst[idx] = v[u];
+                    }
+                }
+                __syncwarp();
+            };
+            if (nl) warp_bounds(tl);
             uint32_t a0 = bound(tl, ln), a1 = bound(tl, ln + 32);
             uint32_t b0 = bound(tl + 1, ln), b1 = bound(tl + 1, ln + 32);
             for (uint32_t tile = tl; tile < ntile; ++tile) {
@@ -720,11 +757,14 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                         const uint32_t ae = (pe + 1) & ~1u;  // <= cap2 (even)
                         const bool last = pe == e1;
                         publish(l | ((last ? lflag : 0u) << 7) | (tile << 10), ab, pos, pe,
-                                tbl + ab, (ae - ab) * 8u);
+                                tbl + ab, (ae - ab) * 8u, &S.wbs[tile & 1][l][0]);
                         if (last) break;
                         pos = pe;
                     }
                 }
+                // next tile's warp bounds (the ring is usually full here, so the
+                // loads overlap the wait for a free slot)
+                if (tile + 1 < ntile) warp_bounds(tile + 1);
                 a0 = b0;
                 a1 = b1;
                 b0 = c0;
@@ -756,18 +796,19 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     const uint2* const ring0 = ring;
     while (kk < nwork) {
         mbar_wait_sleep_u32(full0 + 8 * slot, phase);
-        const SlotMeta M = S.meta[slot];
+        struct {
+            uint32_t info, base, lo, hi;
+        } M = {S.meta[slot].info, S.meta[slot].base, S.meta[slot].lo, S.meta[slot].hi};
         const uint32_t list = M.info & 127u, flags = (M.info >> 7) & 7u, tile = M.info >> 10;
         const uint32_t kbase = tile * TILE;
         if (list != CACHE_LIST) {
-            if (M.hi > M.lo) {
-                // this warp's equal share of the chunk's entry pairs
-                const uint32_t qa = (M.lo - M.base) >> 1, qb = (M.hi - M.base + 1) >> 1;
-                const uint32_t np = qb - qa;
-                const uint32_t q0 = qa + (np * wid) / SEL_CW, q1 = qa + (np * (wid + 1)) / SEL_CW;
+            // this warp's entries: those with keys in its own 512-key range
+            const uint32_t ga = max(M.lo, S.meta[slot].wb[wid]), gb = min(M.hi, S.meta[slot].wb[wid + 1]);
+            if (gb > ga) {
+                const uint32_t plo = ga - M.base, phi = gb - M.base;  // valid [plo, phi)
+                const uint32_t q0 = plo >> 1, q1 = (phi + 1) >> 1;
                 const uint4* st4 = reinterpret_cast<const uint4*>(ring0 + slot * SLOT_E);
                 const double w = S.cw[list];
-                const uint32_t plo = M.lo - M.base, phi = M.hi - M.base;  // valid [plo, phi)
                 // two pairs (four entries) per lane per step, all loads issued
                 // before the adds: keys are unique within a list, so the four
                 // read-modify-writes are independent
@@ -822,8 +863,8 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             slot = 0;
             phase ^= 1u;
         }
-        if (!(flags & F_LIST_END)) continue;
-        cbar();  // the list is fully accumulated before the next one (or the filter)
+        // each warp owns its keys in every tile: lists accumulate in order per
+        // key without a CTA barrier, and the filter reads only the warp's keys
         if (!(flags & F_TILE_END)) continue;
 
         // ---- tile end: this warp's 512 keys -> pool candidates ----
@@ -965,8 +1006,8 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     atomicMax(&S.cut, static_cast<uint32_t>(b));
             }
         }
-        cbar();  // accumulator clear before the next tile's first list
         if (!(flags & F_PROB_END)) continue;
+        cbar();  // every warp's log and histogram counts are in
 
         if (unit_meta) {  // part unit / shard: hand histogram + log lengths on
             uint32_t* const um = unit_meta + static_cast<size_t>(kk) * UNIT_META;
