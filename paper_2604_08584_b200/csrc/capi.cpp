@@ -731,6 +731,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         split = static_cast<uint32_t>(std::min<uint64_t>(std::min<uint64_t>(split, 16), min_tiles));
         split = std::max<uint32_t>(split, 1);
     }
+    if (const char* fs = std::getenv("CSATTN_FORCE_SPLIT")) {  // experiments only
+        split = static_cast<uint32_t>(std::min<uint64_t>(
+            std::max<uint64_t>(std::strtoull(fs, nullptr, 10), 1), std::min<uint64_t>(16, min_tiles)));
+    }
     // retry list of problems whose speculative cut proved too high: [count, ids...]
     ctx->retry.ensure((nq + 1) * 4);
     if (live) ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");

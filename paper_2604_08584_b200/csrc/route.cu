@@ -25,7 +25,8 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     __shared__ float q[DMAX], qn[DMAX];
     __shared__ double csc[MAX_TABLES];
     __shared__ uint32_t ids[MAXM * MAXTAU], nids[MAXM], zero_mask;
-    __shared__ uint32_t lists[MAXL], lsub[MAXL], nl;
+    __shared__ uint32_t lists[MAXL], lsub[MAXL], nl, llive[MAXL];
+    __shared__ double lmin[MAXL], lmax[MAXL];
     const DecodeProblem& P = probs[blockIdx.x];
     if (!(P.mode & MODE_SEARCH)) return;
     const SessionDev& sd = *P.s;
@@ -57,7 +58,20 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
         const uint32_t off = sd.offs[b], w = sd.widths[b];
         const float* c = sd.cent + static_cast<size_t>(C) * off + static_cast<size_t>(j) * w;
         double acc = 0.0;
-        for (uint32_t t = 0; t < w; ++t) acc = __fma_rn((double)qn[off + t], (double)__ldg(c + t), acc);
+        if ((w & 3u) == 0u && ((C * off + j * w) & 3u) == 0u) {  // 16-byte rows: vector loads
+            const float4* c4 = reinterpret_cast<const float4*>(c);
+#pragma unroll 4
+            for (uint32_t t4 = 0; t4 < w / 4; ++t4) {
+                const float4 v = __ldg(c4 + t4);
+                const float* qs = qn + off + 4 * t4;
+                acc = __fma_rn((double)qs[0], (double)v.x, acc);
+                acc = __fma_rn((double)qs[1], (double)v.y, acc);
+                acc = __fma_rn((double)qs[2], (double)v.z, acc);
+                acc = __fma_rn((double)qs[3], (double)v.w, acc);
+            }
+        } else {
+            for (uint32_t t = 0; t < w; ++t) acc = __fma_rn((double)qn[off + t], (double)__ldg(c + t), acc);
+        }
         csc[x] = acc;
     }
     __syncthreads();
@@ -134,15 +148,24 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     // bounds on every accumulated score: a pool key's score is a sum of
     // w_l * score over a non-empty subset of the gathered lists, each score in
     // [tmin_l, tmax_l] (the lists' live score bounds)
+    // the lists' live lengths and score bounds, loaded lane-parallel (one
+    // round trip); the sums below stay sequential in list order
+    if (tid < nl) {
+        const uint32_t t = lists[tid];
+        const uint32_t lv = __ldcg(sd.live_g + t);
+        const float2 mm = __ldcg(sd.tmm + t);
+        const double w = sd.weights[lsub[tid]];
+        lmin[tid] = lv ? w * static_cast<double>(mm.x) : 0.0;
+        lmax[tid] = lv ? w * static_cast<double>(mm.y) : 0.0;
+        llive[tid] = lv;
+    }
+    __syncthreads();
     if (tid == 0) {
         double neg = 0.0, pos = 0.0, amin = DBL_MAX, bmax = -DBL_MAX;
         bool any = false, any_neg = false, any_pos = false;
         for (uint32_t l = 0; l < nl; ++l) {
-            const uint32_t t = lists[l];
-            if (__ldcg(sd.live_g + t) == 0) continue;
-            const float2 mm = __ldcg(sd.tmm + t);
-            const double w = sd.weights[lsub[l]];
-            const double a = w * static_cast<double>(mm.x), b = w * static_cast<double>(mm.y);
+            if (llive[l] == 0) continue;
+            const double a = lmin[l], b = lmax[l];
             any = true;
             if (a < 0.0) { neg += a; any_neg = true; }
             if (b > 0.0) { pos += b; any_pos = true; }
@@ -160,7 +183,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     }
     if (wid == 0) {  // gathered_entries (CostCounters): live lengths of the lists
         uint32_t g = 0;
-        for (uint32_t l = ln; l < nl; l += 32) g += __ldcg(sd.live_g + lists[l]);
+        for (uint32_t l = ln; l < nl; l += 32) g += llive[l];
         for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
         if (ln == 0) {
             Rp->gathered_lo = g;

@@ -30,8 +30,16 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 srows = list(csv.reader(io.StringIO(src)))
 if len(srows) > 3:
     hh = srows[1]
-    data = srows[2:]
     i_s = hh.index("Warp Stall Sampling (All Samples)")
+
+    def _num(x):
+        try:
+            float(x or 0)
+            return True
+        except ValueError:
+            return False
+
+    data = [r for r in srows[2:] if len(r) > i_s and _num(r[i_s])]  # one kernel's rows
     i_src = hh.index("Source")
     tot = sum(float(r[i_s] or 0) for r in data) or 1
     top = sorted(range(len(data)), key=lambda i: -float(data[i][i_s] or 0))[:25]
