@@ -226,8 +226,10 @@ __device__ __forceinline__ float4 ld_row4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
+// GR=4 at 64 registers: 8 CTAs/SM (one 4-byte spill) beat 72 registers / 7 CTAs
+// on this memory-latency-bound loop (c3 277 -> 262 us)
 template <bool PARTIAL, int GR>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
-__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 7 : 5)
+__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 8 : 5)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
                  uint32_t* __restrict__ counters) {
@@ -487,7 +489,7 @@ cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
-    // GR=4 (72 regs, 7 CTAs/SM) for large launches; GR=8 (more rows in flight
+    // GR=4 (64 regs, 8 CTAs/SM) for large launches; GR=8 (more rows in flight
     // per warp) for small ones: c2's 224 chunks 29 -> 23 us, while c4's 832 per
     // layer and c3's 13312 are faster with GR=4. CSATTN_ATT_GR=4|8 forces.
     const int gr_env = std::getenv("CSATTN_ATT_GR") ? std::atoi(std::getenv("CSATTN_ATT_GR")) : 0;

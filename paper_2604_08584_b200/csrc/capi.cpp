@@ -493,10 +493,6 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         fail(CSATTN_ERR_PARAMETER, "selected/weights stride " + std::to_string(sel_stride) +
                                        " is below K = " + std::to_string(maxK));
     const auto hta = std::chrono::steady_clock::now();
-    if (host) {
-        require_finite(keys, ns * d, "appended key");
-        require_finite(values, ns * d, "appended value");
-    }
     const auto htb = std::chrono::steady_clock::now();
     if (maxN > csa::SELECT_MAX_CONTEXT)
         fail(CSATTN_ERR_CAPACITY, "context of " + std::to_string(maxN) +
@@ -523,9 +519,13 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         if (weights) o_w = carve(nq * sel_stride * 4);
         ctx->stage.ensure(total);
         char* base = ctx->stage.as<char>();
+        // copies first (scratch staging: harmless if the scan below refuses),
+        // so the DMA overlaps the scan
         upload(ctx, base + o_q, q, nq * d * 4, true);
         upload(ctx, base + o_k, keys, ns * d * 4, true);
         upload(ctx, base + o_v, values, ns * d * 4, true);
+        require_finite(keys, ns * d, "appended key");
+        require_finite(values, ns * d, "appended value");
         dq = reinterpret_cast<float*>(base + o_q);
         dk = reinterpret_cast<float*>(base + o_k);
         dv = reinterpret_cast<float*>(base + o_v);
@@ -638,15 +638,15 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     const auto htd = std::chrono::steady_clock::now();
     // attention work list: ceil(K / ATT_ROWS) chunk-CTAs per problem
-    std::vector<uint32_t> cbase(nq + 1), cprob;
+    // (cbase = first chunk of each problem; the per-chunk problem ids are written
+    // straight into the pinned slot below)
+    std::vector<uint32_t> cbase(nq + 1);
+    uint64_t nchunks = 0;
     for (uint64_t i = 0; i < nq; ++i) {
-        cbase[i] = static_cast<uint32_t>(cprob.size());
-        if (in_union[i]) continue;
-        const uint64_t nc = (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
-        cprob.insert(cprob.end(), nc, static_cast<uint32_t>(i));
+        cbase[i] = static_cast<uint32_t>(nchunks);
+        if (!in_union[i]) nchunks += (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
     }
-    cbase[nq] = static_cast<uint32_t>(cprob.size());
-    const uint64_t nchunks = cprob.size();
+    cbase[nq] = static_cast<uint32_t>(nchunks);
     if (nq > ctx->counters_n) {
         ctx->counters.alloc(nq * 4);
         ck(cudaMemsetAsync(ctx->counters.p, 0, nq * 4, ctx->stream), "memset");
@@ -687,7 +687,11 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     std::memcpy(hb, ctx->hprobs.data(), dbytes);
     std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
     std::memcpy(hb + boff, cbase.data(), (nq + 1) * 4);
-    std::memcpy(hb + poff, cprob.data(), nchunks * 4);
+    {
+        uint32_t* cp = reinterpret_cast<uint32_t*>(hb + poff);
+        for (uint64_t i = 0; i < nq; ++i)
+            std::fill(cp + cbase[i], cp + cbase[i + 1], static_cast<uint32_t>(i));
+    }
     if (ngroups) {
         std::memcpy(hb + uoff, ugP.data(), ngroups * 4);
         std::memcpy(hb + u_gm, ugmem.data(), ugmem.size() * 4);

@@ -1439,9 +1439,18 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
                           uint32_t split, uint32_t* unit_meta, cudaStream_t st) {
     const size_t smem = select_smem();
-    cudaError_t e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
+    {  // once per device (a host call per launch otherwise)
+        static bool set[64] = {};
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= 64 || !set[dev]) {
+            e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            if (dev >= 0 && dev < 64) set[dev] = true;
+        }
+    }
     select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap,
                                                    retry_in, retry_in_count, retry_out,
                                                    retry_out_count, spec_keep, split, unit_meta);
