@@ -466,14 +466,15 @@ def main():
     t0 = time.perf_counter()
     data = dict(zip(my_heads, gen_heads(cs, my_heads, P + n_layers * n_seq * T + args.cpu_steps)))
     t_gen = time.perf_counter() - t0
-    base_sessions = {}
     t0 = time.perf_counter()
-    for g in my_heads:
-        q, k, v = data[g]
-        pooled = np.ascontiguousarray(np.concatenate([q[:P, r] for r in range(GROUP)]))
-        ic = cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
-        base_sessions[g] = cs.prefill(ctx, pooled, k[:P], v[:P], widths, ic, rc, group=GROUP,
-                                      max_decode_steps=T)
+    # the layer's KV heads in one csattn_prefill_batch (one k-means launch)
+    rows_b = [(np.ascontiguousarray(np.concatenate([data[g][0][:P, r] for r in range(GROUP)])),
+               data[g][1][:P], data[g][2][:P]) for g in my_heads]
+    ics = [cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
+           for g in my_heads]
+    base_sessions = dict(zip(my_heads, cs.prefill_batch(ctx, rows_b, widths, ics, rc, group=GROUP,
+                                                        max_decode_steps=T)))
+    del rows_b
     t_build = time.perf_counter() - t0
     # Session order: layer-major, then KV head, then sequence. Sequence 0 of
     # layer 0 is the prefilled session; every other (layer, sequence) is a fork

@@ -186,6 +186,22 @@ csattn_status csattn_prefill(csattn_ctx ctx, const float* queries, uint64_t n_qu
                              const csattn_index_config* icfg,
                              const csattn_retrieval_config* rcfg, uint64_t group,
                              uint64_t max_decode_steps, uint32_t flags, csattn_session* out);
+/* A layer's prefill: n sessions (one per KV head) with the same layout and
+ * retrieval config, index configs icfgs[0..n) (e.g. per-head seeds), built with
+ * ONE k-means launch of n x m CTAs (one launch per session leaves most SMs
+ * idle). Session i equals csattn_prefill of rows[i] with icfgs[i]. */
+typedef struct {
+    const float* queries; /* n_queries x d */
+    uint64_t n_queries;
+    const float* keys;    /* n_rows x d */
+    const float* values;  /* n_rows x d */
+    uint64_t n_rows;
+} csattn_prefill_rows;
+csattn_status csattn_prefill_batch(csattn_ctx ctx, uint64_t n, const csattn_prefill_rows* rows,
+                                   uint64_t d, const uint64_t* widths, uint64_t m,
+                                   const csattn_index_config* icfgs,
+                                   const csattn_retrieval_config* rcfg, uint64_t group,
+                                   uint64_t max_decode_steps, uint32_t flags, csattn_session* out);
 
 /* build_index_from_centroids (index.cpp:179-202): caller-supplied unit centroid
  * rows, packed per subspace: subspace b holds C x widths[b] floats, subspaces

@@ -32,7 +32,7 @@ __all__ = [
     "Error", "DimensionError", "ParameterError", "DataError", "BadMagicError", "VersionError",
     "TruncatedError", "CorruptError", "PropertyError", "StreamExhaustedError", "CudaError",
     "CapacityError", "IndexConfig", "RetrievalConfig", "SyntheticSpec", "CostCounters",
-    "DecodeStepReport", "Context", "Session", "prefill", "prefill_from_centroids",
+    "DecodeStepReport", "Context", "Session", "prefill", "prefill_batch", "prefill_from_centroids",
     "import_index", "run_decode", "keep_count", "parse_schedule", "h2d_bytes", "make_synthetic",
     "uniform_widths", "lib",
 ]
@@ -524,6 +524,35 @@ def prefill(ctx: Context, queries, keys, values, widths, index_cfg: IndexConfig,
                                 C.byref(ic), C.byref(rc), group, max_decode_steps,
                                 _abi.HOST_BUFFERS if qh else 0, C.byref(h)))
     return Session(ctx, h)
+
+
+def prefill_batch(ctx: Context, rows, widths, index_cfg, cfg: RetrievalConfig,
+                  group: int = 1, max_decode_steps: int = 1024) -> list[Session]:
+    """A layer's prefill (csattn_prefill_batch): rows = [(queries, keys, values), ...]
+    as host arrays, one entry per KV head; index_cfg is one IndexConfig or one per
+    entry. One k-means launch for all of them; session i equals
+    prefill(ctx, *rows[i], widths, index_cfg[i], ...)."""
+    cfgs = list(index_cfg) if isinstance(index_cfg, (list, tuple)) else [index_cfg] * len(rows)
+    if len(cfgs) != len(rows):
+        raise ParameterError("one index config per prefill entry")
+    d = sum(widths)
+    keep, arr = [], (_abi.PrefillRowsC * len(rows))()
+    for i, (q, k, v) in enumerate(rows):
+        q, k, v = _f32(q), _f32(k), _f32(v)
+        if d == 0 or q.size % d or k.size % d:
+            raise DimensionError("prefill rows are not a multiple of d")
+        if v.size != k.size:
+            raise DimensionError("prefill key/value counts differ")
+        keep += [q, k, v]
+        arr[i] = _abi.PrefillRowsC(q.ctypes.data, q.size // d, k.ctypes.data, v.ctypes.data,
+                                   k.size // d)
+    ics = (_abi.IndexConfigC * len(rows))(*[c.c() for c in cfgs])
+    rc, w = cfg.c()
+    hs = (C.c_void_p * len(rows))()
+    _check(lib().csattn_prefill_batch(ctx.h, len(rows), arr, d, _widths_arr(widths), len(widths),
+                                      ics, C.byref(rc), group, max_decode_steps,
+                                      _abi.HOST_BUFFERS, hs))
+    return [Session(ctx, C.c_void_p(h)) for h in hs]
 
 
 def prefill_from_centroids(ctx: Context, centroids, keys, values, widths,

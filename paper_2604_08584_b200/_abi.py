@@ -22,6 +22,11 @@ STATUS_NAMES = {
 }
 
 
+class PrefillRowsC(C.Structure):
+    _fields_ = [("queries", C.c_void_p), ("n_queries", C.c_uint64), ("keys", C.c_void_p),
+                ("values", C.c_void_p), ("n_rows", C.c_uint64)]
+
+
 class IndexConfigC(C.Structure):
     _fields_ = [("alpha", C.c_double), ("list_capacity", C.c_uint64),
                 ("normalize_keys", C.c_int32), ("score_bits", C.c_int32),
@@ -107,6 +112,8 @@ SIGNATURES = {
     "csattn_ctx_profile_read": (C.c_int, [vp, P(C.c_double), P(u64), i32]),
     "csattn_prefill": (C.c_int, [vp, vp, u64, vp, vp, u64, u64, P(u64), u64, P(IndexConfigC),
                                  P(RetrievalConfigC), u64, u64, u32, P(vp)]),
+    "csattn_prefill_batch": (C.c_int, [vp, u64, P(PrefillRowsC), u64, P(u64), u64, P(IndexConfigC),
+                                       P(RetrievalConfigC), u64, u64, u32, P(vp)]),
     "csattn_prefill_from_centroids": (C.c_int, [vp, vp, u64, vp, vp, u64, u64, P(u64), u64,
                                                 P(IndexConfigC), P(RetrievalConfigC), u64, u64,
                                                 u32, P(vp)]),

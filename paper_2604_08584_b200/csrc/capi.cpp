@@ -1295,110 +1295,171 @@ csattn_status csattn_ctx_profile_read(csattn_ctx ctx, double* ms, uint64_t* step
 }
 
 // prefill (session.cpp:25-44) -> build_index (index.cpp:145-177) on the GPU.
+}  // extern "C"
+
+namespace {
+
+// One session's prefill (prefill, session.cpp:25-44): validation, session,
+// rows and the per-subspace k-means jobs (setup), then the status check and
+// the table build (finish). csattn_prefill runs one; csattn_prefill_batch runs
+// a layer's sessions with ONE k-means launch of n x m CTAs (the jobs, and so
+// the tables, are identical to n single prefills).
+struct PrefillWork {
+    std::unique_ptr<csattn_session_s> s;
+    DevMem dq, drng, train, best, run, assign, sums, counts, status, info;
+    std::vector<csa::KmeansJob> hj;
+    bool full_batch = false;
+};
+
+void prefill_setup(PrefillWork& W, csattn_ctx ctx, const float* queries, uint64_t nq,
+                   const float* keys, const float* values, uint64_t p, uint64_t d,
+                   const uint64_t* widths, uint64_t m, const csattn_index_config* icfg,
+                   const csattn_retrieval_config* rcfg, uint64_t group, uint64_t max_steps,
+                   bool host) {
+    validate_layout(widths, m, d);
+    if (nq == 0) fail(CSATTN_ERR_PARAMETER, "prefill must be non-empty");
+    validate_retrieval(rcfg, m);
+    check_rows(keys, values, p, d, host);
+    validate_index(icfg);
+    if (p == 0) fail(CSATTN_ERR_PARAMETER, "cannot build over an empty prefill");
+    const uint64_t C = icfg->centroids;
+    for (uint64_t b = 0; b < m; ++b)
+        if (C * widths[b] > csa::KM_MAX_KW)
+            fail(CSATTN_ERR_PARAMETER, "B200 build supports C * width <= " +
+                                           std::to_string(csa::KM_MAX_KW));
+    if (nq >= 0x7fffffffull) fail(CSATTN_ERR_PARAMETER, "too many query rows");
+    double alpha;
+    const uint64_t L = list_capacity_of(icfg, p, &alpha);
+    W.s = new_session(ctx, d, widths, m, C, L, p, group, max_steps, rcfg);
+    csattn_session_s* s = W.s.get();
+    s->alpha = alpha;
+    s->h.normalize_keys = icfg->normalize_keys ? 1u : 0u;
+    s->score_bits = icfg->score_bits;
+    attach_rows(s, keys, values, host);
+    cudaStream_t st = ctx->stream;
+    // ---- per-subspace exact k-means, one CTA per subspace ----
+    W.dq.alloc(nq * d * sizeof(float));
+    upload(ctx, W.dq.p, queries, nq * d * sizeof(float), host);
+    const uint32_t iters = static_cast<uint32_t>(icfg->iterations);
+    const uint32_t bcfg = static_cast<uint32_t>(std::min<uint64_t>(icfg->batch_size, 0xffffffffu));
+    const size_t ndraw = csa::kmeans_rng_draws(static_cast<uint32_t>(C), iters,
+                                               static_cast<uint32_t>(nq), bcfg);
+    std::vector<unsigned long long> draws(m * ndraw);
+    for (uint64_t b = 0; b < m; ++b) {
+        // cc.seed = mix_seed(seed, b) (index.cpp:170); Rng = mt19937_64
+        uint64_t z = icfg->seed + 0x9e3779b97f4a7c15ULL * (b + 1);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        std::mt19937_64 gen(z ^ (z >> 31));
+        for (size_t i = 0; i < ndraw; ++i) draws[b * ndraw + i] = gen();
+    }
+    W.drng.alloc(draws.size() * 8);
+    // synchronous: `draws` is a host temporary
+    ck(cudaMemcpyAsync(W.drng.p, draws.data(), draws.size() * 8, cudaMemcpyDefault, st), "copy in");
+    ck(cudaStreamSynchronize(st), "rng upload");
+    uint64_t wsum = 0;
+    for (uint64_t b = 0; b < m; ++b) wsum += widths[b];
+    W.train.alloc(nq * wsum * sizeof(float));
+    W.best.alloc(m * nq * sizeof(double));
+    W.run.alloc(m * nq * sizeof(double));
+    W.assign.alloc(m * 2 * nq * sizeof(uint32_t));
+    W.sums.alloc(C * wsum * sizeof(double));
+    W.counts.alloc(m * C * sizeof(uint32_t));
+    W.status.alloc(m * sizeof(int));
+    W.info.alloc(m * 2 * sizeof(uint32_t));
+    ck(cudaMemsetAsync(W.status.p, 0, m * sizeof(int), st), "memset");
+    ck(cudaMemsetAsync(W.info.p, 0, m * 2 * sizeof(uint32_t), st), "memset");
+    W.hj.resize(m);
+    for (uint64_t b = 0; b < m; ++b) {
+        csa::KmeansJob& J = W.hj[b];
+        const uint32_t off = s->h.offs[b];
+        J.q = W.dq.as<float>();
+        J.n_total = static_cast<uint32_t>(nq);
+        J.d = static_cast<uint32_t>(d);
+        J.off = off;
+        J.w = static_cast<uint32_t>(widths[b]);
+        J.k = static_cast<uint32_t>(C);
+        J.iters = iters;
+        J.batch_cfg = bcfg;
+        J.pad = 0;
+        J.tol = icfg->tolerance;
+        J.rng = W.drng.as<unsigned long long>() + b * ndraw;
+        J.train = W.train.as<float>() + nq * off;
+        J.best = W.best.as<double>() + b * nq;
+        J.run = W.run.as<double>() + b * nq;
+        J.assign = W.assign.as<uint32_t>() + b * 2 * nq;
+        J.sums = W.sums.as<double>() + C * off;
+        J.counts = W.counts.as<uint32_t>() + b * C;
+        J.cent = s->cent.as<float>() + C * off;
+        J.status = W.status.as<int>() + b;
+        J.info = W.info.as<uint32_t>() + 2 * b;
+    }
+    const uint64_t bt = bcfg == 0 ? std::min<uint64_t>(4096, nq) : std::min<uint64_t>(bcfg, nq);
+    W.full_batch = bt >= nq;
+}
+
+// one k-means launch over every job of `works`, then each session's checks + build
+void prefill_run(csattn_ctx ctx, std::vector<PrefillWork>& works) {
+    cudaStream_t st = ctx->stream;
+    std::vector<csa::KmeansJob> all;
+    for (auto& W : works) all.insert(all.end(), W.hj.begin(), W.hj.end());
+    DevMem jobs;
+    jobs.alloc(all.size() * sizeof(csa::KmeansJob));
+    upload(ctx, jobs.p, all.data(), all.size() * sizeof(csa::KmeansJob), true);
+    ck(csa::launch_kmeans(jobs.as<csa::KmeansJob>(), static_cast<uint32_t>(all.size()), st),
+       "kmeans launch");
+    ctx->launches += 1;
+    std::vector<std::vector<int>> hs(works.size());
+    for (size_t i = 0; i < works.size(); ++i) {
+        hs[i].resize(works[i].hj.size());
+        ck(cudaMemcpyAsync(hs[i].data(), works[i].status.p, hs[i].size() * sizeof(int),
+                           cudaMemcpyDeviceToHost, st),
+           "status");
+    }
+    ck(cudaStreamSynchronize(st), "kmeans");
+    for (size_t i = 0; i < works.size(); ++i)
+        for (int v : hs[i]) {
+            if (v == 4) fail(CSATTN_ERR_DATA, "every training row is zero");
+            if (v == 9)
+                fail(CSATTN_ERR_PROPERTY, works[i].full_batch
+                                              ? "clustering objective increased in a full-batch iteration"
+                                              : "mini-batch clustering objective diverged");
+        }
+    for (auto& W : works) build_tables(W.s.get());
+}
+
+}  // namespace
+
+extern "C" {
+
 csattn_status csattn_prefill(csattn_ctx ctx, const float* queries, uint64_t nq, const float* keys,
                              const float* values, uint64_t p, uint64_t d, const uint64_t* widths,
                              uint64_t m, const csattn_index_config* icfg,
                              const csattn_retrieval_config* rcfg, uint64_t group,
                              uint64_t max_steps, uint32_t flags, csattn_session* out) {
     return guard([&] {
-        const bool host = flags & CSATTN_HOST_BUFFERS;
-        validate_layout(widths, m, d);
-        if (nq == 0) fail(CSATTN_ERR_PARAMETER, "prefill must be non-empty");
-        validate_retrieval(rcfg, m);
-        check_rows(keys, values, p, d, host);
-        validate_index(icfg);
-        if (p == 0) fail(CSATTN_ERR_PARAMETER, "cannot build over an empty prefill");
-        const uint64_t C = icfg->centroids;
-        for (uint64_t b = 0; b < m; ++b)
-            if (C * widths[b] > csa::KM_MAX_KW)
-                fail(CSATTN_ERR_PARAMETER, "B200 build supports C * width <= " +
-                                               std::to_string(csa::KM_MAX_KW));
-        if (nq >= 0x7fffffffull) fail(CSATTN_ERR_PARAMETER, "too many query rows");
-        double alpha;
-        const uint64_t L = list_capacity_of(icfg, p, &alpha);
-        auto s = new_session(ctx, d, widths, m, C, L, p, group, max_steps, rcfg);
-        s->alpha = alpha;
-        s->h.normalize_keys = icfg->normalize_keys ? 1u : 0u;
-        s->score_bits = icfg->score_bits;
-        attach_rows(s.get(), keys, values, host);
-        cudaStream_t st = ctx->stream;
-        // ---- per-subspace exact k-means, one CTA per subspace ----
-        DevMem dq;
-        dq.alloc(nq * d * sizeof(float));
-        upload(ctx, dq.p, queries, nq * d * sizeof(float), host);
-        const uint32_t iters = static_cast<uint32_t>(icfg->iterations);
-        const uint32_t bcfg = static_cast<uint32_t>(std::min<uint64_t>(icfg->batch_size, 0xffffffffu));
-        const size_t ndraw = csa::kmeans_rng_draws(static_cast<uint32_t>(C), iters,
-                                                   static_cast<uint32_t>(nq), bcfg);
-        std::vector<unsigned long long> draws(m * ndraw);
-        for (uint64_t b = 0; b < m; ++b) {
-            // cc.seed = mix_seed(seed, b) (index.cpp:170); Rng = mt19937_64
-            uint64_t z = icfg->seed + 0x9e3779b97f4a7c15ULL * (b + 1);
-            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-            std::mt19937_64 gen(z ^ (z >> 31));
-            for (size_t i = 0; i < ndraw; ++i) draws[b * ndraw + i] = gen();
-        }
-        DevMem drng, train, best, run, assign, sums, counts, status, info, jobs;
-        drng.alloc(draws.size() * 8);
-        upload(ctx, drng.p, draws.data(), draws.size() * 8, true);
-        uint64_t wsum = 0;
-        for (uint64_t b = 0; b < m; ++b) wsum += widths[b];
-        train.alloc(nq * wsum * sizeof(float));
-        best.alloc(m * nq * sizeof(double));
-        run.alloc(m * nq * sizeof(double));
-        assign.alloc(m * 2 * nq * sizeof(uint32_t));
-        sums.alloc(C * wsum * sizeof(double));
-        counts.alloc(m * C * sizeof(uint32_t));
-        status.alloc(m * sizeof(int));
-        info.alloc(m * 2 * sizeof(uint32_t));
-        ck(cudaMemsetAsync(status.p, 0, m * sizeof(int), st), "memset");
-        ck(cudaMemsetAsync(info.p, 0, m * 2 * sizeof(uint32_t), st), "memset");
-        std::vector<csa::KmeansJob> hj(m);
-        for (uint64_t b = 0; b < m; ++b) {
-            csa::KmeansJob& J = hj[b];
-            const uint32_t off = s->h.offs[b];
-            J.q = dq.as<float>();
-            J.n_total = static_cast<uint32_t>(nq);
-            J.d = static_cast<uint32_t>(d);
-            J.off = off;
-            J.w = static_cast<uint32_t>(widths[b]);
-            J.k = static_cast<uint32_t>(C);
-            J.iters = iters;
-            J.batch_cfg = bcfg;
-            J.pad = 0;
-            J.tol = icfg->tolerance;
-            J.rng = drng.as<unsigned long long>() + b * ndraw;
-            J.train = train.as<float>() + nq * off;
-            J.best = best.as<double>() + b * nq;
-            J.run = run.as<double>() + b * nq;
-            J.assign = assign.as<uint32_t>() + b * 2 * nq;
-            J.sums = sums.as<double>() + C * off;
-            J.counts = counts.as<uint32_t>() + b * C;
-            J.cent = s->cent.as<float>() + C * off;
-            J.status = status.as<int>() + b;
-            J.info = info.as<uint32_t>() + 2 * b;
-        }
-        jobs.alloc(m * sizeof(csa::KmeansJob));
-        upload(ctx, jobs.p, hj.data(), m * sizeof(csa::KmeansJob), true);
-        ck(csa::launch_kmeans(jobs.as<csa::KmeansJob>(), static_cast<uint32_t>(m), st), "kmeans launch");
-        ctx->launches += 1;
-        std::vector<int> hs(m);
-        ck(cudaMemcpyAsync(hs.data(), status.p, m * sizeof(int), cudaMemcpyDeviceToHost, st), "status");
-        ck(cudaStreamSynchronize(st), "kmeans");
-        const bool full_batch = [&] {
-            const uint64_t bt = bcfg == 0 ? std::min<uint64_t>(4096, nq) : std::min<uint64_t>(bcfg, nq);
-            return bt >= nq;
-        }();
-        for (uint64_t b = 0; b < m; ++b) {
-            if (hs[b] == 4) fail(CSATTN_ERR_DATA, "every training row is zero");
-            if (hs[b] == 9)
-                fail(CSATTN_ERR_PROPERTY, full_batch
-                                              ? "clustering objective increased in a full-batch iteration"
-                                              : "mini-batch clustering objective diverged");
-        }
-        build_tables(s.get());
-        *out = s.release();
+        std::vector<PrefillWork> works(1);
+        prefill_setup(works[0], ctx, queries, nq, keys, values, p, d, widths, m, icfg, rcfg, group,
+                      max_steps, flags & CSATTN_HOST_BUFFERS);
+        prefill_run(ctx, works);
+        *out = works[0].s.release();
+    });
+}
+
+csattn_status csattn_prefill_batch(csattn_ctx ctx, uint64_t n, const csattn_prefill_rows* rows,
+                                   uint64_t d, const uint64_t* widths, uint64_t m,
+                                   const csattn_index_config* icfgs,
+                                   const csattn_retrieval_config* rcfg, uint64_t group,
+                                   uint64_t max_steps, uint32_t flags, csattn_session* out) {
+    return guard([&] {
+        if (n == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
+        std::vector<PrefillWork> works(n);
+        for (uint64_t i = 0; i < n; ++i)
+            prefill_setup(works[i], ctx, rows[i].queries, rows[i].n_queries, rows[i].keys,
+                          rows[i].values, rows[i].n_rows, d, widths, m, icfgs + i, rcfg, group, max_steps,
+                          flags & CSATTN_HOST_BUFFERS);
+        prefill_run(ctx, works);
+        for (uint64_t i = 0; i < n; ++i) out[i] = works[i].s.release();
     });
 }
 

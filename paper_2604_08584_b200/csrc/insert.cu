@@ -116,7 +116,20 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
         double s = 0.0;
         if (!(S.zero_mask & (1u << b))) {
             const float* c = sd.cent + static_cast<size_t>(C) * off + static_cast<size_t>(j) * w;
-            for (uint32_t x = 0; x < w; ++x) s = __fma_rn((double)__ldg(c + x), (double)S.ks[off + x], s);
+            if ((w & 3u) == 0u && ((C * off + j * w) & 3u) == 0u) {  // 16-byte rows: vector loads
+                const float4* c4 = reinterpret_cast<const float4*>(c);
+#pragma unroll 4
+                for (uint32_t x4 = 0; x4 < w / 4; ++x4) {
+                    const float4 v = __ldg(c4 + x4);
+                    const float* ks = S.ks + off + 4 * x4;
+                    s = __fma_rn((double)v.x, (double)ks[0], s);
+                    s = __fma_rn((double)v.y, (double)ks[1], s);
+                    s = __fma_rn((double)v.z, (double)ks[2], s);
+                    s = __fma_rn((double)v.w, (double)ks[3], s);
+                }
+            } else {
+                for (uint32_t x = 0; x < w; ++x) s = __fma_rn((double)__ldg(c + x), (double)S.ks[off + x], s);
+            }
         }
         const float sc = __double2float_rn(s);
         uint32_t nu = sd.n_used[t];

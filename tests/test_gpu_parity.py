@@ -387,3 +387,32 @@ def test_attend128_no_weights_path(ctx, monkeypatch, gr, group):
                 assert (rs >= P).any()  # appended rows are in the set: mixed batches run
             worst = max(worst, rel_err(out[h], ro))
     assert worst <= 1e-3, worst
+
+
+def test_prefill_batch_equals_single_prefills(ctx):
+    """csattn_prefill_batch (one k-means launch for a layer's KV heads, per-head
+    seeds) builds exactly the sessions n single prefills build: centroids and
+    tables bit-identical, and the first decode step selects the same keys."""
+    P, d, grp = 3072, 64, 2
+    widths = cs.uniform_widths(d, 8)
+    rc = cs.RetrievalConfig()
+    rows, ics = [], []
+    for h in range(3):
+        q, k, v = workload(P, 2, d, seed=90 + h)
+        rows.append((np.concatenate([q[:P]] * grp), k[:P], v[:P]))
+        ics.append(cs.IndexConfig(alpha=0.2, centroids=16, seed=7 + h, score_bits=32))
+    batch = cs.prefill_batch(ctx, rows, widths, ics, rc, group=grp, max_decode_steps=2)
+    for (qq, k, v), ic, b in zip(rows, ics, batch):
+        single = cs.prefill(ctx, qq, k, v, widths, ic, rc, group=grp, max_decode_steps=2)
+        ea, eb = b.export_index(), single.export_index()
+        assert np.array_equal(ea[3], eb[3]), "centroids differ"
+        assert tables_equal(ea, eb)
+        Q = np.stack([qq[5], qq[P + 9]]).astype(np.float32)
+        ra = b.decode_step(Q, k[1], v[1])
+        rb = single.decode_step(Q, k[1], v[1])
+        for x, y in zip(ra, rb):
+            assert np.array_equal(x.selected, y.selected)
+    # an all-zero training set in one entry refuses the whole batch
+    bad = [rows[0], (np.zeros_like(rows[1][0]), rows[1][1], rows[1][2])]
+    with pytest.raises(cs.DataError):
+        cs.prefill_batch(ctx, bad, widths, ics[:2], rc, group=grp)
