@@ -215,7 +215,7 @@ struct csattn_ctx_s {
     int num_sms = 148;
     // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
     // retry pass — used by the tests to exercise it)
-    double spec_keep = std::getenv("CSATTN_SPEC_KEEP") ? std::atof(std::getenv("CSATTN_SPEC_KEEP")) : 0.7;
+    double spec_keep = std::getenv("CSATTN_SPEC_KEEP") ? std::atof(std::getenv("CSATTN_SPEC_KEEP")) : 0.9;
     uint64_t counters_n = 0;
     // select-kernel phase timestamps (env CSATTN_PHASE_PROF=1; diagnostics only)
     bool phase_prof = std::getenv("CSATTN_PHASE_PROF") != nullptr;

@@ -1,26 +1,28 @@
 // select.cu — CSAttention decode, part 1: gather + accumulate + top-K on sm_100a.
 //
-// Persistent kernel, one 544-thread CTA per SM; CTA b takes problems
+// Persistent kernel, two 288-thread CTAs per SM; CTA b takes problems
 // b, b + grid, ... (a problem = one (session, query head) decode search).
 //
 //   producer warp   streams the gathered lists (route.cu's plan) tile by tile:
-//                   for each 8192-key tile and each list, the list's entries
+//                   for each 4096-key tile and each list, the list's entries
 //                   with keys in the tile ([blk_off(tile), blk_off(tile+1)),
 //                   the tables are index-sorted) are copied by TMA bulk copies
 //                   (cp.async.bulk, L2 evict_first, mbarrier complete_tx) into
-//                   a 7-slot ring. It runs ahead across tile and problem
+//                   a 6-slot ring. It runs ahead across tile and problem
 //                   boundaries, so the next problem's lists are in flight while
 //                   the current one is being selected.
-//   16 consumer     accumulate list by list in gathered-list order (the
+//   8 consumer      accumulate list by list in gathered-list order (the
 //   warps           reference's per-key order [gather_lists :95-109,
-//                   reduce_by_key :111-148]): each warp takes an equal slice of
-//                   the list's segment (keys are unique within a list, so the
-//                   fp64 shared-memory RMWs never collide) and a named barrier
-//                   separates lists: score(i) = sum_l w_b(l) * double(score_l(i)).
+//                   reduce_by_key :111-148]): warp w owns keys [512w, 512w+512)
+//                   of every tile and takes, from each list's segment, exactly
+//                   the entries in its range (bounds from blk_off, passed by the
+//                   producer in the slot metadata), so no two warps touch a key
+//                   and no CTA barrier separates lists:
+//                   score(i) = sum_l w_b(l) * double(score_l(i)).
 //                   At the end of a tile each warp turns its 512 keys into pool
 //                   candidates [select_topk :150-228 pool rules]: a cheap
 //                   compare against the current cut compacts the survivors in
-//                   place, then only those are binned into a 4096-bin linear
+//                   place, then only those are binned into a 2048-bin linear
 //                   histogram fixed up front by route.cu's score bounds (a
 //                   monotone map, so bins never split equal scores) and
 //                   appended to the warp's candidate log. The cut is the highest
@@ -332,7 +334,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // consumer warps: load problem p's descriptor, list weights, score bounds
 // Speculation: the previous search's threshold score t of this (session, head)
-// seeds the cut at lo + spec_keep * (t - lo) (spec_keep = 0.7 by default,
+// seeds the cut at lo + spec_keep * (t - lo) (spec_keep = 0.9 by default,
 // 0 disables). The final phase verifies that the threshold bin is at or above
 // it; otherwise the problem is redone without speculation by the retry pass,
 // so the result never depends on the guess.
