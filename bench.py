@@ -291,13 +291,14 @@ def run_c5(args, config, P, rank, world, local):
     t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     full = []
-    for g in heads:
-        q, k, v = data[g]
-        pooled = np.ascontiguousarray(np.concatenate([q[:P, r] for r in range(GROUP)]))
-        ic = cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
-        full.append(cs.prefill(ctxs[0], pooled, k[:P], v[:P], widths, ic, rc, group=GROUP,
-                               max_decode_steps=1))
-        del pooled
+    for g0 in range(0, len(heads), 4):  # 4 heads per csattn_prefill_batch (host RAM: pooled queries)
+        hb = heads[g0:g0 + 4]
+        rows_b = [(np.ascontiguousarray(np.concatenate([data[g][0][:P, r] for r in range(GROUP)])),
+                   data[g][1][:P], data[g][2][:P]) for g in hb]
+        ics = [cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
+               for g in hb]
+        full += cs.prefill_batch(ctxs[0], rows_b, widths, ics, rc, group=GROUP, max_decode_steps=1)
+        del rows_b
     t_build = time.perf_counter() - t0
     if world == 1:
         grp = ShardGroup.local(ctxs, full, max_decode_steps=T)
