@@ -441,7 +441,9 @@ csattn_status csattn_shard_buffer_words(csattn_session shard, uint64_t* hist_wor
                                         uint64_t* bucket_words, uint64_t* partial_floats,
                                         uint64_t* victim_words);
 /* One phase of a sharded decode step for n shard sessions of this shard
- * (one per KV head, groups as in csattn_decode_batch). */
+ * (one per KV head, groups as in csattn_decode_batch). Phases are enqueued on
+ * the context's stream and never synchronize it: the collectives between
+ * phases must run on (or be ordered with) that stream. */
 csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t n, const csattn_session* shards,
                                 int32_t phase, const csattn_shard_io* io);
 

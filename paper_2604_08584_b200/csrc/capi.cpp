@@ -1941,7 +1941,9 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                     s->step += 1;
                 }
                 ctx->sh_scanned = false;
-                ck(cudaStreamSynchronize(st), "shard step");
+                // no stream sync: the next step's descriptor copies are stream-
+                // ordered after these kernels (pageable sources are staged before
+                // cudaMemcpyAsync returns), and the collectives run on this stream
                 break;
             default:
                 fail(CSATTN_ERR_PARAMETER, "unknown shard phase");

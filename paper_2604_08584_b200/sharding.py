@@ -247,11 +247,24 @@ class ShardGroup:
             coll_all_reduce_min_u64([bb[key] for bb in bufs], self.dist)
 
         A = self._abi
+        import os
+        prof = os.environ.get("CSATTN_SHARD_PROF")  # diagnostics: per-phase CUDA events
+        marks = []
+
+        def mark(name):
+            if prof:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(torch.cuda.current_stream(dev))
+                marks.append((name, e))
+        mark("start")
         for bb in bufs:
             bb["fail"].zero_()
         run(A.SHARD_SCAN)
+        mark("scan")
         all_reduce_sum("ghist")
+        mark("ghist")
         run(A.SHARD_BUCKET)
+        mark("bucket")
         # the speculative cut (previous step's threshold) missed on some query
         # head: every shard saw the same global histogram; rescan without it
         fail = torch.stack([bb["fail"] for bb in bufs]).max()
@@ -264,15 +277,32 @@ class ShardGroup:
             run(A.SHARD_RESCAN)
             all_reduce_sum("ghist")
             run(A.SHARD_BUCKET)
+        mark("fail-check")
         all_gather("bucket", "bucket_all")
         run(A.SHARD_MARK)
+        mark("mark")
         all_gather("counts", "counts_all")
         run(A.SHARD_EMIT)
+        mark("emit")
         all_gather("partial", "partial_all")
         run(A.SHARD_MERGE)
+        mark("merge")
         run(A.SHARD_VICTIM)
         all_reduce_min_u64("victim")
         run(A.SHARD_INSERT)
+        mark("insert")
+        if prof:
+            marks[-1][1].synchronize()
+            acc = getattr(self, "_prof", {})
+            for (_, a), (n, b) in zip(marks, marks[1:]):
+                acc[n] = acc.get(n, 0.0) + a.elapsed_time(b)
+            acc["_steps"] = acc.get("_steps", 0) + 1
+            self._prof = acc
+            if acc["_steps"] % 8 == 0:
+                import sys
+                print("[shard prof] ms/step: " + ", ".join(
+                    f"{k} {v / acc['_steps']:.3f}" for k, v in acc.items() if k != "_steps"),
+                    file=sys.stderr)
         out = bufs[0]["out"]
         if not want_selected:
             return out, None
