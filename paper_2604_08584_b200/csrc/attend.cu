@@ -59,7 +59,7 @@ template <int NC, int VEC>
 __global__ void __launch_bounds__(ATT_THREADS)
 attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
               const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
-              uint32_t* __restrict__ counters) {
+              uint32_t* __restrict__ counters, uint32_t rows) {
     __shared__ float wm[ATT_WARPS], ws[ATT_WARPS];
     __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
     __shared__ uint32_t is_last;
@@ -71,8 +71,8 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const uint32_t rw = j * ATT_ROWS + w * (ATT_ROWS / ATT_WARPS);  // this warp's first row
-    const uint32_t nrw = rw < K ? min(ATT_ROWS / ATT_WARPS, K - rw) : 0u;
+    const uint32_t rw = j * rows + w * (rows / ATT_WARPS);  // this warp's first row
+    const uint32_t nrw = rw < K ? min(rows / ATT_WARPS, K - rw) : 0u;
     const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
 
     float q[NC][VEC];
@@ -232,7 +232,7 @@ template <bool PARTIAL, int GR>  // PARTIAL: sharded steps write (max, sum, acc[
 __global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 8 : 5)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
-                 uint32_t* __restrict__ counters) {
+                 uint32_t* __restrict__ counters, uint32_t rows) {
     constexpr int NC = 1, VEC = 4;
     __shared__ float wm[ATT_WARPS], ws[ATT_WARPS];
     __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
@@ -245,8 +245,8 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const uint32_t j = c - chunk_base[p];
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const uint32_t rw = j * ATT_ROWS + w * (ATT_ROWS / ATT_WARPS);  // this warp's first row
-    const uint32_t nrw = rw < K ? min(ATT_ROWS / ATT_WARPS, K - rw) : 0u;
+    const uint32_t rw = j * rows + w * (rows / ATT_WARPS);  // this warp's first row
+    const uint32_t nrw = rw < K ? min(rows / ATT_WARPS, K - rw) : 0u;
     const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
     const float* const kpre = sd.kpre;
     const float* const vpre = sd.vpre;
@@ -486,20 +486,21 @@ cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t npr
 
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
-                          uint32_t* counters, uint32_t d, cudaStream_t st, bool partial) {
+                          uint32_t* counters, uint32_t d, cudaStream_t st, bool partial,
+                          uint32_t rows) {
 #define CSA_ATT(NC, VEC) \
-    attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters)
+    attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows)
     // GR=4 (64 regs, 8 CTAs/SM) for large launches; GR=8 (more rows in flight
     // per warp) for small ones: c2's 224 chunks 29 -> 23 us, while c4's 832 per
     // layer and c3's 13312 are faster with GR=4. CSATTN_ATT_GR=4|8 forces.
     const int gr_env = std::getenv("CSATTN_ATT_GR") ? std::atoi(std::getenv("CSATTN_ATT_GR")) : 0;
     const int gr = gr_env == 4 || gr_env == 8 ? gr_env : (nchunks < 148u * 3u ? 8 : 4);
     if (d == 128 && partial) {
-        if (gr == 4) attend128_kernel<true, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
-        else attend128_kernel<true, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+        if (gr == 4) attend128_kernel<true, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
+        else attend128_kernel<true, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
     } else if (d == 128) {
-        if (gr == 4) attend128_kernel<false, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
-        else attend128_kernel<false, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters);
+        if (gr == 4) attend128_kernel<false, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
+        else attend128_kernel<false, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
     } else if (d % 4 == 0) {
         if (d <= 128) CSA_ATT(1, 4);
         else if (d <= 256) CSA_ATT(2, 4);

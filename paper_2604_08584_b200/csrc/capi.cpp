@@ -641,10 +641,16 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     // (cbase = first chunk of each problem; the per-chunk problem ids are written
     // straight into the pinned slot below)
     std::vector<uint32_t> cbase(nq + 1);
+    uint64_t n256 = 0;
+    for (uint64_t i = 0; i < nq; ++i)
+        if (!in_union[i]) n256 += (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
+    uint32_t arows = csa::attend_rows(n256);  // c3: 512 (attend 262 -> 251 us)
+    if (const char* ar = std::getenv("CSATTN_ATT_ROWS"))  // tests: force 256 / 512
+        arows = std::atoi(ar) == 512 ? csa::ATT_ROWS_BIG : csa::ATT_ROWS;
     uint64_t nchunks = 0;
     for (uint64_t i = 0; i < nq; ++i) {
         cbase[i] = static_cast<uint32_t>(nchunks);
-        if (!in_union[i]) nchunks += (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
+        if (!in_union[i]) nchunks += (Ks[i] + arows - 1) / arows;
     }
     cbase[nq] = static_cast<uint32_t>(nchunks);
     if (nq > ctx->counters_n) {
@@ -797,7 +803,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     if (nchunks && live)
         ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
-                              ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream),
+                              ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream,
+                              false, arows),
            "attend launch");
     if (ngroups) {
         auto u32 = [&](size_t off) { return reinterpret_cast<const uint32_t*>(db + off); };

@@ -416,3 +416,28 @@ def test_prefill_batch_equals_single_prefills(ctx):
     bad = [rows[0], (np.zeros_like(rows[1][0]), rows[1][1], rows[1][2])]
     with pytest.raises(cs.DataError):
         cs.prefill_batch(ctx, bad, widths, ics[:2], rc, group=grp)
+
+
+@pytest.mark.parametrize("rows", ["256", "512"])
+def test_attend_chunk_rows(ctx, monkeypatch, rows):
+    """Attention chunking by 256 or 512 rows per CTA (512 is chosen for large
+    launches such as c3): same selected sets as the reference, outputs within
+    1e-3, for d = 128 (attend128) and d = 64 (generic kernel)."""
+    monkeypatch.setenv("CSATTN_ATT_ROWS", rows)
+    for d, P in ((128, 8192), (64, 4096)):
+        T = 6
+        q, k, v = workload(P, T, d, seed=83)
+        widths = cs.uniform_widths(d, 8)
+        ic = cs.IndexConfig(alpha=0.2, centroids=32, seed=1, score_bits=32)
+        rc = cs.RetrievalConfig(keep_ratio=0.2)  # K = 1639 / 820: several chunks
+        qq = np.concatenate([q[:P]] * 4)
+        g = cs.prefill(ctx, qq, k[:P], v[:P], widths, ic, rc, group=4, max_decode_steps=T)
+        r = _checker("ref").prefill(qq, k[:P], v[:P], widths, ic, rc, 4)
+        worst = 0.0
+        for t in range(T):
+            Q = np.stack([q[P + t] * (1 + 0.05 * h) for h in range(4)]).astype(np.float32)
+            out, sel = cs.decode_batch([g], Q, k[P + t][None], v[P + t][None])
+            for h, (rs, ro, _, _) in enumerate(r.step(Q, k[P + t], v[P + t])):
+                assert np.array_equal(sel[h, :len(rs)], rs), (d, t, h)
+                worst = max(worst, rel_err(out[h], ro))
+        assert worst <= 1e-3, (d, worst)
