@@ -265,28 +265,41 @@ class ShardGroup:
         mark("ghist")
         run(A.SHARD_BUCKET)
         mark("bucket")
-        # the speculative cut (previous step's threshold) missed on some query
-        # head: every shard saw the same global histogram; rescan without it
+        # Did the speculative cut (previous step's threshold) miss on some query
+        # head? The flag goes to pinned host memory asynchronously and is read
+        # once MERGE is queued, so the host never waits mid-step. On a miss
+        # every shard saw the same global histogram: rescan without speculation
+        # and redo bucket..merge (mark clears its bitmap, emit/merge overwrite
+        # their outputs; nothing persistent changes before INSERT).
         fail = torch.stack([bb["fail"] for bb in bufs]).max()
         if self.dist is not None:
             self.dist.all_reduce(fail, op=self.dist.ReduceOp.MAX)
-        if int(fail.item()):
+        if getattr(self, "_fail_host", None) is None:
+            self._fail_host = torch.zeros((1,), dtype=fail.dtype, pin_memory=True)
+        self._fail_host.copy_(fail.reshape(1), non_blocking=True)
+        fail_ev = torch.cuda.Event()
+        fail_ev.record(torch.cuda.current_stream(dev))
+
+        def select_tail():
+            all_gather("bucket", "bucket_all")
+            run(A.SHARD_MARK)
+            mark("mark")
+            all_gather("counts", "counts_all")
+            run(A.SHARD_EMIT)
+            mark("emit")
+            all_gather("partial", "partial_all")
+            run(A.SHARD_MERGE)
+            mark("merge")
+        select_tail()
+        fail_ev.synchronize()
+        if int(self._fail_host[0]):
             self.rescans = getattr(self, "rescans", 0) + 1
             for bb in bufs:
                 bb["fail"].zero_()
             run(A.SHARD_RESCAN)
             all_reduce_sum("ghist")
             run(A.SHARD_BUCKET)
-        mark("fail-check")
-        all_gather("bucket", "bucket_all")
-        run(A.SHARD_MARK)
-        mark("mark")
-        all_gather("counts", "counts_all")
-        run(A.SHARD_EMIT)
-        mark("emit")
-        all_gather("partial", "partial_all")
-        run(A.SHARD_MERGE)
-        mark("merge")
+            select_tail()
         run(A.SHARD_VICTIM)
         all_reduce_min_u64("victim")
         run(A.SHARD_INSERT)
