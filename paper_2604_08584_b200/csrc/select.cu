@@ -1087,14 +1087,30 @@ select_merge_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __
     uint32_t* bidx = reinterpret_cast<uint32_t*>(bkey + BKT);       // BKT
     const uint32_t tid = threadIdx.x, p = blockIdx.x;
     if (tid == 0) S.nbkt = 0;
+    const uint32_t* um = unit_meta + static_cast<size_t>(p) * split * UNIT_META;
+    // the parts' histograms summed with every part's load in flight at once
+    // (issued before setup_problem's dependent descriptor loads)
+    constexpr uint32_t HX = (NB + NCB + SEL_CT - 1) / SEL_CT;  // words per thread
+    uint32_t hv[HX];
+#pragma unroll
+    for (uint32_t i = 0; i < HX; ++i) hv[i] = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < static_cast<uint32_t>(MAXPART); ++j) {
+        const uint32_t* u = um + static_cast<size_t>(j < split ? j : 0u) * UNIT_META;
+#pragma unroll
+        for (uint32_t i = 0; i < HX; ++i) {
+            const uint32_t x = tid + i * SEL_CT;
+            const uint32_t v = (j < split && x < NB + NCB) ? __ldcg(u + x) : 0u;
+            hv[i] += v;
+        }
+    }
     ProbState st;
     // the parts' speculative cut (same hint, read before any part finished)
     setup_problem(S, probs, plans, p, st, true, spec_keep);  // ends with a barrier
-    const uint32_t* um = unit_meta + static_cast<size_t>(p) * split * UNIT_META;
-    for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) {
-        uint32_t v = 0;
-        for (uint32_t j = 0; j < split; ++j) v += __ldcg(um + static_cast<size_t>(j) * UNIT_META + x);
-        hist[x] = v;
+#pragma unroll
+    for (uint32_t i = 0; i < HX; ++i) {
+        const uint32_t x = tid + i * SEL_CT;
+        if (x < NB + NCB) hist[x] = hv[i];
     }
     if (tid < split * SEL_CW) {
         const uint32_t j = tid / SEL_CW, w = tid % SEL_CW;
