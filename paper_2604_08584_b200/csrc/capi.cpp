@@ -645,8 +645,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     for (uint64_t i = 0; i < nq; ++i)
         if (!in_union[i]) n256 += (Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
     uint32_t arows = csa::attend_rows(n256);  // c3: 512 (attend 262 -> 251 us)
-    if (const char* ar = std::getenv("CSATTN_ATT_ROWS"))  // tests: force 256 / 512
-        arows = std::atoi(ar) == 512 ? csa::ATT_ROWS_BIG : csa::ATT_ROWS;
+    if (const char* ar = std::getenv("CSATTN_ATT_ROWS")) {  // tests: force 128 / 256 / 512
+        const int v = std::atoi(ar);
+        arows = v == 512 ? csa::ATT_ROWS_BIG : (v == 128 ? csa::ATT_ROWS_SMALL : csa::ATT_ROWS);
+    }
     uint64_t nchunks = 0;
     for (uint64_t i = 0; i < nq; ++i) {
         cbase[i] = static_cast<uint32_t>(nchunks);

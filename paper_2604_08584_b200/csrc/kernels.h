@@ -58,10 +58,13 @@ cudaError_t launch_shard_emit(const DecodeProblem* probs, const RoutePlan* plans
                               uint32_t* bitmap, uint32_t bm_words, uint32_t* kdev, cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
-constexpr uint32_t ATT_ROWS = 256;      // rows per chunk-CTA (small launches)
-constexpr uint32_t ATT_ROWS_BIG = 512;  // when 256-row chunks would fill > 4 waves
+constexpr uint32_t ATT_ROWS = 256;      // rows per chunk-CTA (mid-size launches)
+constexpr uint32_t ATT_ROWS_BIG = 512;  // when 256-row chunks would fill > 4 waves (c3)
+constexpr uint32_t ATT_ROWS_SMALL = 128;  // when they would give < 2 CTAs per SM (c2)
 // rows per chunk-CTA for a launch whose 256-row chunking has n256 chunks
-inline uint32_t attend_rows(uint64_t n256) { return n256 > 148ull * 8 * 4 ? ATT_ROWS_BIG : ATT_ROWS; }
+inline uint32_t attend_rows(uint64_t n256) {
+    return n256 > 148ull * 8 * 4 ? ATT_ROWS_BIG : (n256 < 148ull * 2 ? ATT_ROWS_SMALL : ATT_ROWS);
+}
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial = false,

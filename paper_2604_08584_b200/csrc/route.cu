@@ -33,11 +33,17 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     const uint32_t m = sd.m, C = sd.C, d = sd.d, tid = threadIdx.x;
     RoutePlan& plan = plans[blockIdx.x];
     DecodeReport* Rp = reinterpret_cast<DecodeReport*>(P.rep);
+    // q and the layout in one round trip (later phases read them from smem)
+    __shared__ uint32_t soff[MAXM], swid[MAXM];
     for (uint32_t t = tid; t < d; t += blockDim.x) q[t] = P.q[t];
+    if (tid < m) {
+        soff[tid] = sd.offs[tid];
+        swid[tid] = sd.widths[tid];
+    }
     if (tid == 0) zero_mask = 0;
     __syncthreads();
     if (tid < m) {
-        const uint32_t off = sd.offs[tid], w = sd.widths[tid];
+        const uint32_t off = soff[tid], w = swid[tid];
         double n2 = 0.0;
         for (uint32_t t = 0; t < w; ++t) {
             const double x = q[off + t];
@@ -55,7 +61,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
     for (uint32_t x = tid; x < m * C; x += blockDim.x) {
         const uint32_t b = x / C, j = x - b * C;
         if (zero_mask & (1u << b)) continue;
-        const uint32_t off = sd.offs[b], w = sd.widths[b];
+        const uint32_t off = soff[b], w = swid[b];
         const float* c = sd.cent + static_cast<size_t>(C) * off + static_cast<size_t>(j) * w;
         double acc = 0.0;
         if ((w & 3u) == 0u && ((C * off + j * w) & 3u) == 0u) {  // 16-byte rows: vector loads
@@ -126,7 +132,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
         uint32_t n = 0;
         unsigned long long dots = 0;
         for (uint32_t b = 0; b < m; ++b) {
-            if (!(zero_mask & (1u << b))) dots += static_cast<unsigned long long>(C) * sd.widths[b];
+            if (!(zero_mask & (1u << b))) dots += static_cast<unsigned long long>(C) * swid[b];
             for (uint32_t r = 0; r < nids[b]; ++r) {
                 lists[n] = b * C + ids[b * MAXTAU + r];
                 lsub[n] = b;

@@ -418,10 +418,10 @@ def test_prefill_batch_equals_single_prefills(ctx):
         cs.prefill_batch(ctx, bad, widths, ics[:2], rc, group=grp)
 
 
-@pytest.mark.parametrize("rows", ["256", "512"])
+@pytest.mark.parametrize("rows", ["128", "256", "512"])
 def test_attend_chunk_rows(ctx, monkeypatch, rows):
-    """Attention chunking by 256 or 512 rows per CTA (512 is chosen for large
-    launches such as c3): same selected sets as the reference, outputs within
+    """Attention chunking by 128, 256 or 512 rows per CTA (chosen by launch
+    size: c2 128, c4 256, c3 512): same selected sets as the reference, outputs within
     1e-3, for d = 128 (attend128) and d = 64 (generic kernel)."""
     monkeypatch.setenv("CSATTN_ATT_ROWS", rows)
     for d, P in ((128, 8192), (64, 4096)):
