@@ -92,6 +92,19 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
         S.nbuf = 0;
         S.applied = 0;
     }
+    // this thread's first table's state does not depend on the key: load it
+    // now, overlapped with the key load and normalization (non-sharded path;
+    // a table is touched by exactly one thread in phase A)
+    const bool pf = threadIdx.x < T && sd.L != 0 && !sd.sharded;
+    uint32_t pf_nu = 0, pf_live = 0, pf_cnt = 0;
+    LowEnt pf_victim{};
+    if (pf) {
+        const uint32_t t = threadIdx.x;
+        pf_nu = sd.n_used[t];
+        pf_live = sd.live[t];
+        pf_cnt = sd.low_cnt[t];
+        if (pf_live >= sd.L && pf_cnt) pf_victim = sd.low[static_cast<size_t>(t) * LOW_Q + pf_cnt - 1];
+    }
     __syncthreads();
     if (sd.normalize_keys && threadIdx.x < m) {
         // normalize_keys: score against the normalized slice (l2_normalize)
@@ -132,7 +145,8 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
             }
         }
         const float sc = __double2float_rn(s);
-        uint32_t nu = sd.n_used[t];
+        const bool mine = pf && t == threadIdx.x;  // prefetched above
+        uint32_t nu = mine ? pf_nu : sd.n_used[t];
         if (new_blk) sd.blk_off[static_cast<size_t>(t) * sd.nb_stride + (N >> KEY_BLOCK_SHIFT)] = nu;
         uint32_t applied = 0;
         if (sd.L != 0 && sd.sharded) {
@@ -193,15 +207,15 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
                 sd.live[t] = live;
             }
         } else if (sd.L != 0) {
-            const uint32_t live = sd.live[t];
-            uint32_t cnt = sd.low_cnt[t];
+            const uint32_t live = mine ? pf_live : sd.live[t];
+            uint32_t cnt = mine ? pf_cnt : sd.low_cnt[t];
             LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
             uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
             const bool full = live >= sd.L;
             const bool complete = cnt == live;  // buffer holds every live entry
             bool ok = true;
             if (full) {
-                const LowEnt victim = lo[cnt - 1];
+                const LowEnt victim = mine ? pf_victim : lo[cnt - 1];
                 if (!(sc > victim.score)) {
                     ok = false;  // strict win required (index.cpp:25)
                 } else {
