@@ -64,11 +64,13 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
     __shared__ uint32_t is_last;
     const uint32_t c = blockIdx.x;
-    const uint32_t p = chunk_prob[c];
+    // chunk entry: problem | chunk index << 20 (chunks may come in any order)
+    const uint32_t cpk = chunk_prob[c];
+    const uint32_t p = cpk & 0xfffffu;
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
     const uint32_t d = sd.d, K = P.K, P0 = sd.P;
-    const uint32_t j = c - chunk_base[p];
+    const uint32_t j = cpk >> 20;
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     const uint32_t rw = j * rows + w * (rows / ATT_WARPS);  // this warp's first row
@@ -165,7 +167,7 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
     float M = -FLT_MAX;
 #pragma unroll
     for (int i = 0; i < ATT_WARPS; ++i) M = fmaxf(M, wm[i]);
-    float* pp = part + static_cast<size_t>(c) * (d + 2);
+    float* pp = part + static_cast<size_t>(chunk_base[p] + j) * (d + 2);
     if (threadIdx.x == 0) {
         float S = 0.0f;
         for (int i = 0; i < ATT_WARPS; ++i)
@@ -238,11 +240,13 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
     __shared__ uint32_t is_last;
     const uint32_t c = blockIdx.x;
-    const uint32_t p = chunk_prob[c];
+    // chunk entry: problem | chunk index << 20 (chunks may come in any order)
+    const uint32_t cpk = chunk_prob[c];
+    const uint32_t p = cpk & 0xfffffu;
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
     const uint32_t d = 128, K = P.K, P0 = sd.P;
-    const uint32_t j = c - chunk_base[p];
+    const uint32_t j = cpk >> 20;
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
     const uint32_t rw = j * rows + w * (rows / ATT_WARPS);  // this warp's first row
@@ -398,7 +402,7 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     float M = -FLT_MAX;
 #pragma unroll
     for (int i = 0; i < ATT_WARPS; ++i) M = fmaxf(M, wm[i]);
-    float* pp = part + static_cast<size_t>(c) * (d + 2);
+    float* pp = part + static_cast<size_t>(chunk_base[p] + j) * (d + 2);
     if (threadIdx.x == 0) {
         float S = 0.0f;
         for (int i = 0; i < ATT_WARPS; ++i)

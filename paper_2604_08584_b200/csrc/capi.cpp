@@ -542,10 +542,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     ctx->hiprobs.resize(ns);
     uint64_t qi = 0;
     std::vector<uint32_t> searched(nq);
+    std::vector<const float*> pre_of(nq);  // each problem's prefill rows (attend chunk order)
     for (uint64_t i = 0; i < ns; ++i) {
         csattn_session s = ss[i];
         const uint64_t n = s->N;
         for (uint64_t h = 0; h < s->group; ++h, ++qi) {
+            pre_of[qi] = s->h.kpre;
             HeadState& hs = s->hs[h];
             csa::DecodeProblem& P = ctx->hprobs[qi];
             const bool srch = !hs.has_cache || (s->step % s->rc.search_period) == 0;
@@ -696,9 +698,33 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
     std::memcpy(hb + boff, cbase.data(), (nq + 1) * 4);
     {
+        // chunk entries (problem | chunk index << 20). Problems on one prefill
+        // (a KV head's sequences x query heads) go chunk-major, so the CTAs in
+        // flight work on similar key ranges of the shared rows (L2 reuse);
+        // CSATTN_ATT_ORDER=problem keeps problem-major order
         uint32_t* cp = reinterpret_cast<uint32_t*>(hb + poff);
-        for (uint64_t i = 0; i < nq; ++i)
-            std::fill(cp + cbase[i], cp + cbase[i + 1], static_cast<uint32_t>(i));
+        static const bool pmajor = [] {
+            const char* o = std::getenv("CSATTN_ATT_ORDER");
+            return o && std::strcmp(o, "problem") == 0;
+        }();
+        uint64_t at = 0;
+        if (pmajor) {
+            for (uint64_t i = 0; i < nq; ++i)
+                for (uint32_t j = 0; j < cbase[i + 1] - cbase[i]; ++j)
+                    cp[at++] = static_cast<uint32_t>(i) | (j << 20);
+        } else {
+            uint64_t g0 = 0;
+            while (g0 < nq) {  // runs of consecutive problems on the same prefill
+                uint64_t g1 = g0 + 1;
+                while (g1 < nq && pre_of[g1] == pre_of[g0]) ++g1;
+                uint32_t mx = 0;
+                for (uint64_t i = g0; i < g1; ++i) mx = std::max(mx, cbase[i + 1] - cbase[i]);
+                for (uint32_t j = 0; j < mx; ++j)
+                    for (uint64_t i = g0; i < g1; ++i)
+                        if (j < cbase[i + 1] - cbase[i]) cp[at++] = static_cast<uint32_t>(i) | (j << 20);
+                g0 = g1;
+            }
+        }
     }
     if (ngroups) {
         std::memcpy(hb + uoff, ugP.data(), ngroups * 4);
@@ -1848,8 +1874,8 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
             std::vector<uint32_t> cbase(nq + 1), cprob;
             for (uint64_t i = 0; i < nq; ++i) {
                 cbase[i] = static_cast<uint32_t>(cprob.size());
-                cprob.insert(cprob.end(), (ctx->sh_Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS,
-                             static_cast<uint32_t>(i));
+                const uint64_t nc = (ctx->sh_Ks[i] + csa::ATT_ROWS - 1) / csa::ATT_ROWS;
+                for (uint32_t j = 0; j < nc; ++j) cprob.push_back(static_cast<uint32_t>(i) | (j << 20));
             }
             cbase[nq] = static_cast<uint32_t>(cprob.size());
             ctx->sh_nchunks = cprob.size();
