@@ -496,13 +496,13 @@ cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows)
     // GR=4 (64 regs, 8 CTAs/SM) for large launches; GR=8 (more rows in flight
     // per warp) for small ones: c2 (224 x 256 rows, run as 448 x 128) 29 -> 19 us,
-    // while c4's 832 x 256 per layer and c3's 6656 x 512 are faster with GR=4.
-    // CSATTN_ATT_GR=4|8 forces.
+    // while c4's 832 x 256 per layer is faster with GR=4. CSATTN_ATT_GR=4|8 forces.
     const int gr_env = std::getenv("CSATTN_ATT_GR") ? std::atoi(std::getenv("CSATTN_ATT_GR")) : 0;
     // (launch size in 256-row units, whatever the chunk size)
+    // and 512-row chunks (c3, chunk-major order: 250 -> 245 us with GR=8)
     const int gr = gr_env == 4 || gr_env == 8
                        ? gr_env
-                       : (static_cast<uint64_t>(nchunks) * rows < 148ull * 3 * 256 ? 8 : 4);
+                       : ((rows >= 512u || static_cast<uint64_t>(nchunks) * rows < 148ull * 3 * 256) ? 8 : 4);
     if (d == 128 && partial) {
         if (gr == 4) attend128_kernel<true, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
         else attend128_kernel<true, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
