@@ -15,19 +15,27 @@ rows [P + s*T, P + (s+1)*T).
 A step = one decode step of the whole layer for all 16 sequences: centroid
 routing, gather/accumulate, top-K, sparse attention for 512 (sequence, query
 head) problems, then append + streaming insert for 128 (sequence, KV head)
-sessions: 2 kernel launches.
+sessions: 5 kernel launches (route, select, select retry pass, attend, insert).
 
 value = device time per layer-step in microseconds (lower is better), CUDA
 events on the launching stream, max over ranks. e2e = the same through the
 public C ABI with host (pinned) buffers, H2D of the step's q/k/v and D2H of
-its outputs inside the timed region. Multi-GPU: KV heads are sharded across
-ranks (rank r owns heads g with g % N == r), no data-path collective, so the
-layer latency should fall with N ("strong" scaling).
+its outputs inside the timed region. Multi-GPU (--gpus N): one process per
+GPU — bench.py spawns the N ranks itself when it is not already under torchrun
+— KV heads are sharded across ranks (rank r owns heads g with g % N == r), no
+data-path collective, so the layer latency should fall with N ("strong").
 
---impl reference: the reference CPU implementation (oracle/_ref, built from the
-unmodified sources) on the box's host cores: a bounded sample of the same
-workload (one sequence, H KV heads built by the reference's own build_index,
-one host thread per KV head), scaled to the full layer-step.
+parity: the reference library (oracle/_ref) steps sequence 0 of every KV head
+of layer 0 through the same steps as the GPU arm from the same tables; the
+line reports whether every selected set of the read-back step is identical
+and the worst relative output error over all steps (north_star: sets exact,
+outputs <= 1e-3). cpu_baseline is timed on those same reference steps.
+
+--impl reference: the reference CPU implementation (oracle/_ref, built from
+the unmodified sources; no product code is loaded) on the box's host cores:
+its own build_index for every KV head, then the FULL layer step of the
+config (c3: 16 sequences x 8 KV heads, each sequence its own Session copy)
+timed on all host threads — no scaling (c4/c5: a bounded sample, scaled).
 """
 from __future__ import annotations
 
@@ -78,9 +86,10 @@ def keep_count(rho: float, n: int) -> int:
     return max(1, int(math.ceil(rho * n - 1e-9)))
 
 
-def gen_head(cs, g: int, rows: int):
-    """Synthetic rows of KV head g: 4 query streams (dwells), keys, values."""
-    seed = mix_seed(2026, g)
+def gen_head(cs, g: int, rows: int, layer: int = 0):
+    """Synthetic rows of KV head g of layer `layer`: 4 query streams (dwells),
+    keys, values. Layer l offsets the seeds by 100*l."""
+    seed = mix_seed(2026 + 100 * layer, g)
     qs = []
     k = v = None
     for dw in DWELLS:
@@ -92,9 +101,45 @@ def gen_head(cs, g: int, rows: int):
     return np.stack(qs, 1), k, v  # q: [rows, 4, d]
 
 
-def gen_heads(cs, heads, rows):
+def gen_heads(cs, heads, rows, layer=0):
     with ThreadPoolExecutor(max_workers=min(16, 4 * len(heads))) as ex:
-        return list(ex.map(lambda g: gen_head(cs, g, rows), heads))
+        return list(ex.map(lambda g: gen_head(cs, g, rows, layer), heads))
+
+
+def launch_ranks(n: int) -> None:
+    """bench.py --gpus N outside torchrun: one process per GPU, launched here
+    (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* as torchrun sets them). Fails
+    loudly when fewer than N GPUs are visible."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        raise SystemExit(f"bench.py --gpus {n}: only {have} GPU(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    rcs = [p.wait() for p in procs]
+    sys.exit(max(rcs))
+
+
+def init_dist(local: int):
+    """torch.distributed over NCCL (one process per GPU); NCCL's init lines
+    (communicator ranks) go to the log."""
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t = torch.ones(1, device="cuda")
+    dist.all_reduce(t)  # creates the communicator now, not inside a timed region
+    return dist
 
 
 class ClockSampler:
@@ -175,81 +220,169 @@ def ncu_traffic(kernel: str, config: str):
 # reference arm / cpu baseline
 # --------------------------------------------------------------------------
 
-def run_reference(args, P, n_seq, rank):
-    """The reference CPU implementation on this host: bounded sample, scaled."""
+class _Spec:
+    """SyntheticSpec (synthetic.hpp:16-28) for the reference generator."""
+
+    def __init__(self, rows, seed, dwell):
+        self.rows, self.dim, self.clusters, self.seed = rows, D, 8, seed
+        self.plant_fraction, self.plant_scale, self.query_noise, self.dwell = 0.08, 6.0, 0.05, dwell
+
+
+class _RefIndexCfg:
+    """IndexConfig of the bench (alpha 0.2, C 64, 10 iterations, f32 scores)."""
+
+    def __init__(self, seed):
+        self.seed = seed
+
+    def c(self):
+        from oracle import _cstructs as cst
+        return cst.IndexConfigC(0.2, 0, 0, 32, C_CENT, 10, 0, self.seed, 1e-7)
+
+
+class _RefRetrievalCfg:
+    """RetrievalConfig defaults (retrieval.hpp:17-32): rho 0.05, R 32, period 1, tau 1."""
+
+    def c(self):
+        from oracle import _cstructs as cst
+        return cst.RetrievalConfigC(0.05, 1, 32, None, 0, 1, -float("inf"), 1, 0), None
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def ref_head(ob, g, rows, layer=0):
+    """KV head g of layer `layer` from the REFERENCE generator: q [rows, 4, d], k, v."""
+    seed = mix_seed(2026 + 100 * layer, g)
+    qs, k, v = [], None, None
+    for dw in DWELLS:
+        q, kk, vv = ob.ref_make_synthetic(_Spec(rows, seed, dw))
+        qs.append(q)
+        if k is None:
+            k, v = kk, vv
+    return np.stack(qs, 1), k, v
+
+
+def run_reference(args, P, n_seq, n_layers, rank):
+    """The reference CPU implementation on this host (oracle/_ref only: no
+    product module or library is loaded). Every KV head is built by the
+    reference's own build_index over its 4 heads' pooled prefill queries; each
+    of the n_seq sequences is its own Session copy (session.hpp:19-31); a
+    timed step is one decode step of EVERY (sequence, KV head) session of the
+    layer on all host threads. c3: the full 16 x 8 layer step, unscaled. c4:
+    one layer timed, x32 layers. c5: two KV heads at 1M, scaled to 8."""
     if rank != 0:
         return None
-    import paper_2604_08584_b200 as cs  # host-side generator only (bit-identical)
     from oracle import bindings as ob
     if not ob.ref_available():
         return {"impl": "reference", "unavailable": "oracle/_ref/libcsattn_ref.so not built"}
-    cores = os.cpu_count() or 1
-    H = max(1, min(N_KV, cores))
+    threads = host_threads()
     steps, warm = args.steps, args.warmup
     T = steps + warm
-    heads = list(range(H))
-    data = gen_heads(cs, heads, P + T)
+    heads = list(range(N_KV)) if P <= 131072 else [0, 1]
     widths = [D // M] * M
-    rc = cs.RetrievalConfig()
+    rc = _RefRetrievalCfg()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(threads, 8)) as ex:
+        data = list(ex.map(lambda g: ref_head(ob, g, P + n_seq * T), heads))
+    t_gen = time.perf_counter() - t0
 
-    def build(g):
-        q, k, v = data[g]
+    def build(i):
+        q, k, v = data[i]
         pooled = np.ascontiguousarray(np.concatenate([q[:P, r] for r in range(GROUP)]))
-        ic = cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
-        return ob.RefSession.prefill(pooled, k[:P], v[:P], widths, ic, rc, GROUP)
+        return ob.RefSession.prefill(pooled, k[:P], v[:P], widths, _RefIndexCfg(mix_seed(1, heads[i])),
+                                     rc, GROUP)
 
     t0 = time.perf_counter()
-    with ThreadPoolExecutor(max_workers=H) as ex:
-        sess = list(ex.map(build, heads))
+    with ThreadPoolExecutor(max_workers=min(threads, len(heads))) as ex:
+        base = list(ex.map(build, range(len(heads))))
     build_s = time.perf_counter() - t0
-    qs = np.stack([data[g][0][P:P + T] for g in heads])     # [H, T, 4, d]
-    ks = np.stack([data[g][1][P:P + T] for g in heads])     # [H, T, d]
-    vs = np.stack([data[g][2][P:P + T] for g in heads])
-    ob.ref_bench(sess, qs[:, :warm], ks[:, :warm], vs[:, :warm], warm, H) if warm else None
-    sec = ob.ref_bench(sess, qs[:, warm:], ks[:, warm:], vs[:, warm:], steps, H)
-    per_step = sec / steps                                   # H KV heads in parallel
-    sessions_total = N_KV * n_seq
-    layer_us = per_step * (sessions_total / H) * 1e6
-    sample = (f"1 sequence x {H} KV heads (group {GROUP}, {4 * H} query heads) at N={P}, "
-              f"reference build_index ({build_s:.1f}s, untimed), {steps} timed steps on {H} "
-              f"threads; scaled x{sessions_total / H:g} to the full layer-step")
-    return {"layer_us": layer_us, "cores": H, "sample": sample, "kind": "reference",
-            "per_kvhead_step_ms": per_step * 1e3}
+    # sessions: head-major, then sequence (sequence s decodes rows P + s*T + t)
+    sess, qs, ks, vs = [], [], [], []
+    for i, g in enumerate(heads):
+        q, k, v = data[i]
+        for s_ in range(n_seq):
+            sess.append(base[i] if s_ == 0 else base[i].fork())
+            r0 = P + s_ * T
+            qs.append(q[r0:r0 + T])
+            ks.append(k[r0:r0 + T])
+            vs.append(v[r0:r0 + T])
+    qs, ks, vs = np.stack(qs), np.stack(ks), np.stack(vs)   # [n, T, 4, d], [n, T, d]
+    if warm:
+        ob.ref_bench(sess, qs[:, :warm], ks[:, :warm], vs[:, :warm], warm, threads)
+    sec = ob.ref_bench(sess, qs[:, warm:], ks[:, warm:], vs[:, warm:], steps, threads)
+    per_step_us = sec / steps * 1e6                          # the timed sessions, all threads
+    scale = (N_KV / len(heads)) * n_layers
+    layer_us = per_step_us * scale
+    what = (f"{n_seq} sequence(s) x {len(heads)} KV heads (GQA {GROUP}, {len(sess)} sessions, "
+            f"{len(sess) * GROUP} query heads) at N={P}")
+    sample = (f"{what}: every session stepped {steps} timed steps after {warm} warm-up on "
+              f"{threads} threads; reference build_index per KV head ({build_s:.1f}s, untimed)"
+              + (f"; scaled x{scale:g} (KV heads x layers)" if scale != 1 else "; unscaled"))
+    return {"layer_us": layer_us, "cores": threads, "sample": sample, "kind": "reference",
+            "cpu_model": cpu_model(), "setup_s": {"synthetic": round(t_gen, 2),
+                                                  "build": round(build_s, 2)}}
 
 
-def cpu_baseline_from_gpu(cs, ob, sessions_by_head, data, P, n_seq, steps, T_used):
-    """cpu_baseline leg of our arm: the reference's decode path (oracle/_ref) on
-    the tables the GPU built (bit-identical to build_index, tests/), one host
-    thread per KV head, bounded sample of the same workload."""
-    if not ob.ref_available():
-        return None
-    cores = os.cpu_count() or 1
-    heads = sorted(sessions_by_head)[:max(1, min(len(sessions_by_head), cores))]
+def reference_parity(ob, base_sessions, data, P, T, t_sel, outd, seld, heads, rows_of):
+    """Parity gate + cpu_baseline of our arm: the reference (oracle/_ref) steps
+    sequence 0 of each given KV head through the GPU arm's steps 0..t_sel from
+    the same starting tables (the GPU build, bit-identical to build_index:
+    tests/test_gpu_scale.py), with the same inputs. Returns the comparison
+    (every output of those steps, the selected sets of the read-back step
+    t_sel) and the reference's own step time on the host cores."""
     widths = [D // M] * M
-    rc = cs.RetrievalConfig()
+    rc = _RefRetrievalCfg()
     refs = []
     for g in heads:
-        s = sessions_by_head[g]
-        inf = s.info()
-        lens, idx, sc, cent = s.export_index()
+        lens, idx, sc, cent, L, alpha = base_sessions[g]
         q, k, v = data[g]
-        kk, vv = s.read_kv(0, inf.context_len)
-        refs.append(ob.RefSession.from_index(cent, lens, idx, sc, inf.list_capacity, inf.alpha,
-                                             kk, vv, widths, rc, GROUP))
-    # continue sequence 0 of each head from where the GPU left it
-    base = P + T_used
-    qs = np.stack([data[g][0][base:base + steps] for g in heads])
-    ks = np.stack([data[g][1][base:base + steps] for g in heads])
-    vs = np.stack([data[g][2][base:base + steps] for g in heads])
-    sec = ob.ref_bench(refs, qs, ks, vs, steps, len(heads))
-    per_step = sec / steps
-    sessions_total = N_KV * n_seq
-    return {"value": per_step * (sessions_total / len(heads)) * 1e6, "unit": "us",
-            "cores": len(heads), "kind": "reference",
-            "sample": (f"reference decode path (oracle/_ref) on the GPU-built tables of "
-                       f"{len(heads)} KV heads x 1 sequence (group {GROUP}) at N~{base}, "
-                       f"{steps} steps, one thread per KV head; scaled "
-                       f"x{sessions_total / len(heads):g} to the full layer-step")}
+        refs.append(ob.RefSession.from_index(cent, lens, idx, sc, L, alpha, k[:P], v[:P], widths, rc,
+                                             GROUP))
+    worst, sets_equal, n_cmp = 0.0, True, 0
+    walls, per_head = [], []
+    threads = min(host_threads(), len(heads))
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        def one(i, t):
+            g = heads[i]
+            q, k, v = data[g]
+            t0 = time.perf_counter()
+            r = refs[i].step(q[P + t], k[P + t], v[P + t])
+            return r, time.perf_counter() - t0
+
+        for t in range(t_sel + 1):
+            t0 = time.perf_counter()
+            res = list(ex.map(lambda i: one(i, t), range(len(heads))))
+            walls.append(time.perf_counter() - t0)
+            per_head.append(float(np.mean([x[1] for x in res])))
+            for i, (r, _) in enumerate(res):
+                row0 = rows_of[heads[i]]
+                for h, (sel, out, _, _) in enumerate(r):
+                    o = outd[t, row0 + h]
+                    worst = max(worst, float(np.linalg.norm(o - out) / max(np.linalg.norm(out), 1e-30)))
+                    if t == t_sel:
+                        sets_equal &= bool(np.array_equal(seld[row0 + h, :len(sel)], sel))
+                        n_cmp += 1
+    return {"sets_equal": sets_equal, "max_rel_err": worst, "steps": t_sel + 1,
+            "problems": len(heads) * GROUP, "sets_compared": n_cmp,
+            "tolerance": 1e-3, "pass": bool(sets_equal and worst <= 1e-3),
+            "what": ("sequence 0 of every KV head of layer 0 (GQA 4): outputs of every step "
+                     "0..t, selected sets of the read-back step t, vs oracle/_ref from the same "
+                     "tables")}, float(np.median(walls)), float(np.median(per_head)), threads
 
 
 # --------------------------------------------------------------------------
@@ -270,10 +403,7 @@ def run_c5(args, config, P, rank, world, local):
     from paper_2604_08584_b200.sharding import ShardGroup
 
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(local) if world > 1 else None
     stream = torch.cuda.Stream()
     n_total = max(4, world)
     L = n_total // world
@@ -408,9 +538,13 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
 
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        launch_ranks(args.gpus)  # exits with the ranks' status
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     P, n_seq, n_layers, desc = CONFIGS[args.config]
     config = {"workload": f"{args.config}: {desc}", "prefill": P, "sequences": n_seq,
               "layers": n_layers,
@@ -418,7 +552,7 @@ def main():
               "alpha": 0.2, "rho": 0.05, "window": 32, "tau": 1}
 
     if args.impl == "reference":
-        res = run_reference(args, P, n_seq * n_layers, rank)
+        res = run_reference(args, P, n_seq, n_layers, rank)
         if rank != 0:
             return
         if "unavailable" in res:
@@ -431,8 +565,9 @@ def main():
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference make_synthetic)", "config": config,
             "cpu_baseline": {"value": v, "unit": "us", "cores": res["cores"], "kind": "reference",
-                             "sample": res["sample"]},
+                             "sample": res["sample"], "cpu_model": res["cpu_model"]},
             "e2e": {"value": v, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": res["setup_s"],
         }))
         return
 
@@ -444,10 +579,7 @@ def main():
     if args.config == "c5":
         return run_c5(args, config, P, rank, world, local)
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(local) if world > 1 else None
     stream = torch.cuda.Stream()
     ctx = cs.Context(local, stream.cuda_stream)
     if args.config == "c2o":  # offload mode
@@ -463,34 +595,45 @@ def main():
     my_heads = kv_head_shard(N_KV, world, rank)
     widths = [D // M] * M
     rc = cs.RetrievalConfig()
-
-    t0 = time.perf_counter()
-    data = dict(zip(my_heads, gen_heads(cs, my_heads, P + n_layers * n_seq * T + args.cpu_steps)))
-    t_gen = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    # the layer's KV heads in one csattn_prefill_batch (one k-means launch)
-    rows_b = [(np.ascontiguousarray(np.concatenate([data[g][0][:P, r] for r in range(GROUP)])),
-               data[g][1][:P], data[g][2][:P]) for g in my_heads]
-    ics = [cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
-           for g in my_heads]
-    base_sessions = dict(zip(my_heads, cs.prefill_batch(ctx, rows_b, widths, ics, rc, group=GROUP,
-                                                        max_decode_steps=T)))
-    del rows_b
-    t_build = time.perf_counter() - t0
-    # Session order: layer-major, then KV head, then sequence. Sequence 0 of
-    # layer 0 is the prefilled session; every other (layer, sequence) is a fork
-    # of it (tables copied, prefill rows shared: c3's 16 sequences share one
-    # prefill; c4's layers start from layer 0's tables, build time only), and
-    # decodes its own rows of the head's stream, [P + (l*n_seq + s)*T, +T).
-    t0 = time.perf_counter()
+    parity_on = rank == 0 and not args.no_cpu_baseline
+    # Per layer: the KV heads' synthetic rows (layer l seeds offset by 100*l),
+    # ONE csattn_prefill_batch (one k-means launch for the layer's heads), then
+    # the sequences: sequence 0 is the prefilled session, sequences 1.. are
+    # forks (tables copied, prefill rows shared: c3's 16 sequences share one
+    # prefill). Every layer has its own KV rows and tables (c4: 32 distinct
+    # layers). Sequence s decodes rows [P + s*T, P + (s+1)*T) of its head.
+    # Session order: layer-major, then KV head, then sequence.
+    t_gen = t_build = t_fork = 0.0
     sessions, rows = [], []
+    dec = {}          # (layer, g) -> decode rows (q [n_seq*T, 4, d], k, v)
+    parity_src = {}   # layer 0: g -> starting tables (export) for the reference parity gate
+    data0 = {}        # layer 0: g -> (q, k, v) prefill + sequence-0 rows (reference parity)
     for layer in range(n_layers):
+        t0 = time.perf_counter()
+        data = dict(zip(my_heads, gen_heads(cs, my_heads, P + n_seq * T, layer)))
+        t_gen += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rows_b = [(np.ascontiguousarray(np.concatenate([data[g][0][:P, r] for r in range(GROUP)])),
+                   data[g][1][:P], data[g][2][:P]) for g in my_heads]
+        ics = [cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1 + 100 * layer, g),
+                              score_bits=32) for g in my_heads]
+        base = dict(zip(my_heads, cs.prefill_batch(ctx, rows_b, widths, ics, rc, group=GROUP,
+                                                   max_decode_steps=T)))
+        del rows_b
+        t_build += time.perf_counter() - t0
+        if layer == 0 and parity_on:
+            for g in my_heads:
+                inf = base[g].info()
+                parity_src[g] = (*base[g].export_index(), inf.list_capacity, inf.alpha)
+                data0[g] = (data[g][0][:P + T], data[g][1][:P + T], data[g][2][:P + T])
+        t0 = time.perf_counter()
         for g in my_heads:
             for s in range(n_seq):
-                first = layer == 0 and s == 0
-                sessions.append(base_sessions[g] if first else base_sessions[g].fork(T))
-                rows.append((g, layer * n_seq + s))
-    t_fork = time.perf_counter() - t0
+                sessions.append(base[g] if s == 0 else base[g].fork(T))
+                rows.append((layer, g, s))
+            dec[(layer, g)] = tuple(x[P:] for x in data[g])
+        t_fork += time.perf_counter() - t0
+        del data, base
     ns = len(sessions)
     nq = ns * GROUP
     ns_l = ns // n_layers  # sessions per layer (a layer = one decode_batch call)
@@ -500,17 +643,17 @@ def main():
     qh = np.empty((T, nq, D), np.float32)
     kh = np.empty((T, ns, D), np.float32)
     vh = np.empty((T, ns, D), np.float32)
-    for i, (g, s) in enumerate(rows):
-        q, k, v = data[g]
-        r0 = P + s * T
+    for i, (layer, g, s) in enumerate(rows):
+        q, k, v = dec[(layer, g)]
+        r0 = s * T
         qh[:, i * GROUP:(i + 1) * GROUP] = q[r0:r0 + T]
         kh[:, i] = k[r0:r0 + T]
         vh[:, i] = v[r0:r0 + T]
+    del dec
     qd = torch.from_numpy(qh).cuda()
     kd = torch.from_numpy(kh).cuda()
     vd = torch.from_numpy(vh).cuda()
     outd = torch.empty((T, nq, D), dtype=torch.float32, device="cuda")
-    L = base_sessions[my_heads[0]].info().list_capacity
     torch.cuda.synchronize()
     lib = cs.lib()
 
@@ -593,6 +736,7 @@ def main():
     seld = torch.zeros((nq, maxK), dtype=torch.int32, device="cuda")
     step(t, flags=0, sel=seld, sel_stride=maxK)
     Ka = keep_count(0.05, P + t)
+    t_sel = t
     t += 1
     selh = seld.cpu().numpy().astype(np.int64)[:, :Ka]
     uniq_rows = 0
@@ -687,12 +831,28 @@ def main():
         assert all(torch.isfinite(b[3]).all() for b in bufs)
         t += graph_steps
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # ---- parity gate + cpu baseline: oracle/_ref on sequence 0 of layer 0's KV
+    # heads, the same steps 0..t_sel from the same tables (rank 0, N = 1) ----
+    cpu = parity = None
+    if parity_on and world == 1:
         try:
             from oracle import bindings as ob
-            cpu = cpu_baseline_from_gpu(cs, ob, base_sessions, data, P, n_seq * n_layers,
-                                        args.cpu_steps, t)
+            if ob.ref_available():
+                rows_of = {g: gi * n_seq * GROUP for gi, g in enumerate(my_heads)}
+                pick = np.concatenate([np.arange(r, r + GROUP) for r in rows_of.values()])
+                out_h = np.zeros((t_sel + 1, nq, D), np.float32)
+                out_h[:, pick] = outd[:t_sel + 1, pick].cpu().numpy()
+                parity, wall, per_head, thr = reference_parity(
+                    ob, parity_src, data0, P, T, t_sel, out_h, selh, my_heads, rows_of)
+                scale = n_seq * n_layers
+                cpu = {"value": wall * scale * 1e6, "unit": "us", "cores": thr, "kind": "reference",
+                       "cpu_model": cpu_model(), "host_threads": host_threads(),
+                       "per_kvhead_step_ms_1thread": per_head * 1e3,
+                       "sample": (f"reference decode path (oracle/_ref) of sequence 0 of the "
+                                  f"{len(my_heads)} KV heads of layer 0 (GQA {GROUP}), "
+                                  f"{t_sel + 1} steps from N={P} (the parity-gate steps), one "
+                                  f"thread per KV head; median step wall time x{scale} "
+                                  f"(sequences x layers) to the full step")}
         except Exception as e:  # reported, never fatal for the GPU number
             cpu = {"value": None, "error": str(e)[:200]}
 
@@ -727,6 +887,7 @@ def main():
             "setup_s": {"synthetic": round(t_gen, 2), "gpu_build": round(t_build, 2),
                         "fork": round(t_fork, 2)},
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line))
     if dist:

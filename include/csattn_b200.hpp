@@ -329,12 +329,15 @@ class Session {
         csattn_session_info info{};
         check(csattn_session_info_get(h_, &info));
         dim_ = info.dim;
+        pushed_ = this->cfg;
+        pushed_.k_bump = nullptr;
     }
     ~Session() {
         if (h_) csattn_session_destroy(h_);
     }
     Session(Session&& o) noexcept
         : cfg(std::move(o.cfg)), step(o.step), h2d_elem_bytes(o.h2d_elem_bytes), totals(o.totals),
+          last_worst_(o.last_worst_), pushed_(std::move(o.pushed_)),
           h_(std::exchange(o.h_, nullptr)), layout_(std::move(o.layout_)),
           centroids_(std::move(o.centroids_)), dim_(o.dim_) {}
     Session(const Session&) = delete;
@@ -347,7 +350,36 @@ class Session {
         Session s(out, layout_, cfg);
         s.step = step;
         s.totals = totals;
+        s.last_worst_ = last_worst_;
+        s.pushed_ = pushed_;
         return s;
+    }
+
+    // `cfg` is a public member (session.hpp:19-31): hand any change to the
+    // device session before the next step
+    void sync_config() {
+        const RetrievalConfig& a = cfg;
+        const RetrievalConfig& b = pushed_;
+        if (a.keep_ratio == b.keep_ratio && a.search_period == b.search_period &&
+            a.recent_window == b.recent_window && a.weights == b.weights &&
+            a.backoff_tau == b.backoff_tau && a.backoff_threshold == b.backoff_threshold &&
+            a.recent_passthrough == b.recent_passthrough)
+            return;
+        const csattn_retrieval_config rc = cfg.c();
+        check(csattn_session_set_retrieval(h_, &rc));
+        pushed_ = cfg;
+        pushed_.k_bump = nullptr;
+    }
+
+    // decode_search's k_bump input (retrieval.cpp:257-263): the worst best
+    // cosine of state.last_selection, i.e. of THIS query on a searching step
+    // (!has_cache || step % period == 0, :237-238) and of the last search's
+    // query otherwise
+    double k_bump_cosine(std::span<const float> q) {
+        const csattn_session_info in = info();
+        const bool searching = in.steps == 0 || in.steps % std::max<std::size_t>(cfg.search_period, 1) == 0;
+        if (searching) last_worst_ = worst_best_cosine(q);
+        return last_worst_;
     }
 
     csattn_session handle() const { return h_; }
@@ -443,6 +475,9 @@ class Session {
     CostCounters totals;
 
    private:
+    double last_worst_ = 1.0;  // worst best-cosine of the last search (k_bump)
+    RetrievalConfig pushed_;   // the configuration the device session holds
+
     const std::vector<float>& centroids() const {  // immutable after the build
         if (centroids_.empty()) {
             const csattn_session_info in = info();
@@ -624,11 +659,14 @@ inline DecodeStepReport decode_step(Session& session, std::span<const float> q,
     const std::size_t d = session.dim();
     if (q.size() != d || new_key.size() != d || new_value.size() != d)
         throw DimensionError("decode step inputs must have width d");
+    if (session.info().group != 1)
+        throw ParameterError("decode_step takes one query: this session serves a GQA group of " +
+                             std::to_string(session.info().group) + " heads (use csattn_decode_step)");
+    session.sync_config();
     const std::size_t n = session.size();
     uint64_t k_override = 0;
     if (session.cfg.k_bump)
-        k_override = session.cfg.k_bump(keep_count(session.cfg.keep_ratio, n),
-                                         session.worst_best_cosine(q));
+        k_override = session.cfg.k_bump(keep_count(session.cfg.keep_ratio, n), session.k_bump_cosine(q));
     DecodeStepReport r;
     std::vector<uint32_t> sel(n);
     std::vector<float> out(d), w(n);
@@ -724,6 +762,11 @@ inline GraphRun run_decode_graph(Session& session, std::span<const float> querie
     if (available < steps)
         throw StreamExhaustedError("decode streams run out at step " + std::to_string(available) +
                                    " of " + std::to_string(steps));
+    if (session.info().group != 1)
+        throw ParameterError("run_decode_graph takes one query per step: this session serves a GQA group");
+    if (session.cfg.k_bump)
+        throw ParameterError("run_decode_graph has no per-step k_bump hook: use run_decode");
+    session.sync_config();
     GraphRun r;
     if (steps == 0) return r;
     const std::size_t n0 = session.size();

@@ -15,7 +15,7 @@ import os
 
 import numpy as np
 
-from paper_2604_08584_b200 import _abi
+from oracle import _cstructs as _abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_LIB = os.path.join(HERE, "_ref", "libcsattn_ref.so")
@@ -54,6 +54,8 @@ def ref_lib():
                                    P(vp)]
         L.csref_candidates.argtypes = [vp, u64, vp, vp, u64, P(u64)]
         L.csref_free.argtypes = [vp]
+        L.csref_fork.argtypes = [vp, P(vp)]
+        L.csref_set_retrieval.argtypes = [vp, P(_abi.RetrievalConfigC)]
         L.csref_info.argtypes = [vp, P(u64), P(u64), P(u64), P(u64)]
         L.csref_export.argtypes = [vp, vp, vp, vp, u64, vp]
         L.csref_step.argtypes = [vp, vp, vp, vp, vp, u64, vp, vp, P(_abi.StepReportC), P(u64)]
@@ -116,6 +118,12 @@ def _f32(a):
     return np.ascontiguousarray(a, dtype=np.float32)
 
 
+def _rcfg(rcfg):
+    """(checker-side RetrievalConfigC, weights array kept alive with it)"""
+    rc, w = rcfg.c()
+    return _abi.as_struct(_abi.RetrievalConfigC, rc), w
+
+
 def _w(widths):
     return (C.c_uint64 * len(widths))(*[int(x) for x in widths])
 
@@ -168,8 +176,8 @@ class RefSession(_Base):
         L = ref_lib()
         d = sum(widths)
         q, k, v = _f32(queries), _f32(keys), _f32(values)
-        ic = icfg.c()
-        rc, w = rcfg.c()
+        ic = _abi.as_struct(_abi.IndexConfigC, icfg.c())
+        rc, w = _rcfg(rcfg)
         h = C.c_void_p()
         st = L.csref_prefill(q.ctypes.data, q.size // d, k.ctypes.data, v.ctypes.data,
                              k.size // d, d, _w(widths), len(widths), C.byref(ic), C.byref(rc),
@@ -183,8 +191,8 @@ class RefSession(_Base):
         d = sum(widths)
         c = _f32(cent).reshape(-1)
         k, v = _f32(keys), _f32(values)
-        ic = icfg.c()
-        rc, w = rcfg.c()
+        ic = _abi.as_struct(_abi.IndexConfigC, icfg.c())
+        rc, w = _rcfg(rcfg)
         h = C.c_void_p()
         st = L.csref_prefill_from_centroids(c.ctypes.data, c.size // d, k.ctypes.data,
                                             v.ctypes.data, k.size // d, d, _w(widths),
@@ -198,7 +206,7 @@ class RefSession(_Base):
         """load_index (deserialize_index) + KvStore + Session over the image."""
         a = np.frombuffer(bytes(data), np.uint8)
         k, v = _f32(keys), _f32(values)
-        rc, w = rcfg.c()
+        rc, w = _rcfg(rcfg)
         h = C.c_void_p()
         cls._chk(ref_lib().csref_load(a.ctypes.data, a.size, k.ctypes.data, v.ctypes.data, d,
                                       C.byref(rc), group, C.byref(h)))
@@ -222,7 +230,7 @@ class RefSession(_Base):
         idx = np.ascontiguousarray(idx, np.uint32)
         sc = _f32(sc)
         k, v = _f32(keys), _f32(values)
-        rc, w = rcfg.c()
+        rc, w = _rcfg(rcfg)
         h = C.c_void_p()
         cls._chk(ref_lib().csref_import(c.ctypes.data, c.size // d, lens.ctypes.data,
                                         idx.ctypes.data, sc.ctypes.data, idx.shape[1], L, alpha,
@@ -238,6 +246,19 @@ class RefSession(_Base):
         s = cls(ref_lib(), h, d, group, n.value, L.value, c.value * m.value)
         s.C = c.value
         s.m = m.value
+        return s
+
+    def set_retrieval(self, rcfg):
+        rc, w = _rcfg(rcfg)
+        self._keep_w = w
+        self._chk(ref_lib().csref_set_retrieval(self.h, C.byref(rc)))
+
+    def fork(self):
+        """An independent copy (Session is a value type in the reference)."""
+        h = C.c_void_p()
+        self._chk(ref_lib().csref_fork(self.h, C.byref(h)))
+        s = type(self)(self.lib, h, self.d, self.group, self.n, self.L, self.T)
+        s.C, s.m = self.C, self.m
         return s
 
     def candidates(self, head=0):
@@ -281,8 +302,8 @@ class OraSession(_Base):
         L = ora_lib()
         d = sum(widths)
         q, k, v = _f32(queries), _f32(keys), _f32(values)
-        ic = icfg.c()
-        rc, w = rcfg.c()
+        ic = _abi.as_struct(_abi.IndexConfigC, icfg.c())
+        rc, w = _rcfg(rcfg)
         h = C.c_void_p()
         cls._chk(L.ora_prefill(q.ctypes.data, q.size // d, k.ctypes.data, v.ctypes.data,
                                k.size // d, d, _w(widths), len(widths), C.byref(ic),
@@ -297,8 +318,8 @@ class OraSession(_Base):
         d = sum(widths)
         c = _f32(cent).reshape(-1)
         k, v = _f32(keys), _f32(values)
-        ic = icfg.c()
-        rc, w = rcfg.c()
+        ic = _abi.as_struct(_abi.IndexConfigC, icfg.c())
+        rc, w = _rcfg(rcfg)
         h = C.c_void_p()
         cls._chk(L.ora_prefill_from_centroids(c.ctypes.data, c.size // d, k.ctypes.data,
                                               v.ctypes.data, k.size // d, d, _w(widths),

@@ -295,6 +295,18 @@ int csref_import(const float* cent, uint64_t c, const uint32_t* lens, const uint
 
 void csref_free(void* h) { delete static_cast<Group*>(h); }
 
+// Session::cfg is a public member (session.hpp:19-31): change it between steps.
+int csref_set_retrieval(void* h, const csattn_retrieval_config* rc) {
+    return guarded([&] { static_cast<Group*>(h)->session.cfg = rcfg_of(rc); });
+}
+
+// A copy of a session (Session is a value type, session.hpp:19-31): KvStore,
+// CsIndex and every query head's SearchState — one more independent sequence
+// over the same prefill (the batch-decode sequences of config c3).
+int csref_fork(void* h, void** out) {
+    return guarded([&] { *out = new Group(*static_cast<Group*>(h)); });
+}
+
 int csref_info(void* h, uint64_t* n, uint64_t* l, uint64_t* c, uint64_t* m) {
     return guarded([&] {
         const Group* g = static_cast<Group*>(h);

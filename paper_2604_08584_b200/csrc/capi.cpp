@@ -172,6 +172,7 @@ struct csattn_ctx_s {
             if (s.done) cudaEventDestroy(s.done);
         }
         if (cap_host) cudaFreeHost(cap_host);
+        for (uint32_t* pg : bad_pages) cudaFreeHost(pg);
     }
     std::vector<unsigned char> hrep;
     // kernel timing (csattn_ctx_profile)
@@ -224,6 +225,23 @@ struct csattn_ctx_s {
     double phase_dbg[3] = {0, 0, 0};
     uint64_t phase_retry = 0, phase_probs = 0;
     uint64_t phase_n = 0;
+    // non-finite append flags (insert.cu sets a session's flag instead of
+    // appending a non-finite row): pinned host words the kernel writes
+    // directly, one per session, handed out from 4096-word pages
+    std::vector<uint32_t*> bad_pages;
+    std::vector<uint32_t*> bad_free;
+    uint32_t* take_bad_flag() {
+        if (bad_free.empty()) {
+            void* pg = nullptr;
+            ck(cudaMallocHost(&pg, 4096 * sizeof(uint32_t)), "cudaMallocHost");
+            bad_pages.push_back(static_cast<uint32_t*>(pg));
+            for (int i = 4095; i >= 0; --i) bad_free.push_back(static_cast<uint32_t*>(pg) + i);
+        }
+        uint32_t* f = bad_free.back();
+        bad_free.pop_back();
+        *f = 0;
+        return f;
+    }
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t take_event() {
         if (!ev_pool.empty()) {
@@ -252,6 +270,11 @@ struct csattn_session_s {
     std::vector<double> weights;
     std::vector<HeadState> hs;
     std::vector<uint64_t> widths;
+    // non-finite appended row seen by insert.cu (pinned word from the ctx pool);
+    // `poisoned`: such a row was found only after later steps were queued
+    // (CSATTN_NO_SYNC), so the host's context length ran ahead of the store
+    uint32_t* bad = nullptr;
+    bool poisoned = false;
 
     ~csattn_session_s();
     uint64_t T() const { return static_cast<uint64_t>(h.m) * h.C; }
@@ -407,6 +430,7 @@ std::unique_ptr<csattn_session_s> new_session(csattn_ctx ctx, uint64_t d, const 
     h.sharded = 0;
     h.live_g = h.live;  // unsharded: the global count is the local one
     s->hs.assign(group, HeadState{});
+    s->bad = ctx->take_bad_flag();
     return s;
 }
 
@@ -456,6 +480,44 @@ void check_rows(const float* keys, const float* values, uint64_t p, uint64_t d, 
     }
 }
 
+// A session whose insert kernel refused a non-finite row (KvStore::append,
+// core.cpp:71-79) after the host had queued later steps on it: its context
+// length ran ahead of its store, so it only reports the error from then on.
+void check_not_poisoned(csattn_session s) {
+    if (!s->poisoned && s->bad && *reinterpret_cast<volatile uint32_t*>(s->bad)) s->poisoned = true;
+    if (s->poisoned)
+        fail(CSATTN_ERR_DATA,
+             "appended row contains a non-finite value (found after later steps were queued; "
+             "the session is unusable)");
+}
+
+// After a synchronised step: a session whose appended row was non-finite kept
+// its KV rows and tables (the kernel skipped the append and the insert), so its
+// context length goes back; the search state advanced, as decode_search's does
+// before KvStore::append throws (session.cpp:57-81). Raises DataError.
+void check_appended(const csattn_session* ss, uint64_t ns) {
+    uint32_t first = 0;
+    for (uint64_t i = 0; i < ns; ++i) {
+        volatile uint32_t* f = ss[i]->bad;
+        if (f && *f) {
+            if (!first) first = *f;
+            *f = 0;
+            ss[i]->N -= 1;
+        }
+    }
+    if (first)
+        fail(CSATTN_ERR_DATA, first == 1 ? "appended key contains a non-finite value"
+                                         : "appended value contains a non-finite value");
+}
+
+// one session twice in a batch would append and insert twice at one N
+void check_distinct(const csattn_session* ss, uint64_t ns) {
+    std::vector<csattn_session> u(ss, ss + ns);
+    std::sort(u.begin(), u.end());
+    if (std::adjacent_find(u.begin(), u.end()) != u.end())
+        fail(CSATTN_ERR_PARAMETER, "a session appears twice in one decode batch");
+}
+
 struct Outs {
     float* out;
     uint32_t* sel;
@@ -473,9 +535,11 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const uint32_t d = ss[0]->h.d;
     uint64_t nq = 0, maxN = 0, maxK = 0;
     std::vector<uint64_t> Ks;
+    check_distinct(ss, ns);
     for (uint64_t i = 0; i < ns; ++i) {
         csattn_session s = ss[i];
         if (s->ctx != ctx) fail(CSATTN_ERR_PARAMETER, "sessions belong to another context");
+        if (!ctx->capture) check_not_poisoned(s);
         if (s->h.d != d) fail(CSATTN_ERR_DIMENSION, "sessions differ in head dimension");
         if (s->step >= s->max_steps)
             fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
@@ -574,6 +638,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         I.value = dv + i * d;
         I.rep = s->irep.as<uint32_t>();
         I.N = static_cast<uint32_t>(n);
+        I.bad = s->bad;
         I.pad = 0;
     }
     const auto ht1 = std::chrono::steady_clock::now();
@@ -1003,7 +1068,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
     }
     const auto ht3 = std::chrono::steady_clock::now();
-    if (host || !(flags & CSATTN_NO_SYNC)) ck(cudaStreamSynchronize(ctx->stream), "decode step");
+    if (host || !(flags & CSATTN_NO_SYNC)) {
+        ck(cudaStreamSynchronize(ctx->stream), "decode step");
+        check_appended(ss, ns);
+    }
     if (ctx->host_prof && host) {  // host-buffer calls: phases (CSATTN_HOST_PROF=1; diagnostics only)
         const auto ht4 = std::chrono::steady_clock::now();
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
@@ -1050,10 +1118,9 @@ void import_tables(csattn_session_s* s, const uint32_t* lens, const uint32_t* in
         std::vector<uint32_t> pos_of(n);
         for (uint32_t p = 0; p < n; ++p) {
             ent[t * cap2 + p] = make_uint2(ix[order[p]], 0);
-            // -0.0f -> +0.0f: equal in every comparison, and select.cu uses
-            // -0.0 as its "not gathered" marker
-            const float f = sc[order[p]] == 0.0f ? 0.0f : sc[order[p]];
-            std::memcpy(&ent[t * cap2 + p].y, &f, 4);
+            // the stored bits stay as given (a -0.0f score is kept, so an
+            // export is byte-identical); select.cu canonicalises at accumulation
+            std::memcpy(&ent[t * cap2 + p].y, &sc[order[p]], 4);
             pos_of[order[p]] = p;
         }
         nused[t] = n;
@@ -1285,6 +1352,7 @@ csattn_status csattn_ctx_destroy(csattn_ctx ctx) {
 csattn_session_s::~csattn_session_s() {
     if (ctx) {
         cudaStreamSynchronize(ctx->stream);
+        if (bad) ctx->bad_free.push_back(bad);
         ctx_release(ctx);
     }
 }
@@ -1803,6 +1871,7 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                 csattn_session s = ss[i];
                 if (s->ctx != ctx) fail(CSATTN_ERR_PARAMETER, "sessions belong to another context");
                 if (s->h.d != d) fail(CSATTN_ERR_DIMENSION, "sessions differ in head dimension");
+                check_not_poisoned(s);  // a non-finite row refused by an earlier INSERT phase
                 if (s->step >= s->max_steps)
                     fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
                                                   std::to_string(s->max_steps));
@@ -1867,6 +1936,7 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                 I.value = io->new_values + i * d;
                 I.rep = s->irep.as<uint32_t>();
                 I.N = static_cast<uint32_t>(s->N);
+                I.bad = s->bad;
                 I.pad = 0;
             }
             // attention work list: ceil(K / ATT_ROWS) chunk-CTAs per problem (global K:
@@ -2075,8 +2145,17 @@ csattn_status csattn_session_info_get(csattn_session s, csattn_session_info* o) 
 csattn_status csattn_session_set_retrieval(csattn_session s, const csattn_retrieval_config* rc) {
     return guard([&] {
         validate_retrieval(rc, s->h.m);
-        if (rc->search_period > 1 && !s->cache.p)
+        if (rc->search_period > 1 && !s->cache.p) {
+            // decode_search would reuse state.cached from the last search on
+            // the next off-period step (retrieval.cpp:237-238); without a kept
+            // candidate cache that set is gone, so refuse instead of diverging
+            for (const HeadState& h : s->hs)
+                if (h.has_cache)
+                    fail(CSATTN_ERR_PARAMETER,
+                         "B200 path: raising search_period above 1 after decode steps needs "
+                         "csattn_session_keep_candidates(1) before those steps");
             s->cache.alloc(s->group * s->h.max_ctx * sizeof(double));
+        }
         set_retrieval(s, rc);
         push_dev(s);
         ck(cudaStreamSynchronize(s->ctx->stream), "set_retrieval");
@@ -2191,8 +2270,10 @@ void run_graph(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, uint64_t T
     const bool host = flags & CSATTN_HOST_BUFFERS;
     const uint64_t d = ss[0]->h.d;
     uint64_t nq = 0;
+    check_distinct(ss, ns);
     for (uint64_t i = 0; i < ns; ++i) {
         if (ss[i]->ctx != ctx) fail(CSATTN_ERR_PARAMETER, "sessions belong to another context");
+        check_not_poisoned(ss[i]);
         if (ss[i]->step + T > ss[i]->max_steps)
             fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
                                           std::to_string(ss[i]->max_steps));
@@ -2357,6 +2438,8 @@ void run_graph(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, uint64_t T
                      us(hs0, h0), us(h0, h1), us(h1, h2), us(h2, h3), us(h3, h4));
     }
     ck(e, "decode run");
+    // a non-finite row inside a graph run: later steps already ran on it
+    for (uint64_t i = 0; i < ns; ++i) check_not_poisoned(ss[i]);
 }
 
 }  // namespace

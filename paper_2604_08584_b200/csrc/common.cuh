@@ -129,6 +129,8 @@ struct InsertProblem {
     const float* key;
     const float* value;
     uint32_t* rep;     // InsertReport: applied count + mask (T bytes)
+    uint32_t* bad;     // set to 1 when the row is non-finite (KvStore::append's
+                       // DataError, core.cpp:71-79): nothing is appended or inserted
     uint32_t N;        // key index of the appended row (= pre-append N)
     uint32_t pad;
 };

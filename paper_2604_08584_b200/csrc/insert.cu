@@ -77,15 +77,31 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
     const InsertProblem& P = probs[blockIdx.x];
     const SessionDev& sd = *P.s;
     const uint32_t d = sd.d, m = sd.m, C = sd.C, T = m * C, N = P.N;
-    // KvStore::append: row N lands at tail row N - P (on the owner shard)
+    // KvStore::append rejects a non-finite row before touching the store
+    // (core.cpp:71-79): the whole append + insert is skipped and flagged (the
+    // host raises DataError), so the KV rows and tables stay as they were
+    int kbad = 0, vbad = 0;
     for (uint32_t x = threadIdx.x; x < d; x += blockDim.x) {
-        const float kx = P.key[x];
-        if (sd.owner) {
-            sd.ktail[static_cast<size_t>(N - sd.P) * d + x] = kx;
-            sd.vtail[static_cast<size_t>(N - sd.P) * d + x] = P.value[x];
-        }
+        const float kx = P.key[x], vx = P.value[x];
+        kbad |= !isfinite(kx);
+        vbad |= !isfinite(vx);
         S.ks[x] = kx;
     }
+    kbad = __syncthreads_or(kbad);
+    vbad = __syncthreads_or(vbad);
+    if (kbad | vbad) {  // 1: the key (checked first, as require_finite), 2: the value
+        if (threadIdx.x == 0) {
+            if (P.bad) *P.bad = kbad ? 1u : 2u;
+            P.rep[0] = 0u;
+        }
+        return;
+    }
+    // row N lands at tail row N - P (on the owner shard)
+    if (sd.owner)
+        for (uint32_t x = threadIdx.x; x < d; x += blockDim.x) {
+            sd.ktail[static_cast<size_t>(N - sd.P) * d + x] = S.ks[x];
+            sd.vtail[static_cast<size_t>(N - sd.P) * d + x] = P.value[x];
+        }
     if (threadIdx.x == 0) {
         S.zero_mask = 0;
         S.nref = 0;

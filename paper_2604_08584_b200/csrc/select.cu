@@ -107,11 +107,15 @@ __device__ __forceinline__ double absent_d() {
     return __longlong_as_double(static_cast<long long>(ABSENT));
 }
 // The tile accumulator marks "not gathered" with -0.0: a gathered key's sum
-// starts as 0.0 + w*s (reduce_by_key) and table scores are never -0.0f (they
-// are fp64 dot sums from +0.0; imports canonicalise), so no sum is -0.0 and
-// -0.0 + w*s == 0.0 + w*s.
+// starts as 0.0 + w*s (reduce_by_key). Table scores CAN be -0.0f (float() of a
+// negative dot below 2^-150, index.cpp:81 / retrieval.cpp:293-294), so every
+// term is canonicalised to +0.0 when zero (canon0 below): then no term and no
+// sum is -0.0, and -0.0 + x == 0.0 + x for every canonical term x.
 constexpr unsigned long long NEG0 = 0x8000000000000000ull;
 __device__ __forceinline__ double neg0_d() { return __longlong_as_double(static_cast<long long>(NEG0)); }
+__device__ __forceinline__ uint32_t canon0(uint32_t f32_bits) {  // -0.0f -> +0.0f
+    return f32_bits == 0x80000000u ? 0u : f32_bits;
+}
 __device__ __forceinline__ bool is_neg0(double v) {
     return static_cast<unsigned long long>(__double_as_longlong(v)) == NEG0;
 }
@@ -828,15 +832,19 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     double* const a2 = acc + ((v2 ? f.x : kbase) - kbase);
                     double* const a3 = acc + ((v3 ? f.z : kbase) - kbase);
                     const double o0 = *a0, o1 = *a1, o2 = *a2, o3 = *a3;
-                    double x0 = static_cast<double>(__uint_as_float(e.y));
-                    double x1 = static_cast<double>(__uint_as_float(e.w));
-                    double x2 = static_cast<double>(__uint_as_float(f.y));
-                    double x3 = static_cast<double>(__uint_as_float(f.w));
-                    if constexpr (!decltype(unit_weight)::value) {  // w * double(s)
-                        x0 = __dmul_rn(w, x0);
-                        x1 = __dmul_rn(w, x1);
-                        x2 = __dmul_rn(w, x2);
-                        x3 = __dmul_rn(w, x3);
+                    // a -0.0f table score (float(dot) of a tiny negative dot,
+                    // index.cpp:81) is a present key at 0.0 + (-0.0) = +0.0 in
+                    // reduce_by_key: canonicalise it so the sum never equals
+                    // the -0.0 "not gathered" marker
+                    double x0 = static_cast<double>(__uint_as_float(canon0(e.y)));
+                    double x1 = static_cast<double>(__uint_as_float(canon0(e.w)));
+                    double x2 = static_cast<double>(__uint_as_float(canon0(f.y)));
+                    double x3 = static_cast<double>(__uint_as_float(canon0(f.w)));
+                    if constexpr (!decltype(unit_weight)::value) {  // 0.0 + w * double(s)
+                        x0 = __dadd_rn(__dmul_rn(w, x0), 0.0);
+                        x1 = __dadd_rn(__dmul_rn(w, x1), 0.0);
+                        x2 = __dadd_rn(__dmul_rn(w, x2), 0.0);
+                        x3 = __dadd_rn(__dmul_rn(w, x3), 0.0);
                     }
                     if (v0) *a0 = __dadd_rn(o0, x0);
                     if (v1) *a1 = __dadd_rn(o1, x1);

@@ -9,6 +9,7 @@
 // reference with exact selected sets and output agreement (:113-151),
 // counters (:66-82, :153-168), stream exhaustion message (:179-196), and
 // table equality after streaming inserts (acceptance.cpp:229-267).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -217,6 +218,74 @@ static void dense_compare() {
     std::printf("dense compare: recall %.4f (step 0), l2 %.3g: done\n", *br[0].recall, *br[0].l2_error);
 }
 
+// k_bump (retrieval.cpp:257-263) is fed the worst best-cosine of the LAST
+// SEARCH: this query's on searching steps, the last searching query's on
+// reuse steps (period > 1). A cosine-dependent K makes any mix-up visible.
+// Then a mid-session change of the public Session::cfg (session.hpp:19-31)
+// reaches the device session before the next step.
+static void kbump_and_cfg(const char* schedule) {
+    const std::size_t P = 3000, T = 12, d = 64, m = 8;
+    R::SyntheticSpec spec;
+    spec.rows = P + T;
+    spec.dim = d;
+    spec.seed = 41;
+    const R::SyntheticWorkload w = R::make_synthetic(spec);
+    const std::span<const float> q(w.queries), k(w.keys), v(w.values);
+    R::IndexConfig ric;
+    ric.cluster.seed = 3;
+    ric.cluster.centroids = 16;
+    ric.score_bits = 32;
+    B::IndexConfig bic;
+    bic.cluster.seed = 3;
+    bic.cluster.centroids = 16;
+    bic.score_bits = 32;
+    const auto [rho, period] = R::parse_schedule(schedule);
+    auto bump = [](std::size_t kk, double worst) {
+        return kk + static_cast<std::size_t>(std::floor(4000.0 * (1.0 - worst)));
+    };
+    R::RetrievalConfig rrc;
+    rrc.keep_ratio = rho;
+    rrc.search_period = period;
+    rrc.k_bump = bump;
+    B::RetrievalConfig brc;
+    brc.keep_ratio = rho;
+    brc.search_period = period;
+    brc.k_bump = bump;
+    R::Session rs = R::prefill(q.subspan(0, P * d), k.subspan(0, P * d), v.subspan(0, P * d),
+                               R::SubspaceLayout::uniform(d, m), ric, rrc);
+    B::Session bs = B::prefill(q.subspan(0, P * d), k.subspan(0, P * d), v.subspan(0, P * d),
+                               B::SubspaceLayout::uniform(d, m), bic, brc, T);
+    std::size_t diff = 0, bumped = 0;
+    for (std::size_t t = 0; t < T; ++t) {
+        if (t == 7) {  // public cfg change between steps: window and weights
+            rs.cfg.recent_window = 8;
+            bs.cfg.recent_window = 8;
+            rs.cfg.weights.assign(m, 1.0);
+            rs.cfg.weights[2] = 2.5;
+            bs.cfg.weights = rs.cfg.weights;
+        }
+        const auto a = R::decode_step(rs, q.subspan((P + t) * d, d), k.subspan((P + t) * d, d),
+                                      v.subspan((P + t) * d, d), false);
+        const auto b = B::decode_step(bs, q.subspan((P + t) * d, d), k.subspan((P + t) * d, d),
+                                      v.subspan((P + t) * d, d), false);
+        diff += a.selected != b.selected || a.k != b.k || a.searched != b.searched;
+        bumped += a.k != R::keep_count(rho, P + t);
+    }
+    CHECK(diff == 0, "k_bump %s: %zu of %zu steps differ", schedule, diff, T);
+    CHECK(bumped > 0, "k_bump %s never changed K", schedule);
+    // a GQA session serves `group` queries per step: the single-query calls refuse it
+    std::vector<float> q4(4 * P * d);
+    for (std::size_t r = 0; r < 4; ++r)
+        std::copy(q.begin(), q.begin() + P * d, q4.begin() + r * P * d);
+    B::Session g4 = B::prefill(q4, k.subspan(0, P * d), v.subspan(0, P * d),
+                               B::SubspaceLayout::uniform(d, m), bic, B::RetrievalConfig{}, 4, 4);
+    const std::string e = thrown<B::ParameterError>([&] {
+        B::decode_step(g4, q.subspan(P * d, d), k.subspan(P * d, d), v.subspan(P * d, d), false);
+    });
+    CHECK(e.find("GQA group of 4") != std::string::npos, "group refusal: '%s'", e.c_str());
+    std::printf("k_bump %s + cfg change: %zu/%zu steps equal, %zu bumped\n", schedule, T - diff, T, bumped);
+}
+
 static void errors() {
     const std::size_t d = 16, P = 64;
     std::vector<float> q(P * d, 0.5f), k(P * d, 0.25f), v(P * d, 1.0f);
@@ -265,6 +334,8 @@ int main() {
     lifecycle(4096, 12, 128, 8, 2026, "0.05-step-1", true);   // BASELINE config 1
     lifecycle(2000, 10, 64, 8, 7, "0.15-step-4", true);       // period reuse
     lifecycle(1500, 6, 64, 4, 11, "0.05-step-1", false);      // window competes
+    kbump_and_cfg("0.05-step-1");
+    kbump_and_cfg("0.15-step-4");
     if (failures) {
         std::printf("%d FAILURES\n", failures);
         return 1;
