@@ -828,9 +828,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         max_tiles = std::max(max_tiles, nt);
     }
     uint32_t split = 1;
-    const uint64_t slots = 2ull * static_cast<uint64_t>(ctx->num_sms);  // select CTAs resident
+    const uint64_t slots = static_cast<uint64_t>(csa::select_ctas_per_sm()) * ctx->num_sms;  // resident
     if (nq < slots && !ctx->no_split) {
-        split = static_cast<uint32_t>((2ull * ctx->num_sms + nq - 1) / nq);
+        split = static_cast<uint32_t>((slots + nq - 1) / nq);
         split = static_cast<uint32_t>(std::min<uint64_t>(std::min<uint64_t>(split, 16), min_tiles));
         split = std::max<uint32_t>(split, 1);
     }
@@ -1889,7 +1889,7 @@ csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t ns, const csattn_sessio
                 const uint64_t khi = ss[i]->h.owner ? ss[i]->N : ss[i]->h.key_hi;
                 mintiles = std::min(mintiles, (khi - ss[i]->h.key_lo + tile - 1) / tile);
             }
-            const uint64_t slots = 2ull * static_cast<uint64_t>(ctx->num_sms);
+            const uint64_t slots = static_cast<uint64_t>(csa::select_ctas_per_sm()) * ctx->num_sms;
             // (default 1: the shard phases after the scan walk every part's log;
             // CSATTN_SHARD_SPLIT=1 enables part units here)
             uint64_t split = (nq < slots && ctx->shard_split) ? (slots + nq - 1) / nq : 1;

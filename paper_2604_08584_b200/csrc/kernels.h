@@ -30,6 +30,7 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
 // log_cap entries each, unit_meta: select_unit_meta_words() per unit) and
 // finalised by the merge kernel (one CTA per problem).
 uint32_t select_unit_meta_words();
+uint32_t select_ctas_per_sm();  // resident select CTAs per SM (grid = this x SMs)
 uint32_t select_tile_keys();
 cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 uint32_t split, const uint32_t* unit_meta, const uint32_t* log_idx,

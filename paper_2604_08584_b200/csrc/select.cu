@@ -70,11 +70,13 @@ static_assert(TILE * 64 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bi
 static_assert(SELECT_MAX_CONTEXT / TILE <= 128 && MAXL < 127, "chunk info fields");
 static_assert(UNIT_META == NB + NCB + SEL_CW && SEL_CW == 8, "unit metadata layout");
 
-// One ring chunk: info = list | flags << 7 | tile << 10; entries at table
-// positions [lo, hi), staged from position `base` (even, 16-byte aligned).
+// One ring chunk: info = list | flags << 7 | tile << 10; the chunk stages the
+// table positions from `base` (even, 16-byte aligned). wr[w] = consumer warp
+// w's entries as slot-relative positions [x, y) (its own key range of the
+// tile intersected with the chunk; y <= x when it has none).
 struct SlotMeta {
-    uint32_t info, base, lo, hi;
-    uint32_t wb[SEL_CW + 1];  // table position of consumer warp w's first key: warp w owns [wb[w], wb[w+1])
+    uint32_t info, base, pad0, pad1;
+    uint2 wr[SEL_CW];
 };
 static_assert(WKEYS % KEY_BLOCK == 0, "warp key ranges are whole key blocks");
 constexpr uint32_t WBLKS = WKEYS / KEY_BLOCK;  // key blocks per warp range
@@ -664,13 +666,18 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             const uint32_t slot = c % NSLOT;
             if (c >= static_cast<uint32_t>(NSLOT))
                 mbar_wait_sleep(&S.empty[slot], ((c / NSLOT) - 1) & 1u);
-            if (wb && ln <= SEL_CW) S.meta[slot].wb[ln] = wb[ln];
+            if (ln < SEL_CW) {  // consumer warp ln's slot-relative entry range
+                uint2 r = make_uint2(0u, 0u);
+                if (wb) {
+                    const uint32_t a = max(lo, wb[ln]), b = min(hi, wb[ln + 1]);
+                    r = b > a ? make_uint2(a - base, b - base) : make_uint2(0u, 0u);
+                }
+                S.meta[slot].wr[ln] = r;
+            }
             __syncwarp();  // lane 0's arrive below releases the other lanes' writes too
             if (ln == 0) {
                 S.meta[slot].info = info;
                 S.meta[slot].base = base;
-                S.meta[slot].lo = lo;
-                S.meta[slot].hi = hi;
                 if (bytes) {
                     mbar_expect_tx(&S.full[slot], bytes);
                     bulk_g2s_hint(ring + static_cast<size_t>(slot) * SLOT_E, src, bytes,
@@ -710,33 +717,48 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                                       : __ldcg(n_used + t);
             };
             // per-warp key-range bounds of every list in tile `tile` (the
-            // consumer warps own fixed 512-key ranges: no per-list barrier)
-            auto warp_bounds = [&](uint32_t tile) {
-                const uint32_t n = nl * (SEL_CW + 1);
+            // consumer warps own fixed 512-key ranges: no per-list barrier):
+            // nl x (SEL_CW + 1) table positions, three per lane. Loaded one
+            // tile ahead into registers (issued before the current tile's
+            // chunks are published, stored after), so the blk_off misses
+            // overlap the ring waits instead of stalling the stream.
+            const uint32_t nwb = nl * (SEL_CW + 1);
+            auto wb_load = [&](uint32_t tile, uint32_t (&v)[3]) {
+#pragma unroll
+                for (int u = 0; u < 3; ++u) {
+                    const uint32_t idx = u * 32 + ln;
+                    v[u] = 0;
+                    if (idx < nwb && tile < ntile) {
+                        const uint32_t l = idx / (SEL_CW + 1), j = idx - l * (SEL_CW + 1);
+                        const uint32_t t = S.plist[l];
+                        const uint32_t kb = tile * TILE_BLKS + j * WBLKS;
+                        v[u] = kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
+                                              : __ldcg(n_used + t);
+                    }
+                }
+            };
+            auto wb_store = [&](uint32_t tile, const uint32_t (&v)[3]) {
                 uint32_t* const dst = &S.wbs[tile & 1][0][0];
-                for (uint32_t b0_ = 0; b0_ < n; b0_ += 96) {
-                    uint32_t v[3];
 #pragma unroll
-                    for (int u = 0; u < 3; ++u) {
-                        const uint32_t idx = b0_ + u * 32 + ln;
-                        v[u] = 0;
-                        if (idx < n) {
-                            const uint32_t l = idx / (SEL_CW + 1), j = idx - l * (SEL_CW + 1);
-                            const uint32_t t = S.plist[l];
-                            const uint32_t kb = tile * TILE_BLKS + j * WBLKS;
-                            v[u] = kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
-                                                  : __ldcg(n_used + t);
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 3; ++u) {
-                        const uint32_t idx = b0_ + u * 32 + ln;
-                        if (idx < n) dst[idx] = v[u];
-                    }
+                for (int u = 0; u < 3; ++u) {
+                    const uint32_t idx = u * 32 + ln;
+                    if (idx < nwb) dst[idx] = v[u];
+                }
+                // more than 10 lists (tau > 1 backoff): the rest synchronously
+                for (uint32_t idx = 96 + ln; idx < nwb; idx += 32) {
+                    const uint32_t l = idx / (SEL_CW + 1), j = idx - l * (SEL_CW + 1);
+                    const uint32_t t = S.plist[l];
+                    const uint32_t kb = tile * TILE_BLKS + j * WBLKS;
+                    dst[idx] = kb <= last_blk ? __ldcg(blk_off + static_cast<size_t>(t) * nb_stride + kb)
+                                              : __ldcg(n_used + t);
                 }
                 __syncwarp();
             };
-            if (nl) warp_bounds(tl);
+            uint32_t wv[3];
+            if (nl) {
+                wb_load(tl, wv);
+                wb_store(tl, wv);
+            }
             uint32_t a0 = bound(tl, ln), a1 = bound(tl, ln + 32);
             uint32_t b0 = bound(tl + 1, ln), b1 = bound(tl + 1, ln + 32);
             for (uint32_t tile = tl; tile < ntile; ++tile) {
@@ -747,6 +769,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     continue;
                 }
                 const uint32_t c0 = bound(tile + 2, ln), c1 = bound(tile + 2, ln + 32);
+                wb_load(tile + 1, wv);  // stored after this tile's chunks are out
                 for (uint32_t l = 0; l < nl; ++l) {
                     const uint32_t e0 = __shfl_sync(0xffffffffu, l < 32 ? a0 : a1, l & 31);
                     const uint32_t e1 = __shfl_sync(0xffffffffu, l < 32 ? b0 : b1, l & 31);
@@ -768,9 +791,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                         pos = pe;
                     }
                 }
-                // next tile's warp bounds (the ring is usually full here, so the
-                // loads overlap the wait for a free slot)
-                if (tile + 1 < ntile) warp_bounds(tile + 1);
+                if (tile + 1 < ntile) wb_store(tile + 1, wv);
                 a0 = b0;
                 a1 = b1;
                 b0 = c0;
@@ -797,60 +818,74 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     double* wlog_sc = log_sc + log_base(kk);
     uint16_t* const wcidx = cidx + wid * WKEYS;
     double* const wacc = acc + wid * WKEYS;
-    uint32_t slot = 0, phase = 0;  // ring position of the next chunk
+    uint32_t slot = 0, phase = 0;  // ring position of the next chunk to fetch
     const uint32_t full0 = smem_u32(&S.full[0]), empty0 = smem_u32(&S.empty[0]);
-    const uint2* const ring0 = ring;
-    while (kk < nwork) {
+    const uint32_t ring_s = smem_u32(ring), acc_s = smem_u32(acc);
+    // A chunk = (info, this warp's slot-relative range wr, the first 128 of
+    // its entries in registers, its slot). (Fetching the next chunk before
+    // accumulating the current one measured 4x slower: not done.)
+    struct Chunk {
+        uint32_t info, slot;
+        uint2 wr;
+        uint2 e[4];
+    };
+    auto fetch = [&](Chunk& c) {  // the chunk at (slot, phase): wait, read, advance
         mbar_wait_sleep_u32(full0 + 8 * slot, phase);
-        struct {
-            uint32_t info, base, lo, hi;
-        } M = {S.meta[slot].info, S.meta[slot].base, S.meta[slot].lo, S.meta[slot].hi};
-        const uint32_t list = M.info & 127u, flags = (M.info >> 7) & 7u, tile = M.info >> 10;
+        c.slot = slot;
+        c.info = S.meta[slot].info;
+        c.wr = S.meta[slot].wr[wid];
+        const uint32_t eb = ring_s + slot * (SLOT_E * 8u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t q = c.wr.x + ln + 32u * u;
+            c.e[u] = lds_u2(eb + q * 8u);  // the ring has a 128-entry tail pad
+            if (q >= c.wr.y) c.e[u].x = TOMB;
+        }
+        if (++slot == NSLOT) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    };
+    auto rmw = [&](const uint2 (&e)[4], uint32_t accb, double w, auto unit_weight) {
+        double o[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (!(e[u].x & TOMB)) o[u] = lds_f64(accb + e[u].x * 8u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            // a -0.0f table score (float(dot) of a tiny negative dot,
+            // index.cpp:81) is a present key at 0.0 + (-0.0) = +0.0 in
+            // reduce_by_key: s + 0.0f canonicalises it, so no term (and no
+            // sum) equals the -0.0 "not gathered" marker
+            double x = static_cast<double>(__fadd_rn(__uint_as_float(e[u].y), 0.0f));
+            if constexpr (!decltype(unit_weight)::value)  // 0.0 + w * double(s)
+                x = __dadd_rn(__dmul_rn(w, x), 0.0);
+            if (!(e[u].x & TOMB)) sts_f64(accb + e[u].x * 8u, __dadd_rn(o[u], x));
+        }
+    };
+    Chunk cur;
+    fetch(cur);
+    while (kk < nwork) {
+        const uint32_t list = cur.info & 127u, flags = (cur.info >> 7) & 7u, tile = cur.info >> 10;
         const uint32_t kbase = tile * TILE;
         if (list != CACHE_LIST) {
-            // this warp's entries: those with keys in its own 512-key range
-            const uint32_t ga = max(M.lo, S.meta[slot].wb[wid]), gb = min(M.hi, S.meta[slot].wb[wid + 1]);
-            if (gb > ga) {
-                const uint32_t plo = ga - M.base, phi = gb - M.base;  // valid [plo, phi)
-                const uint32_t q0 = plo >> 1, q1 = (phi + 1) >> 1;
-                const uint4* st4 = reinterpret_cast<const uint4*>(ring0 + slot * SLOT_E);
+            if (cur.wr.y > cur.wr.x) {
+                const uint32_t accb = acc_s - kbase * 8u;  // shared address of key k: accb + 8k
                 const double w = S.cw[list];
-                // two pairs (four entries) per lane per step, all loads issued
-                // before the adds: keys are unique within a list, so the four
-                // read-modify-writes are independent
                 auto run = [&](auto unit_weight) {
-                for (uint32_t q = q0 + ln; q < q1; q += 64) {
-                    const bool h2 = q + 32 < q1;
-                    const uint4 e = st4[q];
-                    const uint4 f = h2 ? st4[q + 32] : make_uint4(TOMB, 0, TOMB, 0);
-                    const bool v0 = 2 * q >= plo && !(e.x & TOMB);
-                    const bool v1 = 2 * q + 1 < phi && !(e.z & TOMB);
-                    const bool v2 = !(f.x & TOMB);
-                    const bool v3 = 2 * q + 65 < phi && !(f.z & TOMB);
-                    double* const a0 = acc + ((v0 ? e.x : kbase) - kbase);
-                    double* const a1 = acc + ((v1 ? e.z : kbase) - kbase);
-                    double* const a2 = acc + ((v2 ? f.x : kbase) - kbase);
-                    double* const a3 = acc + ((v3 ? f.z : kbase) - kbase);
-                    const double o0 = *a0, o1 = *a1, o2 = *a2, o3 = *a3;
-                    // a -0.0f table score (float(dot) of a tiny negative dot,
-                    // index.cpp:81) is a present key at 0.0 + (-0.0) = +0.0 in
-                    // reduce_by_key: canonicalise it so the sum never equals
-                    // the -0.0 "not gathered" marker
-                    double x0 = static_cast<double>(__uint_as_float(canon0(e.y)));
-                    double x1 = static_cast<double>(__uint_as_float(canon0(e.w)));
-                    double x2 = static_cast<double>(__uint_as_float(canon0(f.y)));
-                    double x3 = static_cast<double>(__uint_as_float(canon0(f.w)));
-                    if constexpr (!decltype(unit_weight)::value) {  // 0.0 + w * double(s)
-                        x0 = __dadd_rn(__dmul_rn(w, x0), 0.0);
-                        x1 = __dadd_rn(__dmul_rn(w, x1), 0.0);
-                        x2 = __dadd_rn(__dmul_rn(w, x2), 0.0);
-                        x3 = __dadd_rn(__dmul_rn(w, x3), 0.0);
+                    rmw(cur.e, accb, w, unit_weight);
+                    // ranges longer than 128 entries: the rest from the slot
+                    const uint32_t eb = ring_s + cur.slot * (SLOT_E * 8u);
+                    for (uint32_t p0 = cur.wr.x + 128 + ln; p0 < cur.wr.y; p0 += 128) {
+                        uint2 e[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t q = p0 + 32u * u;
+                            e[u] = lds_u2(eb + q * 8u);
+                            if (q >= cur.wr.y) e[u].x = TOMB;
+                        }
+                        rmw(e, accb, w, unit_weight);
                     }
-                    if (v0) *a0 = __dadd_rn(o0, x0);
-                    if (v1) *a1 = __dadd_rn(o1, x1);
-                    if (v2) *a2 = __dadd_rn(o2, x2);
-                    if (v3) *a3 = __dadd_rn(o3, x3);
-                }
                 };
                 if (w == 1.0) run(std::true_type{});  // w * double(s) == double(s)
                 else run(std::false_type{});
@@ -868,14 +903,13 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             }
         }
         __syncwarp();
-        if (ln == 0) mbar_arrive_u32(empty0 + 8 * slot);
-        if (++slot == NSLOT) {
-            slot = 0;
-            phase ^= 1u;
-        }
+        if (ln == 0) mbar_arrive_u32(empty0 + 8 * cur.slot);
         // each warp owns its keys in every tile: lists accumulate in order per
         // key without a CTA barrier, and the filter reads only the warp's keys
-        if (!(flags & F_TILE_END)) continue;
+        if (!(flags & F_TILE_END)) {
+            fetch(cur);
+            continue;
+        }
 
         // ---- tile end: this warp's 512 keys -> pool candidates ----
         {
@@ -1016,7 +1050,10 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     atomicMax(&S.cut, static_cast<uint32_t>(b));
             }
         }
-        if (!(flags & F_PROB_END)) continue;
+        if (!(flags & F_PROB_END)) {
+            fetch(cur);
+            continue;
+        }
         cbar();  // every warp's log and histogram counts are in
 
         if (unit_meta) {  // part unit / shard: hand histogram + log lengths on
@@ -1038,6 +1075,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 wlog_idx = log_idx + log_base(kk);
                 wlog_sc = log_sc + log_base(kk);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
+                fetch(cur);  // the next problem's first chunk
             } else {
                 cbar();
             }
@@ -1068,6 +1106,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 wlog_idx = log_idx + log_base(kk);
                 wlog_sc = log_sc + log_base(kk);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
+                fetch(cur);  // the next problem's first chunk
             } else {
                 cbar();
             }
@@ -1433,7 +1472,7 @@ uint32_t shard_pstate_bytes() { return sizeof(ShardPState); }
 
 static size_t select_smem() {
     return ((sizeof(SelHdr) + 127) & ~size_t(127)) + TILE * 8 + (NB + NCB) * 4 + BKT * 12 +
-           SEL_CW * WKEYS * 2 + static_cast<size_t>(NSLOT) * SLOT_E * 8;
+           SEL_CW * WKEYS * 2 + (static_cast<size_t>(NSLOT) * SLOT_E + 128) * 8;
 }
 
 uint32_t select_grid(uint32_t nprob, int num_sms) {
@@ -1442,6 +1481,7 @@ uint32_t select_grid(uint32_t nprob, int num_sms) {
 }
 
 uint32_t select_unit_meta_words() { return UNIT_META; }
+uint32_t select_ctas_per_sm() { return 2; }
 uint32_t select_tile_keys() { return TILE; }
 
 cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,

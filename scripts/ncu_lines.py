@@ -1,31 +1,40 @@
-"""Per-CUDA-source-line instruction and stall totals from an ncu report.
-usage: python scripts/ncu_lines.py report.ncu-rep [top] [kernel-regex]"""
-import csv, io, subprocess, sys
-rep = sys.argv[1]
+"""Per-source-line totals from `ncu -i X --page source --csv --print-source sass,cuda`:
+instructions executed, stall samples, shared wavefronts. Usage:
+  python scripts/ncu_lines.py src.csv [top_n]"""
+import csv
+import sys
+
+path = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-kf = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
-out = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(out)))
-res = []
-f = None
-hdr = None
+rows = list(csv.reader(open(path)))
+fname, hdr, out = None, None, []
 for r in rows:
-    if len(r) == 2 and r[0] == "File Path":
-        f = r[1].split("/")[-1]
+    if not r:
         continue
-    if r and r[0] == "Line No":
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
         hdr = r
         continue
-    if hdr and r and r[0] not in ("", "Function Name"):
-        i_s = hdr.index("Warp Stall Sampling (All Samples)")
-        i_e = hdr.index("Instructions Executed")
+    if hdr is None or r[0] in ("", "Function Name"):
+        continue
+    try:
+        ln = int(r[0])
+    except ValueError:
+        continue
+    def g(name):
         try:
-            res.append((f, int(r[0]), r[1].strip()[:70], float(r[i_s] or 0), float(r[i_e] or 0)))
-        except ValueError:
-            pass
-ts = sum(x[3] for x in res) or 1
-te = sum(x[4] for x in res) or 1
-print(f"total samples {ts:.0f} inst {te:.0f}")
-for x in sorted(res, key=lambda x: -(x[3] / ts + x[4] / te))[:top]:
-    print(f"{x[0]:>12s}:{x[1]:<5d} stall {x[3] / ts * 100:5.1f}%  inst {x[4] / te * 100:5.1f}%  {x[2]}")
+            return float(r[hdr.index(name)])
+        except (ValueError, IndexError):
+            return 0.0
+    out.append((fname, ln, r[1].strip()[:70], g("Instructions Executed"), g("Warp Stall Sampling (All Samples)"),
+                g("L1 Wavefronts Shared"), g("L1 Wavefronts Shared Ideal")))
+ti = sum(o[3] for o in out) or 1
+ts = sum(o[4] for o in out) or 1
+tw = sum(o[5] for o in out) or 1
+print(f"total inst {ti:.3e}  stall samples {ts:.0f}  smem wavefronts {tw:.3e}")
+for key, lab in ((3, "instructions"), (4, "stall samples"), (5, "smem wavefronts")):
+    print(f"--- top by {lab}")
+    for o in sorted(out, key=lambda o: -o[key])[:top]:
+        print(f"{o[0]}:{o[1]:<5} inst {o[3]/ti*100:5.1f}%  stall {o[4]/ts*100:5.1f}%  smem {o[5]/tw*100:5.1f}% (ideal {o[6]/max(o[5],1):.2f})  {o[2]}")
