@@ -317,6 +317,57 @@ csattn_status csattn_dense_attention(csattn_session s, const float* q, const uin
 csattn_status csattn_dense_topk(csattn_session s, const float* q, uint64_t k, uint32_t* out,
                                 uint32_t flags);
 
+/* ---- Function-level API: the reference's free functions on host values ----
+ * (index.hpp:79-96, retrieval.hpp:40-118, core.hpp:96-102). All buffers are
+ * host memory; the work runs on ctx's device with the decode path's exact
+ * arithmetic. The C++ facade wraps them with the reference's signatures. */
+
+/* score_keys (index.cpp:68-91) generalised: for centroid j (widths[j] floats,
+ * packed one after another in `centroids`, scoring key dims
+ * [offsets[j], offsets[j] + widths[j])) and key i < n (keys: n x d):
+ * out[j*n + i] = float(sum_t double(c[t]) * double(k_i[off + t])).
+ * normalize: 0 raw keys; 1 score_keys' normalize_keys (divide by the slice
+ * norm, zero slice -> 0); 2 streaming_insert's (retrieval.cpp:283-291: score
+ * the l2_normalize'd f32 slice, zero slice -> 0). out64 (instead of out):
+ * the unrounded fp64 sums (centroid_scores, clustering.cpp:242-250). */
+csattn_status csattn_score_keys(csattn_ctx ctx, const float* centroids, uint64_t n_centroids,
+                                const uint64_t* offsets, const uint64_t* widths, const float* keys,
+                                uint64_t n, uint64_t d, int32_t normalize, float* out, double* out64);
+/* TopList::from_scores (index.cpp:46-62): the min(capacity, n) best of n
+ * scores by (score desc, index asc), in that order. */
+csattn_status csattn_toplist_from_scores(csattn_ctx ctx, const float* scores, uint64_t n,
+                                         uint64_t capacity, uint32_t* out_indices, float* out_scores,
+                                         uint64_t* out_len);
+/* select_centroids (retrieval.cpp:40-87) over unit centroids packed per
+ * subspace (C x widths[b] floats each, subspaces concatenated): ids[b*tau ..]
+ * the counts[b] selected centroid ids of subspace b (1, or up to tau on
+ * backoff), best_cosine[b], dot_ops. */
+csattn_status csattn_select_centroids(csattn_ctx ctx, const float* centroids, uint64_t c,
+                                      const uint64_t* widths, uint64_t m, const float* q,
+                                      uint64_t tau, double threshold, uint32_t* ids, uint32_t* counts,
+                                      double* best_cosine, uint64_t* dot_ops);
+/* reduce_by_key (retrieval.cpp:111-148): lists in gathered order with their
+ * weights (w_b of each list's subspace) -> ascending unique keys, fp64 sums
+ * of w * double(score) in list order, source counts. capacity bounds out_*. */
+csattn_status csattn_reduce_by_key(csattn_ctx ctx, uint64_t n_lists, const uint64_t* lens,
+                                   const uint32_t* const* indices, const float* const* scores,
+                                   const double* weights, uint32_t* out_indices, double* out_scores,
+                                   uint32_t* out_counts, uint64_t capacity, uint64_t* out_n);
+/* select_topk (retrieval.cpp:150-228) of a candidate set (ascending keys,
+ * fp64 scores) for a context of n keys: out gets K ascending indices (K =
+ * k_override ? min(k_override, n) : keep_count(rho, n)), *out_k = K. Runs the
+ * decode select kernel on the candidates as its cached scores. */
+csattn_status csattn_select_topk(csattn_ctx ctx, const uint32_t* cand_indices, const double* cand_scores,
+                                 uint64_t n_cand, uint64_t n, const csattn_retrieval_config* rcfg,
+                                 uint64_t k_override, uint32_t* out, uint64_t* out_k);
+/* dense_attention / dense_topk (core.cpp:118-192) over host rows (n x d). */
+csattn_status csattn_dense_attention_rows(csattn_ctx ctx, const float* q, const float* keys,
+                                          const float* values, uint64_t n, uint64_t d,
+                                          const uint32_t* mask, uint64_t n_mask, float* out,
+                                          float* weights);
+csattn_status csattn_dense_topk_rows(csattn_ctx ctx, const float* q, const float* keys, uint64_t n,
+                                     uint64_t d, uint64_t k, uint32_t* out);
+
 /* ---- CSAT v1 index image (index.hpp:98-121) ----
  * Little-endian image written by serialize_index (index.cpp:289-318) and
  * validated by deserialize_index (:320-396): "CSAT" | version u16 | flags u16 |

@@ -127,7 +127,7 @@ struct SubspaceLayout {
     }
     static SubspaceLayout uniform(std::size_t dim, std::size_t subspaces) {
         if (subspaces == 0 || subspaces > dim)
-            throw ParameterError("uniform layout needs 1 <= m <= d");
+            throw ParameterError("uniform layout requires 1 <= m <= d");
         std::vector<std::size_t> s(subspaces, dim / subspaces);
         for (std::size_t b = 0; b < dim % subspaces; ++b) s[b] += 1;
         return SubspaceLayout(std::move(s));
@@ -188,6 +188,39 @@ struct TopList {
     float min_score() const {
         return scores.empty() ? -std::numeric_limits<float>::infinity() : scores.back();
     }
+    // index.cpp:22-44: a full list admits (index, score) only when the score
+    // strictly beats its minimum (evicting it); sorted position by (score
+    // desc, index asc). A host value-type operation: the device tables of a
+    // Session take the same decision in insert.cu.
+    bool try_insert(std::uint32_t index, float score) {
+        if (capacity == 0) return false;
+        if (full()) {
+            if (!(score > scores.back())) return false;
+            scores.pop_back();
+            indices.pop_back();
+        }
+        std::size_t lo = 0, hi = scores.size();
+        while (lo < hi) {
+            const std::size_t mid = (lo + hi) / 2;
+            const bool precedes = scores[mid] != score ? scores[mid] > score : indices[mid] < index;
+            if (precedes) lo = mid + 1;
+            else hi = mid;
+        }
+        scores.insert(scores.begin() + static_cast<std::ptrdiff_t>(lo), score);
+        indices.insert(indices.begin() + static_cast<std::ptrdiff_t>(lo), index);
+        return true;
+    }
+    // index.cpp:46-62, on the device (defined below)
+    static TopList from_scores(std::span<const float> scores, std::uint32_t capacity);
+};
+
+// clustering.hpp:31-41
+struct FitStats {
+    std::vector<double> objective;
+    std::size_t reseeded = 0;
+    std::size_t degenerate_points = 0;
+    std::size_t duplicated_seeds = 0;
+    std::size_t dot_ops = 0;
 };
 
 struct CentroidSet {
@@ -195,6 +228,8 @@ struct CentroidSet {
     std::vector<float> centroids;  // count x dim, unit rows
     std::size_t count = 0;
     std::size_t dim = 0;
+    FitStats stats;
+    std::span<const float> centroid(std::size_t j) const { return {centroids.data() + j * dim, dim}; }
 };
 
 // Host image of the device tables (Session::export_index).
@@ -309,6 +344,466 @@ class Context {
    private:
     csattn_ctx h_ = nullptr;
 };
+
+// ===========================================================================
+// Function-level API (core.hpp:47-102, index.hpp:79-96, retrieval.hpp:40-118):
+// the reference's free functions on host values. Compute runs on the device
+// through the C ABI (score_keys / TopList::from_scores / select_centroids /
+// reduce_by_key / select_topk / dense_attention / dense_topk / the insert
+// scoring); container bookkeeping (KvStore rows, gather_lists views,
+// TopList::try_insert on a host list) stays with the host value, as in the
+// reference. A Session is the device-resident form of the same path.
+// ===========================================================================
+
+// ---- core.hpp:47-68 / core.cpp:52-88 ----
+class KvStore {
+   public:
+    explicit KvStore(std::size_t dim) : dim_(dim) {
+        if (dim == 0) throw ParameterError("head dimension must be >= 1");
+    }
+    KvStore(std::size_t dim, std::span<const float> prefill_keys, std::span<const float> prefill_values)
+        : KvStore(dim) {
+        if (prefill_keys.size() % dim != 0 || prefill_values.size() % dim != 0)
+            throw DimensionError("prefill rows are not a multiple of d");
+        if (prefill_keys.size() != prefill_values.size())
+            throw DimensionError("prefill key/value counts differ");
+        require_finite(prefill_keys, "prefill keys");
+        require_finite(prefill_values, "prefill values");
+        keys_.assign(prefill_keys.begin(), prefill_keys.end());
+        values_.assign(prefill_values.begin(), prefill_values.end());
+        prefill_len_ = prefill_keys.size() / dim;
+        total_len_ = prefill_len_;
+    }
+    void append(std::span<const float> key, std::span<const float> value) {
+        if (key.size() != dim_ || value.size() != dim_)
+            throw DimensionError("appended key/value width does not match d");
+        require_finite(key, "appended key");
+        require_finite(value, "appended value");
+        keys_.insert(keys_.end(), key.begin(), key.end());
+        values_.insert(values_.end(), value.begin(), value.end());
+        total_len_ += 1;
+    }
+    std::span<const float> key(std::size_t i) const { return {keys_.data() + i * dim_, dim_}; }
+    std::span<const float> value(std::size_t i) const { return {values_.data() + i * dim_, dim_}; }
+    std::size_t dim() const { return dim_; }
+    std::size_t size() const { return total_len_; }
+    std::size_t prefill_len() const { return prefill_len_; }
+    const float* key_data() const { return keys_.data(); }
+    const float* value_data() const { return values_.data(); }
+
+   private:
+    static void require_finite(std::span<const float> v, const char* what) {
+        for (float x : v)
+            if (!std::isfinite(x)) throw DataError(std::string(what) + " contains a non-finite value");
+    }
+    std::size_t dim_;
+    std::size_t prefill_len_ = 0;
+    std::size_t total_len_ = 0;
+    std::vector<float> keys_, values_;
+};
+
+// core.cpp:89-116: value helpers the callers use to prepare inputs
+inline double dot(std::span<const float> a, std::span<const float> b) {
+    double acc = 0.0;
+    for (std::size_t i = 0; i < a.size(); ++i) acc += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+    return acc;
+}
+inline std::vector<std::span<const float>> split_subspaces(std::span<const float> v, const SubspaceLayout& layout) {
+    if (v.size() != layout.dim())
+        throw DimensionError("vector length " + std::to_string(v.size()) + " does not match layout dimension " +
+                             std::to_string(layout.dim()));
+    std::vector<std::span<const float>> out;
+    for (std::size_t b = 0; b < layout.count(); ++b) out.push_back(layout.slice(v, b));
+    return out;
+}
+inline bool l2_normalize(std::span<float> v) {
+    double norm2 = 0.0;
+    for (float x : v) norm2 += static_cast<double>(x) * static_cast<double>(x);
+    if (norm2 == 0.0) return true;
+    const double inv = 1.0 / std::sqrt(norm2);
+    for (float& x : v) x = static_cast<float>(x * inv);
+    return false;
+}
+
+// core.cpp:118-169 (masked or full), on the device
+inline AttentionOutput dense_attention(std::span<const float> q, const KvStore& kv,
+                                       std::optional<std::span<const std::uint32_t>> mask = std::nullopt,
+                                       Context& ctx = Context::default_context()) {
+    if (kv.size() == 0) throw ParameterError("attention over an empty KV store");
+    if (q.size() != kv.dim()) throw DimensionError("query width does not match KV dimension");
+    if (mask && mask->empty()) throw ParameterError("attention over an empty index set");
+    const std::size_t rows = mask ? mask->size() : kv.size();
+    AttentionOutput out;
+    out.output.resize(kv.dim());
+    out.weights.resize(rows);
+    check(csattn_dense_attention_rows(ctx.handle(), q.data(), kv.key_data(), kv.value_data(), kv.size(),
+                                      kv.dim(), mask ? mask->data() : nullptr, mask ? mask->size() : 0,
+                                      out.output.data(), out.weights.data()));
+    return out;
+}
+
+// core.cpp:171-192, on the device
+inline std::vector<std::uint32_t> dense_topk(std::span<const float> q, const KvStore& kv, std::size_t k,
+                                             Context& ctx = Context::default_context()) {
+    if (k < 1 || k > kv.size()) throw ParameterError("top-k count out of range: " + std::to_string(k));
+    if (q.size() != kv.dim()) throw DimensionError("query width does not match KV dimension");
+    std::vector<std::uint32_t> out(k);
+    check(csattn_dense_topk_rows(ctx.handle(), q.data(), kv.key_data(), kv.size(), kv.dim(), k, out.data()));
+    return out;
+}
+
+// clustering.cpp:242-250: every centroid's fp64 dot with v (v as given), on the device
+inline std::vector<double> centroid_scores(std::span<const float> v, const CentroidSet& cs,
+                                           Context& ctx = Context::default_context()) {
+    if (v.size() != cs.dim) throw DimensionError("vector width does not match centroid width");
+    std::vector<double> out(cs.count);
+    if (cs.count == 0) return out;
+    std::vector<uint64_t> off(cs.count, 0), wid(cs.count, cs.dim);
+    check(csattn_score_keys(ctx.handle(), cs.centroids.data(), cs.count, off.data(), wid.data(), v.data(), 1,
+                            cs.dim, 0, nullptr, out.data()));
+    return out;
+}
+
+inline TopList TopList::from_scores(std::span<const float> scores, std::uint32_t capacity) {
+    TopList l;
+    l.capacity = capacity;
+    const std::size_t keep = std::min<std::size_t>(capacity, scores.size());
+    l.indices.resize(keep);
+    l.scores.resize(keep);
+    if (keep == 0) return l;
+    uint64_t n = 0;
+    check(csattn_toplist_from_scores(Context::default_context().handle(), scores.data(), scores.size(), capacity,
+                                     l.indices.data(), l.scores.data(), &n));
+    return l;
+}
+
+// ---- index.hpp:79-96 ----
+struct BuildStats {
+    std::size_t cluster_dot_ops = 0;  // not reported by the device k-means (stays 0)
+    std::size_t score_dot_ops = 0;
+};
+
+// index.cpp:68-91, on the device
+inline std::vector<float> score_keys(std::span<const float> centroid, const KvStore& kv,
+                                     const SubspaceLayout& layout, std::size_t b, bool normalize_keys,
+                                     std::size_t n_keys, Context& ctx = Context::default_context()) {
+    if (b >= layout.count()) throw ParameterError("subspace id out of range");
+    if (centroid.size() != layout.sizes[b]) throw DimensionError("centroid width does not match subspace width");
+    if (n_keys > kv.size()) throw ParameterError("asked to score more keys than the store holds");
+    std::vector<float> out(n_keys);
+    if (n_keys == 0) return out;
+    const uint64_t off = layout.offsets[b], wid = layout.sizes[b];
+    check(csattn_score_keys(ctx.handle(), centroid.data(), 1, &off, &wid, kv.key_data(), n_keys, kv.dim(),
+                            normalize_keys ? 1 : 0, out.data(), nullptr));
+    return out;
+}
+
+namespace detail {
+inline void validate_index_config(const IndexConfig& c) {
+    if (c.list_capacity == 0 && !(c.alpha > 0.0 && c.alpha <= 1.0))
+        throw ParameterError("alpha must lie in (0, 1]");
+    if (c.score_bits != 16 && c.score_bits != 32) throw ParameterError("score width must be 16 or 32 bits");
+    if (c.cluster.centroids == 0) throw ParameterError("centroid count must be >= 1");
+}
+// the tables of a device session, as the host CsIndex (TopList order)
+inline CsIndex index_of(csattn_session h, const SubspaceLayout& layout) {
+    csattn_session_info in{};
+    check(csattn_session_info_get(h, &in));
+    const std::size_t T = in.subspaces * in.centroids;
+    const std::size_t stride = std::max<std::size_t>(in.list_capacity, 1);
+    std::vector<uint32_t> lens(T), idx(T * stride);
+    std::vector<float> sc(T * stride), cent(in.centroids * in.dim);
+    check(csattn_session_export(h, lens.data(), idx.data(), sc.data(), stride, cent.data()));
+    CsIndex ix(layout);
+    ix.alpha = in.alpha;
+    ix.list_capacity = static_cast<uint32_t>(in.list_capacity);
+    ix.prefill_len = in.prefill_len;
+    ix.normalize_keys = in.normalize_keys != 0;
+    ix.score_bits = in.score_bits;
+    for (std::size_t b = 0; b < layout.count(); ++b) {
+        CentroidSet cs;
+        cs.subspace_id = b;
+        cs.count = in.centroids;
+        cs.dim = layout.sizes[b];
+        const float* src = cent.data() + in.centroids * layout.offsets[b];
+        cs.centroids.assign(src, src + cs.count * cs.dim);
+        ix.centroid_sets.push_back(std::move(cs));
+    }
+    for (std::size_t t = 0; t < T; ++t) {
+        TopList l;
+        l.capacity = static_cast<uint32_t>(in.list_capacity);
+        l.indices.assign(idx.begin() + t * stride, idx.begin() + t * stride + lens[t]);
+        l.scores.assign(sc.begin() + t * stride, sc.begin() + t * stride + lens[t]);
+        ix.tables.push_back(std::move(l));
+    }
+    return ix;
+}
+struct SessionHandle {  // a transient device session
+    csattn_session h = nullptr;
+    ~SessionHandle() {
+        if (h) csattn_session_destroy(h);
+    }
+};
+}  // namespace detail
+
+// index.cpp:145-177: device k-means per subspace + device tables, exported
+inline CsIndex build_index(std::span<const float> queries, std::size_t query_count, const KvStore& kv,
+                           const SubspaceLayout& layout, const IndexConfig& config, BuildStats* stats = nullptr,
+                           Context& ctx = Context::default_context()) {
+    detail::validate_index_config(config);
+    if (query_count == 0) throw ParameterError("need at least one query row");
+    if (queries.size() != query_count * layout.dim()) throw DimensionError("query buffer does not match count x d");
+    if (layout.dim() != kv.dim()) throw DimensionError("layout dimension does not match KV dimension");
+    if (kv.prefill_len() == 0) throw ParameterError("cannot build over an empty prefill");
+    const std::size_t d = kv.dim(), p = kv.prefill_len();
+    std::vector<uint64_t> widths(layout.sizes.begin(), layout.sizes.end());
+    const csattn_index_config ic = config.c();
+    const csattn_retrieval_config rc = RetrievalConfig{}.c();
+    detail::SessionHandle s;
+    check(csattn_prefill(ctx.handle(), queries.data(), query_count, kv.key_data(), kv.value_data(), p, d,
+                         widths.data(), widths.size(), &ic, &rc, 1, 1, CSATTN_HOST_BUFFERS, &s.h));
+    CsIndex ix = detail::index_of(s.h, layout);
+    if (stats) stats->score_dot_ops += p * d * ix.centroids_per_subspace();
+    return ix;
+}
+
+// index.cpp:179-202: the same tables from given centroids, on the device
+inline CsIndex build_index_from_centroids(std::vector<CentroidSet> centroid_sets, const KvStore& kv,
+                                          const SubspaceLayout& layout, const IndexConfig& config,
+                                          BuildStats* stats = nullptr,
+                                          Context& ctx = Context::default_context()) {
+    detail::validate_index_config(config);
+    if (layout.dim() != kv.dim()) throw DimensionError("layout dimension does not match KV dimension");
+    if (kv.prefill_len() == 0) throw ParameterError("cannot build over an empty prefill");
+    if (centroid_sets.size() != layout.count()) throw DimensionError("need one centroid set per subspace");
+    const std::size_t c = centroid_sets[0].count;
+    if (c == 0) throw ParameterError("centroid sets are empty");
+    std::vector<float> packed;
+    for (std::size_t b = 0; b < centroid_sets.size(); ++b) {
+        if (centroid_sets[b].count != c) throw DimensionError("centroid counts differ across subspaces");
+        if (centroid_sets[b].dim != layout.sizes[b])
+            throw DimensionError("centroid width does not match subspace " + std::to_string(b));
+        packed.insert(packed.end(), centroid_sets[b].centroids.begin(),
+                      centroid_sets[b].centroids.begin() + static_cast<std::ptrdiff_t>(c * layout.sizes[b]));
+    }
+    const std::size_t d = kv.dim(), p = kv.prefill_len();
+    std::vector<uint64_t> widths(layout.sizes.begin(), layout.sizes.end());
+    IndexConfig cfg = config;
+    cfg.cluster.centroids = c;
+    const csattn_index_config ic = cfg.c();
+    const csattn_retrieval_config rc = RetrievalConfig{}.c();
+    detail::SessionHandle s;
+    check(csattn_prefill_from_centroids(ctx.handle(), packed.data(), c, kv.key_data(), kv.value_data(), p, d,
+                                        widths.data(), widths.size(), &ic, &rc, 1, 1, CSATTN_HOST_BUFFERS, &s.h));
+    CsIndex ix = detail::index_of(s.h, layout);
+    for (std::size_t b = 0; b < ix.centroid_sets.size(); ++b) ix.centroid_sets[b].stats = centroid_sets[b].stats;
+    if (stats) stats->score_dot_ops += p * d * c;
+    return ix;
+}
+
+// ---- retrieval.hpp:41-118 ----
+struct CandidateSet {
+    std::vector<std::uint32_t> indices;        // ascending
+    std::vector<double> scores;                // aligned weighted sums
+    std::vector<std::uint32_t> source_counts;  // contributing subspaces
+    std::size_t size() const { return indices.size(); }
+};
+
+struct CentroidSelection {
+    std::vector<std::vector<std::uint32_t>> per_subspace;
+    std::vector<double> best_cosine;
+    std::size_t dot_ops = 0;
+};
+
+// retrieval.cpp:40-87, on the device (route.cu)
+inline CentroidSelection select_centroids(std::span<const float> q, const CsIndex& index, std::size_t tau,
+                                          double threshold, Context& ctx = Context::default_context()) {
+    if (q.size() != index.layout.dim()) throw DimensionError("query width does not match index dimension");
+    if (tau == 0) throw ParameterError("backoff tau must be >= 1");
+    const std::size_t m = index.subspaces(), c = index.centroids_per_subspace();
+    std::vector<float> packed;
+    for (const CentroidSet& cs : index.centroid_sets)
+        packed.insert(packed.end(), cs.centroids.begin(), cs.centroids.end());
+    std::vector<uint64_t> widths(index.layout.sizes.begin(), index.layout.sizes.end());
+    std::vector<uint32_t> ids(m * tau), counts(m);
+    CentroidSelection sel;
+    sel.best_cosine.resize(m);
+    uint64_t dots = 0;
+    check(csattn_select_centroids(ctx.handle(), packed.data(), c, widths.data(), m, q.data(), tau, threshold,
+                                  ids.data(), counts.data(), sel.best_cosine.data(), &dots));
+    sel.dot_ops = dots;
+    for (std::size_t b = 0; b < m; ++b)
+        sel.per_subspace.emplace_back(ids.begin() + static_cast<std::ptrdiff_t>(b * tau),
+                                      ids.begin() + static_cast<std::ptrdiff_t>(b * tau + counts[b]));
+    return sel;
+}
+
+struct GatheredLists {
+    std::vector<const TopList*> lists;
+    std::vector<std::size_t> subspace;
+    std::size_t total_entries() const {
+        std::size_t n = 0;
+        for (const TopList* l : lists) n += l->indices.size();
+        return n;
+    }
+};
+
+// retrieval.cpp:95-109: views of the selected tables, (b, selection) order
+inline GatheredLists gather_lists(const CsIndex& index, const CentroidSelection& selection) {
+    if (selection.per_subspace.size() != index.subspaces())
+        throw DimensionError("selection does not cover every subspace");
+    GatheredLists out;
+    for (std::size_t b = 0; b < selection.per_subspace.size(); ++b)
+        for (std::uint32_t j : selection.per_subspace[b]) {
+            if (j >= index.centroids_per_subspace()) throw ParameterError("centroid id out of range");
+            out.lists.push_back(&index.table(b, j));
+            out.subspace.push_back(b);
+        }
+    return out;
+}
+
+// retrieval.cpp:111-148, on the device (fnapi.cu reduce_lists_kernel)
+inline CandidateSet reduce_by_key(const GatheredLists& gathered, std::span<const double> weights,
+                                  Context& ctx = Context::default_context()) {
+    const std::size_t nl = gathered.lists.size();
+    std::vector<uint64_t> lens(nl);
+    std::vector<const uint32_t*> idx(nl);
+    std::vector<const float*> sc(nl);
+    std::vector<double> w(nl);
+    for (std::size_t l = 0; l < nl; ++l) {
+        const std::size_t b = gathered.subspace[l];
+        if (b >= weights.size()) throw DimensionError("need one weight per subspace");
+        w[l] = weights[b];
+        lens[l] = gathered.lists[l]->indices.size();
+        idx[l] = gathered.lists[l]->indices.data();
+        sc[l] = gathered.lists[l]->scores.data();
+    }
+    const std::size_t cap = gathered.total_entries();
+    CandidateSet out;
+    out.indices.resize(cap);
+    out.scores.resize(cap);
+    out.source_counts.resize(cap);
+    uint64_t n = 0;
+    if (cap)
+        check(csattn_reduce_by_key(ctx.handle(), nl, lens.data(), idx.data(), sc.data(), w.data(),
+                                   out.indices.data(), out.scores.data(), out.source_counts.data(), cap, &n));
+    out.indices.resize(n);
+    out.scores.resize(n);
+    out.source_counts.resize(n);
+    return out;
+}
+
+// retrieval.cpp:150-228, on the device (the decode select kernel over the
+// candidates as its cached scores)
+inline std::vector<std::uint32_t> select_topk(const CandidateSet& candidates, const KvStore& kv,
+                                              const RetrievalConfig& cfg, std::size_t k_override = 0,
+                                              Context& ctx = Context::default_context()) {
+    const std::size_t n = kv.size();
+    if (n == 0) throw ParameterError("cannot select from an empty context");
+    const std::size_t k = k_override ? std::min(k_override, n) : keep_count(cfg.keep_ratio, n);
+    std::vector<std::uint32_t> out(k);
+    uint64_t got = 0;
+    const csattn_retrieval_config rc = cfg.c();
+    check(csattn_select_topk(ctx.handle(), candidates.indices.data(), candidates.scores.data(), candidates.size(),
+                             n, &rc, k_override, out.data(), &got));
+    out.resize(got);
+    return out;
+}
+
+struct SearchState {
+    std::size_t step = 0;
+    CandidateSet cached;
+    bool has_cache = false;
+    CentroidSelection last_selection;
+};
+
+struct SearchResult {
+    std::vector<std::uint32_t> selected;
+    std::size_t k = 0;
+    bool searched = false;
+    std::size_t centroid_dot_ops = 0;
+    std::size_t gathered_entries = 0;
+    std::size_t reduce_ops = 0;
+};
+
+// retrieval.cpp:230-270: the same composition, each stage on the device
+inline SearchResult decode_search(std::span<const float> q, const CsIndex& index, const KvStore& kv,
+                                  const RetrievalConfig& cfg, SearchState& state,
+                                  Context& ctx = Context::default_context()) {
+    if (cfg.search_period == 0) throw ParameterError("search period must be >= 1");
+    SearchResult result;
+    result.searched = !state.has_cache || state.step % cfg.search_period == 0;
+    if (result.searched) {
+        CentroidSelection sel = select_centroids(q, index, cfg.backoff_tau, cfg.backoff_threshold, ctx);
+        const GatheredLists gathered = gather_lists(index, sel);
+        std::vector<double> ones;
+        std::span<const double> w = cfg.weights;
+        if (w.empty()) {
+            ones.assign(index.subspaces(), 1.0);
+            w = ones;
+        } else if (w.size() != index.subspaces()) {
+            throw DimensionError("need one weight per subspace");
+        }
+        result.centroid_dot_ops = sel.dot_ops;
+        result.gathered_entries = gathered.total_entries();
+        result.reduce_ops = result.gathered_entries;
+        state.cached = reduce_by_key(gathered, w, ctx);
+        state.last_selection = std::move(sel);
+        state.has_cache = true;
+    }
+    std::size_t k_override = 0;
+    if (cfg.k_bump) {
+        double worst = 1.0;
+        for (double c : state.last_selection.best_cosine) worst = std::min(worst, c);
+        k_override = cfg.k_bump(keep_count(cfg.keep_ratio, kv.size()), worst);
+    }
+    result.selected = select_topk(state.cached, kv, cfg, k_override, ctx);
+    result.k = result.selected.size();
+    state.step += 1;
+    return result;
+}
+
+struct InsertReport {
+    std::size_t attempted = 0;
+    std::size_t applied = 0;
+    std::size_t dot_ops = 0;
+    std::vector<std::uint8_t> applied_mask;
+};
+
+// retrieval.cpp:272-301: the key's m x C scores on the device (the
+// l2_normalize'd slices when the index normalizes keys), then each host
+// table's strict-win admission
+inline InsertReport streaming_insert(std::span<const float> new_key, std::uint32_t key_index, CsIndex& index,
+                                     Context& ctx = Context::default_context()) {
+    if (new_key.size() != index.layout.dim()) throw DimensionError("key width does not match index dimension");
+    const std::size_t m = index.subspaces(), c = index.centroids_per_subspace();
+    InsertReport report;
+    report.applied_mask.assign(m * c, 0);
+    if (m * c == 0) return report;
+    std::vector<float> packed;
+    std::vector<uint64_t> off, wid;
+    for (std::size_t b = 0; b < m; ++b) {
+        const CentroidSet& cs = index.centroid_sets[b];
+        packed.insert(packed.end(), cs.centroids.begin(), cs.centroids.end());
+        for (std::size_t j = 0; j < c; ++j) {
+            off.push_back(index.layout.offsets[b]);
+            wid.push_back(index.layout.sizes[b]);
+        }
+    }
+    std::vector<float> s(m * c);
+    check(csattn_score_keys(ctx.handle(), packed.data(), m * c, off.data(), wid.data(), new_key.data(), 1,
+                            index.layout.dim(), index.normalize_keys ? 2 : 0, s.data(), nullptr));
+    for (std::size_t b = 0; b < m; ++b)
+        for (std::size_t j = 0; j < c; ++j) {
+            report.dot_ops += index.centroid_sets[b].dim;
+            report.attempted += 1;
+            if (index.table(b, j).try_insert(key_index, s[b * c + j])) {
+                report.applied += 1;
+                report.applied_mask[b * c + j] = 1;
+            }
+        }
+    return report;
+}
 
 // ---- session.hpp:19-42 ----
 struct DecodeStepReport {

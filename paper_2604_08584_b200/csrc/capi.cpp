@@ -2526,4 +2526,341 @@ csattn_status csattn_dense_topk(csattn_session s, const float* q, uint64_t k, ui
     });
 }
 
+// ---------------------------------------------------------------------------
+// Function-level API (the reference's free functions on host values,
+// index.hpp / retrieval.hpp / core.hpp): inputs are uploaded, the work runs on
+// the device with the hot path's arithmetic, results are copied back.
+// ---------------------------------------------------------------------------
+
+csattn_status csattn_score_keys(csattn_ctx ctx, const float* centroids, uint64_t n_centroids,
+                                const uint64_t* offsets, const uint64_t* widths, const float* keys,
+                                uint64_t n, uint64_t d, int32_t normalize, float* out, double* out64) {
+    return guard([&] {
+        if (normalize < 0 || normalize > 2) fail(CSATTN_ERR_PARAMETER, "normalize mode must be 0, 1 or 2");
+        if (n_centroids == 0 || n == 0) return;
+        std::vector<uint32_t> coff(n_centroids), kof(n_centroids), wid(n_centroids);
+        uint64_t cn = 0;
+        for (uint64_t j = 0; j < n_centroids; ++j) {
+            if (widths[j] == 0 || offsets[j] + widths[j] > d)
+                fail(CSATTN_ERR_DIMENSION, "centroid " + std::to_string(j) + " does not fit the key width");
+            coff[j] = static_cast<uint32_t>(cn);
+            kof[j] = static_cast<uint32_t>(offsets[j]);
+            wid[j] = static_cast<uint32_t>(widths[j]);
+            cn += widths[j];
+        }
+        cudaStream_t st = ctx->stream;
+        DevMem dc, dk, dm, dout;
+        dc.alloc(cn * 4);
+        dk.alloc(n * d * 4);
+        dm.alloc(n_centroids * 12);
+        dout.alloc(n_centroids * n * (out64 ? 8 : 4));
+        uint32_t* m = dm.as<uint32_t>();
+        ck(cudaMemcpyAsync(dc.p, centroids, cn * 4, cudaMemcpyHostToDevice, st), "score centroids");
+        ck(cudaMemcpyAsync(dk.p, keys, n * d * 4, cudaMemcpyHostToDevice, st), "score keys");
+        ck(cudaMemcpyAsync(m, coff.data(), n_centroids * 4, cudaMemcpyHostToDevice, st), "score meta");
+        ck(cudaMemcpyAsync(m + n_centroids, kof.data(), n_centroids * 4, cudaMemcpyHostToDevice, st), "score meta");
+        ck(cudaMemcpyAsync(m + 2 * n_centroids, wid.data(), n_centroids * 4, cudaMemcpyHostToDevice, st), "score meta");
+        ck(csa::launch_score_multi(dc.as<float>(), m, m + n_centroids, m + 2 * n_centroids,
+                                   static_cast<uint32_t>(n_centroids), dk.as<float>(), static_cast<uint32_t>(n),
+                                   static_cast<uint32_t>(d), normalize, out64 ? nullptr : dout.as<float>(),
+                                   out64 ? dout.as<double>() : nullptr, st),
+           "score launch");
+        if (out64)
+            ck(cudaMemcpyAsync(out64, dout.p, n_centroids * n * 8, cudaMemcpyDeviceToHost, st), "score out");
+        else
+            ck(cudaMemcpyAsync(out, dout.p, n_centroids * n * 4, cudaMemcpyDeviceToHost, st), "score out");
+        ck(cudaStreamSynchronize(st), "score keys");
+        ctx->launches += 1;
+    });
+}
+
+csattn_status csattn_toplist_from_scores(csattn_ctx ctx, const float* scores, uint64_t n,
+                                         uint64_t capacity, uint32_t* out_indices, float* out_scores,
+                                         uint64_t* out_len) {
+    return guard([&] {
+        const uint64_t keep = std::min(capacity, n);
+        *out_len = keep;
+        if (keep == 0) return;
+        if (n >= 0x7fffffffull) fail(CSATTN_ERR_PARAMETER, "too many scores");
+        cudaStream_t st = ctx->stream;
+        const size_t sb = csa::toplist_scratch_bytes(static_cast<uint32_t>(n));
+        DevMem ds, dsort, scratch;
+        ds.alloc(n * 4);
+        dsort.alloc(n * 8);
+        scratch.alloc(sb);
+        ck(cudaMemcpyAsync(ds.p, scores, n * 4, cudaMemcpyHostToDevice, st), "toplist scores");
+        ck(csa::launch_toplist(ds.as<float>(), static_cast<uint32_t>(n), dsort.as<unsigned long long>(),
+                               scratch.p, sb, st),
+           "toplist sort");
+        std::vector<unsigned long long> keys(keep);
+        ck(cudaMemcpyAsync(keys.data(), dsort.p, keep * 8, cudaMemcpyDeviceToHost, st), "toplist out");
+        ck(cudaStreamSynchronize(st), "toplist");
+        for (uint64_t r = 0; r < keep; ++r) {
+            const uint32_t i = ~static_cast<uint32_t>(keys[r]);
+            out_indices[r] = i;
+            out_scores[r] = scores[i];
+        }
+        ctx->launches += 2;
+    });
+}
+
+csattn_status csattn_select_centroids(csattn_ctx ctx, const float* centroids, uint64_t c,
+                                      const uint64_t* widths, uint64_t m, const float* q,
+                                      uint64_t tau, double threshold, uint32_t* ids, uint32_t* counts,
+                                      double* best_cosine, uint64_t* dot_ops) {
+    return guard([&] {
+        uint64_t d = 0;
+        for (uint64_t b = 0; b < m; ++b) d += widths[b];
+        validate_layout(widths, m, d);
+        if (c == 0 || c * m > csa::MAX_TABLES) fail(CSATTN_ERR_PARAMETER, "centroid count out of range");
+        if (tau == 0) fail(CSATTN_ERR_PARAMETER, "backoff tau must be >= 1");
+        const uint64_t take = std::min<uint64_t>(tau, c);
+        if (take > static_cast<uint64_t>(csa::MAXTAU))
+            fail(CSATTN_ERR_CAPACITY, "backoff tau above " + std::to_string(csa::MAXTAU) + " centroids");
+        cudaStream_t st = ctx->stream;
+        csa::SessionDev h{};
+        h.d = static_cast<uint32_t>(d);
+        h.m = static_cast<uint32_t>(m);
+        h.C = static_cast<uint32_t>(c);
+        uint64_t off = 0;
+        for (uint64_t b = 0; b < m; ++b) {
+            h.widths[b] = static_cast<uint32_t>(widths[b]);
+            h.offs[b] = static_cast<uint32_t>(off);
+            h.weights[b] = 1.0;
+            off += widths[b];
+        }
+        h.tau = static_cast<uint32_t>(take);
+        h.threshold = threshold;
+        h.passthrough = 1;
+        const uint64_t T = c * m;
+        DevMem dcent, dmeta, dsd, dprob, dplan, drep, dq;
+        dcent.alloc(c * d * 4);
+        dmeta.alloc(T * 12);  // tmm (float2) + live_g: zero (no tables)
+        dsd.alloc(sizeof(csa::SessionDev));
+        dprob.alloc(sizeof(csa::DecodeProblem));
+        dplan.alloc(sizeof(csa::RoutePlan));
+        drep.alloc(sizeof(csa::DecodeReport));
+        dq.alloc(d * 4);
+        ck(cudaMemsetAsync(dmeta.p, 0, T * 12, st), "route meta");
+        h.cent = dcent.as<float>();
+        h.tmm = dmeta.as<float2>();
+        h.live_g = reinterpret_cast<uint32_t*>(dmeta.as<char>() + T * 8);
+        csa::DecodeProblem P{};
+        P.s = dsd.as<csa::SessionDev>();
+        P.q = dq.as<float>();
+        P.rep = drep.as<uint32_t>();
+        P.mode = csa::MODE_SEARCH;
+        ck(cudaMemcpyAsync(dcent.p, centroids, c * d * 4, cudaMemcpyHostToDevice, st), "route centroids");
+        ck(cudaMemcpyAsync(dq.p, q, d * 4, cudaMemcpyHostToDevice, st), "route q");
+        ck(cudaMemcpyAsync(dsd.p, &h, sizeof(h), cudaMemcpyHostToDevice, st), "route session");
+        ck(cudaMemcpyAsync(dprob.p, &P, sizeof(P), cudaMemcpyHostToDevice, st), "route problem");
+        ck(csa::launch_route(dprob.as<csa::DecodeProblem>(), dplan.as<csa::RoutePlan>(), 1, st), "route launch");
+        csa::RoutePlan plan;
+        csa::DecodeReport rep;
+        ck(cudaMemcpyAsync(&plan, dplan.p, sizeof(plan), cudaMemcpyDeviceToHost, st), "route plan");
+        ck(cudaMemcpyAsync(&rep, drep.p, sizeof(rep), cudaMemcpyDeviceToHost, st), "route report");
+        ck(cudaStreamSynchronize(st), "route");
+        for (uint64_t b = 0; b < m; ++b) counts[b] = 0;
+        for (uint32_t l = 0; l < plan.nl; ++l) {
+            const uint32_t b = plan.lsub[l];
+            ids[b * tau + counts[b]] = plan.lists[l] - b * static_cast<uint32_t>(c);
+            counts[b] += 1;
+        }
+        for (uint64_t b = 0; b < m; ++b) best_cosine[b] = rep.best_cos[b];
+        *dot_ops = (static_cast<uint64_t>(rep.dot_ops_hi) << 32) | rep.dot_ops_lo;
+        ctx->launches += 1;
+    });
+}
+
+csattn_status csattn_reduce_by_key(csattn_ctx ctx, uint64_t n_lists, const uint64_t* lens,
+                                   const uint32_t* const* indices, const float* const* scores,
+                                   const double* weights, uint32_t* out_indices, double* out_scores,
+                                   uint32_t* out_counts, uint64_t capacity, uint64_t* out_n) {
+    return guard([&] {
+        std::vector<uint64_t> off(n_lists + 1, 0);
+        uint32_t nkeys = 0;
+        for (uint64_t l = 0; l < n_lists; ++l) {
+            off[l + 1] = off[l] + lens[l];
+            for (uint64_t r = 0; r < lens[l]; ++r) nkeys = std::max(nkeys, indices[l][r] + 1);
+        }
+        const uint64_t E = off[n_lists];
+        *out_n = 0;
+        if (E == 0) return;
+        std::vector<uint32_t> hidx(E);
+        std::vector<float> hsc(E);
+        for (uint64_t l = 0; l < n_lists; ++l) {
+            std::copy(indices[l], indices[l] + lens[l], hidx.begin() + off[l]);
+            std::copy(scores[l], scores[l] + lens[l], hsc.begin() + off[l]);
+        }
+        cudaStream_t st = ctx->stream;
+        DevMem doff, didx, dsc, dw, dacc, dcnt;
+        doff.alloc(off.size() * 8);
+        didx.alloc(E * 4);
+        dsc.alloc(E * 4);
+        dw.alloc(std::max<uint64_t>(n_lists, 1) * 8);
+        dacc.alloc(static_cast<size_t>(nkeys) * 8);
+        dcnt.alloc(static_cast<size_t>(nkeys) * 4);
+        ck(cudaMemcpyAsync(doff.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st), "reduce offsets");
+        ck(cudaMemcpyAsync(didx.p, hidx.data(), E * 4, cudaMemcpyHostToDevice, st), "reduce indices");
+        ck(cudaMemcpyAsync(dsc.p, hsc.data(), E * 4, cudaMemcpyHostToDevice, st), "reduce scores");
+        ck(cudaMemcpyAsync(dw.p, weights, n_lists * 8, cudaMemcpyHostToDevice, st), "reduce weights");
+        ck(csa::launch_reduce_lists(static_cast<uint32_t>(n_lists), doff.as<uint64_t>(), didx.as<uint32_t>(),
+                                    dsc.as<float>(), dw.as<double>(), dacc.as<double>(), dcnt.as<uint32_t>(),
+                                    nkeys, st),
+           "reduce launch");
+        std::vector<double> acc(nkeys);
+        std::vector<uint32_t> cnt(nkeys);
+        ck(cudaMemcpyAsync(acc.data(), dacc.p, nkeys * 8, cudaMemcpyDeviceToHost, st), "reduce out");
+        ck(cudaMemcpyAsync(cnt.data(), dcnt.p, nkeys * 4, cudaMemcpyDeviceToHost, st), "reduce counts");
+        ck(cudaStreamSynchronize(st), "reduce");
+        uint64_t n = 0;
+        for (uint32_t i = 0; i < nkeys; ++i) {
+            if (!cnt[i]) continue;
+            if (n >= capacity) fail(CSATTN_ERR_PARAMETER, "candidate capacity exceeded");
+            out_indices[n] = i;
+            out_scores[n] = acc[i];
+            out_counts[n] = cnt[i];
+            ++n;
+        }
+        *out_n = n;
+        ctx->launches += 1;
+    });
+}
+
+csattn_status csattn_select_topk(csattn_ctx ctx, const uint32_t* cand_indices, const double* cand_scores,
+                                 uint64_t n_cand, uint64_t n, const csattn_retrieval_config* rcfg,
+                                 uint64_t k_override, uint32_t* out, uint64_t* out_k) {
+    return guard([&] {
+        if (n == 0) fail(CSATTN_ERR_PARAMETER, "cannot select from an empty context");
+        if (n > csa::SELECT_MAX_CONTEXT)
+            fail(CSATTN_ERR_CAPACITY, "context of " + std::to_string(n) + " keys exceeds one GPU's decode search");
+        const uint64_t K = k_override ? std::min<uint64_t>(k_override, n) : keep_count(rcfg->keep_ratio, n);
+        *out_k = K;
+        const bool pt = rcfg->recent_passthrough != 0;
+        // the dense candidate-score array the select kernel reads in its
+        // cached-score mode (search_period reuse), absent keys NaN-boxed
+        std::vector<double> dense(n);
+        const unsigned long long absent = 0x7ff4deadbeef0000ull;
+        double absent_d;
+        std::memcpy(&absent_d, &absent, 8);
+        std::fill(dense.begin(), dense.end(), absent_d);
+        double lo = 0.0, hi = 0.0;
+        bool any = false;
+        for (uint64_t c = 0; c < n_cand; ++c) {
+            if (cand_indices[c] >= n) continue;
+            const double v = cand_scores[c];
+            dense[cand_indices[c]] = v;
+            lo = any ? std::min(lo, v) : v;
+            hi = any ? std::max(hi, v) : v;
+            any = true;
+        }
+        if (!pt) {  // window keys compete at 0 when absent
+            lo = std::min(lo, 0.0);
+            hi = std::max(hi, 0.0);
+        }
+        cudaStream_t st = ctx->stream;
+        csa::SessionDev h{};
+        h.window = static_cast<uint32_t>(std::min<uint64_t>(rcfg->recent_window, 0xffffffffull));
+        h.passthrough = pt ? 1 : 0;
+        const uint64_t log_cap = (n + csa::SELECT_LOG_ALIGN - 1) / csa::SELECT_LOG_ALIGN * csa::SELECT_LOG_ALIGN;
+        DevMem dsd, dprob, dplan, drep, dcache, dcb, dsel, dlog_i, dlog_s, dretry;
+        dsd.alloc(sizeof(csa::SessionDev));
+        dprob.alloc(sizeof(csa::DecodeProblem));
+        dplan.alloc(sizeof(csa::RoutePlan));
+        drep.alloc(sizeof(csa::DecodeReport));
+        dcache.alloc(n * 8);
+        dcb.alloc(4 * 8);
+        dsel.alloc(K * 4);
+        dlog_i.alloc(log_cap * 4);
+        dlog_s.alloc(log_cap * 8);
+        dretry.alloc(8);
+        const double cb[4] = {lo, hi, 0.0, 0.0};  // no speculation hint
+        csa::DecodeProblem P{};
+        P.s = dsd.as<csa::SessionDev>();
+        P.sel = dsel.as<uint32_t>();
+        P.cache = dcache.as<double>();
+        P.cbounds = dcb.as<double>();
+        P.rep = drep.as<uint32_t>();
+        P.N = static_cast<uint32_t>(n);
+        P.K = static_cast<uint32_t>(K);
+        P.n_cache = static_cast<uint32_t>(n);
+        P.mode = 0;  // no search: the cached (given) candidate scores
+        ck(cudaMemcpyAsync(dsd.p, &h, sizeof(h), cudaMemcpyHostToDevice, st), "topk session");
+        ck(cudaMemcpyAsync(dprob.p, &P, sizeof(P), cudaMemcpyHostToDevice, st), "topk problem");
+        ck(cudaMemcpyAsync(dcache.p, dense.data(), n * 8, cudaMemcpyHostToDevice, st), "topk candidates");
+        ck(cudaMemcpyAsync(dcb.p, cb, sizeof(cb), cudaMemcpyHostToDevice, st), "topk bounds");
+        ck(cudaMemsetAsync(dretry.p, 0, 8, st), "topk retry");
+        uint32_t* rc = dretry.as<uint32_t>();
+        ck(csa::launch_select(dprob.as<csa::DecodeProblem>(), dplan.as<csa::RoutePlan>(), 1, 1,
+                              dlog_i.as<uint32_t>(), dlog_s.as<double>(), static_cast<uint32_t>(log_cap),
+                              nullptr, nullptr, rc + 1, rc, 0.0, 1, nullptr, st),
+           "topk select launch");
+        ck(cudaMemcpyAsync(out, dsel.p, K * 4, cudaMemcpyDeviceToHost, st), "topk out");
+        ck(cudaStreamSynchronize(st), "select topk");
+        ctx->launches += 1;
+    });
+}
+
+csattn_status csattn_dense_attention_rows(csattn_ctx ctx, const float* q, const float* keys,
+                                          const float* values, uint64_t n, uint64_t d,
+                                          const uint32_t* mask, uint64_t n_mask, float* out,
+                                          float* weights) {
+    return guard([&] {
+        if (n == 0) fail(CSATTN_ERR_PARAMETER, "attention over an empty KV store");
+        uint64_t rows = n;
+        if (mask) {
+            if (n_mask == 0) fail(CSATTN_ERR_PARAMETER, "attention over an empty index set");
+            for (uint64_t r = 0; r < n_mask; ++r)
+                if (mask[r] >= n) fail(CSATTN_ERR_PARAMETER, "mask index " + std::to_string(mask[r]) + " out of range");
+            rows = n_mask;
+        }
+        cudaStream_t st = ctx->stream;
+        const size_t scratch = csa::dense_scratch_bytes(static_cast<uint32_t>(rows), static_cast<uint32_t>(d));
+        DevMem dk, dv, dq, dm, dout, dw, ds;
+        dk.alloc(n * d * 4);
+        dv.alloc(n * d * 4);
+        dq.alloc(d * 4);
+        dm.alloc(rows * 4);
+        dout.alloc(d * 4);
+        dw.alloc(rows * 4);
+        ds.alloc(scratch);
+        ck(cudaMemcpyAsync(dk.p, keys, n * d * 4, cudaMemcpyHostToDevice, st), "dense keys");
+        ck(cudaMemcpyAsync(dv.p, values, n * d * 4, cudaMemcpyHostToDevice, st), "dense values");
+        ck(cudaMemcpyAsync(dq.p, q, d * 4, cudaMemcpyHostToDevice, st), "dense q");
+        if (mask) ck(cudaMemcpyAsync(dm.p, mask, n_mask * 4, cudaMemcpyHostToDevice, st), "dense mask");
+        ck(csa::launch_dense_attention(dq.as<float>(), dk.as<float>(), nullptr, dv.as<float>(), nullptr,
+                                       static_cast<uint32_t>(n), mask ? dm.as<uint32_t>() : nullptr,
+                                       static_cast<uint32_t>(rows), static_cast<uint32_t>(d), dout.as<float>(),
+                                       weights ? dw.as<float>() : nullptr, ds.p, st),
+           "dense attention launch");
+        if (out) ck(cudaMemcpyAsync(out, dout.p, d * 4, cudaMemcpyDeviceToHost, st), "dense out");
+        if (weights) ck(cudaMemcpyAsync(weights, dw.p, rows * 4, cudaMemcpyDeviceToHost, st), "dense weights");
+        ck(cudaStreamSynchronize(st), "dense attention");
+        ctx->launches += 5;
+    });
+}
+
+csattn_status csattn_dense_topk_rows(csattn_ctx ctx, const float* q, const float* keys, uint64_t n,
+                                     uint64_t d, uint64_t k, uint32_t* out) {
+    return guard([&] {
+        if (k < 1 || k > n) fail(CSATTN_ERR_PARAMETER, "top-k count out of range: " + std::to_string(k));
+        cudaStream_t st = ctx->stream;
+        const size_t scratch = csa::dense_scratch_bytes(static_cast<uint32_t>(n), static_cast<uint32_t>(d));
+        DevMem dk, dq, dout, ds;
+        dk.alloc(n * d * 4);
+        dq.alloc(d * 4);
+        dout.alloc(k * 4);
+        ds.alloc(scratch);
+        ck(cudaMemcpyAsync(dk.p, keys, n * d * 4, cudaMemcpyHostToDevice, st), "topk keys");
+        ck(cudaMemcpyAsync(dq.p, q, d * 4, cudaMemcpyHostToDevice, st), "topk q");
+        ck(csa::launch_dense_topk(dq.as<float>(), dk.as<float>(), nullptr, static_cast<uint32_t>(n),
+                                  static_cast<uint32_t>(n), static_cast<uint32_t>(d), static_cast<uint32_t>(k),
+                                  dout.as<uint32_t>(), ds.p, scratch, st),
+           "dense topk launch");
+        ck(cudaMemcpyAsync(out, dout.p, k * 4, cudaMemcpyDeviceToHost, st), "topk out");
+        ck(cudaStreamSynchronize(st), "dense topk");
+        ctx->launches += 4;
+    });
+}
+
 }  // extern "C"

@@ -121,4 +121,16 @@ cudaError_t launch_build_lists(const SessionDev* s_dev, const SessionDev& s_host
                                const float* scores, cudaStream_t st);
 
 
+// fnapi.cu: the function-level API kernels (score_keys / streaming_insert
+// scoring, reduce_by_key, TopList::from_scores)
+cudaError_t launch_score_multi(const float* cent, const uint32_t* coff, const uint32_t* kof,
+                               const uint32_t* wid, uint32_t ncent, const float* keys, uint32_t n,
+                               uint32_t d, int mode, float* out, double* out64, cudaStream_t st);
+cudaError_t launch_reduce_lists(uint32_t nl, const uint64_t* off, const uint32_t* idx, const float* sc,
+                                const double* w, double* acc, uint32_t* cnt, uint32_t nkeys,
+                                cudaStream_t st);
+size_t toplist_scratch_bytes(uint32_t n);
+cudaError_t launch_toplist(const float* scores, uint32_t n, unsigned long long* sorted, void* scratch,
+                           size_t scratch_bytes, cudaStream_t st);
+
 }  // namespace csa

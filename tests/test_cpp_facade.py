@@ -19,6 +19,21 @@ def test_cpp_facade_matches_reference_library():
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout + r.stderr
 
 
+FN_BIN = os.path.join(HERE, "cpp", "test_fn")
+
+
+@pytest.mark.gpu
+def test_cpp_function_level_api_matches_reference_tests():
+    """test_index.cpp:60-301 and test_retrieval.cpp:134-577 ported onto the
+    facade's free functions (GPU-backed), cross-checked against the reference
+    library (tests/cpp/test_fn.cpp)."""
+    if not os.path.exists(FN_BIN):
+        pytest.skip("tests/cpp/test_fn not built (needs /root/reference at build time)")
+    r = subprocess.run([FN_BIN], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
+
+
 def test_cpp_facade_header_compiles_standalone(tmp_path):
     """The facade header is self-contained C++20 over the C ABI (no CUDA, no torch)."""
     root = os.path.dirname(HERE)
