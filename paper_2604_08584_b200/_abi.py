@@ -126,6 +126,14 @@ SIGNATURES = {
     "csattn_shard_buffer_words": (C.c_int, [vp, P(u64), P(u64), P(u64), P(u64)]),
     "csattn_shard_step": (C.c_int, [vp, u64, P(vp), C.c_int32, P(ShardIoC)]),
     "csattn_dense_topk": (C.c_int, [vp, vp, u64, vp, u32]),
+    # function-level API (host values, device compute)
+    "csattn_score_keys": (C.c_int, [vp, vp, u64, vp, vp, vp, u64, u64, C.c_int32, vp, vp]),
+    "csattn_toplist_from_scores": (C.c_int, [vp, vp, u64, u64, vp, vp, vp]),
+    "csattn_select_centroids": (C.c_int, [vp, vp, u64, vp, u64, vp, u64, C.c_double, vp, vp, vp, vp]),
+    "csattn_reduce_by_key": (C.c_int, [vp, u64, vp, vp, vp, vp, vp, vp, vp, u64, vp]),
+    "csattn_select_topk": (C.c_int, [vp, vp, vp, u64, u64, vp, u64, vp, vp]),
+    "csattn_dense_attention_rows": (C.c_int, [vp, vp, vp, vp, u64, u64, vp, u64, vp, vp]),
+    "csattn_dense_topk_rows": (C.c_int, [vp, vp, vp, u64, u64, u64, vp]),
     "csattn_ctx_set_kv_placement": (C.c_int, [vp, C.c_int32]),
     "csattn_f32_to_f16": (C.c_uint16, [C.c_float]),
     "csattn_f16_to_f32": (C.c_float, [C.c_uint16]),
