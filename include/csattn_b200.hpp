@@ -988,6 +988,58 @@ class Session {
     std::size_t dim_ = 0;
 };
 
+// metrics.cpp:9-30 / :40-46 (host cost models and the recall metric)
+inline double recall_at_k(std::span<const std::uint32_t> selected, std::span<const std::uint32_t> truth) {
+    if (truth.empty()) throw ParameterError("recall is undefined against an empty truth set");
+    std::vector<std::uint32_t> a(selected.begin(), selected.end()), b(truth.begin(), truth.end());
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    std::size_t hits = 0, i = 0, j = 0;
+    while (i < a.size() && j < b.size()) {
+        if (a[i] < b[j]) ++i;
+        else if (b[j] < a[i]) ++j;
+        else {
+            ++hits;
+            ++i;
+            ++j;
+        }
+    }
+    return static_cast<double>(hits) / static_cast<double>(b.size());
+}
+inline std::size_t table_bytes(std::size_t m, std::size_t c, std::size_t l, std::size_t d,
+                               std::size_t bytes_per_score) {
+    if (m == 0 || c == 0 || d == 0 || bytes_per_score == 0) throw ParameterError("size model needs positive parameters");
+    return m * c * l * (4 + bytes_per_score) + bytes_per_score * c * d;
+}
+
+// Session(KvStore, CsIndex, cfg) (session.hpp:19-31): a device session over a
+// host index value and its prefill rows (csattn_session_import)
+inline Session make_session(const KvStore& kv, const CsIndex& index, const RetrievalConfig& cfg,
+                            std::size_t max_decode_steps = 4096, Context& ctx = Context::default_context()) {
+    const std::size_t d = kv.dim(), m = index.subspaces(), c = index.centroids_per_subspace();
+    if (index.layout.dim() != d) throw DimensionError("layout dimension does not match KV dimension");
+    std::vector<float> cent;
+    for (const CentroidSet& cs : index.centroid_sets) cent.insert(cent.end(), cs.centroids.begin(), cs.centroids.end());
+    std::size_t stride = 1;
+    for (const TopList& l : index.tables) stride = std::max(stride, l.indices.size());
+    std::vector<uint32_t> lens(index.tables.size()), idx(index.tables.size() * stride, 0);
+    std::vector<float> sc(index.tables.size() * stride, 0.0f);
+    for (std::size_t t = 0; t < index.tables.size(); ++t) {
+        const TopList& l = index.tables[t];
+        lens[t] = static_cast<uint32_t>(l.indices.size());
+        std::copy(l.indices.begin(), l.indices.end(), idx.begin() + static_cast<std::ptrdiff_t>(t * stride));
+        std::copy(l.scores.begin(), l.scores.end(), sc.begin() + static_cast<std::ptrdiff_t>(t * stride));
+    }
+    std::vector<uint64_t> widths(index.layout.sizes.begin(), index.layout.sizes.end());
+    const csattn_retrieval_config rc = cfg.c();
+    csattn_session s = nullptr;
+    check(csattn_session_import(ctx.handle(), cent.data(), c, lens.data(), idx.data(), sc.data(), stride,
+                                index.list_capacity, index.alpha, index.normalize_keys ? 1 : 0, index.score_bits,
+                                kv.key_data(), kv.value_data(), kv.size(), d, widths.data(), m, &rc, 1,
+                                max_decode_steps, &s));
+    return Session(s, index.layout, cfg);
+}
+
 // ---- index.hpp:98-121: the CSAT v1 image of a host CsIndex ----
 struct IndexFootprint {
     std::size_t header_bytes = 0;

@@ -34,6 +34,20 @@ def test_cpp_function_level_api_matches_reference_tests():
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+ACC_BIN = os.path.join(HERE, "cpp", "test_acceptance")
+
+
+@pytest.mark.gpu
+def test_cpp_acceptance_gate_on_gpu():
+    """acceptance.cpp criteria 1-10 through the facade on the GPU, including the
+    calibrated recall 0.5509 (P=7936, d=64, 256 steps) reproduced exactly."""
+    if not os.path.exists(ACC_BIN):
+        pytest.skip("tests/cpp/test_acceptance not built (needs /root/reference at build time)")
+    r = subprocess.run([ACC_BIN], capture_output=True, text=True, timeout=1500)
+    print(r.stdout)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
+
+
 def test_cpp_facade_header_compiles_standalone(tmp_path):
     """The facade header is self-contained C++20 over the C ABI (no CUDA, no torch)."""
     root = os.path.dirname(HERE)
