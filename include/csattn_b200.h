@@ -162,6 +162,8 @@ csattn_status csattn_ctx_synchronize(csattn_ctx ctx);
 #define CSATTN_KV_DEVICE 0
 #define CSATTN_KV_HOST 1
 csattn_status csattn_ctx_set_kv_placement(csattn_ctx ctx, int32_t placement);
+/* The CUDA stream (cudaStream_t) the context enqueues on. */
+void* csattn_ctx_stream(csattn_ctx ctx);
 /* Number of CUDA kernels this context has launched (driver-side evidence). */
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx);
 /* Kernel timing: when enabled, the three kernels of every decode step
@@ -497,6 +499,12 @@ csattn_status csattn_shard_buffer_words(csattn_session shard, uint64_t* hist_wor
  * phases must run on (or be ordered with) that stream. */
 csattn_status csattn_shard_step(csattn_ctx ctx, uint64_t n, const csattn_session* shards,
                                 int32_t phase, const csattn_shard_io* io);
+/* Local combine steps of the collectives between phases (device pointers,
+ * enqueued on ctx's stream): dst[i] += src[i] over uint32 (histograms, flags),
+ * dst[i] = min(dst[i], src[i]) over uint64 (victim keys). The C++ orchestrator
+ * include/csattn_b200_shard.hpp uses them with its local / NCCL transports. */
+csattn_status csattn_buffer_add_u32(csattn_ctx ctx, uint32_t* dst, const uint32_t* src, uint64_t count);
+csattn_status csattn_buffer_min_u64(csattn_ctx ctx, uint64_t* dst, const uint64_t* src, uint64_t count);
 
 #ifdef __cplusplus
 }

@@ -126,6 +126,9 @@ SIGNATURES = {
     "csattn_shard_buffer_words": (C.c_int, [vp, P(u64), P(u64), P(u64), P(u64)]),
     "csattn_shard_step": (C.c_int, [vp, u64, P(vp), C.c_int32, P(ShardIoC)]),
     "csattn_dense_topk": (C.c_int, [vp, vp, u64, vp, u32]),
+    "csattn_ctx_stream": (vp, [vp]),
+    "csattn_buffer_add_u32": (C.c_int, [vp, vp, vp, u64]),
+    "csattn_buffer_min_u64": (C.c_int, [vp, vp, vp, u64]),
     # function-level API (host values, device compute)
     "csattn_score_keys": (C.c_int, [vp, vp, u64, vp, vp, vp, u64, u64, C.c_int32, vp, vp]),
     "csattn_toplist_from_scores": (C.c_int, [vp, vp, u64, u64, vp, vp, vp]),

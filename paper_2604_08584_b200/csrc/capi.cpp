@@ -2863,4 +2863,22 @@ csattn_status csattn_dense_topk_rows(csattn_ctx ctx, const float* q, const float
     });
 }
 
+void* csattn_ctx_stream(csattn_ctx ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+csattn_status csattn_buffer_add_u32(csattn_ctx ctx, uint32_t* dst, const uint32_t* src, uint64_t count) {
+    return guard([&] {
+        ck(csa::launch_buf_add_u32(dst, src, count, ctx->stream), "buffer add");
+        ctx->launches += count ? 1 : 0;
+    });
+}
+
+csattn_status csattn_buffer_min_u64(csattn_ctx ctx, uint64_t* dst, const uint64_t* src, uint64_t count) {
+    return guard([&] {
+        ck(csa::launch_buf_min_u64(reinterpret_cast<unsigned long long*>(dst),
+                                   reinterpret_cast<const unsigned long long*>(src), count, ctx->stream),
+           "buffer min");
+        ctx->launches += count ? 1 : 0;
+    });
+}
+
 }  // extern "C"

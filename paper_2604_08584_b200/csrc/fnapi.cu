@@ -99,6 +99,31 @@ __global__ void toplist_keys_kernel(const float* __restrict__ s, uint32_t n,
     keys[i] = (static_cast<unsigned long long>(o) << 32) | static_cast<uint32_t>(~i);
 }
 
+__global__ void buf_add_u32_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        dst[i] += src[i];
+}
+__global__ void buf_min_u64_kernel(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src,
+                                   uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i] < dst[i] ? src[i] : dst[i];
+}
+
+cudaError_t launch_buf_add_u32(uint32_t* dst, const uint32_t* src, uint64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t b = (n + 255) / 256;
+    buf_add_u32_kernel<<<static_cast<unsigned>(b < 1184 ? b : 1184), 256, 0, st>>>(dst, src, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_buf_min_u64(unsigned long long* dst, const unsigned long long* src, uint64_t n, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t b = (n + 255) / 256;
+    buf_min_u64_kernel<<<static_cast<unsigned>(b < 1184 ? b : 1184), 256, 0, st>>>(dst, src, n);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_score_multi(const float* cent, const uint32_t* coff, const uint32_t* kof,
                                const uint32_t* wid, uint32_t ncent, const float* keys, uint32_t n,
                                uint32_t d, int mode, float* out, double* out64, cudaStream_t st) {

@@ -110,6 +110,28 @@ def coll_all_reduce_min_u64(bufs, dist=None):
         b.copy_(m)
 
 
+class HostStagedDist:
+    """torch.distributed with every collective staged through host memory:
+    for a transport without device tensors (gloo), or several ranks on one GPU
+    (NCCL refuses two ranks on the same device). Same calls as the subset of
+    torch.distributed that ShardGroup uses."""
+
+    def __init__(self, dist):
+        self.d = dist
+        self.ReduceOp = dist.ReduceOp
+
+    def all_reduce(self, t, op=None):
+        h = t.cpu()
+        self.d.all_reduce(h, op=self.d.ReduceOp.SUM if op is None else op)
+        t.copy_(h)
+
+    def all_gather(self, parts, t):
+        hp = [p.cpu() for p in parts]
+        self.d.all_gather(hp, t.cpu())
+        for p, h in zip(parts, hp):
+            p.copy_(h)
+
+
 class ShardGroup:
     """Sharded decode of a set of KV-head sessions.
 

@@ -48,6 +48,22 @@ def test_cpp_acceptance_gate_on_gpu():
     assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+SHARD_BIN = os.path.join(HERE, "cpp", "test_shard")
+
+
+@pytest.mark.gpu
+def test_cpp_sequence_sharded_layer_local_and_nccl():
+    """include/csattn_b200_shard.hpp (+ _nccl.hpp): the native sharded decode
+    equals the unsharded sessions (selections exact, outputs <= 1e-3, tables
+    after inserts), over the local transport and a real NCCL communicator."""
+    if not os.path.exists(SHARD_BIN):
+        pytest.skip("tests/cpp/test_shard not built (needs /root/reference at build time)")
+    r = subprocess.run([SHARD_BIN], capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT"))
+    print(r.stdout)
+    assert r.returncode == 0 and "ALL OK" in r.stdout, r.stdout[-4000:] + r.stderr[-3000:]
+
+
 def test_cpp_facade_header_compiles_standalone(tmp_path):
     """The facade header is self-contained C++20 over the C ABI (no CUDA, no torch)."""
     root = os.path.dirname(HERE)
