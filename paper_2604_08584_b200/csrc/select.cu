@@ -922,54 +922,58 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             const uint32_t kw = kbase + wid * WKEYS;  // this warp's first key
             const bool tile_win = kbase + TILE > wlo;  // holds window keys
             double2* const a2 = reinterpret_cast<double2*>(wacc);
+            if (!tile_win && !st.store_cache) {
+                // common case (every key below the window, nothing cached): one
+                // pass per lane over its 16 keys (8 pairs, all loads in flight)
+                // builds a survivor mask; the survivors are binned and logged
+                // in rounds (about 8% of keys), then the slice is reset
+                double2 v[WKEYS / 64];
+#pragma unroll
+                for (uint32_t u = 0; u < WKEYS / 64; ++u) v[u] = a2[u * 32 + ln];
+                if (need) {
+                    uint32_t sm = 0;  // bit 2u + c: key 64u + 2ln + c survives the cheap compare
+                    if (cut_lo > 0.0) {  // the -0.0 marker fails `>= cut_lo` by itself
+#pragma unroll
+                        for (uint32_t u = 0; u < WKEYS / 64; ++u)
+                            sm |= (v[u].x >= cut_lo ? 1u : 0u) << (2 * u) | (v[u].y >= cut_lo ? 2u : 0u) << (2 * u);
+                    } else {
+#pragma unroll
+                        for (uint32_t u = 0; u < WKEYS / 64; ++u)
+                            sm |= ((!is_neg0(v[u].x) && v[u].x >= cut_lo) ? 1u : 0u) << (2 * u) |
+                                  ((!is_neg0(v[u].y) && v[u].y >= cut_lo) ? 2u : 0u) << (2 * u);
+                    }
+                    while (__any_sync(0xffffffffu, sm != 0)) {
+                        bool a = false;
+                        uint32_t b = 0, koff = 0;
+                        double sc = 0.0;
+                        if (sm) {
+                            const uint32_t bit = __ffs(sm) - 1;
+                            sm &= sm - 1;
+                            koff = 64 * (bit >> 1) + 2 * ln + (bit & 1);
+                            sc = wacc[koff];  // not reset yet
+                            b = bin_of(sc, lo, scale);
+                            a = b >= cut;
+                        }
+                        const unsigned m = __ballot_sync(0xffffffffu, a);
+                        if (a) {
+                            const uint32_t pos = wlog_n + __popc(m & ((1u << ln) - 1u));
+                            wlog_idx[pos] = kw + koff;
+                            wlog_sc[pos] = sc;
+                            atomicAdd(&hist[b], 1u);
+                            atomicAdd(&coarse[b >> 5], 1u);
+                        }
+                        wlog_n += __popc(m);
+                    }
+                }
+                __syncwarp();  // survivors read before the reset
+                const double2 nz = make_double2(neg0_d(), neg0_d());
+#pragma unroll
+                for (uint32_t u = 0; u < WKEYS / 64; ++u) a2[u * 32 + ln] = nz;
+            } else {
             // pass 1: cheap compare, survivors compacted to the front of the
             // warp's accumulator slice (positions never pass the read front)
             uint32_t nadm = 0;
-            if (!tile_win && !st.store_cache) {
-                // common case: every key below the window, nothing cached —
-                // four keys per lane per step
-                if (need) {
-#pragma unroll 2
-                    for (uint32_t u = 0; u < WKEYS / 128; ++u) {
-                        const uint32_t lp = u * 64 + ln;
-                        const double2 v = a2[lp], x = a2[lp + 32];
-                        const bool k0 = !is_neg0(v.x) && v.x >= cut_lo;
-                        const bool k1 = !is_neg0(v.y) && v.y >= cut_lo;
-                        const bool k2 = !is_neg0(x.x) && x.x >= cut_lo;
-                        const bool k3 = !is_neg0(x.y) && x.y >= cut_lo;
-                        const unsigned m0 = __ballot_sync(0xffffffffu, k0);
-                        const unsigned m1 = __ballot_sync(0xffffffffu, k1);
-                        const unsigned m2 = __ballot_sync(0xffffffffu, k2);
-                        const unsigned m3 = __ballot_sync(0xffffffffu, k3);
-                        if (m0 | m1 | m2 | m3) {
-                            const unsigned lt = (1u << ln) - 1u;
-                            const uint32_t n0 = __popc(m0), n1 = n0 + __popc(m1), n2 = n1 + __popc(m2);
-                            __syncwarp();  // every lane has read its keys
-                            if (k0) {
-                                const uint32_t pos = nadm + __popc(m0 & lt);
-                                wacc[pos] = v.x;
-                                wcidx[pos] = static_cast<uint16_t>(2 * lp);
-                            }
-                            if (k1) {
-                                const uint32_t pos = nadm + n0 + __popc(m1 & lt);
-                                wacc[pos] = v.y;
-                                wcidx[pos] = static_cast<uint16_t>(2 * lp + 1);
-                            }
-                            if (k2) {
-                                const uint32_t pos = nadm + n1 + __popc(m2 & lt);
-                                wacc[pos] = x.x;
-                                wcidx[pos] = static_cast<uint16_t>(2 * lp + 64);
-                            }
-                            if (k3) {
-                                const uint32_t pos = nadm + n2 + __popc(m3 & lt);
-                                wacc[pos] = x.y;
-                                wcidx[pos] = static_cast<uint16_t>(2 * lp + 65);
-                            }
-                            nadm += n2 + __popc(m3);
-                        }
-                    }
-                }
-            } else {
+            {
 #pragma unroll 2
                 for (uint32_t u = 0; u < WKEYS / 64; ++u) {
                     const uint32_t lp = u * 32 + ln;
@@ -1042,6 +1046,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
 #pragma unroll
             for (uint32_t u = 0; u < WKEYS / 64; ++u)
                 a2[u * 32 + ln] = make_double2(neg0_d(), neg0_d());
+            }  // generic path
             // raise the cut (stale counts only under-estimate: still safe)
             if (need && (tile % SEL_CW) == static_cast<uint32_t>(wid)) {
                 uint32_t ab;
