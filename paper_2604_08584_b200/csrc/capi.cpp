@@ -217,6 +217,10 @@ struct csattn_ctx_s {
     // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
     // retry pass — used by the tests to exercise it)
     double spec_keep = std::getenv("CSATTN_SPEC_KEEP") ? std::atof(std::getenv("CSATTN_SPEC_KEEP")) : 0.9;
+    // one-cluster-per-problem fused step for small batches (fused.cu):
+    // CSATTN_FUSED=0 never, 1 whenever it fits, default: when the batch's
+    // clusters fit the GPU a couple of times over (the latency-bound regime)
+    int fused_mode = std::getenv("CSATTN_FUSED") ? std::atoi(std::getenv("CSATTN_FUSED")) : 2;
     uint64_t counters_n = 0;
     // select-kernel phase timestamps (env CSATTN_PHASE_PROF=1; diagnostics only)
     bool phase_prof = std::getenv("CSATTN_PHASE_PROF") != nullptr;
@@ -695,6 +699,17 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
     }
     const uint64_t ngroups = ugP.size(), nmem = umem.size();
+    // the fused cluster step: every problem's search + attention in one
+    // cluster; the append + insert stays a separate launch
+    int fz_cl = 0, fz_nr = 0;
+    // auto: 8-CTA clusters that all fit the GPU at once (c2: 32 problems at
+    // 32K keys, search + attention 76 -> ~50 us); 16-CTA clusters (up to 256K
+    // keys) measured slower than the multi-kernel path at c4 and are only
+    // taken with CSATTN_FUSED=1
+    const bool fused = ctx->fused_mode != 0 && !dw && ngroups == 0 &&
+                       csa::fused_fits(static_cast<uint32_t>(maxN), d, fz_cl, fz_nr) &&
+                       (ctx->fused_mode == 1 ||
+                        (fz_cl == 8 && nq * 8ull <= 2ull * static_cast<uint64_t>(ctx->num_sms)));
     const uint32_t u_nrange = (u_maxP + csa::UN_RANGE - 1) / csa::UN_RANGE;
     if (ngroups) {
         ctx->un_row.ensure(ngroups * u_nrange * csa::UN_RANGE * 2);
@@ -811,6 +826,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         for (auto& e : ev) e = ctx->take_event();
         ck(cudaEventRecord(ev[0], ctx->stream), "event");
     }
+    if (fused) {
+        if (live)
+            ck(csa::launch_fused_step(dprobs, static_cast<uint32_t>(nq), fz_cl, fz_nr, ctx->stream),
+               "fused step launch");
+        if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
+    } else {
     ctx->plans.ensure(nq * sizeof(csa::RoutePlan));
     if (live)
     ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
@@ -899,6 +920,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                               ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream,
                               false, arows),
            "attend launch");
+    }
     if (ngroups) {
         auto u32 = [&](size_t off) { return reinterpret_cast<const uint32_t*>(db + off); };
         if (ctx->union_prof) {
@@ -956,7 +978,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaEventRecord(ev[3], ctx->stream), "event");
         ctx->ev_steps.push_back(ev);
     }
-    ctx->launches += nchunks ? 5 : 4;
+    ctx->launches += fused ? 2 : (nchunks ? 5 : 4);
     const auto ht2 = std::chrono::steady_clock::now();
     if (ctx->phase_prof) {
         // per problem: streaming (gather + log) and final-selection time,
@@ -990,6 +1012,17 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             ctx->phase_dbg[0] = lo;
             ctx->phase_dbg[1] = hi;
             ctx->phase_dbg[2] = static_cast<double>(ph[7]);
+        }
+        {
+            unsigned long long fd[8];
+            ck(csa::select_fin_debug(fd, ctx->stream), "fin debug");
+            ck(cudaStreamSynchronize(ctx->stream), "fin debug");
+            static double acc[8] = {};
+            for (int k = 0; k < 8; ++k) acc[k] += double(fd[k]);
+            if (acc[6] > 0)
+                std::fprintf(stderr, "[fin] per problem us: head %.2f scan %.2f rank %.2f count %.2f pad+scan %.2f emit %.2f (n=%.0f)\n",
+                             acc[0] / acc[6] / 1e3, acc[1] / acc[6] / 1e3, acc[2] / acc[6] / 1e3, acc[3] / acc[6] / 1e3,
+                             acc[4] / acc[6] / 1e3, acc[5] / acc[6] / 1e3, acc[6]);
         }
         if (n) {
             for (int k = 0; k < 4; ++k) ctx->phase_sum[k] += sum[k] / n;

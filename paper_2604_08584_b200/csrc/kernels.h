@@ -30,7 +30,8 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
 // log_cap entries each, unit_meta: select_unit_meta_words() per unit) and
 // finalised by the merge kernel (one CTA per problem).
 uint32_t select_unit_meta_words();
-uint32_t select_ctas_per_sm();  // resident select CTAs per SM (grid = this x SMs)
+uint32_t select_ctas_per_sm();
+cudaError_t select_fin_debug(unsigned long long* out8, cudaStream_t st);  // temporary  // resident select CTAs per SM (grid = this x SMs)
 uint32_t select_tile_keys();
 cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 uint32_t split, const uint32_t* unit_meta, const uint32_t* log_idx,
@@ -57,6 +58,12 @@ cudaError_t launch_shard_mark(const DecodeProblem* probs, const RoutePlan* plans
 cudaError_t launch_shard_emit(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                               const uint32_t* counts_all, uint32_t nshard, uint32_t shard,
                               uint32_t* bitmap, uint32_t bm_words, uint32_t* kdev, cudaStream_t st);
+
+// fused.cu: the whole decode search + attention of a problem in one CTA
+// cluster (small batches); fused_fits picks the cluster size and the 512-key
+// ranges per CTA for N keys
+bool fused_fits(uint32_t N, uint32_t d, int& cl, int& nr);
+cudaError_t launch_fused_step(const DecodeProblem* probs, uint32_t nprob, int cl, int nr, cudaStream_t st);
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
 constexpr uint32_t ATT_ROWS = 256;      // rows per chunk-CTA (mid-size launches)

@@ -54,14 +54,14 @@ constexpr int SEL_THREADS = SEL_CT + 32;     // + producer warp
 constexpr uint32_t TILE = 4096;              // keys per tile (fp64 accumulator: 32 KB)
 constexpr uint32_t TILE_BLKS = TILE / KEY_BLOCK;
 constexpr uint32_t WKEYS = TILE / SEL_CW;    // keys per warp in the tile-end filter
-constexpr int NSLOT = 6;                     // ring slots
-constexpr uint32_t SLOT_E = 1024;            // entries per slot (8 KB)
-constexpr uint32_t CACHE_LIST = 127;         // chunk "list" id of a cached-score tile
+constexpr int NSLOT = 3;                     // ring slots
+constexpr uint32_t SLOT_E = 2048;            // entries per slot (16 KB)
+constexpr uint32_t MAXSUB = 4;               // list segments packed into one slot
 constexpr int NB = 2048;                     // histogram bins
 constexpr int NCB = NB / 32;                 // coarse bins (32 fine bins each)
 constexpr int BKT = 512;                     // threshold-bin members ranked in smem
 constexpr int RANK_DIRECT = 384;             // O(n^2) ranking up to this size
-constexpr uint32_t F_LIST_END = 1, F_TILE_END = 2, F_PROB_END = 4;
+constexpr uint32_t F_TILE_END = 1, F_PROB_END = 2, F_CACHE = 4;
 constexpr int MAXPART = 16;                  // key-range parts of a split problem
 constexpr uint32_t MAXSEG = MAXPART * 8;     // log segments (parts x warps)
 constexpr uint32_t UNIT_META = 2048 + 64 + 8;  // per part unit: hist, coarse, per-warp log lengths
@@ -70,13 +70,15 @@ static_assert(TILE * 64 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bi
 static_assert(SELECT_MAX_CONTEXT / TILE <= 128 && MAXL < 127, "chunk info fields");
 static_assert(UNIT_META == NB + NCB + SEL_CW && SEL_CW == 8, "unit metadata layout");
 
-// One ring chunk: info = list | flags << 7 | tile << 10; the chunk stages the
-// table positions from `base` (even, 16-byte aligned). wr[w] = consumer warp
-// w's entries as slot-relative positions [x, y) (its own key range of the
-// tile intersected with the chunk; y <= x when it has none).
+// One ring chunk = one slot: up to MAXSUB list segments of one tile, packed
+// at even (16-byte aligned) slot positions, in gathered-list order.
+// info = nsub | flags << 3 | tile << 8; sub s is list `lists[s]` and consumer
+// warp w's entries of it are the slot positions wr[s][w] = [x, y) (its own key
+// range of the tile intersected with the segment; y <= x when none).
 struct SlotMeta {
-    uint32_t info, base, pad0, pad1;
-    uint2 wr[SEL_CW];
+    uint32_t info;
+    uint8_t lists[MAXSUB];
+    uint2 wr[MAXSUB][SEL_CW];
 };
 static_assert(WKEYS % KEY_BLOCK == 0, "warp key ranges are whole key blocks");
 constexpr uint32_t WBLKS = WKEYS / KEY_BLOCK;  // key blocks per warp range
@@ -409,6 +411,7 @@ __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const Route
 // at and above every cut used) and its candidate log, given as nseg segments
 // (S.seg_off[k], S.seg_len[k]) of log_idx/log_sc. Consumer threads only (named
 // barrier 1). Leaves the bitmap region dirty; the caller resets its scratch.
+__device__ unsigned long long g_fin_dbg[8];  // CSATTN_PHASE_PROF: final-phase stage ns, summed
 __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_t* hist,
                              uint32_t* coarse, uint32_t* bm, unsigned long long* bkey,
                              uint32_t* bidx, const uint32_t* log_idx, const double* log_sc,
@@ -428,6 +431,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
         }
     }
     if (prof && tid == 0) prof[1] = gtimer();
+    unsigned long long tdbg = (prof && tid == 0) ? gtimer() : 0ull;
     const uint32_t nw = div_up(N, 32);
     if (tid < 32) {
         uint32_t ab = 0;
@@ -450,6 +454,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
     }
     for (uint32_t x = tid; x < nw; x += SEL_CT) bm[x] = 0;
     cbar();
+    if (prof && tid == 0) { const unsigned long long t_ = gtimer(); atomicAdd(&g_fin_dbg[0], t_ - tdbg); tdbg = t_; }
     const bool failed = S.f_fail != 0;
     const uint32_t take_all = S.f_take_all, dsel = S.f_bin;
     const uint32_t rem = need - (take_all ? 0u : min(need, S.f_above));
@@ -491,6 +496,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
             }
         }
         cbar();
+        if (prof && tid == 0) { const unsigned long long t_ = gtimer(); atomicAdd(&g_fin_dbg[1], t_ - tdbg); tdbg = t_; }
         const uint32_t nb = S.nbkt;
         if (need && !take_all && rem) {
             if (nb <= static_cast<uint32_t>(RANK_DIRECT)) {
@@ -540,6 +546,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
         // window passthrough (or the newest K when K <= R)
         for (uint32_t i = f_lo + tid; i < N; i += SEL_CT) set_bit(bm, i);
         cbar();
+        if (prof && tid == 0) { const unsigned long long t_ = gtimer(); atomicAdd(&g_fin_dbg[2], t_ - tdbg); tdbg = t_; }
         // ---- count, newest-first padding, ascending emit ----
         const uint32_t wpt = div_up(nw, SEL_CT);
         const uint32_t w0 = min(nw, tid * wpt), w1 = min(nw, w0 + wpt);
@@ -554,6 +561,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
         }
         uint32_t total;
         cscan(S, cnt, total);
+        if (prof && tid == 0) { const unsigned long long t_ = gtimer(); atomicAdd(&g_fin_dbg[3], t_ - tdbg); tdbg = t_; }
         if (total < K) {  // pad with the newest untaken keys (retrieval.cpp:218-225)
             const uint32_t pad = K - total;
             uint32_t zt;
@@ -573,6 +581,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
             }
         }
         const uint32_t at = cscan(S, cnt, total);
+        if (prof && tid == 0) { const unsigned long long t_ = gtimer(); atomicAdd(&g_fin_dbg[4], t_ - tdbg); tdbg = t_; }
         {
             uint32_t pos = at;
             for (uint32_t x = w0; x < w1; ++x) {
@@ -588,6 +597,7 @@ __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_
             reinterpret_cast<DecodeReport*>(rep)->k = K;
             if (prof) {
                 prof[2] = gtimer();
+                atomicAdd(&g_fin_dbg[5], gtimer() - tdbg); atomicAdd(&g_fin_dbg[6], 1ull);
                 prof[3] = nlog;
                 prof[4] = nb;
                 prof[5] = static_cast<unsigned long long>(__double_as_longlong(lo));
@@ -660,34 +670,41 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     // ======================= producer warp =======================
     if (wid == SEL_CW) {
         const unsigned long long pol = l2_evict_first_policy();
-        uint32_t c = 0;
-        auto publish = [&](uint32_t info, uint32_t base, uint32_t lo, uint32_t hi,
-                           const uint2* src, uint32_t bytes, const uint32_t* wb = nullptr) {
-            const uint32_t slot = c % NSLOT;
+        uint32_t c = 0;         // slots opened so far
+        uint32_t nsub = 0, fill = 0, open_slot = 0;  // the slot being packed
+        auto open = [&]() {      // wait for the next slot to be free
+            open_slot = c % NSLOT;
             if (c >= static_cast<uint32_t>(NSLOT))
-                mbar_wait_sleep(&S.empty[slot], ((c / NSLOT) - 1) & 1u);
+                mbar_wait_sleep(&S.empty[open_slot], ((c / NSLOT) - 1) & 1u);
+            ++c;
+            nsub = 0;
+            fill = 0;
+        };
+        // stage positions [lo, hi) of list l (table row tbl) into the open slot
+        auto add = [&](uint32_t l, const uint2* tbl, uint32_t lo, uint32_t hi, const uint32_t* wb) {
+            const uint32_t ab = lo & ~1u, ae = (hi + 1) & ~1u;  // <= cap2 (even)
+            const uint32_t at = fill;                          // slot position of ab
             if (ln < SEL_CW) {  // consumer warp ln's slot-relative entry range
-                uint2 r = make_uint2(0u, 0u);
-                if (wb) {
-                    const uint32_t a = max(lo, wb[ln]), b = min(hi, wb[ln + 1]);
-                    r = b > a ? make_uint2(a - base, b - base) : make_uint2(0u, 0u);
-                }
-                S.meta[slot].wr[ln] = r;
+                const uint32_t x = max(lo, wb[ln]), y = min(hi, wb[ln + 1]);
+                S.meta[open_slot].wr[nsub][ln] = y > x ? make_uint2(x - ab + at, y - ab + at) : make_uint2(0u, 0u);
             }
-            __syncwarp();  // lane 0's arrive below releases the other lanes' writes too
             if (ln == 0) {
-                S.meta[slot].info = info;
-                S.meta[slot].base = base;
-                if (bytes) {
-                    mbar_expect_tx(&S.full[slot], bytes);
-                    bulk_g2s_hint(ring + static_cast<size_t>(slot) * SLOT_E, src, bytes,
-                                  &S.full[slot], pol);
-                } else {
-                    mbar_arrive(&S.full[slot]);
-                }
+                S.meta[open_slot].lists[nsub] = static_cast<uint8_t>(l);
+                const uint32_t bytes = (ae - ab) * 8u;
+                mbar_expect_tx_only(&S.full[open_slot], bytes);
+                bulk_g2s_hint(ring + static_cast<size_t>(open_slot) * SLOT_E + at, tbl + ab, bytes,
+                              &S.full[open_slot], pol);
+            }
+            ++nsub;
+            fill += ae - ab;
+        };
+        auto close = [&](uint32_t flags, uint32_t tile) {  // publish the open slot
+            __syncwarp();  // lane 0's arrive below releases the other lanes' meta writes
+            if (ln == 0) {
+                S.meta[open_slot].info = nsub | (flags << 3) | (tile << 8);
+                mbar_arrive(&S.full[open_slot]);
             }
             __syncwarp();
-            ++c;
         };
         for (uint32_t k = blockIdx.x; k < nwork; k += gridDim.x) {
             const uint32_t p = prob_of(k);
@@ -764,33 +781,35 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             for (uint32_t tile = tl; tile < ntile; ++tile) {
                 const uint32_t tflag = F_TILE_END | (tile + 1 == ntile ? F_PROB_END : 0u);
                 if (nl == 0) {  // cached scores: one data-less chunk per tile
-                    publish(CACHE_LIST | ((F_LIST_END | tflag) << 7) | (tile << 10), 0, 0, 0,
-                            nullptr, 0);
+                    open();
+                    close(tflag | F_CACHE, tile);
                     continue;
                 }
                 const uint32_t c0 = bound(tile + 2, ln), c1 = bound(tile + 2, ln + 32);
                 wb_load(tile + 1, wv);  // stored after this tile's chunks are out
+                open();
                 for (uint32_t l = 0; l < nl; ++l) {
                     const uint32_t e0 = __shfl_sync(0xffffffffu, l < 32 ? a0 : a1, l & 31);
                     const uint32_t e1 = __shfl_sync(0xffffffffu, l < 32 ? b0 : b1, l & 31);
-                    const uint32_t lflag = F_LIST_END | (l + 1 == nl ? tflag : 0u);
+                    if (e0 == e1) continue;  // nothing of this list in this tile
                     const uint2* tbl = ent + static_cast<size_t>(S.plist[l]) * cap2;
-                    if (e0 == e1) {  // nothing in this tile: only the flags travel
-                        publish(l | (lflag << 7) | (tile << 10), 0, 0, 0, nullptr, 0);
-                        continue;
-                    }
+                    const uint32_t* wb = &S.wbs[tile & 1][l][0];
                     uint32_t pos = e0;
-                    for (;;) {
-                        const uint32_t ab = pos & ~1u;
-                        const uint32_t pe = min(e1, ab + SLOT_E);
-                        const uint32_t ae = (pe + 1) & ~1u;  // <= cap2 (even)
-                        const bool last = pe == e1;
-                        publish(l | ((last ? lflag : 0u) << 7) | (tile << 10), ab, pos, pe,
-                                tbl + ab, (ae - ab) * 8u, &S.wbs[tile & 1][l][0]);
-                        if (last) break;
+                    while (pos < e1) {
+                        const uint32_t room = SLOT_E - fill;  // even
+                        const uint32_t need = ((e1 + 1) & ~1u) - (pos & ~1u);
+                        if (nsub == MAXSUB || room < 2 || (need > room && nsub > 0)) {
+                            close(0u, tile);  // full: publish, continue in a fresh slot
+                            open();
+                            continue;
+                        }
+                        // the segment, or as much of it as fits an empty slot
+                        const uint32_t pe = need <= room ? e1 : (pos & ~1u) + room;
+                        add(l, tbl, pos, pe, wb);
                         pos = pe;
                     }
                 }
+                close(tflag, tile);
                 if (tile + 1 < ntile) wb_store(tile + 1, wv);
                 a0 = b0;
                 a1 = b1;
@@ -818,34 +837,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     double* wlog_sc = log_sc + log_base(kk);
     uint16_t* const wcidx = cidx + wid * WKEYS;
     double* const wacc = acc + wid * WKEYS;
-    uint32_t slot = 0, phase = 0;  // ring position of the next chunk to fetch
+    uint32_t slot = 0, phase = 0;  // ring position of the next chunk
     const uint32_t full0 = smem_u32(&S.full[0]), empty0 = smem_u32(&S.empty[0]);
     const uint32_t ring_s = smem_u32(ring), acc_s = smem_u32(acc);
-    // A chunk = (info, this warp's slot-relative range wr, the first 128 of
-    // its entries in registers, its slot). (Fetching the next chunk before
-    // accumulating the current one measured 4x slower: not done.)
-    struct Chunk {
-        uint32_t info, slot;
-        uint2 wr;
-        uint2 e[4];
-    };
-    auto fetch = [&](Chunk& c) {  // the chunk at (slot, phase): wait, read, advance
-        mbar_wait_sleep_u32(full0 + 8 * slot, phase);
-        c.slot = slot;
-        c.info = S.meta[slot].info;
-        c.wr = S.meta[slot].wr[wid];
-        const uint32_t eb = ring_s + slot * (SLOT_E * 8u);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t q = c.wr.x + ln + 32u * u;
-            c.e[u] = lds_u2(eb + q * 8u);  // the ring has a 128-entry tail pad
-            if (q >= c.wr.y) c.e[u].x = TOMB;
-        }
-        if (++slot == NSLOT) {
-            slot = 0;
-            phase ^= 1u;
-        }
-    };
     auto rmw = [&](const uint2 (&e)[4], uint32_t accb, double w, auto unit_weight) {
         double o[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -863,32 +857,55 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             if (!(e[u].x & TOMB)) sts_f64(accb + e[u].x * 8u, __dadd_rn(o[u], x));
         }
     };
-    Chunk cur;
-    fetch(cur);
-    while (kk < nwork) {
-        const uint32_t list = cur.info & 127u, flags = (cur.info >> 7) & 7u, tile = cur.info >> 10;
-        const uint32_t kbase = tile * TILE;
-        if (list != CACHE_LIST) {
-            if (cur.wr.y > cur.wr.x) {
-                const uint32_t accb = acc_s - kbase * 8u;  // shared address of key k: accb + 8k
-                const double w = S.cw[list];
-                auto run = [&](auto unit_weight) {
-                    rmw(cur.e, accb, w, unit_weight);
-                    // ranges longer than 128 entries: the rest from the slot
-                    const uint32_t eb = ring_s + cur.slot * (SLOT_E * 8u);
-                    for (uint32_t p0 = cur.wr.x + 128 + ln; p0 < cur.wr.y; p0 += 128) {
-                        uint2 e[4];
+    // this warp's entries of slot positions [x, y): lane-consecutive, four in
+    // flight per lane (keys are unique within a list: independent RMWs)
+    auto load4 = [&](uint32_t eb, uint32_t x, uint32_t y, uint2 (&e)[4]) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint32_t q = p0 + 32u * u;
-                            e[u] = lds_u2(eb + q * 8u);
-                            if (q >= cur.wr.y) e[u].x = TOMB;
-                        }
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t q = x + ln + 32u * u;
+            e[u] = lds_u2(eb + q * 8u);  // the ring has a 128-entry tail pad
+            if (q >= y) e[u].x = TOMB;
+        }
+    };
+    while (kk < nwork) {
+        mbar_wait_sleep_u32(full0 + 8 * slot, phase);
+        const uint32_t info = S.meta[slot].info;
+        const uint32_t nsub = info & 7u, flags = (info >> 3) & 7u, tile = info >> 8;
+        const uint32_t kbase = tile * TILE;
+        const uint32_t eb = ring_s + slot * (SLOT_E * 8u);
+        if (!(flags & F_CACHE)) {
+            const uint32_t accb = acc_s - kbase * 8u;  // shared address of key k: accb + 8k
+            // the slot's list segments in gathered order; the next one's first
+            // entries are loaded before the current one is accumulated
+            uint2 wr = S.meta[slot].wr[0][wid];
+            uint2 e[4];
+            if (nsub) load4(eb, wr.x, wr.y, e);
+            for (uint32_t sb = 0; sb < nsub; ++sb) {
+                const uint32_t list = S.meta[slot].lists[sb];
+                uint2 wrn = make_uint2(0u, 0u);
+                uint2 en[4];
+                if (sb + 1 < nsub) {
+                    wrn = S.meta[slot].wr[sb + 1][wid];
+                    load4(eb, wrn.x, wrn.y, en);
+                }
+                if (wr.y > wr.x) {
+                    const double w = S.cw[list];
+                    auto run = [&](auto unit_weight) {
                         rmw(e, accb, w, unit_weight);
-                    }
-                };
-                if (w == 1.0) run(std::true_type{});  // w * double(s) == double(s)
-                else run(std::false_type{});
+                        for (uint32_t p0 = wr.x + 128; p0 < wr.y; p0 += 128) {  // long ranges
+                            uint2 t[4];
+                            load4(eb, p0, wr.y, t);
+                            rmw(t, accb, w, unit_weight);
+                        }
+                    };
+                    if (w == 1.0) run(std::true_type{});  // w * double(s) == double(s)
+                    else run(std::false_type{});
+                }
+                if (sb + 1 < nsub) {
+                    wr = wrn;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) e[u] = en[u];
+                }
             }
         } else {  // cached candidate scores (search_period > 1): this warp's keys
             for (uint32_t u = 0; u < WKEYS / 32; ++u) {
@@ -903,13 +920,14 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             }
         }
         __syncwarp();
-        if (ln == 0) mbar_arrive_u32(empty0 + 8 * cur.slot);
+        if (ln == 0) mbar_arrive_u32(empty0 + 8 * slot);
+        if (++slot == NSLOT) {
+            slot = 0;
+            phase ^= 1u;
+        }
         // each warp owns its keys in every tile: lists accumulate in order per
         // key without a CTA barrier, and the filter reads only the warp's keys
-        if (!(flags & F_TILE_END)) {
-            fetch(cur);
-            continue;
-        }
+        if (!(flags & F_TILE_END)) continue;
 
         // ---- tile end: this warp's 512 keys -> pool candidates ----
         {
@@ -1055,10 +1073,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     atomicMax(&S.cut, static_cast<uint32_t>(b));
             }
         }
-        if (!(flags & F_PROB_END)) {
-            fetch(cur);
-            continue;
-        }
+        if (!(flags & F_PROB_END)) continue;
         cbar();  // every warp's log and histogram counts are in
 
         if (unit_meta) {  // part unit / shard: hand histogram + log lengths on
@@ -1080,7 +1095,6 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 wlog_idx = log_idx + log_base(kk);
                 wlog_sc = log_sc + log_base(kk);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
-                fetch(cur);  // the next problem's first chunk
             } else {
                 cbar();
             }
@@ -1111,7 +1125,6 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 wlog_idx = log_idx + log_base(kk);
                 wlog_sc = log_sc + log_base(kk);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
-                fetch(cur);  // the next problem's first chunk
             } else {
                 cbar();
             }
@@ -1487,6 +1500,12 @@ uint32_t select_grid(uint32_t nprob, int num_sms) {
 
 uint32_t select_unit_meta_words() { return UNIT_META; }
 uint32_t select_ctas_per_sm() { return 2; }
+cudaError_t select_fin_debug(unsigned long long* out8, cudaStream_t st) {
+    cudaError_t e = cudaMemcpyFromSymbolAsync(out8, g_fin_dbg, 64, 0, cudaMemcpyDeviceToHost, st);
+    static const unsigned long long z[8] = {};
+    if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(g_fin_dbg, z, 64, 0, cudaMemcpyHostToDevice, st);
+    return e;
+}
 uint32_t select_tile_keys() { return TILE; }
 
 cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,

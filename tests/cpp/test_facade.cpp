@@ -116,12 +116,20 @@ static void lifecycle(std::size_t P, std::size_t T, std::size_t d, std::size_t m
     }
     CHECK(sel_diff == 0, "P=%zu %s: %zu of %zu selected sets differ", P, schedule, sel_diff, T);
     {
+        // the graph run asks for no softmax weights, so small batches take the
+        // fused cluster step (fused.cu) whose attention sums in another order
+        // than attend128's chunks: same selected sets, outputs within 1e-5
         const B::GraphRun gr = B::run_decode_graph(bg, tail(q), tail(k), tail(v), T);
         std::size_t gdiff = 0;
-        for (std::size_t t = 0; t < T; ++t)
-            gdiff += gr.selected[t] != br[t].selected ||
-                     !std::equal(br[t].attention.output.begin(), br[t].attention.output.end(),
-                                 gr.outputs.begin() + t * d);
+        for (std::size_t t = 0; t < T; ++t) {
+            double e2 = 0.0, n2 = 0.0;
+            for (std::size_t x = 0; x < d; ++x) {
+                const double a = br[t].attention.output[x], b = gr.outputs[t * d + x];
+                e2 += (a - b) * (a - b);
+                n2 += a * a;
+            }
+            gdiff += gr.selected[t] != br[t].selected || std::sqrt(e2 / n2) > 1e-5;
+        }
         CHECK(gdiff == 0, "P=%zu %s: %zu of %zu graph-run steps differ", P, schedule, gdiff, T);
         CHECK(bg.serialize() == bs.serialize(), "P=%zu: graph-run tables differ", P);
     }
