@@ -166,6 +166,10 @@ csattn_status csattn_ctx_set_kv_placement(csattn_ctx ctx, int32_t placement);
 void* csattn_ctx_stream(csattn_ctx ctx);
 /* Number of CUDA kernels this context has launched (driver-side evidence). */
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx);
+/* Table builds on this context that ran the tcgen05 screen (build_tc.cu),
+ * and how many of those were rebuilt by the plain fp64 kernels because a
+ * table's screen was inconclusive (results are identical either way). */
+csattn_status csattn_ctx_build_stats(csattn_ctx ctx, uint64_t* tc_builds, uint64_t* fallbacks);
 /* Kernel timing: when enabled, the three kernels of every decode step
  * (select, attend, insert) are bracketed by CUDA events on the context's
  * stream. read returns the summed milliseconds per kernel (ms[3]) and the

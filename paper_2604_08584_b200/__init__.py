@@ -257,6 +257,14 @@ class Context:
     def launches(self) -> int:
         return lib().csattn_ctx_launch_count(self.h)
 
+    @property
+    def build_stats(self) -> tuple:
+        """(table builds through the tcgen05 screen, of those rebuilt by the
+        plain fp64 kernels because a table's screen was inconclusive)."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(lib().csattn_ctx_build_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def profile(self, enable: bool = True):
         """Bracket every decode / insert launch with CUDA events on this stream."""
         _check(lib().csattn_ctx_profile(self.h, int(enable)))

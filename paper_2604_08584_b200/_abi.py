@@ -108,6 +108,7 @@ SIGNATURES = {
     "csattn_ctx_destroy": (C.c_int, [vp]),
     "csattn_ctx_synchronize": (C.c_int, [vp]),
     "csattn_ctx_launch_count": (u64, [vp]),
+    "csattn_ctx_build_stats": (C.c_int, [vp, P(u64), P(u64)]),
     "csattn_ctx_profile": (C.c_int, [vp, i32]),
     "csattn_ctx_profile_read": (C.c_int, [vp, P(C.c_double), P(u64), i32]),
     "csattn_prefill": (C.c_int, [vp, vp, u64, vp, vp, u64, u64, P(u64), u64, P(IndexConfigC),

@@ -76,6 +76,7 @@ __device__ __forceinline__ unsigned long long sel_key(float s, uint32_t i) {
 
 struct BuildSmem {
     RefillSmem r;
+    uint32_t hist[2048];  // 11-bit radix digits
     float rmin[BL_THREADS / 32], rmax[BL_THREADS / 32];
 };
 
@@ -87,28 +88,22 @@ build_lists_kernel(const SessionDev* __restrict__ sp, const float* __restrict__ 
     const float* sc = scores + static_cast<size_t>(t) * P;
     const uint32_t keep = sd.L < P ? sd.L : P;
     unsigned long long thr = 0;  // select iff sel_key >= thr
-    if (keep < P)
-        thr = cta_kth_largest(S.r, P, keep, [&](uint32_t i) { return sel_key(sc[i], i); });
+    if (keep < P) {
+        auto key_of = [&](uint32_t i) { return sel_key(sc[i], i); };
+        unsigned long long mn, mx;
+        cta_minmax(S.r, P, key_of, mn, mx);
+        thr = cta_kth_largest_mm<11>(S.r, S.hist, P, keep, mn, mx, key_of);
+    }
     uint2* e = sd.ent + static_cast<size_t>(t) * sd.cap2;
-    uint32_t out = 0;
     float smin = INFINITY, smax = -INFINITY;  // live score bounds (SessionDev::tmm)
-    for (uint32_t c0 = 0; c0 < P; c0 += blockDim.x) {
-        const uint32_t i = c0 + threadIdx.x;
-        float s = 0.0f;
-        uint32_t keepi = 0;
-        if (i < P) {
-            s = sc[i];
-            keepi = sel_key(s, i) >= thr ? 1u : 0u;
-        }
-        uint32_t tot;
-        const uint32_t ex = tbl_block_excl_scan(S.r, keepi, tot);
-        if (keepi) {
-            e[out + ex] = make_uint2(i, __float_as_uint(s));
+    const uint32_t out = cta_compact(
+        S.r, P, false, [&](uint32_t i) { return sc[i]; },
+        [&](uint32_t i, float s) { return sel_key(s, i) >= thr; },
+        [&](uint32_t pos, uint32_t i, float s) {
+            e[pos] = make_uint2(i, __float_as_uint(s));
             smin = fminf(smin, s);
             smax = fmaxf(smax, s);
-        }
-        out += tot;
-    }
+        });
     for (int o = 16; o; o >>= 1) {
         smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, o));
         smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));

@@ -203,6 +203,8 @@ struct csattn_ctx_s {
     DevMem dense;  // dense oracle scratch (dense.cu)
     // KV placement of sessions created from now on (csattn_ctx_set_kv_placement)
     bool kv_host = false;
+    // table builds through the tcgen05 screen, and those rebuilt by the fp64 path
+    uint64_t build_tc = 0, build_fallback = 0;
     bool host_prof = std::getenv("CSATTN_HOST_PROF") != nullptr;
     double host_sum[4] = {0, 0, 0, 0}, host_sub[4] = {0, 0, 0, 0}, host_sub2[3] = {0, 0, 0};
     uint64_t host_n = 0;
@@ -457,6 +459,28 @@ void attach_rows(csattn_session_s* s, const float* keys, const float* values, bo
 // assemble_index on the device (index.cpp:107-141)
 void build_tables(csattn_session_s* s) {
     push_dev(s);
+    csattn_ctx ctx = s->ctx;
+    // the tcgen05 screen + exact fp64 rescore (build_tc.cu); CSATTN_BUILD=fp64
+    // forces the plain fp64 kernels. Mapped-host KV rows stay on the fp64 path.
+    const char* mode = std::getenv("CSATTN_BUILD");
+    const bool force_fp64 = mode && std::strcmp(mode, "fp64") == 0;
+    if (!force_fp64 && !s->pre->k.host && csa::build_tc_eligible(s->h)) {
+        const char* qm = std::getenv("CSATTN_BUILD_QMARGIN");  // test hook
+        const float qmargin = qm ? static_cast<float>(std::atof(qm)) : 0.0f;
+        DevMem scratch, fail;
+        scratch.alloc(csa::build_tc_scratch_bytes(s->h, nullptr));
+        fail.alloc(4);
+        ck(csa::launch_build_tc(s->dev.as<csa::SessionDev>(), s->h, scratch.p, qmargin, fail.as<uint32_t>(),
+                                ctx->stream),
+           "build_tc launch");
+        ctx->launches += 4;
+        uint32_t nfail = 0;
+        ck(cudaMemcpyAsync(&nfail, fail.p, 4, cudaMemcpyDeviceToHost, ctx->stream), "build_tc flag");
+        ck(cudaStreamSynchronize(ctx->stream), "build_tc");
+        ctx->build_tc += 1;
+        if (nfail == 0) return;
+        ctx->build_fallback += 1;  // a table's screen was inconclusive: rebuild exactly
+    }
     DevMem scores;
     scores.alloc(s->T() * s->h.P * sizeof(float));
     ck(csa::launch_build_scores(s->dev.as<csa::SessionDev>(), s->h, scores.as<float>(),
@@ -1405,6 +1429,14 @@ csattn_status csattn_ctx_synchronize(csattn_ctx ctx) {
 }
 
 uint64_t csattn_ctx_launch_count(csattn_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+csattn_status csattn_ctx_build_stats(csattn_ctx ctx, uint64_t* tc_builds, uint64_t* fallbacks) {
+    return guard([&] {
+        if (!ctx) fail(CSATTN_ERR_PARAMETER, "null context");
+        if (tc_builds) *tc_builds = ctx->build_tc;
+        if (fallbacks) *fallbacks = ctx->build_fallback;
+    });
+}
 
 csattn_status csattn_ctx_profile(csattn_ctx ctx, int32_t enable) {
     return guard([&] { ctx->profile = enable != 0; });

@@ -30,8 +30,10 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
 // log_cap entries each, unit_meta: select_unit_meta_words() per unit) and
 // finalised by the merge kernel (one CTA per problem).
 uint32_t select_unit_meta_words();
-uint32_t select_ctas_per_sm();
-cudaError_t select_fin_debug(unsigned long long* out8, cudaStream_t st);  // temporary  // resident select CTAs per SM (grid = this x SMs)
+uint32_t select_ctas_per_sm();  // resident select CTAs per SM (grid = this x SMs)
+// CSATTN_PHASE_PROF only: the final-selection stage times (ns, summed over
+// problems; [6] = problem count) accumulated since the library loaded.
+cudaError_t select_fin_debug(unsigned long long* out8, cudaStream_t st);
 uint32_t select_tile_keys();
 cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                                 uint32_t split, const uint32_t* unit_meta, const uint32_t* log_idx,
@@ -126,6 +128,14 @@ cudaError_t launch_shard_extract(const SessionDev* full_dev, const SessionDev* s
                                  uint32_t tables, uint32_t key_lo, uint32_t key_hi, cudaStream_t st);
 cudaError_t launch_build_lists(const SessionDev* s_dev, const SessionDev& s_host,
                                const float* scores, cudaStream_t st);
+// tcgen05 screen + exact rescore build (build_tc.cu): eligibility (layout,
+// sizes, driver entry point), scratch size, and the 4-kernel launch; fail_dev
+// counts tables whose screen was inconclusive (the host then rebuilds with
+// build_scores/build_lists).
+bool build_tc_eligible(const SessionDev& sh);
+size_t build_tc_scratch_bytes(const SessionDev& sh, uint32_t* cap_out);
+cudaError_t launch_build_tc(const SessionDev* s_dev, const SessionDev& sh, void* scratch, float qmargin,
+                            uint32_t* fail_dev, cudaStream_t st);
 
 
 // fnapi.cu: the function-level API kernels (score_keys / streaming_insert
