@@ -15,7 +15,10 @@ rows [P + s*T, P + (s+1)*T).
 A step = one decode step of the whole layer for all 16 sequences: centroid
 routing, gather/accumulate, top-K, sparse attention for 512 (sequence, query
 head) problems, then append + streaming insert for 128 (sequence, KV head)
-sessions: 5 kernel launches (route, select, select retry pass, attend, insert).
+sessions: 5 kernel launches (route, select, select retry pass, attend, insert)
+for batches that fill the GPU (c3, c4); small batches (c2) run the fused
+cluster step instead (fused.cu: one launch for route + select + attend, then
+insert).
 
 value = device time per layer-step in microseconds (lower is better), CUDA
 events on the launching stream, max over ranks. e2e = the same through the
