@@ -183,6 +183,11 @@ struct csattn_ctx_s {
     DevMem log_idx, log_sc; // select.cu candidate logs: log_rows x log_cap
     DevMem retry;           // select.cu retry list (speculative cut too high)
     DevMem ulog_idx, ulog_sc, umeta;  // split select: per part-unit logs + histograms
+    // mixed (tail-split) select: piece logs + histograms, per-problem piece
+    // counters (zero between steps: the finalising CTA resets its problem's)
+    DevMem mlog_idx, mlog_sc, mumeta, pdone;
+    uint64_t pdone_n = 0;
+    bool tail_split = !(std::getenv("CSATTN_TAIL_SPLIT") && std::atoi(std::getenv("CSATTN_TAIL_SPLIT")) == 0);
     // sharded steps (csattn_shard_step): descriptors + scratch kept across phases
     DevMem sh_desc, sh_pstate, sh_bitmap, sh_kdev, sh_ulog_idx, sh_ulog_sc, sh_umeta, sh_chunks;
     std::vector<csa::DecodeProblem> sh_hprobs;
@@ -216,6 +221,9 @@ struct csattn_ctx_s {
     uint64_t un_items = 0, un_tiles = 0, un_launches = 0;
     uint64_t log_cap = 0, log_rows = 0;
     int num_sms = 148;
+    // SMs the decode-step select grid assumes (CSATTN_SELECT_SMS: a test hook
+    // that shrinks the grid so small batches exercise the round/tail logic)
+    int sel_sms = std::getenv("CSATTN_SELECT_SMS") ? std::max(1, std::atoi(std::getenv("CSATTN_SELECT_SMS"))) : 0;
     // select speculation margin (CSATTN_SPEC_KEEP; 0 disables, > 1 forces the
     // retry pass — used by the tests to exercise it)
     double spec_keep = std::getenv("CSATTN_SPEC_KEEP") ? std::atof(std::getenv("CSATTN_SPEC_KEEP")) : 0.9;
@@ -767,6 +775,68 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->counters_n = nq;
     }
     ctx->part.ensure(nchunks * (d + 2) * sizeof(float));
+    // Mixed select plan: problems beyond whole rounds of the select grid are
+    // cut into contiguous tile pieces spread over the CTAs (one piece range
+    // per CTA), instead of a second, partly idle round.
+    std::vector<uint4> m_items;
+    std::vector<uint32_t> m_cta;
+    std::vector<uint2> m_pinfo, m_slot;
+    uint64_t m_log = 0;
+    {
+        const uint64_t G = csa::select_grid(static_cast<uint32_t>(nq), ctx->sel_sms ? ctx->sel_sms : ctx->num_sms);
+        const uint64_t tile = csa::select_tile_keys();
+        if (!fused && ctx->tail_split && nq > G && nq % G != 0) {
+            const uint64_t W = nq / G * G;
+            std::vector<uint64_t> tpre(1, 0);  // tail tile prefix
+            uint64_t tmax = 1;
+            for (uint64_t i = W; i < nq; ++i) {
+                const uint64_t nt = (ctx->hprobs[i].N + tile - 1) / tile;
+                tpre.push_back(tpre.back() + nt);
+                tmax = std::max(tmax, nt);
+            }
+            const uint64_t TT = tpre.back();
+            // piece ranges of >= 1 tile and <= MAXPART pieces per problem
+            const uint64_t Gp = std::max<uint64_t>(1, std::min<uint64_t>({G, TT, 15 * TT / tmax}));
+            m_cta.assign(G + 1, 0);
+            m_pinfo.assign(nq, make_uint2(0, 0));
+            bool ok = true;
+            uint64_t q = 0;  // tail problem cursor (relative to W)
+            for (uint64_t c = 0; c < G; ++c) {
+                m_cta[c] = static_cast<uint32_t>(m_items.size());
+                for (uint64_t pw = c; pw < W; pw += G)
+                    m_items.push_back(make_uint4(static_cast<uint32_t>(pw), 0u,
+                                                 static_cast<uint32_t>((ctx->hprobs[pw].N + tile - 1) / tile),
+                                                 csa::NO_SLOT));
+                if (c >= Gp) continue;
+                uint64_t a = c * TT / Gp;
+                const uint64_t b = (c + 1) * TT / Gp;
+                while (a < b) {
+                    while (tpre[q + 1] <= a) ++q;
+                    const uint64_t e = std::min(b, tpre[q + 1]);
+                    const uint32_t pr = static_cast<uint32_t>(W + q);
+                    const uint32_t sl = static_cast<uint32_t>(m_slot.size());
+                    if (m_pinfo[pr].y == 0) m_pinfo[pr].x = sl;
+                    if (++m_pinfo[pr].y > csa::SELECT_MAX_PART) ok = false;
+                    const uint64_t nt = e - a;
+                    m_slot.push_back(make_uint2(static_cast<uint32_t>(m_log),
+                                                static_cast<uint32_t>(nt * tile / csa::SELECT_CONSUMER_WARPS)));
+                    m_log += nt * tile;
+                    m_items.push_back(make_uint4(pr, static_cast<uint32_t>(a - tpre[q]),
+                                                 static_cast<uint32_t>(e - tpre[q]), sl));
+                    a = e;
+                }
+            }
+            m_cta[G] = static_cast<uint32_t>(m_items.size());
+            if (!ok || m_log > 0xffffffffull) {
+                m_items.clear();
+                m_cta.clear();
+                m_pinfo.clear();
+                m_slot.clear();
+                m_log = 0;
+            }
+        }
+    }
+    const bool mixed_sel = !m_items.empty();
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t dbytes = nq * sizeof(csa::DecodeProblem);
     const size_t ibytes = ns * sizeof(csa::InsertProblem);
@@ -776,7 +846,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const size_t uoff = poff + al(nchunks * 4);  // union tables: gP | gmember | members | mgroup
     const size_t u_gm = uoff + al(ngroups * 4), u_m = u_gm + al(ugmem.size() * 4);
     const size_t u_mg = u_m + al(nmem * 4);
-    const size_t need = u_mg + nmem * 4;
+    const size_t m_it = u_mg + al(nmem * 4);  // mixed select: items | cta_items | pinfo | slotinfo
+    const size_t m_ct = m_it + al(m_items.size() * 16), m_pi = m_ct + al(m_cta.size() * 4);
+    const size_t m_si = m_pi + al(m_pinfo.size() * 8);
+    const size_t need = m_si + m_slot.size() * 8;
     char *hb = nullptr, *db = nullptr;
     if (slot) {
         if (need > slot->cap) {
@@ -836,6 +909,12 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         std::memcpy(hb + u_m, umem.data(), nmem * 4);
         std::memcpy(hb + u_mg, umgrp.data(), nmem * 4);
     }
+    if (mixed_sel) {
+        std::memcpy(hb + m_it, m_items.data(), m_items.size() * 16);
+        std::memcpy(hb + m_ct, m_cta.data(), m_cta.size() * 4);
+        std::memcpy(hb + m_pi, m_pinfo.data(), m_pinfo.size() * 8);
+        std::memcpy(hb + m_si, m_slot.data(), m_slot.size() * 8);
+    }
     if (!cap)  // a captured step's descriptors go up with its chunk (run_graph)
         ck(cudaMemcpyAsync(db, hb, need, cudaMemcpyHostToDevice, ctx->stream),
            "descriptor upload");
@@ -861,7 +940,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
                          ctx->stream),
        "route launch");
-    const uint32_t sgrid = csa::select_grid(static_cast<uint32_t>(nq), ctx->num_sms);
+    const int sel_sms = ctx->sel_sms ? ctx->sel_sms : ctx->num_sms;
+    const uint32_t sgrid = csa::select_grid(static_cast<uint32_t>(nq), sel_sms);
     // Split select for small batches: with fewer problems than CTA slots, each
     // problem's key range is cut into `split` part units (>= one tile each)
     // that run in parallel, then merged (select_merge_kernel).
@@ -873,7 +953,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         max_tiles = std::max(max_tiles, nt);
     }
     uint32_t split = 1;
-    const uint64_t slots = static_cast<uint64_t>(csa::select_ctas_per_sm()) * ctx->num_sms;  // resident
+    const uint64_t slots = static_cast<uint64_t>(csa::select_ctas_per_sm()) * sel_sms;  // resident
     if (nq < slots && !ctx->no_split) {
         split = static_cast<uint32_t>((slots + nq - 1) / nq);
         split = static_cast<uint32_t>(std::min<uint64_t>(std::min<uint64_t>(split, 16), min_tiles));
@@ -897,6 +977,25 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ctx->log_idx.alloc(ctx->log_rows * ctx->log_cap * 4);
         ctx->log_sc.alloc(ctx->log_rows * ctx->log_cap * 8);
     }
+    csa::SelMixed smx;
+    if (mixed_sel) {
+        ctx->mlog_idx.ensure(m_log * 4);
+        ctx->mlog_sc.ensure(m_log * 8);
+        ctx->mumeta.ensure(m_slot.size() * csa::select_unit_meta_words() * 4);
+        if (nq > ctx->pdone_n) {
+            ctx->pdone.alloc(nq * 4);
+            ck(cudaMemsetAsync(ctx->pdone.p, 0, nq * 4, ctx->stream), "memset");
+            ctx->pdone_n = nq;
+        }
+        smx.items = reinterpret_cast<const uint4*>(db + m_it);
+        smx.cta_items = reinterpret_cast<const uint32_t*>(db + m_ct);
+        smx.pinfo = reinterpret_cast<const uint2*>(db + m_pi);
+        smx.slotinfo = reinterpret_cast<const uint2*>(db + m_si);
+        smx.pdone = ctx->pdone.as<uint32_t>();
+        smx.plog_idx = ctx->mlog_idx.as<uint32_t>();
+        smx.plog_sc = ctx->mlog_sc.as<double>();
+        smx.umeta = ctx->mumeta.as<uint32_t>();
+    }
     if (!live) {
         if (split > 1) {  // grow the split buffers only
             const uint64_t ucap = (max_tiles + split - 1) / split * tile;
@@ -909,7 +1008,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
                               sgrid, ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
                               static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
-                              rcount, ctx->spec_keep, 1, nullptr, ctx->stream),
+                              rcount, ctx->spec_keep, 1, nullptr, ctx->stream, mixed_sel ? &smx : nullptr),
            "select launch");
     } else {
         // per-unit logs: a unit has at most ceil(max_tiles / split) tiles

@@ -21,11 +21,34 @@ uint32_t select_grid(uint32_t nprob, int num_sms);
 //   retry_in/retry_in_count: when non-null, process only the listed problems,
 //   without speculation (the second pass); retry_out/retry_out_count: where the
 //   first pass lists problems whose speculative cut proved too high.
+// Mixed mode (tail split): when the problems do not fill whole rounds of
+// the grid, every CTA takes its whole problems and then a contiguous piece
+// of the remaining problems' tiles. items[i] = (problem, tile_lo, tile_hi,
+// slot), slot = NO_SLOT for a whole problem; CTA c owns items
+// [cta_items[c], cta_items[c+1]). A piece dumps its histogram + per-warp log
+// lengths to umeta[slot] and its log to plog at slotinfo[slot] = (offset,
+// per-warp stride); pinfo[p] = (first slot, pieces) of a split problem; the
+// CTA whose atomicAdd on pdone[p] completes the count merges and finalises
+// it (pdone must start at zero; the finaliser resets it).
+constexpr uint32_t NO_SLOT = 0xffffffffu;
+constexpr uint32_t SELECT_MAX_PART = 16;      // pieces per problem (seg tables)
+constexpr uint32_t SELECT_CONSUMER_WARPS = 8;  // per-warp log regions
+struct SelMixed {
+    const uint4* items = nullptr;
+    const uint32_t* cta_items = nullptr;
+    const uint2* pinfo = nullptr;
+    const uint2* slotinfo = nullptr;
+    uint32_t* pdone = nullptr;
+    uint32_t* plog_idx = nullptr;
+    double* plog_sc = nullptr;
+    uint32_t* umeta = nullptr;
+};
 cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
                           const uint32_t* retry_in, const uint32_t* retry_in_count,
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
-                          uint32_t split, uint32_t* unit_meta, cudaStream_t st);
+                          uint32_t split, uint32_t* unit_meta, cudaStream_t st,
+                          const SelMixed* mixed = nullptr);
 // split > 1: each problem's tiles are cut into `split` part units (logs of
 // log_cap entries each, unit_meta: select_unit_meta_words() per unit) and
 // finalised by the merge kernel (one CTA per problem).

@@ -64,6 +64,7 @@ constexpr int RANK_DIRECT = 384;             // O(n^2) ranking up to this size
 constexpr uint32_t F_TILE_END = 1, F_PROB_END = 2, F_CACHE = 4;
 constexpr int MAXPART = 16;                  // key-range parts of a split problem
 constexpr uint32_t MAXSEG = MAXPART * 8;     // log segments (parts x warps)
+static_assert(SELECT_MAX_PART == MAXPART && SELECT_CONSUMER_WARPS == SEL_CW, "kernels.h mirrors");
 constexpr uint32_t UNIT_META = 2048 + 64 + 8;  // per part unit: hist, coarse, per-warp log lengths
 constexpr unsigned long long ABSENT = 0x7ff4deadbeef0000ull;  // NaN box: key not gathered
 static_assert(TILE * 64 == SELECT_MAX_CONTEXT, "bitmap capacity = accumulator bits");
@@ -94,7 +95,7 @@ struct SelHdr {
     uint32_t seg_len[MAXSEG], seg_off[MAXSEG], seg_pre[MAXSEG + 1];
     uint32_t wsum[SEL_CW];
     // final-phase broadcasts
-    uint32_t f_bin, f_above, f_count, f_take_all, f_fail;
+    uint32_t f_bin, f_above, f_count, f_take_all, f_fail, f_last;
     unsigned long long tk;
     uint32_t tx;
 };
@@ -619,25 +620,42 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
               uint32_t log_cap, const uint32_t* __restrict__ retry_in,
               const uint32_t* __restrict__ retry_in_count, uint32_t* __restrict__ retry_out,
               uint32_t* __restrict__ retry_out_count, double spec_keep, uint32_t split,
-              uint32_t* __restrict__ unit_meta) {
+              uint32_t* __restrict__ unit_meta, const SelMixed mx) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // The work sequence of this CTA: units b, b + grid, ... A unit is problem
     // u / split, tiles [part u % split] of its key range; split == 1 (one unit
     // per problem, finalised here) or split > 1 (part units dump histogram and
     // log lengths to unit_meta; select_merge_kernel finalises). The retry pass
     // walks the retry list (split == 1 only).
-    const uint32_t nwork = retry_in ? __ldcg(retry_in_count) : nprob * split;
-    if (blockIdx.x >= nwork) return;
-    auto prob_of = [&](uint32_t k) { return retry_in ? __ldcg(retry_in + k) : k / split; };
+    // Mixed mode (mx.items): this CTA walks its own item list, whole problems
+    // (finalised here) then tail pieces (part units: histogram + log to
+    // mx.umeta / the part logs; the CTA finishing a problem's LAST piece
+    // merges them and finalises it), so 512 problems over 296 slots cost
+    // 1.73 problems per CTA instead of two rounds.
+    const bool mixed = mx.items != nullptr;
+    const uint32_t it0 = mixed ? __ldg(mx.cta_items + blockIdx.x) : 0u;
+    const uint32_t it1 = mixed ? __ldg(mx.cta_items + blockIdx.x + 1) : 0u;
+    const uint32_t nwork = mixed ? it1 : (retry_in ? __ldcg(retry_in_count) : nprob * split);
+    const uint32_t kfirst = mixed ? it0 : blockIdx.x, kstep = mixed ? 1u : gridDim.x;
+    if (kfirst >= nwork) return;
+    auto prob_of = [&](uint32_t k) {
+        return mixed ? __ldg(&mx.items[k].x) : (retry_in ? __ldcg(retry_in + k) : k / split);
+    };
     // unit k's tiles: part k % split of the problem's tile range (a shard's
-    // range [tile_lo, tile_hi), else all tiles of its N keys)
+    // range [tile_lo, tile_hi), else all tiles of its N keys); mixed: the item's
     auto tiles_of = [&](uint32_t k, const DecodeProblem& P, uint32_t& tl, uint32_t& th) {
+        if (mixed) {
+            tl = __ldg(&mx.items[k].y);
+            th = __ldg(&mx.items[k].z);
+            return;
+        }
         const uint32_t t0 = P.tile_hi ? P.tile_lo : 0u;
         const uint32_t t1 = P.tile_hi ? P.tile_hi : div_up(P.N, TILE);
         const uint32_t nt = t1 - t0, j = retry_in ? 0u : k % split;
         tl = t0 + (nt * j) / split;
         th = t0 + (nt * (j + 1)) / split;
     };
+    auto slot_of = [&](uint32_t k) { return mixed ? __ldg(&mx.items[k].w) : NO_SLOT; };
     const bool speculate = (retry_out != nullptr || unit_meta != nullptr) && !retry_in;
     SelHdr& S = *reinterpret_cast<SelHdr*>(smem_raw);
     unsigned char* p0 = smem_raw + ((sizeof(SelHdr) + 127) & ~size_t(127));
@@ -706,7 +724,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             }
             __syncwarp();
         };
-        for (uint32_t k = blockIdx.x; k < nwork; k += gridDim.x) {
+        for (uint32_t k = kfirst; k < nwork; k += kstep) {
             const uint32_t p = prob_of(k);
             const DecodeProblem& P = probs[p];
             const SessionDev& sd = *P.s;
@@ -821,20 +839,34 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     }
 
     // ======================= consumer warps =======================
-    uint32_t kk = blockIdx.x;
+    uint32_t kk = kfirst;
     uint32_t p = prob_of(kk);
     ProbState st;
     setup_problem(S, probs, plans, p, st, speculate, spec_keep);
     // warp w logs into its own region (it owns 1/8 of every tile's keys): the
-    // CTA's log (split == 1) or the unit's (split > 1, log_cap per unit)
+    // CTA's log (split == 1, mixed whole items), the unit's (split > 1,
+    // log_cap per unit) or the piece's (mixed part items: mx.slotinfo)
     uint32_t wlog_n = 0;
     auto log_base = [&](uint32_t k) -> size_t {
         return (split == 1 ? static_cast<size_t>(0) : static_cast<size_t>(k) * log_cap -
                                                           static_cast<size_t>(blockIdx.x) * log_cap) +
                static_cast<size_t>(wid) * (log_cap / SEL_CW);
     };
-    uint32_t* wlog_idx = log_idx + log_base(kk);
-    double* wlog_sc = log_sc + log_base(kk);
+    auto set_log = [&](uint32_t k, uint32_t*& li, double*& ls) {
+        const uint32_t sl = slot_of(k);
+        if (sl != NO_SLOT) {
+            const uint2 si = __ldg(mx.slotinfo + sl);
+            const size_t b = static_cast<size_t>(si.x) + static_cast<size_t>(wid) * si.y;
+            li = mx.plog_idx + b;
+            ls = mx.plog_sc + b;
+        } else {
+            li = log_idx + log_base(k);
+            ls = log_sc + log_base(k);
+        }
+    };
+    uint32_t* wlog_idx;
+    double* wlog_sc;
+    set_log(kk, wlog_idx, wlog_sc);
     uint16_t* const wcidx = cidx + wid * WKEYS;
     double* const wacc = acc + wid * WKEYS;
     uint32_t slot = 0, phase = 0;  // ring position of the next chunk
@@ -1092,8 +1124,58 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             kk += gridDim.x;
             if (kk < nwork) {
                 p = prob_of(kk);
-                wlog_idx = log_idx + log_base(kk);
-                wlog_sc = log_sc + log_base(kk);
+                set_log(kk, wlog_idx, wlog_sc);
+                setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
+            } else {
+                cbar();
+            }
+            continue;
+        }
+        const uint32_t slot = slot_of(kk);
+        if (slot != NO_SLOT) {  // mixed-mode piece: dump, and the last piece merges
+            uint32_t* const um = mx.umeta + static_cast<size_t>(slot) * UNIT_META;
+            if (ln == 0) um[NB + NCB + wid] = wlog_n;
+            for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) {
+                um[x] = hist[x];
+                hist[x] = 0;
+            }
+            __threadfence();  // this piece's log, histogram and lengths before the count
+            cbar();
+            const uint2 pi = __ldg(mx.pinfo + p);  // (first slot, pieces) of the problem
+            if (tid == 0) S.f_last = atomicAdd(mx.pdone + p, 1u) + 1u == pi.y ? 1u : 0u;
+            cbar();
+            if (S.f_last) {
+                __threadfence();  // the other pieces' data (they fenced before counting)
+                for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) {
+                    uint32_t v = 0;
+                    for (uint32_t j = 0; j < pi.y; ++j)
+                        v += __ldcg(mx.umeta + static_cast<size_t>(pi.x + j) * UNIT_META + x);
+                    hist[x] = v;
+                }
+                if (tid < pi.y * SEL_CW) {
+                    const uint32_t j = tid / SEL_CW, w = tid % SEL_CW;
+                    const uint2 si = __ldg(mx.slotinfo + pi.x + j);
+                    S.seg_len[tid] = __ldcg(mx.umeta + static_cast<size_t>(pi.x + j) * UNIT_META + NB + NCB + w);
+                    S.seg_off[tid] = si.x + w * si.y;
+                }
+                cbar();
+                final_select(S, st, p, hist, coarse, bm, bkey, bidx, mx.plog_idx, mx.plog_sc, pi.y * SEL_CW,
+                             retry_out, retry_out_count);
+                const uint32_t nw = div_up(st.N, 32);
+                cbar();  // bitmap emitted, scratch free
+                for (uint32_t x = tid; x < div_up(nw, 2); x += SEL_CT) acc[x] = neg0_d();
+                for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) hist[x] = 0;
+                if (tid == 0) mx.pdone[p] = 0;  // ready for the next step
+            }
+            if (tid == 0) {
+                S.cut = 0;
+                S.nbkt = 0;
+            }
+            wlog_n = 0;
+            kk += kstep;
+            if (kk < nwork) {
+                p = prob_of(kk);
+                set_log(kk, wlog_idx, wlog_sc);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
             } else {
                 cbar();
@@ -1119,11 +1201,10 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 S.nbkt = 0;
             }
             wlog_n = 0;
-            kk += gridDim.x;
+            kk += kstep;
             if (kk < nwork) {
                 p = prob_of(kk);
-                wlog_idx = log_idx + log_base(kk);
-                wlog_sc = log_sc + log_base(kk);
+                set_log(kk, wlog_idx, wlog_sc);
                 setup_problem(S, probs, plans, p, st, speculate, spec_keep);  // ends with a barrier
             } else {
                 cbar();
@@ -1527,7 +1608,7 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
                           const uint32_t* retry_in, const uint32_t* retry_in_count,
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
-                          uint32_t split, uint32_t* unit_meta, cudaStream_t st) {
+                          uint32_t split, uint32_t* unit_meta, cudaStream_t st, const SelMixed* mixed) {
     const size_t smem = select_smem();
     {  // once per device (a host call per launch otherwise)
         static bool set[64] = {};
@@ -1543,7 +1624,8 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
     }
     select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap,
                                                    retry_in, retry_in_count, retry_out,
-                                                   retry_out_count, spec_keep, split, unit_meta);
+                                                   retry_out_count, spec_keep, split, unit_meta,
+                                                   mixed ? *mixed : SelMixed{});
     return cudaGetLastError();
 }
 
