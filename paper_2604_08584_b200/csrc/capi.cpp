@@ -166,7 +166,12 @@ struct csattn_ctx_s {
     size_t cap_step = 0, cap_bytes = 0;
     void* cap_host = nullptr;
     DevMem cap_dev, run_stage;
+    // side stream for the attention work-list upload (runs beside select)
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_ev = nullptr;
     ~csattn_ctx_s() {
+        if (side) cudaStreamDestroy(side);
+        if (side_ev) cudaEventDestroy(side_ev);
         for (Slot& s : ring) {
             if (s.host) cudaFreeHost(s.host);
             if (s.done) cudaEventDestroy(s.done);
@@ -621,9 +626,11 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         char* base = ctx->stage.as<char>();
         // copies first (scratch staging: harmless if the scan below refuses),
         // so the DMA overlaps the scan
-        upload(ctx, base + o_q, q, nq * d * 4, true);
-        upload(ctx, base + o_k, keys, ns * d * 4, true);
-        upload(ctx, base + o_v, values, ns * d * 4, true);
+        // host-buffer calls: the inputs are host memory by contract (an
+        // explicit direction skips the runtime's pointer lookup)
+        ck(cudaMemcpyAsync(base + o_q, q, nq * d * 4, cudaMemcpyHostToDevice, ctx->stream), "copy in");
+        ck(cudaMemcpyAsync(base + o_k, keys, ns * d * 4, cudaMemcpyHostToDevice, ctx->stream), "copy in");
+        ck(cudaMemcpyAsync(base + o_v, values, ns * d * 4, cudaMemcpyHostToDevice, ctx->stream), "copy in");
         require_finite(keys, ns * d, "appended key");
         require_finite(values, ns * d, "appended value");
         dq = reinterpret_cast<float*>(base + o_q);
@@ -838,18 +845,22 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     const bool mixed_sel = !m_items.empty();
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    // descriptor layout, in two parts uploaded separately: A (problems,
+    // inserts, mixed-select tables) before the route/select launches, B (the
+    // attention work list and union tables) built and uploaded while select
+    // runs on the GPU
     const size_t dbytes = nq * sizeof(csa::DecodeProblem);
     const size_t ibytes = ns * sizeof(csa::InsertProblem);
     const size_t ioff = al(dbytes);
-    const size_t boff = ioff + al(ibytes);
+    const size_t m_it = ioff + al(ibytes);  // mixed select: items | cta_items | pinfo | slotinfo
+    const size_t m_ct = m_it + al(m_items.size() * 16), m_pi = m_ct + al(m_cta.size() * 4);
+    const size_t m_si = m_pi + al(m_pinfo.size() * 8);
+    const size_t boff = m_si + al(m_slot.size() * 8);  // part B
     const size_t poff = boff + al((nq + 1) * 4);
     const size_t uoff = poff + al(nchunks * 4);  // union tables: gP | gmember | members | mgroup
     const size_t u_gm = uoff + al(ngroups * 4), u_m = u_gm + al(ugmem.size() * 4);
     const size_t u_mg = u_m + al(nmem * 4);
-    const size_t m_it = u_mg + al(nmem * 4);  // mixed select: items | cta_items | pinfo | slotinfo
-    const size_t m_ct = m_it + al(m_items.size() * 16), m_pi = m_ct + al(m_cta.size() * 4);
-    const size_t m_si = m_pi + al(m_pinfo.size() * 8);
-    const size_t need = m_si + m_slot.size() * 8;
+    const size_t need = u_mg + nmem * 4;
     char *hb = nullptr, *db = nullptr;
     if (slot) {
         if (need > slot->cap) {
@@ -871,8 +882,21 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         db = ctx->cap_dev.as<char>() + ctx->cap_off[t];
     }
     if (live) {
-    std::memcpy(hb, ctx->hprobs.data(), dbytes);
-    std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
+        std::memcpy(hb, ctx->hprobs.data(), dbytes);
+        std::memcpy(hb + ioff, ctx->hiprobs.data(), ibytes);
+        if (mixed_sel) {
+            std::memcpy(hb + m_it, m_items.data(), m_items.size() * 16);
+            std::memcpy(hb + m_ct, m_cta.data(), m_cta.size() * 4);
+            std::memcpy(hb + m_pi, m_pinfo.data(), m_pinfo.size() * 8);
+            std::memcpy(hb + m_si, m_slot.data(), m_slot.size() * 8);
+        }
+        if (!cap)  // a captured step's descriptors go up with its chunk (run_graph)
+            ck(cudaMemcpyAsync(db, hb, boff, cudaMemcpyHostToDevice, ctx->stream), "descriptor upload");
+    }
+    bool staged_b = false;
+    auto stage_b = [&]() {  // part B: the attention work list (+ union tables)
+    if (!live || staged_b) return;
+    staged_b = true;
     std::memcpy(hb + boff, cbase.data(), (nq + 1) * 4);
     {
         // chunk entries (problem | chunk index << 20). Problems on one prefill
@@ -909,16 +933,21 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         std::memcpy(hb + u_m, umem.data(), nmem * 4);
         std::memcpy(hb + u_mg, umgrp.data(), nmem * 4);
     }
-    if (mixed_sel) {
-        std::memcpy(hb + m_it, m_items.data(), m_items.size() * 16);
-        std::memcpy(hb + m_ct, m_cta.data(), m_cta.size() * 4);
-        std::memcpy(hb + m_pi, m_pinfo.data(), m_pinfo.size() * 8);
-        std::memcpy(hb + m_si, m_slot.data(), m_slot.size() * 8);
+    if (!cap) {
+        // on a side stream, joined to the step's stream by an event before
+        // attend: the copy overlaps the select kernel instead of sitting
+        // between the two. (The slot's earlier use finished: the host waited
+        // on slot->done before reusing it.)
+        if (!ctx->side) {
+            ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
+            ck(cudaEventCreateWithFlags(&ctx->side_ev, cudaEventDisableTiming), "event");
+        }
+        ck(cudaMemcpyAsync(db + boff, hb + boff, need - boff, cudaMemcpyHostToDevice, ctx->side),
+           "work list upload");
+        ck(cudaEventRecord(ctx->side_ev, ctx->side), "event");
+        ck(cudaStreamWaitEvent(ctx->stream, ctx->side_ev, 0), "work list wait");
     }
-    if (!cap)  // a captured step's descriptors go up with its chunk (run_graph)
-        ck(cudaMemcpyAsync(db, hb, need, cudaMemcpyHostToDevice, ctx->stream),
-           "descriptor upload");
-    }
+    };
     const csa::DecodeProblem* dprobs = reinterpret_cast<const csa::DecodeProblem*>(db);
     const csa::InsertProblem* diprobs = reinterpret_cast<const csa::InsertProblem*>(db + ioff);
     const uint32_t* dcbase = reinterpret_cast<const uint32_t*>(db + boff);
@@ -1038,6 +1067,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                           0.0, 1, nullptr, ctx->stream),
        "select retry launch");
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
+    stage_b();  // built while route / select run
     if (nchunks && live)
         ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
                               ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream,
@@ -1045,6 +1075,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
            "attend launch");
     }
     if (ngroups) {
+        stage_b();
         auto u32 = [&](size_t off) { return reinterpret_cast<const uint32_t*>(db + off); };
         if (ctx->union_prof) {
             ctx->un_prof.ensure(static_cast<size_t>(ctx->num_sms) * 160 * 8);

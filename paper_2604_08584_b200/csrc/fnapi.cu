@@ -111,6 +111,52 @@ __global__ void buf_min_u64_kernel(unsigned long long* __restrict__ dst, const u
         dst[i] = src[i] < dst[i] ? src[i] : dst[i];
 }
 
+// Up to 4 (src, dst, bytes) copies in one launch: the decode step's inputs
+// read straight from pinned host memory over the host link (one launch
+// instead of one DMA call per buffer; the host-side cost of a copy call is
+// larger than the transfer of these few hundred KB). 16-byte granules when
+// every pointer and size allows, else 4-byte.
+struct CopySegs {
+    const void* src[4];
+    void* dst[4];
+    uint64_t bytes[4];
+    uint32_t n, wide;
+};
+__global__ void copy_segs_kernel(const CopySegs c) {
+    for (uint32_t k = 0; k < c.n; ++k) {
+        if (c.wide) {
+            const uint4* s = static_cast<const uint4*>(c.src[k]);
+            uint4* d = static_cast<uint4*>(c.dst[k]);
+            const uint64_t m = c.bytes[k] / 16;
+            for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) d[i] = s[i];
+        } else {
+            const uint32_t* s = static_cast<const uint32_t*>(c.src[k]);
+            uint32_t* d = static_cast<uint32_t*>(c.dst[k]);
+            const uint64_t m = c.bytes[k] / 4;
+            for (uint64_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) d[i] = s[i];
+        }
+    }
+}
+
+cudaError_t launch_copy_segs(const void* const* src, void* const* dst, const uint64_t* bytes, uint32_t n,
+                             cudaStream_t st) {
+    CopySegs c{};
+    c.n = n < 4 ? n : 4;
+    c.wide = 1;
+    uint64_t mx = 0;
+    for (uint32_t k = 0; k < c.n; ++k) {
+        c.src[k] = src[k];
+        c.dst[k] = dst[k];
+        c.bytes[k] = bytes[k];
+        if ((reinterpret_cast<uintptr_t>(src[k]) | reinterpret_cast<uintptr_t>(dst[k]) | bytes[k]) & 15u) c.wide = 0;
+        mx = bytes[k] > mx ? bytes[k] : mx;
+    }
+    const uint64_t items = mx / (c.wide ? 16 : 4);
+    const uint64_t blocks = (items + 255) / 256;
+    copy_segs_kernel<<<static_cast<unsigned>(blocks < 296 ? (blocks ? blocks : 1) : 296), 256, 0, st>>>(c);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_buf_add_u32(uint32_t* dst, const uint32_t* src, uint64_t n, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const uint64_t b = (n + 255) / 256;

@@ -172,6 +172,9 @@ cudaError_t launch_reduce_lists(uint32_t nl, const uint64_t* off, const uint32_t
 size_t toplist_scratch_bytes(uint32_t n);
 // shard collectives' local combine steps (csattn_buffer_add_u32 / _min_u64)
 cudaError_t launch_buf_add_u32(uint32_t* dst, const uint32_t* src, uint64_t n, cudaStream_t st);
+// up to 4 copies in one kernel (device-accessible sources, e.g. pinned host memory)
+cudaError_t launch_copy_segs(const void* const* src, void* const* dst, const uint64_t* bytes, uint32_t n,
+                             cudaStream_t st);
 cudaError_t launch_buf_min_u64(unsigned long long* dst, const unsigned long long* src, uint64_t n, cudaStream_t st);
 cudaError_t launch_toplist(const float* scores, uint32_t n, unsigned long long* sorted, void* scratch,
                            size_t scratch_bytes, cudaStream_t st);
