@@ -937,6 +937,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                     wr = wrn;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) e[u] = en[u];
+                    // a key of this list and of the next may sit in different
+                    // lanes: order the RMWs (memory model, not just issue order)
+                    __syncwarp();
                 }
             }
         } else {  // cached candidate scores (search_period > 1): this warp's keys

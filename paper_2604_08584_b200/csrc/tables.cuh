@@ -154,6 +154,7 @@ __device__ unsigned long long cta_kth_largest_mm(RefillSmem& S, uint32_t* hist, 
             }
             const uint32_t rem = S.b_rem, ex = inc - sum;
             const uint32_t hit = __ballot_sync(0xffffffffu, ex < rem && inc >= rem);
+            __syncwarp();  // every lane's reads of the state before the hit lane writes it
             if (lane == static_cast<uint32_t>(__ffs(hit) - 1)) {
                 uint32_t c = ex;
                 int dsel;
