@@ -169,9 +169,14 @@ struct csattn_ctx_s {
     // side stream for the attention work-list upload (runs beside select)
     cudaStream_t side = nullptr;
     cudaEvent_t side_ev = nullptr;
+    // append + insert beside the attention (CSATTN_INSERT_OVERLAP=0: after it)
+    cudaEvent_t ins_fork = nullptr, ins_join = nullptr;
+    bool insert_overlap = !(std::getenv("CSATTN_INSERT_OVERLAP") && std::atoi(std::getenv("CSATTN_INSERT_OVERLAP")) == 0);
     ~csattn_ctx_s() {
         if (side) cudaStreamDestroy(side);
         if (side_ev) cudaEventDestroy(side_ev);
+        if (ins_fork) cudaEventDestroy(ins_fork);
+        if (ins_join) cudaEventDestroy(ins_join);
         for (Slot& s : ring) {
             if (s.host) cudaFreeHost(s.host);
             if (s.done) cudaEventDestroy(s.done);
@@ -938,10 +943,6 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         // attend: the copy overlaps the select kernel instead of sitting
         // between the two. (The slot's earlier use finished: the host waited
         // on slot->done before reusing it.)
-        if (!ctx->side) {
-            ck(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "side stream");
-            ck(cudaEventCreateWithFlags(&ctx->side_ev, cudaEventDisableTiming), "event");
-        }
         ck(cudaMemcpyAsync(db + boff, hb + boff, need - boff, cudaMemcpyHostToDevice, ctx->side),
            "work list upload");
         ck(cudaEventRecord(ctx->side_ev, ctx->side), "event");
@@ -958,6 +959,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         for (auto& e : ev) e = ctx->take_event();
         ck(cudaEventRecord(ev[0], ctx->stream), "event");
     }
+    bool ins_forked = false;  // insert launched on the side stream (joined below)
     if (fused) {
         if (live)
             ck(csa::launch_fused_step(dprobs, static_cast<uint32_t>(nq), fz_cl, fz_nr, ctx->stream),
@@ -1066,8 +1068,18 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                           static_cast<uint32_t>(ctx->log_cap), rcount + 1, rcount, nullptr, nullptr,
                           0.0, 1, nullptr, ctx->stream),
        "select retry launch");
+    stage_b();  // built while route / select run (its upload goes first on the side stream)
+    // The append + streaming insert touches the tables and the appended KV
+    // row only: it runs beside the attention of this step (which reads rows
+    // [0, N) and the selection) once the search has read the tables.
+    if (live && ctx->insert_overlap) {
+        ck(cudaEventRecord(ctx->ins_fork, ctx->stream), "event");
+        ck(cudaStreamWaitEvent(ctx->side, ctx->ins_fork, 0), "insert fork");
+        ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->side), "insert launch");
+        ck(cudaEventRecord(ctx->ins_join, ctx->side), "event");
+        ins_forked = true;
+    }
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
-    stage_b();  // built while route / select run
     if (nchunks && live)
         ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
                               ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream,
@@ -1123,7 +1135,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
     }
     if (ctx->profile) ck(cudaEventRecord(ev[2], ctx->stream), "event");
-    if (live) ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
+    if (ins_forked)
+        ck(cudaStreamWaitEvent(ctx->stream, ctx->ins_join, 0), "insert join");
+    else if (live)
+        ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
     if (slot) {
         ck(cudaEventRecord(slot->done, ctx->stream), "event");
         slot->used = true;
@@ -1471,6 +1486,11 @@ csattn_status csattn_ctx_create(int device, void* stream, csattn_ctx* out) {
             ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
             c->own = true;
         }
+        // the side stream + its events exist before any graph capture
+        ck(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+        ck(cudaEventCreateWithFlags(&c->side_ev, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->ins_fork, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->ins_join, cudaEventDisableTiming), "event");
         *out = c.release();
     });
 }
