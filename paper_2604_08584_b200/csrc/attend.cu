@@ -230,14 +230,17 @@ __device__ __forceinline__ float4 ld_row4(const float* p) {
 
 // GR=4 at 64 registers: 8 CTAs/SM (one 4-byte spill) beat 72 registers / 7 CTAs
 // on this memory-latency-bound loop (c3 277 -> 262 us)
-// PIPE (GR = 4): the next group's K/V rows are loaded while the current one
-// is reduced (register double buffer): the loads stay in flight through the
-// shuffles, exp and PV instead of only between groups.
-template <bool PARTIAL, int GR, bool PIPE = false>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
-__global__ void __launch_bounds__(ATT_THREADS, PIPE ? 5 : (GR == 4 ? 8 : 5))
+// WARP (GQA sessions of ATT_WARPS query heads): a CTA is (session, chunk j)
+// and warp h attends head h's rows [j*rows/4, (j+1)*rows/4): the four heads
+// of a KV head read largely the same rows at about the same time on one SM,
+// so the rows they share are served from L1. Each warp writes its own
+// (problem, chunk) partial; the last warp of a problem merges them.
+template <bool PARTIAL, int GR, bool WARP = false>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
+__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 8 : 5)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
                  uint32_t* __restrict__ counters, uint32_t rows) {
+    static_assert(!(WARP && PARTIAL), "WARP: unsharded steps only");
     constexpr int NC = 1, VEC = 4;
     __shared__ float wm[ATT_WARPS], ws[ATT_WARPS];
     __shared__ float wacc[ATT_WARPS][NC * 32 * VEC];
@@ -245,14 +248,15 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     const uint32_t c = blockIdx.x;
     // chunk entry: problem | chunk index << 20 (chunks may come in any order)
     const uint32_t cpk = chunk_prob[c];
-    const uint32_t p = cpk & 0xfffffu;
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    const uint32_t p = (cpk & 0xfffffu) + (WARP ? static_cast<uint32_t>(w) : 0u);
     const DecodeProblem& P = probs[p];
     const SessionDev& sd = *P.s;
     const uint32_t d = 128, K = P.K, P0 = sd.P;
     const uint32_t j = cpk >> 20;
     const uint32_t nch = chunk_base[p + 1] - chunk_base[p];
-    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    const uint32_t rw = j * rows + w * (rows / ATT_WARPS);  // this warp's first row
+    if (WARP && j >= nch) return;  // (heads of a session share K: never taken)
+    const uint32_t rw = WARP ? j * (rows / ATT_WARPS) : j * rows + w * (rows / ATT_WARPS);  // this warp's first row
     const uint32_t nrw = rw < K ? min(rows / ATT_WARPS, K - rw) : 0u;
     const bool want_w = (P.mode & MODE_WEIGHTS) && P.weights;
     const float* const kpre = sd.kpre;
@@ -277,92 +281,6 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
 
     float m = -FLT_MAX, s = 0.0f;
     float acc[NC][VEC] = {{0.0f, 0.0f, 0.0f, 0.0f}};
-    if constexpr (PIPE) {
-        static_assert(GR == 4, "PIPE: 4-row groups");
-        // this warp's row offsets (element offset | tail bit); rows past nrw
-        // repeat the warp's first row (finite data, zero probability)
-        __shared__ uint32_t offs[ATT_WARPS][ATT_ROWS_BIG / ATT_WARPS];
-        const uint32_t wrows = rows / ATT_WARPS;
-        uint32_t o0 = 0;
-        if (nrw) {
-            const uint32_t i = __ldg(P.sel + rw);
-            o0 = i < P0 ? i * d : ((i - P0) * d) | 0x80000000u;
-        }
-        for (uint32_t x = ln; x < wrows; x += 32) {
-            uint32_t o = o0;
-            if (x < nrw) {
-                const uint32_t i = __ldg(P.sel + rw + x);
-                o = i < P0 ? i * d : ((i - P0) * d) | 0x80000000u;
-            }
-            offs[w][x] = o;
-        }
-        __syncwarp();
-        const uint32_t ng = (nrw + GR - 1) / GR;
-        auto load = [&](uint32_t g, float4 (&kk)[GR], float4 (&vv)[GR]) {
-#pragma unroll
-            for (int u = 0; u < GR; ++u) {
-                const uint32_t o = offs[w][g * GR + u];
-                const uint32_t e = (o & 0x7fffffffu) + 4 * ln;
-                const bool tl = o & 0x80000000u;
-                kk[u] = ld_row4((tl ? ktail : kpre) + e);
-                vv[u] = ld_row4((tl ? vtail : vpre) + e);
-            }
-        };
-        auto compute = [&](uint32_t g, const float4 (&kk)[GR], const float4 (&vv)[GR]) {
-            float pd[GR];
-#pragma unroll
-            for (int u = 0; u < GR; ++u)
-                pd[u] = fmaf(q4.w, kk[u].w, fmaf(q4.z, kk[u].z, fmaf(q4.y, kk[u].y, q4.x * kk[u].x)));
-            float h2[2];
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const float send = up16 ? pd[t] : pd[t + 2];
-                const float keep = up16 ? pd[t + 2] : pd[t];
-                h2[t] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-            }
-            const float send = up8 ? h2[0] : h2[1];
-            const float keep = up8 ? h2[1] : h2[0];
-            float lg = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-            lg += __shfl_xor_sync(0xffffffffu, lg, 4);
-            lg += __shfl_xor_sync(0xffffffffu, lg, 2);
-            lg += __shfl_xor_sync(0xffffffffu, lg, 1);
-            const bool valid = g * GR + myrow < nrw;
-            float gm = valid ? lg : -FLT_MAX;
-            gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 8));
-            gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, 16));
-            if (__builtin_expect(gm > m, 0)) {
-                const float f = ex2f(m - gm);
-                s *= f;
-#pragma unroll
-                for (int v = 0; v < VEC; ++v) acc[0][v] *= f;
-                m = gm;
-            }
-            const float pr = valid ? ex2f(lg - m) : 0.0f;
-            float ps = pr;
-            ps += __shfl_xor_sync(0xffffffffu, ps, 8);
-            ps += __shfl_xor_sync(0xffffffffu, ps, 16);
-            s += ps;
-#pragma unroll
-            for (int u = 0; u < GR; ++u) {
-                const float pu = __shfl_sync(0xffffffffu, pr, ((u >> 1) & 1) * 16 + (u & 1) * 8);
-                acc[0][0] = fmaf(pu, vv[u].x, acc[0][0]);
-                acc[0][1] = fmaf(pu, vv[u].y, acc[0][1]);
-                acc[0][2] = fmaf(pu, vv[u].z, acc[0][2]);
-                acc[0][3] = fmaf(pu, vv[u].w, acc[0][3]);
-            }
-            if (want_w && valid && (ln & 7) == 0) P.weights[rw + g * GR + myrow] = lg * LN2;
-        };
-        float4 ka[GR], va[GR], kb[GR], vb[GR];
-        if (ng) load(0, ka, va);
-        for (uint32_t g = 0; g < ng; g += 2) {
-            if (g + 1 < ng) load(g + 1, kb, vb);
-            compute(g, ka, va);
-            if (g + 1 < ng) {
-                if (g + 2 < ng) load(g + 2, ka, va);
-                compute(g + 1, kb, vb);
-            }
-        }
-    } else {
     for (uint32_t b0 = 0; b0 < nrw; b0 += 32) {  // 32-row index batches
     const uint32_t r0 = rw + b0;
     const uint32_t nr = min(32u, nrw - b0);
@@ -478,7 +396,44 @@ attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __rest
     else
         groups(std::false_type{}, std::false_type{});
     }
-    }  // !PIPE
+    if constexpr (WARP) {
+        // ---- warp partial of (problem, chunk j); the last warp merges ----
+        float* pw = part + static_cast<size_t>(chunk_base[p] + j) * (d + 2);
+        if (ln == 0) {
+            pw[0] = nrw ? m * LN2 : -FLT_MAX;
+            pw[1] = nrw ? s : 0.0f;
+        }
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) pw[2 + ln * VEC + v] = acc[0][v];
+        __threadfence();
+        __syncwarp();
+        uint32_t lastw = 0;
+        if (ln == 0) lastw = atomicAdd(counters + p, 1u) == nch - 1 ? 1u : 0u;
+        if (!__shfl_sync(0xffffffffu, lastw, 0)) return;
+        __threadfence();
+        const float* pb = part + static_cast<size_t>(chunk_base[p]) * (d + 2);
+        float GM = -FLT_MAX;
+        for (uint32_t k = ln; k < nch; k += 32) GM = fmaxf(GM, __ldcg(pb + k * (d + 2)));
+        for (int o = 16; o; o >>= 1) GM = fmaxf(GM, __shfl_xor_sync(0xffffffffu, GM, o));
+        float GS = 0.0f, o4[VEC] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (uint32_t k = 0; k < nch; ++k) {  // chunk order
+            const float sk = __ldcg(pb + k * (d + 2) + 1);
+            if (sk > 0.0f) {
+                const float f = expf(__ldcg(pb + k * (d + 2)) - GM);
+                GS += sk * f;
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) o4[v] += __ldcg(pb + k * (d + 2) + 2 + ln * VEC + v) * f;
+            }
+        }
+        const float inv = 1.0f / GS;
+        if (P.out)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) P.out[ln * VEC + v] = o4[v] * inv;
+        if (want_w)
+            for (uint32_t r = ln; r < K; r += 32) P.weights[r] = expf(__ldcg(P.weights + r) - GM) * inv;
+        if (ln == 0) counters[p] = 0;  // ready for the next step
+        return;
+    }
     // ---- CTA partial ----
     if (ln == 0) {
         wm[w] = nrw ? m : -FLT_MAX;
@@ -581,24 +536,22 @@ cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t npr
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial,
-                          uint32_t rows) {
+                          uint32_t rows, bool warp_heads) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows)
     // GR=4 (64 regs, 8 CTAs/SM) for large launches; GR=8 (more rows in flight
     // per warp) for small ones: c2 (224 x 256 rows, run as 448 x 128) 29 -> 19 us,
     // while c4's 832 x 256 per layer is faster with GR=4. CSATTN_ATT_GR=4|8 forces.
     const int gr_env = std::getenv("CSATTN_ATT_GR") ? std::atoi(std::getenv("CSATTN_ATT_GR")) : 0;
-    if (d == 128 && gr_env == 44) {  // experiment: pipelined 4-row groups
-        if (partial) attend128_kernel<true, 4, true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
-        else attend128_kernel<false, 4, true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
-        return cudaGetLastError();
-    }
     // (launch size in 256-row units, whatever the chunk size)
     // and 512-row chunks (c3, chunk-major order: 250 -> 245 us with GR=8)
     const int gr = gr_env == 4 || gr_env == 8
                        ? gr_env
                        : ((rows >= 512u || static_cast<uint64_t>(nchunks) * rows < 148ull * 3 * 256) ? 8 : 4);
-    if (d == 128 && partial) {
+    if (d == 128 && warp_heads && !partial) {
+        if (gr == 4) attend128_kernel<false, 4, true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
+        else attend128_kernel<false, 8, true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
+    } else if (d == 128 && partial) {
         if (gr == 4) attend128_kernel<true, 4><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
         else attend128_kernel<true, 8><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
     } else if (d == 128) {

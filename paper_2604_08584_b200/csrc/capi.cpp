@@ -198,6 +198,9 @@ struct csattn_ctx_s {
     DevMem mlog_idx, mlog_sc, mumeta, pdone;
     uint64_t pdone_n = 0;
     bool tail_split = !(std::getenv("CSATTN_TAIL_SPLIT") && std::atoi(std::getenv("CSATTN_TAIL_SPLIT")) == 0);
+    // GQA warp-per-head attention, opt-in (CSATTN_ATT_GQA=1): measured slower
+    // at c3 (attend 252 -> 275 us: 4x the partials, little L1 reuse)
+    bool att_gqa = std::getenv("CSATTN_ATT_GQA") && std::atoi(std::getenv("CSATTN_ATT_GQA")) == 1;
     // sharded steps (csattn_shard_step): descriptors + scratch kept across phases
     DevMem sh_desc, sh_pstate, sh_bitmap, sh_kdev, sh_ulog_idx, sh_ulog_sc, sh_umeta, sh_chunks;
     std::vector<csa::DecodeProblem> sh_hprobs;
@@ -775,12 +778,24 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         const int v = std::atoi(ar);
         arows = v == 512 ? csa::ATT_ROWS_BIG : (v == 128 ? csa::ATT_ROWS_SMALL : csa::ATT_ROWS);
     }
-    uint64_t nchunks = 0;
+    // GQA sessions of 4 query heads (d = 128, no union groups): one CTA per
+    // (session, chunk), warp h = head h over arows / 4 rows (attend.cu WARP:
+    // the heads' shared rows come from L1); cbase then counts per-warp
+    // partials, and the CTA entries are one per (session, chunk)
+    bool att_warp = ctx->att_gqa && d == 128 && ngroups == 0 && arows >= 128;
+    for (uint64_t i = 0; i < ns && att_warp; ++i) att_warp = ss[i]->group == 4;
+    const uint32_t prow = att_warp ? arows / 4 : arows;  // rows per partial
+    uint64_t nchunks = 0;  // partials
     for (uint64_t i = 0; i < nq; ++i) {
         cbase[i] = static_cast<uint32_t>(nchunks);
-        if (!in_union[i]) nchunks += (Ks[i] + arows - 1) / arows;
+        if (!in_union[i]) nchunks += (Ks[i] + prow - 1) / prow;
     }
     cbase[nq] = static_cast<uint32_t>(nchunks);
+    uint64_t ncta = nchunks;  // attention CTAs
+    if (att_warp) {
+        ncta = 0;
+        for (uint64_t i = 0; i < nq; i += 4) ncta = ncta + cbase[i + 1] - cbase[i];
+    }
     if (nq > ctx->counters_n) {
         ctx->counters.alloc(nq * 4);
         ck(cudaMemsetAsync(ctx->counters.p, 0, nq * 4, ctx->stream), "memset");
@@ -862,7 +877,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     const size_t m_si = m_pi + al(m_pinfo.size() * 8);
     const size_t boff = m_si + al(m_slot.size() * 8);  // part B
     const size_t poff = boff + al((nq + 1) * 4);
-    const size_t uoff = poff + al(nchunks * 4);  // union tables: gP | gmember | members | mgroup
+    const size_t uoff = poff + al(ncta * 4);  // union tables: gP | gmember | members | mgroup
     const size_t u_gm = uoff + al(ngroups * 4), u_m = u_gm + al(ugmem.size() * 4);
     const size_t u_mg = u_m + al(nmem * 4);
     const size_t need = u_mg + nmem * 4;
@@ -914,8 +929,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             return o && std::strcmp(o, "problem") == 0;
         }();
         uint64_t at = 0;
+        const uint64_t step = att_warp ? 4 : 1;  // entries per session (WARP) or per problem
         if (pmajor) {
-            for (uint64_t i = 0; i < nq; ++i)
+            for (uint64_t i = 0; i < nq; i += step)
                 for (uint32_t j = 0; j < cbase[i + 1] - cbase[i]; ++j)
                     cp[at++] = static_cast<uint32_t>(i) | (j << 20);
         } else {
@@ -924,9 +940,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                 uint64_t g1 = g0 + 1;
                 while (g1 < nq && pre_of[g1] == pre_of[g0]) ++g1;
                 uint32_t mx = 0;
-                for (uint64_t i = g0; i < g1; ++i) mx = std::max(mx, cbase[i + 1] - cbase[i]);
+                for (uint64_t i = g0; i < g1; i += step) mx = std::max(mx, cbase[i + 1] - cbase[i]);
                 for (uint32_t j = 0; j < mx; ++j)
-                    for (uint64_t i = g0; i < g1; ++i)
+                    for (uint64_t i = g0; i < g1; i += step)
                         if (j < cbase[i + 1] - cbase[i]) cp[at++] = static_cast<uint32_t>(i) | (j << 20);
                 g0 = g1;
             }
@@ -1081,9 +1097,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     }
     if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     if (nchunks && live)
-        ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(nchunks),
+        ck(csa::launch_attend(dprobs, dcprob, dcbase, static_cast<uint32_t>(ncta),
                               ctx->part.as<float>(), ctx->counters.as<uint32_t>(), d, ctx->stream,
-                              false, arows),
+                              false, arows, att_warp),
            "attend launch");
     }
     if (ngroups) {

@@ -101,7 +101,7 @@ inline uint32_t attend_rows(uint64_t n256) {
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
                           uint32_t* counters, uint32_t d, cudaStream_t st, bool partial = false,
-                          uint32_t rows = ATT_ROWS);
+                          uint32_t rows = ATT_ROWS, bool warp_heads = false);
 
 // attend_union.cu: problems sharing a prefill (groups of <= UN_GROUP
 // members), by prefill row range: each union row is read once per group

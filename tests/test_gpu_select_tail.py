@@ -23,21 +23,24 @@ def _need_ref():
         pytest.skip("oracle/_ref not built")
 
 
-@pytest.mark.parametrize("P,F,sms,spec,tail", [
-    (20000, 11, 8, None, None),   # 44 problems, grid 16: 2 rounds + 12 split problems (5 tiles each)
-    (9000, 9, 4, None, None),     # 36 problems, grid 8: 4 rounds + 4 split problems
-    (20000, 11, 8, "2.0", None),  # every speculative cut fails: retry pass
-    (20000, 11, 8, None, "0"),    # tail split off: plain rounds
+@pytest.mark.parametrize("P,F,sms,spec,tail,gqa", [
+    (20000, 11, 8, None, None, None),  # 44 problems, grid 16: 2 rounds + 12 split problems (5 tiles each)
+    (9000, 9, 4, None, None, None),    # 36 problems, grid 8: 4 rounds + 4 split problems
+    (20000, 11, 8, "2.0", None, None), # every speculative cut fails: retry pass
+    (20000, 11, 8, None, "0", None),   # tail split off: plain rounds
+    (20000, 11, 8, None, None, "1"),   # + the opt-in warp-per-head (GQA) attention
 ])
-def test_tail_split_batch_equals_reference(monkeypatch, P, F, sms, spec, tail):
+def test_tail_split_batch_equals_reference(monkeypatch, P, F, sms, spec, tail, gqa):
     monkeypatch.setenv("CSATTN_SELECT_SMS", str(sms))
     monkeypatch.setenv("CSATTN_FUSED", "0")
+    if gqa:
+        monkeypatch.setenv("CSATTN_ATT_GQA", gqa)
     if spec:
         monkeypatch.setenv("CSATTN_SPEC_KEEP", spec)
     if tail:
         monkeypatch.setenv("CSATTN_TAIL_SPLIT", tail)
     ctx = cs.Context(0)
-    T, d = 4, 64
+    T, d = 4, (128 if gqa else 64)  # the warp-per-head attention is the d = 128 kernel
     q, k, v = workload(P, 32, d, seed=P + F)
     widths = cs.uniform_widths(d, 4)
     ic = cs.IndexConfig(alpha=0.2, centroids=16, seed=1, score_bits=32)
