@@ -71,6 +71,8 @@ CONFIGS = {
                           "LSE / victim collectives"),
 }
 N_KV, GROUP, D, M, C_CENT = 8, 4, 128, 8, 64
+ALPHA = 0.2  # --preset ultra: C = 128, alpha = 0.1 (the paper's ultra-long preset)
+PRESET = "default"
 DWELLS = (32, 16, 64, 8)
 METRIC = "decode-step sparse-attn latency (us) & HBM GB/s vs roofline, 128K ctx, 95% sparsity"
 
@@ -239,7 +241,7 @@ class _RefIndexCfg:
 
     def c(self):
         from oracle import _cstructs as cst
-        return cst.IndexConfigC(0.2, 0, 0, 32, C_CENT, 10, 0, self.seed, 1e-7)
+        return cst.IndexConfigC(ALPHA, 0, 0, 32, C_CENT, 10, 0, self.seed, 1e-7)
 
 
 class _RefRetrievalCfg:
@@ -428,7 +430,7 @@ def run_c5(args, config, P, rank, world, local):
         hb = heads[g0:g0 + 4]
         rows_b = [(np.ascontiguousarray(np.concatenate([data[g][0][:P, r] for r in range(GROUP)])),
                    data[g][1][:P], data[g][2][:P]) for g in hb]
-        ics = [cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
+        ics = [cs.IndexConfig(alpha=ALPHA, centroids=C_CENT, seed=mix_seed(1, g), score_bits=32)
                for g in hb]
         full += cs.prefill_batch(ctxs[0], rows_b, widths, ics, rc, group=GROUP, max_decode_steps=1)
         del rows_b
@@ -537,9 +539,14 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--preset", default="default", choices=["default", "ultra"],
+                    help="ultra: the paper's ultra-long preset, C = 128 centroids, alpha = 0.1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.preset == "ultra":
+        global C_CENT, ALPHA, PRESET
+        C_CENT, ALPHA, PRESET = 128, 0.1, "ultra-long (C=128, alpha=0.1)"
 
     if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         launch_ranks(args.gpus)  # exits with the ranks' status
@@ -552,7 +559,7 @@ def main():
     config = {"workload": f"{args.config}: {desc}", "prefill": P, "sequences": n_seq,
               "layers": n_layers,
               "kv_heads": N_KV, "q_heads": N_KV * GROUP, "d": D, "m": M, "C": C_CENT,
-              "alpha": 0.2, "rho": 0.05, "window": 32, "tau": 1}
+              "alpha": ALPHA, "rho": 0.05, "window": 32, "tau": 1, "preset": PRESET}
 
     if args.impl == "reference":
         res = run_reference(args, P, n_seq, n_layers, rank)
@@ -618,7 +625,7 @@ def main():
         t0 = time.perf_counter()
         rows_b = [(np.ascontiguousarray(np.concatenate([data[g][0][:P, r] for r in range(GROUP)])),
                    data[g][1][:P], data[g][2][:P]) for g in my_heads]
-        ics = [cs.IndexConfig(alpha=0.2, centroids=C_CENT, seed=mix_seed(1 + 100 * layer, g),
+        ics = [cs.IndexConfig(alpha=ALPHA, centroids=C_CENT, seed=mix_seed(1 + 100 * layer, g),
                               score_bits=32) for g in my_heads]
         base = dict(zip(my_heads, cs.prefill_batch(ctx, rows_b, widths, ics, rc, group=GROUP,
                                                    max_decode_steps=T)))
