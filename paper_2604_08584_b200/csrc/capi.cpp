@@ -1088,7 +1088,9 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     // The append + streaming insert touches the tables and the appended KV
     // row only: it runs beside the attention of this step (which reads rows
     // [0, N) and the selection) once the search has read the tables.
-    if (live && ctx->insert_overlap) {
+    // (not inside a captured graph: a forked insert branch measured slower
+    // there, 761 -> 885 us per c3 step)
+    if (live && !cap && ctx->insert_overlap) {
         ck(cudaEventRecord(ctx->ins_fork, ctx->stream), "event");
         ck(cudaStreamWaitEvent(ctx->side, ctx->ins_fork, 0), "insert fork");
         ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->side), "insert launch");
