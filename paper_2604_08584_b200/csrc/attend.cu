@@ -223,20 +223,21 @@ attend_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restric
 // partial dots reduced across the warp by a transposed butterfly (9 shuffles
 // for 8 rows: after it, lane l holds the logit of row ((l>>4)&1)*4 +
 // ((l>>3)&1)*2 + ((l>>2)&1)), so exp / max / sum run lane-parallel.
-// GR rows per group: 8 (96 regs, 5 CTAs/SM) or 4 (<= 64 regs, 8 CTAs/SM)
+// GR rows per group: 8 (72 regs, 7 CTAs/SM) or 4 (<= 64 regs, 8 CTAs/SM)
 __device__ __forceinline__ float4 ld_row4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
 
-// GR=4 at 64 registers: 8 CTAs/SM (one 4-byte spill) beat 72 registers / 7 CTAs
-// on this memory-latency-bound loop (c3 277 -> 262 us)
+// GR=8 capped at 72 registers (7 CTAs/SM, an 8-byte spill): more warps in
+// flight beat the 90-register / 5-CTA build on this memory-latency-bound
+// loop (c3 250 -> 221 us; 6 CTAs: 231, 8 CTAs at 64 registers: 235)
 // WARP (GQA sessions of ATT_WARPS query heads): a CTA is (session, chunk j)
 // and warp h attends head h's rows [j*rows/4, (j+1)*rows/4): the four heads
 // of a KV head read largely the same rows at about the same time on one SM,
 // so the rows they share are served from L1. Each warp writes its own
 // (problem, chunk) partial; the last warp of a problem merges them.
 template <bool PARTIAL, int GR, bool WARP = false>  // PARTIAL: sharded steps write (max, sum, acc[d]) unnormalised
-__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 8 : 5)
+__global__ void __launch_bounds__(ATT_THREADS, GR == 4 ? 8 : 7)
 attend128_kernel(const DecodeProblem* __restrict__ probs, const uint32_t* __restrict__ chunk_prob,
                  const uint32_t* __restrict__ chunk_base, float* __restrict__ part,
                  uint32_t* __restrict__ counters, uint32_t rows) {
@@ -539,15 +540,11 @@ cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob
                           uint32_t rows, bool warp_heads) {
 #define CSA_ATT(NC, VEC) \
     attend_kernel<NC, VEC><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows)
-    // GR=4 (64 regs, 8 CTAs/SM) for large launches; GR=8 (more rows in flight
-    // per warp) for small ones: c2 (224 x 256 rows, run as 448 x 128) 29 -> 19 us,
-    // while c4's 832 x 256 per layer is faster with GR=4. CSATTN_ATT_GR=4|8 forces.
+    // GR=8 at 72 registers (7 CTAs/SM): c3 attend 250 -> 221 us, c4 1692 ->
+    // 1550 us per model step against GR=4 at 64 registers (8 CTAs/SM);
+    // CSATTN_ATT_GR=4 forces the 4-row groups
     const int gr_env = std::getenv("CSATTN_ATT_GR") ? std::atoi(std::getenv("CSATTN_ATT_GR")) : 0;
-    // (launch size in 256-row units, whatever the chunk size)
-    // and 512-row chunks (c3, chunk-major order: 250 -> 245 us with GR=8)
-    const int gr = gr_env == 4 || gr_env == 8
-                       ? gr_env
-                       : ((rows >= 512u || static_cast<uint64_t>(nchunks) * rows < 148ull * 3 * 256) ? 8 : 4);
+    const int gr = gr_env == 4 ? 4 : 8;
     if (d == 128 && warp_heads && !partial) {
         if (gr == 4) attend128_kernel<false, 4, true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
         else attend128_kernel<false, 8, true><<<nchunks, ATT_THREADS, 0, st>>>(probs, chunk_prob, chunk_base, part, counters, rows);
