@@ -198,6 +198,9 @@ struct csattn_ctx_s {
     DevMem mlog_idx, mlog_sc, mumeta, pdone;
     uint64_t pdone_n = 0;
     bool tail_split = !(std::getenv("CSATTN_TAIL_SPLIT") && std::atoi(std::getenv("CSATTN_TAIL_SPLIT")) == 0);
+    // small batches through the mixed pieces too (CSATTN_SMALL_MIXED=0: part
+    // units + select_merge_kernel)
+    bool small_mixed = !(std::getenv("CSATTN_SMALL_MIXED") && std::atoi(std::getenv("CSATTN_SMALL_MIXED")) == 0);
     // GQA warp-per-head attention, opt-in (CSATTN_ATT_GQA=1): measured slower
     // at c3 (attend 252 -> 275 us: 4x the partials, little L1 reuse)
     bool att_gqa = std::getenv("CSATTN_ATT_GQA") && std::atoi(std::getenv("CSATTN_ATT_GQA")) == 1;
@@ -809,10 +812,19 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     std::vector<uint32_t> m_cta;
     std::vector<uint2> m_pinfo, m_slot;
     uint64_t m_log = 0;
+    uint64_t m_grid = 0;
     {
-        const uint64_t G = csa::select_grid(static_cast<uint32_t>(nq), ctx->sel_sms ? ctx->sel_sms : ctx->num_sms);
+        // small batches (fewer problems than CTA slots): every problem is
+        // cut into pieces over all slots, finalised in-kernel by its last
+        // piece (instead of part units + select_merge_kernel)
+        const int sms = ctx->sel_sms ? ctx->sel_sms : ctx->num_sms;
+        const uint64_t slots = static_cast<uint64_t>(csa::select_ctas_per_sm()) * sms;
+        const bool small = nq < slots;
+        const uint64_t G = small ? slots : csa::select_grid(static_cast<uint32_t>(nq), sms);
         const uint64_t tile = csa::select_tile_keys();
-        if (!fused && ctx->tail_split && nq > G && nq % G != 0) {
+        if (!fused && ctx->tail_split &&
+            ((nq > G && nq % G != 0) || (small && ctx->small_mixed && !ctx->no_split))) {
+            m_grid = G;
             const uint64_t W = nq / G * G;
             std::vector<uint64_t> tpre(1, 0);  // tail tile prefix
             uint64_t tmax = 1;
@@ -1010,6 +1022,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         split = static_cast<uint32_t>(std::min<uint64_t>(
             std::max<uint64_t>(std::strtoull(fs, nullptr, 10), 1), std::min<uint64_t>(16, min_tiles)));
     }
+    if (mixed_sel) split = 1;  // the mixed pieces replace part units
     // retry list of problems whose speculative cut proved too high: [count, ids...]
     ctx->retry.ensure((nq + 1) * 4);
     if (live) ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
@@ -1053,7 +1066,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         }
     } else if (split == 1) {
         ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
-                              sgrid, ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
+                              mixed_sel ? static_cast<uint32_t>(m_grid) : sgrid, ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
                               static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
                               rcount, ctx->spec_keep, 1, nullptr, ctx->stream, mixed_sel ? &smx : nullptr),
            "select launch");

@@ -1,8 +1,8 @@
 """Mixed-mode select (tail split): when a batch's problems do not fill whole
 rounds of the select grid, the problems past the last full round are cut
-into tile pieces spread over all CTAs; the CTA finishing a problem's last
-piece merges the pieces' histograms and logs and finalises it inside the
-select kernel. CSATTN_SELECT_SMS shrinks the grid so small batches take that
+into tile pieces spread over all CTAs (a batch smaller than the grid: every
+problem); the CTA finishing a problem's last piece merges the pieces'
+histograms and logs and finalises it inside the select kernel. CSATTN_SELECT_SMS shrinks the grid so small batches take that
 path. Every selected set must equal the reference's (oracle/_ref) decode of
 the same fork, outputs within 1e-3, tables equal after the inserts; also with
 the speculative cut forced to fail (retry pass over split problems) and with
@@ -23,22 +23,22 @@ def _need_ref():
         pytest.skip("oracle/_ref not built")
 
 
-@pytest.mark.parametrize("P,F,sms,spec,tail,gqa", [
-    (20000, 11, 8, None, None, None),  # 44 problems, grid 16: 2 rounds + 12 split problems (5 tiles each)
-    (9000, 9, 4, None, None, None),    # 36 problems, grid 8: 4 rounds + 4 split problems
-    (20000, 11, 8, "2.0", None, None), # every speculative cut fails: retry pass
-    (20000, 11, 8, None, "0", None),   # tail split off: plain rounds
-    (20000, 11, 8, None, None, "1"),   # + the opt-in warp-per-head (GQA) attention
+@pytest.mark.parametrize("P,F,sms,env", [
+    (20000, 11, 8, {}),                            # 44 problems, grid 16: 2 rounds + 12 split problems (5 tiles each)
+    (9000, 9, 4, {}),                              # 36 problems, grid 8: 4 rounds + 4 split problems
+    (20000, 11, 8, {"CSATTN_SPEC_KEEP": "2.0"}),   # every speculative cut fails: retry pass
+    (20000, 11, 8, {"CSATTN_TAIL_SPLIT": "0"}),    # tail split off: plain rounds
+    (20000, 11, 8, {"CSATTN_ATT_GQA": "1"}),       # + the opt-in warp-per-head (GQA) attention
+    (20000, 11, 64, {}),                           # small batch (44 < 128 slots): every problem in pieces
+    (20000, 11, 64, {"CSATTN_SMALL_MIXED": "0"}),  # small batch: part units + select_merge_kernel
+    (20000, 11, 64, {"CSATTN_SPEC_KEEP": "2.0"}),  # small batch, all pieces' speculation fails
 ])
-def test_tail_split_batch_equals_reference(monkeypatch, P, F, sms, spec, tail, gqa):
+def test_tail_split_batch_equals_reference(monkeypatch, P, F, sms, env):
     monkeypatch.setenv("CSATTN_SELECT_SMS", str(sms))
     monkeypatch.setenv("CSATTN_FUSED", "0")
-    if gqa:
-        monkeypatch.setenv("CSATTN_ATT_GQA", gqa)
-    if spec:
-        monkeypatch.setenv("CSATTN_SPEC_KEEP", spec)
-    if tail:
-        monkeypatch.setenv("CSATTN_TAIL_SPLIT", tail)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    gqa = "CSATTN_ATT_GQA" in env
     ctx = cs.Context(0)
     T, d = 4, (128 if gqa else 64)  # the warp-per-head attention is the d = 128 kernel
     q, k, v = workload(P, 32, d, seed=P + F)
