@@ -642,8 +642,11 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(cudaMemcpyAsync(base + o_q, q, nq * d * 4, cudaMemcpyHostToDevice, ctx->stream), "copy in");
         ck(cudaMemcpyAsync(base + o_k, keys, ns * d * 4, cudaMemcpyHostToDevice, ctx->stream), "copy in");
         ck(cudaMemcpyAsync(base + o_v, values, ns * d * 4, cudaMemcpyHostToDevice, ctx->stream), "copy in");
-        require_finite(keys, ns * d, "appended key");
-        require_finite(values, ns * d, "appended value");
+        // a non-finite appended row is refused on the device (insert.cu: the
+        // append + insert of that session are skipped, its flag is read after
+        // the synchronised step and raises DataError with the search state
+        // advanced, as decode_search runs before KvStore::append throws,
+        // session.cpp:57-81) -- no host scan of the rows on the critical path
         dq = reinterpret_cast<float*>(base + o_q);
         dk = reinterpret_cast<float*>(base + o_k);
         dv = reinterpret_cast<float*>(base + o_v);
