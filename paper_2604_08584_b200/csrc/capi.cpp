@@ -123,6 +123,27 @@ void require_finite(const float* v, size_t n, const char* what) {
     if (bad) fail(CSATTN_ERR_DATA, std::string(what) + " contains a non-finite value");
 }
 
+// The mixed-select work plan of the last step (run_step), reused while the
+// grid and every problem's tile count stay the same.
+struct MixedPlan {
+    bool valid = false;
+    uint64_t G = 0, log = 0;
+    std::vector<uint32_t> tiles;
+    std::vector<uint4> items;
+    std::vector<uint32_t> cta;
+    std::vector<uint2> pinfo, slot;
+    void clear() {
+        valid = false;
+        G = 0;
+        log = 0;
+        tiles.clear();
+        items.clear();
+        cta.clear();
+        pinfo.clear();
+        slot.clear();
+    }
+};
+
 struct SharedRows {
     DevMem k, v;
 };
@@ -196,6 +217,8 @@ struct csattn_ctx_s {
     // mixed (tail-split) select: piece logs + histograms, per-problem piece
     // counters (zero between steps: the finalising CTA resets its problem's)
     DevMem mlog_idx, mlog_sc, mumeta, pdone;
+    MixedPlan mplan;
+    std::vector<uint32_t> tiles_scratch;
     uint64_t pdone_n = 0;
     bool tail_split = !(std::getenv("CSATTN_TAIL_SPLIT") && std::atoi(std::getenv("CSATTN_TAIL_SPLIT")) == 0);
     // small batches through the mixed pieces too (CSATTN_SMALL_MIXED=0: part
@@ -810,12 +833,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     ctx->part.ensure(nchunks * (d + 2) * sizeof(float));
     // Mixed select plan: problems beyond whole rounds of the select grid are
     // cut into contiguous tile pieces spread over the CTAs (one piece range
-    // per CTA), instead of a second, partly idle round.
-    std::vector<uint4> m_items;
-    std::vector<uint32_t> m_cta;
-    std::vector<uint2> m_pinfo, m_slot;
-    uint64_t m_log = 0;
-    uint64_t m_grid = 0;
+    // per CTA), instead of a second, partly idle round. The
+    // plan depends only on the grid and the problems' tile counts, which
+    // change once per 4096 appended keys: it is rebuilt only then.
+    MixedPlan& mp = ctx->mplan;
     {
         // small batches (fewer problems than CTA slots): every problem is
         // cut into pieces over all slots, finalised in-kernel by its last
@@ -825,30 +846,37 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         const bool small = nq < slots;
         const uint64_t G = small ? slots : csa::select_grid(static_cast<uint32_t>(nq), sms);
         const uint64_t tile = csa::select_tile_keys();
-        if (!fused && ctx->tail_split &&
-            ((nq > G && nq % G != 0) || (small && ctx->small_mixed && !ctx->no_split))) {
-            m_grid = G;
+        const bool want = !fused && ctx->tail_split &&
+                          ((nq > G && nq % G != 0) || (small && ctx->small_mixed && !ctx->no_split));
+        ctx->tiles_scratch.resize(nq);
+        for (uint64_t i = 0; i < nq; ++i)
+            ctx->tiles_scratch[i] = static_cast<uint32_t>((ctx->hprobs[i].N + tile - 1) / tile);
+        if (!want) {
+            mp.clear();
+        } else if (!(mp.valid && mp.G == G && mp.tiles == ctx->tiles_scratch)) {
+            mp.clear();
+            mp.valid = true;
+            mp.G = G;
+            mp.tiles = ctx->tiles_scratch;
+            const std::vector<uint32_t>& tl = mp.tiles;
             const uint64_t W = nq / G * G;
             std::vector<uint64_t> tpre(1, 0);  // tail tile prefix
             uint64_t tmax = 1;
             for (uint64_t i = W; i < nq; ++i) {
-                const uint64_t nt = (ctx->hprobs[i].N + tile - 1) / tile;
-                tpre.push_back(tpre.back() + nt);
-                tmax = std::max(tmax, nt);
+                tpre.push_back(tpre.back() + tl[i]);
+                tmax = std::max<uint64_t>(tmax, tl[i]);
             }
             const uint64_t TT = tpre.back();
             // piece ranges of >= 1 tile and <= MAXPART pieces per problem
             const uint64_t Gp = std::max<uint64_t>(1, std::min<uint64_t>({G, TT, 15 * TT / tmax}));
-            m_cta.assign(G + 1, 0);
-            m_pinfo.assign(nq, make_uint2(0, 0));
+            mp.cta.assign(G + 1, 0);
+            mp.pinfo.assign(nq, make_uint2(0, 0));
             bool ok = true;
             uint64_t q = 0;  // tail problem cursor (relative to W)
             for (uint64_t c = 0; c < G; ++c) {
-                m_cta[c] = static_cast<uint32_t>(m_items.size());
+                mp.cta[c] = static_cast<uint32_t>(mp.items.size());
                 for (uint64_t pw = c; pw < W; pw += G)
-                    m_items.push_back(make_uint4(static_cast<uint32_t>(pw), 0u,
-                                                 static_cast<uint32_t>((ctx->hprobs[pw].N + tile - 1) / tile),
-                                                 csa::NO_SLOT));
+                    mp.items.push_back(make_uint4(static_cast<uint32_t>(pw), 0u, tl[pw], csa::NO_SLOT));
                 if (c >= Gp) continue;
                 uint64_t a = c * TT / Gp;
                 const uint64_t b = (c + 1) * TT / Gp;
@@ -856,28 +884,33 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                     while (tpre[q + 1] <= a) ++q;
                     const uint64_t e = std::min(b, tpre[q + 1]);
                     const uint32_t pr = static_cast<uint32_t>(W + q);
-                    const uint32_t sl = static_cast<uint32_t>(m_slot.size());
-                    if (m_pinfo[pr].y == 0) m_pinfo[pr].x = sl;
-                    if (++m_pinfo[pr].y > csa::SELECT_MAX_PART) ok = false;
+                    const uint32_t sl = static_cast<uint32_t>(mp.slot.size());
+                    if (mp.pinfo[pr].y == 0) mp.pinfo[pr].x = sl;
+                    if (++mp.pinfo[pr].y > csa::SELECT_MAX_PART) ok = false;
                     const uint64_t nt = e - a;
-                    m_slot.push_back(make_uint2(static_cast<uint32_t>(m_log),
-                                                static_cast<uint32_t>(nt * tile / csa::SELECT_CONSUMER_WARPS)));
-                    m_log += nt * tile;
-                    m_items.push_back(make_uint4(pr, static_cast<uint32_t>(a - tpre[q]),
-                                                 static_cast<uint32_t>(e - tpre[q]), sl));
+                    mp.slot.push_back(make_uint2(static_cast<uint32_t>(mp.log),
+                                                 static_cast<uint32_t>(nt * tile / csa::SELECT_CONSUMER_WARPS)));
+                    mp.log += nt * tile;
+                    mp.items.push_back(make_uint4(pr, static_cast<uint32_t>(a - tpre[q]),
+                                                  static_cast<uint32_t>(e - tpre[q]), sl));
                     a = e;
                 }
             }
-            m_cta[G] = static_cast<uint32_t>(m_items.size());
-            if (!ok || m_log > 0xffffffffull) {
-                m_items.clear();
-                m_cta.clear();
-                m_pinfo.clear();
-                m_slot.clear();
-                m_log = 0;
+            mp.cta[G] = static_cast<uint32_t>(mp.items.size());
+            if (!ok || mp.log > 0xffffffffull) {  // no plan: plain rounds / part units
+                const std::vector<uint32_t> keep = mp.tiles;
+                mp.clear();
+                mp.valid = true;
+                mp.G = G;
+                mp.tiles = keep;
             }
         }
     }
+    const std::vector<uint4>& m_items = mp.items;
+    const std::vector<uint32_t>& m_cta = mp.cta;
+    const std::vector<uint2>& m_pinfo = mp.pinfo;
+    const std::vector<uint2>& m_slot = mp.slot;
+    const uint64_t m_log = mp.log, m_grid = mp.G;
     const bool mixed_sel = !m_items.empty();
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     // descriptor layout, in two parts uploaded separately: A (problems,
