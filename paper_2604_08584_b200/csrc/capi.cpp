@@ -224,6 +224,9 @@ struct csattn_ctx_s {
     // small batches through the mixed pieces too (CSATTN_SMALL_MIXED=0: part
     // units + select_merge_kernel)
     bool small_mixed = !(std::getenv("CSATTN_SMALL_MIXED") && std::atoi(std::getenv("CSATTN_SMALL_MIXED")) == 0);
+    // mixed select: half the CTAs take their pieces before their whole
+    // problems (CSATTN_ORDER_SWAP=0: all whole problems first)
+    bool order_swap = !(std::getenv("CSATTN_ORDER_SWAP") && std::atoi(std::getenv("CSATTN_ORDER_SWAP")) == 0);
     // GQA warp-per-head attention, opt-in (CSATTN_ATT_GQA=1): measured slower
     // at c3 (attend 252 -> 275 us: 4x the partials, little L1 reuse)
     bool att_gqa = std::getenv("CSATTN_ATT_GQA") && std::atoi(std::getenv("CSATTN_ATT_GQA")) == 1;
@@ -877,9 +880,19 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             uint64_t q = 0;  // tail problem cursor (relative to W)
             for (uint64_t c = 0; c < G; ++c) {
                 mp.cta[c] = static_cast<uint32_t>(mp.items.size());
-                for (uint64_t pw = c; pw < W; pw += G)
-                    mp.items.push_back(make_uint4(static_cast<uint32_t>(pw), 0u, tl[pw], csa::NO_SLOT));
-                if (c >= Gp) continue;
+                // the two CTAs of an SM (c, c + G/2) take their whole problems
+                // and their pieces in opposite orders, so one streams while
+                // the other runs a final selection
+                const bool pieces_first = ctx->order_swap && c >= G / 2;
+                auto whole = [&]() {
+                    for (uint64_t pw = c; pw < W; pw += G)
+                        mp.items.push_back(make_uint4(static_cast<uint32_t>(pw), 0u, tl[pw], csa::NO_SLOT));
+                };
+                if (!pieces_first) whole();
+                if (c >= Gp) {
+                    if (pieces_first) whole();
+                    continue;
+                }
                 uint64_t a = c * TT / Gp;
                 const uint64_t b = (c + 1) * TT / Gp;
                 while (a < b) {
@@ -897,6 +910,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
                                                   static_cast<uint32_t>(e - tpre[q]), sl));
                     a = e;
                 }
+                if (pieces_first) whole();
             }
             mp.cta[G] = static_cast<uint32_t>(mp.items.size());
             if (!ok || mp.log > 0xffffffffull) {  // no plan: plain rounds / part units
