@@ -1149,11 +1149,25 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             cbar();
             if (S.f_last) {
                 __threadfence();  // the other pieces' data (they fenced before counting)
-                for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) {
-                    uint32_t v = 0;
-                    for (uint32_t j = 0; j < pi.y; ++j)
-                        v += __ldcg(mx.umeta + static_cast<size_t>(pi.x + j) * UNIT_META + x);
-                    hist[x] = v;
+                {  // the pieces' histograms, every piece's words in flight at once
+                    constexpr uint32_t HX = (NB + NCB + SEL_CT - 1) / SEL_CT;  // words per thread
+                    uint32_t hv[HX];
+#pragma unroll
+                    for (uint32_t i = 0; i < HX; ++i) hv[i] = 0;
+#pragma unroll 4
+                    for (uint32_t j = 0; j < pi.y; ++j) {
+                        const uint32_t* u = mx.umeta + static_cast<size_t>(pi.x + j) * UNIT_META;
+#pragma unroll
+                        for (uint32_t i = 0; i < HX; ++i) {
+                            const uint32_t x = tid + i * SEL_CT;
+                            if (x < NB + NCB) hv[i] += __ldcg(u + x);
+                        }
+                    }
+#pragma unroll
+                    for (uint32_t i = 0; i < HX; ++i) {
+                        const uint32_t x = tid + i * SEL_CT;
+                        if (x < NB + NCB) hist[x] = hv[i];
+                    }
                 }
                 if (tid < pi.y * SEL_CW) {
                     const uint32_t j = tid / SEL_CW, w = tid % SEL_CW;
