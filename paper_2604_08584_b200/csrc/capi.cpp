@@ -219,6 +219,7 @@ struct csattn_ctx_s {
     DevMem mlog_idx, mlog_sc, mumeta, pdone;
     MixedPlan mplan;
     std::vector<uint32_t> tiles_scratch;
+    std::vector<uint64_t> Ks_scratch;  // run_step: per-problem K
     uint64_t pdone_n = 0;
     bool tail_split = !(std::getenv("CSATTN_TAIL_SPLIT") && std::atoi(std::getenv("CSATTN_TAIL_SPLIT")) == 0);
     // small batches through the mixed pieces too (CSATTN_SMALL_MIXED=0: part
@@ -592,7 +593,8 @@ void check_appended(const csattn_session* ss, uint64_t ns) {
 
 // one session twice in a batch would append and insert twice at one N
 void check_distinct(const csattn_session* ss, uint64_t ns) {
-    std::vector<csattn_session> u(ss, ss + ns);
+    static thread_local std::vector<csattn_session> u;
+    u.assign(ss, ss + ns);
     std::sort(u.begin(), u.end());
     if (std::adjacent_find(u.begin(), u.end()) != u.end())
         fail(CSATTN_ERR_PARAMETER, "a session appears twice in one decode batch");
@@ -614,7 +616,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     if (ns == 0) fail(CSATTN_ERR_PARAMETER, "no sessions");
     const uint32_t d = ss[0]->h.d;
     uint64_t nq = 0, maxN = 0, maxK = 0;
-    std::vector<uint64_t> Ks;
+    std::vector<uint64_t>& Ks = ctx->Ks_scratch;
+    Ks.clear();
     check_distinct(ss, ns);
     for (uint64_t i = 0; i < ns; ++i) {
         csattn_session s = ss[i];
@@ -624,9 +627,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         if (s->step >= s->max_steps)
             fail(CSATTN_ERR_CAPACITY, "session is full: max_decode_steps = " +
                                           std::to_string(s->max_steps));
+        const uint64_t Ks_ = keep_count(s->rc.keep_ratio, s->N);  // the session's heads share N
         for (uint64_t h = 0; h < s->group; ++h) {
             const uint64_t ko = k_override ? k_override[nq + h] : 0;
-            const uint64_t K = ko ? std::min<uint64_t>(ko, s->N) : keep_count(s->rc.keep_ratio, s->N);
+            const uint64_t K = ko ? std::min<uint64_t>(ko, s->N) : Ks_;
             Ks.push_back(K);
             maxK = std::max(maxK, K);
         }
