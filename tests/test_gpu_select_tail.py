@@ -32,19 +32,26 @@ def _need_ref():
     (20000, 11, 64, {}),                           # small batch (44 < 128 slots): every problem in pieces
     (20000, 11, 64, {"CSATTN_SMALL_MIXED": "0"}),  # small batch: part units + select_merge_kernel
     (20000, 11, 64, {"CSATTN_SPEC_KEEP": "2.0"}),  # small batch, all pieces' speculation fails
+    (20000, 11, 8, {"rc": "period4"}),             # cached candidate scores on non-search steps
+    (20000, 11, 64, {"rc": "period4"}),
+    (20000, 11, 8, {"rc": "no_passthrough"}),      # window keys compete at score 0
+    (20000, 11, 64, {"rc": "no_passthrough"}),
 ])
 def test_tail_split_batch_equals_reference(monkeypatch, P, F, sms, env):
     monkeypatch.setenv("CSATTN_SELECT_SMS", str(sms))
     monkeypatch.setenv("CSATTN_FUSED", "0")
     for key, val in env.items():
-        monkeypatch.setenv(key, val)
+        if key != "rc":
+            monkeypatch.setenv(key, val)
     gqa = "CSATTN_ATT_GQA" in env
+    rc_kw = {"period4": dict(search_period=4, keep_ratio=0.15),
+             "no_passthrough": dict(recent_passthrough=False)}.get(env.get("rc"), {})
     ctx = cs.Context(0)
     T, d = 4, (128 if gqa else 64)  # the warp-per-head attention is the d = 128 kernel
     q, k, v = workload(P, 32, d, seed=P + F)
     widths = cs.uniform_widths(d, 4)
     ic = cs.IndexConfig(alpha=0.2, centroids=16, seed=1, score_bits=32)
-    rc = cs.RetrievalConfig(keep_ratio=0.05)
+    rc = cs.RetrievalConfig(**{"keep_ratio": 0.05, **rc_kw})
     qq = np.ascontiguousarray(np.concatenate([q[:P]] * 4))
     base = cs.prefill(ctx, qq, k[:P], v[:P], widths, ic, rc, group=4, max_decode_steps=T)
     batch = [base.fork(T) for _ in range(F)]
