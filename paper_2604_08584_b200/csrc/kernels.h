@@ -92,11 +92,13 @@ cudaError_t launch_fused_step(const DecodeProblem* probs, uint32_t nprob, int cl
 
 // attend.cu: split-K sparse attention over the selected rows, ATT_ROWS per CTA
 constexpr uint32_t ATT_ROWS = 256;      // rows per chunk-CTA (mid-size launches)
-constexpr uint32_t ATT_ROWS_BIG = 512;  // when 256-row chunks would fill > 4 waves (c3)
+constexpr uint32_t ATT_ROWS_BIG = 512;  // from ~7 CTAs per SM of 256-row chunks (c3; c3 on 4 / 8 GPUs)
 constexpr uint32_t ATT_ROWS_SMALL = 128;  // when they would give < 2 CTAs per SM (c2)
 // rows per chunk-CTA for a launch whose 256-row chunking has n256 chunks
+// (measured with GR = 8 at 7 CTAs/SM: c3 on 8 GPUs' share, 1664 chunks, 51 ->
+// 43 us with 512 rows; c4's 832 chunks per layer stay faster at 256)
 inline uint32_t attend_rows(uint64_t n256) {
-    return n256 > 148ull * 8 * 4 ? ATT_ROWS_BIG : (n256 < 148ull * 2 ? ATT_ROWS_SMALL : ATT_ROWS);
+    return n256 > 148ull * 7 ? ATT_ROWS_BIG : (n256 < 148ull * 2 ? ATT_ROWS_SMALL : ATT_ROWS);
 }
 cudaError_t launch_attend(const DecodeProblem* probs, const uint32_t* chunk_prob,
                           const uint32_t* chunk_base, uint32_t nchunks, float* part,
