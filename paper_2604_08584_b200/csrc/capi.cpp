@@ -192,6 +192,12 @@ struct csattn_ctx_s {
     cudaEvent_t side_ev = nullptr;
     // append + insert beside the attention (CSATTN_INSERT_OVERLAP=0: after it)
     cudaEvent_t ins_fork = nullptr, ins_join = nullptr;
+    // select launched as a programmatic dependent of route (CSATTN_PDL=0: off)
+    // (CSATTN_PDL=1/2/3: route's trigger at its start / once its lists are
+    // known / at its exit; default: at its start when route leaves SMs idle
+    // (nq <= SMs, c4: -127 us per 32 layers), else at its exit (c3: an early
+    // start cost +9 us, the exit trigger saves 3 us))
+    int pdl = std::getenv("CSATTN_PDL") ? std::atoi(std::getenv("CSATTN_PDL")) : 4;
     bool insert_overlap = !(std::getenv("CSATTN_INSERT_OVERLAP") && std::atoi(std::getenv("CSATTN_INSERT_OVERLAP")) == 0);
     ~csattn_ctx_s() {
         if (side) cudaStreamDestroy(side);
@@ -1051,9 +1057,16 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         if (ctx->profile) ck(cudaEventRecord(ev[1], ctx->stream), "event");
     } else {
     ctx->plans.ensure(nq * sizeof(csa::RoutePlan));
+    // retry list of problems whose speculative cut proved too high: [count, ids...]
+    // (cleared before route: nothing may sit between route and the
+    // programmatically launched select)
+    ctx->retry.ensure((nq + 1) * 4);
+    if (live) ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
     if (live)
     ck(csa::launch_route(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
-                         ctx->stream),
+                         ctx->stream,
+                         ctx->pdl == 4 ? (nq <= static_cast<uint64_t>(ctx->num_sms) ? 1 : 0)
+                                       : (ctx->pdl == 1 || ctx->pdl == 2 ? ctx->pdl : 0)),
        "route launch");
     const int sel_sms = ctx->sel_sms ? ctx->sel_sms : ctx->num_sms;
     const uint32_t sgrid = csa::select_grid(static_cast<uint32_t>(nq), sel_sms);
@@ -1079,9 +1092,6 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             std::max<uint64_t>(std::strtoull(fs, nullptr, 10), 1), std::min<uint64_t>(16, min_tiles)));
     }
     if (mixed_sel) split = 1;  // the mixed pieces replace part units
-    // retry list of problems whose speculative cut proved too high: [count, ids...]
-    ctx->retry.ensure((nq + 1) * 4);
-    if (live) ck(cudaMemsetAsync(ctx->retry.p, 0, 4, ctx->stream), "memset");
     uint32_t* const rcount = ctx->retry.as<uint32_t>();
     if (maxN > ctx->log_cap || sgrid > ctx->log_rows) {  // non-split / retry-pass logs
         // sized for the sessions' full capacity, so it is not re-grown every step
@@ -1124,7 +1134,8 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
         ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq),
                               mixed_sel ? static_cast<uint32_t>(m_grid) : sgrid, ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
                               static_cast<uint32_t>(ctx->log_cap), nullptr, nullptr, rcount + 1,
-                              rcount, ctx->spec_keep, 1, nullptr, ctx->stream, mixed_sel ? &smx : nullptr),
+                              rcount, ctx->spec_keep, 1, nullptr, ctx->stream, mixed_sel ? &smx : nullptr,
+                              ctx->pdl != 0 && !ctx->profile),
            "select launch");
     } else {
         // per-unit logs: a unit has at most ceil(max_tiles / split) tiles
@@ -1151,7 +1162,7 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     ck(csa::launch_select(dprobs, ctx->plans.as<csa::RoutePlan>(), static_cast<uint32_t>(nq), sgrid,
                           ctx->log_idx.as<uint32_t>(), ctx->log_sc.as<double>(),
                           static_cast<uint32_t>(ctx->log_cap), rcount + 1, rcount, nullptr, nullptr,
-                          0.0, 1, nullptr, ctx->stream),
+                          0.0, 1, nullptr, ctx->stream, nullptr, ctx->pdl != 0 && !ctx->profile),
        "select retry launch");
     stage_b();  // built while route / select run (its upload goes first on the side stream)
     // The append + streaming insert touches the tables and the appended KV

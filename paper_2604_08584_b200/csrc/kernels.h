@@ -10,8 +10,10 @@
 namespace csa {
 
 // route.cu: centroid routing + score bounds, one CTA per problem
+// trig: where a programmatically launched select may start (1: at the CTA's
+// start, 2: once its lists are known, 0: at its exit)
 cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob,
-                         cudaStream_t st);
+                         cudaStream_t st, int trig = 0);
 
 // select.cu: streaming gather + top-K, persistent (one CTA per SM, problems
 // strided over the grid). log_idx/log_sc: grid x log_cap candidate-log slots.
@@ -48,7 +50,11 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
                           const uint32_t* retry_in, const uint32_t* retry_in_count,
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
                           uint32_t split, uint32_t* unit_meta, cudaStream_t st,
-                          const SelMixed* mixed = nullptr);
+                          const SelMixed* mixed = nullptr, bool pdl = false);
+// pdl: launched as a programmatic dependent of the previous kernel in the
+// stream (the route launch): its CTAs start, and run their shared-memory
+// prologue, while route finishes; they wait (griddepcontrol.wait) before the
+// first read of the route plans.
 // split > 1: each problem's tiles are cut into `split` part units (logs of
 // log_cap entries each, unit_meta: select_unit_meta_words() per unit) and
 // finalised by the merge kernel (one CTA per problem).

@@ -21,12 +21,15 @@ constexpr int RT_THREADS = 256;
 constexpr int RT_WARPS = RT_THREADS / 32;
 
 __global__ void __launch_bounds__(RT_THREADS)
-route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ plans) {
+route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ plans, int trig) {
     __shared__ float q[DMAX], qn[DMAX];
     __shared__ double csc[MAX_TABLES];
     __shared__ uint32_t ids[MAXM * MAXTAU], nids[MAXM], zero_mask;
     __shared__ uint32_t lists[MAXL], lsub[MAXL], nl, llive[MAXL];
     __shared__ double lmin[MAXL], lmax[MAXL];
+    // the select launch that follows may start its prologue now (it waits
+    // for this grid's completion before reading the plans)
+    if (trig == 1) asm volatile("griddepcontrol.launch_dependents;");
     const DecodeProblem& P = probs[blockIdx.x];
     if (!(P.mode & MODE_SEARCH)) return;
     const SessionDev& sd = *P.s;
@@ -146,6 +149,7 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
         Rp->dot_ops_hi = static_cast<uint32_t>(dots >> 32);
     }
     __syncthreads();
+    if (trig == 2) asm volatile("griddepcontrol.launch_dependents;");
     if (tid < nl) {
         plan.lists[tid] = lists[tid];
         plan.lsub[tid] = lsub[tid];
@@ -199,8 +203,8 @@ route_kernel(const DecodeProblem* __restrict__ probs, RoutePlan* __restrict__ pl
 }
 
 cudaError_t launch_route(const DecodeProblem* probs, RoutePlan* plans, uint32_t nprob,
-                         cudaStream_t st) {
-    route_kernel<<<nprob, RT_THREADS, 0, st>>>(probs, plans);
+                         cudaStream_t st, int trig) {
+    route_kernel<<<nprob, RT_THREADS, 0, st>>>(probs, plans, trig);
     return cudaGetLastError();
 }
 

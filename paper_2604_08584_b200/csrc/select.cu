@@ -633,6 +633,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     // merges them and finalises it), so 512 problems over 296 slots cost
     // 1.73 problems per CTA instead of two rounds.
     const bool mixed = mx.items != nullptr;
+    // the retry pass (a programmatic dependent of the first pass) reads the
+    // retry list the first pass wrote
+    if (retry_in) asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t it0 = mixed ? __ldg(mx.cta_items + blockIdx.x) : 0u;
     const uint32_t it1 = mixed ? __ldg(mx.cta_items + blockIdx.x + 1) : 0u;
     const uint32_t nwork = mixed ? it1 : (retry_in ? __ldcg(retry_in_count) : nprob * split);
@@ -684,6 +687,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     for (uint32_t i = tid; i < TILE; i += SEL_THREADS) acc[i] = neg0_d();
     for (uint32_t i = tid; i < NB + NCB; i += SEL_THREADS) hist[i] = 0;
     __syncthreads();
+    // programmatic launch: the route plans are visible after this (a no-op
+    // for a normal launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // ======================= producer warp =======================
     if (wid == SEL_CW) {
@@ -1625,7 +1631,8 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
                           uint32_t grid, uint32_t* log_idx, double* log_sc, uint32_t log_cap,
                           const uint32_t* retry_in, const uint32_t* retry_in_count,
                           uint32_t* retry_out, uint32_t* retry_out_count, double spec_keep,
-                          uint32_t split, uint32_t* unit_meta, cudaStream_t st, const SelMixed* mixed) {
+                          uint32_t split, uint32_t* unit_meta, cudaStream_t st, const SelMixed* mixed,
+                          bool pdl) {
     const size_t smem = select_smem();
     {  // once per device (a host call per launch otherwise)
         static bool set[64] = {};
@@ -1639,10 +1646,25 @@ cudaError_t launch_select(const DecodeProblem* probs, const RoutePlan* plans, ui
             if (dev >= 0 && dev < 64) set[dev] = true;
         }
     }
+    const SelMixed mx = mixed ? *mixed : SelMixed{};
+    if (pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(SEL_THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, select_kernel, probs, plans, nprob, log_idx, log_sc, log_cap,
+                                  retry_in, retry_in_count, retry_out, retry_out_count, spec_keep,
+                                  split, unit_meta, mx);
+    }
     select_kernel<<<grid, SEL_THREADS, smem, st>>>(probs, plans, nprob, log_idx, log_sc, log_cap,
                                                    retry_in, retry_in_count, retry_out,
-                                                   retry_out_count, spec_keep, split, unit_meta,
-                                                   mixed ? *mixed : SelMixed{});
+                                                   retry_out_count, spec_keep, split, unit_meta, mx);
     return cudaGetLastError();
 }
 

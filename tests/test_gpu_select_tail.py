@@ -36,6 +36,10 @@ def _need_ref():
     (20000, 11, 64, {"rc": "period4"}),
     (20000, 11, 8, {"rc": "no_passthrough"}),      # window keys compete at score 0
     (20000, 11, 64, {"rc": "no_passthrough"}),
+    # route -> select programmatic launch (default here: select starts at route's start)
+    (20000, 11, 8, {"CSATTN_PDL": "0"}),                             # off
+    (20000, 11, 8, {"CSATTN_PDL": "2", "CSATTN_SPEC_KEEP": "2.0"}),  # trigger once lists are known, + retry pass
+    (20000, 11, 64, {"CSATTN_PDL": "3", "CSATTN_SPEC_KEEP": "2.0"}), # trigger at route's exit, + retry pass
 ])
 def test_tail_split_batch_equals_reference(monkeypatch, P, F, sms, env):
     monkeypatch.setenv("CSATTN_SELECT_SMS", str(sms))
