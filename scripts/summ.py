@@ -1,3 +1,4 @@
+# bench JSON lines -> one summary line each (step, e2e, kernel shares, roofline fractions, clocks)
 import json, sys
 for f in sys.argv[1:]:
     try:
