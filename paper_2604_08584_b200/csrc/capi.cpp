@@ -1235,8 +1235,10 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
     if (ctx->profile) ck(cudaEventRecord(ev[2], ctx->stream), "event");
     if (ins_forked)
         ck(cudaStreamWaitEvent(ctx->stream, ctx->ins_join, 0), "insert join");
-    else if (live)
-        ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream), "insert launch");
+    else if (live)  // after the fused step: a programmatic dependent of it
+        ck(csa::launch_insert(diprobs, static_cast<uint32_t>(ns), ctx->stream, nullptr,
+                              fused && ctx->pdl != 0 && !ctx->profile),
+           "insert launch");
     if (slot) {
         ck(cudaEventRecord(slot->done, ctx->stream), "event");
         slot->used = true;

@@ -435,6 +435,9 @@ fused_step_kernel(const DecodeProblem* __restrict__ probs, uint32_t nr) {
     const SessionDev& sd = *P.s;
     const uint32_t tid = threadIdx.x, wid = tid >> 5, ln = tid & 31;
     const uint32_t N = P.N, K = P.K, d = sd.d;
+    // the insert that follows (a programmatic dependent) may start its
+    // key-scoring prologue now; it waits for this grid before any table write
+    asm volatile("griddepcontrol.launch_dependents;");
     const bool search = P.mode & MODE_SEARCH;
     const bool store_cache = (P.mode & MODE_STORE_CACHE) && P.cache;
     const bool pt = sd.passthrough != 0;

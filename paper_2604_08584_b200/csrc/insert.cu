@@ -113,13 +113,19 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
     // a table is touched by exactly one thread in phase A)
     const bool pf = threadIdx.x < T && sd.L != 0 && !sd.sharded;
     uint32_t pf_nu = 0, pf_live = 0, pf_cnt = 0;
-    LowEnt pf_victim{};
+    LowEnt pf_victim{}, pf_lo0{};
+    float2 pf_mm{};
     if (pf) {
         const uint32_t t = threadIdx.x;
         pf_nu = sd.n_used[t];
         pf_live = sd.live[t];
         pf_cnt = sd.low_cnt[t];
-        if (pf_live >= sd.L && pf_cnt) pf_victim = sd.low[static_cast<size_t>(t) * LOW_Q + pf_cnt - 1];
+        pf_mm = sd.tmm[t];
+        if (pf_cnt) {
+            const LowEnt* lo = sd.low + static_cast<size_t>(t) * LOW_Q;
+            pf_lo0 = lo[0];
+            if (pf_live >= sd.L) pf_victim = lo[pf_cnt - 1];
+        }
     }
     __syncthreads();
     if (sd.normalize_keys && threadIdx.x < m) {
@@ -161,6 +167,11 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
             }
         }
         const float sc = __double2float_rn(s);
+        // programmatic dependent launch (fused step -> insert): everything
+        // above reads only the key, the centroids and table state that the
+        // previous kernel does not write; the table writes below wait for it
+        // (it gathers these tables). Without the launch attribute: a no-op.
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const bool mine = pf && t == threadIdx.x;  // prefetched above
         uint32_t nu = mine ? pf_nu : sd.n_used[t];
         if (new_blk) sd.blk_off[static_cast<size_t>(t) * sd.nb_stride + (N >> KEY_BLOCK_SHIFT)] = nu;
@@ -243,7 +254,7 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
                 applied = 1;
                 e[nu] = make_uint2(N, __float_as_uint(sc));
                 {  // live score bounds (evictions only raise the min: kept as a bound)
-                    float2 mm = sd.tmm[t];
+                    float2 mm = mine ? pf_mm : sd.tmm[t];
                     mm = live == 0 ? make_float2(sc, sc)
                                    : make_float2(fminf(mm.x, sc), fmaxf(mm.y, sc));
                     sd.tmm[t] = mm;
@@ -258,8 +269,10 @@ insert_kernel(const InsertProblem* __restrict__ probs, const unsigned long long*
                     ins = complete;  // an empty, incomplete buffer is refilled instead
                 else if (complete && cnt < static_cast<uint32_t>(LOW_Q))
                     ins = true;
-                else
-                    ins = ev_before(sc, N, lo[0].score, lo[0].key);
+                else {  // lo[0] is the same entry after an eviction (cnt >= 1 left)
+                    const LowEnt l0 = mine ? pf_lo0 : lo[0];
+                    ins = ev_before(sc, N, l0.score, l0.key);
+                }
                 if (ins) {
                     const uint32_t k = atomicAdd(&S.nbuf, 1u);
                     S.buflist[k] = t;
@@ -327,7 +340,19 @@ cudaError_t launch_shard_victim(const InsertProblem* probs, uint32_t nprob,
 }
 
 cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st,
-                          const unsigned long long* gvk) {
+                          const unsigned long long* gvk, bool pdl) {
+    if (pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nprob);
+        cfg.blockDim = dim3(INS_THREADS);
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, insert_kernel, probs, gvk);
+    }
     insert_kernel<<<nprob, INS_THREADS, 0, st>>>(probs, gvk);
     return cudaGetLastError();
 }

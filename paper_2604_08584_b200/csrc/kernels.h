@@ -146,8 +146,11 @@ cudaError_t launch_shard_merge(const float* parts, uint32_t nshard, uint32_t npr
 
 // insert.cu: append + streaming insert, one CTA per session
 //   gvk: sharded sessions only, per session x table the global victim key
+//   pdl: a programmatic dependent of the previous kernel (the fused step): the
+//   key's scores and the table state are read while that kernel finishes; the
+//   table writes wait for it (griddepcontrol.wait)
 cudaError_t launch_insert(const InsertProblem* probs, uint32_t nprob, cudaStream_t st,
-                          const unsigned long long* gvk = nullptr);
+                          const unsigned long long* gvk = nullptr, bool pdl = false);
 cudaError_t launch_shard_victim(const InsertProblem* probs, uint32_t nprob,
                                 unsigned long long* vk, cudaStream_t st);
 
