@@ -1282,6 +1282,63 @@ void run_step(csattn_ctx ctx, uint64_t ns, const csattn_session* ss, const float
             ctx->phase_dbg[1] = hi;
             ctx->phase_dbg[2] = static_cast<double>(ph[7]);
         }
+        {  // select CTA timeline of this step: start / end spread relative to the first start
+            const uint32_t nc = static_cast<uint32_t>(std::min<uint64_t>(2 * ctx->num_sms, 1024));
+            std::vector<unsigned long long> ts(10 * nc);
+            ck(csa::select_cta_times(ts.data(), nc, ctx->stream), "cta times");
+            ck(cudaStreamSynchronize(ctx->stream), "cta times");
+            std::vector<double> st_, en_;
+            unsigned long long t0 = ~0ull;
+            for (uint32_t c = 0; c < nc; ++c) if (ts[2 * c]) t0 = std::min(t0, ts[2 * c]);
+            for (uint32_t c = 0; c < nc; ++c)
+                if (ts[2 * c] && ts[2 * c + 1] > ts[2 * c]) {
+                    st_.push_back((ts[2 * c] - t0) / 1e3);
+                    en_.push_back((ts[2 * c + 1] - t0) / 1e3);
+                }
+            if (!en_.empty()) {
+                std::sort(st_.begin(), st_.end());
+                std::sort(en_.begin(), en_.end());
+                auto qv = [](const std::vector<double>& v, double f) { return v[std::min(v.size() - 1, size_t(f * v.size()))]; };
+                std::fprintf(stderr, "[cta] n=%zu start q50 %.1f max %.1f | end min %.1f q10 %.1f q50 %.1f q90 %.1f max %.1f us\n",
+                             en_.size(), qv(st_, 0.5), st_.back(), en_.front(), qv(en_, 0.1), qv(en_, 0.5), qv(en_, 0.9), en_.back());
+                // item-end events: per event index, count by type (1 piece, 2 piece+finalise,
+                // 3 whole problem) and the mean time
+                {  // mean item duration by type (from the previous event / the CTA start)
+                    double dsum[4] = {0, 0, 0, 0};
+                    uint32_t dn[4] = {0, 0, 0, 0};
+                    for (uint32_t c = 0; c < nc; ++c) {
+                        if (!ts[2 * c]) continue;
+                        unsigned long long prev = ts[2 * c];
+                        for (uint32_t j = 0; j < 8; ++j) {
+                            const unsigned long long e = ts[2 * nc + c * 8 + j];
+                            const unsigned long long t = e >> 2;
+                            if (!e || t < prev || t > ts[2 * c + 1]) break;
+                            dsum[e & 3] += (t - prev) / 1e3;
+                            dn[e & 3]++;
+                            prev = t;
+                        }
+                    }
+                    std::fprintf(stderr, "[cta]   mean item time: piece %.1f us (n=%u), piece+finalise %.1f us (n=%u), whole %.1f us (n=%u)\n",
+                                 dn[1] ? dsum[1] / dn[1] : 0.0, dn[1], dn[2] ? dsum[2] / dn[2] : 0.0, dn[2],
+                                 dn[3] ? dsum[3] / dn[3] : 0.0, dn[3]);
+                }
+                for (uint32_t j = 0; j < 8; ++j) {
+                    double sum = 0;
+                    uint32_t cnt[4] = {0, 0, 0, 0}, n = 0;
+                    for (uint32_t c = 0; c < nc; ++c) {
+                        const unsigned long long e = ts[2 * nc + c * 8 + j];
+                        if (!e || !ts[2 * c]) continue;
+                        const unsigned long long t = e >> 2;
+                        if (t < ts[2 * c] || t > ts[2 * c + 1]) continue;  // stale (earlier launch)
+                        sum += (t - t0) / 1e3;
+                        cnt[e & 3]++;
+                        ++n;
+                    }
+                    if (n) std::fprintf(stderr, "[cta]   event %u: n=%u (piece %u, piece+fin %u, whole %u) mean t %.1f us\n",
+                                        j, n, cnt[1], cnt[2], cnt[3], sum / n);
+                }
+            }
+        }
         {
             unsigned long long fd[8];
             ck(csa::select_fin_debug(fd, ctx->stream), "fin debug");

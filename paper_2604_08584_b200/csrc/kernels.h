@@ -62,6 +62,8 @@ uint32_t select_unit_meta_words();
 uint32_t select_ctas_per_sm();  // resident select CTAs per SM (grid = this x SMs)
 // CSATTN_PHASE_PROF only: the final-selection stage times (ns, summed over
 // problems; [6] = problem count) accumulated since the library loaded.
+// CSATTN_PHASE_PROF: per select CTA (start, end) globaltimer stamps of the last launch
+cudaError_t select_cta_times(unsigned long long* out, uint32_t n, cudaStream_t st);
 cudaError_t select_fin_debug(unsigned long long* out8, cudaStream_t st);
 uint32_t select_tile_keys();
 cudaError_t launch_select_merge(const DecodeProblem* probs, const RoutePlan* plans, uint32_t nprob,

@@ -412,7 +412,10 @@ __device__ void setup_problem(SelHdr& S, const DecodeProblem* probs, const Route
 // at and above every cut used) and its candidate log, given as nseg segments
 // (S.seg_off[k], S.seg_len[k]) of log_idx/log_sc. Consumer threads only (named
 // barrier 1). Leaves the bitmap region dirty; the caller resets its scratch.
-__device__ unsigned long long g_fin_dbg[8];  // CSATTN_PHASE_PROF: final-phase stage ns, summed
+__device__ unsigned long long g_fin_dbg[8];
+constexpr uint32_t SEL_TS_MAX = 1024;            // CSATTN_PHASE_PROF: per-CTA start / end
+__device__ unsigned long long g_cta_ts[2 * SEL_TS_MAX];
+__device__ unsigned long long g_cta_ev[8 * SEL_TS_MAX];  // (globaltimer << 2) | item type  // CSATTN_PHASE_PROF: final-phase stage ns, summed
 __device__ void final_select(SelHdr& S, const ProbState& st, uint32_t p, uint32_t* hist,
                              uint32_t* coarse, uint32_t* bm, unsigned long long* bkey,
                              uint32_t* bidx, const uint32_t* log_idx, const double* log_sc,
@@ -690,6 +693,12 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
     // programmatic launch: the route plans are visible after this (a no-op
     // for a normal launch)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool cta_prof = probs[0].prof != nullptr && blockIdx.x < SEL_TS_MAX;
+    if (cta_prof && tid == 0) g_cta_ts[2 * blockIdx.x] = gtimer();
+    uint32_t nev = 0;  // CSATTN_PHASE_PROF: item-end events of this CTA (thread 0)
+    auto stamp = [&](uint32_t type) {
+        if (cta_prof && tid == 0 && nev < 8) g_cta_ev[blockIdx.x * 8 + nev++] = (gtimer() << 2) | type;
+    };
 
     // ======================= producer warp =======================
     if (wid == SEL_CW) {
@@ -1189,6 +1198,9 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                 for (uint32_t x = tid; x < div_up(nw, 2); x += SEL_CT) acc[x] = neg0_d();
                 for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) hist[x] = 0;
                 if (tid == 0) mx.pdone[p] = 0;  // ready for the next step
+                stamp(2);
+            } else {
+                stamp(1);
             }
             if (tid == 0) {
                 S.cut = 0;
@@ -1216,6 +1228,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
                          retry_out_count);
             const uint32_t nw = div_up(st.N, 32);
             cbar();  // bitmap emitted, scratch free
+            stamp(3);
             // ---- reset for the next problem ----
             for (uint32_t x = tid; x < div_up(nw, 2); x += SEL_CT) acc[x] = neg0_d();
             for (uint32_t x = tid; x < NB + NCB; x += SEL_CT) hist[x] = 0;
@@ -1234,6 +1247,7 @@ select_kernel(const DecodeProblem* __restrict__ probs, const RoutePlan* __restri
             }
         }
     }
+    if (cta_prof && tid == 0) g_cta_ts[2 * blockIdx.x + 1] = gtimer();
 }
 
 // Finalise split problems (split > 1): sum the parts' histograms (each part's
@@ -1608,6 +1622,13 @@ cudaError_t select_fin_debug(unsigned long long* out8, cudaStream_t st) {
     cudaError_t e = cudaMemcpyFromSymbolAsync(out8, g_fin_dbg, 64, 0, cudaMemcpyDeviceToHost, st);
     static const unsigned long long z[8] = {};
     if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(g_fin_dbg, z, 64, 0, cudaMemcpyHostToDevice, st);
+    return e;
+}
+cudaError_t select_cta_times(unsigned long long* out, uint32_t n, cudaStream_t st) {
+    n = n < SEL_TS_MAX ? n : SEL_TS_MAX;
+    cudaError_t e = cudaMemcpyFromSymbolAsync(out, g_cta_ts, 16 * n, 0, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyFromSymbolAsync(out + 2 * n, g_cta_ev, 64 * n, 0, cudaMemcpyDeviceToHost, st);
     return e;
 }
 uint32_t select_tile_keys() { return TILE; }
