@@ -4,7 +4,9 @@ initcheck): every decode kernel on both select paths plus the table build.
     build_lists),
   * 2 decode steps of 80 forks in one batch (320 problems: the persistent
     non-split select with speculation, the retry pass, 512-row attend chunks),
-  * 2 decode steps of 2 forks (split part units + select_merge_kernel),
+  * 2 decode steps of 2 forks (8 problems: the fused cluster step, with the
+    insert as its programmatic dependent; CSATTN_FUSED=0 takes the mixed
+    select pieces instead),
   * a search_period = 4 session (candidate cache store / reuse).
 Run: compute-sanitizer --tool <t> python scripts/sanitize_workload.py"""
 import os
