@@ -90,3 +90,40 @@ def test_fused_threshold_bin_overflow(monkeypatch):
     g = cs.prefill(ctx, q[:P], k[:P], v[:P], widths, ic, rc, max_decode_steps=T)
     r = ob.RefSession.prefill(q[:P], k[:P], v[:P], widths, ic, rc, 1)
     lockstep(g, r, q, k, v, P, T, want_weights=False)
+
+
+def _pdl_batch(monkeypatch, pdl, P, T, nf):
+    monkeypatch.setenv("CSATTN_FUSED", "1")
+    monkeypatch.setenv("CSATTN_PDL", str(pdl))
+    ctx = cs.Context(0)  # reads CSATTN_FUSED / CSATTN_PDL
+    d, grp = 128, 4
+    q, k, v = workload(P, T + nf, d, seed=13)
+    widths = cs.uniform_widths(d, 8)
+    ic = cs.IndexConfig(alpha=0.05, centroids=16, seed=1, score_bits=32)  # small L: many evictions
+    qq = np.concatenate([q[:P]] * grp)
+    base = cs.prefill(ctx, qq, k[:P], v[:P], widths, ic, cs.RetrievalConfig(), group=grp,
+                      max_decode_steps=T)
+    forks = [base.fork(T) for _ in range(nf)]
+    outs, sels = [], []
+    for t in range(T):
+        Q = np.stack([q[P + f + t] for f in range(nf) for _ in range(grp)])
+        out, sel = cs.decode_batch(forks, Q, k[P + t:P + t + nf], v[P + t:P + t + nf])
+        outs.append(out.copy())
+        sels.append(sel.copy())
+    return outs, sels, [f.export_index() for f in forks]
+
+
+def test_insert_programmatic_dependent_of_fused_step(monkeypatch):
+    """The insert after the fused step is a programmatic dependent (it scores the
+    key and reads table state while the fused kernel runs, and writes the tables
+    after griddepcontrol.wait): outputs, selected sets and the tables after every
+    step's inserts are bit-identical to the serialised launch (CSATTN_PDL=0), over
+    a c2-like batch (8 sessions x GQA 4) with frequent evictions."""
+    a = _pdl_batch(monkeypatch, 4, 20000, 12, 8)
+    b = _pdl_batch(monkeypatch, 0, 20000, 12, 8)
+    for oa, ob_ in zip(a[0], b[0]):
+        assert np.array_equal(oa, ob_)
+    for sa, sb in zip(a[1], b[1]):
+        assert np.array_equal(sa, sb)
+    for ta, tb in zip(a[2], b[2]):
+        assert tables_equal(ta, tb)
